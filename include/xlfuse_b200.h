@@ -1,0 +1,115 @@
+/*
+ * xlfuse_b200.h -- C ABI of the B200-native cross-layer fused CNN inference
+ * path (arXiv 2007.06000).  Plain pointers and sizes only; no torch or C++
+ * types cross this boundary.  Library: paper_2007_06000_b200/libxlfuse_b200.so
+ *
+ * Each entry point names the reference interface it replaces
+ * (reference repository proj/, file:line).  All functions return XLF_OK or an
+ * error code; the message is available from xlf_last_error() (thread-local).
+ * Device entry points are asynchronous on the given cudaStream_t (passed as
+ * void*; NULL = the legacy default stream) unless documented otherwise.
+ */
+#ifndef XLFUSE_B200_H
+#define XLFUSE_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Mirrors xlfuse::ErrorKind (include/xlfuse/error.hpp:12-19) plus CUDA / argument errors. */
+typedef enum {
+    XLF_OK = 0,
+    XLF_E_IO = 1,
+    XLF_E_PARSE = 2,
+    XLF_E_VALIDATION = 3,
+    XLF_E_INFEASIBLE = 4,
+    XLF_E_VERIFICATION = 5,
+    XLF_E_INTERNAL = 6,
+    XLF_E_CUDA = 7,
+    XLF_E_ARG = 8
+} xlf_status;
+
+/* Which partition the device executes. */
+typedef enum {
+    XLF_PART_REFERENCE = 0, /* detect_fusion_blocks (fusion.cpp:147-226): straight/split/merge, concat unfused */
+    XLF_PART_B200 = 1,      /* + pool epilogues, concat sinks, shared-input multi-branch kernels */
+    XLF_PART_UNFUSED = 2    /* one kernel per layer (the unfused sm_100a baseline) */
+} xlf_partition;
+
+typedef enum {
+    XLF_FP32_EXACT = 0, /* bit-exact with run_reference (reference.cpp:16-57) */
+    XLF_FP32 = 1,       /* FFMA, <= 1e-5 norm-wise */
+    XLF_BF16 = 2        /* bf16 operands, fp32 accumulate, <= 1e-2 norm-wise */
+} xlf_precision;
+
+typedef struct xlf_graph xlf_graph;
+typedef struct xlf_engine xlf_engine;
+
+const char* xlf_last_error(void);
+const char* xlf_version(void);
+
+/* ---- graph and planner (host only) ------------------------------------ */
+
+/* parse_graph + infer_shapes + fold_elementwise (graph.cpp:221-256, :405-417,
+ * fusion.cpp:24-51) on the reference's structured-text graph format. */
+xlf_status xlf_graph_parse(const char* text, xlf_graph** out);
+void xlf_graph_destroy(xlf_graph* g);
+/* JSON: name, inputs, outputs, layers (kind, inputs, shape, conv/pool params). */
+xlf_status xlf_graph_json(const xlf_graph* g, char* buf, size_t cap, size_t* need);
+/* serialize_graph (graph.cpp:266-301) of the prepared graph. */
+xlf_status xlf_graph_serialize(const xlf_graph* g, char* buf, size_t cap, size_t* need);
+
+/* detect_fusion_blocks (fusion.cpp:147-226) / B200 partition, as
+ * block_assignment_report text (fusion.cpp:228-256) or JSON. */
+xlf_status xlf_block_report(const xlf_graph* g, int partition, char* buf, size_t cap, size_t* need);
+xlf_status xlf_blocks_json(const xlf_graph* g, int partition, char* buf, size_t cap, size_t* need);
+/* classify_mode (fusion.cpp:53-128): names separated by ','; JSON result. */
+xlf_status xlf_classify_mode(const xlf_graph* g, const char* names_csv, char* buf, size_t cap, size_t* need);
+/* plan_tiling (tiling.cpp:240-419) for a block of the reference partition at
+ * an explicit geometry on `device` ("titan_xp" | "tesla_p4" | "b200" or a
+ * device document, device.cpp:38-62); serialize_plan text (tiling.cpp:493). */
+xlf_status xlf_plan_tiling(const xlf_graph* g, const char* block_id, int tile_h, int tile_w, int grid_h, int grid_w,
+                           const char* device, char* buf, size_t cap, size_t* need);
+/* Modelled 16-B store transactions fused / unfused (cost_model.cpp:43-55, titan_xp). */
+xlf_status xlf_store_tx(const xlf_graph* g, const char* block_id, long long* fused, long long* unfused);
+/* Device program of a partition (host-only planning: kernel steps, tiles,
+ * shared bytes, tensor placement) as JSON; batch_hint steers the tile choice. */
+xlf_status xlf_device_plan_json(const xlf_graph* g, int partition, int batch_hint, char* buf, size_t cap, size_t* need);
+/* seeded_weights (tensor.cpp:42-62) in save_weights stream order (tensor.cpp:64-95).
+ * out may be NULL to query *count. */
+xlf_status xlf_seeded_weights(const xlf_graph* g, uint64_t seed, float* out, size_t cap, size_t* count);
+
+/* ---- device executor (replaces simulate_graph fused_exec.cpp:313-349 and
+ *      run_fused_block fused_exec.cpp:30-311) ----------------------------- */
+
+/* weights: save_weights stream order, reference layout [oc][ic/g][kh][kw] + bias. */
+xlf_status xlf_engine_create(const xlf_graph* g, int device, int partition, int precision, const float* weights,
+                             size_t n_weights, int max_batch, xlf_engine** out);
+void xlf_engine_destroy(xlf_engine* e);
+/* JSON description: steps (kernels, tiles, shared bytes, MACs, algorithmic bytes), tensors. */
+xlf_status xlf_engine_json(const xlf_engine* e, char* buf, size_t cap, size_t* need);
+int xlf_engine_num_steps(const xlf_engine* e);
+int xlf_engine_launches_per_forward(const xlf_engine* e);
+/* Device input, NCHW fp32 (reference layout, images stacked). */
+xlf_status xlf_engine_set_input(xlf_engine* e, const float* d_nchw, int batch, void* stream);
+/* Input generated on device from SeededStream(seed) (tensor.cpp:19-40):
+ * image n = stream elements [(first_image+n)*CHW, ...). */
+xlf_status xlf_engine_set_input_seeded(xlf_engine* e, uint64_t seed, uint64_t first_image, int batch, void* stream);
+/* All blocks of the partition (one CUDA-graph launch when use_graph != 0). */
+xlf_status xlf_engine_forward(xlf_engine* e, int batch, int use_graph, void* stream);
+/* One step (fused block or singleton) of the partition. */
+xlf_status xlf_engine_run_step(xlf_engine* e, int step, int batch, void* stream);
+/* Tensor `name` (any materialised layer output) as NCHW fp32 into d_nchw. */
+xlf_status xlf_engine_read(xlf_engine* e, const char* name, float* d_nchw, int batch, void* stream);
+/* End to end from host memory: H2D of the NCHW input, forward, D2H of tensor
+ * `name` into h_out (NCHW). Synchronous. */
+xlf_status xlf_engine_run_host(xlf_engine* e, const float* h_in_nchw, int batch, const char* name, float* h_out_nchw,
+                               void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* XLFUSE_B200_H */

@@ -1,0 +1,90 @@
+"""ctypes binding of the C ABI (include/xlfuse_b200.h).
+
+The shared library is built in-tree by ``__graft_entry__.build()`` (or
+``make -C paper_2007_06000_b200/csrc``).  There is no fallback: if the
+library is missing every call raises.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libxlfuse_b200.so")
+
+# Every symbol include/xlfuse_b200.h declares (checked by tests/test_abi.py).
+SYMBOLS = [
+    "xlf_last_error", "xlf_version", "xlf_graph_parse", "xlf_graph_destroy", "xlf_graph_json", "xlf_graph_serialize",
+    "xlf_block_report", "xlf_blocks_json", "xlf_classify_mode", "xlf_plan_tiling", "xlf_store_tx", "xlf_device_plan_json", "xlf_seeded_weights",
+    "xlf_engine_create", "xlf_engine_destroy", "xlf_engine_json", "xlf_engine_num_steps",
+    "xlf_engine_launches_per_forward", "xlf_engine_set_input", "xlf_engine_set_input_seeded", "xlf_engine_forward",
+    "xlf_engine_run_step", "xlf_engine_read", "xlf_engine_run_host",
+]
+
+STATUS = {0: "ok", 1: "io", 2: "parse", 3: "validation", 4: "infeasible", 5: "verification", 6: "internal", 7: "cuda",
+          8: "arg"}
+
+
+class XlfError(RuntimeError):
+    """Mirrors xlfuse::Error (error.hpp:21-35): ``kind`` is the ErrorKind name."""
+
+    def __init__(self, code: int, message: str):
+        self.code = code
+        self.kind = STATUS.get(code, "internal")
+        super().__init__(f"[{self.kind}] {message}")
+
+
+_LIB = None
+
+
+def lib() -> ctypes.CDLL:
+    global _LIB
+    if _LIB is not None:
+        return _LIB
+    if not os.path.exists(LIB_PATH):
+        raise RuntimeError(f"{LIB_PATH} is missing: run __graft_entry__.build() (no CPU fallback exists)")
+    L = ctypes.CDLL(LIB_PATH)
+    c_char_pp = ctypes.c_char_p
+    vp, sz, szp = ctypes.c_void_p, ctypes.c_size_t, ctypes.POINTER(ctypes.c_size_t)
+    f32p = ctypes.POINTER(ctypes.c_float)
+    L.xlf_last_error.restype = ctypes.c_char_p
+    L.xlf_version.restype = ctypes.c_char_p
+    L.xlf_graph_parse.argtypes = [c_char_pp, ctypes.POINTER(vp)]
+    L.xlf_graph_destroy.argtypes = [vp]
+    L.xlf_graph_destroy.restype = None
+    for fn in ("xlf_graph_json", "xlf_graph_serialize"):
+        getattr(L, fn).argtypes = [vp, ctypes.c_char_p, sz, szp]
+    for fn in ("xlf_block_report", "xlf_blocks_json"):
+        getattr(L, fn).argtypes = [vp, ctypes.c_int, ctypes.c_char_p, sz, szp]
+    L.xlf_classify_mode.argtypes = [vp, c_char_pp, ctypes.c_char_p, sz, szp]
+    L.xlf_plan_tiling.argtypes = [vp, c_char_pp] + [ctypes.c_int] * 4 + [c_char_pp, ctypes.c_char_p, sz, szp]
+    L.xlf_store_tx.argtypes = [vp, c_char_pp, ctypes.POINTER(ctypes.c_longlong), ctypes.POINTER(ctypes.c_longlong)]
+    L.xlf_device_plan_json.argtypes = [vp, ctypes.c_int, ctypes.c_int, ctypes.c_char_p, sz, szp]
+    L.xlf_seeded_weights.argtypes = [vp, ctypes.c_uint64, f32p, sz, szp]
+    L.xlf_engine_create.argtypes = [vp, ctypes.c_int, ctypes.c_int, ctypes.c_int, f32p, sz, ctypes.c_int, ctypes.POINTER(vp)]
+    L.xlf_engine_destroy.argtypes = [vp]
+    L.xlf_engine_destroy.restype = None
+    L.xlf_engine_json.argtypes = [vp, ctypes.c_char_p, sz, szp]
+    L.xlf_engine_num_steps.argtypes = [vp]
+    L.xlf_engine_launches_per_forward.argtypes = [vp]
+    L.xlf_engine_set_input.argtypes = [vp, vp, ctypes.c_int, vp]
+    L.xlf_engine_set_input_seeded.argtypes = [vp, ctypes.c_uint64, ctypes.c_uint64, ctypes.c_int, vp]
+    L.xlf_engine_forward.argtypes = [vp, ctypes.c_int, ctypes.c_int, vp]
+    L.xlf_engine_run_step.argtypes = [vp, ctypes.c_int, ctypes.c_int, vp]
+    L.xlf_engine_read.argtypes = [vp, c_char_pp, vp, ctypes.c_int, vp]
+    L.xlf_engine_run_host.argtypes = [vp, f32p, ctypes.c_int, c_char_pp, f32p, vp]
+    _LIB = L
+    return L
+
+
+def check(rc: int) -> None:
+    if rc != 0:
+        raise XlfError(rc, lib().xlf_last_error().decode())
+
+
+def text_call(fn, *args) -> str:
+    need = ctypes.c_size_t()
+    check(fn(*args, None, 0, ctypes.byref(need)))
+    buf = ctypes.create_string_buffer(need.value)
+    check(fn(*args, buf, need.value, ctypes.byref(need)))
+    return buf.value.decode()

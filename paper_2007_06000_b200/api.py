@@ -1,0 +1,289 @@
+"""Python face of the drop-in API.
+
+Names, argument meaning and error behaviour follow the reference
+(reference proj/include/xlfuse/*.hpp): ``Graph``, ``FusionBlock``,
+``detect_fusion_blocks``, ``classify_mode``, ``plan_tiling``,
+``run_fused_block``, ``simulate_graph``, ``seeded_weights``.  Everything is
+computed by the C++ library / sm_100a kernels behind the C ABI
+(include/xlfuse_b200.h); this module only marshals arguments.  Device
+tensors are torch CUDA tensors (torch is plumbing for device memory and
+streams); host tensors are numpy arrays.  Layouts at this boundary are the
+reference's: NCHW float32 (CHW per image, images stacked).
+"""
+from __future__ import annotations
+
+import ctypes
+import json
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _lib
+from ._lib import XlfError, check, lib, text_call
+
+PARTITIONS = {"reference": 0, "b200": 1, "unfused": 2}
+PRECISIONS = {"fp32_exact": 0, "fp32": 1, "bf16": 2}
+
+
+@dataclass
+class FusionBlock:
+    """fusion.hpp:21-33."""
+    id: str
+    mode: str
+    members: list
+    producer_stage: list = field(default_factory=list)
+    consumer_stage: list = field(default_factory=list)
+    stores_intermediate: bool = False
+
+    def fused(self) -> bool:
+        return self.mode != "unfused"
+
+
+@dataclass
+class ModeResult:
+    """fusion.hpp:41-46."""
+    accepted: bool
+    mode: str
+    escaping_intermediate: bool
+    reject_reason: str
+
+
+class Graph:
+    """A prepared graph: parse_graph + infer_shapes + fold_elementwise
+    (graph.cpp:221-256, :405-417, fusion.cpp:24-51), owned by the C++ library."""
+
+    def __init__(self, text: str):
+        h = ctypes.c_void_p()
+        check(lib().xlf_graph_parse(text.encode(), ctypes.byref(h)))
+        self._h = h
+        self.text = text
+        info = json.loads(text_call(lib().xlf_graph_json, h))
+        self.name = info["name"]
+        self.inputs = [(i["name"], tuple(i["shape"])) for i in info["inputs"]]
+        self.outputs = info["outputs"]
+        self.layers = info["layers"]
+        self._by_name = {l["name"]: l for l in self.layers}
+
+    @classmethod
+    def load(cls, path: str) -> "Graph":
+        with open(path) as fh:
+            return cls(fh.read())
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h and _lib._LIB is not None:
+            lib().xlf_graph_destroy(h)
+            self._h = None
+
+    def find_layer(self, name):
+        return self._by_name.get(name)
+
+    def shape_of(self, name):
+        for n, s in self.inputs:
+            if n == name:
+                return s
+        return tuple(self._by_name[name]["shape"])
+
+    def consumers_of(self, name):
+        return [l["name"] for l in self.layers if name in l["inputs"]]
+
+    def serialize(self) -> str:
+        return text_call(lib().xlf_graph_serialize, self._h)
+
+    def conv_weight_spans(self):
+        """(layer, offset, filter_count, bias_count) in save_weights order."""
+        out, pos = [], 0
+        for l in self.layers:
+            if l["kind"] != "conv":
+                continue
+            c = l["conv"]
+            nf = c["out_channels"] * (c["in_channels"] // c["group"]) * c["kernel"][0] * c["kernel"][1]
+            nb = c["out_channels"] if c["bias"] else 0
+            out.append((l["name"], pos, nf, nb))
+            pos += nf + nb
+        return out
+
+
+def parse_graph(text: str) -> Graph:
+    return Graph(text)
+
+
+def load_graph(path: str) -> Graph:
+    return Graph.load(path)
+
+
+def detect_fusion_blocks(g: Graph, partition: str = "reference") -> list:
+    """fusion.cpp:147-226 (partition='reference'); 'b200' adds pool
+    epilogues/prologues and all-reader splits; 'unfused' = one per layer."""
+    raw = json.loads(text_call(lib().xlf_blocks_json, g._h, PARTITIONS[partition]))
+    return [FusionBlock(**b) for b in raw]
+
+
+def block_assignment_report(g: Graph, partition: str = "reference") -> str:
+    return text_call(lib().xlf_block_report, g._h, PARTITIONS[partition])
+
+
+def classify_mode(g: Graph, candidate) -> ModeResult:
+    return ModeResult(**json.loads(text_call(lib().xlf_classify_mode, g._h, ",".join(candidate).encode())))
+
+
+def plan_tiling(g: Graph, block_id: str, tile, grid, device: str = "titan_xp") -> str:
+    """serialize_plan(plan_tiling(...)) text (tiling.cpp:240-419, :493-527)."""
+    return text_call(lib().xlf_plan_tiling, g._h, block_id.encode(), tile[0], tile[1], grid[0], grid[1], device.encode())
+
+
+def store_transactions(g: Graph, block_id: str):
+    f, u = ctypes.c_longlong(), ctypes.c_longlong()
+    check(lib().xlf_store_tx(g._h, block_id.encode(), ctypes.byref(f), ctypes.byref(u)))
+    return f.value, u.value
+
+
+def device_plan(g: Graph, partition: str = "b200", batch_hint: int = 1) -> dict:
+    """Host-only device program (kernel steps, tiles, tensor placement)."""
+    return json.loads(text_call(lib().xlf_device_plan_json, g._h, PARTITIONS[partition], batch_hint))
+
+
+def seeded_weights(g: Graph, seed: int) -> np.ndarray:
+    """tensor.cpp:42-62, flattened in save_weights order (tensor.cpp:64-95)."""
+    n = ctypes.c_size_t()
+    check(lib().xlf_seeded_weights(g._h, seed, None, 0, ctypes.byref(n)))
+    out = np.empty(n.value, np.float32)
+    check(lib().xlf_seeded_weights(g._h, seed, out.ctypes.data_as(ctypes.POINTER(ctypes.c_float)), n.value, ctypes.byref(n)))
+    return out
+
+
+def _stream_ptr(stream):
+    import torch
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return ctypes.c_void_p(s.cuda_stream)
+
+
+class Engine:
+    """Device executor (successor of simulate_graph, fused_exec.cpp:313-349)."""
+
+    def __init__(self, g: Graph, weights: np.ndarray, partition: str = "b200", precision: str = "fp32_exact",
+                 max_batch: int = 1, device: int = 0):
+        self.graph = g
+        w = np.ascontiguousarray(weights, np.float32)
+        h = ctypes.c_void_p()
+        check(lib().xlf_engine_create(g._h, device, PARTITIONS[partition], PRECISIONS[precision],
+                                      w.ctypes.data_as(ctypes.POINTER(ctypes.c_float)), w.size, max_batch, ctypes.byref(h)))
+        self._h = h
+        self.partition, self.precision, self.max_batch, self.device = partition, precision, max_batch, device
+        self.info = json.loads(text_call(lib().xlf_engine_json, h))
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h and _lib._LIB is not None:
+            lib().xlf_engine_destroy(h)
+            self._h = None
+
+    @property
+    def steps(self):
+        return self.info["plan"]["steps"]
+
+    @property
+    def launches_per_forward(self) -> int:
+        return lib().xlf_engine_launches_per_forward(self._h)
+
+    def set_input(self, x, stream=None):
+        """x: torch CUDA float32 NCHW [batch, C, H, W] (contiguous)."""
+        assert x.is_cuda and x.dtype.is_floating_point and x.is_contiguous()
+        check(lib().xlf_engine_set_input(self._h, ctypes.c_void_p(x.data_ptr()), x.shape[0], _stream_ptr(stream)))
+
+    def set_input_seeded(self, seed: int, batch: int, first_image: int = 0, stream=None):
+        check(lib().xlf_engine_set_input_seeded(self._h, seed, first_image, batch, _stream_ptr(stream)))
+
+    def forward(self, batch: int, use_graph: bool = True, stream=None):
+        check(lib().xlf_engine_forward(self._h, batch, int(use_graph), _stream_ptr(stream)))
+
+    def run_step(self, index: int, batch: int, stream=None):
+        check(lib().xlf_engine_run_step(self._h, index, batch, _stream_ptr(stream)))
+
+    def read(self, name: str, batch: int, stream=None):
+        import torch
+        shape = self.graph.shape_of(name)
+        out = torch.empty((batch,) + tuple(shape), dtype=torch.float32, device=f"cuda:{self.device}")
+        check(lib().xlf_engine_read(self._h, name.encode(), ctypes.c_void_p(out.data_ptr()), batch, _stream_ptr(stream)))
+        return out
+
+    def run_host(self, x: np.ndarray, name: str, stream=None) -> np.ndarray:
+        """End to end from host memory (H2D + forward + D2H), synchronous."""
+        x = np.ascontiguousarray(x, np.float32)
+        out = np.empty((x.shape[0],) + tuple(self.graph.shape_of(name)), np.float32)
+        f32p = ctypes.POINTER(ctypes.c_float)
+        check(lib().xlf_engine_run_host(self._h, x.ctypes.data_as(f32p), x.shape[0], name.encode(),
+                                        out.ctypes.data_as(f32p), _stream_ptr(stream)))
+        return out
+
+    def materialized(self):
+        return [n for n, t in self.info["plan"]["tensors"].items() if t["materialized"]]
+
+
+def simulate_graph(g: Graph, x, weights: np.ndarray, partition: str = "b200", precision: str = "fp32_exact",
+                   names=None):
+    """Runs the whole schedule on the GPU (fused_exec.cpp:313-349 semantics);
+    x: torch CUDA NCHW batch.  Returns {name: torch NCHW} for `names` (default:
+    graph outputs)."""
+    e = Engine(g, weights, partition, precision, max_batch=x.shape[0])
+    e.set_input(x)
+    e.forward(x.shape[0])
+    names = names or g.outputs
+    return {n: e.read(n, x.shape[0]) for n in names}
+
+
+def block_subgraph(g: Graph, block: FusionBlock) -> tuple:
+    """Graph text holding exactly one block: its external inputs become graph
+    inputs and its stored tensors (cost_model.cpp:21-41) graph outputs."""
+    members = [l for l in g.layers if l["name"] in block.members]
+    names = {l["name"] for l in members}
+    ext = []
+    for l in members:
+        for i in l["inputs"]:
+            if i not in names and i not in ext:
+                ext.append(i)
+    outs = list(block.consumer_stage) if block.fused() else list(block.members)
+    for p in block.producer_stage:
+        if g.consumers_of(p) and any(c not in names for c in g.consumers_of(p)) or p in g.outputs:
+            outs.append(p)
+    lines = [f"name {g.name}_{block.id}"]
+    for i in ext:
+        c, h, w = g.shape_of(i)
+        lines += ["input {", f"  name {i}", f"  shape [{c}, {h}, {w}]", "}"]
+    for l in members:
+        lines += ["layer {", f"  name {l['name']}", f"  kind {l['kind']}", f"  inputs [{', '.join(l['inputs'])}]"]
+        if l["kind"] == "conv":
+            c = l["conv"]
+            lines += [f"  out_channels {c['out_channels']}", f"  kernel [{c['kernel'][0]}, {c['kernel'][1]}]",
+                      f"  pad {c['pad']}", f"  stride {c['stride']}", f"  group {c['group']}",
+                      f"  bias {'true' if c['bias'] else 'false'}", f"  activation {'relu' if c['relu'] else 'none'}"]
+        if l["kind"] == "pool":
+            p = l["pool"]
+            lines += [f"  pool {p['kind']}", f"  kernel {p['kernel']}", f"  stride {p['stride']}", f"  pad {p['pad']}"]
+        lines.append("}")
+    lines += [f"output {o}" for o in outs]
+    return "\n".join(lines) + "\n", ext, outs
+
+
+def block_weights(g: Graph, block: FusionBlock, weights: np.ndarray) -> np.ndarray:
+    parts = []
+    for name, off, nf, nb in g.conv_weight_spans():
+        if name in block.members:
+            parts.append(weights[off:off + nf + nb])
+    return np.concatenate(parts) if parts else np.zeros(0, np.float32)
+
+
+def run_fused_block(g: Graph, block: FusionBlock, values: dict, weights: np.ndarray, precision: str = "fp32_exact"):
+    """fused_exec.cpp:30-311 on the GPU: reads the block's inputs from
+    ``values`` (torch CUDA NCHW), returns its stored tensors."""
+    if not block.fused():
+        raise XlfError(6, "run_fused_block: block is not fused")
+    text, ext, outs = block_subgraph(g, block)
+    sub = Graph(text)
+    if len(sub.inputs) != 1:
+        raise XlfError(3, "run_fused_block: blocks with more than one external input are run through simulate_graph")
+    x = values[ext[0]]
+    e = Engine(sub, block_weights(g, block, weights), "reference", precision, max_batch=x.shape[0])
+    e.set_input(x)
+    e.forward(x.shape[0])
+    return {o: e.read(o, x.shape[0]) for o in outs}

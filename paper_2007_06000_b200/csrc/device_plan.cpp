@@ -1,0 +1,677 @@
+#include "device_plan.hpp"
+
+#include <algorithm>
+#include <cmath>
+#include <functional>
+#include <set>
+#include <sstream>
+
+#include "common.hpp"
+
+namespace xlf {
+
+const char* to_string(Partition p) {
+    switch (p) {
+    case Partition::reference: return "reference";
+    case Partition::b200: return "b200";
+    case Partition::unfused: return "unfused";
+    }
+    return "?";
+}
+
+namespace {
+
+int round4(int c) { return (c + 3) & ~3; }
+int smem_pitch(int c) {
+    int p = round4(c) + 4;  // +4 floats: consecutive cells land on different banks
+    if (p % 32 == 0) p += 4;
+    return p;
+}
+
+std::map<std::string, int> topo_index(const Graph& g) {
+    std::map<std::string, int> idx;
+    int i = 0;
+    for (const Layer* l : topo_order(g)) idx[l->name] = i++;
+    return idx;
+}
+
+// Window of a layer as a reader of its input: kernel, stride, pad.
+struct Window {
+    int kh = 1, kw = 1, stride = 1, pad = 0;
+};
+Window window_of(const Layer& l) {
+    Window w;
+    if (l.kind == LayerKind::conv) w = {l.conv->kernel_h, l.conv->kernel_w, l.conv->stride, l.conv->pad};
+    else if (l.kind == LayerKind::pool) w = {l.pool->kernel, l.pool->kernel, l.pool->stride, l.pool->pad};
+    return w;
+}
+
+bool escapes(const Graph& g, const std::string& p, const std::vector<std::string>& members) {
+    if (g.is_output(p)) return true;
+    for (const std::string& c : g.consumers_of(p))
+        if (std::find(members.begin(), members.end(), c) == members.end()) return true;
+    return false;
+}
+
+FusionBlock make_block(int& next, FusionMode m, std::vector<std::string> prod, std::vector<std::string> cons, bool esc) {
+    FusionBlock b;
+    b.id = "b" + std::to_string(next++);
+    b.mode = m;
+    b.producer_stage = prod;
+    b.consumer_stage = cons;
+    b.members = prod;
+    b.members.insert(b.members.end(), cons.begin(), cons.end());
+    b.stores_intermediate = esc;
+    return b;
+}
+
+}  // namespace
+
+// B200 partition.  Pass 1 is the reference's greedy conv pass (merge > split >
+// straight) except that a split keeps EVERY compatible conv reader (an
+// inception-style reduce feeding three branches stays one block).  Pass 2
+// adds what the reference always rejects (fusion.cpp:66-69): a pool as the
+// consumer of a conv (conv -> bias -> ReLU -> pool, the paper's straight mode)
+// and a pool as the producer of a conv (inception's pool-projection branch).
+std::vector<FusionBlock> detect_fusion_blocks_b200(const Graph& g) {
+    if (!g.shapes_inferred()) fail(ErrorKind::internal, "detect_fusion_blocks requires inferred shapes");
+    std::vector<FusionBlock> blocks;
+    std::set<std::string> taken;
+    int next = 0;
+    auto is_free = [&](const std::string& n, LayerKind k) {
+        const Layer* l = g.find_layer(n);
+        return l && l->kind == k && !taken.count(n);
+    };
+    auto push = [&](FusionBlock b) {
+        for (const std::string& m : b.members) taken.insert(m);
+        blocks.push_back(std::move(b));
+    };
+    const auto order = topo_order(g);
+    for (const Layer* l : order) {
+        if (taken.count(l->name) || l->kind != LayerKind::conv) continue;
+        const auto readers = g.consumers_of(l->name);
+        bool merged = false;
+        for (const std::string& rn : readers) {
+            const Layer* r = g.find_layer(rn);
+            if (r->kind != LayerKind::add || taken.count(rn)) continue;
+            const std::string &a = r->inputs[0], &b = r->inputs[1];
+            if (a == b || !is_free(a, LayerKind::conv) || !is_free(b, LayerKind::conv)) continue;
+            std::vector<std::string> mem{a, b, rn};
+            push(make_block(next, FusionMode::merge, {a, b}, {rn}, escapes(g, a, mem) || escapes(g, b, mem)));
+            merged = true;
+            break;
+        }
+        if (merged) continue;
+        std::vector<std::string> convs;
+        for (const std::string& rn : readers)
+            if (is_free(rn, LayerKind::conv)) convs.push_back(rn);
+        if (convs.empty()) continue;
+        // Largest set of readers sharing stride and output extent (first wins ties).
+        std::vector<std::string> best;
+        for (const std::string& c0 : convs) {
+            const Layer* a = g.find_layer(c0);
+            std::vector<std::string> grp;
+            for (const std::string& c : convs) {
+                const Layer* b = g.find_layer(c);
+                if (b->conv->stride == a->conv->stride && b->out_shape->height == a->out_shape->height &&
+                    b->out_shape->width == a->out_shape->width)
+                    grp.push_back(c);
+            }
+            if (grp.size() > best.size()) best = grp;
+        }
+        std::vector<std::string> mem{l->name};
+        mem.insert(mem.end(), best.begin(), best.end());
+        push(make_block(next, best.size() >= 2 ? FusionMode::split : FusionMode::straight, {l->name}, best,
+                        escapes(g, l->name, mem)));
+    }
+    for (const Layer* l : order) {
+        if (taken.count(l->name) || g.is_output(l->name)) continue;
+        const auto readers = g.consumers_of(l->name);
+        if (readers.size() != 1) continue;
+        const std::string& c = readers[0];
+        if (l->kind == LayerKind::conv && is_free(c, LayerKind::pool))
+            push(make_block(next, FusionMode::straight, {l->name}, {c}, false));
+        else if (l->kind == LayerKind::pool && is_free(c, LayerKind::conv))
+            push(make_block(next, FusionMode::straight, {l->name}, {c}, false));
+    }
+    for (const Layer* l : order) {
+        if (taken.count(l->name)) continue;
+        FusionBlock b;
+        b.id = "b" + std::to_string(next++);
+        b.members = {l->name};
+        taken.insert(l->name);
+        blocks.push_back(std::move(b));
+    }
+    return blocks;
+}
+
+namespace {
+
+// Step for one block of any partition.
+StepSpec step_for_block(const Graph& g, const FusionBlock& b) {
+    StepSpec s;
+    s.id = b.id;
+    s.mode = b.mode;
+    s.layers = b.members;
+    if (!b.fused()) {
+        const Layer& l = *g.find_layer(b.members[0]);
+        switch (l.kind) {
+        case LayerKind::concat: s.kind = StepSpec::CONCAT_COPY, s.tag = "concat"; break;
+        case LayerKind::add: s.kind = StepSpec::ADD, s.tag = "add"; break;
+        case LayerKind::relu: s.kind = StepSpec::RELU, s.tag = "relu"; break;
+        default: {
+            s.kind = StepSpec::FUSED;
+            s.tag = to_string(l.kind);
+            OpSpec op;
+            op.layer = l.name, op.stage = 1, op.emit = true;
+            s.ops.push_back(op);
+        }
+        }
+        s.inputs = l.inputs;
+        s.out_h = l.out_shape->height, s.out_w = l.out_shape->width;
+        return s;
+    }
+    s.kind = StepSpec::FUSED;
+    s.tag = to_string(b.mode);
+    for (const std::string& p : b.producer_stage) {
+        const Layer& l = *g.find_layer(p);
+        OpSpec op;
+        op.layer = p, op.stage = 1, op.staged = true;
+        op.emit = op.own_only = escapes(g, p, b.members);
+        auto it = std::find(s.inputs.begin(), s.inputs.end(), l.inputs[0]);
+        if (it == s.inputs.end()) s.inputs.push_back(l.inputs[0]), op.xin = int(s.inputs.size()) - 1;
+        else op.xin = int(it - s.inputs.begin());
+        s.ops.push_back(op);
+    }
+    for (const std::string& c : b.consumer_stage) {
+        const Layer& l = *g.find_layer(c);
+        OpSpec op;
+        op.layer = c, op.stage = 2, op.emit = true;
+        for (const std::string& in : l.inputs)
+            for (size_t i = 0; i < b.producer_stage.size(); ++i)
+                if (b.producer_stage[i] == in) op.srcs.push_back(int(i));
+        s.ops.push_back(op);
+        if (g.find_layer(c)->kind == LayerKind::pool && s.tag == "straight") s.tag = "straight+pool";
+    }
+    const Layer& last = *g.find_layer(b.consumer_stage[0]);
+    s.out_h = last.out_shape->height, s.out_w = last.out_shape->width;
+    return s;
+}
+
+struct OpGeom {
+    int ext_h, ext_w, org_mul, org_sub, d;
+};
+
+// Lays out one fused step at tile (th, tw).  Returns shared bytes, or -1 when
+// the ops cannot share one tiling (differing strides / scales).
+long long layout_step(const Graph& g, const StepSpec& s, int th, int tw, FusedParams* fp) {
+    const int nops = int(s.ops.size());
+    if (nops > kMaxOps || s.inputs.size() > size_t(kMaxIns)) return -1;
+    std::vector<OpGeom> geo(size_t(nops), OpGeom{th, tw, 1, 0, 0});
+    // staged buffers: lead L, stride S, trails per producer op
+    std::vector<int> bufidx(size_t(nops), -1);
+    int nbufs = 0;
+    for (int i = 0; i < nops; ++i) {
+        const OpSpec& op = s.ops[size_t(i)];
+        if (op.stage != 1 || !op.staged) continue;
+        int S = -1, L = 0, Th = 1, Tw = 1;
+        bool add_reader = false;
+        for (const OpSpec& c : s.ops) {
+            if (c.stage != 2 || std::find(c.srcs.begin(), c.srcs.end(), i) == c.srcs.end()) continue;
+            const Layer& cl = *g.find_layer(c.layer);
+            if (cl.kind == LayerKind::add) {
+                add_reader = true;
+                continue;
+            }
+            const Window w = window_of(cl);
+            if (S >= 0 && S != w.stride) return -1;
+            S = w.stride;
+            L = std::max(L, w.pad);
+            Th = std::max(Th, w.kh - w.pad), Tw = std::max(Tw, w.kw - w.pad);
+        }
+        if (add_reader) {
+            if (S > 1 || L > 0) return -1;
+            S = 1;
+        }
+        if (S < 0) S = 1;
+        if (op.own_only) Th = std::max(Th, S), Tw = std::max(Tw, S);
+        geo[size_t(i)] = {(th - 1) * S + L + Th, (tw - 1) * S + L + Tw, S, L, 0};
+        bufidx[size_t(i)] = nbufs++;
+    }
+    if (nbufs > kMaxBufs) return -1;
+    // stage-2 offsets into their buffers
+    for (int i = 0; i < nops; ++i) {
+        const OpSpec& op = s.ops[size_t(i)];
+        if (op.stage != 2) continue;
+        const Layer& l = *g.find_layer(op.layer);
+        const int L = geo[size_t(op.srcs[0])].org_sub;
+        geo[size_t(i)].d = l.kind == LayerKind::add ? 0 : L - window_of(l).pad;
+    }
+    // block input regions
+    long long floats = 0;
+    std::vector<FIn> ins(s.inputs.size());
+    for (size_t xi = 0; xi < s.inputs.size(); ++xi) {
+        int scale = -1, XL = 0;
+        for (int i = 0; i < nops; ++i) {
+            const OpSpec& op = s.ops[size_t(i)];
+            if (op.stage != 1 || op.xin != int(xi)) continue;
+            const Window w = window_of(*g.find_layer(op.layer));
+            const int sc = geo[size_t(i)].org_mul * w.stride;
+            if (scale >= 0 && sc != scale) return -1;
+            scale = sc;
+            XL = std::max(XL, geo[size_t(i)].org_sub * w.stride + w.pad);
+        }
+        int eh = 0, ew = 0;
+        for (int i = 0; i < nops; ++i) {
+            const OpSpec& op = s.ops[size_t(i)];
+            if (op.stage != 1 || op.xin != int(xi)) continue;
+            const Window w = window_of(*g.find_layer(op.layer));
+            OpGeom& og = geo[size_t(i)];
+            og.d = XL - (og.org_sub * w.stride + w.pad);
+            eh = std::max(eh, og.d + (og.ext_h - 1) * w.stride + w.kh);
+            ew = std::max(ew, og.d + (og.ext_w - 1) * w.stride + w.kw);
+        }
+        const TensorShape xs = g.shape_of(s.inputs[xi]);
+        FIn& in = ins[xi];
+        in = FIn{};
+        in.c = s.ctile ? s.ctile : round4(xs.channels), in.h = xs.height, in.w = xs.width;
+        in.org_mul = scale < 0 ? 1 : scale, in.org_sub = XL;
+        in.ext_h = eh, in.ext_w = ew, in.cpitch = smem_pitch(in.c);
+        in.smem_off = int(floats);
+        floats += (long long)eh * ew * in.cpitch;
+    }
+    std::vector<FBuf> bufs(static_cast<size_t>(nbufs));
+    for (int i = 0; i < nops; ++i) {
+        if (bufidx[size_t(i)] < 0) continue;
+        const TensorShape os = *g.find_layer(s.ops[size_t(i)].layer)->out_shape;
+        FBuf& b = bufs[size_t(bufidx[size_t(i)])];
+        b.channels = os.channels, b.cpitch = smem_pitch(os.channels);
+        b.ext_h = geo[size_t(i)].ext_h, b.ext_w = geo[size_t(i)].ext_w;
+        b.smem_off = int(floats);
+        floats += (long long)b.ext_h * b.ext_w * b.cpitch;
+    }
+    if (fp) {
+        *fp = FusedParams{};
+        fp->nins = int(ins.size());
+        for (size_t i = 0; i < ins.size(); ++i) fp->in[i] = ins[i];
+        fp->tile_h = th, fp->tile_w = tw;
+        fp->out_h = s.out_h, fp->out_w = s.out_w;
+        fp->grid_h = (s.out_h + th - 1) / th, fp->grid_w = (s.out_w + tw - 1) / tw;
+        fp->nops = nops, fp->nbufs = nbufs, fp->smem_floats = int(floats);
+        fp->ctile = s.ctile;
+        fp->cgroups = s.ctile ? round4(g.shape_of(s.inputs[0]).channels) / s.ctile : 1;
+        for (int i = 0; i < nbufs; ++i) fp->bufs[i] = bufs[size_t(i)];
+        for (int i = 0; i < nops; ++i) {
+            const OpSpec& os = s.ops[size_t(i)];
+            const Layer& l = *g.find_layer(os.layer);
+            FOp& o = fp->ops[i];
+            o = FOp{};
+            o.stage = os.stage, o.xin = os.xin;
+            o.src = os.srcs.empty() ? -1 : bufidx[size_t(os.srcs[0])];
+            o.src2 = os.srcs.size() > 1 ? bufidx[size_t(os.srcs[1])] : -1;
+            o.buf = bufidx[size_t(i)];
+            o.emit = os.emit, o.own_only = os.own_only;
+            const TensorShape out = *l.out_shape;
+            o.H = out.height, o.W = out.width;
+            o.cout = out.channels, o.cout_pad = round4(out.channels);
+            const Window w = window_of(l);
+            o.kh = w.kh, o.kw = w.kw, o.stride = w.stride, o.pad = w.pad;
+            o.group = 1;
+            if (l.kind == LayerKind::conv) {
+                o.kind = OP_CONV;
+                o.cin = l.conv->in_channels, o.group = l.conv->group, o.relu = l.conv->activation == Activation::relu;
+            } else if (l.kind == LayerKind::pool) {
+                o.kind = l.pool->kind == PoolKind::max ? OP_MAXPOOL : OP_AVGPOOL;
+                o.cin = out.channels;
+                if (s.ctile) o.cout_pad = s.ctile;
+            } else {
+                o.kind = OP_ADD;
+                o.cin = out.channels;
+            }
+            o.d = geo[size_t(i)].d;
+            o.ext_h = geo[size_t(i)].ext_h, o.ext_w = geo[size_t(i)].ext_w;
+            o.org_mul = geo[size_t(i)].org_mul, o.org_sub = geo[size_t(i)].org_sub;
+        }
+    }
+    return floats * 4;
+}
+
+double macs_per_output(const Layer& l) {
+    if (l.kind == LayerKind::conv) return double(l.conv->macs_per_output());
+    if (l.kind == LayerKind::pool) return double(l.pool->kernel) * l.pool->kernel;
+    return 1.0;
+}
+
+// Tile choice: minimise modelled time = waves x per-CTA work / occupancy
+// benefit, with per-CTA work including halo recompute and partial-tile waste.
+bool choose_tile_at(const Graph& g, StepSpec& s, int batch_hint, int smem_budget);
+
+// Pool-only steps whose full-channel region never fits shared memory (a
+// global average pool over 13x13x1000) are tiled over channels as well.
+bool choose_tile(const Graph& g, StepSpec& s, int batch_hint, int smem_budget) {
+    s.ctile = 0;
+    if (choose_tile_at(g, s, batch_hint, smem_budget)) return true;
+    bool pools = s.inputs.size() == 1;
+    for (const OpSpec& op : s.ops) pools &= op.stage == 1 && g.find_layer(op.layer)->kind == LayerKind::pool;
+    if (!pools) return false;
+    const int C = round4(g.shape_of(s.inputs[0]).channels);
+    for (int ct = C - 4; ct >= 4; ct -= 4) {
+        if (C % ct) continue;
+        s.ctile = ct;
+        if (choose_tile_at(g, s, batch_hint, smem_budget)) return true;
+    }
+    s.ctile = 0;
+    return false;
+}
+
+bool choose_tile_at(const Graph& g, StepSpec& s, int batch_hint, int smem_budget) {
+    double best = 1e300;
+    int bh = 0, bw = 0, bsm = 0;
+    const int lim_h = std::min(s.out_h, 32), lim_w = std::min(s.out_w, 32);
+    for (int th = 1; th <= lim_h; ++th)
+        for (int tw = 1; tw <= lim_w; ++tw) {
+            FusedParams fp;
+            const long long sm = layout_step(g, s, th, tw, &fp);
+            if (sm < 0 || sm > smem_budget) continue;
+            double work = 0;
+            for (int i = 0; i < fp.nops; ++i) {
+                const FOp& o = fp.ops[i];
+                work += double(o.ext_h) * o.ext_w * o.cout_pad * macs_per_output(*g.find_layer(s.ops[size_t(i)].layer));
+            }
+            for (int i = 0; i < fp.nins; ++i) work += double(fp.in[i].ext_h) * fp.in[i].ext_w * fp.in[i].c;
+            const double ctas = double(fp.grid_h) * fp.grid_w * fp.cgroups * std::max(batch_hint, 1);
+            const int occ = std::max(1, std::min(8, int((228 * 1024) / (sm + 1024))));
+            const double waves = std::ceil(ctas / (148.0 * occ));
+            const double t = waves * work * occ / std::min(double(occ), 2.0) + 2000.0 * waves;
+            if (t < best * 0.999 || (t <= best * 1.001 && long(th) * tw > long(bh) * bw)) best = t, bh = th, bw = tw, bsm = int(sm);
+        }
+    if (!bh) return false;
+    s.tile_h = bh, s.tile_w = bw, s.smem_bytes = bsm;
+    return true;
+}
+
+void fill_stats(const Graph& g, const DevicePlan& plan, StepSpec& s) {
+    s.macs = 0, s.bytes_algorithmic = 0, s.macs_executed = 0;
+    for (const std::string& in : s.inputs) s.bytes_algorithmic += double(g.shape_of(in).elements()) * 4;
+    if (s.kind == StepSpec::CONCAT_COPY) {
+        s.bytes_algorithmic *= 2;
+        return;
+    }
+    for (const OpSpec& op : s.ops) {
+        const Layer& l = *g.find_layer(op.layer);
+        if (l.kind == LayerKind::conv) {
+            s.macs += double(l.out_shape->elements()) * double(l.conv->macs_per_output());
+            s.bytes_algorithmic += double(l.conv->weight_count() + l.conv->bias_count()) * 4;
+        }
+        if (op.emit) s.bytes_algorithmic += double(l.out_shape->elements()) * 4;
+    }
+    if (s.kind != StepSpec::FUSED) {
+        s.bytes_algorithmic += double(g.shape_of(s.layers[0]).elements()) * 4;
+        return;
+    }
+    FusedParams fp;
+    layout_step(g, s, s.tile_h, s.tile_w, &fp);
+    const double tiles = double(fp.grid_h) * fp.grid_w;
+    for (int i = 0; i < fp.nops; ++i) {
+        const Layer& l = *g.find_layer(s.ops[size_t(i)].layer);
+        if (l.kind == LayerKind::conv)
+            s.macs_executed += tiles * fp.ops[i].ext_h * fp.ops[i].ext_w * l.out_shape->channels * double(l.conv->macs_per_output());
+    }
+    (void)plan;
+}
+
+}  // namespace
+
+DevicePlan plan_device(const Graph& g, Partition part, int batch_hint, int smem_budget) {
+    if (!g.shapes_inferred()) fail(ErrorKind::internal, "plan_device requires inferred shapes");
+    DevicePlan plan;
+    plan.partition = part;
+    if (part == Partition::reference) plan.blocks = detect_fusion_blocks(g);
+    else if (part == Partition::b200) plan.blocks = detect_fusion_blocks_b200(g);
+    else {
+        int next = 0;
+        for (const Layer* l : topo_order(g)) {
+            FusionBlock b;
+            b.id = "b" + std::to_string(next++);
+            b.members = {l->name};
+            plan.blocks.push_back(b);
+        }
+    }
+    // Execute in topological order of each block's first member (fused_exec.cpp:322-332).
+    const auto tix = topo_index(g);
+    auto first = [&](const FusionBlock& b) {
+        int m = 1 << 30;
+        for (const std::string& n : b.members) m = std::min(m, tix.at(n));
+        return m;
+    };
+    std::vector<FusionBlock> ordered = plan.blocks;
+    std::stable_sort(ordered.begin(), ordered.end(), [&](const FusionBlock& a, const FusionBlock& b) { return first(a) < first(b); });
+
+    std::vector<StepSpec> steps;
+    for (const FusionBlock& b : ordered) {
+        StepSpec s = step_for_block(g, b);
+        if (s.kind == StepSpec::FUSED && !choose_tile(g, s, batch_hint, smem_budget)) {
+            if (!b.fused()) fail(ErrorKind::infeasible, "layer " + b.members[0] + " does not fit shared memory at any tile");
+            // Fused block infeasible on chip: run its members as singletons.
+            for (const std::string& m : b.members) {
+                FusionBlock one;
+                one.id = b.id + "." + m;
+                one.members = {m};
+                StepSpec t = step_for_block(g, one);
+                if (t.kind == StepSpec::FUSED && !choose_tile(g, t, batch_hint, smem_budget))
+                    fail(ErrorKind::infeasible, "layer " + m + " does not fit shared memory at any tile");
+                steps.push_back(t);
+            }
+            continue;
+        }
+        steps.push_back(s);
+    }
+
+    // B200: shared-input multi-branch kernels.  Steps whose stage-1 ops all
+    // read the same single tensor and whose outputs share one extent run as
+    // one kernel (one staged input region), if the union still fits.
+    if (part == Partition::b200) {
+        std::vector<char> gone(steps.size(), 0);
+        for (size_t i = 0; i < steps.size(); ++i) {
+            if (gone[i] || steps[i].kind != StepSpec::FUSED || steps[i].inputs.size() != 1) continue;
+            for (size_t j = i + 1; j < steps.size(); ++j) {
+                if (gone[j] || steps[j].kind != StepSpec::FUSED || steps[j].inputs != steps[i].inputs) continue;
+                if (steps[j].out_h != steps[i].out_h || steps[j].out_w != steps[i].out_w) continue;
+                StepSpec m = steps[i];
+                const int base = int(m.ops.size());
+                for (OpSpec op : steps[j].ops) {
+                    for (int& si : op.srcs) si += base;
+                    m.ops.push_back(op);
+                }
+                std::stable_sort(m.ops.begin(), m.ops.end(), [](const OpSpec& a, const OpSpec& b) { return a.stage < b.stage; });
+                // re-map srcs after the stage sort
+                std::vector<std::string> names;
+                for (const OpSpec& op : m.ops) names.push_back(op.layer);
+                for (OpSpec& op : m.ops) {
+                    if (op.stage != 2) continue;
+                    const Layer& l = *g.find_layer(op.layer);
+                    op.srcs.clear();
+                    for (const std::string& in : l.inputs)
+                        for (size_t k = 0; k < names.size(); ++k)
+                            if (names[k] == in) op.srcs.push_back(int(k));
+                }
+                m.layers.insert(m.layers.end(), steps[j].layers.begin(), steps[j].layers.end());
+                m.id += "+" + steps[j].id;
+                m.tag = "multi-branch";
+                m.mode = FusionMode::merge;
+                if (!choose_tile(g, m, batch_hint, smem_budget)) continue;
+                steps[i] = m;
+                gone[j] = 1;
+            }
+        }
+        std::vector<StepSpec> kept;
+        for (size_t i = 0; i < steps.size(); ++i)
+            if (!gone[i]) kept.push_back(steps[i]);
+        steps.swap(kept);
+    }
+
+    // Which tensors exist in HBM: graph inputs, every emitted op output, every
+    // non-fused singleton output.
+    std::set<std::string> materialized;
+    for (const GraphInput& in : g.inputs) materialized.insert(in.name);
+    for (const StepSpec& s : steps) {
+        if (s.kind != StepSpec::FUSED) materialized.insert(s.layers[0]);
+        for (const OpSpec& op : s.ops)
+            if (op.emit) materialized.insert(op.layer);
+    }
+    // Concat elision (B200): every input of a concat that is consumed by the
+    // concat alone becomes a channel-offset view of the concat's allocation.
+    std::map<std::string, std::pair<std::string, int>> view_of;  // tensor -> (concat, channel offset)
+    std::set<std::string> elided;
+    if (part == Partition::b200) {
+        for (const Layer& l : g.layers) {
+            if (l.kind != LayerKind::concat || !materialized.count(l.name)) continue;
+            bool ok = true;
+            int off = 0;
+            for (const std::string& in : l.inputs) {
+                const Layer* p = g.find_layer(in);
+                const TensorShape s = g.shape_of(in);
+                ok &= p != nullptr && !g.is_output(in) && g.consumers_of(in).size() == 1 && materialized.count(in) &&
+                      s.channels % 4 == 0 && !view_of.count(in);
+                off += s.channels;
+            }
+            if (!ok) continue;
+            off = 0;
+            for (const std::string& in : l.inputs) {
+                view_of[in] = {l.name, off};
+                off += g.shape_of(in).channels;
+            }
+            elided.insert(l.name);
+        }
+        std::vector<StepSpec> kept;
+        for (StepSpec& s : steps)
+            if (!(s.kind == StepSpec::CONCAT_COPY && elided.count(s.layers[0]))) kept.push_back(s);
+        steps.swap(kept);
+    }
+    std::function<TensorSlot(const std::string&)> resolve = [&](const std::string& n) -> TensorSlot {
+        auto it = plan.tensors.find(n);
+        if (it != plan.tensors.end()) return it->second;
+        const TensorShape s = g.shape_of(n);
+        TensorSlot t;
+        t.materialized = true, t.C = s.channels, t.H = s.height, t.W = s.width;
+        auto v = view_of.find(n);
+        if (v != view_of.end()) {
+            const TensorSlot host = resolve(v->second.first);
+            t.alloc = host.alloc, t.cstride = host.cstride, t.coff = host.coff + v->second.second;
+        } else {
+            t.alloc = int(plan.alloc_floats.size()), t.cstride = round4(s.channels), t.coff = 0;
+            plan.alloc_floats.push_back((long long)s.height * s.width * t.cstride);
+        }
+        plan.tensors[n] = t;
+        return t;
+    };
+    for (const GraphInput& in : g.inputs) resolve(in.name);
+    for (const Layer* l : topo_order(g))
+        if (materialized.count(l->name)) resolve(l->name);
+    for (const Layer& l : g.layers)
+        if (!plan.tensors.count(l.name)) plan.tensors[l.name] = TensorSlot{};
+
+    long long woff = 0;
+    for (const Layer& l : g.layers) {
+        if (l.kind != LayerKind::conv) continue;
+        const ConvParams& c = *l.conv;
+        plan.w_off[l.name] = woff;
+        woff += (long long)(c.in_channels / c.group) * c.kernel_h * c.kernel_w * round4(c.out_channels);
+        plan.b_off[l.name] = woff;
+        woff += round4(c.out_channels);
+    }
+    plan.weight_floats = woff;
+    for (StepSpec& s : steps) fill_stats(g, plan, s);
+    plan.steps = steps;
+    return plan;
+}
+
+std::vector<float> pack_weights(const Graph& g, const DevicePlan& plan, const float* flat, size_t count) {
+    std::vector<float> out(size_t(plan.weight_floats), 0.0f);
+    size_t pos = 0;
+    for (const Layer& l : g.layers) {
+        if (l.kind != LayerKind::conv) continue;
+        const ConvParams& c = *l.conv;
+        const int cin_g = c.in_channels / c.group, cp = round4(c.out_channels);
+        const size_t nf = size_t(c.weight_count()), nb = size_t(c.bias_count());
+        if (pos + nf + nb > count) fail(ErrorKind::validation, "weights: stream too short for layer '" + l.name + "'");
+        float* w = out.data() + plan.w_off.at(l.name);
+        for (int oc = 0; oc < c.out_channels; ++oc)
+            for (int ic = 0; ic < cin_g; ++ic)
+                for (int y = 0; y < c.kernel_h; ++y)
+                    for (int x = 0; x < c.kernel_w; ++x)
+                        w[((size_t(ic) * c.kernel_h + y) * c.kernel_w + x) * cp + oc] =
+                            flat[pos + ((size_t(oc) * cin_g + ic) * c.kernel_h + y) * c.kernel_w + x];
+        pos += nf;
+        float* b = out.data() + plan.b_off.at(l.name);
+        for (size_t i = 0; i < nb; ++i) b[i] = flat[pos + i];
+        pos += nb;
+    }
+    if (pos != count)
+        fail(ErrorKind::validation, "weights: stream holds " + std::to_string(count) + " floats, graph needs " + std::to_string(pos));
+    return out;
+}
+
+FusedParams make_params(const Graph& g, const DevicePlan& plan, const StepSpec& s,
+                        const std::vector<float*>& alloc_base, const float* wbase) {
+    FusedParams fp;
+    if (layout_step(g, s, s.tile_h, s.tile_w, &fp) < 0) fail(ErrorKind::internal, "step " + s.id + ": layout failed");
+    for (int i = 0; i < fp.nins; ++i) {
+        const TensorSlot& t = plan.tensors.at(s.inputs[size_t(i)]);
+        fp.in[i].x = alloc_base[size_t(t.alloc)];
+        fp.in[i].cstride = t.cstride, fp.in[i].coff = t.coff;
+    }
+    for (int i = 0; i < fp.nops; ++i) {
+        const OpSpec& os = s.ops[size_t(i)];
+        FOp& o = fp.ops[i];
+        if (o.kind == OP_CONV) {
+            o.w = wbase + plan.w_off.at(os.layer);
+            o.b = wbase + plan.b_off.at(os.layer);
+        }
+        if (o.emit) {
+            const TensorSlot& t = plan.tensors.at(os.layer);
+            o.out = alloc_base[size_t(t.alloc)];
+            o.out_cstride = t.cstride, o.out_coff = t.coff;
+        }
+    }
+    return fp;
+}
+
+std::string describe_plan_json(const Graph& g, const DevicePlan& plan) {
+    std::ostringstream os;
+    auto q = [](const std::string& s) { return "\"" + s + "\""; };
+    os << "{\"partition\":" << q(to_string(plan.partition)) << ",\"steps\":[";
+    for (size_t i = 0; i < plan.steps.size(); ++i) {
+        const StepSpec& s = plan.steps[i];
+        static const char* kinds[] = {"fused", "concat_copy", "add", "relu"};
+        os << (i ? "," : "") << "{\"id\":" << q(s.id) << ",\"kind\":" << q(kinds[s.kind]) << ",\"tag\":" << q(s.tag)
+           << ",\"mode\":" << q(to_string(s.mode)) << ",\"tile\":[" << s.tile_h << "," << s.tile_w
+           << "],\"out\":[" << s.out_h << "," << s.out_w << "],\"smem_bytes\":" << s.smem_bytes << ",\"macs\":" << s.macs
+           << ",\"macs_executed\":" << s.macs_executed << ",\"bytes_algorithmic\":" << s.bytes_algorithmic << ",\"inputs\":[";
+        for (size_t k = 0; k < s.inputs.size(); ++k) os << (k ? "," : "") << q(s.inputs[k]);
+        os << "],\"layers\":[";
+        for (size_t k = 0; k < s.layers.size(); ++k) os << (k ? "," : "") << q(s.layers[k]);
+        os << "],\"ops\":[";
+        for (size_t k = 0; k < s.ops.size(); ++k) {
+            const OpSpec& o = s.ops[k];
+            os << (k ? "," : "") << "{\"layer\":" << q(o.layer) << ",\"stage\":" << o.stage << ",\"staged\":"
+               << (o.staged ? "true" : "false") << ",\"emit\":" << (o.emit ? "true" : "false") << "}";
+        }
+        os << "]}";
+    }
+    os << "],\"tensors\":{";
+    bool firstt = true;
+    for (const auto& [n, t] : plan.tensors) {
+        os << (firstt ? "" : ",") << q(n) << ":{\"materialized\":" << (t.materialized ? "true" : "false")
+           << ",\"alloc\":" << t.alloc << ",\"cstride\":" << t.cstride << ",\"coff\":" << t.coff << ",\"shape\":[" << t.C
+           << "," << t.H << "," << t.W << "]}";
+        firstt = false;
+    }
+    os << "},\"alloc_floats\":[";
+    for (size_t i = 0; i < plan.alloc_floats.size(); ++i) os << (i ? "," : "") << plan.alloc_floats[i];
+    os << "],\"weight_floats\":" << plan.weight_floats << "}";
+    (void)g;
+    return os.str();
+}
+
+}  // namespace xlf

@@ -1,0 +1,88 @@
+// Device program: how a prepared graph is executed by the sm_100a kernels.
+//
+// The planner turns a partition (reference FusionBlocks, the B200
+// extension, or one-kernel-per-layer) into an ordered list of kernel steps
+// whose ops are the graph's layers, plus a tensor table saying where every
+// materialised tensor lives in HBM (NHWC, channel pitch padded to 4 floats;
+// tensors consumed only by a concat are views into the concat's allocation
+// in the B200 partition).  Fused intermediates have no HBM slot at all.
+#pragma once
+
+#include <map>
+#include <string>
+#include <vector>
+
+#include "fused_params.hpp"
+#include "fusion.hpp"
+#include "graph.hpp"
+
+namespace xlf {
+
+enum class Partition { reference = 0, b200 = 1, unfused = 2 };
+const char* to_string(Partition p);
+
+struct TensorSlot {
+    bool materialized = false;
+    int alloc = -1;               // allocation index
+    int cstride = 0, coff = 0;    // channel pitch of the allocation, offset of this tensor
+    int C = 0, H = 0, W = 0;
+};
+
+struct OpSpec {
+    std::string layer;
+    int stage = 1;
+    bool staged = false;     // result kept in a shared buffer
+    bool emit = false;       // result stored to HBM
+    bool own_only = false;   // staged + emitted escaping intermediate
+    int xin = 0;             // stage 1: which block input it reads
+    std::vector<int> srcs;   // stage 2: indices (into ops) of the stage-1 ops it reads
+};
+
+struct StepSpec {
+    enum Kind { FUSED, CONCAT_COPY, ADD, RELU } kind = FUSED;
+    std::string id;                    // block id (partition's naming)
+    FusionMode mode = FusionMode::unfused;
+    std::string tag;                   // "split", "straight+pool", "multi-branch", "conv", ...
+    std::vector<std::string> inputs;   // block inputs (tensor names)
+    std::vector<OpSpec> ops;
+    std::vector<std::string> layers;   // every layer executed by this step
+    int out_h = 0, out_w = 0;
+    int tile_h = 0, tile_w = 0;
+    int ctile = 0;                     // channel tile of pool-only steps (0 = all)
+    int smem_bytes = 0;
+    // statistics (per image)
+    double macs = 0;            // algorithmic MACs (no halo recompute)
+    double macs_executed = 0;   // including halo recompute and edge waste
+    double bytes_algorithmic = 0;  // inputs once + weights once + outputs once (fp32)
+};
+
+struct DevicePlan {
+    Partition partition = Partition::b200;
+    std::vector<FusionBlock> blocks;     // the partition, reference vocabulary
+    std::vector<StepSpec> steps;
+    std::map<std::string, TensorSlot> tensors;
+    std::vector<long long> alloc_floats;  // per image
+    // weights: offsets (floats) into one packed device buffer, per conv layer
+    std::map<std::string, long long> w_off, b_off;
+    long long weight_floats = 0;
+};
+
+// Blocks of the B200 partition (reference vocabulary: producer/consumer stages).
+std::vector<FusionBlock> detect_fusion_blocks_b200(const Graph& g);
+
+// batch_hint steers the tile choice (enough CTAs to fill 148 SMs).
+DevicePlan plan_device(const Graph& g, Partition part, int batch_hint = 1, int smem_budget_bytes = 227 * 1024);
+
+// Packs reference-layout weights (save_weights stream order, tensor.cpp:64-95)
+// into the device layout of `plan`: per conv [cin/group][kh][kw][cout_pad4]
+// followed by bias[cout_pad4].
+std::vector<float> pack_weights(const Graph& g, const DevicePlan& plan, const float* flat, size_t count);
+
+// Builds the launch descriptor of a FUSED step; `base(t)` returns the device
+// address of image 0 of tensor slot allocation, `wbase` the packed weights.
+FusedParams make_params(const Graph& g, const DevicePlan& plan, const StepSpec& s,
+                        const std::vector<float*>& alloc_base, const float* wbase);
+
+std::string describe_plan_json(const Graph& g, const DevicePlan& plan);
+
+}  // namespace xlf

@@ -1,0 +1,212 @@
+#include "engine.hpp"
+
+#include <algorithm>
+#include <sstream>
+
+#include "common.hpp"
+#include "fused_params.hpp"
+
+namespace xlf {
+
+// kernels_fp32.cu
+cudaError_t init_fused_fp32();
+cudaError_t launch_fused_fp32(const FusedParams& P, int batch, bool exact, cudaStream_t st);
+cudaError_t launch_concat_copy(const float* src, int scs, int sco, float* dst, int dcs, int dco, int C, long long pixels, cudaStream_t st);
+cudaError_t launch_eltwise(int op, const float* a, int acs, int aco, const float* b, int bcs, int bco, float* o, int ocs, int oco,
+                           int C, long long pixels, cudaStream_t st);
+cudaError_t launch_nchw_to_nhwc(const float* src, float* dst, int N, int C, int H, int W, int cs, cudaStream_t st);
+cudaError_t launch_nhwc_to_nchw(const float* src, int cs, int coff, float* dst, int N, int C, int H, int W, cudaStream_t st);
+cudaError_t launch_seeded_nhwc(float* dst, unsigned long long seed, unsigned long long first_image, int N, int C, int H, int W,
+                               int cs, cudaStream_t st);
+
+const char* to_string(Precision p) {
+    switch (p) {
+    case Precision::fp32_exact: return "fp32_exact";
+    case Precision::fp32: return "fp32";
+    case Precision::bf16: return "bf16";
+    }
+    return "?";
+}
+
+void cuda_check(cudaError_t e, const char* what) {
+    if (e != cudaSuccess) fail(ErrorKind::cuda, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+float seeded_value(uint64_t seed, uint64_t i) {
+    uint64_t z = (seed ? seed : 0x9e3779b97f4a7c15ULL) + (i + 1) * 0x9e3779b97f4a7c15ULL;
+    z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ULL;
+    z = (z ^ (z >> 27)) * 0x94d049bb133111ebULL;
+    z = z ^ (z >> 31);
+    return static_cast<float>(z >> 40) * (1.0f / 16777216.0f) - 0.5f;
+}
+
+std::vector<float> seeded_weights(const Graph& g, uint64_t seed) {
+    const uint64_t ws = seed ^ 0xabcdef1234567890ULL;
+    std::vector<float> out;
+    for (const Layer& l : g.layers) {
+        if (l.kind != LayerKind::conv) continue;
+        if (l.conv->in_channels <= 0) fail(ErrorKind::internal, "seeded_weights: run infer_shapes first (layer '" + l.name + "')");
+        const size_t n = size_t(l.conv->weight_count() + l.conv->bias_count());
+        const size_t base = out.size();
+        out.resize(base + n);
+        for (size_t i = 0; i < n; ++i) out[base + i] = seeded_value(ws, base + i);
+    }
+    return out;
+}
+
+Engine::Engine(const Graph& g, int device, Partition part, Precision prec, const float* weights, size_t nweights, int max_batch)
+    : g_(g), device_(device), prec_(prec), max_batch_(max_batch) {
+    if (!g_.shapes_inferred()) fail(ErrorKind::internal, "engine: graph shapes not inferred");
+    if (max_batch < 1) fail(ErrorKind::validation, "engine: max_batch must be >= 1");
+    if (prec == Precision::bf16) fail(ErrorKind::validation, "engine: bf16 path not built in this library");
+    if (g_.inputs.size() != 1) fail(ErrorKind::validation, "engine: graphs with exactly one input are supported");
+    cuda_check(cudaSetDevice(device), "cudaSetDevice");
+    plan_ = plan_device(g_, part, max_batch);
+    cuda_check(init_fused_fp32(), "kernel attributes");
+    std::vector<float> packed = pack_weights(g_, plan_, weights, nweights);
+    cuda_check(cudaMalloc(&weights_, std::max<size_t>(packed.size(), 1) * 4), "cudaMalloc(weights)");
+    cuda_check(cudaMemcpy(weights_, packed.data(), packed.size() * 4, cudaMemcpyHostToDevice), "weights H2D");
+    for (long long f : plan_.alloc_floats) {
+        float* p = nullptr;
+        const size_t bytes = size_t(f) * size_t(max_batch) * 4;
+        cuda_check(cudaMalloc(&p, bytes), "cudaMalloc(activations)");
+        cuda_check(cudaMemset(p, 0, bytes), "cudaMemset");  // channel padding stays zero
+        allocs_.push_back(p);
+    }
+    size_t most = 0;
+    for (const auto& [n, t] : plan_.tensors)
+        if (t.materialized) most = std::max(most, size_t(t.C) * t.H * t.W);
+    staging_floats_ = most * size_t(max_batch);
+    cuda_check(cudaMalloc(&staging_, staging_floats_ * 4), "cudaMalloc(staging)");
+    params_.resize(plan_.steps.size());
+    for (size_t i = 0; i < plan_.steps.size(); ++i)
+        if (plan_.steps[i].kind == StepSpec::FUSED) params_[i] = make_params(g_, plan_, plan_.steps[i], allocs_, weights_);
+}
+
+Engine::~Engine() {
+    cudaSetDevice(device_);
+    for (auto& [b, ge] : graphs_) cudaGraphExecDestroy(ge);
+    for (float* p : allocs_) cudaFree(p);
+    cudaFree(weights_);
+    cudaFree(staging_);
+}
+
+const TensorSlot& Engine::slot(const std::string& n) const {
+    auto it = plan_.tensors.find(n);
+    if (it == plan_.tensors.end()) fail(ErrorKind::validation, "no tensor '" + n + "'");
+    if (!it->second.materialized) fail(ErrorKind::validation, "tensor '" + n + "' is a fused intermediate (never stored to HBM)");
+    return it->second;
+}
+
+void Engine::set_input_nchw(const std::string& name, const float* d, int batch, cudaStream_t st) {
+    if (batch < 1 || batch > max_batch_) fail(ErrorKind::validation, "batch out of range");
+    const TensorSlot& t = slot(name);
+    cuda_check(launch_nchw_to_nhwc(d, allocs_[size_t(t.alloc)], batch, t.C, t.H, t.W, t.cstride, st), "nchw_to_nhwc");
+}
+
+void Engine::set_input_seeded(const std::string& name, uint64_t seed, uint64_t first_image, int batch, cudaStream_t st) {
+    if (batch < 1 || batch > max_batch_) fail(ErrorKind::validation, "batch out of range");
+    const TensorSlot& t = slot(name);
+    cuda_check(launch_seeded_nhwc(allocs_[size_t(t.alloc)], seed, first_image, batch, t.C, t.H, t.W, t.cstride, st), "seeded fill");
+}
+
+void Engine::launch_step(size_t i, int batch, cudaStream_t st) {
+    const StepSpec& s = plan_.steps[i];
+    switch (s.kind) {
+    case StepSpec::FUSED:
+        cuda_check(launch_fused_fp32(params_[i], batch, prec_ == Precision::fp32_exact, st), "fused block");
+        return;
+    case StepSpec::CONCAT_COPY: {
+        const TensorSlot& o = slot(s.layers[0]);
+        int off = 0;
+        for (const std::string& in : s.inputs) {
+            const TensorSlot& t = slot(in);
+            cuda_check(launch_concat_copy(allocs_[size_t(t.alloc)], t.cstride, t.coff, allocs_[size_t(o.alloc)], o.cstride,
+                                          o.coff + off, t.C, (long long)batch * t.H * t.W, st),
+                       "concat copy");
+            off += t.C;
+        }
+        return;
+    }
+    case StepSpec::ADD:
+    case StepSpec::RELU: {
+        const TensorSlot& o = slot(s.layers[0]);
+        const TensorSlot& a = slot(s.inputs[0]);
+        const TensorSlot& b = s.kind == StepSpec::ADD ? slot(s.inputs[1]) : a;
+        cuda_check(launch_eltwise(s.kind == StepSpec::ADD ? 0 : 1, allocs_[size_t(a.alloc)], a.cstride, a.coff,
+                                  allocs_[size_t(b.alloc)], b.cstride, b.coff, allocs_[size_t(o.alloc)], o.cstride, o.coff, o.C,
+                                  (long long)batch * o.H * o.W, st),
+                   "eltwise");
+        return;
+    }
+    }
+}
+
+void Engine::run_step(int index, int batch, cudaStream_t st) {
+    if (index < 0 || index >= num_steps()) fail(ErrorKind::validation, "step index out of range");
+    if (batch < 1 || batch > max_batch_) fail(ErrorKind::validation, "batch out of range");
+    cuda_check(cudaSetDevice(device_), "cudaSetDevice");
+    launch_step(size_t(index), batch, st);
+}
+
+void Engine::forward(int batch, cudaStream_t st, bool use_graph) {
+    if (batch < 1 || batch > max_batch_) fail(ErrorKind::validation, "batch out of range");
+    cuda_check(cudaSetDevice(device_), "cudaSetDevice");
+    if (!use_graph) {
+        for (size_t i = 0; i < plan_.steps.size(); ++i) launch_step(i, batch, st);
+        return;
+    }
+    auto it = graphs_.find(batch);
+    if (it == graphs_.end()) {
+        cudaGraph_t graph;
+        cuda_check(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal), "begin capture");
+        try {
+            for (size_t i = 0; i < plan_.steps.size(); ++i) launch_step(i, batch, st);
+        } catch (...) {
+            cudaStreamEndCapture(st, &graph);
+            throw;
+        }
+        cuda_check(cudaStreamEndCapture(st, &graph), "end capture");
+        cudaGraphExec_t exec;
+        cuda_check(cudaGraphInstantiate(&exec, graph, 0), "graph instantiate");
+        cudaGraphDestroy(graph);
+        it = graphs_.emplace(batch, exec).first;
+    }
+    cuda_check(cudaGraphLaunch(it->second, st), "graph launch");
+}
+
+void Engine::read_output_nchw(const std::string& name, float* d, int batch, cudaStream_t st) {
+    const TensorSlot& t = slot(name);
+    cuda_check(launch_nhwc_to_nchw(allocs_[size_t(t.alloc)], t.cstride, t.coff, d, batch, t.C, t.H, t.W, st), "nhwc_to_nchw");
+}
+
+void Engine::run_host(const float* h_in, int batch, const std::string& out_name, float* h_out, cudaStream_t st) {
+    if (batch < 1 || batch > max_batch_) fail(ErrorKind::validation, "batch out of range");
+    cuda_check(cudaSetDevice(device_), "cudaSetDevice");
+    const GraphInput& in = g_.inputs[0];
+    const size_t n_in = size_t(in.shape.elements()) * batch;
+    cuda_check(cudaMemcpyAsync(staging_, h_in, n_in * 4, cudaMemcpyHostToDevice, st), "H2D input");
+    set_input_nchw(in.name, staging_, batch, st);
+    forward(batch, st, true);
+    const TensorSlot& t = slot(out_name);
+    const size_t n_out = size_t(t.C) * t.H * t.W * batch;
+    if (n_out > staging_floats_) fail(ErrorKind::validation, "output larger than the staging buffer");
+    read_output_nchw(out_name, staging_, batch, st);
+    cuda_check(cudaMemcpyAsync(h_out, staging_, n_out * 4, cudaMemcpyDeviceToHost, st), "D2H output");
+    cuda_check(cudaStreamSynchronize(st), "sync");
+}
+
+int Engine::launches_per_forward() const {
+    int n = 0;
+    for (const StepSpec& s : plan_.steps) n += s.kind == StepSpec::CONCAT_COPY ? int(s.inputs.size()) : 1;
+    return n;
+}
+
+std::string Engine::describe_json() const {
+    std::ostringstream os;
+    os << "{\"precision\":\"" << to_string(prec_) << "\",\"max_batch\":" << max_batch_
+       << ",\"launches_per_forward\":" << launches_per_forward() << ",\"plan\":" << describe_plan_json(g_, plan_) << "}";
+    return os.str();
+}
+
+}  // namespace xlf

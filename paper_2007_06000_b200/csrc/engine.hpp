@@ -1,0 +1,72 @@
+// Device executor: the B200 successor of simulate_graph (reference
+// fused_exec.cpp:313-349).  One Engine = one graph on one GPU at one
+// precision and partition, with weights resident in HBM, activations in a
+// per-tensor arena sized for max_batch images, and one CUDA graph per batch
+// size so a forward pass is a single graph launch.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <map>
+#include <string>
+#include <vector>
+
+#include "device_plan.hpp"
+#include "graph.hpp"
+
+namespace xlf {
+
+enum class Precision { fp32_exact = 0, fp32 = 1, bf16 = 2 };
+const char* to_string(Precision p);
+
+class Engine {
+public:
+    Engine(const Graph& g, int device, Partition part, Precision prec, const float* weights, size_t nweights, int max_batch);
+    ~Engine();
+    Engine(const Engine&) = delete;
+    Engine& operator=(const Engine&) = delete;
+
+    // Inputs: device NCHW fp32 (reference layout, images stacked), or the
+    // seeded stream generated in place (image n = stream elements [n*CHW, ...)).
+    void set_input_nchw(const std::string& name, const float* d_nchw, int batch, cudaStream_t st);
+    void set_input_seeded(const std::string& name, uint64_t seed, uint64_t first_image, int batch, cudaStream_t st);
+    // All steps for `batch` images (replays a captured CUDA graph when use_graph).
+    void forward(int batch, cudaStream_t st, bool use_graph = true);
+    // One step only (per-block timing / run_fused_block).
+    void run_step(int index, int batch, cudaStream_t st);
+    // NHWC arena -> NCHW fp32.
+    void read_output_nchw(const std::string& name, float* d_nchw, int batch, cudaStream_t st);
+    // End to end with host buffers: H2D, forward, D2H of `out_name`, sync.
+    void run_host(const float* h_in_nchw, int batch, const std::string& out_name, float* h_out_nchw, cudaStream_t st);
+
+    const Graph& graph() const { return g_; }
+    const DevicePlan& plan() const { return plan_; }
+    int num_steps() const { return int(plan_.steps.size()); }
+    int launches_per_forward() const;
+    std::string describe_json() const;
+    int max_batch() const { return max_batch_; }
+
+private:
+    void launch_step(size_t i, int batch, cudaStream_t st);
+    const TensorSlot& slot(const std::string& n) const;
+
+    Graph g_;
+    DevicePlan plan_;
+    int device_;
+    Precision prec_;
+    int max_batch_;
+    std::vector<float*> allocs_;
+    float* weights_ = nullptr;
+    float* staging_ = nullptr;  // NCHW input staging for run_host
+    size_t staging_floats_ = 0;
+    std::vector<struct FusedParams> params_;
+    std::map<int, cudaGraphExec_t> graphs_;
+};
+
+std::vector<float> seeded_weights(const Graph& g, uint64_t seed);  // tensor.cpp:42-62 semantics
+float seeded_value(uint64_t seed, uint64_t index);                    // SeededStream element
+
+void cuda_check(cudaError_t e, const char* what);
+
+}  // namespace xlf

@@ -1,0 +1,401 @@
+// fp32 SIMT kernels for sm_100a: the generic fused-block kernel (all fusion
+// modes, interpreted from a FusedParams descriptor), plus the elementwise,
+// concat-copy and layout kernels of the executor.
+//
+// Numerics.  EXACT = true reproduces the reference oracle bit for bit:
+// every output accumulates  acc = acc + w*x  with separately rounded
+// multiply and add (__fmul_rn/__fadd_rn, never contracted) in the oracle's
+// order ic -> kh -> kw (reference.cpp:34-49), then adds the bias and applies
+// ReLU as (acc < 0 ? 0 : acc) (reference.cpp:50-51).  Out-of-image taps read
+// staged zeros instead of being skipped; adding a +-0 product never changes a
+// non-(-0) accumulator, and acc starts at +0, so the result is identical.
+// EXACT = false uses FFMA in the same order (<= 1e-5 norm-wise).
+//
+// Thread mapping inside an op: a work unit is PX output cells x 4 output
+// channels; lanes run over channel quads first (weights: coalesced float4
+// loads through L1, inputs: shared-memory broadcasts), then over cells.
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "fused_params.hpp"
+
+namespace xlf {
+
+namespace {
+
+constexpr int kThreads = 256;
+#define kNegInf __int_as_float(0xff800000)
+
+template <bool EXACT>
+__device__ __forceinline__ float mac(float acc, float x, float w) {
+    if constexpr (EXACT) return __fadd_rn(acc, __fmul_rn(w, x));
+    else return fmaf(w, x, acc);
+}
+
+template <bool EXACT>
+__device__ __forceinline__ float addb(float a, float b) {
+    if constexpr (EXACT) return __fadd_rn(a, b);
+    else return a + b;
+}
+
+__device__ __forceinline__ float relu_ref(float v) { return v < 0.0f ? 0.0f : v; }
+
+__device__ __forceinline__ void cp_async16(float* smem, const float* gmem, bool valid) {
+    const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+    const int bytes = valid ? 16 : 0;  // src-size 0 => 16 zero bytes
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(s), "l"(gmem), "r"(bytes));
+}
+
+struct TileCtx {
+    int n, oy0, ox0, ty, tx, c0;
+};
+
+// Source of an op: base pointer in shared memory + geometry.
+struct Src {
+    const float* p;
+    int w, cp;  // region width (cells), channel pitch (floats)
+};
+
+__device__ __forceinline__ Src src_of(const FusedParams& P, const FOp& op, const float* smem, int which) {
+    if (op.stage == 1) {
+        const FIn& in = P.in[op.xin];
+        return {smem + in.smem_off, in.ext_w, in.cpitch};
+    }
+    const FBuf& b = P.bufs[which];
+    return {smem + b.smem_off, b.ext_w, b.cpitch};
+}
+
+// Writes 4 channels of one computed cell: shared buffer (0 outside the
+// tensor = the consumer's padding) and/or global NHWC.
+__device__ __forceinline__ void store_cell(const FusedParams& P, const FOp& op, float* smem, const TileCtx& t, int cell,
+                                           int q, float4 v) {
+    const int r = cell / op.ext_w, c = cell - r * op.ext_w;
+    const int gy = t.oy0 * op.org_mul - op.org_sub + r;
+    const int gx = t.ox0 * op.org_mul - op.org_sub + c;
+    const bool inside = gy >= 0 && gy < op.H && gx >= 0 && gx < op.W;
+    if (op.buf >= 0) {
+        const FBuf& b = P.bufs[op.buf];
+        *reinterpret_cast<float4*>(smem + b.smem_off + cell * b.cpitch + 4 * q) = inside ? v : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+    if (!op.emit || !inside) return;
+    if (op.own_only) {
+        // Ownership slab of this tile (fused_exec.cpp:192-209): rows
+        // [oy0*S, (oy0+th)*S), the last tile extends to the tensor edge.
+        const int S = op.org_mul;
+        const int y1 = t.ty == P.grid_h - 1 ? op.H : min(op.H, (t.oy0 + P.tile_h) * S);
+        const int x1 = t.tx == P.grid_w - 1 ? op.W : min(op.W, (t.ox0 + P.tile_w) * S);
+        if (gy < t.oy0 * S || gy >= y1 || gx < t.ox0 * S || gx >= x1) return;
+    }
+    float* dst = op.out + ((size_t(t.n) * op.H + gy) * op.W + gx) * op.out_cstride + op.out_coff + t.c0 + 4 * q;
+    *reinterpret_cast<float4*>(dst) = v;
+}
+
+template <int KH, int KW, int PX, bool EXACT, bool GROUPED>
+__device__ void conv_op(const FusedParams& P, const FOp& op, float* smem, const TileCtx& t) {
+    const Src s = src_of(P, op, smem, op.src);
+    const int kh_ = KH ? KH : op.kh, kw_ = KW ? KW : op.kw;
+    const int ncell = op.ext_h * op.ext_w;
+    const int Q = op.cout_pad >> 2;
+    const int npb = (ncell + PX - 1) / PX;
+    const int cin_g = op.cin / op.group, cout_g = op.cout / op.group;
+    const int wstride = op.cout_pad;
+    for (int u = threadIdx.x; u < npb * Q; u += kThreads) {
+        const int pb = u / Q, q = u - pb * Q;
+        int base[PX];
+#pragma unroll
+        for (int i = 0; i < PX; ++i) {
+            int cell = pb + i * npb;
+            cell = cell < ncell ? cell : 0;
+            const int r = cell / op.ext_w, c = cell - r * op.ext_w;
+            base[i] = ((r * op.stride + op.d) * s.w + c * op.stride + op.d) * s.cp;
+        }
+        int gch[4] = {0, 0, 0, 0};
+        if constexpr (GROUPED) {
+#pragma unroll
+            for (int j = 0; j < 4; ++j) gch[j] = min((4 * q + j) / cout_g, op.group - 1) * cin_g;
+        }
+        float acc[PX][4];
+#pragma unroll
+        for (int i = 0; i < PX; ++i) acc[i][0] = acc[i][1] = acc[i][2] = acc[i][3] = 0.0f;
+        const float* wq = op.w + 4 * q;
+        for (int ic = 0; ic < cin_g; ++ic) {
+#pragma unroll
+            for (int kh = 0; kh < (KH ? KH : 16); ++kh) {
+                if (!KH && kh >= kh_) break;
+#pragma unroll
+                for (int kw = 0; kw < (KW ? KW : 16); ++kw) {
+                    if (!KW && kw >= kw_) break;
+                    const float4 w4 = __ldg(reinterpret_cast<const float4*>(wq + ((ic * kh_ + kh) * kw_ + kw) * wstride));
+                    const int off = (kh * s.w + kw) * s.cp + ic;
+#pragma unroll
+                    for (int i = 0; i < PX; ++i) {
+                        if constexpr (!GROUPED) {
+                            const float xv = s.p[base[i] + off];
+                            acc[i][0] = mac<EXACT>(acc[i][0], xv, w4.x);
+                            acc[i][1] = mac<EXACT>(acc[i][1], xv, w4.y);
+                            acc[i][2] = mac<EXACT>(acc[i][2], xv, w4.z);
+                            acc[i][3] = mac<EXACT>(acc[i][3], xv, w4.w);
+                        } else {
+                            acc[i][0] = mac<EXACT>(acc[i][0], s.p[base[i] + off + gch[0]], w4.x);
+                            acc[i][1] = mac<EXACT>(acc[i][1], s.p[base[i] + off + gch[1]], w4.y);
+                            acc[i][2] = mac<EXACT>(acc[i][2], s.p[base[i] + off + gch[2]], w4.z);
+                            acc[i][3] = mac<EXACT>(acc[i][3], s.p[base[i] + off + gch[3]], w4.w);
+                        }
+                    }
+                }
+            }
+        }
+        const float4 b4 = __ldg(reinterpret_cast<const float4*>(op.b + 4 * q));
+#pragma unroll
+        for (int i = 0; i < PX; ++i) {
+            const int cell = pb + i * npb;
+            if (cell >= ncell) continue;
+            float4 v = make_float4(addb<EXACT>(acc[i][0], b4.x), addb<EXACT>(acc[i][1], b4.y),
+                                   addb<EXACT>(acc[i][2], b4.z), addb<EXACT>(acc[i][3], b4.w));
+            if (op.relu) v = make_float4(relu_ref(v.x), relu_ref(v.y), relu_ref(v.z), relu_ref(v.w));
+            store_cell(P, op, smem, t, cell, q, v);
+        }
+    }
+}
+
+// Max / avg pool with the reference's semantics: padding reads 0.0 for both
+// kinds (reference.cpp:73-76), avg divides by the full window (:80-83); the
+// window is summed in kh, kw order.
+template <bool AVG>
+__device__ void pool_op(const FusedParams& P, const FOp& op, float* smem, const TileCtx& t) {
+    const Src s = src_of(P, op, smem, op.src);
+    const int ncell = op.ext_h * op.ext_w, Q = op.cout_pad >> 2;
+    const float inv = static_cast<float>(op.kh * op.kw);
+    for (int u = threadIdx.x; u < ncell * Q; u += kThreads) {
+        const int cell = u / Q, q = u - cell * Q;
+        const int r = cell / op.ext_w, c = cell - r * op.ext_w;
+        const float* p0 = s.p + ((r * op.stride + op.d) * s.w + c * op.stride + op.d) * s.cp + 4 * q;
+        float4 a = AVG ? make_float4(0.f, 0.f, 0.f, 0.f) : make_float4(kNegInf, kNegInf, kNegInf, kNegInf);
+        for (int kh = 0; kh < op.kh; ++kh)
+            for (int kw = 0; kw < op.kw; ++kw) {
+                const float4 v = *reinterpret_cast<const float4*>(p0 + (kh * s.w + kw) * s.cp);
+                if (AVG) {
+                    a.x = __fadd_rn(a.x, v.x), a.y = __fadd_rn(a.y, v.y), a.z = __fadd_rn(a.z, v.z), a.w = __fadd_rn(a.w, v.w);
+                } else {
+                    a.x = a.x < v.x ? v.x : a.x, a.y = a.y < v.y ? v.y : a.y;
+                    a.z = a.z < v.z ? v.z : a.z, a.w = a.w < v.w ? v.w : a.w;
+                }
+            }
+        if (AVG) a = make_float4(__fdiv_rn(a.x, inv), __fdiv_rn(a.y, inv), __fdiv_rn(a.z, inv), __fdiv_rn(a.w, inv));
+        store_cell(P, op, smem, t, cell, q, a);
+    }
+}
+
+// Elementwise add of two staged buffers (reference merge sink, fused_exec.cpp:217-235).
+__device__ void add_op(const FusedParams& P, const FOp& op, float* smem, const TileCtx& t) {
+    const FBuf& a = P.bufs[op.src];
+    const FBuf& b = P.bufs[op.src2];
+    const int ncell = op.ext_h * op.ext_w, Q = op.cout_pad >> 2;
+    for (int u = threadIdx.x; u < ncell * Q; u += kThreads) {
+        const int cell = u / Q, q = u - cell * Q;
+        const int r = cell / op.ext_w, c = cell - r * op.ext_w;
+        const float4 x = *reinterpret_cast<const float4*>(smem + a.smem_off + (r * a.ext_w + c) * a.cpitch + 4 * q);
+        const float4 y = *reinterpret_cast<const float4*>(smem + b.smem_off + (r * b.ext_w + c) * b.cpitch + 4 * q);
+        store_cell(P, op, smem, t, cell, q,
+                   make_float4(__fadd_rn(x.x, y.x), __fadd_rn(x.y, y.y), __fadd_rn(x.z, y.z), __fadd_rn(x.w, y.w)));
+    }
+}
+
+template <bool EXACT>
+__device__ __forceinline__ void run_op(const FusedParams& P, const FOp& op, float* smem, const TileCtx& t) {
+    if (op.kind == OP_MAXPOOL) return pool_op<false>(P, op, smem, t);
+    if (op.kind == OP_AVGPOOL) return pool_op<true>(P, op, smem, t);
+    if (op.kind == OP_ADD) return add_op(P, op, smem, t);
+    const int ncell = op.ext_h * op.ext_w;
+    const bool big = ncell * (op.cout_pad >> 2) >= 8 * kThreads;
+    if (op.group != 1) return conv_op<0, 0, 4, EXACT, true>(P, op, smem, t);
+    if (op.kh == 1 && op.kw == 1) {
+        if (big) return conv_op<1, 1, 8, EXACT, false>(P, op, smem, t);
+        return conv_op<1, 1, 4, EXACT, false>(P, op, smem, t);
+    }
+    if (op.kh == 3 && op.kw == 3) {
+        if (big) return conv_op<3, 3, 8, EXACT, false>(P, op, smem, t);
+        return conv_op<3, 3, 4, EXACT, false>(P, op, smem, t);
+    }
+    if (op.kh == 5 && op.kw == 5) return conv_op<5, 5, 4, EXACT, false>(P, op, smem, t);
+    return conv_op<0, 0, 4, EXACT, false>(P, op, smem, t);
+}
+
+template <bool EXACT>
+__global__ void __launch_bounds__(kThreads) fused_block_kernel(const __grid_constant__ FusedParams P) {
+    extern __shared__ __align__(16) float smem[];
+    TileCtx t;
+    t.n = blockIdx.y;
+    t.ty = blockIdx.x / P.grid_w;
+    t.tx = blockIdx.x - t.ty * P.grid_w;
+    t.oy0 = t.ty * P.tile_h;
+    t.ox0 = t.tx * P.tile_w;
+    t.c0 = blockIdx.z * P.ctile;
+    // Stage the block inputs (zero outside the image) with 16-byte cp.async.
+    for (int k = 0; k < P.nins; ++k) {
+        const FIn& in = P.in[k];
+        const int Q = in.c >> 2, ncell = in.ext_h * in.ext_w;
+        const int gy0 = t.oy0 * in.org_mul - in.org_sub, gx0 = t.ox0 * in.org_mul - in.org_sub;
+        const float* img = in.x + size_t(t.n) * in.h * in.w * in.cstride + in.coff + t.c0;
+        for (int u = threadIdx.x; u < ncell * Q; u += kThreads) {
+            const int cell = u / Q, q = u - cell * Q;
+            const int r = cell / in.ext_w, c = cell - r * in.ext_w;
+            const int gy = gy0 + r, gx = gx0 + c;
+            const bool ok = gy >= 0 && gy < in.h && gx >= 0 && gx < in.w;
+            const float* src = ok ? img + (size_t(gy) * in.w + gx) * in.cstride + 4 * q : in.x;
+            cp_async16(smem + in.smem_off + cell * in.cpitch + 4 * q, src, ok);
+        }
+    }
+    asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;\n" ::: "memory");
+    __syncthreads();
+    for (int i = 0; i < P.nops; ++i)
+        if (P.ops[i].stage == 1) run_op<EXACT>(P, P.ops[i], smem, t);
+    __syncthreads();  // producer stage complete for this tile (fused_exec.cpp:212)
+    for (int i = 0; i < P.nops; ++i)
+        if (P.ops[i].stage == 2) run_op<EXACT>(P, P.ops[i], smem, t);
+}
+
+// ----------------------------------------------------------------- executor kernels
+
+// Concat as an explicit copy (unfused / reference partitions): dst channels
+// [dst_coff, dst_coff + C) of every pixel from src channels [src_coff, ...).
+__global__ void concat_copy_kernel(const float* __restrict__ src, int src_cstride, int src_coff, float* __restrict__ dst,
+                                   int dst_cstride, int dst_coff, int C4, long long pixels) {
+    const long long total = pixels * C4;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total; i += (long long)gridDim.x * blockDim.x) {
+        const long long p = i / C4;
+        const int q = int(i - p * C4);
+        *reinterpret_cast<float4*>(dst + p * dst_cstride + dst_coff + 4 * q) =
+            __ldg(reinterpret_cast<const float4*>(src + p * src_cstride + src_coff + 4 * q));
+    }
+}
+
+// Unfused add / relu (reference.cpp:97-110).  C is the logical channel count.
+__global__ void eltwise_kernel(int op, const float* __restrict__ a, int a_cs, int a_co, const float* __restrict__ b, int b_cs,
+                               int b_co, float* __restrict__ o, int o_cs, int o_co, int C, long long pixels) {
+    const long long total = pixels * C;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total; i += (long long)gridDim.x * blockDim.x) {
+        const long long p = i / C;
+        const int c = int(i - p * C);
+        const float x = a[p * a_cs + a_co + c];
+        o[p * o_cs + o_co + c] = op == 0 ? __fadd_rn(x, b[p * b_cs + b_co + c]) : op == 1 ? relu_ref(x) : x;
+    }
+}
+
+// NCHW fp32 (reference layout, batch-stacked) -> NHWC with channel pitch cs.
+__global__ void nchw_to_nhwc_kernel(const float* __restrict__ src, float* __restrict__ dst, int N, int C, int H, int W, int cs) {
+    const long long total = (long long)N * H * W * cs;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total; i += (long long)gridDim.x * blockDim.x) {
+        const int c = int(i % cs);
+        const long long p = i / cs;
+        const int x = int(p % W), y = int((p / W) % H);
+        const long long n = p / ((long long)W * H);
+        dst[i] = c < C ? src[((n * C + c) * H + y) * W + x] : 0.0f;
+    }
+}
+
+__global__ void nhwc_to_nchw_kernel(const float* __restrict__ src, int cs, int coff, float* __restrict__ dst, int N, int C, int H,
+                                    int W) {
+    const long long total = (long long)N * C * H * W;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total; i += (long long)gridDim.x * blockDim.x) {
+        const int x = int(i % W);
+        const int y = int((i / W) % H);
+        const int c = int((i / ((long long)W * H)) % C);
+        const long long n = i / ((long long)W * H * C);
+        dst[i] = src[((n * H + y) * W + x) * cs + coff + c];
+    }
+}
+
+// SeededStream on device (tensor.cpp:19-29): element i of the stream is
+// mix(seed + (i+1)*phi), so images are generated in place, NHWC, without a
+// host copy.  Element (n, c, y, x) has stream index ((n*C + c)*H + y)*W + x
+// (image n = elements [n*CHW, (n+1)*CHW)).
+__device__ __forceinline__ float stream_at(unsigned long long seed, unsigned long long i) {
+    unsigned long long z = seed + (i + 1ull) * 0x9e3779b97f4a7c15ull;
+    z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ull;
+    z = (z ^ (z >> 27)) * 0x94d049bb133111ebull;
+    z = z ^ (z >> 31);
+    return __fsub_rn(__fmul_rn(static_cast<float>(z >> 40), 1.0f / 16777216.0f), 0.5f);
+}
+
+__global__ void seeded_nhwc_kernel(float* __restrict__ dst, unsigned long long seed, unsigned long long first_image, int N, int C,
+                                   int H, int W, int cs) {
+    const long long total = (long long)N * H * W * cs;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total; i += (long long)gridDim.x * blockDim.x) {
+        const int c = int(i % cs);
+        const long long p = i / cs;
+        const int x = int(p % W), y = int((p / W) % H);
+        const long long n = p / ((long long)W * H);
+        const unsigned long long idx = (((first_image + n) * C + c) * H + y) * (unsigned long long)W + x;
+        dst[i] = c < C ? stream_at(seed, idx) : 0.0f;
+    }
+}
+
+__global__ void seeded_flat_kernel(float* __restrict__ dst, unsigned long long seed, unsigned long long first, long long n) {
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+        dst[i] = stream_at(seed, first + i);
+}
+
+int grid_for(long long work) {
+    long long b = (work + 255) / 256;
+    return int(b < 148 * 16 ? (b < 1 ? 1 : b) : 148 * 16);
+}
+
+}  // namespace
+
+// ----------------------------------------------------------------- host launchers
+
+cudaError_t init_fused_fp32() {
+    cudaError_t e = cudaFuncSetAttribute(fused_block_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    if (e != cudaSuccess) return e;
+    return cudaFuncSetAttribute(fused_block_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+}
+
+cudaError_t launch_fused_fp32(const FusedParams& P, int batch, bool exact, cudaStream_t st) {
+    const dim3 grid(P.grid_h * P.grid_w, batch, P.cgroups);
+    const size_t smem = size_t(P.smem_floats) * 4;
+    if (exact) fused_block_kernel<true><<<grid, kThreads, smem, st>>>(P);
+    else fused_block_kernel<false><<<grid, kThreads, smem, st>>>(P);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_concat_copy(const float* src, int scs, int sco, float* dst, int dcs, int dco, int C, long long pixels,
+                               cudaStream_t st) {
+    if (C % 4 == 0 && scs % 4 == 0 && sco % 4 == 0 && dcs % 4 == 0 && dco % 4 == 0) {
+        concat_copy_kernel<<<grid_for(pixels * (C / 4)), 256, 0, st>>>(src, scs, sco, dst, dcs, dco, C / 4, pixels);
+        return cudaGetLastError();
+    }
+    // ragged channel counts: scalar copy (never touches neighbouring channels)
+    eltwise_kernel<<<grid_for(pixels * C), 256, 0, st>>>(2, src, scs, sco, src, scs, sco, dst, dcs, dco, C, pixels);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_eltwise(int op, const float* a, int acs, int aco, const float* b, int bcs, int bco, float* o, int ocs, int oco,
+                           int C, long long pixels, cudaStream_t st) {
+    eltwise_kernel<<<grid_for(pixels * C), 256, 0, st>>>(op, a, acs, aco, b, bcs, bco, o, ocs, oco, C, pixels);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_nchw_to_nhwc(const float* src, float* dst, int N, int C, int H, int W, int cs, cudaStream_t st) {
+    nchw_to_nhwc_kernel<<<grid_for((long long)N * H * W * cs), 256, 0, st>>>(src, dst, N, C, H, W, cs);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_nhwc_to_nchw(const float* src, int cs, int coff, float* dst, int N, int C, int H, int W, cudaStream_t st) {
+    nhwc_to_nchw_kernel<<<grid_for((long long)N * C * H * W), 256, 0, st>>>(src, cs, coff, dst, N, C, H, W);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_seeded_nhwc(float* dst, unsigned long long seed, unsigned long long first_image, int N, int C, int H, int W,
+                               int cs, cudaStream_t st) {
+    seeded_nhwc_kernel<<<grid_for((long long)N * H * W * cs), 256, 0, st>>>(dst, seed ? seed : 0x9e3779b97f4a7c15ull, first_image,
+                                                                           N, C, H, W, cs);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_seeded_flat(float* dst, unsigned long long seed, unsigned long long first, long long n, cudaStream_t st) {
+    seeded_flat_kernel<<<grid_for(n), 256, 0, st>>>(dst, seed ? seed : 0x9e3779b97f4a7c15ull, first, n);
+    return cudaGetLastError();
+}
+
+}  // namespace xlf
