@@ -1,0 +1,355 @@
+"""Benchmark of the B200 fused CNN inference path (BASELINE.json metric:
+"fused-block us & SqueezeNet img/s at 1/2/4/8 B200; HBM bytes saved vs
+unfused").
+
+Headline (`value`): SqueezeNet v1.1 inference, 256 images per GPU (BASELINE
+config 5), images/s over all ranks, inputs resident in HBM (generated on
+device from the reference's SeededStream), one step = one forward of the
+whole partition.  `e2e`: the same through the C ABI with host buffers (H2D of
+the NCHW input + D2H of the logits inside the timed region).  `blocks`: the
+fused-block configs 1-4 (straight / merge / split / inception) in us per block,
+fused vs the unfused sm_100a kernels, with algorithmic HBM bytes saved.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--precision fp32|fp32_exact]
+    python bench.py --impl reference ...   # the reference's own CPU path
+
+Multi-GPU: launched by torchrun, one rank per GPU; the batch is sharded
+(rank r generates images [r*256, (r+1)*256)), no collective on the data path;
+the step time is the max over ranks.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+BASELINE_METRIC = "fused-block µs & SqueezeNet img/s at 1/2/4/8 B200; HBM bytes saved vs unfused"
+PER_GPU_BATCH = 256
+BLOCK_CONFIGS = [  # (config, graph, batch) -- BASELINE.json configs[0..3]
+    ("straight", "straight", 1),
+    ("merge", "merge", 8),
+    ("split", "fire", 32),
+    ("inception", "inc3a", 64),
+]
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            p = json.load(fh)
+        return p["hbm_gbs"], p["bf16_tflops"], "measured"
+    except Exception:
+        return 6650.0, 1590.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.path = tempfile.mktemp(suffix=".csv")
+
+    def __enter__(self):
+        q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap")
+        try:
+            self.fh = open(self.path, "w")
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}", "--format=csv,noheader,nounits",
+                                          "-lms", "100"], stdout=self.fh, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+        time.sleep(0.15)
+        return self
+
+    def __exit__(self, *exc):
+        if self.proc:
+            self.proc.terminate()
+            self.proc.wait()
+            self.fh.close()
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        try:
+            for line in open(self.path):
+                parts = [p.strip() for p in line.split(",")]
+                if len(parts) < 7:
+                    continue
+                sm.append(float(parts[0]))
+                mx = float(parts[1])
+                for n, v in zip(names, parts[3:7]):
+                    if v.lower() == "active":
+                        reasons.add(n)
+        except Exception:
+            pass
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ----------------------------------------------------------------------------- reference arm
+
+def cpu_reference_rate(images: int, threads: int):
+    """images/s of the reference's own CPU path (run_reference per image,
+    reference.cpp:126-142, OpenMP across images) on SqueezeNet v1.1, from
+    oracle/_ref when the reference compiled here, else the oracle port."""
+    import numpy as np
+
+    from oracle import oracle as O
+    from oracle import ref as R
+    text = open(os.path.join(ROOT, "paper_2007_06000_b200", "graphs", "squeezenet11.graph")).read()
+    og = O.load_graph(text)
+    x = O.seeded_batch(og, 42, images)
+    t0 = time.perf_counter()
+    if R.available():
+        R.run(text, x, "pool10", og.shape_of("pool10"), wseed=42, mode=0, threads=threads)
+        kind = "reference"
+    else:
+        O.run_batch(og, x, O.seeded_weights(og, 42), ["pool10"], threads=threads)
+        kind = "port"
+    dt = time.perf_counter() - t0
+    return images / dt, kind, dt
+
+
+def run_reference_arm(args, rank, world):
+    if rank != 0:
+        return
+    threads = os.cpu_count() or 1
+    per_step = threads  # one image per host thread per step
+    for _ in range(args.warmup):
+        cpu_reference_rate(per_step, threads)
+    rates, kinds, secs = [], set(), 0.0
+    for _ in range(args.steps):
+        r, k, dt = cpu_reference_rate(per_step, threads)
+        rates.append(r)
+        kinds.add(k)
+        secs += dt
+    value = per_step * args.steps / secs
+    kind = kinds.pop()
+    line = {
+        "impl": "reference", "metric": BASELINE_METRIC, "value": round(value, 3), "unit": "images/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(1000 * secs / args.steps, 3),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": {"workload": "squeezenet_v1.1 224x224, reference CPU run_reference (oracle/_ref)", "images_per_step": per_step,
+                   "parallelism": f"openmp x{threads} over images"},
+        "cpu_baseline": {"value": round(value, 3), "unit": "images/s", "cores": threads, "kind": kind,
+                         "sample": f"{per_step} images per step x {args.steps} steps"},
+        "e2e": {"value": round(value, 3), "unit": "images/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ----------------------------------------------------------------------------- our arm
+
+def time_blocks(X, torch, precision, reps=20):
+    """us per fused block (B200 partition) vs the unfused kernels of the same
+    layers, BASELINE configs 1-4, inputs resident, best-of and mean."""
+    out = {}
+    st = torch.cuda.current_stream()
+    for cfg, gname, batch in BLOCK_CONFIGS:
+        g = X.load_graph(X.graph_path(gname))
+        w = X.seeded_weights(g, 42)
+        res = {"batch": batch}
+        for part in ("b200", "unfused"):
+            e = X.Engine(g, w, part, precision, max_batch=batch)
+            e.set_input_seeded(42, batch)
+            for _ in range(3):
+                e.forward(batch, use_graph=True)
+            torch.cuda.synchronize()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            ts = []
+            for _ in range(reps):
+                a.record(st)
+                e.forward(batch, use_graph=True)
+                b.record(st)
+                b.synchronize()
+                ts.append(a.elapsed_time(b) * 1000.0)
+            steps = e.steps
+            hbm = sum(s["bytes_algorithmic"] for s in steps) * batch
+            res[part] = {"us_median": round(statistics.median(ts), 2), "us_min": round(min(ts), 2),
+                         "kernels": e.launches_per_forward, "hbm_bytes_algorithmic": int(hbm)}
+            del e
+        res["speedup"] = round(res["unfused"]["us_median"] / res["b200"]["us_median"], 3)
+        res["hbm_bytes_saved_algorithmic"] = res["unfused"]["hbm_bytes_algorithmic"] - res["b200"]["hbm_bytes_algorithmic"]
+        out[cfg] = res
+    return out
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--precision", default="fp32", choices=["fp32", "fp32_exact"])
+    ap.add_argument("--no-blocks", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        return run_reference_arm(args, rank, world)
+
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    import paper_2007_06000_b200 as X
+
+    torch.cuda.set_device(local)
+    if world > 1:
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    g = X.load_graph(X.graph_path("squeezenet11"))
+    w = X.seeded_weights(g, 42)
+    B = PER_GPU_BATCH
+    e = X.Engine(g, w, "b200", args.precision, max_batch=B, device=local)
+    st = torch.cuda.current_stream()
+    # rank r's shard: images [r*B, (r+1)*B) of the seeded stream (no exchange)
+    e.set_input_seeded(42, B, first_image=rank * B)
+    nsteps = len(e.steps)
+
+    def barrier():
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    for _ in range(args.warmup):
+        e.forward(B, use_graph=True)
+    barrier()
+
+    # --- timed region: K forwards, every step bracketed by CUDA events on the
+    # launching stream (per-kernel durations for the roofline come from here).
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(nsteps + 1)] for _ in range(args.steps)]
+    with ClockSampler(local) as clk:
+        barrier()
+        t0 = torch.cuda.Event(enable_timing=True)
+        t1 = torch.cuda.Event(enable_timing=True)
+        t0.record(st)
+        for k in range(args.steps):
+            evs[k][0].record(st)
+            for i in range(nsteps):
+                e.run_step(i, B)
+                evs[k][i + 1].record(st)
+        t1.record(st)
+        barrier()
+    total_ms = t0.elapsed_time(t1)
+    step_ms = torch.tensor([total_ms / args.steps], device="cuda")
+    if world > 1:
+        dist.all_reduce(step_ms, op=dist.ReduceOp.MAX)
+    ms_per_step = float(step_ms.item())
+    per_step_kernel_ms = [statistics.mean(evs[k][i].elapsed_time(evs[k][i + 1]) for k in range(args.steps))
+                          for i in range(nsteps)]
+
+    # --- e2e through the C ABI with host buffers (pinned), same metric.
+    c, h, wd = g.inputs[0][1]
+    pin_in = torch.empty((B, c, h, wd), dtype=torch.float32).pin_memory()
+    x_np = pin_in.numpy()
+    x_np[:] = np.random.default_rng(rank).random((B, c, h, wd), dtype=np.float32) - 0.5
+    pin_out = torch.empty((B, 1000, 1, 1), dtype=torch.float32).pin_memory()
+    out_np = pin_out.numpy()
+    import ctypes
+    f32p = ctypes.POINTER(ctypes.c_float)
+    L = X.api.lib()
+
+    def e2e_step():
+        X.api.check(L.xlf_engine_run_host(e._h, x_np.ctypes.data_as(f32p), B, b"pool10", out_np.ctypes.data_as(f32p),
+                                          X.api._stream_ptr(None)))
+
+    for _ in range(2):
+        e2e_step()
+    barrier()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e2e_steps = max(3, min(args.steps, 10))
+    a.record(st)
+    for _ in range(e2e_steps):
+        e2e_step()
+    b.record(st)
+    barrier()
+    e2e_ms = torch.tensor([a.elapsed_time(b) / e2e_steps], device="cuda")
+    if world > 1:
+        dist.all_reduce(e2e_ms, op=dist.ReduceOp.MAX)
+    e2e_ms = float(e2e_ms.item())
+
+    blocks = None
+    if rank == 0 and not args.no_blocks:
+        blocks = time_blocks(X, torch, args.precision)
+
+    if rank == 0:
+        hbm_peak, tf_peak, src = peaks()
+        dom = max(range(nsteps), key=lambda i: per_step_kernel_ms[i])
+        s = e.steps[dom]
+        alg_bytes = s["bytes_algorithmic"] * B
+        achieved = alg_bytes / (per_step_kernel_ms[dom] * 1e-3) / 1e9
+        traffic = None
+        tpath = os.path.join(ROOT, "profiles", "traffic.json")
+        if os.path.exists(tpath):
+            try:
+                traffic = json.load(open(tpath)).get(s["id"])
+            except Exception:
+                traffic = None
+        flops = 2 * s["macs"] * B
+        simt_peak = 148 * 128 * 2 * (clk.summary()["sm_mhz"] or 1965) * 1e6 / 1e12
+        cpu = None
+        if not args.no_cpu:
+            threads = os.cpu_count() or 1
+            rate, kind, dt = cpu_reference_rate(threads, threads)
+            cpu = {"value": round(rate, 3), "unit": "images/s", "cores": threads, "kind": kind,
+                   "sample": f"{threads} images of squeezenet_v1.1 224x224 ({dt:.1f} s)"}
+        value = world * B / (ms_per_step * 1e-3)
+        line = {
+            "metric": BASELINE_METRIC,
+            "value": round(value, 2),
+            "unit": "images/s",
+            "n_gpus": world,
+            "steps": args.steps,
+            "warmup": args.warmup,
+            "ms_per_step": round(ms_per_step, 4),
+            "higher_is_better": True,
+            "scaling": "weak",
+            "vs_baseline": None,
+            "dtype": "f32",
+            "precision": args.precision,
+            "data": "synthetic (SeededStream(42) inputs generated on device, seeded_weights(42))",
+            "config": {"workload": "squeezenet_v1.1 224x224 inference, b200 partition (8 fused fire blocks, conv1+pool1 fused)",
+                       "batch_per_gpu": B, "global_batch": B * world, "parallelism": f"batch-sharded dp{world}, no collective",
+                       "l2": "inputs larger than L2 (205 MB NHWC input per GPU)"},
+            "e2e": {"value": round(world * B / (e2e_ms * 1e-3), 2), "unit": "images/s",
+                    "h2d_bytes_per_step": int(B * c * h * wd * 4), "d2h_bytes_per_step": int(B * 1000 * 4),
+                    "path": "xlf_engine_run_host (C ABI), pinned host buffers"},
+            "roofline": {"bound": "hbm", "kernel": s["id"] + ":" + s["tag"], "achieved": round(achieved, 2),
+                         "peak": hbm_peak, "peak_source": src, "unit": "GB/s", "frac": round(achieved / hbm_peak, 4),
+                         "traffic": traffic, "algorithmic_bytes_per_launch": int(alg_bytes),
+                         "launch_ms": round(per_step_kernel_ms[dom], 4),
+                         "share_of_step": round(per_step_kernel_ms[dom] / sum(per_step_kernel_ms), 4),
+                         "fp32_simt": {"achieved_tflops": round(flops / (per_step_kernel_ms[dom] * 1e-3) / 1e12, 3),
+                                       "peak_tflops": round(simt_peak, 2)}},
+            "kernels_ms": {f"{st_['id']}:{st_['tag']}": round(t, 4) for st_, t in zip(e.steps, per_step_kernel_ms)},
+            "cpu_baseline": cpu,
+            "gpu_launches": args.steps * e.launches_per_forward,
+            "clocks": clk.summary(),
+            "blocks": blocks,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

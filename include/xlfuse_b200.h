@@ -77,7 +77,8 @@ xlf_status xlf_plan_tiling(const xlf_graph* g, const char* block_id, int tile_h,
 xlf_status xlf_store_tx(const xlf_graph* g, const char* block_id, long long* fused, long long* unfused);
 /* Device program of a partition (host-only planning: kernel steps, tiles,
  * shared bytes, tensor placement) as JSON; batch_hint steers the tile choice. */
-xlf_status xlf_device_plan_json(const xlf_graph* g, int partition, int batch_hint, char* buf, size_t cap, size_t* need);
+xlf_status xlf_device_plan_json(const xlf_graph* g, int partition, int precision, int batch_hint, char* buf, size_t cap,
+                                size_t* need);
 /* seeded_weights (tensor.cpp:42-62) in save_weights stream order (tensor.cpp:64-95).
  * out may be NULL to query *count. */
 xlf_status xlf_seeded_weights(const xlf_graph* g, uint64_t seed, float* out, size_t cap, size_t* count);

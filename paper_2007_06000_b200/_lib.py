@@ -59,7 +59,7 @@ def lib() -> ctypes.CDLL:
     L.xlf_classify_mode.argtypes = [vp, c_char_pp, ctypes.c_char_p, sz, szp]
     L.xlf_plan_tiling.argtypes = [vp, c_char_pp] + [ctypes.c_int] * 4 + [c_char_pp, ctypes.c_char_p, sz, szp]
     L.xlf_store_tx.argtypes = [vp, c_char_pp, ctypes.POINTER(ctypes.c_longlong), ctypes.POINTER(ctypes.c_longlong)]
-    L.xlf_device_plan_json.argtypes = [vp, ctypes.c_int, ctypes.c_int, ctypes.c_char_p, sz, szp]
+    L.xlf_device_plan_json.argtypes = [vp, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_char_p, sz, szp]
     L.xlf_seeded_weights.argtypes = [vp, ctypes.c_uint64, f32p, sz, szp]
     L.xlf_engine_create.argtypes = [vp, ctypes.c_int, ctypes.c_int, ctypes.c_int, f32p, sz, ctypes.c_int, ctypes.POINTER(vp)]
     L.xlf_engine_destroy.argtypes = [vp]

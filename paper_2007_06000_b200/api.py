@@ -138,9 +138,9 @@ def store_transactions(g: Graph, block_id: str):
     return f.value, u.value
 
 
-def device_plan(g: Graph, partition: str = "b200", batch_hint: int = 1) -> dict:
+def device_plan(g: Graph, partition: str = "b200", batch_hint: int = 1, precision: str = "fp32") -> dict:
     """Host-only device program (kernel steps, tiles, tensor placement)."""
-    return json.loads(text_call(lib().xlf_device_plan_json, g._h, PARTITIONS[partition], batch_hint))
+    return json.loads(text_call(lib().xlf_device_plan_json, g._h, PARTITIONS[partition], PRECISIONS[precision], batch_hint))
 
 
 def seeded_weights(g: Graph, seed: int) -> np.ndarray:

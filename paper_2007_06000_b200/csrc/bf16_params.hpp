@@ -1,0 +1,82 @@
+// Launch descriptor of the bf16 tensor-core fused-block kernel
+// (kernels_bf16.cu).  Same execution model as FusedParams (fused_params.hpp):
+// stage the block inputs, stage-1 ops, stage-2 ops; but activations are bf16
+// (fp32 accumulate) and conv ops with stride 1 / group 1 / Cin % 16 == 0 run
+// as implicit GEMMs on tcgen05 with the accumulator in TMEM.
+//
+// Shared-memory activation layout ("planes"): a region of ext_h x ext_w cells
+// with C channels is C/8 planes; plane p holds channels [8p, 8p+8) of every
+// cell as 16 bytes, cells row-major.  This is the UMMA K-major SWIZZLE_NONE
+// canonical layout with the cell index as M: 8 consecutive cells of a row are
+// one 8x16-byte core matrix, so
+//   * a 1x1 conv over the whole region is an M = cells GEMM (SBO = 128 B),
+//   * a kh x kw conv producing an 8-wide strip of rows reads, for tap (dy, dx),
+//     the same planes from start address + ((row+dy+d)*ext_w + col+dx+d)*16 with
+//     SBO = ext_w*16 B -- the shifted-window implicit GEMM, no im2col copy,
+//   * LBO = plane bytes steps K by 8 channels.
+// Block inputs are loaded by one 5-D TMA per input (box {8 ch, ext_w, ext_h,
+// C/8 planes, 1 image}, zero fill outside the image = conv padding).
+#pragma once
+
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <stdint.h>
+
+#include "fused_params.hpp"
+
+namespace xlf {
+
+enum : int { BOP_MMA = 0, BOP_SIMT_CONV = 1, BOP_MAXPOOL = 2, BOP_AVGPOOL = 3, BOP_ADD = 4 };
+
+constexpr int kBMaxOps = 8;
+constexpr int kBMaxBufs = 4;
+constexpr int kBMaxUnits = 24;  // (op, N block) pairs
+constexpr int kRingSlots = 3;
+
+struct BOp {
+    int kind, stage, xin, src, src2, buf, emit, own_only;
+    int cin, cin_pad, cout, npad, group, kh, kw, stride, pad, relu;
+    int d;
+    int ext_h, ext_w;       // computed region (cells), rows x cols
+    int org_mul, org_sub;   // global cell row = tile_origin*org_mul - org_sub + r
+    int H, W;               // output tensor extent
+    // MMA tiling
+    int contig;             // 1: M = consecutive cells of the whole region (1x1 over its source)
+    int strips, mtiles;     // windowed: strips of 8 columns x blocks of 16 rows
+    int nblocks, nb;        // N split into nblocks of nb (<= 256) accumulator columns
+    int ksteps, chunk_steps;
+    const __nv_bfloat16* wmma;  // [nblock][kh*kw][cin_pad/8][nb][8]
+    const float* wsimt;         // [cin/group][kh][kw][cout_pad4] (SIMT convs)
+    const float* bias;          // [npad] fp32 (zeros when the layer has no bias)
+    __nv_bfloat16* out;
+    int out_cstride, out_coff;
+};
+
+struct BRegion {
+    int c8;             // planes (channels / 8)
+    int ext_h, ext_w;   // cells
+    int plane_bytes;    // ext_h * ext_w * 16
+    int smem_off;       // bytes from the dynamic smem base
+};
+
+struct BIn {
+    BRegion r;
+    int h, w, cstride, coff;  // NHWC bf16 tensor
+    int org_mul, org_sub;
+    const __nv_bfloat16* x;
+};
+
+struct alignas(64) BParams {
+    CUtensorMap xmap[kMaxIns];  // 5-D maps: {8, W, H, cstride/8, N}
+    int nins;
+    BIn in[kMaxIns];
+    int tile_h, tile_w, grid_h, grid_w, out_h, out_w;
+    int nops, nbufs;
+    BOp ops[kBMaxOps];
+    BRegion bufs[kBMaxBufs];
+    int ring_off, chunk_bytes;
+    int smem_bytes, tmem_cols;
+    int ctile, cgroups;  // channel tiling of pool-only steps (0 = all channels)
+};
+
+}  // namespace xlf

@@ -228,11 +228,12 @@ xlf_status xlf_store_tx(const xlf_graph* h, const char* block_id, long long* fus
     });
 }
 
-xlf_status xlf_device_plan_json(const xlf_graph* h, int part, int batch_hint, char* buf, size_t cap, size_t* need) {
+xlf_status xlf_device_plan_json(const xlf_graph* h, int part, int prec, int batch_hint, char* buf, size_t cap, size_t* need) {
     return guard([&] {
         need_ptr(h, "graph");
         if (part < 0 || part > 2) xlf::fail(xlf::ErrorKind::validation, "unknown partition");
-        put(xlf::describe_plan_json(h->g, xlf::plan_device(h->g, xlf::Partition(part), batch_hint)), buf, cap, need);
+        put(xlf::describe_plan_json(h->g, xlf::plan_device(h->g, xlf::Partition(part), batch_hint, 227 * 1024, prec == XLF_BF16)),
+            buf, cap, need);
     });
 }
 

@@ -391,8 +391,9 @@ bool choose_tile_at(const Graph& g, StepSpec& s, int batch_hint, int smem_budget
 }
 
 void fill_stats(const Graph& g, const DevicePlan& plan, StepSpec& s) {
+    const double es = plan.bf16 ? 2.0 : 4.0;  // bytes per activation / weight element
     s.macs = 0, s.bytes_algorithmic = 0, s.macs_executed = 0;
-    for (const std::string& in : s.inputs) s.bytes_algorithmic += double(g.shape_of(in).elements()) * 4;
+    for (const std::string& in : s.inputs) s.bytes_algorithmic += double(g.shape_of(in).elements()) * es;
     if (s.kind == StepSpec::CONCAT_COPY) {
         s.bytes_algorithmic *= 2;
         return;
@@ -401,12 +402,16 @@ void fill_stats(const Graph& g, const DevicePlan& plan, StepSpec& s) {
         const Layer& l = *g.find_layer(op.layer);
         if (l.kind == LayerKind::conv) {
             s.macs += double(l.out_shape->elements()) * double(l.conv->macs_per_output());
-            s.bytes_algorithmic += double(l.conv->weight_count() + l.conv->bias_count()) * 4;
+            s.bytes_algorithmic += double(l.conv->weight_count() + l.conv->bias_count()) * es;
         }
-        if (op.emit) s.bytes_algorithmic += double(l.out_shape->elements()) * 4;
+        if (op.emit) s.bytes_algorithmic += double(l.out_shape->elements()) * es;
     }
     if (s.kind != StepSpec::FUSED) {
-        s.bytes_algorithmic += double(g.shape_of(s.layers[0]).elements()) * 4;
+        s.bytes_algorithmic += double(g.shape_of(s.layers[0]).elements()) * es;
+        return;
+    }
+    if (plan.bf16) {
+        s.macs_executed = s.macs;
         return;
     }
     FusedParams fp;
@@ -417,15 +422,19 @@ void fill_stats(const Graph& g, const DevicePlan& plan, StepSpec& s) {
         if (l.kind == LayerKind::conv)
             s.macs_executed += tiles * fp.ops[i].ext_h * fp.ops[i].ext_w * l.out_shape->channels * double(l.conv->macs_per_output());
     }
-    (void)plan;
 }
 
 }  // namespace
 
-DevicePlan plan_device(const Graph& g, Partition part, int batch_hint, int smem_budget) {
+DevicePlan plan_device(const Graph& g, Partition part, int batch_hint, int smem_budget, bool bf16) {
     if (!g.shapes_inferred()) fail(ErrorKind::internal, "plan_device requires inferred shapes");
     DevicePlan plan;
     plan.partition = part;
+    plan.bf16 = bf16;
+    const int cpad = bf16 ? 8 : 4;  // channel padding of HBM tensors (16 bytes)
+    auto tile = [&](StepSpec& st) {
+        return bf16 ? choose_tile_bf16(g, st, batch_hint, smem_budget - 1024) : choose_tile(g, st, batch_hint, smem_budget);
+    };
     if (part == Partition::reference) plan.blocks = detect_fusion_blocks(g);
     else if (part == Partition::b200) plan.blocks = detect_fusion_blocks_b200(g);
     else {
@@ -450,7 +459,7 @@ DevicePlan plan_device(const Graph& g, Partition part, int batch_hint, int smem_
     std::vector<StepSpec> steps;
     for (const FusionBlock& b : ordered) {
         StepSpec s = step_for_block(g, b);
-        if (s.kind == StepSpec::FUSED && !choose_tile(g, s, batch_hint, smem_budget)) {
+        if (s.kind == StepSpec::FUSED && !tile(s)) {
             if (!b.fused()) fail(ErrorKind::infeasible, "layer " + b.members[0] + " does not fit shared memory at any tile");
             // Fused block infeasible on chip: run its members as singletons.
             for (const std::string& m : b.members) {
@@ -458,7 +467,7 @@ DevicePlan plan_device(const Graph& g, Partition part, int batch_hint, int smem_
                 one.id = b.id + "." + m;
                 one.members = {m};
                 StepSpec t = step_for_block(g, one);
-                if (t.kind == StepSpec::FUSED && !choose_tile(g, t, batch_hint, smem_budget))
+                if (t.kind == StepSpec::FUSED && !tile(t))
                     fail(ErrorKind::infeasible, "layer " + m + " does not fit shared memory at any tile");
                 steps.push_back(t);
             }
@@ -499,7 +508,7 @@ DevicePlan plan_device(const Graph& g, Partition part, int batch_hint, int smem_
                 m.id += "+" + steps[j].id;
                 m.tag = "multi-branch";
                 m.mode = FusionMode::merge;
-                if (!choose_tile(g, m, batch_hint, smem_budget)) continue;
+                if (!tile(m)) continue;
                 steps[i] = m;
                 gone[j] = 1;
             }
@@ -532,7 +541,7 @@ DevicePlan plan_device(const Graph& g, Partition part, int batch_hint, int smem_
                 const Layer* p = g.find_layer(in);
                 const TensorShape s = g.shape_of(in);
                 ok &= p != nullptr && !g.is_output(in) && g.consumers_of(in).size() == 1 && materialized.count(in) &&
-                      s.channels % 4 == 0 && !view_of.count(in);
+                      s.channels % cpad == 0 && !view_of.count(in);
                 off += s.channels;
             }
             if (!ok) continue;
@@ -559,7 +568,7 @@ DevicePlan plan_device(const Graph& g, Partition part, int batch_hint, int smem_
             const TensorSlot host = resolve(v->second.first);
             t.alloc = host.alloc, t.cstride = host.cstride, t.coff = host.coff + v->second.second;
         } else {
-            t.alloc = int(plan.alloc_floats.size()), t.cstride = round4(s.channels), t.coff = 0;
+            t.alloc = int(plan.alloc_floats.size()), t.cstride = (s.channels + cpad - 1) / cpad * cpad, t.coff = 0;
             plan.alloc_floats.push_back((long long)s.height * s.width * t.cstride);
         }
         plan.tensors[n] = t;

@@ -58,6 +58,7 @@ struct StepSpec {
 
 struct DevicePlan {
     Partition partition = Partition::b200;
+    bool bf16 = false;                   // element type of the HBM tensors (else fp32)
     std::vector<FusionBlock> blocks;     // the partition, reference vocabulary
     std::vector<StepSpec> steps;
     std::map<std::string, TensorSlot> tensors;
@@ -71,7 +72,17 @@ struct DevicePlan {
 std::vector<FusionBlock> detect_fusion_blocks_b200(const Graph& g);
 
 // batch_hint steers the tile choice (enough CTAs to fill 148 SMs).
-DevicePlan plan_device(const Graph& g, Partition part, int batch_hint = 1, int smem_budget_bytes = 227 * 1024);
+// bf16: plan for the tensor-core kernel (kernels_bf16.cu): bf16 NHWC tensors
+// with channels padded to 8, tiles from its geometry (device_plan_bf16.cpp).
+DevicePlan plan_device(const Graph& g, Partition part, int batch_hint = 1, int smem_budget_bytes = 227 * 1024,
+                       bool bf16 = false);
+
+// device_plan_bf16.cpp
+bool bf16_mma_ok(const Layer& l);
+void bf16_nblocks(int cout, int* nblocks, int* nb);
+long long layout_bf16(const Graph& g, const StepSpec& s, int th, int tw, struct BParams* P);
+bool choose_tile_bf16(const Graph& g, StepSpec& s, int batch_hint, int smem_budget);
+std::vector<uint16_t> pack_weights_bf16(const Graph& g, const float* flat, size_t count, std::map<std::string, long long>& off);
 
 // Packs reference-layout weights (save_weights stream order, tensor.cpp:64-95)
 // into the device layout of `plan`: per conv [cin/group][kh][kw][cout_pad4]

@@ -1,0 +1,370 @@
+// Geometry of the bf16 tensor-core kernel (kernels_bf16.cu) for a step of
+// the device program: per-op MMA/SIMT choice, regions, TMEM columns, shared
+// bytes, and the bf16 weight packing the MMA B operand reads.
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+
+#include "bf16_params.hpp"
+#include "common.hpp"
+#include "device_plan.hpp"
+
+namespace xlf {
+
+namespace {
+
+int r8(int c) { return (c + 7) & ~7; }
+int r16(int c) { return (c + 15) & ~15; }
+int r128(int c) { return (c + 127) & ~127; }
+int cdiv(int a, int b) { return (a + b - 1) / b; }
+int pow2_cols(int c) {
+    if (c <= 0) return 0;
+    int p = 32;
+    while (p < c) p <<= 1;
+    return p;
+}
+
+struct Win {
+    int kh = 1, kw = 1, stride = 1, pad = 0;
+};
+Win win(const Layer& l) {
+    if (l.kind == LayerKind::conv) return {l.conv->kernel_h, l.conv->kernel_w, l.conv->stride, l.conv->pad};
+    if (l.kind == LayerKind::pool) return {l.pool->kernel, l.pool->kernel, l.pool->stride, l.pool->pad};
+    return {};
+}
+
+constexpr int kChunkBytes = 16 * 1024;
+constexpr int kSlack = 2048;  // contiguous-M tiles may read up to 127 cells past a plane
+
+}  // namespace
+
+bool bf16_mma_ok(const Layer& l) {
+    return l.kind == LayerKind::conv && l.conv->stride == 1 && l.conv->group == 1 && l.conv->in_channels % 16 == 0;
+}
+
+// N blocking of an MMA conv: nblocks x nb accumulator columns, nb % 16 == 0, nb <= 256.
+void bf16_nblocks(int cout, int* nblocks, int* nb) {
+    const int n16 = r16(cout);
+    *nblocks = cdiv(n16, 256);
+    *nb = r16(cdiv(n16, *nblocks));
+}
+
+long long layout_bf16(const Graph& g, const StepSpec& s, int th, int tw, BParams* P) {
+    const int nops = int(s.ops.size());
+    if (nops > kBMaxOps || s.inputs.size() > size_t(kMaxIns)) return -1;
+    struct G {
+        int ext_h, ext_w, mul, sub, d;
+        bool mma, contig;
+    };
+    std::vector<G> geo(static_cast<size_t>(nops));
+    std::vector<int> bufidx(static_cast<size_t>(nops), -1);
+    const int rows_m = cdiv(th, 16) * 16;  // windowed MMA ops over the tile compute whole 16-row blocks
+    const int cols_m = cdiv(tw, 8) * 8;
+    int nbufs = 0;
+    for (int i = 0; i < nops; ++i) {
+        const Layer& l = *g.find_layer(s.ops[size_t(i)].layer);
+        geo[size_t(i)] = {th, tw, 1, 0, 0, bf16_mma_ok(l), false};
+    }
+    // staged buffers: lead L, stride S, trail T from the readers (+ the rows /
+    // columns windowed MMA readers over-read)
+    for (int i = 0; i < nops; ++i) {
+        const OpSpec& op = s.ops[size_t(i)];
+        if (op.stage != 1 || !op.staged) continue;
+        int S = -1, L = 0, Th = 1, Tw = 1;
+        bool add_reader = false;
+        for (const OpSpec& c : s.ops) {
+            if (c.stage != 2 || std::find(c.srcs.begin(), c.srcs.end(), i) == c.srcs.end()) continue;
+            const Layer& cl = *g.find_layer(c.layer);
+            if (cl.kind == LayerKind::add) {
+                add_reader = true;
+                continue;
+            }
+            const Win w = win(cl);
+            if (S >= 0 && S != w.stride) return -1;
+            S = w.stride, L = std::max(L, w.pad);
+            Th = std::max(Th, w.kh - w.pad), Tw = std::max(Tw, w.kw - w.pad);
+        }
+        if (add_reader) {
+            if (S > 1 || L > 0) return -1;
+            S = 1;
+        }
+        if (S < 0) S = 1;
+        if (op.own_only) Th = std::max(Th, S), Tw = std::max(Tw, S);
+        int eh = (th - 1) * S + L + Th, ew = (tw - 1) * S + L + Tw;
+        for (const OpSpec& c : s.ops) {
+            if (c.stage != 2 || std::find(c.srcs.begin(), c.srcs.end(), i) == c.srcs.end()) continue;
+            const Layer& cl = *g.find_layer(c.layer);
+            if (!bf16_mma_ok(cl)) continue;
+            const Win w = win(cl);
+            eh = std::max(eh, rows_m - 1 + w.kh - 1 + (L - w.pad) + 1);
+            ew = std::max(ew, cols_m - 1 + w.kw - 1 + (L - w.pad) + 1);
+        }
+        G& gi = geo[size_t(i)];
+        gi.ext_h = eh, gi.ext_w = ew, gi.mul = S, gi.sub = L;
+        bufidx[size_t(i)] = nbufs++;
+    }
+    if (nbufs > kBMaxBufs) return -1;
+
+    // block inputs
+    std::vector<BIn> ins(s.inputs.size());
+    std::vector<int> XLs(s.inputs.size()), scales(s.inputs.size());
+    for (size_t xi = 0; xi < s.inputs.size(); ++xi) {
+        int scale = -1, XL = 0;
+        for (int i = 0; i < nops; ++i) {
+            const OpSpec& op = s.ops[size_t(i)];
+            if (op.stage != 1 || op.xin != int(xi)) continue;
+            const Win w = win(*g.find_layer(op.layer));
+            const int sc = geo[size_t(i)].mul * w.stride;
+            if (scale >= 0 && sc != scale) return -1;
+            scale = sc;
+            XL = std::max(XL, geo[size_t(i)].sub * w.stride + w.pad);
+        }
+        XLs[xi] = XL, scales[xi] = scale < 0 ? 1 : scale;
+    }
+    // 1x1 stride-1 MMA producers whose buffer readers all have stride 1 run in
+    // contiguous-M mode: their region IS the input region (d = 0), so every
+    // 128 consecutive cells form one GEMM tile.
+    for (int i = 0; i < nops; ++i) {
+        const OpSpec& op = s.ops[size_t(i)];
+        G& gi = geo[size_t(i)];
+        const Layer& l = *g.find_layer(op.layer);
+        if (op.stage != 1 || !gi.mma || l.conv->kernel_h != 1 || l.conv->kernel_w != 1 || l.conv->pad != 0) continue;
+        if (scales[size_t(op.xin)] != 1) continue;
+        gi.contig = true;
+    }
+    for (size_t xi = 0; xi < s.inputs.size(); ++xi) {
+        const int XL = XLs[xi];
+        int eh = 0, ew = 0;
+        for (int i = 0; i < nops; ++i) {
+            const OpSpec& op = s.ops[size_t(i)];
+            if (op.stage != 1 || op.xin != int(xi)) continue;
+            const Win w = win(*g.find_layer(op.layer));
+            G& gi = geo[size_t(i)];
+            if (gi.contig) continue;
+            gi.d = XL - (gi.sub * w.stride + w.pad);
+            const int rh = gi.mma ? cdiv(gi.ext_h, 16) * 16 : gi.ext_h;
+            const int rw = gi.mma ? cdiv(gi.ext_w, 8) * 8 : gi.ext_w;
+            eh = std::max(eh, gi.d + (rh - 1) * w.stride + w.kh);
+            ew = std::max(ew, gi.d + (rw - 1) * w.stride + w.kw);
+        }
+        // contiguous producers: their buffer = this region; readers' reach
+        for (int i = 0; i < nops; ++i) {
+            const OpSpec& op = s.ops[size_t(i)];
+            if (op.stage != 1 || op.xin != int(xi) || !geo[size_t(i)].contig) continue;
+            eh = std::max(eh, geo[size_t(i)].ext_h + (XL - geo[size_t(i)].sub));
+            ew = std::max(ew, geo[size_t(i)].ext_w + (XL - geo[size_t(i)].sub));
+            for (const OpSpec& c : s.ops) {
+                if (c.stage != 2 || std::find(c.srcs.begin(), c.srcs.end(), i) == c.srcs.end()) continue;
+                const Layer& cl = *g.find_layer(c.layer);
+                const Win w = win(cl);
+                const bool cm = bf16_mma_ok(cl);
+                const int rh = cm ? rows_m : th, rw = cm ? cols_m : tw;
+                const int d = cl.kind == LayerKind::add ? 0 : XL - w.pad;
+                eh = std::max(eh, d + (rh - 1) * w.stride + w.kh);
+                ew = std::max(ew, d + (rw - 1) * w.stride + w.kw);
+            }
+        }
+        for (int i = 0; i < nops; ++i) {
+            const OpSpec& op = s.ops[size_t(i)];
+            if (op.stage != 1 || op.xin != int(xi) || !geo[size_t(i)].contig) continue;
+            G& gi = geo[size_t(i)];
+            gi.ext_h = eh, gi.ext_w = ew, gi.sub = XL, gi.d = 0;
+        }
+        const TensorShape xs = g.shape_of(s.inputs[xi]);
+        BIn& in = ins[xi];
+        in = BIn{};
+        in.r.c8 = (s.ctile ? s.ctile : r8(xs.channels)) / 8;
+        in.r.ext_h = eh, in.r.ext_w = ew;
+        in.h = xs.height, in.w = xs.width;
+        in.org_mul = scales[xi], in.org_sub = XL;
+        if (eh > 256 || ew > 256) return -1;  // TMA box limit
+    }
+    // readers' offsets into buffers
+    for (int i = 0; i < nops; ++i) {
+        const OpSpec& op = s.ops[size_t(i)];
+        if (op.stage != 2) continue;
+        const Layer& l = *g.find_layer(op.layer);
+        const int L = geo[size_t(op.srcs[0])].sub;
+        geo[size_t(i)].d = l.kind == LayerKind::add ? 0 : L - win(l).pad;
+    }
+    // shared memory
+    long long bytes = 0;
+    auto region = [&](BRegion& r) {
+        r.plane_bytes = r128(r.ext_h * r.ext_w * 16);
+        r.smem_off = int(bytes);
+        bytes += (long long)r.c8 * r.plane_bytes + kSlack;
+    };
+    for (BIn& in : ins) region(in.r);
+    std::vector<BRegion> bufs(static_cast<size_t>(nbufs));
+    for (int i = 0; i < nops; ++i) {
+        if (bufidx[size_t(i)] < 0) continue;
+        BRegion& b = bufs[size_t(bufidx[size_t(i)])];
+        b.c8 = r8(g.find_layer(s.ops[size_t(i)].layer)->out_shape->channels) / 8;
+        b.ext_h = geo[size_t(i)].ext_h, b.ext_w = geo[size_t(i)].ext_w;
+        region(b);
+    }
+    bool any_mma = false;
+    int tmem = 0;
+    std::vector<BOp> ops(static_cast<size_t>(nops));
+    for (int i = 0; i < nops; ++i) {
+        const OpSpec& os = s.ops[size_t(i)];
+        const Layer& l = *g.find_layer(os.layer);
+        const G& gi = geo[size_t(i)];
+        BOp& o = ops[size_t(i)];
+        o = BOp{};
+        o.stage = os.stage, o.xin = os.xin;
+        o.src = os.srcs.empty() ? -1 : bufidx[size_t(os.srcs[0])];
+        o.src2 = os.srcs.size() > 1 ? bufidx[size_t(os.srcs[1])] : -1;
+        o.buf = bufidx[size_t(i)];
+        o.emit = os.emit, o.own_only = os.own_only;
+        const TensorShape out = *l.out_shape;
+        o.H = out.height, o.W = out.width, o.cout = out.channels;
+        const Win w = win(l);
+        o.kh = w.kh, o.kw = w.kw, o.stride = w.stride, o.pad = w.pad, o.group = 1;
+        o.d = gi.d, o.ext_h = gi.ext_h, o.ext_w = gi.ext_w, o.org_mul = gi.mul, o.org_sub = gi.sub;
+        o.npad = r8(out.channels);
+        if (l.kind == LayerKind::conv) {
+            o.cin = l.conv->in_channels, o.group = l.conv->group, o.relu = l.conv->activation == Activation::relu;
+            o.cin_pad = r8(o.cin);
+            if (gi.mma) {
+                o.kind = BOP_MMA;
+                o.contig = gi.contig;
+                bf16_nblocks(out.channels, &o.nblocks, &o.nb);
+                o.npad = o.nblocks * o.nb;
+                if (o.contig) o.strips = 1, o.mtiles = cdiv(o.ext_h * o.ext_w, 128);
+                else o.strips = cdiv(o.ext_w, 8), o.mtiles = o.strips * cdiv(o.ext_h, 16);
+                o.ksteps = o.kh * o.kw * (o.cin / 16);
+                o.chunk_steps = std::max(1, kChunkBytes / (o.nb * 32));
+                if (o.mtiles * o.nb > 512) return -1;  // TMEM: 512 columns
+                tmem = std::max(tmem, o.mtiles * o.nb);
+                any_mma = true;
+            } else {
+                o.kind = BOP_SIMT_CONV;
+            }
+        } else if (l.kind == LayerKind::pool) {
+            o.kind = l.pool->kind == PoolKind::max ? BOP_MAXPOOL : BOP_AVGPOOL;
+            o.cin = out.channels;
+            if (s.ctile) o.npad = s.ctile;
+        } else {
+            o.kind = BOP_ADD;
+            o.cin = out.channels;
+        }
+    }
+    bytes = (bytes + 1023) & ~1023LL;
+    const long long ring_off = bytes;
+    if (any_mma) bytes += (long long)kRingSlots * kChunkBytes;
+    if (P) {
+        std::memset(static_cast<void*>(P), 0, sizeof(BParams));
+        P->nins = int(ins.size());
+        for (size_t i = 0; i < ins.size(); ++i) P->in[i] = ins[i];
+        P->tile_h = th, P->tile_w = tw;
+        P->out_h = s.out_h, P->out_w = s.out_w;
+        P->grid_h = cdiv(s.out_h, th), P->grid_w = cdiv(s.out_w, tw);
+        P->nops = nops, P->nbufs = nbufs;
+        for (int i = 0; i < nops; ++i) P->ops[i] = ops[size_t(i)];
+        for (int i = 0; i < nbufs; ++i) P->bufs[i] = bufs[size_t(i)];
+        P->ring_off = int(ring_off), P->chunk_bytes = kChunkBytes;
+        P->smem_bytes = int(bytes);
+        P->ctile = s.ctile;
+        P->cgroups = s.ctile ? r8(g.shape_of(s.inputs[0]).channels) / s.ctile : 1;
+        P->tmem_cols = pow2_cols(tmem);
+    }
+    return bytes;
+}
+
+// Tile choice for the bf16 kernel: memory-bound blocks, so the model is the
+// bytes a CTA moves (input region incl. halo re-reads, outputs) plus a small
+// MMA term, over waves of CTAs resident per SM (shared memory and TMEM).
+static bool choose_tile_bf16_at(const Graph& g, StepSpec& s, int batch_hint, int smem_budget);
+
+// Pool-only steps too wide for shared memory (13x13x1000 global average pool)
+// are also tiled over channels (channel c in -> channel c out).
+bool choose_tile_bf16(const Graph& g, StepSpec& s, int batch_hint, int smem_budget) {
+    s.ctile = 0;
+    if (choose_tile_bf16_at(g, s, batch_hint, smem_budget)) return true;
+    bool pools = s.inputs.size() == 1;
+    for (const OpSpec& op : s.ops) pools &= op.stage == 1 && g.find_layer(op.layer)->kind == LayerKind::pool;
+    if (!pools) return false;
+    const int C = r8(g.shape_of(s.inputs[0]).channels);
+    for (int ct = C - 8; ct >= 8; ct -= 8) {
+        if (C % ct) continue;
+        s.ctile = ct;
+        if (choose_tile_bf16_at(g, s, batch_hint, smem_budget)) return true;
+    }
+    s.ctile = 0;
+    return false;
+}
+
+static bool choose_tile_bf16_at(const Graph& g, StepSpec& s, int batch_hint, int smem_budget) {
+    double best = 1e300;
+    int bh = 0, bw = 0, bsm = 0;
+    for (int th = 1; th <= std::min(s.out_h, 32); ++th)
+        for (int tw = 1; tw <= std::min(s.out_w, 32); ++tw) {
+            BParams* P = new BParams;
+            const long long sm = layout_bf16(g, s, th, tw, P);
+            if (sm < 0 || sm > smem_budget) {
+                delete P;
+                continue;
+            }
+            double in_bytes = 0, mma = 0, simt = 0;
+            for (int i = 0; i < P->nins; ++i) in_bytes += double(P->in[i].r.c8) * P->in[i].r.ext_h * P->in[i].r.ext_w * 16;
+            for (int i = 0; i < P->nops; ++i) {
+                const BOp& o = P->ops[i];
+                if (o.kind == BOP_MMA) mma += double(o.mtiles) * 128 * o.nblocks * o.nb * o.ksteps * 16;
+                else simt += double(o.ext_h) * o.ext_w * o.npad * o.kh * o.kw * (o.kind == BOP_SIMT_CONV ? o.cin : 1);
+            }
+            const double out_bytes = double(th) * tw * 2.0 * 256;  // order of magnitude; same for all tiles per pixel
+            const double ctas = double(P->grid_h) * P->grid_w * P->cgroups * std::max(batch_hint, 1);
+            int occ = std::max(1, std::min(4, int((227 * 1024) / (sm + 2048))));
+            if (P->tmem_cols) occ = std::min(occ, 512 / P->tmem_cols);
+            const double waves = std::ceil(ctas / (148.0 * occ));
+            // cycles per CTA ~ bytes/(per-SM HBM share) + MMA (8192 MAC/clk/SM) + SIMT (128 FMA/clk)
+            const double per_cta = (in_bytes + out_bytes) / 24.0 + mma / 8192.0 + simt / 128.0 + 1500.0;
+            const double t = waves * per_cta * occ / std::min(double(occ), 2.0);
+            if (t < best * 0.999 || (t <= best * 1.001 && long(th) * tw > long(bh) * bw))
+                best = t, bh = th, bw = tw, bsm = int(sm);
+            delete P;
+        }
+    if (!bh) return false;
+    s.tile_h = bh, s.tile_w = bw, s.smem_bytes = bsm;
+    return true;
+}
+
+// bf16 weights of every MMA-eligible conv: [nblock][tap][cin/8][nb][8].
+std::vector<uint16_t> pack_weights_bf16(const Graph& g, const float* flat, size_t count, std::map<std::string, long long>& off) {
+    std::vector<uint16_t> out;
+    size_t pos = 0;
+    auto bf = [](float f) {
+        uint32_t u;
+        std::memcpy(&u, &f, 4);
+        u += 0x7FFF + ((u >> 16) & 1);  // round to nearest even
+        return uint16_t(u >> 16);
+    };
+    for (const Layer& l : g.layers) {
+        if (l.kind != LayerKind::conv) continue;
+        const ConvParams& c = *l.conv;
+        const size_t nf = size_t(c.weight_count()), nb_ = size_t(c.bias_count());
+        if (pos + nf + nb_ > count) fail(ErrorKind::validation, "weights: stream too short for layer '" + l.name + "'");
+        if (bf16_mma_ok(l)) {
+            int nblocks, nb;
+            bf16_nblocks(c.out_channels, &nblocks, &nb);
+            const int c16 = c.in_channels / 16, taps = c.kernel_h * c.kernel_w, ksteps = taps * c16;
+            const size_t base = out.size();
+            off[l.name] = (long long)base;
+            out.resize(base + size_t(nblocks) * ksteps * nb * 16, 0);
+            for (int oc = 0; oc < c.out_channels; ++oc)
+                for (int ic = 0; ic < c.in_channels; ++ic)
+                    for (int y = 0; y < c.kernel_h; ++y)
+                        for (int x = 0; x < c.kernel_w; ++x) {
+                            const int nbi = oc / nb, n = oc - nbi * nb, tap = y * c.kernel_w + x;
+                            const int step = tap * c16 + ic / 16, half = (ic % 16) / 8;
+                            const size_t dst = ((size_t(nbi) * ksteps + step) * 2 + half) * nb * 8 + size_t(n) * 8 + ic % 8;
+                            out[base + dst] = bf(flat[pos + ((size_t(oc) * c.in_channels + ic) * c.kernel_h + y) * c.kernel_w + x]);
+                        }
+        }
+        pos += nf + nb_;
+    }
+    return out;
+}
+
+}  // namespace xlf

@@ -1,8 +1,13 @@
 #include "engine.hpp"
 
+#include <cuda_bf16.h>
+#include <cudaTypedefs.h>
+
 #include <algorithm>
+#include <cstring>
 #include <sstream>
 
+#include "bf16_params.hpp"
 #include "common.hpp"
 #include "fused_params.hpp"
 
@@ -18,6 +23,18 @@ cudaError_t launch_nchw_to_nhwc(const float* src, float* dst, int N, int C, int 
 cudaError_t launch_nhwc_to_nchw(const float* src, int cs, int coff, float* dst, int N, int C, int H, int W, cudaStream_t st);
 cudaError_t launch_seeded_nhwc(float* dst, unsigned long long seed, unsigned long long first_image, int N, int C, int H, int W,
                                int cs, cudaStream_t st);
+// kernels_bf16.cu
+cudaError_t init_fused_bf16();
+cudaError_t launch_fused_bf16(const BParams& P, int batch, cudaStream_t st);
+cudaError_t launch_nchw_to_nhwc_bf16(const float* src, __nv_bfloat16* dst, int N, int C, int H, int W, int cs, cudaStream_t st);
+cudaError_t launch_nhwc_bf16_to_nchw(const __nv_bfloat16* src, int cs, int coff, float* dst, int N, int C, int H, int W,
+                                     cudaStream_t st);
+cudaError_t launch_seeded_nhwc_bf16(__nv_bfloat16* dst, unsigned long long seed, unsigned long long first_image, int N, int C, int H,
+                                    int W, int cs, cudaStream_t st);
+cudaError_t launch_concat_copy_bf16(const __nv_bfloat16* src, int scs, int sco, __nv_bfloat16* dst, int dcs, int dco, int C,
+                                    long long pixels, cudaStream_t st);
+cudaError_t launch_eltwise_bf16(int op, const __nv_bfloat16* a, int acs, int aco, const __nv_bfloat16* b, int bcs, int bco,
+                                __nv_bfloat16* o, int ocs, int oco, int C, long long pixels, cudaStream_t st);
 
 const char* to_string(Precision p) {
     switch (p) {
@@ -54,24 +71,63 @@ std::vector<float> seeded_weights(const Graph& g, uint64_t seed) {
     return out;
 }
 
+namespace {
+
+PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+    if (!fn) {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        cuda_check(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q), "cuTensorMapEncodeTiled lookup");
+        if (q != cudaDriverEntryPointSuccess || !p) fail(ErrorKind::cuda, "cuTensorMapEncodeTiled unavailable");
+        fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+    }
+    return fn;
+}
+
+// 4-D map over an NHWC bf16 tensor {cstride, W, H, N}; box = one 8-channel
+// plane of an ext_h x ext_w region (16-byte inner box), zero fill outside.
+void encode_plane_map(CUtensorMap* map, const void* base, int cstride, int W, int H, int N, int ext_w, int ext_h) {
+    const cuuint64_t dims[4] = {cuuint64_t(cstride), cuuint64_t(W), cuuint64_t(H), cuuint64_t(N)};
+    const cuuint64_t strides[3] = {cuuint64_t(cstride) * 2, cuuint64_t(W) * cstride * 2, cuuint64_t(H) * W * cstride * 2};
+    const cuuint32_t box[4] = {8, cuuint32_t(ext_w), cuuint32_t(ext_h), 1};
+    const cuuint32_t estr[4] = {1, 1, 1, 1};
+    const CUresult r = tensor_map_encoder()(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(base), dims, strides, box, estr,
+                                            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                                            CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) fail(ErrorKind::cuda, "cuTensorMapEncodeTiled failed (" + std::to_string(int(r)) + ")");
+}
+
+}  // namespace
+
 Engine::Engine(const Graph& g, int device, Partition part, Precision prec, const float* weights, size_t nweights, int max_batch)
     : g_(g), device_(device), prec_(prec), max_batch_(max_batch) {
     if (!g_.shapes_inferred()) fail(ErrorKind::internal, "engine: graph shapes not inferred");
     if (max_batch < 1) fail(ErrorKind::validation, "engine: max_batch must be >= 1");
-    if (prec == Precision::bf16) fail(ErrorKind::validation, "engine: bf16 path not built in this library");
     if (g_.inputs.size() != 1) fail(ErrorKind::validation, "engine: graphs with exactly one input are supported");
+    const bool bf = prec == Precision::bf16;
+    esz_ = bf ? 2 : 4;
     cuda_check(cudaSetDevice(device), "cudaSetDevice");
-    plan_ = plan_device(g_, part, max_batch);
-    cuda_check(init_fused_fp32(), "kernel attributes");
+    plan_ = plan_device(g_, part, max_batch, 227 * 1024, bf);
+    cuda_check(bf ? init_fused_bf16() : init_fused_fp32(), "kernel attributes");
+    // fp32 packed weights (+ slack: bf16 epilogues read bias up to the N-block padding)
     std::vector<float> packed = pack_weights(g_, plan_, weights, nweights);
-    cuda_check(cudaMalloc(&weights_, std::max<size_t>(packed.size(), 1) * 4), "cudaMalloc(weights)");
+    packed.resize(packed.size() + 1024, 0.0f);
+    cuda_check(cudaMalloc(&weights_, packed.size() * 4), "cudaMalloc(weights)");
     cuda_check(cudaMemcpy(weights_, packed.data(), packed.size() * 4, cudaMemcpyHostToDevice), "weights H2D");
+    std::map<std::string, long long> woff16;
+    if (bf) {
+        std::vector<uint16_t> w16 = pack_weights_bf16(g_, weights, nweights, woff16);
+        w16.resize(w16.size() + 64, 0);
+        cuda_check(cudaMalloc(&weights16_, w16.size() * 2), "cudaMalloc(bf16 weights)");
+        cuda_check(cudaMemcpy(weights16_, w16.data(), w16.size() * 2, cudaMemcpyHostToDevice), "bf16 weights H2D");
+    }
     for (long long f : plan_.alloc_floats) {
-        float* p = nullptr;
-        const size_t bytes = size_t(f) * size_t(max_batch) * 4;
+        void* p = nullptr;
+        const size_t bytes = size_t(f) * size_t(max_batch) * esz_;
         cuda_check(cudaMalloc(&p, bytes), "cudaMalloc(activations)");
         cuda_check(cudaMemset(p, 0, bytes), "cudaMemset");  // channel padding stays zero
-        allocs_.push_back(p);
+        allocs_.push_back(static_cast<float*>(p));
     }
     size_t most = 0;
     for (const auto& [n, t] : plan_.tensors)
@@ -79,8 +135,39 @@ Engine::Engine(const Graph& g, int device, Partition part, Precision prec, const
     staging_floats_ = most * size_t(max_batch);
     cuda_check(cudaMalloc(&staging_, staging_floats_ * 4), "cudaMalloc(staging)");
     params_.resize(plan_.steps.size());
-    for (size_t i = 0; i < plan_.steps.size(); ++i)
-        if (plan_.steps[i].kind == StepSpec::FUSED) params_[i] = make_params(g_, plan_, plan_.steps[i], allocs_, weights_);
+    bparams_.resize(plan_.steps.size());
+    for (size_t i = 0; i < plan_.steps.size(); ++i) {
+        const StepSpec& s = plan_.steps[i];
+        if (s.kind != StepSpec::FUSED) continue;
+        if (!bf) {
+            params_[i] = make_params(g_, plan_, s, allocs_, weights_);
+            continue;
+        }
+        auto P = std::make_unique<BParams>();
+        if (layout_bf16(g_, s, s.tile_h, s.tile_w, P.get()) < 0) fail(ErrorKind::internal, "step " + s.id + ": bf16 layout failed");
+        for (int k = 0; k < P->nins; ++k) {
+            const TensorSlot& t = plan_.tensors.at(s.inputs[size_t(k)]);
+            BIn& in = P->in[k];
+            in.x = reinterpret_cast<const __nv_bfloat16*>(allocs_[size_t(t.alloc)]);
+            in.cstride = t.cstride, in.coff = t.coff;
+            encode_plane_map(&P->xmap[k], in.x, t.cstride, t.W, t.H, max_batch, in.r.ext_w, in.r.ext_h);
+        }
+        for (int k = 0; k < P->nops; ++k) {
+            const OpSpec& os = s.ops[size_t(k)];
+            BOp& o = P->ops[k];
+            if (o.kind == BOP_MMA || o.kind == BOP_SIMT_CONV) {
+                o.wsimt = weights_ + plan_.w_off.at(os.layer);
+                o.bias = weights_ + plan_.b_off.at(os.layer);
+                if (o.kind == BOP_MMA) o.wmma = reinterpret_cast<const __nv_bfloat16*>(weights16_) + woff16.at(os.layer);
+            }
+            if (o.emit) {
+                const TensorSlot& t = plan_.tensors.at(os.layer);
+                o.out = reinterpret_cast<__nv_bfloat16*>(allocs_[size_t(t.alloc)]);
+                o.out_cstride = t.cstride, o.out_coff = t.coff;
+            }
+        }
+        bparams_[i] = std::move(P);
+    }
 }
 
 Engine::~Engine() {
@@ -88,7 +175,9 @@ Engine::~Engine() {
     for (auto& [b, ge] : graphs_) cudaGraphExecDestroy(ge);
     for (float* p : allocs_) cudaFree(p);
     cudaFree(weights_);
+    if (weights16_) cudaFree(weights16_);
     cudaFree(staging_);
+    if (capture_) cudaStreamDestroy(capture_);
 }
 
 const TensorSlot& Engine::slot(const std::string& n) const {
@@ -101,29 +190,46 @@ const TensorSlot& Engine::slot(const std::string& n) const {
 void Engine::set_input_nchw(const std::string& name, const float* d, int batch, cudaStream_t st) {
     if (batch < 1 || batch > max_batch_) fail(ErrorKind::validation, "batch out of range");
     const TensorSlot& t = slot(name);
-    cuda_check(launch_nchw_to_nhwc(d, allocs_[size_t(t.alloc)], batch, t.C, t.H, t.W, t.cstride, st), "nchw_to_nhwc");
+    if (esz_ == 2)
+        cuda_check(launch_nchw_to_nhwc_bf16(d, reinterpret_cast<__nv_bfloat16*>(allocs_[size_t(t.alloc)]), batch, t.C, t.H, t.W,
+                                            t.cstride, st),
+                   "nchw_to_nhwc");
+    else
+        cuda_check(launch_nchw_to_nhwc(d, allocs_[size_t(t.alloc)], batch, t.C, t.H, t.W, t.cstride, st), "nchw_to_nhwc");
 }
 
 void Engine::set_input_seeded(const std::string& name, uint64_t seed, uint64_t first_image, int batch, cudaStream_t st) {
     if (batch < 1 || batch > max_batch_) fail(ErrorKind::validation, "batch out of range");
     const TensorSlot& t = slot(name);
-    cuda_check(launch_seeded_nhwc(allocs_[size_t(t.alloc)], seed, first_image, batch, t.C, t.H, t.W, t.cstride, st), "seeded fill");
+    if (esz_ == 2)
+        cuda_check(launch_seeded_nhwc_bf16(reinterpret_cast<__nv_bfloat16*>(allocs_[size_t(t.alloc)]), seed, first_image, batch, t.C,
+                                           t.H, t.W, t.cstride, st),
+                   "seeded fill");
+    else
+        cuda_check(launch_seeded_nhwc(allocs_[size_t(t.alloc)], seed, first_image, batch, t.C, t.H, t.W, t.cstride, st), "seeded fill");
 }
 
 void Engine::launch_step(size_t i, int batch, cudaStream_t st) {
     const StepSpec& s = plan_.steps[i];
+    const bool bf = esz_ == 2;
+    auto b16 = [&](const TensorSlot& t) { return reinterpret_cast<__nv_bfloat16*>(allocs_[size_t(t.alloc)]); };
     switch (s.kind) {
     case StepSpec::FUSED:
-        cuda_check(launch_fused_fp32(params_[i], batch, prec_ == Precision::fp32_exact, st), "fused block");
+        if (bf) cuda_check(launch_fused_bf16(*bparams_[i], batch, st), "fused block (bf16)");
+        else cuda_check(launch_fused_fp32(params_[i], batch, prec_ == Precision::fp32_exact, st), "fused block");
         return;
     case StepSpec::CONCAT_COPY: {
         const TensorSlot& o = slot(s.layers[0]);
         int off = 0;
         for (const std::string& in : s.inputs) {
             const TensorSlot& t = slot(in);
-            cuda_check(launch_concat_copy(allocs_[size_t(t.alloc)], t.cstride, t.coff, allocs_[size_t(o.alloc)], o.cstride,
-                                          o.coff + off, t.C, (long long)batch * t.H * t.W, st),
-                       "concat copy");
+            const long long px = (long long)batch * t.H * t.W;
+            if (bf)
+                cuda_check(launch_concat_copy_bf16(b16(t), t.cstride, t.coff, b16(o), o.cstride, o.coff + off, t.C, px, st), "concat");
+            else
+                cuda_check(launch_concat_copy(allocs_[size_t(t.alloc)], t.cstride, t.coff, allocs_[size_t(o.alloc)], o.cstride,
+                                              o.coff + off, t.C, px, st),
+                           "concat copy");
             off += t.C;
         }
         return;
@@ -133,10 +239,16 @@ void Engine::launch_step(size_t i, int batch, cudaStream_t st) {
         const TensorSlot& o = slot(s.layers[0]);
         const TensorSlot& a = slot(s.inputs[0]);
         const TensorSlot& b = s.kind == StepSpec::ADD ? slot(s.inputs[1]) : a;
-        cuda_check(launch_eltwise(s.kind == StepSpec::ADD ? 0 : 1, allocs_[size_t(a.alloc)], a.cstride, a.coff,
-                                  allocs_[size_t(b.alloc)], b.cstride, b.coff, allocs_[size_t(o.alloc)], o.cstride, o.coff, o.C,
-                                  (long long)batch * o.H * o.W, st),
-                   "eltwise");
+        const int op = s.kind == StepSpec::ADD ? 0 : 1;
+        const long long px = (long long)batch * o.H * o.W;
+        if (bf)
+            cuda_check(launch_eltwise_bf16(op, b16(a), a.cstride, a.coff, b16(b), b.cstride, b.coff, b16(o), o.cstride, o.coff, o.C, px,
+                                           st),
+                       "eltwise");
+        else
+            cuda_check(launch_eltwise(op, allocs_[size_t(a.alloc)], a.cstride, a.coff, allocs_[size_t(b.alloc)], b.cstride, b.coff,
+                                      allocs_[size_t(o.alloc)], o.cstride, o.coff, o.C, px, st),
+                       "eltwise");
         return;
     }
     }
@@ -158,15 +270,18 @@ void Engine::forward(int batch, cudaStream_t st, bool use_graph) {
     }
     auto it = graphs_.find(batch);
     if (it == graphs_.end()) {
+        // Capture on the engine's own stream (the caller's may be the legacy
+        // default stream, which cannot be captured); replay on the caller's.
+        if (!capture_) cuda_check(cudaStreamCreateWithFlags(&capture_, cudaStreamNonBlocking), "capture stream");
         cudaGraph_t graph;
-        cuda_check(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal), "begin capture");
+        cuda_check(cudaStreamBeginCapture(capture_, cudaStreamCaptureModeThreadLocal), "begin capture");
         try {
-            for (size_t i = 0; i < plan_.steps.size(); ++i) launch_step(i, batch, st);
+            for (size_t i = 0; i < plan_.steps.size(); ++i) launch_step(i, batch, capture_);
         } catch (...) {
-            cudaStreamEndCapture(st, &graph);
+            cudaStreamEndCapture(capture_, &graph);
             throw;
         }
-        cuda_check(cudaStreamEndCapture(st, &graph), "end capture");
+        cuda_check(cudaStreamEndCapture(capture_, &graph), "end capture");
         cudaGraphExec_t exec;
         cuda_check(cudaGraphInstantiate(&exec, graph, 0), "graph instantiate");
         cudaGraphDestroy(graph);
@@ -177,7 +292,12 @@ void Engine::forward(int batch, cudaStream_t st, bool use_graph) {
 
 void Engine::read_output_nchw(const std::string& name, float* d, int batch, cudaStream_t st) {
     const TensorSlot& t = slot(name);
-    cuda_check(launch_nhwc_to_nchw(allocs_[size_t(t.alloc)], t.cstride, t.coff, d, batch, t.C, t.H, t.W, st), "nhwc_to_nchw");
+    if (esz_ == 2)
+        cuda_check(launch_nhwc_bf16_to_nchw(reinterpret_cast<const __nv_bfloat16*>(allocs_[size_t(t.alloc)]), t.cstride, t.coff, d,
+                                            batch, t.C, t.H, t.W, st),
+                   "nhwc_to_nchw");
+    else
+        cuda_check(launch_nhwc_to_nchw(allocs_[size_t(t.alloc)], t.cstride, t.coff, d, batch, t.C, t.H, t.W, st), "nhwc_to_nchw");
 }
 
 void Engine::run_host(const float* h_in, int batch, const std::string& out_name, float* h_out, cudaStream_t st) {

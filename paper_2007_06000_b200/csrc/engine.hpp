@@ -9,6 +9,7 @@
 
 #include <cstdint>
 #include <map>
+#include <memory>
 #include <string>
 #include <vector>
 
@@ -59,8 +60,12 @@ private:
     std::vector<float*> allocs_;
     float* weights_ = nullptr;
     float* staging_ = nullptr;  // NCHW input staging for run_host
+    cudaStream_t capture_ = nullptr;  // private stream used only to capture CUDA graphs
     size_t staging_floats_ = 0;
     std::vector<struct FusedParams> params_;
+    std::vector<std::unique_ptr<struct BParams>> bparams_;  // bf16 steps
+    void* weights16_ = nullptr;  // bf16 MMA weights
+    int esz_ = 4;                // bytes per activation element
     std::map<int, cudaGraphExec_t> graphs_;
 };
 

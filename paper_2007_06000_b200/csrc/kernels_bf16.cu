@@ -1,0 +1,447 @@
+// bf16 tensor-core fused-block kernel for sm_100a (tcgen05 + TMEM + TMA).
+//
+// One CTA = (image, output tile).  192 threads in three roles:
+//   warp 4      producer: TMA of the block inputs (one 4-D box per 8-channel
+//               plane, zero fill outside the image) and cp.async.bulk of the
+//               packed weights through a 3-slot ring (full/empty mbarriers);
+//   warp 5      MMA issuer: one thread issues tcgen05.mma (M=128, N<=256,
+//               K=16, bf16 x bf16 -> fp32 in TMEM) for every conv "unit"
+//               (op x N block), commits to the ring and to the unit's
+//               accumulator barrier; the warp owns TMEM alloc/dealloc;
+//   warps 0-3   epilogue + SIMT ops: tcgen05.ld the accumulator (lane = GEMM
+//               row = output cell), bias + ReLU + halo mask, bf16, and either
+//               keep it on chip (shared "planes" buffer that the next stage's
+//               MMAs read with shifted descriptors) or store NHWC to HBM at
+//               the concat channel offset.  Pools / stride-2 convs / adds run
+//               here as SIMT code on the same shared planes.
+// Units execute in order; the issuer starts unit u only after every earlier
+// unit's epilogue signalled (its TMEM columns are free and any buffer it
+// reads is written).  See bf16_params.hpp for the shared-memory layout.
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "bf16_params.hpp"
+#include "umma.cuh"
+
+namespace xlf {
+
+namespace {
+
+using namespace umma;
+
+constexpr int kBThreads = 192;
+
+struct BTile {
+    int n, ty, tx, oy0, ox0, c0;
+};
+
+__device__ __forceinline__ void named_sync_compute() { asm volatile("bar.sync 1, 128;\n" ::: "memory"); }
+
+__device__ __forceinline__ const BRegion& src_region(const BParams& P, const BOp& op, int which) {
+    return op.stage == 1 ? P.in[op.xin].r : P.bufs[which];
+}
+
+// Unit enumeration: (op index, N block) in op order.
+__device__ __forceinline__ int unit_count(const BParams& P) {
+    int u = 0;
+    for (int i = 0; i < P.nops; ++i) u += P.ops[i].kind == BOP_MMA ? P.ops[i].nblocks : 1;
+    return u;
+}
+
+// ------------------------------------------------------------------ producer
+
+__device__ void producer(const BParams& P, uint8_t* smem, const BTile& t, uint64_t* bar_x, uint64_t* ring_full,
+                         uint64_t* ring_empty) {
+    uint32_t bytes = 0;
+    for (int k = 0; k < P.nins; ++k) bytes += uint32_t(P.in[k].r.c8) * uint32_t(P.in[k].r.ext_h * P.in[k].r.ext_w * 16);
+    mbar_expect_tx(bar_x, bytes);
+    for (int k = 0; k < P.nins; ++k) {
+        const BIn& in = P.in[k];
+        const int x0 = t.ox0 * in.org_mul - in.org_sub, y0 = t.oy0 * in.org_mul - in.org_sub;
+        for (int p = 0; p < in.r.c8; ++p)
+            tma_load_4d(smem + in.r.smem_off + p * in.r.plane_bytes, &P.xmap[k], in.coff + t.c0 + 8 * p, x0, y0, t.n, bar_x);
+    }
+    int c = 0;
+    for (int i = 0; i < P.nops; ++i) {
+        const BOp& op = P.ops[i];
+        if (op.kind != BOP_MMA) continue;
+        for (int nbi = 0; nbi < op.nblocks; ++nbi) {
+            const __nv_bfloat16* wb = op.wmma + size_t(nbi) * op.ksteps * op.nb * 16;
+            for (int s0 = 0; s0 < op.ksteps; s0 += op.chunk_steps, ++c) {
+                const int steps = min(op.chunk_steps, op.ksteps - s0);
+                const int slot = c % kRingSlots;
+                if (c >= kRingSlots) mbar_wait(&ring_empty[slot], ((c / kRingSlots) - 1) & 1);
+                const uint32_t b = uint32_t(steps) * op.nb * 32;
+                mbar_expect_tx(&ring_full[slot], b);
+                bulk_g2s(smem + P.ring_off + slot * P.chunk_bytes, wb + size_t(s0) * op.nb * 16, b, &ring_full[slot]);
+            }
+        }
+    }
+}
+
+// ------------------------------------------------------------------ MMA issuer
+
+__device__ void issuer(const BParams& P, uint8_t* smem, uint32_t tmem, uint64_t* bar_x, uint64_t* ring_full,
+                       uint64_t* ring_empty, uint64_t* acc_full, uint64_t* unit_done) {
+    mbar_wait(bar_x, 0);
+    int c = 0, u = 0, waited = 0;
+    const uint32_t sbase = smem_u32(smem);
+    for (int i = 0; i < P.nops; ++i) {
+        const BOp& op = P.ops[i];
+        const int nunits = op.kind == BOP_MMA ? op.nblocks : 1;
+        for (int nbi = 0; nbi < nunits; ++nbi, ++u) {
+            for (; waited < u; ++waited) mbar_wait(&unit_done[waited], 0);
+            if (op.kind != BOP_MMA) continue;
+            fence_after();
+            const BRegion& R = src_region(P, op, op.src);
+            const uint32_t src = sbase + R.smem_off;
+            const int c16 = op.cin_pad / 16;
+            const uint32_t idesc = idesc_bf16(128, op.nb);
+            for (int s0 = 0; s0 < op.ksteps; s0 += op.chunk_steps, ++c) {
+                const int steps = min(op.chunk_steps, op.ksteps - s0);
+                const int slot = c % kRingSlots;
+                mbar_wait(&ring_full[slot], (c / kRingSlots) & 1);
+                fence_after();
+                const uint32_t wslot = sbase + P.ring_off + slot * P.chunk_bytes;
+                for (int sl = 0; sl < steps; ++sl) {
+                    const int s = s0 + sl;
+                    const int tap = s / c16, kc = s - tap * c16;
+                    const int dy = tap / op.kw, dx = tap - dy * op.kw;
+                    const uint64_t bd = sdesc(wslot + sl * op.nb * 32, op.nb * 16, 128, kNoSwizzle);
+                    for (int mt = 0; mt < op.mtiles; ++mt) {
+                        uint32_t a;
+                        uint32_t sbo;
+                        if (op.contig) {
+                            a = src + kc * 2 * R.plane_bytes + mt * 128 * 16;
+                            sbo = 128;
+                        } else {
+                            const int st = mt % op.strips, rb = mt / op.strips;
+                            a = src + kc * 2 * R.plane_bytes + ((rb * 16 + dy + op.d) * R.ext_w + st * 8 + dx + op.d) * 16;
+                            sbo = R.ext_w * 16;
+                        }
+                        mma_bf16(tmem + mt * op.nb, sdesc(a, R.plane_bytes, sbo, kNoSwizzle), bd, idesc, s > 0 ? 1u : 0u);
+                    }
+                }
+                commit(&ring_empty[slot]);
+            }
+            commit(&acc_full[u]);
+        }
+    }
+}
+
+// ------------------------------------------------------------------ epilogue / SIMT
+
+__device__ __forceinline__ bool owns(const BParams& P, const BOp& op, const BTile& t, int gy, int gx) {
+    if (!op.own_only)  // emitted cells: exactly this tile (contiguous-M ops compute a halo'd region)
+        return gy >= t.oy0 && gy < t.oy0 + P.tile_h && gx >= t.ox0 && gx < t.ox0 + P.tile_w;
+    const int S = op.org_mul;
+    const int y1 = t.ty == P.grid_h - 1 ? op.H : min(op.H, (t.oy0 + P.tile_h) * S);
+    const int x1 = t.tx == P.grid_w - 1 ? op.W : min(op.W, (t.ox0 + P.tile_w) * S);
+    return gy >= t.oy0 * S && gy < y1 && gx >= t.ox0 * S && gx < x1;
+}
+
+// Stores 8 channels [ch, ch+8) of one computed cell (fp32 values).
+__device__ __forceinline__ void put8(const BParams& P, const BOp& op, uint8_t* smem, const BTile& t, int r, int c, int ch,
+                                     const float* v8) {
+    const int gy = t.oy0 * op.org_mul - op.org_sub + r, gx = t.ox0 * op.org_mul - op.org_sub + c;
+    const bool inside = gy >= 0 && gy < op.H && gx >= 0 && gx < op.W;
+    __align__(16) __nv_bfloat162 h[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) h[j] = __floats2bfloat162_rn(v8[2 * j], v8[2 * j + 1]);
+    if (op.buf >= 0) {
+        const BRegion& B = P.bufs[op.buf];
+        uint4 val = inside ? *reinterpret_cast<uint4*>(h) : make_uint4(0, 0, 0, 0);
+        *reinterpret_cast<uint4*>(smem + B.smem_off + (ch >> 3) * B.plane_bytes + (r * B.ext_w + c) * 16) = val;
+    }
+    if (op.emit && inside && owns(P, op, t, gy, gx)) {
+        __nv_bfloat16* dst = op.out + ((size_t(t.n) * op.H + gy) * op.W + gx) * op.out_cstride + op.out_coff + t.c0 + ch;
+        *reinterpret_cast<uint4*>(dst) = *reinterpret_cast<uint4*>(h);
+    }
+}
+
+__device__ void epilogue_mma(const BParams& P, const BOp& op, int nbi, uint8_t* smem, uint32_t tmem, const BTile& t) {
+    const int row = threadIdx.x;  // 0..127 == TMEM lane == GEMM row
+    const uint32_t lane_base = uint32_t(threadIdx.x & ~31) << 16;
+    for (int mt = 0; mt < op.mtiles; ++mt) {
+        int r, c;
+        bool valid;
+        if (op.contig) {
+            const int idx = mt * 128 + row;
+            r = idx / op.ext_w, c = idx - r * op.ext_w;
+            valid = idx < op.ext_h * op.ext_w;
+        } else {
+            const int st = mt % op.strips, rb = mt / op.strips;
+            r = rb * 16 + (row >> 3), c = st * 8 + (row & 7);
+            valid = r < op.ext_h && c < op.ext_w;
+        }
+        for (int col = 0; col < op.nb; col += 32) {
+            float v[32];
+            const uint32_t ta = tmem + lane_base + mt * op.nb + col;
+            const int ncol = min(32, op.nb - col);
+            if (ncol == 32) tmem_ld32(ta, v);
+            else tmem_ld16(ta, v);
+            if (!valid) continue;
+            const int ch0 = nbi * op.nb + col;
+            for (int j = 0; j < ncol; ++j) {
+                float x = v[j] + __ldg(op.bias + ch0 + j);
+                v[j] = op.relu ? fmaxf(x, 0.0f) : x;
+            }
+            const int c8end = (op.cout + 7) & ~7;  // never write past the tensor's padded channels
+            for (int j = 0; j < ncol; j += 8)
+                if (ch0 + j < c8end) put8(P, op, smem, t, r, c, ch0 + j, v + j);
+        }
+    }
+}
+
+__device__ __forceinline__ void load8(const uint8_t* smem, const BRegion& R, int cell, int oct, float* f) {
+    const uint4 raw = *reinterpret_cast<const uint4*>(smem + R.smem_off + oct * R.plane_bytes + cell * 16);
+    const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&raw);
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+        const float2 p = __bfloat1622float2(h[j]);
+        f[2 * j] = p.x, f[2 * j + 1] = p.y;
+    }
+}
+
+// Pools (zero padding for max and avg, avg over the full window:
+// reference.cpp:59-88) and adds over shared planes.
+__device__ void simt_pool_add(const BParams& P, const BOp& op, uint8_t* smem, const BTile& t) {
+    const BRegion& R = src_region(P, op, op.src);
+    const int ncell = op.ext_h * op.ext_w, c8 = op.npad / 8;
+    const float inv = 1.0f / float(op.kh * op.kw);
+    for (int u = threadIdx.x; u < ncell * c8; u += 128) {
+        const int cell = u / c8, oct = u - cell * c8;
+        const int r = cell / op.ext_w, c = cell - r * op.ext_w;
+        float acc[8], x[8];
+        if (op.kind == BOP_ADD) {
+            const BRegion& R2 = P.bufs[op.src2];
+            load8(smem, R, r * R.ext_w + c, oct, acc);
+            load8(smem, R2, r * R2.ext_w + c, oct, x);
+            for (int j = 0; j < 8; ++j) acc[j] += x[j];
+        } else {
+            for (int j = 0; j < 8; ++j) acc[j] = op.kind == BOP_MAXPOOL ? __int_as_float(0xff800000) : 0.0f;
+            for (int kh = 0; kh < op.kh; ++kh)
+                for (int kw = 0; kw < op.kw; ++kw) {
+                    load8(smem, R, (r * op.stride + kh + op.d) * R.ext_w + c * op.stride + kw + op.d, oct, x);
+                    for (int j = 0; j < 8; ++j) acc[j] = op.kind == BOP_MAXPOOL ? fmaxf(acc[j], x[j]) : acc[j] + x[j];
+                }
+            if (op.kind == BOP_AVGPOOL)
+                for (int j = 0; j < 8; ++j) acc[j] *= inv;
+        }
+        put8(P, op, smem, t, r, c, oct * 8, acc);
+    }
+}
+
+// Direct conv for what the tensor-core path does not take (stride != 1,
+// groups, Cin not a multiple of 16: SqueezeNet conv1).  fp32 accumulate.
+__device__ void simt_conv(const BParams& P, const BOp& op, uint8_t* smem, const BTile& t) {
+    const BRegion& R = src_region(P, op, op.src);
+    const int ncell = op.ext_h * op.ext_w, c8 = op.npad / 8;
+    const int cin_g = op.cin / op.group, cout_g = op.cout / op.group, cp4 = (op.cout + 3) & ~3;
+    for (int u = threadIdx.x; u < ncell * c8; u += 128) {
+        const int cell = u / c8, oct = u - cell * c8;
+        const int r = cell / op.ext_w, c = cell - r * op.ext_w;
+        float acc[8];
+        for (int j = 0; j < 8; ++j) acc[j] = 0.0f;
+        const int base = (r * op.stride + op.d) * R.ext_w + c * op.stride + op.d;
+        for (int ic = 0; ic < cin_g; ++ic)
+            for (int kh = 0; kh < op.kh; ++kh)
+                for (int kw = 0; kw < op.kw; ++kw) {
+                    const int cell_in = base + kh * R.ext_w + kw;
+                    const float* wrow = op.wsimt + ((ic * op.kh + kh) * op.kw + kw) * cp4;
+#pragma unroll
+                    for (int j = 0; j < 8; ++j) {
+                        const int oc = oct * 8 + j;
+                        if (oc >= op.cout) break;
+                        const int in_c = (oc / cout_g) * cin_g + ic;
+                        const __nv_bfloat16 xv = *reinterpret_cast<const __nv_bfloat16*>(
+                            smem + R.smem_off + (in_c >> 3) * R.plane_bytes + cell_in * 16 + (in_c & 7) * 2);
+                        acc[j] = fmaf(__bfloat162float(xv), __ldg(wrow + oc), acc[j]);
+                    }
+                }
+        for (int j = 0; j < 8; ++j) {
+            const int oc = oct * 8 + j;
+            float x = oc < op.cout ? acc[j] + __ldg(op.bias + oc) : 0.0f;
+            acc[j] = op.relu ? fmaxf(x, 0.0f) : x;
+        }
+        put8(P, op, smem, t, r, c, oct * 8, acc);
+    }
+}
+
+__global__ void __launch_bounds__(kBThreads, 1) fused_bf16_kernel(const __grid_constant__ BParams P) {
+    extern __shared__ __align__(1024) uint8_t smem[];
+    __shared__ __align__(8) uint64_t bar_x, ring_full[kRingSlots], ring_empty[kRingSlots], acc_full[kBMaxUnits],
+        unit_done[kBMaxUnits];
+    __shared__ uint32_t tmem_slot;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    BTile t;
+    t.n = blockIdx.y;
+    t.ty = blockIdx.x / P.grid_w;
+    t.tx = blockIdx.x - t.ty * P.grid_w;
+    t.oy0 = t.ty * P.tile_h;
+    t.ox0 = t.tx * P.tile_w;
+    t.c0 = blockIdx.z * P.ctile;
+    const int units = unit_count(P);
+    if (threadIdx.x == 0) {
+        mbar_init(&bar_x, 1);
+        for (int i = 0; i < kRingSlots; ++i) mbar_init(&ring_full[i], 1), mbar_init(&ring_empty[i], 1);
+        for (int i = 0; i < units; ++i) mbar_init(&acc_full[i], 1), mbar_init(&unit_done[i], 1);
+        mbar_fence_init();
+    }
+    if (warp == 5 && P.tmem_cols) tmem_alloc(&tmem_slot, P.tmem_cols);
+    fence_before();
+    __syncthreads();
+    fence_after();
+    const uint32_t tmem = P.tmem_cols ? tmem_slot : 0;
+
+    if (warp == 4) {
+        if (lane == 0) producer(P, smem, t, &bar_x, ring_full, ring_empty);
+    } else if (warp == 5) {
+        if (lane == 0) issuer(P, smem, tmem, &bar_x, ring_full, ring_empty, acc_full, unit_done);
+        __syncwarp();
+    } else {
+        bool have_x = false;
+        int u = 0;
+        for (int i = 0; i < P.nops; ++i) {
+            const BOp& op = P.ops[i];
+            const int nunits = op.kind == BOP_MMA ? op.nblocks : 1;
+            for (int nbi = 0; nbi < nunits; ++nbi, ++u) {
+                if (op.kind == BOP_MMA) {
+                    mbar_wait(&acc_full[u], 0);
+                    fence_after();
+                    epilogue_mma(P, op, nbi, smem, tmem, t);
+                } else {
+                    if (!have_x) mbar_wait(&bar_x, 0), have_x = true;
+                    if (op.kind == BOP_SIMT_CONV) simt_conv(P, op, smem, t);
+                    else simt_pool_add(P, op, smem, t);
+                }
+                fence_async_smem();
+                fence_before();
+                named_sync_compute();
+                if (threadIdx.x == 0) mbar_arrive(&unit_done[u]);
+            }
+        }
+    }
+    fence_before();
+    __syncthreads();
+    fence_after();
+    if (warp == 5 && P.tmem_cols) tmem_free(tmem, P.tmem_cols);
+}
+
+// ----------------------------------------------------------------- layout kernels (bf16)
+
+__global__ void nchw_f32_to_nhwc_bf16(const float* __restrict__ src, __nv_bfloat16* __restrict__ dst, int N, int C, int H, int W,
+                                      int cs) {
+    const long long total = (long long)N * H * W * cs;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total; i += (long long)gridDim.x * blockDim.x) {
+        const int c = int(i % cs);
+        const long long p = i / cs;
+        const int x = int(p % W), y = int((p / W) % H);
+        const long long n = p / ((long long)W * H);
+        dst[i] = __float2bfloat16(c < C ? src[((n * C + c) * H + y) * W + x] : 0.0f);
+    }
+}
+
+__global__ void nhwc_bf16_to_nchw_f32(const __nv_bfloat16* __restrict__ src, int cs, int coff, float* __restrict__ dst, int N, int C,
+                                      int H, int W) {
+    const long long total = (long long)N * C * H * W;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total; i += (long long)gridDim.x * blockDim.x) {
+        const int x = int(i % W);
+        const int y = int((i / W) % H);
+        const int c = int((i / ((long long)W * H)) % C);
+        const long long n = i / ((long long)W * H * C);
+        dst[i] = __bfloat162float(src[((n * H + y) * W + x) * cs + coff + c]);
+    }
+}
+
+__global__ void seeded_nhwc_bf16(__nv_bfloat16* __restrict__ dst, unsigned long long seed, unsigned long long first_image, int N,
+                                 int C, int H, int W, int cs) {
+    const long long total = (long long)N * H * W * cs;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total; i += (long long)gridDim.x * blockDim.x) {
+        const int c = int(i % cs);
+        const long long p = i / cs;
+        const int x = int(p % W), y = int((p / W) % H);
+        const long long n = p / ((long long)W * H);
+        float v = 0.0f;
+        if (c < C) {
+            unsigned long long z = seed + ((((first_image + n) * C + c) * H + y) * (unsigned long long)W + x + 1ull) *
+                                              0x9e3779b97f4a7c15ull;
+            z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ull;
+            z = (z ^ (z >> 27)) * 0x94d049bb133111ebull;
+            z = z ^ (z >> 31);
+            v = static_cast<float>(z >> 40) * (1.0f / 16777216.0f) - 0.5f;
+        }
+        dst[i] = __float2bfloat16(v);
+    }
+}
+
+__global__ void concat_copy_bf16(const __nv_bfloat16* __restrict__ src, int scs, int sco, __nv_bfloat16* __restrict__ dst, int dcs,
+                                 int dco, int C, long long pixels) {
+    const long long total = pixels * C;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total; i += (long long)gridDim.x * blockDim.x) {
+        const long long p = i / C;
+        const int c = int(i - p * C);
+        dst[p * dcs + dco + c] = src[p * scs + sco + c];
+    }
+}
+
+__global__ void eltwise_bf16(int op, const __nv_bfloat16* __restrict__ a, int acs, int aco, const __nv_bfloat16* __restrict__ b,
+                             int bcs, int bco, __nv_bfloat16* __restrict__ o, int ocs, int oco, int C, long long pixels) {
+    const long long total = pixels * C;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total; i += (long long)gridDim.x * blockDim.x) {
+        const long long p = i / C;
+        const int c = int(i - p * C);
+        const float x = __bfloat162float(a[p * acs + aco + c]);
+        o[p * ocs + oco + c] = __float2bfloat16(op == 0 ? x + __bfloat162float(b[p * bcs + bco + c]) : fmaxf(x, 0.0f));
+    }
+}
+
+int grid_b(long long work) {
+    long long b = (work + 255) / 256;
+    return int(b < 148 * 16 ? (b < 1 ? 1 : b) : 148 * 16);
+}
+
+}  // namespace
+
+cudaError_t init_fused_bf16() {
+    return cudaFuncSetAttribute(fused_bf16_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024 - 1024);
+}
+
+cudaError_t launch_fused_bf16(const BParams& P, int batch, cudaStream_t st) {
+    fused_bf16_kernel<<<dim3(P.grid_h * P.grid_w, batch, P.cgroups), kBThreads, P.smem_bytes, st>>>(P);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_nchw_to_nhwc_bf16(const float* src, __nv_bfloat16* dst, int N, int C, int H, int W, int cs, cudaStream_t st) {
+    nchw_f32_to_nhwc_bf16<<<grid_b((long long)N * H * W * cs), 256, 0, st>>>(src, dst, N, C, H, W, cs);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_nhwc_bf16_to_nchw(const __nv_bfloat16* src, int cs, int coff, float* dst, int N, int C, int H, int W,
+                                     cudaStream_t st) {
+    nhwc_bf16_to_nchw_f32<<<grid_b((long long)N * C * H * W), 256, 0, st>>>(src, cs, coff, dst, N, C, H, W);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_seeded_nhwc_bf16(__nv_bfloat16* dst, unsigned long long seed, unsigned long long first_image, int N, int C, int H,
+                                    int W, int cs, cudaStream_t st) {
+    seeded_nhwc_bf16<<<grid_b((long long)N * H * W * cs), 256, 0, st>>>(dst, seed ? seed : 0x9e3779b97f4a7c15ull, first_image, N,
+                                                                      C, H, W, cs);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_concat_copy_bf16(const __nv_bfloat16* src, int scs, int sco, __nv_bfloat16* dst, int dcs, int dco, int C,
+                                    long long pixels, cudaStream_t st) {
+    concat_copy_bf16<<<grid_b(pixels * C), 256, 0, st>>>(src, scs, sco, dst, dcs, dco, C, pixels);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_eltwise_bf16(int op, const __nv_bfloat16* a, int acs, int aco, const __nv_bfloat16* b, int bcs, int bco,
+                                __nv_bfloat16* o, int ocs, int oco, int C, long long pixels, cudaStream_t st) {
+    eltwise_bf16<<<grid_b(pixels * C), 256, 0, st>>>(op, a, acs, aco, b, bcs, bco, o, ocs, oco, C, pixels);
+    return cudaGetLastError();
+}
+
+}  // namespace xlf
