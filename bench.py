@@ -191,7 +191,7 @@ def main():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--precision", default="fp32", choices=["fp32", "fp32_exact"])
+    ap.add_argument("--precision", default="bf16", choices=["bf16", "fp32", "fp32_exact"])
     ap.add_argument("--no-blocks", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     args = ap.parse_args()
@@ -323,7 +323,7 @@ def main():
             "higher_is_better": True,
             "scaling": "weak",
             "vs_baseline": None,
-            "dtype": "f32",
+            "dtype": "bf16" if args.precision == "bf16" else "f32",
             "precision": args.precision,
             "data": "synthetic (SeededStream(42) inputs generated on device, seeded_weights(42))",
             "config": {"workload": "squeezenet_v1.1 224x224 inference, b200 partition (8 fused fire blocks, conv1+pool1 fused)",
@@ -337,8 +337,9 @@ def main():
                          "traffic": traffic, "algorithmic_bytes_per_launch": int(alg_bytes),
                          "launch_ms": round(per_step_kernel_ms[dom], 4),
                          "share_of_step": round(per_step_kernel_ms[dom] / sum(per_step_kernel_ms), 4),
-                         "fp32_simt": {"achieved_tflops": round(flops / (per_step_kernel_ms[dom] * 1e-3) / 1e12, 3),
-                                       "peak_tflops": round(simt_peak, 2)}},
+                         "compute": {"pipe": "tcgen05 bf16" if args.precision == "bf16" else "fp32 FMA (SIMT)",
+                                     "achieved_tflops": round(flops / (per_step_kernel_ms[dom] * 1e-3) / 1e12, 3),
+                                     "peak_tflops": round(tf_peak if args.precision == "bf16" else simt_peak, 2)}},
             "kernels_ms": {f"{st_['id']}:{st_['tag']}": round(t, 4) for st_, t in zip(e.steps, per_step_kernel_ms)},
             "cpu_baseline": cpu,
             "gpu_launches": args.steps * e.launches_per_forward,

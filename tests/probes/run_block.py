@@ -1,0 +1,28 @@
+"""Runs one graph's forward a few times (profiling target for ncu).
+
+    python tests/probes/run_block.py fire 32 bf16 b200 5
+"""
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))))
+
+import torch  # noqa: E402
+
+import paper_2007_06000_b200 as X  # noqa: E402
+
+
+def main():
+    name, batch, prec, part, reps = sys.argv[1], int(sys.argv[2]), sys.argv[3], sys.argv[4], int(sys.argv[5])
+    g = X.load_graph(X.graph_path(name))
+    e = X.Engine(g, X.seeded_weights(g, 42), part, prec, max_batch=batch)
+    e.set_input_seeded(42, batch)
+    for _ in range(reps):
+        e.forward(batch, use_graph=False)
+    torch.cuda.synchronize()
+    for s in e.steps:
+        print(s["id"], s["tag"], s["tile"], s["smem_bytes"])
+
+
+if __name__ == "__main__":
+    main()

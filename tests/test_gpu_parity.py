@@ -98,7 +98,8 @@ def test_squeezenet_b256_exact_sampled_and_argmax():
         if l.kind == "conv":
             f, b = w[l.name]
             fan = f.shape[1] * f.shape[2] * f.shape[3]
-            w[l.name] = ((f * np.float32(np.sqrt(6.0 / fan))).astype(np.float32), (b * np.float32(0.1)).astype(np.float32))
+            # He-uniform (bound sqrt(6/fan_in)), zero bias: the signal survives 26 layers
+            w[l.name] = ((f * np.float32(2.0 * np.sqrt(6.0 / fan))).astype(np.float32), (b * np.float32(0.0)).astype(np.float32))
     flat = O.flat_weights(og, w)
     import torch
     g = X.Graph(text)
