@@ -52,11 +52,23 @@ struct BOp {
     int out_cstride, out_coff;
 };
 
+// Layout of a shared region: K-blocks of kb_ch channels; inside a K-block
+// cell r occupies row_bytes at r*row_bytes.
+//   kPlanes : kb_ch = 8,  row 16 B, no swizzle (epilogue-written buffers)
+//   kSw32   : kb_ch = 16, row 32 B, 32-byte swizzle  (TMA box of 16 channels)
+//   kSw128  : kb_ch = 64, row 128 B, 128-byte swizzle (TMA box of 64 channels)
+// Swizzles are functions of the absolute shared address (chunk ^= (addr>>7)
+// & mask), identical for TMA writes, UMMA reads and SIMT reads.
+enum : int { kPlanes = 0, kSw32 = 1, kSw128 = 3 };
+
 struct BRegion {
-    int c8;             // planes (channels / 8)
+    int c8;             // channels / 8
     int ext_h, ext_w;   // cells
-    int plane_bytes;    // ext_h * ext_w * 16
+    int plane_bytes;    // bytes per K-block (multiple of 1024 for swizzled modes)
     int smem_off;       // bytes from the dynamic smem base
+    int mode;           // kPlanes / kSw32 / kSw128
+    int kb_ch;          // channels per K-block (8 / 16 / 64)
+    int row_bytes;      // 16 / 32 / 128
 };
 
 struct BIn {

@@ -379,6 +379,15 @@ bool choose_tile_at(const Graph& g, StepSpec& s, int batch_hint, int smem_budget
                 work += double(o.ext_h) * o.ext_w * o.cout_pad * macs_per_output(*g.find_layer(s.ops[size_t(i)].layer));
             }
             for (int i = 0; i < fp.nins; ++i) work += double(fp.in[i].ext_h) * fp.in[i].ext_w * fp.in[i].c;
+            // Weight traffic: every 8-cell block of a unit re-reads its weights
+            // through L1; past ~64 KB they come from L2 each time (conv10: 2 MB).
+            for (int i = 0; i < fp.nops; ++i) {
+                const FOp& o = fp.ops[i];
+                if (o.kind != OP_CONV) continue;
+                const double wb = double(o.cin / o.group) * o.kh * o.kw * o.cout_pad * 4;
+                const double blocks = std::ceil(double(o.ext_h) * o.ext_w / 8.0);
+                work += 0.5 * (wb > 64 * 1024 ? wb * blocks : wb);
+            }
             const double ctas = double(fp.grid_h) * fp.grid_w * fp.cgroups * std::max(batch_hint, 1);
             const int occ = std::max(1, std::min(8, int((228 * 1024) / (sm + 1024))));
             const double waves = std::ceil(ctas / (148.0 * occ));

@@ -190,17 +190,30 @@ long long layout_bf16(const Graph& g, const StepSpec& s, int th, int tw, BParams
     // shared memory
     long long bytes = 0;
     auto region = [&](BRegion& r) {
-        r.plane_bytes = r128(r.ext_h * r.ext_w * 16);
+        const int kbs = r.kb_ch / 8;  // 8-channel groups per K-block
+        if (r.mode == kPlanes) r.plane_bytes = r128(r.ext_h * r.ext_w * r.row_bytes);
+        else r.plane_bytes = (r.ext_h * r.ext_w * r.row_bytes + 1023) & ~1023;
+        bytes = (bytes + 1023) & ~1023LL;  // swizzle atoms / TMA destinations
         r.smem_off = int(bytes);
-        bytes += (long long)r.c8 * r.plane_bytes + kSlack;
+        bytes += (long long)(r.c8 / kbs) * r.plane_bytes + kSlack;
     };
-    for (BIn& in : ins) region(in.r);
+    // Block inputs arrive by TMA: 64-channel (128 B, SWIZZLE_128B) or
+    // 16-channel (32 B, SWIZZLE_32B) boxes when the channel count allows --
+    // few, wide requests -- else 8-channel planes.
+    for (BIn& in : ins) {
+        const int C = in.r.c8 * 8;
+        if (C % 64 == 0) in.r.mode = kSw128, in.r.kb_ch = 64, in.r.row_bytes = 128;
+        else if (C % 16 == 0) in.r.mode = kSw32, in.r.kb_ch = 16, in.r.row_bytes = 32;
+        else in.r.mode = kPlanes, in.r.kb_ch = 8, in.r.row_bytes = 16;
+        region(in.r);
+    }
     std::vector<BRegion> bufs(static_cast<size_t>(nbufs));
     for (int i = 0; i < nops; ++i) {
         if (bufidx[size_t(i)] < 0) continue;
         BRegion& b = bufs[size_t(bufidx[size_t(i)])];
         b.c8 = r8(g.find_layer(s.ops[size_t(i)].layer)->out_shape->channels) / 8;
         b.ext_h = geo[size_t(i)].ext_h, b.ext_w = geo[size_t(i)].ext_w;
+        b.mode = kPlanes, b.kb_ch = 8, b.row_bytes = 16;  // written by the epilogue threads
         region(b);
     }
     bool any_mma = false;
@@ -319,7 +332,10 @@ static bool choose_tile_bf16_at(const Graph& g, StepSpec& s, int batch_hint, int
             if (P->tmem_cols) occ = std::min(occ, 512 / P->tmem_cols);
             const double waves = std::ceil(ctas / (148.0 * occ));
             // cycles per CTA ~ bytes/(per-SM HBM share) + MMA (8192 MAC/clk/SM) + SIMT (128 FMA/clk)
-            const double per_cta = (in_bytes + out_bytes) / 24.0 + mma / 8192.0 + simt / 128.0 + 1500.0;
+            double wbytes = 0;  // weights each CTA streams from L2 through the ring
+            for (int i = 0; i < P->nops; ++i)
+                if (P->ops[i].kind == BOP_MMA) wbytes += double(P->ops[i].nblocks) * P->ops[i].ksteps * P->ops[i].nb * 32;
+            const double per_cta = (in_bytes + out_bytes) / 24.0 + wbytes / 96.0 + mma / 8192.0 + simt / 128.0 + 1500.0;
             const double t = waves * per_cta * occ / std::min(double(occ), 2.0);
             if (t < best * 0.999 || (t <= best * 1.001 && long(th) * tw > long(bh) * bw))
                 best = t, bh = th, bw = tw, bsm = int(sm);

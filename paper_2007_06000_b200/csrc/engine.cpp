@@ -33,6 +33,8 @@ cudaError_t launch_seeded_nhwc_bf16(__nv_bfloat16* dst, unsigned long long seed,
                                     int W, int cs, cudaStream_t st);
 cudaError_t launch_concat_copy_bf16(const __nv_bfloat16* src, int scs, int sco, __nv_bfloat16* dst, int dcs, int dco, int C,
                                     long long pixels, cudaStream_t st);
+cudaError_t launch_s2d_bf16(const float* src, unsigned long long seed, unsigned long long first_image, __nv_bfloat16* dst, int N,
+                            int C, int H, int W, int cs, cudaStream_t st);
 cudaError_t launch_eltwise_bf16(int op, const __nv_bfloat16* a, int acs, int aco, const __nv_bfloat16* b, int bcs, int bco,
                                 __nv_bfloat16* o, int ocs, int oco, int C, long long pixels, cudaStream_t st);
 
@@ -85,17 +87,66 @@ PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
     return fn;
 }
 
-// 4-D map over an NHWC bf16 tensor {cstride, W, H, N}; box = one 8-channel
-// plane of an ext_h x ext_w region (16-byte inner box), zero fill outside.
-void encode_plane_map(CUtensorMap* map, const void* base, int cstride, int W, int H, int N, int ext_w, int ext_h) {
+// 4-D map over an NHWC bf16 tensor {cstride, W, H, N}; box = one K-block
+// (kb_ch channels: 8 unswizzled, 16 with SWIZZLE_32B, 64 with SWIZZLE_128B)
+// of an ext_h x ext_w region, zero fill outside the image.
+void encode_region_map(CUtensorMap* map, const void* base, int cstride, int W, int H, int N, const BRegion& r) {
     const cuuint64_t dims[4] = {cuuint64_t(cstride), cuuint64_t(W), cuuint64_t(H), cuuint64_t(N)};
     const cuuint64_t strides[3] = {cuuint64_t(cstride) * 2, cuuint64_t(W) * cstride * 2, cuuint64_t(H) * W * cstride * 2};
-    const cuuint32_t box[4] = {8, cuuint32_t(ext_w), cuuint32_t(ext_h), 1};
+    const cuuint32_t box[4] = {cuuint32_t(r.kb_ch), cuuint32_t(r.ext_w), cuuint32_t(r.ext_h), 1};
     const cuuint32_t estr[4] = {1, 1, 1, 1};
-    const CUresult r = tensor_map_encoder()(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(base), dims, strides, box, estr,
-                                            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
-                                            CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-    if (r != CUDA_SUCCESS) fail(ErrorKind::cuda, "cuTensorMapEncodeTiled failed (" + std::to_string(int(r)) + ")");
+    const CUtensorMapSwizzle sw = r.mode == kSw128 ? CU_TENSOR_MAP_SWIZZLE_128B
+                                  : r.mode == kSw32 ? CU_TENSOR_MAP_SWIZZLE_32B
+                                                    : CU_TENSOR_MAP_SWIZZLE_NONE;
+    const CUresult res = tensor_map_encoder()(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(base), dims, strides, box,
+                                              estr, CU_TENSOR_MAP_INTERLEAVE_NONE, sw, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                                              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (res != CUDA_SUCCESS) fail(ErrorKind::cuda, "cuTensorMapEncodeTiled failed (" + std::to_string(int(res)) + ")");
+}
+
+// bf16 only: a stride-2, pad-0 conv reading the graph input (SqueezeNet conv1:
+// 3x3/2 on 3 channels) cannot use the stride-1 implicit GEMM.  Rewrite it as a
+// stride-1 ceil(k/2) x ceil(k/2) conv over the space-to-depth input
+// (4 phases x C channels, padded to 16): out(y,x) = sum over phase (py,px),
+// tap (ty,tx) of in(2(y+ty)+py, 2(x+tx)+px) * W[2ty+py][2tx+px]; identical
+// sums, so the conv runs on tensor cores.  Returns false when not applicable.
+bool rewrite_s2d(Graph& g, std::vector<float>& w) {
+    if (g.inputs.size() != 1) return false;
+    const GraphInput in = g.inputs[0];
+    const int C = in.shape.channels;
+    if (4 * C > 16 || in.shape.height % 2 || in.shape.width % 2) return false;
+    const auto readers = g.consumers_of(in.name);
+    if (readers.size() != 1) return false;
+    Layer* l = g.find_layer(readers[0]);
+    if (l->kind != LayerKind::conv || l->conv->stride != 2 || l->conv->pad != 0 || l->conv->group != 1 || l->conv->kernel_h > 4 ||
+        l->conv->kernel_w > 4)
+        return false;
+    // new weights for this layer (save_weights order: filter then bias, layers in file order)
+    size_t off = 0;
+    for (const Layer& x : g.layers) {
+        if (&x == l) break;
+        if (x.kind == LayerKind::conv) off += size_t(x.conv->weight_count() + x.conv->bias_count());
+    }
+    const ConvParams c = *l->conv;
+    const int kh2 = (c.kernel_h + 1) / 2, kw2 = (c.kernel_w + 1) / 2, cin2 = 16;
+    std::vector<float> f2(size_t(c.out_channels) * cin2 * kh2 * kw2, 0.0f);
+    for (int oc = 0; oc < c.out_channels; ++oc)
+        for (int ci = 0; ci < C; ++ci)
+            for (int ky = 0; ky < c.kernel_h; ++ky)
+                for (int kx = 0; kx < c.kernel_w; ++kx) {
+                    const int ph = (ky % 2) * 2 + kx % 2, ty = ky / 2, tx = kx / 2;
+                    f2[((size_t(oc) * cin2 + ph * C + ci) * kh2 + ty) * kw2 + tx] =
+                        w[off + ((size_t(oc) * C + ci) * c.kernel_h + ky) * c.kernel_w + kx];
+                }
+    const size_t nf = size_t(c.weight_count());
+    w.erase(w.begin() + long(off), w.begin() + long(off + nf));
+    w.insert(w.begin() + long(off), f2.begin(), f2.end());
+    g.inputs[0].shape = {cin2, in.shape.height / 2, in.shape.width / 2};
+    l->conv->kernel_h = kh2, l->conv->kernel_w = kw2, l->conv->stride = 1, l->conv->in_channels = cin2;
+    const TensorShape before = *l->out_shape;
+    g = infer_shapes(g);
+    if (!(*g.find_layer(readers[0])->out_shape == before)) fail(ErrorKind::internal, "s2d rewrite changed the conv output shape");
+    return true;
 }
 
 }  // namespace
@@ -107,6 +158,13 @@ Engine::Engine(const Graph& g, int device, Partition part, Precision prec, const
     if (g_.inputs.size() != 1) fail(ErrorKind::validation, "engine: graphs with exactly one input are supported");
     const bool bf = prec == Precision::bf16;
     esz_ = bf ? 2 : 4;
+    in_shape_ = g_.inputs[0].shape;
+    std::vector<float> wcopy;
+    if (bf) {
+        wcopy.assign(weights, weights + nweights);
+        s2d_ = rewrite_s2d(g_, wcopy);
+        if (s2d_) weights = wcopy.data(), nweights = wcopy.size();
+    }
     cuda_check(cudaSetDevice(device), "cudaSetDevice");
     plan_ = plan_device(g_, part, max_batch, 227 * 1024, bf);
     cuda_check(bf ? init_fused_bf16() : init_fused_fp32(), "kernel attributes");
@@ -150,7 +208,7 @@ Engine::Engine(const Graph& g, int device, Partition part, Precision prec, const
             BIn& in = P->in[k];
             in.x = reinterpret_cast<const __nv_bfloat16*>(allocs_[size_t(t.alloc)]);
             in.cstride = t.cstride, in.coff = t.coff;
-            encode_plane_map(&P->xmap[k], in.x, t.cstride, t.W, t.H, max_batch, in.r.ext_w, in.r.ext_h);
+            encode_region_map(&P->xmap[k], in.x, t.cstride, t.W, t.H, max_batch, in.r);
         }
         for (int k = 0; k < P->nops; ++k) {
             const OpSpec& os = s.ops[size_t(k)];
@@ -190,7 +248,11 @@ const TensorSlot& Engine::slot(const std::string& n) const {
 void Engine::set_input_nchw(const std::string& name, const float* d, int batch, cudaStream_t st) {
     if (batch < 1 || batch > max_batch_) fail(ErrorKind::validation, "batch out of range");
     const TensorSlot& t = slot(name);
-    if (esz_ == 2)
+    if (s2d_)
+        cuda_check(launch_s2d_bf16(d, 0, 0, reinterpret_cast<__nv_bfloat16*>(allocs_[size_t(t.alloc)]), batch, in_shape_.channels,
+                                   in_shape_.height, in_shape_.width, t.cstride, st),
+                   "space-to-depth input");
+    else if (esz_ == 2)
         cuda_check(launch_nchw_to_nhwc_bf16(d, reinterpret_cast<__nv_bfloat16*>(allocs_[size_t(t.alloc)]), batch, t.C, t.H, t.W,
                                             t.cstride, st),
                    "nchw_to_nhwc");
@@ -201,7 +263,11 @@ void Engine::set_input_nchw(const std::string& name, const float* d, int batch, 
 void Engine::set_input_seeded(const std::string& name, uint64_t seed, uint64_t first_image, int batch, cudaStream_t st) {
     if (batch < 1 || batch > max_batch_) fail(ErrorKind::validation, "batch out of range");
     const TensorSlot& t = slot(name);
-    if (esz_ == 2)
+    if (s2d_)
+        cuda_check(launch_s2d_bf16(nullptr, seed, first_image, reinterpret_cast<__nv_bfloat16*>(allocs_[size_t(t.alloc)]), batch,
+                                   in_shape_.channels, in_shape_.height, in_shape_.width, t.cstride, st),
+                   "seeded space-to-depth input");
+    else if (esz_ == 2)
         cuda_check(launch_seeded_nhwc_bf16(reinterpret_cast<__nv_bfloat16*>(allocs_[size_t(t.alloc)]), seed, first_image, batch, t.C,
                                            t.H, t.W, t.cstride, st),
                    "seeded fill");
@@ -304,7 +370,7 @@ void Engine::run_host(const float* h_in, int batch, const std::string& out_name,
     if (batch < 1 || batch > max_batch_) fail(ErrorKind::validation, "batch out of range");
     cuda_check(cudaSetDevice(device_), "cudaSetDevice");
     const GraphInput& in = g_.inputs[0];
-    const size_t n_in = size_t(in.shape.elements()) * batch;
+    const size_t n_in = size_t(in_shape_.elements()) * batch;  // user-facing NCHW input
     cuda_check(cudaMemcpyAsync(staging_, h_in, n_in * 4, cudaMemcpyHostToDevice, st), "H2D input");
     set_input_nchw(in.name, staging_, batch, st);
     forward(batch, st, true);

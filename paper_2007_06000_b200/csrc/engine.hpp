@@ -66,6 +66,8 @@ private:
     std::vector<std::unique_ptr<struct BParams>> bparams_;  // bf16 steps
     void* weights16_ = nullptr;  // bf16 MMA weights
     int esz_ = 4;                // bytes per activation element
+    bool s2d_ = false;           // bf16: first conv rewritten on a space-to-depth input
+    TensorShape in_shape_;       // user-facing (NCHW) input shape
     std::map<int, cudaGraphExec_t> graphs_;
 };
 

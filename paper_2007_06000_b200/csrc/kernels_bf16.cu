@@ -60,8 +60,10 @@ __device__ void producer(const BParams& P, uint8_t* smem, const BTile& t, uint64
     for (int k = 0; k < P.nins; ++k) {
         const BIn& in = P.in[k];
         const int x0 = t.ox0 * in.org_mul - in.org_sub, y0 = t.oy0 * in.org_mul - in.org_sub;
-        for (int p = 0; p < in.r.c8; ++p)
-            tma_load_4d(smem + in.r.smem_off + p * in.r.plane_bytes, &P.xmap[k], in.coff + t.c0 + 8 * p, x0, y0, t.n, bar_x);
+        const int nkb = in.r.c8 * 8 / in.r.kb_ch;
+        for (int kb = 0; kb < nkb; ++kb)
+            tma_load_4d(smem + in.r.smem_off + kb * in.r.plane_bytes, &P.xmap[k], in.coff + t.c0 + kb * in.r.kb_ch, x0, y0, t.n,
+                        bar_x);
     }
     int c = 0;
     for (int i = 0; i < P.nops; ++i) {
@@ -110,18 +112,24 @@ __device__ void issuer(const BParams& P, uint8_t* smem, uint32_t tmem, uint64_t*
                     const int tap = s / c16, kc = s - tap * c16;
                     const int dy = tap / op.kw, dx = tap - dy * op.kw;
                     const uint64_t bd = sdesc(wslot + sl * op.nb * 32, op.nb * 16, 128, kNoSwizzle);
+                    // K16 step kc inside the source region's K-blocks
+                    uint32_t kofs, lbo, layout;
+                    if (R.mode == kPlanes) kofs = kc * 2 * R.plane_bytes, lbo = R.plane_bytes, layout = kNoSwizzle;
+                    else if (R.mode == kSw32) kofs = kc * R.plane_bytes, lbo = 16, layout = kSW32;
+                    else kofs = (kc >> 2) * R.plane_bytes + (kc & 3) * 32, lbo = 16, layout = kSW128;
                     for (int mt = 0; mt < op.mtiles; ++mt) {
-                        uint32_t a;
+                        int cell;
                         uint32_t sbo;
                         if (op.contig) {
-                            a = src + kc * 2 * R.plane_bytes + mt * 128 * 16;
-                            sbo = 128;
+                            cell = mt * 128;
+                            sbo = 8 * R.row_bytes;
                         } else {
                             const int st = mt % op.strips, rb = mt / op.strips;
-                            a = src + kc * 2 * R.plane_bytes + ((rb * 16 + dy + op.d) * R.ext_w + st * 8 + dx + op.d) * 16;
-                            sbo = R.ext_w * 16;
+                            cell = (rb * 16 + dy + op.d) * R.ext_w + st * 8 + dx + op.d;
+                            sbo = R.ext_w * R.row_bytes;
                         }
-                        mma_bf16(tmem + mt * op.nb, sdesc(a, R.plane_bytes, sbo, kNoSwizzle), bd, idesc, s > 0 ? 1u : 0u);
+                        const uint32_t a = src + kofs + cell * R.row_bytes;
+                        mma_bf16(tmem + mt * op.nb, sdesc(a, lbo, sbo, layout), bd, idesc, s > 0 ? 1u : 0u);
                     }
                 }
                 commit(&ring_empty[slot]);
@@ -195,8 +203,20 @@ __device__ void epilogue_mma(const BParams& P, const BOp& op, int nbi, uint8_t* 
     }
 }
 
+// Shared byte offset of 16-byte chunk `oct` (channels [8*oct, 8*oct+8)) of a
+// cell, honouring the region's swizzle (a function of the absolute address).
+__device__ __forceinline__ uint32_t chunk_off(const uint8_t* smem, const BRegion& R, int cell, int oct) {
+    const int per = R.kb_ch >> 3;  // 16-byte chunks per row
+    const int kb = oct / per, j = oct - kb * per;
+    const uint32_t off = R.smem_off + kb * R.plane_bytes + cell * R.row_bytes + j * 16;
+    if (R.mode == kPlanes) return off;
+    const uint32_t a = smem_u32(smem) + off;
+    const uint32_t mask = R.mode == kSw128 ? 7u : 1u;
+    return off ^ (((a >> 7) & mask) << 4);
+}
+
 __device__ __forceinline__ void load8(const uint8_t* smem, const BRegion& R, int cell, int oct, float* f) {
-    const uint4 raw = *reinterpret_cast<const uint4*>(smem + R.smem_off + oct * R.plane_bytes + cell * 16);
+    const uint4 raw = *reinterpret_cast<const uint4*>(smem + chunk_off(smem, R, cell, oct));
     const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&raw);
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
@@ -257,7 +277,7 @@ __device__ void simt_conv(const BParams& P, const BOp& op, uint8_t* smem, const 
                         if (oc >= op.cout) break;
                         const int in_c = (oc / cout_g) * cin_g + ic;
                         const __nv_bfloat16 xv = *reinterpret_cast<const __nv_bfloat16*>(
-                            smem + R.smem_off + (in_c >> 3) * R.plane_bytes + cell_in * 16 + (in_c & 7) * 2);
+                            smem + chunk_off(smem, R, cell_in, in_c >> 3) + (in_c & 7) * 2);
                         acc[j] = fmaf(__bfloat162float(xv), __ldg(wrow + oc), acc[j]);
                     }
                 }
@@ -377,6 +397,38 @@ __global__ void seeded_nhwc_bf16(__nv_bfloat16* __restrict__ dst, unsigned long 
     }
 }
 
+// Space-to-depth input for a stride-2 first conv (see Engine: the conv is
+// rewritten as a stride-1 conv on 2x2 phases so it runs on tensor cores):
+// dst[n][Y][X][(py*2+px)*C + c] = src[n][c][2Y+py][2X+px], channels >= 4C zero.
+// Source is NCHW fp32 (src != nullptr) or the SeededStream (seed, first_image).
+__global__ void s2d_bf16(const float* __restrict__ src, unsigned long long seed, unsigned long long first_image,
+                         __nv_bfloat16* __restrict__ dst, int N, int C, int H, int W, int cs) {
+    const int H2 = H / 2, W2 = W / 2;
+    const long long total = (long long)N * H2 * W2 * cs;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total; i += (long long)gridDim.x * blockDim.x) {
+        const int ci = int(i % cs);
+        const long long p = i / cs;
+        const int X = int(p % W2), Y = int((p / W2) % H2);
+        const long long n = p / ((long long)W2 * H2);
+        float v = 0.0f;
+        if (ci < 4 * C) {
+            const int ph = ci / C, c = ci - ph * C;
+            const int y = 2 * Y + (ph >> 1), x = 2 * X + (ph & 1);
+            const unsigned long long idx = (((unsigned long long)n * C + c) * H + y) * (unsigned long long)W + x;
+            if (src) {
+                v = src[idx];
+            } else {
+                unsigned long long z = seed + (first_image * (unsigned long long)C * H * W + idx + 1ull) * 0x9e3779b97f4a7c15ull;
+                z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ull;
+                z = (z ^ (z >> 27)) * 0x94d049bb133111ebull;
+                z = z ^ (z >> 31);
+                v = static_cast<float>(z >> 40) * (1.0f / 16777216.0f) - 0.5f;
+            }
+        }
+        dst[i] = __float2bfloat16(v);
+    }
+}
+
 __global__ void concat_copy_bf16(const __nv_bfloat16* __restrict__ src, int scs, int sco, __nv_bfloat16* __restrict__ dst, int dcs,
                                  int dco, int C, long long pixels) {
     const long long total = pixels * C;
@@ -429,6 +481,13 @@ cudaError_t launch_seeded_nhwc_bf16(__nv_bfloat16* dst, unsigned long long seed,
                                     int W, int cs, cudaStream_t st) {
     seeded_nhwc_bf16<<<grid_b((long long)N * H * W * cs), 256, 0, st>>>(dst, seed ? seed : 0x9e3779b97f4a7c15ull, first_image, N,
                                                                       C, H, W, cs);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_s2d_bf16(const float* src, unsigned long long seed, unsigned long long first_image, __nv_bfloat16* dst, int N,
+                            int C, int H, int W, int cs, cudaStream_t st) {
+    s2d_bf16<<<grid_b((long long)N * (H / 2) * (W / 2) * cs), 256, 0, st>>>(src, seed ? seed : 0x9e3779b97f4a7c15ull, first_image, dst,
+                                                                          N, C, H, W, cs);
     return cudaGetLastError();
 }
 
