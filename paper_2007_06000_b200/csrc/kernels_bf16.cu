@@ -1,14 +1,14 @@
 // bf16 tensor-core fused-block kernel for sm_100a (tcgen05 + TMEM + TMA).
 //
-// One CTA = (image, output tile).  192 threads in three roles:
-//   warp 4      producer: TMA of the block inputs (one 4-D box per 8-channel
+// One CTA = (image, output tile).  320 threads in three roles:
+//   warp 8      producer: TMA of the block inputs (one 4-D box per 8-channel
 //               plane, zero fill outside the image) and cp.async.bulk of the
 //               packed weights through a 3-slot ring (full/empty mbarriers);
-//   warp 5      MMA issuer: one thread issues tcgen05.mma (M=128, N<=256,
+//   warp 9      MMA issuer: one thread issues tcgen05.mma (M=128, N<=256,
 //               K=16, bf16 x bf16 -> fp32 in TMEM) for every conv "unit"
 //               (op x N block), commits to the ring and to the unit's
 //               accumulator barrier; the warp owns TMEM alloc/dealloc;
-//   warps 0-3   epilogue + SIMT ops: tcgen05.ld the accumulator (lane = GEMM
+//   warps 0-7   epilogue + SIMT ops: tcgen05.ld the accumulator (lane = GEMM
 //               row = output cell), bias + ReLU + halo mask, bf16, and either
 //               keep it on chip (shared "planes" buffer that the next stage's
 //               MMAs read with shifted descriptors) or store NHWC to HBM at
@@ -31,13 +31,14 @@ namespace {
 
 using namespace umma;
 
-constexpr int kBThreads = 192;
+constexpr int kCompute = 256;                 // warps 0-7: epilogue + SIMT ops
+constexpr int kBThreads = kCompute + 64;      // warp 8: producer, warp 9: MMA issuer
 
 struct BTile {
     int n, ty, tx, oy0, ox0, c0;
 };
 
-__device__ __forceinline__ void named_sync_compute() { asm volatile("bar.sync 1, 128;\n" ::: "memory"); }
+__device__ __forceinline__ void named_sync_compute() { asm volatile("bar.sync 1, %0;\n" ::"n"(kCompute) : "memory"); }
 
 __device__ __forceinline__ const BRegion& src_region(const BParams& P, const BOp& op, int which) {
     return op.stage == 1 ? P.in[op.xin].r : P.bufs[which];
@@ -150,28 +151,72 @@ __device__ __forceinline__ bool owns(const BParams& P, const BOp& op, const BTil
     return gy >= t.oy0 * S && gy < y1 && gx >= t.ox0 * S && gx < x1;
 }
 
-// Stores 8 channels [ch, ch+8) of one computed cell (fp32 values).
-__device__ __forceinline__ void put8(const BParams& P, const BOp& op, uint8_t* smem, const BTile& t, int r, int c, int ch,
-                                     const float* v8) {
+// Destination of one computed cell: the on-chip buffer (planes layout) and/or
+// its NHWC pixel in HBM.  Computed once per cell, reused for every channel.
+struct CellDst {
+    bool valid, inside;
+    uint8_t* sbuf;        // plane-0 address of the cell in the shared buffer, or null
+    int plane_bytes;
+    __nv_bfloat16* gdst;  // channel-0 address of the pixel (concat offset applied), or null
+};
+
+__device__ __forceinline__ CellDst cell_dst(const BParams& P, const BOp& op, uint8_t* smem, const BTile& t, int r, int c, bool valid) {
+    CellDst d;
     const int gy = t.oy0 * op.org_mul - op.org_sub + r, gx = t.ox0 * op.org_mul - op.org_sub + c;
-    const bool inside = gy >= 0 && gy < op.H && gx >= 0 && gx < op.W;
-    __align__(16) __nv_bfloat162 h[4];
-#pragma unroll
-    for (int j = 0; j < 4; ++j) h[j] = __floats2bfloat162_rn(v8[2 * j], v8[2 * j + 1]);
+    d.valid = valid;
+    d.inside = gy >= 0 && gy < op.H && gx >= 0 && gx < op.W;
+    d.sbuf = nullptr, d.gdst = nullptr, d.plane_bytes = 0;
     if (op.buf >= 0) {
         const BRegion& B = P.bufs[op.buf];
-        uint4 val = inside ? *reinterpret_cast<uint4*>(h) : make_uint4(0, 0, 0, 0);
-        *reinterpret_cast<uint4*>(smem + B.smem_off + (ch >> 3) * B.plane_bytes + (r * B.ext_w + c) * 16) = val;
+        d.sbuf = smem + B.smem_off + (r * B.ext_w + c) * 16;
+        d.plane_bytes = B.plane_bytes;
     }
-    if (op.emit && inside && owns(P, op, t, gy, gx)) {
-        __nv_bfloat16* dst = op.out + ((size_t(t.n) * op.H + gy) * op.W + gx) * op.out_cstride + op.out_coff + t.c0 + ch;
-        *reinterpret_cast<uint4*>(dst) = *reinterpret_cast<uint4*>(h);
+    if (op.emit && valid && d.inside && owns(P, op, t, gy, gx))
+        d.gdst = op.out + ((size_t(t.n) * op.H + gy) * op.W + gx) * op.out_cstride + op.out_coff + t.c0;
+    return d;
+}
+
+__device__ __forceinline__ uint4 pack8(const float* v) {
+    uint4 u;
+    __nv_bfloat162 h;
+    h = __floats2bfloat162_rn(v[0], v[1]), u.x = *reinterpret_cast<uint32_t*>(&h);
+    h = __floats2bfloat162_rn(v[2], v[3]), u.y = *reinterpret_cast<uint32_t*>(&h);
+    h = __floats2bfloat162_rn(v[4], v[5]), u.z = *reinterpret_cast<uint32_t*>(&h);
+    h = __floats2bfloat162_rn(v[6], v[7]), u.w = *reinterpret_cast<uint32_t*>(&h);
+    return u;
+}
+
+// Stores 8 channels [ch, ch+8) of one cell (values already final).
+__device__ __forceinline__ void put8(const CellDst& d, int ch, const float* v8) {
+    const uint4 u = pack8(v8);
+    if (d.sbuf) *reinterpret_cast<uint4*>(d.sbuf + (ch >> 3) * d.plane_bytes) = d.inside ? u : make_uint4(0, 0, 0, 0);
+    if (d.gdst) *reinterpret_cast<uint4*>(d.gdst + ch) = u;
+}
+
+// Bias + ReLU + store of N accumulator columns (channels ch0 ...), unrolled.
+template <int N>
+__device__ __forceinline__ void finish_cols(const BOp& op, const CellDst& d, int ch0, int c8end, float* v) {
+#pragma unroll
+    for (int j = 0; j < N; j += 8) {
+        if (ch0 + j >= c8end) break;
+        const float4 b0 = __ldg(reinterpret_cast<const float4*>(op.bias + ch0 + j));
+        const float4 b1 = __ldg(reinterpret_cast<const float4*>(op.bias + ch0 + j + 4));
+        float* x = v + j;
+        x[0] += b0.x, x[1] += b0.y, x[2] += b0.z, x[3] += b0.w, x[4] += b1.x, x[5] += b1.y, x[6] += b1.z, x[7] += b1.w;
+        if (op.relu)
+#pragma unroll
+            for (int k = 0; k < 8; ++k) x[k] = fmaxf(x[k], 0.0f);
+        put8(d, ch0 + j, x);
     }
 }
 
+// Accumulator -> bias/ReLU/mask -> bf16 -> shared buffer and/or HBM.  Thread
+// (row = tid % 128) owns TMEM lane `row` = GEMM row = one cell; the two
+// warp groups split the accumulator columns in 32-column slices.
 __device__ void epilogue_mma(const BParams& P, const BOp& op, int nbi, uint8_t* smem, uint32_t tmem, const BTile& t) {
-    const int row = threadIdx.x;  // 0..127 == TMEM lane == GEMM row
-    const uint32_t lane_base = uint32_t(threadIdx.x & ~31) << 16;
+    const int row = threadIdx.x & 127, half = threadIdx.x >> 7;
+    const uint32_t lane_base = uint32_t(row & ~31) << 16;
+    const int c8end = (op.cout + 7) & ~7;  // never write past the tensor's padded channels
     for (int mt = 0; mt < op.mtiles; ++mt) {
         int r, c;
         bool valid;
@@ -184,21 +229,19 @@ __device__ void epilogue_mma(const BParams& P, const BOp& op, int nbi, uint8_t* 
             r = rb * 16 + (row >> 3), c = st * 8 + (row & 7);
             valid = r < op.ext_h && c < op.ext_w;
         }
-        for (int col = 0; col < op.nb; col += 32) {
-            float v[32];
+        const CellDst d = cell_dst(P, op, smem, t, r, c, valid);
+        for (int col = half * 32; col < op.nb; col += 64) {
             const uint32_t ta = tmem + lane_base + mt * op.nb + col;
-            const int ncol = min(32, op.nb - col);
-            if (ncol == 32) tmem_ld32(ta, v);
-            else tmem_ld16(ta, v);
-            if (!valid) continue;
             const int ch0 = nbi * op.nb + col;
-            for (int j = 0; j < ncol; ++j) {
-                float x = v[j] + __ldg(op.bias + ch0 + j);
-                v[j] = op.relu ? fmaxf(x, 0.0f) : x;
+            if (op.nb - col >= 32) {
+                float v[32];
+                tmem_ld32(ta, v);
+                if (valid) finish_cols<32>(op, d, ch0, c8end, v);
+            } else {
+                float v[16];
+                tmem_ld16(ta, v);
+                if (valid) finish_cols<16>(op, d, ch0, c8end, v);
             }
-            const int c8end = (op.cout + 7) & ~7;  // never write past the tensor's padded channels
-            for (int j = 0; j < ncol; j += 8)
-                if (ch0 + j < c8end) put8(P, op, smem, t, r, c, ch0 + j, v + j);
         }
     }
 }
@@ -231,7 +274,7 @@ __device__ void simt_pool_add(const BParams& P, const BOp& op, uint8_t* smem, co
     const BRegion& R = src_region(P, op, op.src);
     const int ncell = op.ext_h * op.ext_w, c8 = op.npad / 8;
     const float inv = 1.0f / float(op.kh * op.kw);
-    for (int u = threadIdx.x; u < ncell * c8; u += 128) {
+    for (int u = threadIdx.x; u < ncell * c8; u += kCompute) {
         const int cell = u / c8, oct = u - cell * c8;
         const int r = cell / op.ext_w, c = cell - r * op.ext_w;
         float acc[8], x[8];
@@ -250,7 +293,7 @@ __device__ void simt_pool_add(const BParams& P, const BOp& op, uint8_t* smem, co
             if (op.kind == BOP_AVGPOOL)
                 for (int j = 0; j < 8; ++j) acc[j] *= inv;
         }
-        put8(P, op, smem, t, r, c, oct * 8, acc);
+        put8(cell_dst(P, op, smem, t, r, c, true), oct * 8, acc);
     }
 }
 
@@ -260,7 +303,7 @@ __device__ void simt_conv(const BParams& P, const BOp& op, uint8_t* smem, const 
     const BRegion& R = src_region(P, op, op.src);
     const int ncell = op.ext_h * op.ext_w, c8 = op.npad / 8;
     const int cin_g = op.cin / op.group, cout_g = op.cout / op.group, cp4 = (op.cout + 3) & ~3;
-    for (int u = threadIdx.x; u < ncell * c8; u += 128) {
+    for (int u = threadIdx.x; u < ncell * c8; u += kCompute) {
         const int cell = u / c8, oct = u - cell * c8;
         const int r = cell / op.ext_w, c = cell - r * op.ext_w;
         float acc[8];
@@ -286,7 +329,7 @@ __device__ void simt_conv(const BParams& P, const BOp& op, uint8_t* smem, const 
             float x = oc < op.cout ? acc[j] + __ldg(op.bias + oc) : 0.0f;
             acc[j] = op.relu ? fmaxf(x, 0.0f) : x;
         }
-        put8(P, op, smem, t, r, c, oct * 8, acc);
+        put8(cell_dst(P, op, smem, t, r, c, true), oct * 8, acc);
     }
 }
 
@@ -310,15 +353,15 @@ __global__ void __launch_bounds__(kBThreads, 1) fused_bf16_kernel(const __grid_c
         for (int i = 0; i < units; ++i) mbar_init(&acc_full[i], 1), mbar_init(&unit_done[i], 1);
         mbar_fence_init();
     }
-    if (warp == 5 && P.tmem_cols) tmem_alloc(&tmem_slot, P.tmem_cols);
+    if (warp == 9 && P.tmem_cols) tmem_alloc(&tmem_slot, P.tmem_cols);
     fence_before();
     __syncthreads();
     fence_after();
     const uint32_t tmem = P.tmem_cols ? tmem_slot : 0;
 
-    if (warp == 4) {
+    if (warp == 8) {
         if (lane == 0) producer(P, smem, t, &bar_x, ring_full, ring_empty);
-    } else if (warp == 5) {
+    } else if (warp == 9) {
         if (lane == 0) issuer(P, smem, tmem, &bar_x, ring_full, ring_empty, acc_full, unit_done);
         __syncwarp();
     } else {
@@ -347,7 +390,7 @@ __global__ void __launch_bounds__(kBThreads, 1) fused_bf16_kernel(const __grid_c
     fence_before();
     __syncthreads();
     fence_after();
-    if (warp == 5 && P.tmem_cols) tmem_free(tmem, P.tmem_cols);
+    if (warp == 9 && P.tmem_cols) tmem_free(tmem, P.tmem_cols);
 }
 
 // ----------------------------------------------------------------- layout kernels (bf16)
