@@ -109,6 +109,9 @@ xlf_status xlf_engine_read(xlf_engine* e, const char* name, float* d_nchw, int b
  * `name` into h_out (NCHW). Synchronous. */
 xlf_status xlf_engine_run_host(xlf_engine* e, const float* h_in_nchw, int batch, const char* name, float* h_out_nchw,
                                void* stream);
+/* Profiling aid (engine created with XLF_TRACE=1 in the environment, bf16):
+ * globaltimer stamps of the first CTAs of a step's last launch. */
+xlf_status xlf_engine_trace(const xlf_engine* e, int step, unsigned long long* out, size_t cap, size_t* count);
 
 #ifdef __cplusplus
 }

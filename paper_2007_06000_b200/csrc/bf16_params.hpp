@@ -89,6 +89,16 @@ struct alignas(64) BParams {
     int ring_off, chunk_bytes;
     int smem_bytes, tmem_cols;
     int ctile, cgroups;  // channel tiling of pool-only steps (0 = all channels)
+    // Optional phase trace (XLF_TRACE=1): globaltimer stamps of CTAs with
+    // blockIdx.y == 0 and blockIdx.x < kTraceCtas, kTraceEvents each.
+    unsigned long long* trace;
+};
+
+constexpr int kTraceCtas = 8;
+constexpr int kTraceEvents = 32;
+enum : int {  // trace slots
+    kTrStart = 0, kTrXIssued = 1, kTrXLanded = 2, kTrEnd = 3,
+    kTrUnit = 4  // + 2u: accumulator ready seen by the epilogue, + 2u + 1: unit done
 };
 
 }  // namespace xlf

@@ -316,3 +316,15 @@ xlf_status xlf_engine_run_host(xlf_engine* e, const float* h_in, int batch, cons
 }
 
 }  // extern "C"
+
+extern "C" xlf_status xlf_engine_trace(const xlf_engine* e, int step, unsigned long long* out, size_t cap, size_t* count) {
+    return guard([&] {
+        need_ptr(e, "engine");
+        const std::vector<unsigned long long> t = e->e->trace(step);
+        if (count) *count = t.size();
+        if (out) {
+            if (cap < t.size()) xlf::fail(xlf::ErrorKind::validation, "output buffer too small");
+            std::memcpy(out, t.data(), t.size() * sizeof(unsigned long long));
+        }
+    });
+}

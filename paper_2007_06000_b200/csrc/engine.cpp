@@ -4,6 +4,7 @@
 #include <cudaTypedefs.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <sstream>
 
@@ -224,6 +225,14 @@ Engine::Engine(const Graph& g, int device, Partition part, Precision prec, const
                 o.out_cstride = t.cstride, o.out_coff = t.coff;
             }
         }
+        if (std::getenv("XLF_TRACE")) {  // phase stamps of a few CTAs (profiling aid)
+            unsigned long long* tr = nullptr;
+            const size_t n = size_t(kTraceCtas) * kTraceEvents;
+            cuda_check(cudaMalloc(&tr, n * 8), "cudaMalloc(trace)");
+            cuda_check(cudaMemset(tr, 0, n * 8), "cudaMemset(trace)");
+            P->trace = tr;
+            traces_.push_back(tr);
+        }
         bparams_[i] = std::move(P);
     }
 }
@@ -234,6 +243,7 @@ Engine::~Engine() {
     for (float* p : allocs_) cudaFree(p);
     cudaFree(weights_);
     if (weights16_) cudaFree(weights16_);
+    for (unsigned long long* p : traces_) cudaFree(p);
     cudaFree(staging_);
     if (capture_) cudaStreamDestroy(capture_);
 }
@@ -393,6 +403,19 @@ std::string Engine::describe_json() const {
     os << "{\"precision\":\"" << to_string(prec_) << "\",\"max_batch\":" << max_batch_
        << ",\"launches_per_forward\":" << launches_per_forward() << ",\"plan\":" << describe_plan_json(g_, plan_) << "}";
     return os.str();
+}
+
+}  // namespace xlf
+
+namespace xlf {
+
+std::vector<unsigned long long> Engine::trace(int index) const {
+    if (index < 0 || index >= num_steps()) fail(ErrorKind::validation, "step index out of range");
+    const BParams* P = bparams_[size_t(index)].get();
+    if (!P || !P->trace) fail(ErrorKind::validation, "no trace for this step (bf16 steps with XLF_TRACE=1 only)");
+    std::vector<unsigned long long> out(size_t(kTraceCtas) * kTraceEvents);
+    cuda_check(cudaMemcpy(out.data(), P->trace, out.size() * 8, cudaMemcpyDeviceToHost), "trace D2H");
+    return out;
 }
 
 }  // namespace xlf

@@ -45,6 +45,8 @@ public:
     const DevicePlan& plan() const { return plan_; }
     int num_steps() const { return int(plan_.steps.size()); }
     int launches_per_forward() const;
+    // XLF_TRACE=1 only: per-CTA phase stamps of step `index` (bf16 kernels).
+    std::vector<unsigned long long> trace(int index) const;
     std::string describe_json() const;
     int max_batch() const { return max_batch_; }
 
@@ -64,6 +66,7 @@ private:
     size_t staging_floats_ = 0;
     std::vector<struct FusedParams> params_;
     std::vector<std::unique_ptr<struct BParams>> bparams_;  // bf16 steps
+    std::vector<unsigned long long*> traces_;                // XLF_TRACE buffers
     void* weights16_ = nullptr;  // bf16 MMA weights
     int esz_ = 4;                // bytes per activation element
     bool s2d_ = false;           // bf16: first conv rewritten on a space-to-depth input

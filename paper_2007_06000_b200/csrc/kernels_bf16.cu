@@ -38,6 +38,14 @@ struct BTile {
     int n, ty, tx, oy0, ox0, c0;
 };
 
+__device__ __forceinline__ void stamp(const BParams& P, int ev) {
+    if (P.trace && blockIdx.y == 0 && blockIdx.z == 0 && blockIdx.x < kTraceCtas && ev < kTraceEvents) {
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        P.trace[blockIdx.x * kTraceEvents + ev] = t;
+    }
+}
+
 __device__ __forceinline__ void named_sync_compute() { asm volatile("bar.sync 1, %0;\n" ::"n"(kCompute) : "memory"); }
 
 __device__ __forceinline__ const BRegion& src_region(const BParams& P, const BOp& op, int which) {
@@ -57,6 +65,7 @@ __device__ void producer(const BParams& P, uint8_t* smem, const BTile& t, uint64
                          uint64_t* ring_empty) {
     uint32_t bytes = 0;
     for (int k = 0; k < P.nins; ++k) bytes += uint32_t(P.in[k].r.c8) * uint32_t(P.in[k].r.ext_h * P.in[k].r.ext_w * 16);
+    stamp(P, kTrStart);
     mbar_expect_tx(bar_x, bytes);
     for (int k = 0; k < P.nins; ++k) {
         const BIn& in = P.in[k];
@@ -66,6 +75,7 @@ __device__ void producer(const BParams& P, uint8_t* smem, const BTile& t, uint64
             tma_load_4d(smem + in.r.smem_off + kb * in.r.plane_bytes, &P.xmap[k], in.coff + t.c0 + kb * in.r.kb_ch, x0, y0, t.n,
                         bar_x);
     }
+    stamp(P, kTrXIssued);
     int c = 0;
     for (int i = 0; i < P.nops; ++i) {
         const BOp& op = P.ops[i];
@@ -89,6 +99,7 @@ __device__ void producer(const BParams& P, uint8_t* smem, const BTile& t, uint64
 __device__ void issuer(const BParams& P, uint8_t* smem, uint32_t tmem, uint64_t* bar_x, uint64_t* ring_full,
                        uint64_t* ring_empty, uint64_t* acc_full, uint64_t* unit_done) {
     mbar_wait(bar_x, 0);
+    stamp(P, kTrXLanded);
     int c = 0, u = 0, waited = 0;
     const uint32_t sbase = smem_u32(smem);
     for (int i = 0; i < P.nops; ++i) {
@@ -373,6 +384,7 @@ __global__ void __launch_bounds__(kBThreads, 1) fused_bf16_kernel(const __grid_c
             for (int nbi = 0; nbi < nunits; ++nbi, ++u) {
                 if (op.kind == BOP_MMA) {
                     mbar_wait(&acc_full[u], 0);
+                    if (threadIdx.x == 0) stamp(P, kTrUnit + 2 * u);
                     fence_after();
                     epilogue_mma(P, op, nbi, smem, tmem, t);
                 } else {
@@ -383,7 +395,7 @@ __global__ void __launch_bounds__(kBThreads, 1) fused_bf16_kernel(const __grid_c
                 fence_async_smem();
                 fence_before();
                 named_sync_compute();
-                if (threadIdx.x == 0) mbar_arrive(&unit_done[u]);
+                if (threadIdx.x == 0) mbar_arrive(&unit_done[u]), stamp(P, kTrUnit + 2 * u + 1);
             }
         }
     }
@@ -391,6 +403,7 @@ __global__ void __launch_bounds__(kBThreads, 1) fused_bf16_kernel(const __grid_c
     __syncthreads();
     fence_after();
     if (warp == 9 && P.tmem_cols) tmem_free(tmem, P.tmem_cols);
+    if (threadIdx.x == 0) stamp(P, kTrEnd);
 }
 
 // ----------------------------------------------------------------- layout kernels (bf16)
