@@ -50,6 +50,17 @@ struct BOp {
     const float* bias;          // [npad] fp32 (zeros when the layer has no bias)
     __nv_bfloat16* out;
     int out_cstride, out_coff;
+    int tcol;       // MMA: first TMEM column of this op inside its group
+    int bias_smem;  // byte offset of the op's bias copy in shared memory (-1: none)
+};
+
+// A group is what one commit / one epilogue pass covers: consecutive MMA ops
+// of the same stage (disjoint TMEM columns, issued back to back), or one N
+// block of a wide MMA op, or one SIMT op.
+struct BGroup {
+    int op0, op1;  // ops [op0, op1)
+    int nbi;       // N block (multi-block MMA ops), else 0
+    int mma;       // 1: tensor-core group
 };
 
 // Layout of a shared region: K-blocks of kb_ch channels; inside a K-block
@@ -86,6 +97,9 @@ struct alignas(64) BParams {
     int nops, nbufs;
     BOp ops[kBMaxOps];
     BRegion bufs[kBMaxBufs];
+    int ngroups;
+    BGroup groups[kBMaxUnits];
+    int bias_off, bias_bytes;  // shared copy of every MMA op's bias
     int ring_off, chunk_bytes;
     int smem_bytes, tmem_cols;
     int ctile, cgroups;  // channel tiling of pool-only steps (0 = all channels)

@@ -263,6 +263,47 @@ long long layout_bf16(const Graph& g, const StepSpec& s, int th, int tw, BParams
             o.cin = out.channels;
         }
     }
+    // Groups: consecutive same-stage single-block MMA ops share one commit and
+    // one epilogue pass (disjoint TMEM columns); wide ops get a group per N
+    // block; SIMT ops are their own group.
+    std::vector<BGroup> groups;
+    int gcols = 0;
+    tmem = 0;
+    for (int i = 0; i < nops; ++i) {
+        BOp& o = ops[size_t(i)];
+        if (o.kind != BOP_MMA) {
+            groups.push_back({i, i + 1, 0, 0});
+            continue;
+        }
+        const int cols = o.mtiles * o.nb;
+        if (o.nblocks > 1) {
+            for (int k = 0; k < o.nblocks; ++k) groups.push_back({i, i + 1, k, 1});
+            o.tcol = 0;
+            tmem = std::max(tmem, cols);
+            continue;
+        }
+        const bool join = !groups.empty() && groups.back().mma && groups.back().op1 == i &&
+                          ops[size_t(groups.back().op0)].stage == o.stage && ops[size_t(groups.back().op0)].nblocks == 1 &&
+                          gcols + cols <= 512;
+        if (join) {
+            o.tcol = gcols;
+            gcols += cols;
+            groups.back().op1 = i + 1;
+        } else {
+            o.tcol = 0;
+            gcols = cols;
+            groups.push_back({i, i + 1, 0, 1});
+        }
+        tmem = std::max(tmem, gcols);
+    }
+    if (groups.size() > size_t(kBMaxUnits)) return -1;
+    // shared copy of the biases the epilogues read
+    const long long bias_off = bytes;
+    for (BOp& o : ops) {
+        o.bias_smem = -1;
+        if (o.kind == BOP_MMA) o.bias_smem = int(bytes), bytes += (long long)o.npad * 4;
+    }
+    const long long bias_bytes = bytes - bias_off;
     bytes = (bytes + 1023) & ~1023LL;
     const long long ring_off = bytes;
     if (any_mma) bytes += (long long)kRingSlots * kChunkBytes;
@@ -276,6 +317,9 @@ long long layout_bf16(const Graph& g, const StepSpec& s, int th, int tw, BParams
         P->nops = nops, P->nbufs = nbufs;
         for (int i = 0; i < nops; ++i) P->ops[i] = ops[size_t(i)];
         for (int i = 0; i < nbufs; ++i) P->bufs[i] = bufs[size_t(i)];
+        P->ngroups = int(groups.size());
+        for (size_t i = 0; i < groups.size(); ++i) P->groups[i] = groups[i];
+        P->bias_off = int(bias_off), P->bias_bytes = int(bias_bytes);
         P->ring_off = int(ring_off), P->chunk_bytes = kChunkBytes;
         P->smem_bytes = int(bytes);
         P->ctile = s.ctile;

@@ -52,13 +52,6 @@ __device__ __forceinline__ const BRegion& src_region(const BParams& P, const BOp
     return op.stage == 1 ? P.in[op.xin].r : P.bufs[which];
 }
 
-// Unit enumeration: (op index, N block) in op order.
-__device__ __forceinline__ int unit_count(const BParams& P) {
-    int u = 0;
-    for (int i = 0; i < P.nops; ++i) u += P.ops[i].kind == BOP_MMA ? P.ops[i].nblocks : 1;
-    return u;
-}
-
 // ------------------------------------------------------------------ producer
 
 __device__ void producer(const BParams& P, uint8_t* smem, const BTile& t, uint64_t* bar_x, uint64_t* ring_full,
@@ -76,12 +69,14 @@ __device__ void producer(const BParams& P, uint8_t* smem, const BTile& t, uint64
                         bar_x);
     }
     stamp(P, kTrXIssued);
+    // weights, in exactly the order the issuer consumes them
     int c = 0;
-    for (int i = 0; i < P.nops; ++i) {
-        const BOp& op = P.ops[i];
-        if (op.kind != BOP_MMA) continue;
-        for (int nbi = 0; nbi < op.nblocks; ++nbi) {
-            const __nv_bfloat16* wb = op.wmma + size_t(nbi) * op.ksteps * op.nb * 16;
+    for (int gi = 0; gi < P.ngroups; ++gi) {
+        const BGroup& G = P.groups[gi];
+        if (!G.mma) continue;
+        for (int i = G.op0; i < G.op1; ++i) {
+            const BOp& op = P.ops[i];
+            const __nv_bfloat16* wb = op.wmma + size_t(G.nbi) * op.ksteps * op.nb * 16;
             for (int s0 = 0; s0 < op.ksteps; s0 += op.chunk_steps, ++c) {
                 const int steps = min(op.chunk_steps, op.ksteps - s0);
                 const int slot = c % kRingSlots;
@@ -96,58 +91,66 @@ __device__ void producer(const BParams& P, uint8_t* smem, const BTile& t, uint64
 
 // ------------------------------------------------------------------ MMA issuer
 
+// All MMAs of one op (one N block): K steps in tap-major order (s = tap*c16
+// + kc, the packing order of the weights), every M tile per step.  Descriptors
+// are built once and advanced by adding (byte offset >> 4) to the start field.
+__device__ __forceinline__ void issue_op(const BParams& P, const BOp& op, uint32_t sbase, uint32_t tmem, int& c, uint64_t* ring_full,
+                                         uint64_t* ring_empty) {
+    const BRegion& R = src_region(P, op, op.src);
+    const uint32_t src = sbase + R.smem_off;
+    const int c16 = op.cin_pad / 16;
+    const uint32_t idesc = idesc_bf16(128, op.nb);
+    uint32_t lbo, layout;
+    if (R.mode == kPlanes) lbo = R.plane_bytes, layout = kNoSwizzle;
+    else lbo = 16, layout = R.mode == kSw32 ? kSW32 : kSW128;
+    const uint32_t sbo = op.contig ? 8 * R.row_bytes : R.ext_w * R.row_bytes;
+    const uint64_t adesc0 = sdesc(0, lbo, sbo, layout);
+    const uint64_t bdesc0 = sdesc(0, op.nb * 16, 128, kNoSwizzle);
+    const uint32_t tm = tmem + op.tcol;
+    int kc = 0, dy = 0, dx = 0;
+    for (int s0 = 0; s0 < op.ksteps; s0 += op.chunk_steps, ++c) {
+        const int steps = min(op.chunk_steps, op.ksteps - s0);
+        const int slot = c % kRingSlots;
+        mbar_wait(&ring_full[slot], (c / kRingSlots) & 1);
+        fence_after();
+        const uint32_t wslot = sbase + P.ring_off + slot * P.chunk_bytes;
+        for (int sl = 0; sl < steps; ++sl) {
+            const int s = s0 + sl;
+            const uint64_t bd = bdesc0 + ((wslot + sl * op.nb * 32) >> 4);
+            uint32_t kofs;
+            if (R.mode == kPlanes) kofs = kc * 2 * R.plane_bytes;
+            else if (R.mode == kSw32) kofs = kc * R.plane_bytes;
+            else kofs = (kc >> 2) * R.plane_bytes + (kc & 3) * 32;
+            const uint32_t tap_cells = op.contig ? 0u : uint32_t((dy + op.d) * R.ext_w + dx + op.d);
+            const uint32_t step_addr = src + kofs + tap_cells * R.row_bytes;
+            int mt = 0;
+            for (int rb = 0; mt < op.mtiles; ++rb)
+                for (int st = 0; st < op.strips && mt < op.mtiles; ++st, ++mt) {
+                    const uint32_t cell = op.contig ? uint32_t(mt * 128) : uint32_t(rb * 16 * R.ext_w + st * 8);
+                    mma_bf16(tm + mt * op.nb, adesc0 + ((step_addr + cell * R.row_bytes) >> 4), bd, idesc, s > 0 ? 1u : 0u);
+                }
+            if (++kc == c16) {
+                kc = 0;
+                if (++dx == op.kw) dx = 0, ++dy;
+            }
+        }
+        commit(&ring_empty[slot]);
+    }
+}
+
 __device__ void issuer(const BParams& P, uint8_t* smem, uint32_t tmem, uint64_t* bar_x, uint64_t* ring_full,
                        uint64_t* ring_empty, uint64_t* acc_full, uint64_t* unit_done) {
     mbar_wait(bar_x, 0);
     stamp(P, kTrXLanded);
-    int c = 0, u = 0, waited = 0;
+    int c = 0;
     const uint32_t sbase = smem_u32(smem);
-    for (int i = 0; i < P.nops; ++i) {
-        const BOp& op = P.ops[i];
-        const int nunits = op.kind == BOP_MMA ? op.nblocks : 1;
-        for (int nbi = 0; nbi < nunits; ++nbi, ++u) {
-            for (; waited < u; ++waited) mbar_wait(&unit_done[waited], 0);
-            if (op.kind != BOP_MMA) continue;
-            fence_after();
-            const BRegion& R = src_region(P, op, op.src);
-            const uint32_t src = sbase + R.smem_off;
-            const int c16 = op.cin_pad / 16;
-            const uint32_t idesc = idesc_bf16(128, op.nb);
-            for (int s0 = 0; s0 < op.ksteps; s0 += op.chunk_steps, ++c) {
-                const int steps = min(op.chunk_steps, op.ksteps - s0);
-                const int slot = c % kRingSlots;
-                mbar_wait(&ring_full[slot], (c / kRingSlots) & 1);
-                fence_after();
-                const uint32_t wslot = sbase + P.ring_off + slot * P.chunk_bytes;
-                for (int sl = 0; sl < steps; ++sl) {
-                    const int s = s0 + sl;
-                    const int tap = s / c16, kc = s - tap * c16;
-                    const int dy = tap / op.kw, dx = tap - dy * op.kw;
-                    const uint64_t bd = sdesc(wslot + sl * op.nb * 32, op.nb * 16, 128, kNoSwizzle);
-                    // K16 step kc inside the source region's K-blocks
-                    uint32_t kofs, lbo, layout;
-                    if (R.mode == kPlanes) kofs = kc * 2 * R.plane_bytes, lbo = R.plane_bytes, layout = kNoSwizzle;
-                    else if (R.mode == kSw32) kofs = kc * R.plane_bytes, lbo = 16, layout = kSW32;
-                    else kofs = (kc >> 2) * R.plane_bytes + (kc & 3) * 32, lbo = 16, layout = kSW128;
-                    for (int mt = 0; mt < op.mtiles; ++mt) {
-                        int cell;
-                        uint32_t sbo;
-                        if (op.contig) {
-                            cell = mt * 128;
-                            sbo = 8 * R.row_bytes;
-                        } else {
-                            const int st = mt % op.strips, rb = mt / op.strips;
-                            cell = (rb * 16 + dy + op.d) * R.ext_w + st * 8 + dx + op.d;
-                            sbo = R.ext_w * R.row_bytes;
-                        }
-                        const uint32_t a = src + kofs + cell * R.row_bytes;
-                        mma_bf16(tmem + mt * op.nb, sdesc(a, lbo, sbo, layout), bd, idesc, s > 0 ? 1u : 0u);
-                    }
-                }
-                commit(&ring_empty[slot]);
-            }
-            commit(&acc_full[u]);
-        }
+    for (int gi = 0; gi < P.ngroups; ++gi) {
+        if (gi > 0) mbar_wait(&unit_done[gi - 1], 0);  // earlier groups' epilogues done (in order)
+        const BGroup& G = P.groups[gi];
+        if (!G.mma) continue;
+        fence_after();
+        for (int i = G.op0; i < G.op1; ++i) issue_op(P, P.ops[i], sbase, tmem, c, ring_full, ring_empty);
+        commit(&acc_full[gi]);
     }
 }
 
@@ -206,12 +209,12 @@ __device__ __forceinline__ void put8(const CellDst& d, int ch, const float* v8) 
 
 // Bias + ReLU + store of N accumulator columns (channels ch0 ...), unrolled.
 template <int N>
-__device__ __forceinline__ void finish_cols(const BOp& op, const CellDst& d, int ch0, int c8end, float* v) {
+__device__ __forceinline__ void finish_cols(const BOp& op, const float* bias, const CellDst& d, int ch0, int c8end, float* v) {
 #pragma unroll
     for (int j = 0; j < N; j += 8) {
         if (ch0 + j >= c8end) break;
-        const float4 b0 = __ldg(reinterpret_cast<const float4*>(op.bias + ch0 + j));
-        const float4 b1 = __ldg(reinterpret_cast<const float4*>(op.bias + ch0 + j + 4));
+        const float4 b0 = *reinterpret_cast<const float4*>(bias + ch0 + j);
+        const float4 b1 = *reinterpret_cast<const float4*>(bias + ch0 + j + 4);
         float* x = v + j;
         x[0] += b0.x, x[1] += b0.y, x[2] += b0.z, x[3] += b0.w, x[4] += b1.x, x[5] += b1.y, x[6] += b1.z, x[7] += b1.w;
         if (op.relu)
@@ -228,6 +231,7 @@ __device__ void epilogue_mma(const BParams& P, const BOp& op, int nbi, uint8_t* 
     const int row = threadIdx.x & 127, half = threadIdx.x >> 7;
     const uint32_t lane_base = uint32_t(row & ~31) << 16;
     const int c8end = (op.cout + 7) & ~7;  // never write past the tensor's padded channels
+    const float* bias = reinterpret_cast<const float*>(smem + op.bias_smem);
     for (int mt = 0; mt < op.mtiles; ++mt) {
         int r, c;
         bool valid;
@@ -242,16 +246,16 @@ __device__ void epilogue_mma(const BParams& P, const BOp& op, int nbi, uint8_t* 
         }
         const CellDst d = cell_dst(P, op, smem, t, r, c, valid);
         for (int col = half * 32; col < op.nb; col += 64) {
-            const uint32_t ta = tmem + lane_base + mt * op.nb + col;
+            const uint32_t ta = tmem + op.tcol + lane_base + mt * op.nb + col;
             const int ch0 = nbi * op.nb + col;
             if (op.nb - col >= 32) {
                 float v[32];
                 tmem_ld32(ta, v);
-                if (valid) finish_cols<32>(op, d, ch0, c8end, v);
+                if (valid) finish_cols<32>(op, bias, d, ch0, c8end, v);
             } else {
                 float v[16];
                 tmem_ld16(ta, v);
-                if (valid) finish_cols<16>(op, d, ch0, c8end, v);
+                if (valid) finish_cols<16>(op, bias, d, ch0, c8end, v);
             }
         }
     }
@@ -357,7 +361,7 @@ __global__ void __launch_bounds__(kBThreads, 1) fused_bf16_kernel(const __grid_c
     t.oy0 = t.ty * P.tile_h;
     t.ox0 = t.tx * P.tile_w;
     t.c0 = blockIdx.z * P.ctile;
-    const int units = unit_count(P);
+    const int units = P.ngroups;
     if (threadIdx.x == 0) {
         mbar_init(&bar_x, 1);
         for (int i = 0; i < kRingSlots; ++i) mbar_init(&ring_full[i], 1), mbar_init(&ring_empty[i], 1);
@@ -376,27 +380,32 @@ __global__ void __launch_bounds__(kBThreads, 1) fused_bf16_kernel(const __grid_c
         if (lane == 0) issuer(P, smem, tmem, &bar_x, ring_full, ring_empty, acc_full, unit_done);
         __syncwarp();
     } else {
-        bool have_x = false;
-        int u = 0;
+        // biases of the MMA ops -> shared memory (read by every epilogue)
         for (int i = 0; i < P.nops; ++i) {
             const BOp& op = P.ops[i];
-            const int nunits = op.kind == BOP_MMA ? op.nblocks : 1;
-            for (int nbi = 0; nbi < nunits; ++nbi, ++u) {
-                if (op.kind == BOP_MMA) {
-                    mbar_wait(&acc_full[u], 0);
-                    if (threadIdx.x == 0) stamp(P, kTrUnit + 2 * u);
-                    fence_after();
-                    epilogue_mma(P, op, nbi, smem, tmem, t);
-                } else {
-                    if (!have_x) mbar_wait(&bar_x, 0), have_x = true;
-                    if (op.kind == BOP_SIMT_CONV) simt_conv(P, op, smem, t);
-                    else simt_pool_add(P, op, smem, t);
-                }
-                fence_async_smem();
-                fence_before();
-                named_sync_compute();
-                if (threadIdx.x == 0) mbar_arrive(&unit_done[u]), stamp(P, kTrUnit + 2 * u + 1);
+            if (op.bias_smem < 0) continue;
+            float* dst = reinterpret_cast<float*>(smem + op.bias_smem);
+            for (int k = threadIdx.x; k < op.npad; k += kCompute) dst[k] = __ldg(op.bias + k);
+        }
+        named_sync_compute();
+        bool have_x = false;
+        for (int gi = 0; gi < P.ngroups; ++gi) {
+            const BGroup& G = P.groups[gi];
+            if (G.mma) {
+                mbar_wait(&acc_full[gi], 0);
+                if (threadIdx.x == 0) stamp(P, kTrUnit + 2 * gi);
+                fence_after();
+                for (int i = G.op0; i < G.op1; ++i) epilogue_mma(P, P.ops[i], G.nbi, smem, tmem, t);
+            } else {
+                const BOp& op = P.ops[G.op0];
+                if (!have_x) mbar_wait(&bar_x, 0), have_x = true;
+                if (op.kind == BOP_SIMT_CONV) simt_conv(P, op, smem, t);
+                else simt_pool_add(P, op, smem, t);
             }
+            fence_async_smem();
+            fence_before();
+            named_sync_compute();
+            if (threadIdx.x == 0) mbar_arrive(&unit_done[gi]), stamp(P, kTrUnit + 2 * gi + 1);
         }
     }
     fence_before();
