@@ -442,7 +442,7 @@ DevicePlan plan_device(const Graph& g, Partition part, int batch_hint, int smem_
     plan.bf16 = bf16;
     const int cpad = bf16 ? 8 : 4;  // channel padding of HBM tensors (16 bytes)
     auto tile = [&](StepSpec& st) {
-        return bf16 ? choose_tile_bf16(g, st, batch_hint, smem_budget - 1024) : choose_tile(g, st, batch_hint, smem_budget);
+        return bf16 ? choose_tile_bf16(g, st, batch_hint, smem_budget - 4096) : choose_tile(g, st, batch_hint, smem_budget);
     };
     if (part == Partition::reference) plan.blocks = detect_fusion_blocks(g);
     else if (part == Partition::b200) plan.blocks = detect_fusion_blocks_b200(g);

@@ -54,8 +54,8 @@ __device__ __forceinline__ const BRegion& src_region(const BParams& P, const BOp
 
 // ------------------------------------------------------------------ producer
 
-__device__ void producer(const BParams& P, uint8_t* smem, const BTile& t, uint64_t* bar_x, uint64_t* ring_full,
-                         uint64_t* ring_empty) {
+__device__ void producer(const BParams& P, const CUtensorMap* xmaps, uint8_t* smem, const BTile& t, uint64_t* bar_x,
+                         uint64_t* ring_full, uint64_t* ring_empty) {
     uint32_t bytes = 0;
     for (int k = 0; k < P.nins; ++k) bytes += uint32_t(P.in[k].r.c8) * uint32_t(P.in[k].r.ext_h * P.in[k].r.ext_w * 16);
     stamp(P, kTrStart);
@@ -65,7 +65,7 @@ __device__ void producer(const BParams& P, uint8_t* smem, const BTile& t, uint64
         const int x0 = t.ox0 * in.org_mul - in.org_sub, y0 = t.oy0 * in.org_mul - in.org_sub;
         const int nkb = in.r.c8 * 8 / in.r.kb_ch;
         for (int kb = 0; kb < nkb; ++kb)
-            tma_load_4d(smem + in.r.smem_off + kb * in.r.plane_bytes, &P.xmap[k], in.coff + t.c0 + kb * in.r.kb_ch, x0, y0, t.n,
+            tma_load_4d(smem + in.r.smem_off + kb * in.r.plane_bytes, &xmaps[k], in.coff + t.c0 + kb * in.r.kb_ch, x0, y0, t.n,
                         bar_x);
     }
     stamp(P, kTrXIssued);
@@ -112,6 +112,7 @@ __device__ __forceinline__ void issue_op(const BParams& P, const BOp& op, uint32
         const int steps = min(op.chunk_steps, op.ksteps - s0);
         const int slot = c % kRingSlots;
         mbar_wait(&ring_full[slot], (c / kRingSlots) & 1);
+        if (c == 0) stamp(P, 28);  // first weight chunk landed
         fence_after();
         const uint32_t wslot = sbase + P.ring_off + slot * P.chunk_bytes;
         for (int sl = 0; sl < steps; ++sl) {
@@ -127,14 +128,19 @@ __device__ __forceinline__ void issue_op(const BParams& P, const BOp& op, uint32
             for (int rb = 0; mt < op.mtiles; ++rb)
                 for (int st = 0; st < op.strips && mt < op.mtiles; ++st, ++mt) {
                     const uint32_t cell = op.contig ? uint32_t(mt * 128) : uint32_t(rb * 16 * R.ext_w + st * 8);
-                    mma_bf16(tm + mt * op.nb, adesc0 + ((step_addr + cell * R.row_bytes) >> 4), bd, idesc, s > 0 ? 1u : 0u);
+                    if (elect_one())
+                        mma_bf16(tm + mt * op.nb, adesc0 + ((step_addr + cell * R.row_bytes) >> 4), bd, idesc, s > 0 ? 1u : 0u);
+                    __syncwarp();
+                    if (c == 0 && s == 0 && mt == 0) stamp(P, 26);
+                    if (c == 0 && s == 1 && mt == 0) stamp(P, 27);
                 }
             if (++kc == c16) {
                 kc = 0;
                 if (++dx == op.kw) dx = 0, ++dy;
             }
         }
-        commit(&ring_empty[slot]);
+        if (elect_one()) commit(&ring_empty[slot]);
+        __syncwarp();
     }
 }
 
@@ -149,8 +155,11 @@ __device__ void issuer(const BParams& P, uint8_t* smem, uint32_t tmem, uint64_t*
         const BGroup& G = P.groups[gi];
         if (!G.mma) continue;
         fence_after();
+        if (gi < 2) stamp(P, 29 + 2 * gi);  // group's inputs ready, issue starts
         for (int i = G.op0; i < G.op1; ++i) issue_op(P, P.ops[i], sbase, tmem, c, ring_full, ring_empty);
-        commit(&acc_full[gi]);
+        if (gi < 2) stamp(P, 30 + 2 * gi);  // group issued
+        if (elect_one()) commit(&acc_full[gi]);
+        __syncwarp();
     }
 }
 
@@ -348,12 +357,25 @@ __device__ void simt_conv(const BParams& P, const BOp& op, uint8_t* smem, const 
     }
 }
 
-__global__ void __launch_bounds__(kBThreads, 1) fused_bf16_kernel(const __grid_constant__ BParams P) {
+__global__ void __launch_bounds__(kBThreads, 1) fused_bf16_kernel(const __grid_constant__ BParams Pg) {
     extern __shared__ __align__(1024) uint8_t smem[];
     __shared__ __align__(8) uint64_t bar_x, ring_full[kRingSlots], ring_empty[kRingSlots], acc_full[kBMaxUnits],
         unit_done[kBMaxUnits];
     __shared__ uint32_t tmem_slot;
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    // The descriptor lives in the kernel-parameter constant bank; the op loops
+    // index it with run-time op numbers, and indexed constant loads that miss
+    // the small constant cache stall the single MMA-issuing thread for hundreds
+    // of cycles per instruction.  Work from a shared-memory copy instead (the
+    // tensor maps stay in parameter space, where TMA must read them).
+    __shared__ __align__(64) BParams Ps;
+    {
+        const uint4* src = reinterpret_cast<const uint4*>(&Pg);
+        uint4* dst = reinterpret_cast<uint4*>(&Ps);
+        for (int i = threadIdx.x; i < int(sizeof(BParams) / 16); i += blockDim.x) dst[i] = src[i];
+        __syncthreads();
+    }
+    const BParams& P = Ps;
+    const int warp = __shfl_sync(0xffffffffu, int(threadIdx.x >> 5), 0), lane = threadIdx.x & 31;  // provably warp-uniform
     BTile t;
     t.n = blockIdx.y;
     t.ty = blockIdx.x / P.grid_w;
@@ -375,9 +397,12 @@ __global__ void __launch_bounds__(kBThreads, 1) fused_bf16_kernel(const __grid_c
     const uint32_t tmem = P.tmem_cols ? tmem_slot : 0;
 
     if (warp == 8) {
-        if (lane == 0) producer(P, smem, t, &bar_x, ring_full, ring_empty);
+        if (lane == 0) producer(P, Pg.xmap, smem, t, &bar_x, ring_full, ring_empty);
     } else if (warp == 9) {
-        if (lane == 0) issuer(P, smem, tmem, &bar_x, ring_full, ring_empty, acc_full, unit_done);
+        // Whole warp, warp-uniform control flow, one elected lane issues; the
+        // op fields come from the parameter bank with uniform indices, so the
+        // descriptor arithmetic stays on the uniform datapath (no R2UR per MMA).
+        issuer(Pg, smem, tmem, &bar_x, ring_full, ring_empty, acc_full, unit_done);
         __syncwarp();
     } else {
         // biases of the MMA ops -> shared memory (read by every epilogue)
@@ -392,7 +417,7 @@ __global__ void __launch_bounds__(kBThreads, 1) fused_bf16_kernel(const __grid_c
         for (int gi = 0; gi < P.ngroups; ++gi) {
             const BGroup& G = P.groups[gi];
             if (G.mma) {
-                mbar_wait(&acc_full[gi], 0);
+                mbar_sleep_wait(&acc_full[gi], 0);
                 if (threadIdx.x == 0) stamp(P, kTrUnit + 2 * gi);
                 fence_after();
                 for (int i = G.op0; i < G.op1; ++i) epilogue_mma(P, P.ops[i], G.nbi, smem, tmem, t);
@@ -523,7 +548,8 @@ int grid_b(long long work) {
 }  // namespace
 
 cudaError_t init_fused_bf16() {
-    return cudaFuncSetAttribute(fused_bf16_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024 - 1024);
+    // 227 KB per block minus the static part (barriers + the BParams copy)
+    return cudaFuncSetAttribute(fused_bf16_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024 - 4096);
 }
 
 cudaError_t launch_fused_bf16(const BParams& P, int batch, cudaStream_t st) {

@@ -98,6 +98,17 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, float* v) {
     for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
 }
 
+// One lane of the (converged) warp returns true.
+__device__ __forceinline__ bool elect_one() {
+    uint32_t pred = 0;
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "elect.sync _|p, 0xffffffff;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}\n"
+        : "=r"(pred));
+    return pred != 0;
+}
+
 // ------------------------------------------------------------------ mbarrier
 
 __device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
@@ -119,6 +130,19 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
         "mbarrier.try_wait.parity.shared::cta.b64 done, [%0], %1;\n\t"
         "@!done bra WAIT_%=;\n\t}\n" ::"r"(smem_u32(bar)),
         "r"(parity)
+        : "memory");
+}
+
+// Same, but the thread asks to be suspended (up to `ns`) rather than re-polled:
+// for waiters with nothing else to do (the epilogue warps), so they do not
+// compete with the producer / MMA warps for issue slots and barrier traffic.
+__device__ __forceinline__ void mbar_sleep_wait(uint64_t* bar, uint32_t parity, uint32_t ns = 1000000) {
+    asm volatile(
+        "{\n\t.reg .pred done;\n"
+        "SWAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 done, [%0], %1, %2;\n\t"
+        "@!done bra SWAIT_%=;\n\t}\n" ::"r"(smem_u32(bar)),
+        "r"(parity), "r"(ns)
         : "memory");
 }
 
