@@ -92,51 +92,58 @@ __device__ void producer(const BParams& P, const CUtensorMap* xmaps, uint8_t* sm
 // ------------------------------------------------------------------ MMA issuer
 
 // All MMAs of one op (one N block): K steps in tap-major order (s = tap*c16
-// + kc, the packing order of the weights), every M tile per step.  Descriptors
-// are built once and advanced by adding (byte offset >> 4) to the start field.
+// + kc, the packing order of the weights), every M tile per step.  Every op
+// field is hoisted into locals first and the descriptors are advanced by
+// precomputed deltas (in 16-byte units of the start-address field), so one MMA
+// costs a handful of uniform-datapath instructions.
 __device__ __forceinline__ void issue_op(const BParams& P, const BOp& op, uint32_t sbase, uint32_t tmem, int& c, uint64_t* ring_full,
                                          uint64_t* ring_empty) {
     const BRegion& R = src_region(P, op, op.src);
-    const uint32_t src = sbase + R.smem_off;
-    const int c16 = op.cin_pad / 16;
-    const uint32_t idesc = idesc_bf16(128, op.nb);
+    const int mode = R.mode, plane = R.plane_bytes, rowb = R.row_bytes, ew = R.ext_w;
+    const int ksteps = op.ksteps, csteps = op.chunk_steps, nb = op.nb, mtiles = op.mtiles, strips = op.strips;
+    const int kw = op.kw, d = op.d, contig = op.contig, c16 = op.cin_pad / 16;
+    const uint32_t idesc = idesc_bf16(128, nb);
     uint32_t lbo, layout;
-    if (R.mode == kPlanes) lbo = R.plane_bytes, layout = kNoSwizzle;
-    else lbo = 16, layout = R.mode == kSw32 ? kSW32 : kSW128;
-    const uint32_t sbo = op.contig ? 8 * R.row_bytes : R.ext_w * R.row_bytes;
-    const uint64_t adesc0 = sdesc(0, lbo, sbo, layout);
-    const uint64_t bdesc0 = sdesc(0, op.nb * 16, 128, kNoSwizzle);
-    const uint32_t tm = tmem + op.tcol;
-    int kc = 0, dy = 0, dx = 0;
-    for (int s0 = 0; s0 < op.ksteps; s0 += op.chunk_steps, ++c) {
-        const int steps = min(op.chunk_steps, op.ksteps - s0);
+    if (mode == kPlanes) lbo = plane, layout = kNoSwizzle;
+    else lbo = 16, layout = mode == kSw32 ? kSW32 : kSW128;
+    const uint32_t sbo = contig ? 8 * rowb : ew * rowb;
+    const uint64_t bdesc0 = sdesc(0, nb * 16, 128, kNoSwizzle);
+    const uint32_t ring0 = sbase + P.ring_off, chunkb = P.chunk_bytes;
+    // start-field deltas (16-byte units)
+    const uint32_t d_mt = contig ? (128 * rowb) >> 4 : (8 * rowb) >> 4;       // next M tile / next strip
+    const uint32_t d_rb = ((16 * ew - 8 * (strips - 1)) * rowb) >> 4;          // last strip -> next 16-row block
+    const uint32_t d_dx = rowb >> 4, d_row = ((ew - kw) * rowb) >> 4;          // next tap column / next tap row
+    uint64_t a_tap = sdesc(sbase + R.smem_off + (contig ? 0 : (d * ew + d) * rowb), lbo, sbo, layout);
+    const uint32_t tm0 = tmem + op.tcol;
+    int kc = 0, dx = 0;
+    uint32_t acc = 0;
+    for (int s0 = 0; s0 < ksteps; s0 += csteps, ++c) {
+        const int steps = min(csteps, ksteps - s0);
         const int slot = c % kRingSlots;
         mbar_wait(&ring_full[slot], (c / kRingSlots) & 1);
-        if (c == 0) stamp(P, 28);  // first weight chunk landed
         fence_after();
-        const uint32_t wslot = sbase + P.ring_off + slot * P.chunk_bytes;
+        uint64_t bd = bdesc0 + ((ring0 + slot * chunkb) >> 4);
         for (int sl = 0; sl < steps; ++sl) {
-            const int s = s0 + sl;
-            const uint64_t bd = bdesc0 + ((wslot + sl * op.nb * 32) >> 4);
-            uint32_t kofs;
-            if (R.mode == kPlanes) kofs = kc * 2 * R.plane_bytes;
-            else if (R.mode == kSw32) kofs = kc * R.plane_bytes;
-            else kofs = (kc >> 2) * R.plane_bytes + (kc & 3) * 32;
-            const uint32_t tap_cells = op.contig ? 0u : uint32_t((dy + op.d) * R.ext_w + dx + op.d);
-            const uint32_t step_addr = src + kofs + tap_cells * R.row_bytes;
-            int mt = 0;
-            for (int rb = 0; mt < op.mtiles; ++rb)
-                for (int st = 0; st < op.strips && mt < op.mtiles; ++st, ++mt) {
-                    const uint32_t cell = op.contig ? uint32_t(mt * 128) : uint32_t(rb * 16 * R.ext_w + st * 8);
-                    if (elect_one())
-                        mma_bf16(tm + mt * op.nb, adesc0 + ((step_addr + cell * R.row_bytes) >> 4), bd, idesc, s > 0 ? 1u : 0u);
-                    __syncwarp();
-                    if (c == 0 && s == 0 && mt == 0) stamp(P, 26);
-                    if (c == 0 && s == 1 && mt == 0) stamp(P, 27);
-                }
+            uint32_t kofs;  // K16 step kc inside the region's K-blocks, 16-byte units
+            if (mode == kPlanes) kofs = (kc * 2 * plane) >> 4;
+            else if (mode == kSw32) kofs = (kc * plane) >> 4;
+            else kofs = (((kc >> 2) * plane) >> 4) + (kc & 3) * 2;
+            uint64_t a = a_tap + kofs;
+            uint32_t tcur = tm0;
+            int st = 0;
+            for (int mt = 0; mt < mtiles; ++mt) {
+                if (elect_one()) mma_bf16(tcur, a, bd, idesc, acc);
+                __syncwarp();
+                tcur += nb;
+                if (contig || ++st < strips) a += d_mt;
+                else st = 0, a += d_rb;
+            }
+            acc = 1;
+            bd += (nb * 32) >> 4;
             if (++kc == c16) {
                 kc = 0;
-                if (++dx == op.kw) dx = 0, ++dy;
+                a_tap += d_dx;
+                if (++dx == kw) dx = 0, a_tap += d_row;
             }
         }
         if (elect_one()) commit(&ring_empty[slot]);
