@@ -188,6 +188,8 @@ struct CellDst {
     uint8_t* sbuf;        // plane-0 address of the cell in the shared buffer, or null
     int plane_bytes;
     __nv_bfloat16* gdst;  // channel-0 address of the pixel (concat offset applied), or null
+    uint8_t* ost;         // staging row of the cell (K-block 0), or null
+    int ost_xor;          // swizzle of that row (16-byte chunk index XOR)
 };
 
 __device__ __forceinline__ CellDst cell_dst(const BParams& P, const BOp& op, uint8_t* smem, const BTile& t, int r, int c, bool valid) {
@@ -195,14 +197,26 @@ __device__ __forceinline__ CellDst cell_dst(const BParams& P, const BOp& op, uin
     const int gy = t.oy0 * op.org_mul - op.org_sub + r, gx = t.ox0 * op.org_mul - op.org_sub + c;
     d.valid = valid;
     d.inside = gy >= 0 && gy < op.H && gx >= 0 && gx < op.W;
-    d.sbuf = nullptr, d.gdst = nullptr, d.plane_bytes = 0;
+    d.sbuf = nullptr, d.gdst = nullptr, d.ost = nullptr, d.plane_bytes = 0, d.ost_xor = 0;
     if (op.buf >= 0) {
         const BRegion& B = P.bufs[op.buf];
         d.sbuf = smem + B.smem_off + (r * B.ext_w + c) * 16;
         d.plane_bytes = B.plane_bytes;
     }
-    if (op.emit && valid && d.inside && owns(P, op, t, gy, gx))
-        d.gdst = op.out + ((size_t(t.n) * op.H + gy) * op.W + gx) * op.out_cstride + op.out_coff + t.c0;
+    if (op.emit && valid) {
+        const int ty = gy - t.oy0, tx = gx - t.ox0;
+        if (op.ostage) {
+            // any cell of the tile box (the TMA store clips what lies outside the image)
+            if (ty >= 0 && ty < P.tile_h && tx >= 0 && tx < P.tile_w) {
+                const int cell = ty * P.tile_w + tx;
+                d.ost = smem + op.ost_off + cell * op.ost_rowb;
+                const uint32_t a = smem_u32(d.ost);
+                d.ost_xor = op.ost_kb_ch == 64 ? int((a >> 7) & 7u) : int((a >> 7) & 1u);
+            }
+        } else if (d.inside && owns(P, op, t, gy, gx)) {
+            d.gdst = op.out + ((size_t(t.n) * op.H + gy) * op.W + gx) * op.out_cstride + op.out_coff + t.c0;
+        }
+    }
     return d;
 }
 
@@ -217,15 +231,20 @@ __device__ __forceinline__ uint4 pack8(const float* v) {
 }
 
 // Stores 8 channels [ch, ch+8) of one cell (values already final).
-__device__ __forceinline__ void put8(const CellDst& d, int ch, const float* v8) {
+__device__ __forceinline__ void put8(const CellDst& d, int ch, const float* v8, const BOp& op, int chbase = 0) {
     const uint4 u = pack8(v8);
     if (d.sbuf) *reinterpret_cast<uint4*>(d.sbuf + (ch >> 3) * d.plane_bytes) = d.inside ? u : make_uint4(0, 0, 0, 0);
     if (d.gdst) *reinterpret_cast<uint4*>(d.gdst + ch) = u;
+    if (d.ost) {
+        const int rel = ch - chbase, kb = rel / op.ost_kb_ch, j = (rel - kb * op.ost_kb_ch) >> 3;
+        *reinterpret_cast<uint4*>(d.ost + kb * op.ost_kb_bytes + ((j ^ d.ost_xor) << 4)) = u;
+    }
 }
 
 // Bias + ReLU + store of N accumulator columns (channels ch0 ...), unrolled.
 template <int N>
-__device__ __forceinline__ void finish_cols(const BOp& op, const float* bias, const CellDst& d, int ch0, int c8end, float* v) {
+__device__ __forceinline__ void finish_cols(const BOp& op, const float* bias, const CellDst& d, int ch0, int chbase, int c8end,
+                                            float* v) {
 #pragma unroll
     for (int j = 0; j < N; j += 8) {
         if (ch0 + j >= c8end) break;
@@ -236,7 +255,7 @@ __device__ __forceinline__ void finish_cols(const BOp& op, const float* bias, co
         if (op.relu)
 #pragma unroll
             for (int k = 0; k < 8; ++k) x[k] = fmaxf(x[k], 0.0f);
-        put8(d, ch0 + j, x);
+        put8(d, ch0 + j, x, op, chbase);
     }
 }
 
@@ -267,11 +286,11 @@ __device__ void epilogue_mma(const BParams& P, const BOp& op, int nbi, uint8_t* 
             if (op.nb - col >= 32) {
                 float v[32];
                 tmem_ld32(ta, v);
-                if (valid) finish_cols<32>(op, bias, d, ch0, c8end, v);
+                if (valid) finish_cols<32>(op, bias, d, ch0, nbi * op.nb, c8end, v);
             } else {
                 float v[16];
                 tmem_ld16(ta, v);
-                if (valid) finish_cols<16>(op, bias, d, ch0, c8end, v);
+                if (valid) finish_cols<16>(op, bias, d, ch0, nbi * op.nb, c8end, v);
             }
         }
     }
@@ -324,7 +343,7 @@ __device__ void simt_pool_add(const BParams& P, const BOp& op, uint8_t* smem, co
             if (op.kind == BOP_AVGPOOL)
                 for (int j = 0; j < 8; ++j) acc[j] *= inv;
         }
-        put8(cell_dst(P, op, smem, t, r, c, true), oct * 8, acc);
+        put8(cell_dst(P, op, smem, t, r, c, true), oct * 8, acc, op);
     }
 }
 
@@ -360,7 +379,7 @@ __device__ void simt_conv(const BParams& P, const BOp& op, uint8_t* smem, const 
             float x = oc < op.cout ? acc[j] + __ldg(op.bias + oc) : 0.0f;
             acc[j] = op.relu ? fmaxf(x, 0.0f) : x;
         }
-        put8(cell_dst(P, op, smem, t, r, c, true), oct * 8, acc);
+        put8(cell_dst(P, op, smem, t, r, c, true), oct * 8, acc, op);
     }
 }
 
@@ -437,7 +456,22 @@ __global__ void __launch_bounds__(kBThreads, 1) fused_bf16_kernel(const __grid_c
             fence_async_smem();
             fence_before();
             named_sync_compute();
-            if (threadIdx.x == 0) mbar_arrive(&unit_done[gi]), stamp(P, kTrUnit + 2 * gi + 1);
+            if (threadIdx.x == 0) {
+                if (G.mma) {  // TMA stores of the staged outputs of this group
+                    bool any = false;
+                    for (int i = G.op0; i < G.op1; ++i) {
+                        const BOp& op = P.ops[i];
+                        if (!op.ostage) continue;
+                        const int chans = op.nblocks > 1 ? op.nb : ((op.cout + 15) & ~15);
+                        for (int kb = 0; kb < chans / op.ost_kb_ch; ++kb)
+                            tma_store_4d(&Pg.omap[op.omap], smem + op.ost_off + kb * op.ost_kb_bytes,
+                                         op.out_coff + G.nbi * op.nb + kb * op.ost_kb_ch, t.ox0, t.oy0, t.n);
+                        any = true;
+                    }
+                    if (any) bulk_commit(), bulk_wait_read();  // staging reusable once read
+                }
+                mbar_arrive(&unit_done[gi]), stamp(P, kTrUnit + 2 * gi + 1);
+            }
         }
     }
     fence_before();
