@@ -52,12 +52,6 @@ struct BOp {
     int out_cstride, out_coff;
     int tcol;       // MMA: first TMEM column of this op inside its group
     int bias_smem;  // byte offset of the op's bias copy in shared memory (-1: none)
-    // TMA-store epilogue (emitted MMA ops): the tile's output is staged in
-    // shared memory as the swizzled box image [kb][th*tw cells][row] and written
-    // by cp.async.bulk.tensor stores (which also clip partial edge tiles).
-    int ostage;     // 1: staged + TMA store, 0: direct st.global
-    int omap;       // index into BParams::omap
-    int ost_off, ost_kb_ch, ost_rowb, ost_kb_bytes;
 };
 
 // A group is what one commit / one epilogue pass covers: consecutive MMA ops
@@ -95,11 +89,8 @@ struct BIn {
     const __nv_bfloat16* x;
 };
 
-constexpr int kMaxOuts = 4;
-
 struct alignas(64) BParams {
     CUtensorMap xmap[kMaxIns];   // block inputs: 4-D {cstride, W, H, N}, box = one K-block of the region
-    CUtensorMap omap[kMaxOuts];  // staged outputs: 4-D {cstride, W, H, N}, box = one K-block of the tile
     int nins;
     BIn in[kMaxIns];
     int tile_h, tile_w, grid_h, grid_w, out_h, out_w;

@@ -297,63 +297,6 @@ long long layout_bf16(const Graph& g, const StepSpec& s, int th, int tw, BParams
         tmem = std::max(tmem, gcols);
     }
     if (groups.size() > size_t(kBMaxUnits)) return -1;
-    // TMA-store staging of emitted MMA outputs.  A group's staging may alias
-    // the block-input region when no later group reads the input; otherwise it
-    // shares one dedicated area (groups run one after another, and each
-    // group's stores finish reading shared memory before the next starts).
-    int nomaps = 0;
-    long long own_stage = 0;  // bytes of the dedicated staging area
-    std::vector<long long> group_stage(groups.size(), 0);
-    for (BOp& o : ops) {
-        o.ostage = 0;
-        if (o.kind != BOP_MMA || !o.emit || o.own_only || o.cout % 16 || nomaps >= kMaxOuts) continue;
-        const int chans = o.nblocks > 1 ? o.nb : r16(o.cout);
-        o.ost_kb_ch = (chans % 64 == 0) ? 64 : 16;
-        o.ost_rowb = o.ost_kb_ch * 2;
-        o.ost_kb_bytes = (th * tw * o.ost_rowb + 1023) & ~1023;
-        o.ostage = 1;
-        o.omap = nomaps++;
-    }
-    for (size_t gi = 0; gi < groups.size(); ++gi) {
-        const BGroup& G = groups[gi];
-        if (!G.mma) continue;
-        for (int i = G.op0; i < G.op1; ++i) {
-            BOp& o = ops[size_t(i)];
-            if (!o.ostage) continue;
-            const int chans = o.nblocks > 1 ? o.nb : r16(o.cout);
-            o.ost_off = int(group_stage[gi]);  // relative to the group's staging base for now
-            group_stage[gi] += (long long)(chans / o.ost_kb_ch) * o.ost_kb_bytes;
-        }
-    }
-    auto reads_input = [&](const BGroup& G) {
-        for (int i = G.op0; i < G.op1; ++i)
-            if (ops[size_t(i)].stage == 1) return true;
-        return false;
-    };
-    std::vector<char> alias(groups.size(), 0);
-    for (size_t gi = 0; gi < groups.size(); ++gi) {
-        if (!group_stage[gi]) continue;
-        bool later = false;
-        for (size_t k = gi + 1; k < groups.size(); ++k) later |= reads_input(groups[k]);
-        const long long xbytes = ins.size() == 1 ? (long long)(ins[0].r.c8 * 8 / ins[0].r.kb_ch) * ins[0].r.plane_bytes : 0;
-        alias[gi] = !later && group_stage[gi] <= xbytes;
-        if (!alias[gi]) own_stage = std::max(own_stage, group_stage[gi]);
-    }
-    long long own_off = 0;
-    if (own_stage) {
-        bytes = (bytes + 1023) & ~1023LL;
-        own_off = bytes;
-        bytes += own_stage;
-    }
-    std::vector<char> placed(ops.size(), 0);
-    for (size_t gi = 0; gi < groups.size(); ++gi)
-        for (int i = groups[gi].op0; i < groups[gi].op1; ++i) {
-            BOp& o = ops[size_t(i)];
-            if (!groups[gi].mma || !o.ostage || placed[size_t(i)]) continue;
-            // a multi-block op's groups all agree (each holds only that op)
-            o.ost_off += int(alias[gi] ? ins[0].r.smem_off : own_off);
-            placed[size_t(i)] = 1;
-        }
     // shared copy of the biases the epilogues read
     const long long bias_off = bytes;
     for (BOp& o : ops) {

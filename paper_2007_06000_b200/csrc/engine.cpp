@@ -223,12 +223,6 @@ Engine::Engine(const Graph& g, int device, Partition part, Precision prec, const
                 const TensorSlot& t = plan_.tensors.at(os.layer);
                 o.out = reinterpret_cast<__nv_bfloat16*>(allocs_[size_t(t.alloc)]);
                 o.out_cstride = t.cstride, o.out_coff = t.coff;
-                if (o.ostage) {  // TMA-store map: box = one K-block of the output tile
-                    BRegion box{};
-                    box.kb_ch = o.ost_kb_ch, box.ext_w = P->tile_w, box.ext_h = P->tile_h;
-                    box.mode = o.ost_kb_ch == 64 ? kSw128 : kSw32;
-                    encode_region_map(&P->omap[o.omap], o.out, t.cstride, t.W, t.H, max_batch, box);
-                }
             }
         }
         if (std::getenv("XLF_TRACE")) {  // phase stamps of a few CTAs (profiling aid)

@@ -172,12 +172,42 @@ __device__ void issuer(const BParams& P, uint8_t* smem, uint32_t tmem, uint64_t*
 
 // ------------------------------------------------------------------ epilogue / SIMT
 
-__device__ __forceinline__ bool owns(const BParams& P, const BOp& op, const BTile& t, int gy, int gx) {
-    if (!op.own_only)  // emitted cells: exactly this tile (contiguous-M ops compute a halo'd region)
-        return gy >= t.oy0 && gy < t.oy0 + P.tile_h && gx >= t.ox0 && gx < t.ox0 + P.tile_w;
-    const int S = op.org_mul;
-    const int y1 = t.ty == P.grid_h - 1 ? op.H : min(op.H, (t.oy0 + P.tile_h) * S);
-    const int x1 = t.tx == P.grid_w - 1 ? op.W : min(op.W, (t.ox0 + P.tile_w) * S);
+// Register copy of everything an epilogue / SIMT op needs from the (shared)
+// descriptor.  Epilogues store to shared memory, so the compiler cannot cache
+// descriptor fields read from shared memory across those stores; hoisting
+// them once per op avoids a dependent shared load per field per channel.
+struct EpiOp {
+    int relu, c8end, emit, own_only;
+    int org_mul, org_sub, H, W, out_cstride, out_coff;
+    int tile_h, tile_w, grid_h, grid_w;
+    int buf_ew, buf_plane;
+    uint8_t* buf;           // shared buffer base (planes), or null
+    __nv_bfloat16* out;
+    const float* bias;
+};
+
+__device__ __forceinline__ EpiOp epi_op(const BParams& P, const BOp& op, uint8_t* smem) {
+    EpiOp e;
+    e.relu = op.relu, e.c8end = (op.cout + 7) & ~7, e.emit = op.emit, e.own_only = op.own_only;
+    e.org_mul = op.org_mul, e.org_sub = op.org_sub, e.H = op.H, e.W = op.W;
+    e.out_cstride = op.out_cstride, e.out_coff = op.out_coff;
+    e.tile_h = P.tile_h, e.tile_w = P.tile_w, e.grid_h = P.grid_h, e.grid_w = P.grid_w;
+    e.buf = nullptr, e.buf_ew = 0, e.buf_plane = 0;
+    if (op.buf >= 0) {
+        const BRegion& B = P.bufs[op.buf];
+        e.buf = smem + B.smem_off, e.buf_ew = B.ext_w, e.buf_plane = B.plane_bytes;
+    }
+    e.out = op.out;
+    e.bias = op.bias_smem >= 0 ? reinterpret_cast<const float*>(smem + op.bias_smem) : op.bias;
+    return e;
+}
+
+__device__ __forceinline__ bool owns(const EpiOp& e, const BTile& t, int gy, int gx) {
+    if (!e.own_only)  // emitted cells: exactly this tile (contiguous-M ops compute a halo'd region)
+        return gy >= t.oy0 && gy < t.oy0 + e.tile_h && gx >= t.ox0 && gx < t.ox0 + e.tile_w;
+    const int S = e.org_mul;
+    const int y1 = t.ty == e.grid_h - 1 ? e.H : min(e.H, (t.oy0 + e.tile_h) * S);
+    const int x1 = t.tx == e.grid_w - 1 ? e.W : min(e.W, (t.ox0 + e.tile_w) * S);
     return gy >= t.oy0 * S && gy < y1 && gx >= t.ox0 * S && gx < x1;
 }
 
@@ -186,37 +216,18 @@ __device__ __forceinline__ bool owns(const BParams& P, const BOp& op, const BTil
 struct CellDst {
     bool valid, inside;
     uint8_t* sbuf;        // plane-0 address of the cell in the shared buffer, or null
-    int plane_bytes;
     __nv_bfloat16* gdst;  // channel-0 address of the pixel (concat offset applied), or null
-    uint8_t* ost;         // staging row of the cell (K-block 0), or null
-    int ost_xor;          // swizzle of that row (16-byte chunk index XOR)
 };
 
-__device__ __forceinline__ CellDst cell_dst(const BParams& P, const BOp& op, uint8_t* smem, const BTile& t, int r, int c, bool valid) {
+__device__ __forceinline__ CellDst cell_dst(const EpiOp& e, const BTile& t, int r, int c, bool valid) {
     CellDst d;
-    const int gy = t.oy0 * op.org_mul - op.org_sub + r, gx = t.ox0 * op.org_mul - op.org_sub + c;
+    const int gy = t.oy0 * e.org_mul - e.org_sub + r, gx = t.ox0 * e.org_mul - e.org_sub + c;
     d.valid = valid;
-    d.inside = gy >= 0 && gy < op.H && gx >= 0 && gx < op.W;
-    d.sbuf = nullptr, d.gdst = nullptr, d.ost = nullptr, d.plane_bytes = 0, d.ost_xor = 0;
-    if (op.buf >= 0) {
-        const BRegion& B = P.bufs[op.buf];
-        d.sbuf = smem + B.smem_off + (r * B.ext_w + c) * 16;
-        d.plane_bytes = B.plane_bytes;
-    }
-    if (op.emit && valid) {
-        const int ty = gy - t.oy0, tx = gx - t.ox0;
-        if (op.ostage) {
-            // any cell of the tile box (the TMA store clips what lies outside the image)
-            if (ty >= 0 && ty < P.tile_h && tx >= 0 && tx < P.tile_w) {
-                const int cell = ty * P.tile_w + tx;
-                d.ost = smem + op.ost_off + cell * op.ost_rowb;
-                const uint32_t a = smem_u32(d.ost);
-                d.ost_xor = op.ost_kb_ch == 64 ? int((a >> 7) & 7u) : int((a >> 7) & 1u);
-            }
-        } else if (d.inside && owns(P, op, t, gy, gx)) {
-            d.gdst = op.out + ((size_t(t.n) * op.H + gy) * op.W + gx) * op.out_cstride + op.out_coff + t.c0;
-        }
-    }
+    d.inside = gy >= 0 && gy < e.H && gx >= 0 && gx < e.W;
+    d.sbuf = e.buf ? e.buf + (r * e.buf_ew + c) * 16 : nullptr;
+    d.gdst = nullptr;
+    if (e.emit && valid && d.inside && owns(e, t, gy, gx))
+        d.gdst = e.out + ((size_t(t.n) * e.H + gy) * e.W + gx) * e.out_cstride + e.out_coff + t.c0;
     return d;
 }
 
@@ -231,31 +242,26 @@ __device__ __forceinline__ uint4 pack8(const float* v) {
 }
 
 // Stores 8 channels [ch, ch+8) of one cell (values already final).
-__device__ __forceinline__ void put8(const CellDst& d, int ch, const float* v8, const BOp& op, int chbase = 0) {
+__device__ __forceinline__ void put8(const CellDst& d, int ch, const float* v8, const EpiOp& e) {
     const uint4 u = pack8(v8);
-    if (d.sbuf) *reinterpret_cast<uint4*>(d.sbuf + (ch >> 3) * d.plane_bytes) = d.inside ? u : make_uint4(0, 0, 0, 0);
+    if (d.sbuf) *reinterpret_cast<uint4*>(d.sbuf + (ch >> 3) * e.buf_plane) = d.inside ? u : make_uint4(0, 0, 0, 0);
     if (d.gdst) *reinterpret_cast<uint4*>(d.gdst + ch) = u;
-    if (d.ost) {
-        const int rel = ch - chbase, kb = rel / op.ost_kb_ch, j = (rel - kb * op.ost_kb_ch) >> 3;
-        *reinterpret_cast<uint4*>(d.ost + kb * op.ost_kb_bytes + ((j ^ d.ost_xor) << 4)) = u;
-    }
 }
 
 // Bias + ReLU + store of N accumulator columns (channels ch0 ...), unrolled.
 template <int N>
-__device__ __forceinline__ void finish_cols(const BOp& op, const float* bias, const CellDst& d, int ch0, int chbase, int c8end,
-                                            float* v) {
+__device__ __forceinline__ void finish_cols(const EpiOp& e, const CellDst& d, int ch0, float* v) {
 #pragma unroll
     for (int j = 0; j < N; j += 8) {
-        if (ch0 + j >= c8end) break;
-        const float4 b0 = *reinterpret_cast<const float4*>(bias + ch0 + j);
-        const float4 b1 = *reinterpret_cast<const float4*>(bias + ch0 + j + 4);
+        if (ch0 + j >= e.c8end) break;
+        const float4 b0 = *reinterpret_cast<const float4*>(e.bias + ch0 + j);
+        const float4 b1 = *reinterpret_cast<const float4*>(e.bias + ch0 + j + 4);
         float* x = v + j;
         x[0] += b0.x, x[1] += b0.y, x[2] += b0.z, x[3] += b0.w, x[4] += b1.x, x[5] += b1.y, x[6] += b1.z, x[7] += b1.w;
-        if (op.relu)
+        if (e.relu)
 #pragma unroll
             for (int k = 0; k < 8; ++k) x[k] = fmaxf(x[k], 0.0f);
-        put8(d, ch0 + j, x, op, chbase);
+        put8(d, ch0 + j, x, e);
     }
 }
 
@@ -263,53 +269,59 @@ __device__ __forceinline__ void finish_cols(const BOp& op, const float* bias, co
 // (row = tid % 128) owns TMEM lane `row` = GEMM row = one cell; the two
 // warp groups split the accumulator columns in 32-column slices.
 __device__ void epilogue_mma(const BParams& P, const BOp& op, int nbi, uint8_t* smem, uint32_t tmem, const BTile& t) {
+    const EpiOp e = epi_op(P, op, smem);
+    const int mtiles = op.mtiles, contig = op.contig, ext_w = op.ext_w, ext_h = op.ext_h, strips = op.strips, nb = op.nb;
     const int row = threadIdx.x & 127, half = threadIdx.x >> 7;
-    const uint32_t lane_base = uint32_t(row & ~31) << 16;
-    const int c8end = (op.cout + 7) & ~7;  // never write past the tensor's padded channels
-    const float* bias = reinterpret_cast<const float*>(smem + op.bias_smem);
-    for (int mt = 0; mt < op.mtiles; ++mt) {
+    const uint32_t tbase = tmem + op.tcol + (uint32_t(row & ~31) << 16);
+    const int chbase = nbi * nb;
+    for (int mt = 0; mt < mtiles; ++mt) {
         int r, c;
         bool valid;
-        if (op.contig) {
+        if (contig) {
             const int idx = mt * 128 + row;
-            r = idx / op.ext_w, c = idx - r * op.ext_w;
-            valid = idx < op.ext_h * op.ext_w;
+            r = idx / ext_w, c = idx - r * ext_w;
+            valid = idx < ext_h * ext_w;
         } else {
-            const int st = mt % op.strips, rb = mt / op.strips;
+            const int st = mt % strips, rb = mt / strips;
             r = rb * 16 + (row >> 3), c = st * 8 + (row & 7);
-            valid = r < op.ext_h && c < op.ext_w;
+            valid = r < ext_h && c < ext_w;
         }
-        const CellDst d = cell_dst(P, op, smem, t, r, c, valid);
-        for (int col = half * 32; col < op.nb; col += 64) {
-            const uint32_t ta = tmem + op.tcol + lane_base + mt * op.nb + col;
-            const int ch0 = nbi * op.nb + col;
-            if (op.nb - col >= 32) {
+        const CellDst d = cell_dst(e, t, r, c, valid);
+        for (int col = half * 32; col < nb; col += 64) {
+            const uint32_t ta = tbase + mt * nb + col;
+            if (nb - col >= 32) {
                 float v[32];
                 tmem_ld32(ta, v);
-                if (valid) finish_cols<32>(op, bias, d, ch0, nbi * op.nb, c8end, v);
+                if (valid) finish_cols<32>(e, d, chbase + col, v);
             } else {
                 float v[16];
                 tmem_ld16(ta, v);
-                if (valid) finish_cols<16>(op, bias, d, ch0, nbi * op.nb, c8end, v);
+                if (valid) finish_cols<16>(e, d, chbase + col, v);
             }
         }
     }
 }
 
-// Shared byte offset of 16-byte chunk `oct` (channels [8*oct, 8*oct+8)) of a
-// cell, honouring the region's swizzle (a function of the absolute address).
-__device__ __forceinline__ uint32_t chunk_off(const uint8_t* smem, const BRegion& R, int cell, int oct) {
-    const int per = R.kb_ch >> 3;  // 16-byte chunks per row
-    const int kb = oct / per, j = oct - kb * per;
-    const uint32_t off = R.smem_off + kb * R.plane_bytes + cell * R.row_bytes + j * 16;
-    if (R.mode == kPlanes) return off;
-    const uint32_t a = smem_u32(smem) + off;
-    const uint32_t mask = R.mode == kSw128 ? 7u : 1u;
-    return off ^ (((a >> 7) & mask) << 4);
+// Register copy of a shared region's addressing.  Swizzled regions start on
+// 1024-byte boundaries with 1024-multiple K-block strides, so the swizzle of
+// cell r is (r & 7) for SW128 and ((r >> 2) & 1) for SW32.
+struct RegionView {
+    uint8_t* base;
+    int mode, per, plane, rowb, ew;  // per = 16-byte chunks per row
+};
+
+__device__ __forceinline__ RegionView region_view(const BRegion& R, uint8_t* smem) {
+    return {smem + R.smem_off, R.mode, R.kb_ch >> 3, R.plane_bytes, R.row_bytes, R.ext_w};
 }
 
-__device__ __forceinline__ void load8(const uint8_t* smem, const BRegion& R, int cell, int oct, float* f) {
-    const uint4 raw = *reinterpret_cast<const uint4*>(smem + chunk_off(smem, R, cell, oct));
+__device__ __forceinline__ const uint8_t* chunk_ptr(const RegionView& v, int cell, int oct) {
+    const int kb = oct / v.per, j = oct - kb * v.per;
+    const int sw = v.mode == kSw128 ? (cell & 7) : v.mode == kSw32 ? ((cell >> 2) & 1) : 0;
+    return v.base + kb * v.plane + cell * v.rowb + ((j ^ sw) << 4);
+}
+
+__device__ __forceinline__ void load8(const RegionView& v, int cell, int oct, float* f) {
+    const uint4 raw = *reinterpret_cast<const uint4*>(chunk_ptr(v, cell, oct));
     const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&raw);
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
@@ -321,69 +333,82 @@ __device__ __forceinline__ void load8(const uint8_t* smem, const BRegion& R, int
 // Pools (zero padding for max and avg, avg over the full window:
 // reference.cpp:59-88) and adds over shared planes.
 __device__ void simt_pool_add(const BParams& P, const BOp& op, uint8_t* smem, const BTile& t) {
-    const BRegion& R = src_region(P, op, op.src);
-    const int ncell = op.ext_h * op.ext_w, c8 = op.npad / 8;
-    const float inv = 1.0f / float(op.kh * op.kw);
+    const EpiOp e = epi_op(P, op, smem);
+    const RegionView R = region_view(src_region(P, op, op.src), smem);
+    const RegionView R2 = op.kind == BOP_ADD ? region_view(P.bufs[op.src2], smem) : R;
+    const int kind = op.kind, ext_w = op.ext_w, kh_ = op.kh, kw_ = op.kw, stride = op.stride, dd = op.d;
+    const int ncell = op.ext_h * ext_w, c8 = op.npad / 8;
+    const float inv = 1.0f / float(kh_ * kw_);
     for (int u = threadIdx.x; u < ncell * c8; u += kCompute) {
         const int cell = u / c8, oct = u - cell * c8;
-        const int r = cell / op.ext_w, c = cell - r * op.ext_w;
+        const int r = cell / ext_w, c = cell - r * ext_w;
         float acc[8], x[8];
-        if (op.kind == BOP_ADD) {
-            const BRegion& R2 = P.bufs[op.src2];
-            load8(smem, R, r * R.ext_w + c, oct, acc);
-            load8(smem, R2, r * R2.ext_w + c, oct, x);
+        if (kind == BOP_ADD) {
+            load8(R, r * R.ew + c, oct, acc);
+            load8(R2, r * R2.ew + c, oct, x);
+#pragma unroll
             for (int j = 0; j < 8; ++j) acc[j] += x[j];
         } else {
-            for (int j = 0; j < 8; ++j) acc[j] = op.kind == BOP_MAXPOOL ? __int_as_float(0xff800000) : 0.0f;
-            for (int kh = 0; kh < op.kh; ++kh)
-                for (int kw = 0; kw < op.kw; ++kw) {
-                    load8(smem, R, (r * op.stride + kh + op.d) * R.ext_w + c * op.stride + kw + op.d, oct, x);
-                    for (int j = 0; j < 8; ++j) acc[j] = op.kind == BOP_MAXPOOL ? fmaxf(acc[j], x[j]) : acc[j] + x[j];
+            const bool mx = kind == BOP_MAXPOOL;
+#pragma unroll
+            for (int j = 0; j < 8; ++j) acc[j] = mx ? __int_as_float(0xff800000) : 0.0f;
+            const int base = (r * stride + dd) * R.ew + c * stride + dd;
+            for (int kh = 0; kh < kh_; ++kh)
+                for (int kw = 0; kw < kw_; ++kw) {
+                    load8(R, base + kh * R.ew + kw, oct, x);
+#pragma unroll
+                    for (int j = 0; j < 8; ++j) acc[j] = mx ? fmaxf(acc[j], x[j]) : acc[j] + x[j];
                 }
-            if (op.kind == BOP_AVGPOOL)
+            if (!mx)
+#pragma unroll
                 for (int j = 0; j < 8; ++j) acc[j] *= inv;
         }
-        put8(cell_dst(P, op, smem, t, r, c, true), oct * 8, acc, op);
+        put8(cell_dst(e, t, r, c, true), oct * 8, acc, e);
     }
 }
 
 // Direct conv for what the tensor-core path does not take (stride != 1,
-// groups, Cin not a multiple of 16: SqueezeNet conv1).  fp32 accumulate.
+// groups, Cin not a multiple of 16).  fp32 accumulate.
 __device__ void simt_conv(const BParams& P, const BOp& op, uint8_t* smem, const BTile& t) {
-    const BRegion& R = src_region(P, op, op.src);
-    const int ncell = op.ext_h * op.ext_w, c8 = op.npad / 8;
-    const int cin_g = op.cin / op.group, cout_g = op.cout / op.group, cp4 = (op.cout + 3) & ~3;
+    const EpiOp e = epi_op(P, op, smem);
+    const RegionView R = region_view(src_region(P, op, op.src), smem);
+    const int ext_w = op.ext_w, kh_ = op.kh, kw_ = op.kw, stride = op.stride, dd = op.d, cout = op.cout;
+    const int ncell = op.ext_h * ext_w, c8 = op.npad / 8;
+    const int cin_g = op.cin / op.group, cout_g = cout / op.group, cp4 = (cout + 3) & ~3;
+    const float* wsimt = op.wsimt;
+    const float* gbias = op.bias;
     for (int u = threadIdx.x; u < ncell * c8; u += kCompute) {
         const int cell = u / c8, oct = u - cell * c8;
-        const int r = cell / op.ext_w, c = cell - r * op.ext_w;
+        const int r = cell / ext_w, c = cell - r * ext_w;
         float acc[8];
+#pragma unroll
         for (int j = 0; j < 8; ++j) acc[j] = 0.0f;
-        const int base = (r * op.stride + op.d) * R.ext_w + c * op.stride + op.d;
+        const int base = (r * stride + dd) * R.ew + c * stride + dd;
         for (int ic = 0; ic < cin_g; ++ic)
-            for (int kh = 0; kh < op.kh; ++kh)
-                for (int kw = 0; kw < op.kw; ++kw) {
-                    const int cell_in = base + kh * R.ext_w + kw;
-                    const float* wrow = op.wsimt + ((ic * op.kh + kh) * op.kw + kw) * cp4;
+            for (int kh = 0; kh < kh_; ++kh)
+                for (int kw = 0; kw < kw_; ++kw) {
+                    const int cell_in = base + kh * R.ew + kw;
+                    const float* wrow = wsimt + ((ic * kh_ + kh) * kw_ + kw) * cp4;
 #pragma unroll
                     for (int j = 0; j < 8; ++j) {
                         const int oc = oct * 8 + j;
-                        if (oc >= op.cout) break;
+                        if (oc >= cout) break;
                         const int in_c = (oc / cout_g) * cin_g + ic;
-                        const __nv_bfloat16 xv = *reinterpret_cast<const __nv_bfloat16*>(
-                            smem + chunk_off(smem, R, cell_in, in_c >> 3) + (in_c & 7) * 2);
+                        const __nv_bfloat16 xv = *reinterpret_cast<const __nv_bfloat16*>(chunk_ptr(R, cell_in, in_c >> 3) + (in_c & 7) * 2);
                         acc[j] = fmaf(__bfloat162float(xv), __ldg(wrow + oc), acc[j]);
                     }
                 }
+#pragma unroll
         for (int j = 0; j < 8; ++j) {
             const int oc = oct * 8 + j;
-            float x = oc < op.cout ? acc[j] + __ldg(op.bias + oc) : 0.0f;
-            acc[j] = op.relu ? fmaxf(x, 0.0f) : x;
+            const float x = oc < cout ? acc[j] + __ldg(gbias + oc) : 0.0f;
+            acc[j] = e.relu ? fmaxf(x, 0.0f) : x;
         }
-        put8(cell_dst(P, op, smem, t, r, c, true), oct * 8, acc, op);
+        put8(cell_dst(e, t, r, c, true), oct * 8, acc, e);
     }
 }
 
-__global__ void __launch_bounds__(kBThreads, 1) fused_bf16_kernel(const __grid_constant__ BParams Pg) {
+__global__ void __launch_bounds__(kBThreads, 2) fused_bf16_kernel(const __grid_constant__ BParams Pg) {
     extern __shared__ __align__(1024) uint8_t smem[];
     __shared__ __align__(8) uint64_t bar_x, ring_full[kRingSlots], ring_empty[kRingSlots], acc_full[kBMaxUnits],
         unit_done[kBMaxUnits];
@@ -453,25 +478,10 @@ __global__ void __launch_bounds__(kBThreads, 1) fused_bf16_kernel(const __grid_c
                 if (op.kind == BOP_SIMT_CONV) simt_conv(P, op, smem, t);
                 else simt_pool_add(P, op, smem, t);
             }
-            fence_async_smem();
+            fence_async_smem();  // epilogue-written buffers are read by later MMAs (async proxy)
             fence_before();
             named_sync_compute();
-            if (threadIdx.x == 0) {
-                if (G.mma) {  // TMA stores of the staged outputs of this group
-                    bool any = false;
-                    for (int i = G.op0; i < G.op1; ++i) {
-                        const BOp& op = P.ops[i];
-                        if (!op.ostage) continue;
-                        const int chans = op.nblocks > 1 ? op.nb : ((op.cout + 15) & ~15);
-                        for (int kb = 0; kb < chans / op.ost_kb_ch; ++kb)
-                            tma_store_4d(&Pg.omap[op.omap], smem + op.ost_off + kb * op.ost_kb_bytes,
-                                         op.out_coff + G.nbi * op.nb + kb * op.ost_kb_ch, t.ox0, t.oy0, t.n);
-                        any = true;
-                    }
-                    if (any) bulk_commit(), bulk_wait_read();  // staging reusable once read
-                }
-                mbar_arrive(&unit_done[gi]), stamp(P, kTrUnit + 2 * gi + 1);
-            }
+            if (threadIdx.x == 0) mbar_arrive(&unit_done[gi]), stamp(P, kTrUnit + 2 * gi + 1);
         }
     }
     fence_before();

@@ -41,8 +41,8 @@ def main():
                 continue
             rel = lambda k: f"{(ev[k] - t0) / 1000:7.2f}" if ev[k] else "      -"
             units = " ".join(f"[{rel(4 + 2 * u)} {rel(5 + 2 * u)}]" for u in range(12) if ev[4 + 2 * u] or ev[5 + 2 * u])
-            print(f"  cta{cta}: xiss {rel(1)} xland {rel(2)} w0 {rel(28)} mma1 {rel(26)} mma3 {rel(27)} g0 issue [{rel(29)} {rel(30)}] "
-                  f"g1 issue [{rel(31)}] units {units} end {rel(3)}")
+            print(f"  cta{cta}: xland {rel(2)} g0 issue [{rel(29)} {rel(30)}] g1 issue [{rel(31)}] units {units} "
+                  f"epi0 [{rel(20)} {rel(21)} {rel(22)}] epi1 [{rel(23)} {rel(24)} {rel(25)}] end {rel(3)}")
 
 
 if __name__ == "__main__":
