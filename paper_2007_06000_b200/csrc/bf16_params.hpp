@@ -106,6 +106,9 @@ struct alignas(64) BParams {
     // Optional phase trace (XLF_TRACE=1): globaltimer stamps of CTAs with
     // blockIdx.y == 0 and blockIdx.x < kTraceCtas, kTraceEvents each.
     unsigned long long* trace;
+    // Device-memory copy of this descriptor: the kernel pulls it into shared
+    // memory with one bulk copy instead of per-thread parameter-bank loads.
+    const void* dev_copy;
 };
 
 constexpr int kTraceCtas = 8;

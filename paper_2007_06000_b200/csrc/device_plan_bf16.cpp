@@ -189,9 +189,11 @@ long long layout_bf16(const Graph& g, const StepSpec& s, int th, int tw, BParams
     }
     // shared memory
     long long bytes = 0;
-    auto region = [&](BRegion& r) {
+    // Epilogue-written plane buffers get a plane stride of 16 (mod 128) bytes:
+    // SIMT readers fetch the 8 planes of one cell from 8 different bank groups.
+    auto region = [&](BRegion& r, bool skew = false) {
         const int kbs = r.kb_ch / 8;  // 8-channel groups per K-block
-        if (r.mode == kPlanes) r.plane_bytes = r128(r.ext_h * r.ext_w * r.row_bytes);
+        if (r.mode == kPlanes) r.plane_bytes = r128(r.ext_h * r.ext_w * r.row_bytes) + (skew ? 16 : 0);
         else r.plane_bytes = (r.ext_h * r.ext_w * r.row_bytes + 1023) & ~1023;
         bytes = (bytes + 1023) & ~1023LL;  // swizzle atoms / TMA destinations
         r.smem_off = int(bytes);
@@ -214,7 +216,7 @@ long long layout_bf16(const Graph& g, const StepSpec& s, int th, int tw, BParams
         b.c8 = r8(g.find_layer(s.ops[size_t(i)].layer)->out_shape->channels) / 8;
         b.ext_h = geo[size_t(i)].ext_h, b.ext_w = geo[size_t(i)].ext_w;
         b.mode = kPlanes, b.kb_ch = 8, b.row_bytes = 16;  // written by the epilogue threads
-        region(b);
+        region(b, true);
     }
     bool any_mma = false;
     int tmem = 0;
@@ -372,7 +374,8 @@ static bool choose_tile_bf16_at(const Graph& g, StepSpec& s, int batch_hint, int
             }
             const double out_bytes = double(th) * tw * 2.0 * 256;  // order of magnitude; same for all tiles per pixel
             const double ctas = double(P->grid_h) * P->grid_w * P->cgroups * std::max(batch_hint, 1);
-            int occ = std::max(1, std::min(4, int((227 * 1024) / (sm + 2048))));
+            // 228 KB per SM; per CTA: dynamic + static (~3 KB) + 1 KB driver reserve; <= 2 by registers
+            int occ = std::max(1, std::min(2, int((228 * 1024) / (sm + 4096))));
             if (P->tmem_cols) occ = std::min(occ, 512 / P->tmem_cols);
             const double waves = std::ceil(ctas / (148.0 * occ));
             // cycles per CTA ~ bytes/(per-SM HBM share) + MMA (8192 MAC/clk/SM) + SIMT (128 FMA/clk)

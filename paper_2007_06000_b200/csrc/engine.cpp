@@ -233,6 +233,11 @@ Engine::Engine(const Graph& g, int device, Partition part, Precision prec, const
             P->trace = tr;
             traces_.push_back(tr);
         }
+        void* dev = nullptr;
+        cuda_check(cudaMalloc(&dev, sizeof(BParams)), "cudaMalloc(step descriptor)");
+        pdevs_.push_back(dev);
+        P->dev_copy = dev;
+        cuda_check(cudaMemcpy(dev, P.get(), sizeof(BParams), cudaMemcpyHostToDevice), "step descriptor H2D");
         bparams_[i] = std::move(P);
     }
 }
@@ -244,6 +249,7 @@ Engine::~Engine() {
     cudaFree(weights_);
     if (weights16_) cudaFree(weights16_);
     for (unsigned long long* p : traces_) cudaFree(p);
+    for (void* p : pdevs_) cudaFree(p);
     cudaFree(staging_);
     if (capture_) cudaStreamDestroy(capture_);
 }

@@ -67,6 +67,7 @@ private:
     std::vector<struct FusedParams> params_;
     std::vector<std::unique_ptr<struct BParams>> bparams_;  // bf16 steps
     std::vector<unsigned long long*> traces_;                // XLF_TRACE buffers
+    std::vector<void*> pdevs_;                               // device copies of the bf16 step descriptors
     void* weights16_ = nullptr;  // bf16 MMA weights
     int esz_ = 4;                // bytes per activation element
     bool s2d_ = false;           // bf16: first conv rewritten on a space-to-depth input

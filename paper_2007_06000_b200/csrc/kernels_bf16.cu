@@ -183,7 +183,7 @@ struct EpiOp {
     int buf_ew, buf_plane;
     uint8_t* buf;           // shared buffer base (planes), or null
     __nv_bfloat16* out;
-    const float* bias;
+    uint32_t bias_s;        // shared address of the op's fp32 bias (MMA ops)
 };
 
 __device__ __forceinline__ EpiOp epi_op(const BParams& P, const BOp& op, uint8_t* smem) {
@@ -198,7 +198,7 @@ __device__ __forceinline__ EpiOp epi_op(const BParams& P, const BOp& op, uint8_t
         e.buf = smem + B.smem_off, e.buf_ew = B.ext_w, e.buf_plane = B.plane_bytes;
     }
     e.out = op.out;
-    e.bias = op.bias_smem >= 0 ? reinterpret_cast<const float*>(smem + op.bias_smem) : op.bias;
+    e.bias_s = op.bias_smem >= 0 ? smem_u32(smem + op.bias_smem) : 0u;
     return e;
 }
 
@@ -241,6 +241,24 @@ __device__ __forceinline__ uint4 pack8(const float* v) {
     return u;
 }
 
+__device__ __forceinline__ float4 lds_f4(uint32_t a) {
+    float4 v;
+    asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(a));
+    return v;
+}
+
+__device__ __forceinline__ uint4 lds_u4(uint32_t a) {
+    uint4 v;
+    asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(a));
+    return v;
+}
+
+// Stores 8 bf16 channels [ch, ch+8) of one cell.
+__device__ __forceinline__ void put8u(const CellDst& d, int ch, uint4 u, const EpiOp& e) {
+    if (d.sbuf) *reinterpret_cast<uint4*>(d.sbuf + (ch >> 3) * e.buf_plane) = d.inside ? u : make_uint4(0, 0, 0, 0);
+    if (d.gdst) *reinterpret_cast<uint4*>(d.gdst + ch) = u;
+}
+
 // Stores 8 channels [ch, ch+8) of one cell (values already final).
 __device__ __forceinline__ void put8(const CellDst& d, int ch, const float* v8, const EpiOp& e) {
     const uint4 u = pack8(v8);
@@ -254,8 +272,8 @@ __device__ __forceinline__ void finish_cols(const EpiOp& e, const CellDst& d, in
 #pragma unroll
     for (int j = 0; j < N; j += 8) {
         if (ch0 + j >= e.c8end) break;
-        const float4 b0 = *reinterpret_cast<const float4*>(e.bias + ch0 + j);
-        const float4 b1 = *reinterpret_cast<const float4*>(e.bias + ch0 + j + 4);
+        const float4 b0 = lds_f4(e.bias_s + uint32_t(ch0 + j) * 4u);
+        const float4 b1 = lds_f4(e.bias_s + uint32_t(ch0 + j + 4) * 4u);
         float* x = v + j;
         x[0] += b0.x, x[1] += b0.y, x[2] += b0.z, x[3] += b0.w, x[4] += b1.x, x[5] += b1.y, x[6] += b1.z, x[7] += b1.w;
         if (e.relu)
@@ -330,41 +348,119 @@ __device__ __forceinline__ void load8(const RegionView& v, int cell, int oct, fl
     }
 }
 
-// Pools (zero padding for max and avg, avg over the full window:
-// reference.cpp:59-88) and adds over shared planes.
-__device__ void simt_pool_add(const BParams& P, const BOp& op, uint8_t* smem, const BTile& t) {
-    const EpiOp e = epi_op(P, op, smem);
-    const RegionView R = region_view(src_region(P, op, op.src), smem);
-    const RegionView R2 = op.kind == BOP_ADD ? region_view(P.bufs[op.src2], smem) : R;
-    const int kind = op.kind, ext_w = op.ext_w, kh_ = op.kh, kw_ = op.kw, stride = op.stride, dd = op.d;
+// Byte offset of 16-byte chunk j (within K-block kb) of cell `cell`, for a
+// region whose K-blocks start on 1024-byte boundaries (MODE = region mode).
+template <int MODE>
+__device__ __forceinline__ uint32_t chunk_off(uint32_t kb_base, int cell, int j) {
+    if (MODE == kSw128) return kb_base + uint32_t(cell) * 128u + uint32_t((j ^ (cell & 7)) << 4);
+    if (MODE == kSw32) return kb_base + uint32_t(cell) * 32u + uint32_t((j ^ ((cell >> 2) & 1)) << 4);
+    return kb_base + uint32_t(cell) * 16u;
+}
+
+__device__ __forceinline__ uint32_t bmax2(uint32_t a, uint32_t b) {
+    __nv_bfloat162 x = *reinterpret_cast<__nv_bfloat162*>(&a), y = *reinterpret_cast<__nv_bfloat162*>(&b);
+    __nv_bfloat162 m = __hmax2(x, y);
+    return *reinterpret_cast<uint32_t*>(&m);
+}
+
+// Pools over a shared region (zero padding is already in the region: TMA
+// zero fill / masked epilogue cells), max in bf16 (exact), average in fp32
+// over the full window (reference.cpp:59-88).  Thread u handles 8 channels
+// (oct) of one output cell, octs fastest: the 8 chunks of a cell sit in 8
+// different bank groups in every region mode, and 8 neighbouring threads
+// store one 128-byte run of the NHWC output.
+template <int MODE, int K, bool MX>
+__device__ void pool_fast(const EpiOp& e, const BRegion& Rg, uint8_t* smem, const BOp& op, const BTile& t) {
+    const uint32_t base = smem_u32(smem + Rg.smem_off);
+    const int plane = Rg.plane_bytes, rew = Rg.ext_w;
+    const int ext_w = op.ext_w, stride = op.stride, dd = op.d;
+    const int kh_ = K ? K : op.kh, kw_ = K ? K : op.kw;
     const int ncell = op.ext_h * ext_w, c8 = op.npad / 8;
     const float inv = 1.0f / float(kh_ * kw_);
+    constexpr int kPer = MODE == kSw128 ? 8 : MODE == kSw32 ? 2 : 1;
     for (int u = threadIdx.x; u < ncell * c8; u += kCompute) {
         const int cell = u / c8, oct = u - cell * c8;
         const int r = cell / ext_w, c = cell - r * ext_w;
-        float acc[8], x[8];
-        if (kind == BOP_ADD) {
-            load8(R, r * R.ew + c, oct, acc);
-            load8(R2, r * R2.ew + c, oct, x);
+        const int kb = oct / kPer, j = oct - kb * kPer;
+        const uint32_t kbb = base + uint32_t(kb * plane);
+        const int c0 = (r * stride + dd) * rew + c * stride + dd;
+        uint4 out;
+        if (MX) {
+            uint4 m = lds_u4(chunk_off<MODE>(kbb, c0, j));
 #pragma unroll
-            for (int j = 0; j < 8; ++j) acc[j] += x[j];
+            for (int ky = 0; ky < (K ? K : 1); ++ky)
+                for (int ky2 = 0; ky2 < (K ? 1 : kh_); ++ky2)
+#pragma unroll
+                    for (int kx = 0; kx < (K ? K : 1); ++kx)
+                        for (int kx2 = 0; kx2 < (K ? 1 : kw_); ++kx2) {
+                            const int dy = K ? ky : ky2, dx = K ? kx : kx2;
+                            if (dy == 0 && dx == 0) continue;
+                            const uint4 v = lds_u4(chunk_off<MODE>(kbb, c0 + dy * rew + dx, j));
+                            m.x = bmax2(m.x, v.x), m.y = bmax2(m.y, v.y), m.z = bmax2(m.z, v.z), m.w = bmax2(m.w, v.w);
+                        }
+            out = m;
         } else {
-            const bool mx = kind == BOP_MAXPOOL;
+            float acc[8];
 #pragma unroll
-            for (int j = 0; j < 8; ++j) acc[j] = mx ? __int_as_float(0xff800000) : 0.0f;
-            const int base = (r * stride + dd) * R.ew + c * stride + dd;
-            for (int kh = 0; kh < kh_; ++kh)
-                for (int kw = 0; kw < kw_; ++kw) {
-                    load8(R, base + kh * R.ew + kw, oct, x);
+            for (int q = 0; q < 8; ++q) acc[q] = 0.0f;
+            for (int dy = 0; dy < kh_; ++dy)
+                for (int dx = 0; dx < kw_; ++dx) {
+                    const uint4 v = lds_u4(chunk_off<MODE>(kbb, c0 + dy * rew + dx, j));
+                    const uint32_t w[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
-                    for (int j = 0; j < 8; ++j) acc[j] = mx ? fmaxf(acc[j], x[j]) : acc[j] + x[j];
+                    for (int q = 0; q < 4; ++q) {
+                        const float2 f = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&w[q]));
+                        acc[2 * q] += f.x, acc[2 * q + 1] += f.y;
+                    }
                 }
-            if (!mx)
 #pragma unroll
-                for (int j = 0; j < 8; ++j) acc[j] *= inv;
+            for (int q = 0; q < 8; ++q) acc[q] *= inv;
+            out = pack8(acc);
+        }
+        put8u(cell_dst(e, t, r, c, true), oct * 8, out, e);
+    }
+}
+
+template <int MODE>
+__device__ __forceinline__ void pool_mode(const EpiOp& e, const BRegion& R, uint8_t* smem, const BOp& op, const BTile& t) {
+    if (op.kind == BOP_MAXPOOL) {
+        if (op.kh == 3 && op.kw == 3) pool_fast<MODE, 3, true>(e, R, smem, op, t);
+        else pool_fast<MODE, 0, true>(e, R, smem, op, t);
+    } else {
+        pool_fast<MODE, 0, false>(e, R, smem, op, t);
+    }
+}
+
+// Residual add of two shared plane buffers.
+__device__ void simt_add(const EpiOp& e, const BRegion& A, const BRegion& B, uint8_t* smem, const BOp& op, const BTile& t) {
+    const int ext_w = op.ext_w, ncell = op.ext_h * ext_w, c8 = op.npad / 8;
+    for (int u = threadIdx.x; u < ncell * c8; u += kCompute) {
+        const int cell = u / c8, oct = u - cell * c8;
+        const int r = cell / ext_w, c = cell - r * ext_w;
+        const uint4 a = lds_u4(smem_u32(smem + A.smem_off + oct * A.plane_bytes + (r * A.ext_w + c) * 16));
+        const uint4 b = lds_u4(smem_u32(smem + B.smem_off + oct * B.plane_bytes + (r * B.ext_w + c) * 16));
+        const uint32_t wa[4] = {a.x, a.y, a.z, a.w}, wb[4] = {b.x, b.y, b.z, b.w};
+        float acc[8];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const float2 fa = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&wa[q]));
+            const float2 fb = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&wb[q]));
+            acc[2 * q] = fa.x + fb.x, acc[2 * q + 1] = fa.y + fb.y;
         }
         put8(cell_dst(e, t, r, c, true), oct * 8, acc, e);
     }
+}
+
+__device__ void simt_pool_add(const BParams& P, const BOp& op, uint8_t* smem, const BTile& t) {
+    const EpiOp e = epi_op(P, op, smem);
+    const BRegion& R = src_region(P, op, op.src);
+    if (op.kind == BOP_ADD) {
+        simt_add(e, R, P.bufs[op.src2], smem, op, t);
+        return;
+    }
+    if (R.mode == kSw128) pool_mode<kSw128>(e, R, smem, op, t);
+    else if (R.mode == kSw32) pool_mode<kSw32>(e, R, smem, op, t);
+    else pool_mode<kPlanes>(e, R, smem, op, t);
 }
 
 // Direct conv for what the tensor-core path does not take (stride != 1,
@@ -415,40 +511,39 @@ __global__ void __launch_bounds__(kBThreads, 2) fused_bf16_kernel(const __grid_c
     __shared__ uint32_t tmem_slot;
     // The descriptor lives in the kernel-parameter constant bank; the op loops
     // index it with run-time op numbers, and indexed constant loads that miss
-    // the small constant cache stall the single MMA-issuing thread for hundreds
-    // of cycles per instruction.  Work from a shared-memory copy instead (the
-    // tensor maps stay in parameter space, where TMA must read them).
+    // the small constant cache stall for hundreds of cycles.  The epilogue
+    // warps work from a shared-memory copy, pulled from the device copy with
+    // one bulk copy; the producer (few loads, latency-critical X issue) and
+    // the MMA issuer (uniform indices) read the bank, which also holds the
+    // tensor maps TMA reads.
     __shared__ __align__(64) BParams Ps;
-    {
-        const uint4* src = reinterpret_cast<const uint4*>(&Pg);
-        uint4* dst = reinterpret_cast<uint4*>(&Ps);
-        for (int i = threadIdx.x; i < int(sizeof(BParams) / 16); i += blockDim.x) dst[i] = src[i];
-        __syncthreads();
-    }
-    const BParams& P = Ps;
+    __shared__ __align__(8) uint64_t bar_p;
     const int warp = __shfl_sync(0xffffffffu, int(threadIdx.x >> 5), 0), lane = threadIdx.x & 31;  // provably warp-uniform
-    BTile t;
+    BTile t;  // from the parameter bank (uniform, non-indexed loads)
     t.n = blockIdx.y;
-    t.ty = blockIdx.x / P.grid_w;
-    t.tx = blockIdx.x - t.ty * P.grid_w;
-    t.oy0 = t.ty * P.tile_h;
-    t.ox0 = t.tx * P.tile_w;
-    t.c0 = blockIdx.z * P.ctile;
-    const int units = P.ngroups;
+    t.ty = blockIdx.x / Pg.grid_w;
+    t.tx = blockIdx.x - t.ty * Pg.grid_w;
+    t.oy0 = t.ty * Pg.tile_h;
+    t.ox0 = t.tx * Pg.tile_w;
+    t.c0 = blockIdx.z * Pg.ctile;
     if (threadIdx.x == 0) {
+        mbar_init(&bar_p, 1);
         mbar_init(&bar_x, 1);
         for (int i = 0; i < kRingSlots; ++i) mbar_init(&ring_full[i], 1), mbar_init(&ring_empty[i], 1);
-        for (int i = 0; i < units; ++i) mbar_init(&acc_full[i], 1), mbar_init(&unit_done[i], 1);
+        for (int i = 0; i < Pg.ngroups; ++i) mbar_init(&acc_full[i], 1), mbar_init(&unit_done[i], 1);
         mbar_fence_init();
+        mbar_expect_tx(&bar_p, uint32_t(sizeof(BParams)));
+        bulk_g2s(&Ps, Pg.dev_copy, uint32_t(sizeof(BParams)), &bar_p);
     }
-    if (warp == 9 && P.tmem_cols) tmem_alloc(&tmem_slot, P.tmem_cols);
+    if (warp == 9 && Pg.tmem_cols) tmem_alloc(&tmem_slot, Pg.tmem_cols);
     fence_before();
     __syncthreads();
     fence_after();
-    const uint32_t tmem = P.tmem_cols ? tmem_slot : 0;
+    const BParams& P = Ps;
+    const uint32_t tmem = Pg.tmem_cols ? tmem_slot : 0;
 
     if (warp == 8) {
-        if (lane == 0) producer(P, Pg.xmap, smem, t, &bar_x, ring_full, ring_empty);
+        if (lane == 0) producer(Pg, Pg.xmap, smem, t, &bar_x, ring_full, ring_empty);  // starts before Ps lands
     } else if (warp == 9) {
         // Whole warp, warp-uniform control flow, one elected lane issues; the
         // op fields come from the parameter bank with uniform indices, so the
@@ -456,6 +551,7 @@ __global__ void __launch_bounds__(kBThreads, 2) fused_bf16_kernel(const __grid_c
         issuer(Pg, smem, tmem, &bar_x, ring_full, ring_empty, acc_full, unit_done);
         __syncwarp();
     } else {
+        mbar_wait(&bar_p, 0);
         // biases of the MMA ops -> shared memory (read by every epilogue)
         for (int i = 0; i < P.nops; ++i) {
             const BOp& op = P.ops[i];
@@ -487,7 +583,7 @@ __global__ void __launch_bounds__(kBThreads, 2) fused_bf16_kernel(const __grid_c
     fence_before();
     __syncthreads();
     fence_after();
-    if (warp == 9 && P.tmem_cols) tmem_free(tmem, P.tmem_cols);
+    if (warp == 9 && Pg.tmem_cols) tmem_free(tmem, Pg.tmem_cols);
     if (threadIdx.x == 0) stamp(P, kTrEnd);
 }
 

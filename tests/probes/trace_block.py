@@ -42,7 +42,7 @@ def main():
             rel = lambda k: f"{(ev[k] - t0) / 1000:7.2f}" if ev[k] else "      -"
             units = " ".join(f"[{rel(4 + 2 * u)} {rel(5 + 2 * u)}]" for u in range(12) if ev[4 + 2 * u] or ev[5 + 2 * u])
             print(f"  cta{cta}: xland {rel(2)} g0 issue [{rel(29)} {rel(30)}] g1 issue [{rel(31)}] units {units} "
-                  f"epi0 [{rel(20)} {rel(21)} {rel(22)}] epi1 [{rel(23)} {rel(24)} {rel(25)}] end {rel(3)}")
+                  f"end {rel(3)}")
 
 
 if __name__ == "__main__":
