@@ -162,7 +162,10 @@ def parse_graph(text: str) -> OGraph:
 
 
 def out_dim(n, k, pad, stride):
-    return (n + 2 * pad - k) // stride + 1  # graph.cpp:76-78
+    """graph.cpp:76-78 in C++ int arithmetic: the division truncates toward
+    zero, so a window one cell wider than the padded input still yields 1."""
+    q = n + 2 * pad - k
+    return (q // stride if q >= 0 else -((-q) // stride)) + 1
 
 
 def topo_order(g: OGraph):
@@ -192,10 +195,14 @@ def infer_shapes(g: OGraph) -> OGraph:
             c["cin"] = ins[0][0]
             l.shape = (c["cout"], out_dim(ins[0][1], c["kh"], c["pad"], c["stride"]),
                        out_dim(ins[0][2], c["kw"], c["pad"], c["stride"]))
+            if min(l.shape[1:]) < 1:  # graph.cpp:362-365
+                raise ValueError(f"{l.name}: non-positive output dimension")
         elif l.kind == "pool":
             p = l.pool
             l.shape = (ins[0][0], out_dim(ins[0][1], p["k"], p["pad"], p["stride"]),
                        out_dim(ins[0][2], p["k"], p["pad"], p["stride"]))
+            if min(l.shape[1:]) < 1:  # graph.cpp:374-375
+                raise ValueError(f"{l.name}: non-positive output dimension")
         elif l.kind in ("relu", "add"):
             l.shape = ins[0]
         elif l.kind == "concat":

@@ -240,8 +240,9 @@ def test_random_graphs_exact():
                 f"layer {{\n  name cat\n  kind concat\n  inputs [a, b]\n}}\n"
                 f"layer {{\n  name p\n  kind pool\n  inputs [cat]\n  pool max\n  kernel 3\n  stride 2\n}}\n"
                 "output p\n")
-        og = O.load_graph(text)
-        if og.shape_of("p")[1] < 1:
+        try:
+            og = O.load_graph(text)
+        except ValueError:  # non-positive output dimension: the reference rejects it too
             continue
         w = O.seeded_weights(og, trial)
         x = O.seeded_batch(og, trial + 100, 2)

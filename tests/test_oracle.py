@@ -74,3 +74,24 @@ def test_oracle_matches_reference_library(name):
         # and the reference's own fused interpreter agrees with its oracle
         sim = R.run(text, x, o, g.shape_of(o), weights=O.flat_weights(g, w), mode=1)
         assert np.array_equal(sim, theirs)
+
+
+@pytest.mark.skipif(not R.available(), reason="reference library not built (oracle/_ref)")
+def test_out_dim_truncates_like_the_reference():
+    """conv_out_dim (graph.cpp:76-78) divides in C++ int arithmetic: a 3-wide
+    pool over a 2-wide input gives width (2-3)/2+1 = 1, not floor's 0, and the
+    window reads the zero padding beyond the edge."""
+    text = ("name trunc\ninput {\n  name d\n  shape [5, 7, 2]\n}\n"
+            "layer {\n  name p\n  kind pool\n  inputs [d]\n  pool max\n  kernel 3\n  stride 2\n}\n"
+            "layer {\n  name c\n  kind conv\n  inputs [d]\n  out_channels 3\n  kernel [3, 3]\n  stride 2\n}\n"
+            "output p\noutput c\n")
+    g = O.load_graph(text)
+    assert g.shape_of("p") == (5, 3, 1) and g.shape_of("c") == (3, 3, 1)
+    w = O.seeded_weights(g, 3)
+    x = O.seeded_batch(g, 4, 2)
+    for o in ("p", "c"):
+        mine = O.run_batch(g, x, w, [o])[o]
+        theirs = R.run(text, x, o, g.shape_of(o), weights=O.flat_weights(g, w))
+        assert np.array_equal(mine, theirs), o
+    with pytest.raises(ValueError):
+        O.load_graph(text.replace("shape [5, 7, 2]", "shape [5, 7, 0]"))
