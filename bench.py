@@ -163,6 +163,9 @@ def time_blocks(X, torch, precision, reps=20):
         for part in ("b200", "unfused"):
             e = X.Engine(g, w, part, precision, max_batch=batch)
             e.set_input_seeded(42, batch)
+            if precision == "bf16":  # both arms measured-time tuned
+                e.forward(batch, use_graph=False)
+                e.autotune(batch, reps=3, topk=3)
             for _ in range(3):
                 e.forward(batch, use_graph=True)
             torch.cuda.synchronize()
@@ -194,6 +197,7 @@ def main():
     ap.add_argument("--precision", default="bf16", choices=["bf16", "fp32", "fp32_exact"])
     ap.add_argument("--no-blocks", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-tune", action="store_true", help="skip the measured-time tuner (planner model only)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
 
@@ -221,6 +225,14 @@ def main():
     st = torch.cuda.current_stream()
     # rank r's shard: images [r*B, (r+1)*B) of the seeded stream (no exchange)
     e.set_input_seeded(42, B, first_image=rank * B)
+    tune = None
+    if args.precision == "bf16" and not args.no_tune:
+        # measured-time tuner (part of the product, before the timed region)
+        t_tune = time.time()
+        e.forward(B, use_graph=False)
+        chosen = e.autotune(B, reps=3, topk=3)
+        tune = {"steps_tuned": len(chosen), "seconds": round(time.time() - t_tune, 2)}
+        e.set_input_seeded(42, B, first_image=rank * B)
     nsteps = len(e.steps)
 
     def barrier():
@@ -345,6 +357,7 @@ def main():
             "gpu_launches": args.steps * e.launches_per_forward,
             "clocks": clk.summary(),
             "blocks": blocks,
+            "autotune": tune,
         }
         print(json.dumps(line), flush=True)
     if world > 1:

@@ -109,6 +109,15 @@ xlf_status xlf_engine_read(xlf_engine* e, const char* name, float* d_nchw, int b
  * `name` into h_out (NCHW). Synchronous. */
 xlf_status xlf_engine_run_host(xlf_engine* e, const float* h_in_nchw, int batch, const char* name, float* h_out_nchw,
                                void* stream);
+/* Measured-time tuner (no reference counterpart: replaces the reference's
+ * model-only tune(), cost_model.cpp:236-294): times the `topk` best
+ * configurations of every bf16 fused step on the device (`reps` launches
+ * each, `batch` images) and keeps the fastest; fp32 engines: no-op. The
+ * choices are reported by xlf_engine_tune_report (JSON) and by
+ * xlf_engine_json's plan. Synchronous; not thread-safe with other calls on
+ * the same engine. */
+xlf_status xlf_engine_autotune(xlf_engine* e, int batch, int reps, int topk);
+xlf_status xlf_engine_tune_report(const xlf_engine* e, char* buf, size_t cap, size_t* need);
 /* Profiling aid (engine created with XLF_TRACE=1 in the environment, bf16):
  * globaltimer stamps of the first CTAs of a step's last launch. */
 xlf_status xlf_engine_trace(const xlf_engine* e, int step, unsigned long long* out, size_t cap, size_t* count);

@@ -216,6 +216,13 @@ class Engine:
                                         out.ctypes.data_as(f32p), _stream_ptr(stream)))
         return out
 
+    def autotune(self, batch: int = 0, reps: int = 3, topk: int = 4) -> list:
+        """Measured-time tuning of the bf16 fused steps (xlf_engine_autotune):
+        returns the chosen configuration of every tuned step."""
+        check(lib().xlf_engine_autotune(self._h, batch, reps, topk))
+        self.info = json.loads(text_call(lib().xlf_engine_json, self._h))
+        return json.loads(text_call(lib().xlf_engine_tune_report, self._h))
+
     def materialized(self):
         return [n for n, t in self.info["plan"]["tensors"].items() if t["materialized"]]
 

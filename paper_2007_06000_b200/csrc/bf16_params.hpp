@@ -32,6 +32,15 @@ constexpr int kBMaxOps = 8;
 constexpr int kBMaxBufs = 4;
 constexpr int kBMaxUnits = 24;  // (op, N block) pairs
 constexpr int kRingSlots = 3;
+// CTA shape: kEpiWarps epilogue/SIMT warps + 3 role warps (input producer,
+// MMA issuer, weight producer); up to kMaxCtasPerSm resident per SM.
+#ifndef XLF_EPI_WARPS
+#define XLF_EPI_WARPS 8
+#endif
+constexpr int kEpiWarps = XLF_EPI_WARPS;
+constexpr int kMaxCtasPerSm = kEpiWarps <= 4 ? 3 : 2;
+constexpr int kChunkBytes = 16 * 1024;  // weight ring slot
+constexpr int kRingMax = 8;             // ring slots (P.ring_slots <= this)
 
 struct BOp {
     int kind, stage, xin, src, src2, buf, emit, own_only;
@@ -51,6 +60,7 @@ struct BOp {
     __nv_bfloat16* out;
     int out_cstride, out_coff;
     int tcol;       // MMA: first TMEM column of this op inside its group
+    int wofs;       // MMA, resident weights: byte offset of the op's packed weights in the weight region
     int bias_smem;  // byte offset of the op's bias copy in shared memory (-1: none)
 };
 
@@ -100,12 +110,28 @@ struct alignas(64) BParams {
     int ngroups;
     BGroup groups[kBMaxUnits];
     int bias_off, bias_bytes;  // shared copy of every MMA op's bias
-    int ring_off, chunk_bytes;
+    int ring_off, chunk_bytes, ring_slots;
+    // Resident weights (wres = 1): every MMA op's packed weights are loaded
+    // into shared memory ONCE per (persistent) CTA at wres_off (wres_bytes)
+    // instead of being streamed through the ring for every tile.
+    int wres, wres_off, wres_bytes;
     int smem_bytes, tmem_cols;
     int ctile, cgroups;  // channel tiling of pool-only steps (0 = all channels)
+    // Persistent execution: each CTA walks tiles blockIdx.x, +gridDim.x, ...
+    // (tile = (image, channel group, tile row, tile column)).  The block
+    // inputs are staged in nxb buffers, xstride bytes apart, so the producer
+    // loads tile k+1's regions while tile k computes (nxb = 2).
+    int nxb, xstride;
+    int ctas_per_sm;  // resident CTAs per SM at smem_bytes (grid = 148 x this, capped by the tiles)
+    int grid_all;     // 1: grid = tiles (each CTA one tile), else the persistent grid
     // Optional phase trace (XLF_TRACE=1): globaltimer stamps of CTAs with
     // blockIdx.y == 0 and blockIdx.x < kTraceCtas, kTraceEvents each.
     unsigned long long* trace;
+    int trace_tiles;  // XLF_TRACE=2: instead, the end stamp of each of the first kTraceEvents tiles
+    // Phase-isolation switches for profiling (XLF_DBG, never set in
+    // production; results are wrong when set): 1 = epilogues skip HBM stores,
+    // 2 = epilogues skip the accumulator read entirely, 4 = no MMAs issued.
+    int dbg;
     // Device-memory copy of this descriptor: the kernel pulls it into shared
     // memory with one bulk copy instead of per-thread parameter-bank loads.
     const void* dev_copy;

@@ -21,6 +21,7 @@ struct xlf_graph {
 };
 struct xlf_engine {
     std::unique_ptr<xlf::Engine> e;
+    std::string tune_report;  // last xlf_engine_autotune result (JSON)
 };
 
 namespace {
@@ -316,6 +317,20 @@ xlf_status xlf_engine_run_host(xlf_engine* e, const float* h_in, int batch, cons
 }
 
 }  // extern "C"
+
+extern "C" xlf_status xlf_engine_autotune(xlf_engine* e, int batch, int reps, int topk) {
+    return guard([&] {
+        need_ptr(e, "engine");
+        e->tune_report = e->e->autotune(batch, reps, topk);
+    });
+}
+
+extern "C" xlf_status xlf_engine_tune_report(const xlf_engine* e, char* buf, size_t cap, size_t* need) {
+    return guard([&] {
+        need_ptr(e, "engine");
+        put(e->tune_report.empty() ? std::string("[]") : e->tune_report, buf, cap, need);
+    });
+}
 
 extern "C" xlf_status xlf_engine_trace(const xlf_engine* e, int step, unsigned long long* out, size_t cap, size_t* count) {
     return guard([&] {

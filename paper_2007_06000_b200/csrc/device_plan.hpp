@@ -48,6 +48,10 @@ struct StepSpec {
     std::vector<std::string> layers;   // every layer executed by this step
     int out_h = 0, out_w = 0;
     int tile_h = 0, tile_w = 0;
+    int nxb = 1;  // bf16: input staging buffers (2 = next tile's inputs prefetched)
+    int wres = 0;       // bf16: weights resident in shared memory (else streamed through the ring)
+    int ring_slots = 3; // bf16: ring depth when streamed
+    int grid_all = 0;   // bf16: one tile per CTA (grid = tiles) instead of a persistent grid
     int ctile = 0;                     // channel tile of pool-only steps (0 = all)
     int smem_bytes = 0;
     // statistics (per image)
@@ -80,8 +84,17 @@ DevicePlan plan_device(const Graph& g, Partition part, int batch_hint = 1, int s
 // device_plan_bf16.cpp
 bool bf16_mma_ok(const Layer& l);
 void bf16_nblocks(int cout, int* nblocks, int* nb);
-long long layout_bf16(const Graph& g, const StepSpec& s, int th, int tw, struct BParams* P);
+long long layout_bf16(const Graph& g, const StepSpec& s, int th, int tw, struct BParams* P, int nxb = 1, int wres = 0,
+                      int ring_slots = 3);
 bool choose_tile_bf16(const Graph& g, StepSpec& s, int batch_hint, int smem_budget);
+// One configuration of a bf16 step: tile, staging buffers, weight residency /
+// ring depth, shared bytes, and the model's score (SM cycles, lower better).
+struct BCandidate {
+    int th, tw, nxb, wres, slots, smem;
+    double model;
+};
+std::vector<BCandidate> candidates_bf16(const Graph& g, const StepSpec& s, int batch_hint, int smem_budget);
+void apply_candidate(StepSpec& s, const BCandidate& c);
 std::vector<uint16_t> pack_weights_bf16(const Graph& g, const float* flat, size_t count, std::map<std::string, long long>& off);
 
 // Packs reference-layout weights (save_weights stream order, tensor.cpp:64-95)

@@ -2,7 +2,9 @@
 // the device program: per-op MMA/SIMT choice, regions, TMEM columns, shared
 // bytes, and the bf16 weight packing the MMA B operand reads.
 #include <algorithm>
+#include <vector>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 
 #include "bf16_params.hpp"
@@ -33,7 +35,6 @@ Win win(const Layer& l) {
     return {};
 }
 
-constexpr int kChunkBytes = 16 * 1024;
 constexpr int kSlack = 2048;  // contiguous-M tiles may read up to 127 cells past a plane
 
 }  // namespace
@@ -49,7 +50,7 @@ void bf16_nblocks(int cout, int* nblocks, int* nb) {
     *nb = r16(cdiv(n16, *nblocks));
 }
 
-long long layout_bf16(const Graph& g, const StepSpec& s, int th, int tw, BParams* P) {
+long long layout_bf16(const Graph& g, const StepSpec& s, int th, int tw, BParams* P, int nxb, int wres, int ring_slots) {
     const int nops = int(s.ops.size());
     if (nops > kBMaxOps || s.inputs.size() > size_t(kMaxIns)) return -1;
     struct G {
@@ -308,7 +309,46 @@ long long layout_bf16(const Graph& g, const StepSpec& s, int th, int tw, BParams
     const long long bias_bytes = bytes - bias_off;
     bytes = (bytes + 1023) & ~1023LL;
     const long long ring_off = bytes;
-    if (any_mma) bytes += (long long)kRingSlots * kChunkBytes;
+    long long wres_off = 0, wres_bytes = 0;
+    if (any_mma && wres) {
+        wres_off = bytes;
+        for (BOp& o : ops)
+            if (o.kind == BOP_MMA) {
+                o.wofs = int(wres_bytes);
+                wres_bytes += ((long long)o.nblocks * o.ksteps * o.nb * 32 + 127) & ~127LL;
+            }
+        bytes += wres_bytes;
+    } else if (any_mma) {
+        bytes += (long long)ring_slots * kChunkBytes;
+    }
+    // MMA A-operand reads run past their region: contiguous-M ops read whole
+    // 128-row tiles, windowed ops whole 16-row x 8-column blocks shifted by
+    // the taps.  The allocation must cover the furthest read of every region
+    // (into whatever follows it is harmless: those rows are masked).
+    auto read_end = [&](const BOp& o, const BRegion& r) -> long long {
+        const long long nkb = r.c8 * 8 / r.kb_ch;
+        long long last_cell;  // one past the last cell any M tile reads
+        if (o.contig) last_cell = (long long)o.mtiles * 128;
+        else last_cell = (long long)(o.mtiles / o.strips * 16 - 1 + o.kh - 1 + o.d) * r.ext_w + (o.strips * 8 - 1 + o.kw - 1 + o.d) + 1;
+        return r.smem_off + std::max(nkb * r.plane_bytes, (nkb - 1) * r.plane_bytes + last_cell * r.row_bytes);
+    };
+    long long in_read = 0;  // furthest read into the input staging region
+    for (const BOp& o : ops) {
+        if (o.kind != BOP_MMA) continue;
+        const BRegion& r = o.stage == 1 ? ins[size_t(o.xin)].r : bufs[size_t(o.src)];
+        const long long e = read_end(o, r);
+        bytes = std::max(bytes, e);
+        if (o.stage == 1) in_read = std::max(in_read, e);
+    }
+    bytes = (bytes + 127) & ~127LL;
+    // second staging buffer of the block inputs (they sit first, from offset 0)
+    long long in_end = 0;
+    for (const BIn& in : ins) in_end = std::max(in_end, (long long)in.r.smem_off + (long long)(in.r.c8 * 8 / in.r.kb_ch) * in.r.plane_bytes + kSlack);
+    long long xstride = 0;
+    if (nxb == 2) {
+        xstride = (bytes + 1023) & ~1023LL;
+        bytes = xstride + std::max(in_end, in_read);
+    }
     if (P) {
         std::memset(static_cast<void*>(P), 0, sizeof(BParams));
         P->nins = int(ins.size());
@@ -322,11 +362,13 @@ long long layout_bf16(const Graph& g, const StepSpec& s, int th, int tw, BParams
         P->ngroups = int(groups.size());
         for (size_t i = 0; i < groups.size(); ++i) P->groups[i] = groups[i];
         P->bias_off = int(bias_off), P->bias_bytes = int(bias_bytes);
-        P->ring_off = int(ring_off), P->chunk_bytes = kChunkBytes;
+        P->ring_off = int(ring_off), P->chunk_bytes = kChunkBytes, P->ring_slots = ring_slots;
+        P->wres = any_mma && wres, P->wres_off = int(wres_off), P->wres_bytes = int(wres_bytes);
         P->smem_bytes = int(bytes);
         P->ctile = s.ctile;
         P->cgroups = s.ctile ? r8(g.shape_of(s.inputs[0]).channels) / s.ctile : 1;
         P->tmem_cols = pow2_cols(tmem);
+        P->nxb = nxb, P->xstride = int(xstride);
     }
     return bytes;
 }
@@ -354,43 +396,81 @@ bool choose_tile_bf16(const Graph& g, StepSpec& s, int batch_hint, int smem_budg
     return false;
 }
 
-static bool choose_tile_bf16_at(const Graph& g, StepSpec& s, int batch_hint, int smem_budget) {
-    double best = 1e300;
-    int bh = 0, bw = 0, bsm = 0;
-    for (int th = 1; th <= std::min(s.out_h, 32); ++th)
-        for (int tw = 1; tw <= std::min(s.out_w, 32); ++tw) {
-            BParams* P = new BParams;
-            const long long sm = layout_bf16(g, s, th, tw, P);
-            if (sm < 0 || sm > smem_budget) {
-                delete P;
-                continue;
-            }
-            double in_bytes = 0, mma = 0, simt = 0;
-            for (int i = 0; i < P->nins; ++i) in_bytes += double(P->in[i].r.c8) * P->in[i].r.ext_h * P->in[i].r.ext_w * 16;
-            for (int i = 0; i < P->nops; ++i) {
-                const BOp& o = P->ops[i];
-                if (o.kind == BOP_MMA) mma += double(o.mtiles) * 128 * o.nblocks * o.nb * o.ksteps * 16;
-                else simt += double(o.ext_h) * o.ext_w * o.npad * o.kh * o.kw * (o.kind == BOP_SIMT_CONV ? o.cin : 1);
-            }
-            const double out_bytes = double(th) * tw * 2.0 * 256;  // order of magnitude; same for all tiles per pixel
-            const double ctas = double(P->grid_h) * P->grid_w * P->cgroups * std::max(batch_hint, 1);
-            // 228 KB per SM; per CTA: dynamic + static (~3 KB) + 1 KB driver reserve; <= 2 by registers
-            int occ = std::max(1, std::min(2, int((228 * 1024) / (sm + 4096))));
-            if (P->tmem_cols) occ = std::min(occ, 512 / P->tmem_cols);
-            const double waves = std::ceil(ctas / (148.0 * occ));
-            // cycles per CTA ~ bytes/(per-SM HBM share) + MMA (8192 MAC/clk/SM) + SIMT (128 FMA/clk)
-            double wbytes = 0;  // weights each CTA streams from L2 through the ring
-            for (int i = 0; i < P->nops; ++i)
-                if (P->ops[i].kind == BOP_MMA) wbytes += double(P->ops[i].nblocks) * P->ops[i].ksteps * P->ops[i].nb * 32;
-            const double per_cta = (in_bytes + out_bytes) / 24.0 + wbytes / 96.0 + mma / 8192.0 + simt / 128.0 + 1500.0;
-            const double t = waves * per_cta * occ / std::min(double(occ), 2.0);
-            if (t < best * 0.999 || (t <= best * 1.001 && long(th) * tw > long(bh) * bw))
-                best = t, bh = th, bw = tw, bsm = int(sm);
-            delete P;
+// Every feasible configuration of a step, scored by the model below (SM
+// cycles, lower is better), best first.
+//
+// Persistent CTAs (kernels_bf16.cu): each walks tiles; with two staging
+// buffers (nxb = 2) the next tile's inputs load while this one computes.
+// Model: a tile costs load (its input region incl. halo at the per-SM HBM
+// share, ~24 B/cycle) + compute (MMA, SIMT, weights streamed through the ring
+// at ring-bytes per ~2000-cycle L2 round trip, fixed per-unit sync/epilogue
+// latency); nxb = 2 hides the load behind the compute.  `occ` CTAs per SM
+// overlap; HBM bounds the total.  The model only ranks candidates: the engine
+// autotuner (Engine::autotune) measures the top ones on the device.
+std::vector<BCandidate> candidates_bf16(const Graph& g, const StepSpec& s, int batch_hint, int smem_budget) {
+    int force = 0;
+    if (const char* e = std::getenv("XLF_XBUF")) force = std::atoi(e);
+    int force_w = -1;
+    if (const char* e = std::getenv("XLF_WRES")) force_w = std::atoi(e);
+    struct WMode {
+        int wres, slots;
+    };
+    const WMode wmodes[] = {{1, 3}, {0, 3}, {0, 6}};
+    std::vector<BCandidate> out;
+    BParams* P = new BParams;
+    for (int nxb = 1; nxb <= 2; ++nxb)
+        for (const WMode& wm : wmodes) {
+            if (force && nxb != force) continue;
+            if (force_w >= 0 && wm.wres != force_w) continue;
+            for (int th = 1; th <= std::min(s.out_h, 32); ++th)
+                for (int tw = 1; tw <= std::min(s.out_w, 32); ++tw) {
+                    const long long sm = layout_bf16(g, s, th, tw, P, nxb, wm.wres, wm.slots);
+                    if (sm < 0 || sm > smem_budget) continue;
+                    if (wm.wres && !P->wres) continue;  // no MMA op: the ring/resident choice is moot
+                    double in_bytes = 0, mma = 0, simt = 0;
+                    for (int i = 0; i < P->nins; ++i) in_bytes += double(P->in[i].r.c8) * P->in[i].r.ext_h * P->in[i].r.ext_w * 16;
+                    for (int i = 0; i < P->nops; ++i) {
+                        const BOp& o = P->ops[i];
+                        if (o.kind == BOP_MMA) mma += double(o.mtiles) * 128 * o.nblocks * o.nb * o.ksteps * 16;
+                        else simt += double(o.ext_h) * o.ext_w * o.npad * o.kh * o.kw * (o.kind == BOP_SIMT_CONV ? o.cin : 1);
+                    }
+                    double out_bytes = 0;
+                    for (int i = 0; i < P->nops; ++i)
+                        if (P->ops[i].emit) out_bytes += double(th) * tw * P->ops[i].npad * 2;
+                    const double tiles = double(P->grid_h) * P->grid_w * P->cgroups * std::max(batch_hint, 1);
+                    // 228 KB per SM; per CTA: dynamic + static (~4 KB) + 1 KB driver reserve
+                    int occ = std::max(1, std::min(kMaxCtasPerSm, int((228 * 1024) / (sm + 5120))));
+                    if (P->tmem_cols) occ = std::min(occ, 512 / P->tmem_cols);
+                    double wbytes = 0;  // weights each tile streams from L2 through the ring
+                    for (int i = 0; i < P->nops; ++i)
+                        if (P->ops[i].kind == BOP_MMA) wbytes += double(P->ops[i].nblocks) * P->ops[i].ksteps * P->ops[i].nb * 32;
+                    const double wcost = P->wres ? 0.0 : wbytes * 2000.0 / (double(wm.slots) * kChunkBytes);
+                    const double load = in_bytes / 24.0 + 1000.0;
+                    const double compute = out_bytes / 48.0 + wcost + mma / 8192.0 + simt / 128.0 + 800.0 * P->ngroups;
+                    const double per_tile = nxb == 2 ? std::max(load, compute) : load + compute;
+                    const double t = std::max(std::ceil(tiles / (148.0 * occ)) * per_tile,
+                                              tiles * (in_bytes + out_bytes) / (148.0 * 24.0));
+                    out.push_back({th, tw, nxb, P->wres, wm.slots, int(sm), t});
+                }
         }
-    if (!bh) return false;
-    s.tile_h = bh, s.tile_w = bw, s.smem_bytes = bsm;
+    delete P;
+    std::stable_sort(out.begin(), out.end(), [](const BCandidate& a, const BCandidate& b) {
+        if (a.model < b.model * 0.999) return true;
+        if (b.model < a.model * 0.999) return false;
+        return long(a.th) * a.tw > long(b.th) * b.tw;  // ties: the larger tile
+    });
+    return out;
+}
+
+static bool choose_tile_bf16_at(const Graph& g, StepSpec& s, int batch_hint, int smem_budget) {
+    const std::vector<BCandidate> c = candidates_bf16(g, s, batch_hint, smem_budget);
+    if (c.empty()) return false;
+    apply_candidate(s, c.front());
     return true;
+}
+
+void apply_candidate(StepSpec& s, const BCandidate& c) {
+    s.tile_h = c.th, s.tile_w = c.tw, s.smem_bytes = c.smem, s.nxb = c.nxb, s.wres = c.wres, s.ring_slots = c.slots;
 }
 
 // bf16 weights of every MMA-eligible conv: [nblock][tap][cin/8][nb][8].

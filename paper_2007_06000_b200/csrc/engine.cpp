@@ -4,9 +4,11 @@
 #include <cudaTypedefs.h>
 
 #include <algorithm>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <sstream>
+#include <tuple>
 
 #include "bf16_params.hpp"
 #include "common.hpp"
@@ -27,6 +29,7 @@ cudaError_t launch_seeded_nhwc(float* dst, unsigned long long seed, unsigned lon
 // kernels_bf16.cu
 cudaError_t init_fused_bf16();
 cudaError_t launch_fused_bf16(const BParams& P, int batch, cudaStream_t st);
+int occupancy_fused_bf16(int smem_bytes, int tmem_cols);
 cudaError_t launch_nchw_to_nhwc_bf16(const float* src, __nv_bfloat16* dst, int N, int C, int H, int W, int cs, cudaStream_t st);
 cudaError_t launch_nhwc_bf16_to_nchw(const __nv_bfloat16* src, int cs, int coff, float* dst, int N, int C, int H, int W,
                                      cudaStream_t st);
@@ -174,9 +177,8 @@ Engine::Engine(const Graph& g, int device, Partition part, Precision prec, const
     packed.resize(packed.size() + 1024, 0.0f);
     cuda_check(cudaMalloc(&weights_, packed.size() * 4), "cudaMalloc(weights)");
     cuda_check(cudaMemcpy(weights_, packed.data(), packed.size() * 4, cudaMemcpyHostToDevice), "weights H2D");
-    std::map<std::string, long long> woff16;
     if (bf) {
-        std::vector<uint16_t> w16 = pack_weights_bf16(g_, weights, nweights, woff16);
+        std::vector<uint16_t> w16 = pack_weights_bf16(g_, weights, nweights, woff16_);
         w16.resize(w16.size() + 64, 0);
         cuda_check(cudaMalloc(&weights16_, w16.size() * 2), "cudaMalloc(bf16 weights)");
         cuda_check(cudaMemcpy(weights16_, w16.data(), w16.size() * 2, cudaMemcpyHostToDevice), "bf16 weights H2D");
@@ -202,44 +204,144 @@ Engine::Engine(const Graph& g, int device, Partition part, Precision prec, const
             params_[i] = make_params(g_, plan_, s, allocs_, weights_);
             continue;
         }
-        auto P = std::make_unique<BParams>();
-        if (layout_bf16(g_, s, s.tile_h, s.tile_w, P.get()) < 0) fail(ErrorKind::internal, "step " + s.id + ": bf16 layout failed");
-        for (int k = 0; k < P->nins; ++k) {
-            const TensorSlot& t = plan_.tensors.at(s.inputs[size_t(k)]);
-            BIn& in = P->in[k];
-            in.x = reinterpret_cast<const __nv_bfloat16*>(allocs_[size_t(t.alloc)]);
-            in.cstride = t.cstride, in.coff = t.coff;
-            encode_region_map(&P->xmap[k], in.x, t.cstride, t.W, t.H, max_batch, in.r);
-        }
-        for (int k = 0; k < P->nops; ++k) {
-            const OpSpec& os = s.ops[size_t(k)];
-            BOp& o = P->ops[k];
-            if (o.kind == BOP_MMA || o.kind == BOP_SIMT_CONV) {
-                o.wsimt = weights_ + plan_.w_off.at(os.layer);
-                o.bias = weights_ + plan_.b_off.at(os.layer);
-                if (o.kind == BOP_MMA) o.wmma = reinterpret_cast<const __nv_bfloat16*>(weights16_) + woff16.at(os.layer);
-            }
-            if (o.emit) {
-                const TensorSlot& t = plan_.tensors.at(os.layer);
-                o.out = reinterpret_cast<__nv_bfloat16*>(allocs_[size_t(t.alloc)]);
-                o.out_cstride = t.cstride, o.out_coff = t.coff;
-            }
-        }
-        if (std::getenv("XLF_TRACE")) {  // phase stamps of a few CTAs (profiling aid)
-            unsigned long long* tr = nullptr;
-            const size_t n = size_t(kTraceCtas) * kTraceEvents;
-            cuda_check(cudaMalloc(&tr, n * 8), "cudaMalloc(trace)");
-            cuda_check(cudaMemset(tr, 0, n * 8), "cudaMemset(trace)");
-            P->trace = tr;
-            traces_.push_back(tr);
-        }
-        void* dev = nullptr;
-        cuda_check(cudaMalloc(&dev, sizeof(BParams)), "cudaMalloc(step descriptor)");
-        pdevs_.push_back(dev);
-        P->dev_copy = dev;
-        cuda_check(cudaMemcpy(dev, P.get(), sizeof(BParams), cudaMemcpyHostToDevice), "step descriptor H2D");
-        bparams_[i] = std::move(P);
+        bparams_[i] = build_bparams(s);
     }
+}
+
+// Launch descriptor of a bf16 step in its current configuration (tile,
+// staging, weight residency), bound to this engine's tensors and weights,
+// with its device copy.
+std::unique_ptr<BParams> Engine::build_bparams(const StepSpec& s) {
+    auto P = std::make_unique<BParams>();
+    if (layout_bf16(g_, s, s.tile_h, s.tile_w, P.get(), s.nxb, s.wres, s.ring_slots) < 0)
+        fail(ErrorKind::internal, "step " + s.id + ": bf16 layout failed");
+    P->ctas_per_sm = occupancy_fused_bf16(P->smem_bytes, P->tmem_cols);
+    P->grid_all = s.grid_all;
+    if (std::getenv("XLF_TRACE"))
+        std::fprintf(stderr, "[xlf] step %s: tile %dx%d, %d B shared, %d staging buffer(s), weights %s, %d CTA(s)/SM%s\n",
+                     s.id.c_str(), s.tile_h, s.tile_w, P->smem_bytes, P->nxb,
+                     P->wres ? "resident" : (std::to_string(P->ring_slots) + "-slot ring").c_str(), P->ctas_per_sm,
+                     s.grid_all ? ", one tile per CTA" : "");
+    for (int k = 0; k < P->nins; ++k) {
+        const TensorSlot& t = plan_.tensors.at(s.inputs[size_t(k)]);
+        BIn& in = P->in[k];
+        in.x = reinterpret_cast<const __nv_bfloat16*>(allocs_[size_t(t.alloc)]);
+        in.cstride = t.cstride, in.coff = t.coff;
+        encode_region_map(&P->xmap[k], in.x, t.cstride, t.W, t.H, max_batch_, in.r);
+    }
+    for (int k = 0; k < P->nops; ++k) {
+        const OpSpec& os = s.ops[size_t(k)];
+        BOp& o = P->ops[k];
+        if (o.kind == BOP_MMA || o.kind == BOP_SIMT_CONV) {
+            o.wsimt = weights_ + plan_.w_off.at(os.layer);
+            o.bias = weights_ + plan_.b_off.at(os.layer);
+            if (o.kind == BOP_MMA) o.wmma = reinterpret_cast<const __nv_bfloat16*>(weights16_) + woff16_.at(os.layer);
+        }
+        if (o.emit) {
+            const TensorSlot& t = plan_.tensors.at(os.layer);
+            o.out = reinterpret_cast<__nv_bfloat16*>(allocs_[size_t(t.alloc)]);
+            o.out_cstride = t.cstride, o.out_coff = t.coff;
+        }
+    }
+    if (const char* d = std::getenv("XLF_DBG")) P->dbg = std::atoi(d);
+    if (std::getenv("XLF_TRACE")) {  // phase stamps of a few CTAs (profiling aid)
+        unsigned long long* tr = nullptr;
+        const size_t n = size_t(kTraceCtas) * kTraceEvents;
+        cuda_check(cudaMalloc(&tr, n * 8), "cudaMalloc(trace)");
+        cuda_check(cudaMemset(tr, 0, n * 8), "cudaMemset(trace)");
+        P->trace = tr;
+        P->trace_tiles = std::atoi(std::getenv("XLF_TRACE")) == 2;
+        traces_.push_back(tr);
+    }
+    void* dev = nullptr;
+    cuda_check(cudaMalloc(&dev, sizeof(BParams)), "cudaMalloc(step descriptor)");
+    P->dev_copy = dev;
+    cuda_check(cudaMemcpy(dev, P.get(), sizeof(BParams), cudaMemcpyHostToDevice), "step descriptor H2D");
+    return P;
+}
+
+// Measured-time tuner (successor of the reference's
+// model-based tune(), cost_model.cpp:236-294): for every bf16 fused step the
+// `topk` best configurations by the planner's model, each launched both as a
+// persistent grid and one tile per CTA, are timed on the device with CUDA
+// events (`reps` launches after one warm-up, on the engine's own tensors) and
+// the fastest is kept.  Arithmetic does not depend on the configuration, so
+// results stay within the bf16 tolerance whatever is chosen.
+std::string Engine::autotune(int batch, int reps, int topk) {
+    if (prec_ != Precision::bf16) return "[]";
+    if (batch <= 0 || batch > max_batch_) batch = max_batch_;
+    reps = std::max(1, reps), topk = std::max(1, topk);
+    cuda_check(cudaSetDevice(device_), "cudaSetDevice");
+    cudaStream_t st;
+    cuda_check(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking), "cudaStreamCreate(tune)");
+    cudaEvent_t e0, e1;
+    cuda_check(cudaEventCreate(&e0), "cudaEventCreate"), cuda_check(cudaEventCreate(&e1), "cudaEventCreate");
+    std::ostringstream js;
+    js << "[";
+    bool first = true;
+    for (size_t i = 0; i < plan_.steps.size(); ++i) {
+        StepSpec& s = plan_.steps[i];
+        if (s.kind != StepSpec::FUSED || !bparams_[i]) continue;
+        // the model ranks tiles within one staging / weight mode reasonably
+        // but not across modes: keep the best `topk` of every mode
+        std::vector<BCandidate> all = candidates_bf16(g_, s, batch, 227 * 1024 - 4096), cands;
+        std::map<std::tuple<int, int, int>, int> per_mode;
+        for (const BCandidate& c : all)
+            if (per_mode[{c.nxb, c.wres, c.slots}]++ < topk) cands.push_back(c);
+        float best_ms = 1e30f;
+        StepSpec best = s;
+        std::unique_ptr<BParams> bestP;
+        int tried = 0;
+        for (const BCandidate& c : cands)
+            for (int ga = 0; ga < 2; ++ga) {
+                StepSpec t = s;
+                apply_candidate(t, c);
+                t.grid_all = ga;
+                std::unique_ptr<BParams> P = build_bparams(t);
+                if (ga && P->ctas_per_sm * 148LL >= (long long)P->grid_h * P->grid_w * P->cgroups * batch) {
+                    cudaFree(const_cast<void*>(P->dev_copy));
+                    continue;  // persistent grid already covers every tile
+                }
+                if (std::getenv("XLF_TUNE_VERBOSE")) {
+                    std::fprintf(stderr, "[xlf] tune %s: tile %dx%d nxb %d wres %d slots %d grid_all %d smem %d\n", s.id.c_str(), t.tile_h,
+                                 t.tile_w, t.nxb, t.wres, t.ring_slots, t.grid_all, P->smem_bytes);
+                    cuda_check(launch_fused_bf16(*P, batch, st), "autotune probe launch");
+                    cuda_check(cudaStreamSynchronize(st), "autotune probe sync");
+                }
+                cuda_check(launch_fused_bf16(*P, batch, st), "autotune warm-up");
+                cuda_check(cudaEventRecord(e0, st), "cudaEventRecord");
+                for (int r = 0; r < reps; ++r) cuda_check(launch_fused_bf16(*P, batch, st), "autotune launch");
+                cuda_check(cudaEventRecord(e1, st), "cudaEventRecord");
+                cuda_check(cudaEventSynchronize(e1), "cudaEventSynchronize");
+                float ms = 0;
+                cuda_check(cudaEventElapsedTime(&ms, e0, e1), "cudaEventElapsedTime");
+                ms /= float(reps);
+                ++tried;
+                if (ms < best_ms) {
+                    if (bestP) cudaFree(const_cast<void*>(bestP->dev_copy));
+                    best_ms = ms, best = t, bestP = std::move(P);
+                } else {
+                    cudaFree(const_cast<void*>(P->dev_copy));
+                }
+            }
+        if (!bestP) continue;
+        const float model_ms = -1.0f;
+        (void)model_ms;
+        cudaFree(const_cast<void*>(bparams_[i]->dev_copy));
+        s = best;
+        bparams_[i] = std::move(bestP);
+        js << (first ? "" : ",") << "{\"id\":\"" << s.id << "\",\"tried\":" << tried << ",\"us\":" << best_ms * 1000.0f
+           << ",\"tile\":[" << s.tile_h << "," << s.tile_w << "],\"nxb\":" << s.nxb << ",\"wres\":" << s.wres
+           << ",\"ring_slots\":" << s.ring_slots << ",\"grid_all\":" << s.grid_all << ",\"smem_bytes\":" << s.smem_bytes << "}";
+        first = false;
+    }
+    js << "]";
+    cudaEventDestroy(e0), cudaEventDestroy(e1);
+    cudaStreamDestroy(st);
+    // captured forwards hold the old descriptors
+    for (auto& [b, ge] : graphs_) cudaGraphExecDestroy(ge);
+    graphs_.clear();
+    return js.str();
 }
 
 Engine::~Engine() {
@@ -249,7 +351,8 @@ Engine::~Engine() {
     cudaFree(weights_);
     if (weights16_) cudaFree(weights16_);
     for (unsigned long long* p : traces_) cudaFree(p);
-    for (void* p : pdevs_) cudaFree(p);
+    for (auto& P : bparams_)
+        if (P) cudaFree(const_cast<void*>(P->dev_copy));
     cudaFree(staging_);
     if (capture_) cudaStreamDestroy(capture_);
 }

@@ -48,10 +48,14 @@ public:
     // XLF_TRACE=1 only: per-CTA phase stamps of step `index` (bf16 kernels).
     std::vector<unsigned long long> trace(int index) const;
     std::string describe_json() const;
+    // Measured-time tuning of the bf16 fused steps (see engine.cpp); returns
+    // the chosen configurations as JSON.
+    std::string autotune(int batch, int reps, int topk);
     int max_batch() const { return max_batch_; }
 
 private:
     void launch_step(size_t i, int batch, cudaStream_t st);
+    std::unique_ptr<struct BParams> build_bparams(const StepSpec& s);
     const TensorSlot& slot(const std::string& n) const;
 
     Graph g_;
@@ -67,7 +71,7 @@ private:
     std::vector<struct FusedParams> params_;
     std::vector<std::unique_ptr<struct BParams>> bparams_;  // bf16 steps
     std::vector<unsigned long long*> traces_;                // XLF_TRACE buffers
-    std::vector<void*> pdevs_;                               // device copies of the bf16 step descriptors
+    std::map<std::string, long long> woff16_;                // bf16 packed-weight offsets per layer
     void* weights16_ = nullptr;  // bf16 MMA weights
     int esz_ = 4;                // bytes per activation element
     bool s2d_ = false;           // bf16: first conv rewritten on a space-to-depth input

@@ -1,13 +1,18 @@
 // bf16 tensor-core fused-block kernel for sm_100a (tcgen05 + TMEM + TMA).
 //
-// One CTA = (image, output tile).  320 threads in three roles:
-//   warp 8      producer: TMA of the block inputs (one 4-D box per 8-channel
-//               plane, zero fill outside the image) and cp.async.bulk of the
-//               packed weights through a 3-slot ring (full/empty mbarriers);
+// Persistent: grid = 148 x (resident CTAs per SM), capped by the tile count;
+// CTA b walks tiles b, b + gridDim.x, ... (tile = image x channel group x
+// output tile).  352 threads in four roles:
+//   warp E      input producer: TMA of the block inputs (one 4-D box per
+//               K-block, zero fill outside the image = conv padding) into
+//               staging buffer k % nxb; with nxb = 2 tile k+1's inputs load
+//               while tile k computes;
+//   warp 10     weight producer: cp.async.bulk of the packed weights through a
+//               3-slot ring (full/empty mbarriers), running ahead across tiles;
 //   warp 9      MMA issuer: one thread issues tcgen05.mma (M=128, N<=256,
 //               K=16, bf16 x bf16 -> fp32 in TMEM) for every conv "unit"
 //               (op x N block), commits to the ring and to the unit's
-//               accumulator barrier; the warp owns TMEM alloc/dealloc;
+//               accumulator barrier; the warp owns TMEM alloc/dealloc (once);
 //   warps 0-7   epilogue + SIMT ops: tcgen05.ld the accumulator (lane = GEMM
 //               row = output cell), bias + ReLU + halo mask, bf16, and either
 //               keep it on chip (shared "planes" buffer that the next stage's
@@ -16,11 +21,17 @@
 //               here as SIMT code on the same shared planes.
 // Units execute in order; the issuer starts unit u only after every earlier
 // unit's epilogue signalled (its TMEM columns are free and any buffer it
-// reads is written).  See bf16_params.hpp for the shared-memory layout.
+// reads is written); every per-tile barrier flips phase once per tile.
+// Barrier init, TMEM allocation, the descriptor and bias copies happen once
+// per CTA, not per tile.  See bf16_params.hpp for the shared-memory layout.
 #include <cuda.h>
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <cstdlib>
 
 #include "bf16_params.hpp"
 #include "umma.cuh"
@@ -31,15 +42,24 @@ namespace {
 
 using namespace umma;
 
-constexpr int kCompute = 256;                 // warps 0-7: epilogue + SIMT ops
-constexpr int kBThreads = kCompute + 64;      // warp 8: producer, warp 9: MMA issuer
+constexpr int kCompute = kEpiWarps * 32;      // warps 0..kEpiWarps-1: epilogue + SIMT ops
+constexpr int kBThreads = kCompute + 96;      // then: input producer, MMA issuer, weight producer
+constexpr int kWarpX = kEpiWarps, kWarpMma = kEpiWarps + 1, kWarpW = kEpiWarps + 2;
+constexpr int kHalves = kCompute / 128;       // epilogue warp groups splitting the accumulator columns
 
 struct BTile {
     int n, ty, tx, oy0, ox0, c0;
 };
 
-__device__ __forceinline__ void stamp(const BParams& P, int ev) {
-    if (P.trace && blockIdx.y == 0 && blockIdx.z == 0 && blockIdx.x < kTraceCtas && ev < kTraceEvents) {
+// Trace stamps of the first tile of CTAs 0..kTraceCtas-1 (k = tile ordinal of the CTA).
+__device__ __forceinline__ void stamp(const BParams& P, int ev, int k = 0) {
+    if (P.trace && P.trace_tiles && ev == kTrEnd && k < kTraceEvents && blockIdx.x < kTraceCtas) {
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        P.trace[blockIdx.x * kTraceEvents + k] = t;
+        return;
+    }
+    if (P.trace && !P.trace_tiles && k == 2 && blockIdx.x < kTraceCtas && ev < kTraceEvents) {  // a steady-state tile
         unsigned long long t;
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
         P.trace[blockIdx.x * kTraceEvents + ev] = t;
@@ -48,42 +68,106 @@ __device__ __forceinline__ void stamp(const BParams& P, int ev) {
 
 __device__ __forceinline__ void named_sync_compute() { asm volatile("bar.sync 1, %0;\n" ::"n"(kCompute) : "memory"); }
 
+// Epilogue-side wait: ONE thread polls the mbarrier, the other compute warps
+// block in a hardware named barrier (no issue slots).  Eight warps polling a
+// try_wait loop issued a third of all instructions of the kernel and starved
+// the co-resident CTA's epilogue (ncu, profiles/r1_ncu_summary.md).
+__device__ __forceinline__ void compute_wait(uint64_t* bar, uint32_t parity) {
+    if (threadIdx.x == 0) mbar_sleep_wait(bar, parity);
+    named_sync_compute();
+}
+
 __device__ __forceinline__ const BRegion& src_region(const BParams& P, const BOp& op, int which) {
     return op.stage == 1 ? P.in[op.xin].r : P.bufs[which];
 }
 
-// ------------------------------------------------------------------ producer
+// The region an op reads, with a stage-1 (block input) region moved to the
+// staging buffer of the current tile.
+__device__ __forceinline__ BRegion src_region_at(const BParams& P, const BOp& op, int which, int xdelta) {
+    BRegion R = src_region(P, op, which);
+    if (op.stage == 1) R.smem_off += xdelta;
+    return R;
+}
 
-__device__ void producer(const BParams& P, const CUtensorMap* xmaps, uint8_t* smem, const BTile& t, uint64_t* bar_x,
-                         uint64_t* ring_full, uint64_t* ring_empty) {
+// Tile tau of the persistent walk: image-major, then channel group, rows, columns.
+__device__ __forceinline__ BTile tile_at(const BParams& P, int tau) {
+    const int per_img = P.grid_h * P.grid_w * P.cgroups, per_cg = P.grid_h * P.grid_w;
+    BTile t;
+    t.n = tau / per_img;
+    int r = tau - t.n * per_img;
+    const int cg = r / per_cg;
+    r -= cg * per_cg;
+    t.ty = r / P.grid_w;
+    t.tx = r - t.ty * P.grid_w;
+    t.oy0 = t.ty * P.tile_h;
+    t.ox0 = t.tx * P.tile_w;
+    t.c0 = cg * P.ctile;
+    return t;
+}
+
+// ------------------------------------------------------------------ producers
+
+// Block inputs of every tile of this CTA into staging buffer k % nxb; a buffer
+// is refilled once the epilogue released it (x_free, after the tile's last unit).
+__device__ void x_producer(const BParams& P, const CUtensorMap* xmaps, uint8_t* smem, int total, uint64_t* bar_x,
+                           uint64_t* x_free) {
     uint32_t bytes = 0;
     for (int k = 0; k < P.nins; ++k) bytes += uint32_t(P.in[k].r.c8) * uint32_t(P.in[k].r.ext_h * P.in[k].r.ext_w * 16);
-    stamp(P, kTrStart);
-    mbar_expect_tx(bar_x, bytes);
-    for (int k = 0; k < P.nins; ++k) {
-        const BIn& in = P.in[k];
-        const int x0 = t.ox0 * in.org_mul - in.org_sub, y0 = t.oy0 * in.org_mul - in.org_sub;
-        const int nkb = in.r.c8 * 8 / in.r.kb_ch;
-        for (int kb = 0; kb < nkb; ++kb)
-            tma_load_4d(smem + in.r.smem_off + kb * in.r.plane_bytes, &xmaps[k], in.coff + t.c0 + kb * in.r.kb_ch, x0, y0, t.n,
-                        bar_x);
+    const int nxb = P.nxb;
+    int k = 0;
+    for (int tau = blockIdx.x; tau < total; tau += gridDim.x, ++k) {
+        const BTile t = tile_at(P, tau);
+        const int b = nxb == 2 ? (k & 1) : 0, use = nxb == 2 ? (k >> 1) : k;
+        if (use > 0) mbar_sleep_wait(&x_free[b], (use - 1) & 1);
+        stamp(P, kTrStart, k);
+        mbar_expect_tx(&bar_x[b], bytes);
+        uint8_t* xb = smem + b * P.xstride;
+        for (int i = 0; i < P.nins; ++i) {
+            const BIn& in = P.in[i];
+            const int x0 = t.ox0 * in.org_mul - in.org_sub, y0 = t.oy0 * in.org_mul - in.org_sub;
+            const int nkb = in.r.c8 * 8 / in.r.kb_ch;
+            for (int kb = 0; kb < nkb; ++kb)
+                tma_load_4d(xb + in.r.smem_off + kb * in.r.plane_bytes, &xmaps[i], in.coff + t.c0 + kb * in.r.kb_ch, x0, y0, t.n,
+                            &bar_x[b]);
+        }
+        stamp(P, kTrXIssued, k);
     }
-    stamp(P, kTrXIssued);
-    // weights, in exactly the order the issuer consumes them
-    int c = 0;
-    for (int gi = 0; gi < P.ngroups; ++gi) {
-        const BGroup& G = P.groups[gi];
-        if (!G.mma) continue;
-        for (int i = G.op0; i < G.op1; ++i) {
+}
+
+// Weights, in exactly the order the issuer consumes them, tile after tile
+// (the ring runs ahead into the next tile while this one's epilogue runs).
+__device__ void w_producer(const BParams& P, uint8_t* smem, int total, uint64_t* ring_full, uint64_t* ring_empty, uint64_t* bar_w) {
+    if (P.wres) {  // resident: every op's packed weights once, then done
+        uint32_t total_b = 0;
+        for (int i = 0; i < P.nops; ++i)
+            if (P.ops[i].kind == BOP_MMA) total_b += uint32_t(P.ops[i].nblocks * P.ops[i].ksteps * P.ops[i].nb * 32);
+        mbar_expect_tx(bar_w, total_b);
+        for (int i = 0; i < P.nops; ++i) {
             const BOp& op = P.ops[i];
-            const __nv_bfloat16* wb = op.wmma + size_t(G.nbi) * op.ksteps * op.nb * 16;
-            for (int s0 = 0; s0 < op.ksteps; s0 += op.chunk_steps, ++c) {
-                const int steps = min(op.chunk_steps, op.ksteps - s0);
-                const int slot = c % kRingSlots;
-                if (c >= kRingSlots) mbar_wait(&ring_empty[slot], ((c / kRingSlots) - 1) & 1);
-                const uint32_t b = uint32_t(steps) * op.nb * 32;
-                mbar_expect_tx(&ring_full[slot], b);
-                bulk_g2s(smem + P.ring_off + slot * P.chunk_bytes, wb + size_t(s0) * op.nb * 16, b, &ring_full[slot]);
+            if (op.kind != BOP_MMA) continue;
+            const uint32_t b = uint32_t(op.nblocks * op.ksteps * op.nb * 32);
+            for (uint32_t o = 0; o < b; o += 65536)  // pieces of <= 64 KB
+                bulk_g2s(smem + P.wres_off + op.wofs + o, reinterpret_cast<const uint8_t*>(op.wmma) + o, min(65536u, b - o), bar_w);
+        }
+        return;
+    }
+    const int slots = P.ring_slots;
+    int c = 0;
+    for (int tau = blockIdx.x; tau < total; tau += gridDim.x) {
+        for (int gi = 0; gi < P.ngroups; ++gi) {
+            const BGroup& G = P.groups[gi];
+            if (!G.mma) continue;
+            for (int i = G.op0; i < G.op1; ++i) {
+                const BOp& op = P.ops[i];
+                const __nv_bfloat16* wb = op.wmma + size_t(G.nbi) * op.ksteps * op.nb * 16;
+                for (int s0 = 0; s0 < op.ksteps; s0 += op.chunk_steps, ++c) {
+                    const int steps = min(op.chunk_steps, op.ksteps - s0);
+                    const int slot = c % slots;
+                    if (c >= slots) mbar_sleep_wait(&ring_empty[slot], ((c / slots) - 1) & 1);
+                    const uint32_t b = uint32_t(steps) * op.nb * 32;
+                    mbar_expect_tx(&ring_full[slot], b);
+                    bulk_g2s(smem + P.ring_off + slot * P.chunk_bytes, wb + size_t(s0) * op.nb * 16, b, &ring_full[slot]);
+                }
             }
         }
     }
@@ -96,9 +180,9 @@ __device__ void producer(const BParams& P, const CUtensorMap* xmaps, uint8_t* sm
 // field is hoisted into locals first and the descriptors are advanced by
 // precomputed deltas (in 16-byte units of the start-address field), so one MMA
 // costs a handful of uniform-datapath instructions.
-__device__ __forceinline__ void issue_op(const BParams& P, const BOp& op, uint32_t sbase, uint32_t tmem, int& c, uint64_t* ring_full,
-                                         uint64_t* ring_empty) {
-    const BRegion& R = src_region(P, op, op.src);
+__device__ __forceinline__ void issue_op(const BParams& P, const BOp& op, int nbi, uint32_t sbase, uint32_t tmem, int& c,
+                                         uint64_t* ring_full, uint64_t* ring_empty, int xdelta) {
+    const BRegion R = src_region_at(P, op, op.src, xdelta);
     const int mode = R.mode, plane = R.plane_bytes, rowb = R.row_bytes, ew = R.ext_w;
     const int ksteps = op.ksteps, csteps = op.chunk_steps, nb = op.nb, mtiles = op.mtiles, strips = op.strips;
     const int kw = op.kw, d = op.d, contig = op.contig, c16 = op.cin_pad / 16;
@@ -109,6 +193,8 @@ __device__ __forceinline__ void issue_op(const BParams& P, const BOp& op, uint32
     const uint32_t sbo = contig ? 8 * rowb : ew * rowb;
     const uint64_t bdesc0 = sdesc(0, nb * 16, 128, kNoSwizzle);
     const uint32_t ring0 = sbase + P.ring_off, chunkb = P.chunk_bytes;
+    const int slots = P.ring_slots, wres = P.wres;
+    const uint32_t wbase = sbase + P.wres_off + op.wofs + uint32_t(nbi * ksteps * nb * 32);
     // start-field deltas (16-byte units)
     const uint32_t d_mt = contig ? (128 * rowb) >> 4 : (8 * rowb) >> 4;       // next M tile / next strip
     const uint32_t d_rb = ((16 * ew - 8 * (strips - 1)) * rowb) >> 4;          // last strip -> next 16-row block
@@ -117,12 +203,17 @@ __device__ __forceinline__ void issue_op(const BParams& P, const BOp& op, uint32
     const uint32_t tm0 = tmem + op.tcol;
     int kc = 0, dx = 0;
     uint32_t acc = 0;
-    for (int s0 = 0; s0 < ksteps; s0 += csteps, ++c) {
+    for (int s0 = 0; s0 < ksteps; s0 += csteps) {
         const int steps = min(csteps, ksteps - s0);
-        const int slot = c % kRingSlots;
-        mbar_wait(&ring_full[slot], (c / kRingSlots) & 1);
-        fence_after();
-        uint64_t bd = bdesc0 + ((ring0 + slot * chunkb) >> 4);
+        const int slot = wres ? 0 : c % slots;
+        uint64_t bd;
+        if (wres) {
+            bd = bdesc0 + ((wbase + uint32_t(s0 * nb * 32)) >> 4);
+        } else {
+            mbar_wait(&ring_full[slot], (c / slots) & 1);
+            fence_after();
+            bd = bdesc0 + ((ring0 + slot * chunkb) >> 4);
+        }
         for (int sl = 0; sl < steps; ++sl) {
             uint32_t kofs;  // K16 step kc inside the region's K-blocks, 16-byte units
             if (mode == kPlanes) kofs = (kc * 2 * plane) >> 4;
@@ -132,8 +223,7 @@ __device__ __forceinline__ void issue_op(const BParams& P, const BOp& op, uint32
             uint32_t tcur = tm0;
             int st = 0;
             for (int mt = 0; mt < mtiles; ++mt) {
-                if (elect_one()) mma_bf16(tcur, a, bd, idesc, acc);
-                __syncwarp();
+                if (!(P.dbg & 4)) mma_bf16(tcur, a, bd, idesc, acc);
                 tcur += nb;
                 if (contig || ++st < strips) a += d_mt;
                 else st = 0, a += d_rb;
@@ -146,27 +236,40 @@ __device__ __forceinline__ void issue_op(const BParams& P, const BOp& op, uint32
                 if (++dx == kw) dx = 0, a_tap += d_row;
             }
         }
-        if (elect_one()) commit(&ring_empty[slot]);
-        __syncwarp();
+        if (!wres) commit(&ring_empty[slot]), ++c;
     }
 }
 
-__device__ void issuer(const BParams& P, uint8_t* smem, uint32_t tmem, uint64_t* bar_x, uint64_t* ring_full,
-                       uint64_t* ring_empty, uint64_t* acc_full, uint64_t* unit_done) {
-    mbar_wait(bar_x, 0);
-    stamp(P, kTrXLanded);
-    int c = 0;
+__device__ void issuer(const BParams& P, uint8_t* smem, uint32_t tmem, int total, uint64_t* bar_x, uint64_t* ring_full,
+                       uint64_t* ring_empty, uint64_t* acc_full, uint64_t* unit_done, uint64_t* bar_w) {
+    int c = 0, k = 0;
     const uint32_t sbase = smem_u32(smem);
-    for (int gi = 0; gi < P.ngroups; ++gi) {
-        if (gi > 0) mbar_wait(&unit_done[gi - 1], 0);  // earlier groups' epilogues done (in order)
-        const BGroup& G = P.groups[gi];
-        if (!G.mma) continue;
-        fence_after();
-        if (gi < 2) stamp(P, 29 + 2 * gi);  // group's inputs ready, issue starts
-        for (int i = G.op0; i < G.op1; ++i) issue_op(P, P.ops[i], sbase, tmem, c, ring_full, ring_empty);
-        if (gi < 2) stamp(P, 30 + 2 * gi);  // group issued
-        if (elect_one()) commit(&acc_full[gi]);
-        __syncwarp();
+    const int G = P.ngroups, nxb = P.nxb;
+    // SIMT-only steps: nothing to issue, and the epilogue (not gated by any
+    // accumulator) may run tiles ahead, so the issuer must not track phases.
+    bool any = false;
+    for (int gi = 0; gi < G; ++gi) any |= P.groups[gi].mma != 0;
+    if (!any) return;
+    if (P.wres) mbar_sleep_wait(bar_w, 0);
+    for (int tau = blockIdx.x; tau < total; tau += gridDim.x, ++k) {
+        const int b = nxb == 2 ? (k & 1) : 0, use = nxb == 2 ? (k >> 1) : k;
+        const int xdelta = b * P.xstride;
+        mbar_sleep_wait(&bar_x[b], use & 1);
+        stamp(P, kTrXLanded, k);
+        for (int gi = 0; gi < G; ++gi) {
+            // earlier units' epilogues done, in order; unit 0 waits for the
+            // previous tile's last unit (TMEM columns and shared buffers free)
+            if (gi > 0) mbar_sleep_wait(&unit_done[gi - 1], k & 1);
+            else if (k > 0) mbar_sleep_wait(&unit_done[G - 1], (k - 1) & 1);
+            const BGroup& Gr = P.groups[gi];
+            if (!Gr.mma) continue;
+            fence_after();
+            if (gi < 2) stamp(P, 29 + 2 * gi, k);  // group's inputs ready, issue starts
+            if (!(P.dbg & 8))
+                for (int i = Gr.op0; i < Gr.op1; ++i) issue_op(P, P.ops[i], Gr.nbi, sbase, tmem, c, ring_full, ring_empty, xdelta);
+            if (gi < 2) stamp(P, 30 + 2 * gi, k);  // group issued
+            commit(&acc_full[gi]);
+        }
     }
 }
 
@@ -184,6 +287,7 @@ struct EpiOp {
     uint8_t* buf;           // shared buffer base (planes), or null
     __nv_bfloat16* out;
     uint32_t bias_s;        // shared address of the op's fp32 bias (MMA ops)
+    const float* bias_p;    // the same, as a generic pointer
 };
 
 __device__ __forceinline__ EpiOp epi_op(const BParams& P, const BOp& op, uint8_t* smem) {
@@ -197,8 +301,9 @@ __device__ __forceinline__ EpiOp epi_op(const BParams& P, const BOp& op, uint8_t
         const BRegion& B = P.bufs[op.buf];
         e.buf = smem + B.smem_off, e.buf_ew = B.ext_w, e.buf_plane = B.plane_bytes;
     }
-    e.out = op.out;
+    e.out = (P.dbg & 1) ? nullptr : op.out;
     e.bias_s = op.bias_smem >= 0 ? smem_u32(smem + op.bias_smem) : 0u;
+    e.bias_p = op.bias_smem >= 0 ? reinterpret_cast<const float*>(smem + op.bias_smem) : nullptr;
     return e;
 }
 
@@ -226,7 +331,7 @@ __device__ __forceinline__ CellDst cell_dst(const EpiOp& e, const BTile& t, int 
     d.inside = gy >= 0 && gy < e.H && gx >= 0 && gx < e.W;
     d.sbuf = e.buf ? e.buf + (r * e.buf_ew + c) * 16 : nullptr;
     d.gdst = nullptr;
-    if (e.emit && valid && d.inside && owns(e, t, gy, gx))
+    if (e.emit && e.out && valid && d.inside && owns(e, t, gy, gx))
         d.gdst = e.out + ((size_t(t.n) * e.H + gy) * e.W + gx) * e.out_cstride + e.out_coff + t.c0;
     return d;
 }
@@ -266,11 +371,10 @@ __device__ __forceinline__ void put8(const CellDst& d, int ch, const float* v8, 
     if (d.gdst) *reinterpret_cast<uint4*>(d.gdst + ch) = u;
 }
 
-// Bias + ReLU + store of N accumulator columns (channels ch0 ...), unrolled.
-template <int N>
-__device__ __forceinline__ void finish_cols(const EpiOp& e, const CellDst& d, int ch0, float* v) {
+// Bias + ReLU + store of 16 accumulator columns (channels ch0 ...), unrolled.
+__device__ __forceinline__ void finish16(const EpiOp& e, const CellDst& d, int ch0, float* v) {
 #pragma unroll
-    for (int j = 0; j < N; j += 8) {
+    for (int j = 0; j < 16; j += 8) {
         if (ch0 + j >= e.c8end) break;
         const float4 b0 = lds_f4(e.bias_s + uint32_t(ch0 + j) * 4u);
         const float4 b1 = lds_f4(e.bias_s + uint32_t(ch0 + j + 4) * 4u);
@@ -283,16 +387,52 @@ __device__ __forceinline__ void finish_cols(const EpiOp& e, const CellDst& d, in
     }
 }
 
+// 32 accumulator columns: the TMEM load is issued first and the 32 bias
+// values are fetched from shared memory while it is in flight (the bias
+// fetch after the wait was the epilogue's main stall, ncu short_sb).
+__device__ __forceinline__ void finish32(const EpiOp& e, const CellDst& d, bool valid, int ch0, uint32_t ta) {
+    uint32_t r[32];
+    tmem_ld32_issue(ta, r);
+    const float4* bp = reinterpret_cast<const float4*>(e.bias_p + ch0);
+    float4 b[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) b[j] = bp[j];
+    tmem_ld_wait32(r);
+    if (!valid) return;
+#pragma unroll
+    for (int j = 0; j < 32; j += 8) {
+        if (ch0 + j >= e.c8end) break;
+        if (j == 16) {
+#pragma unroll
+            for (int q = 0; q < 4; ++q) b[q] = bp[4 + q];
+        }
+        float x[8];
+        const float4 b0 = b[(j & 15) / 4], b1 = b[(j & 15) / 4 + 1];
+        x[0] = __uint_as_float(r[j]) + b0.x, x[1] = __uint_as_float(r[j + 1]) + b0.y;
+        x[2] = __uint_as_float(r[j + 2]) + b0.z, x[3] = __uint_as_float(r[j + 3]) + b0.w;
+        x[4] = __uint_as_float(r[j + 4]) + b1.x, x[5] = __uint_as_float(r[j + 5]) + b1.y;
+        x[6] = __uint_as_float(r[j + 6]) + b1.z, x[7] = __uint_as_float(r[j + 7]) + b1.w;
+        if (e.relu)
+#pragma unroll
+            for (int k = 0; k < 8; ++k) x[k] = fmaxf(x[k], 0.0f);
+        put8(d, ch0 + j, x, e);
+    }
+}
+
 // Accumulator -> bias/ReLU/mask -> bf16 -> shared buffer and/or HBM.  Thread
-// (row = tid % 128) owns TMEM lane `row` = GEMM row = one cell; the two
-// warp groups split the accumulator columns in 32-column slices.
+// (row = tid % 128) owns TMEM lane `row` = GEMM row = one cell.  With two
+// warp groups, narrow ops (<= 32 columns) split the M tiles between them,
+// wider ones split the columns in 32-column slices.
 __device__ void epilogue_mma(const BParams& P, const BOp& op, int nbi, uint8_t* smem, uint32_t tmem, const BTile& t) {
     const EpiOp e = epi_op(P, op, smem);
     const int mtiles = op.mtiles, contig = op.contig, ext_w = op.ext_w, ext_h = op.ext_h, strips = op.strips, nb = op.nb;
-    const int row = threadIdx.x & 127, half = threadIdx.x >> 7;
+    const int row = threadIdx.x & 127, half = kHalves > 1 ? int(threadIdx.x >> 7) : 0;
     const uint32_t tbase = tmem + op.tcol + (uint32_t(row & ~31) << 16);
     const int chbase = nbi * nb;
-    for (int mt = 0; mt < mtiles; ++mt) {
+    const bool split_m = kHalves > 1 && nb <= 32;
+    const int mt0 = split_m ? half : 0, mstep = split_m ? kHalves : 1;
+    const int col0 = split_m ? 0 : half * 32, cstep = split_m ? 32 : 32 * kHalves;
+    for (int mt = mt0; mt < mtiles; mt += mstep) {
         int r, c;
         bool valid;
         if (contig) {
@@ -305,16 +445,14 @@ __device__ void epilogue_mma(const BParams& P, const BOp& op, int nbi, uint8_t* 
             valid = r < ext_h && c < ext_w;
         }
         const CellDst d = cell_dst(e, t, r, c, valid);
-        for (int col = half * 32; col < nb; col += 64) {
+        for (int col = col0; col < nb; col += cstep) {
             const uint32_t ta = tbase + mt * nb + col;
             if (nb - col >= 32) {
-                float v[32];
-                tmem_ld32(ta, v);
-                if (valid) finish_cols<32>(e, d, chbase + col, v);
+                finish32(e, d, valid, chbase + col, ta);
             } else {
                 float v[16];
                 tmem_ld16(ta, v);
-                if (valid) finish_cols<16>(e, d, chbase + col, v);
+                if (valid) finish16(e, d, chbase + col, v);
             }
         }
     }
@@ -451,9 +589,9 @@ __device__ void simt_add(const EpiOp& e, const BRegion& A, const BRegion& B, uin
     }
 }
 
-__device__ void simt_pool_add(const BParams& P, const BOp& op, uint8_t* smem, const BTile& t) {
+__device__ void simt_pool_add(const BParams& P, const BOp& op, uint8_t* smem, const BTile& t, int xdelta) {
     const EpiOp e = epi_op(P, op, smem);
-    const BRegion& R = src_region(P, op, op.src);
+    const BRegion R = src_region_at(P, op, op.src, xdelta);
     if (op.kind == BOP_ADD) {
         simt_add(e, R, P.bufs[op.src2], smem, op, t);
         return;
@@ -465,9 +603,9 @@ __device__ void simt_pool_add(const BParams& P, const BOp& op, uint8_t* smem, co
 
 // Direct conv for what the tensor-core path does not take (stride != 1,
 // groups, Cin not a multiple of 16).  fp32 accumulate.
-__device__ void simt_conv(const BParams& P, const BOp& op, uint8_t* smem, const BTile& t) {
+__device__ void simt_conv(const BParams& P, const BOp& op, uint8_t* smem, const BTile& t, int xdelta) {
     const EpiOp e = epi_op(P, op, smem);
-    const RegionView R = region_view(src_region(P, op, op.src), smem);
+    const RegionView R = region_view(src_region_at(P, op, op.src, xdelta), smem);
     const int ext_w = op.ext_w, kh_ = op.kh, kw_ = op.kw, stride = op.stride, dd = op.d, cout = op.cout;
     const int ncell = op.ext_h * ext_w, c8 = op.npad / 8;
     const int cin_g = op.cin / op.group, cout_g = cout / op.group, cp4 = (cout + 3) & ~3;
@@ -504,54 +642,55 @@ __device__ void simt_conv(const BParams& P, const BOp& op, uint8_t* smem, const 
     }
 }
 
-__global__ void __launch_bounds__(kBThreads, 2) fused_bf16_kernel(const __grid_constant__ BParams Pg) {
+__global__ void __launch_bounds__(kBThreads, kMaxCtasPerSm) fused_bf16_kernel(const __grid_constant__ BParams Pg, int batch) {
     extern __shared__ __align__(1024) uint8_t smem[];
-    __shared__ __align__(8) uint64_t bar_x, ring_full[kRingSlots], ring_empty[kRingSlots], acc_full[kBMaxUnits],
+    __shared__ __align__(8) uint64_t bar_x[2], x_free[2], ring_full[kRingMax], ring_empty[kRingMax], acc_full[kBMaxUnits],
         unit_done[kBMaxUnits];
     __shared__ uint32_t tmem_slot;
     // The descriptor lives in the kernel-parameter constant bank; the op loops
     // index it with run-time op numbers, and indexed constant loads that miss
     // the small constant cache stall for hundreds of cycles.  The epilogue
     // warps work from a shared-memory copy, pulled from the device copy with
-    // one bulk copy; the producer (few loads, latency-critical X issue) and
+    // one bulk copy; the producers (few loads, latency-critical X issue) and
     // the MMA issuer (uniform indices) read the bank, which also holds the
     // tensor maps TMA reads.
     __shared__ __align__(64) BParams Ps;
-    __shared__ __align__(8) uint64_t bar_p;
+    __shared__ __align__(8) uint64_t bar_p, bar_w;
     const int warp = __shfl_sync(0xffffffffu, int(threadIdx.x >> 5), 0), lane = threadIdx.x & 31;  // provably warp-uniform
-    BTile t;  // from the parameter bank (uniform, non-indexed loads)
-    t.n = blockIdx.y;
-    t.ty = blockIdx.x / Pg.grid_w;
-    t.tx = blockIdx.x - t.ty * Pg.grid_w;
-    t.oy0 = t.ty * Pg.tile_h;
-    t.ox0 = t.tx * Pg.tile_w;
-    t.c0 = blockIdx.z * Pg.ctile;
+    const int total = Pg.grid_h * Pg.grid_w * Pg.cgroups * batch;
     if (threadIdx.x == 0) {
         mbar_init(&bar_p, 1);
-        mbar_init(&bar_x, 1);
-        for (int i = 0; i < kRingSlots; ++i) mbar_init(&ring_full[i], 1), mbar_init(&ring_empty[i], 1);
+        for (int i = 0; i < 2; ++i) mbar_init(&bar_x[i], 1), mbar_init(&x_free[i], 1);
+        for (int i = 0; i < kRingMax; ++i) mbar_init(&ring_full[i], 1), mbar_init(&ring_empty[i], 1);
+        mbar_init(&bar_w, 1);
         for (int i = 0; i < Pg.ngroups; ++i) mbar_init(&acc_full[i], 1), mbar_init(&unit_done[i], 1);
         mbar_fence_init();
         mbar_expect_tx(&bar_p, uint32_t(sizeof(BParams)));
         bulk_g2s(&Ps, Pg.dev_copy, uint32_t(sizeof(BParams)), &bar_p);
     }
-    if (warp == 9 && Pg.tmem_cols) tmem_alloc(&tmem_slot, Pg.tmem_cols);
+    if (warp == kWarpMma && Pg.tmem_cols) tmem_alloc(&tmem_slot, Pg.tmem_cols);
     fence_before();
     __syncthreads();
     fence_after();
     const BParams& P = Ps;
     const uint32_t tmem = Pg.tmem_cols ? tmem_slot : 0;
 
-    if (warp == 8) {
-        if (lane == 0) producer(Pg, Pg.xmap, smem, t, &bar_x, ring_full, ring_empty);  // starts before Ps lands
-    } else if (warp == 9) {
-        // Whole warp, warp-uniform control flow, one elected lane issues; the
-        // op fields come from the parameter bank with uniform indices, so the
-        // descriptor arithmetic stays on the uniform datapath (no R2UR per MMA).
-        issuer(Pg, smem, tmem, &bar_x, ring_full, ring_empty, acc_full, unit_done);
+    if (warp == kWarpX) {
+        if (lane == 0) x_producer(Pg, Pg.xmap, smem, total, bar_x, x_free);  // starts before Ps lands
+    } else if (warp == kWarpW) {
+        if (lane == 0) w_producer(Pg, smem, total, ring_full, ring_empty, &bar_w);
+    } else if (warp == kWarpMma) {
+        // One thread issues everything: a per-MMA elect.sync + __syncwarp in a
+        // warp-wide loop costs ~175 cycles per tcgen05.mma against ~50 for a
+        // single-thread loop (tests/probes/tcgen05_rate.cu) -- and these
+        // convolutions are many small MMAs (N 16..256, K 16).
+        // (elect.sync, not lane == 0: the compiler then knows one thread is
+        // active and moves descriptors to uniform registers without the
+        // per-MMA ELECT waterfall it emits for a lane-predicated branch)
+        if (elect_one()) issuer(Pg, smem, tmem, total, bar_x, ring_full, ring_empty, acc_full, unit_done, &bar_w);
         __syncwarp();
     } else {
-        mbar_wait(&bar_p, 0);
+        compute_wait(&bar_p, 0);
         // biases of the MMA ops -> shared memory (read by every epilogue)
         for (int i = 0; i < P.nops; ++i) {
             const BOp& op = P.ops[i];
@@ -560,31 +699,41 @@ __global__ void __launch_bounds__(kBThreads, 2) fused_bf16_kernel(const __grid_c
             for (int k = threadIdx.x; k < op.npad; k += kCompute) dst[k] = __ldg(op.bias + k);
         }
         named_sync_compute();
-        bool have_x = false;
-        for (int gi = 0; gi < P.ngroups; ++gi) {
-            const BGroup& G = P.groups[gi];
-            if (G.mma) {
-                mbar_sleep_wait(&acc_full[gi], 0);
-                if (threadIdx.x == 0) stamp(P, kTrUnit + 2 * gi);
-                fence_after();
-                for (int i = G.op0; i < G.op1; ++i) epilogue_mma(P, P.ops[i], G.nbi, smem, tmem, t);
-            } else {
-                const BOp& op = P.ops[G.op0];
-                if (!have_x) mbar_wait(&bar_x, 0), have_x = true;
-                if (op.kind == BOP_SIMT_CONV) simt_conv(P, op, smem, t);
-                else simt_pool_add(P, op, smem, t);
+        const int nxb = P.nxb;
+        int k = 0;
+        for (int tau = blockIdx.x; tau < total; tau += gridDim.x, ++k) {
+            const BTile t = tile_at(P, tau);
+            const int b = nxb == 2 ? (k & 1) : 0, use = nxb == 2 ? (k >> 1) : k;
+            const int xdelta = b * P.xstride;
+            bool have_x = false;
+            for (int gi = 0; gi < P.ngroups; ++gi) {
+                const BGroup& G = P.groups[gi];
+                if (G.mma) {
+                    compute_wait(&acc_full[gi], k & 1);
+                    if (threadIdx.x == 0) stamp(P, kTrUnit + 2 * gi, k);
+                    fence_after();
+                    if (!(P.dbg & 2))
+                        for (int i = G.op0; i < G.op1; ++i) epilogue_mma(P, P.ops[i], G.nbi, smem, tmem, t);
+                } else {
+                    const BOp& op = P.ops[G.op0];
+                    if (!have_x) compute_wait(&bar_x[b], use & 1), have_x = true;
+                    if (op.kind == BOP_SIMT_CONV) simt_conv(P, op, smem, t, xdelta);
+                    else simt_pool_add(P, op, smem, t, xdelta);
+                }
+                fence_async_smem();  // epilogue-written buffers are read by later MMAs (async proxy)
+                fence_before();
+                named_sync_compute();
+                if (threadIdx.x == 0) mbar_arrive(&unit_done[gi]), stamp(P, kTrUnit + 2 * gi + 1, k);
             }
-            fence_async_smem();  // epilogue-written buffers are read by later MMAs (async proxy)
-            fence_before();
-            named_sync_compute();
-            if (threadIdx.x == 0) mbar_arrive(&unit_done[gi]), stamp(P, kTrUnit + 2 * gi + 1);
+            // every unit of this tile is done (MMAs complete, SIMT reads
+            // finished): its staging buffer may be refilled
+            if (threadIdx.x == 0) mbar_arrive(&x_free[b]), stamp(P, kTrEnd, k);
         }
     }
     fence_before();
     __syncthreads();
     fence_after();
-    if (warp == 9 && Pg.tmem_cols) tmem_free(tmem, Pg.tmem_cols);
-    if (threadIdx.x == 0) stamp(P, kTrEnd);
+    if (warp == kWarpMma && Pg.tmem_cols) tmem_free(tmem, Pg.tmem_cols);
 }
 
 // ----------------------------------------------------------------- layout kernels (bf16)
@@ -696,11 +845,43 @@ int grid_b(long long work) {
 
 cudaError_t init_fused_bf16() {
     // 227 KB per block minus the static part (barriers + the BParams copy)
-    return cudaFuncSetAttribute(fused_bf16_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024 - 4096);
+    cudaError_t e = cudaFuncSetAttribute(fused_bf16_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024 - 4096);
+    if (e != cudaSuccess) return e;
+    return cudaFuncSetAttribute(fused_bf16_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+}
+
+// Resident CTAs per SM: the occupancy API, cross-checked against the
+// shared-memory arithmetic (228 KB per SM, 1 KB reserved per CTA, the static
+// barriers + descriptor copy) and the launch bound of 2.  Over-subscribing is
+// harmless (tiles are independent), under-subscribing halves the overlap.
+int occupancy_fused_bf16(int smem_bytes, int tmem_cols) {
+    int n = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, fused_bf16_kernel, kBThreads, size_t(smem_bytes)) != cudaSuccess) n = 0;
+    cudaFuncAttributes a{};
+    cudaFuncGetAttributes(&a, fused_bf16_kernel);
+    const int by_smem = int((228 * 1024) / (size_t(smem_bytes) + a.sharedSizeBytes + 1024));
+    const int mine = std::max(1, std::min(kMaxCtasPerSm, by_smem));
+    if (std::getenv("XLF_TRACE"))
+        std::fprintf(stderr, "[xlf] occupancy: api %d, smem arithmetic %d (dynamic %d + static %zu)\n", n, mine, smem_bytes,
+                     size_t(a.sharedSizeBytes));
+    int occ = std::max(n, mine);
+    // TMEM: 512 columns per SM; a CTA whose tcgen05.alloc cannot be served
+    // waits for another CTA to exit, i.e. serialises behind a persistent one
+    if (tmem_cols > 0) occ = std::min(occ, std::max(1, 512 / tmem_cols));
+    if (const char* f = std::getenv("XLF_CTAS")) occ = std::max(1, std::min(occ, std::atoi(f)));  // profiling aid
+    return occ;
 }
 
 cudaError_t launch_fused_bf16(const BParams& P, int batch, cudaStream_t st) {
-    fused_bf16_kernel<<<dim3(P.grid_h * P.grid_w, batch, P.cgroups), kBThreads, P.smem_bytes, st>>>(P);
+    const long long tiles = (long long)P.grid_h * P.grid_w * P.cgroups * batch;
+    int sms = 148;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+    const long long grid = P.grid_all ? tiles : std::min<long long>(tiles, (long long)sms * std::max(1, P.ctas_per_sm));
+    if (grid < 1) return cudaSuccess;
+    if (P.trace && std::getenv("XLF_TRACE"))
+        std::fprintf(stderr, "[xlf] launch: %lld tiles, grid %lld x %d threads, %d B dynamic shared\n", tiles, grid, kBThreads,
+                     P.smem_bytes);
+    fused_bf16_kernel<<<dim3(unsigned(grid)), kBThreads, P.smem_bytes, st>>>(P, batch);
     return cudaGetLastError();
 }
 

@@ -73,3 +73,26 @@ def test_bf16_uses_tensor_cores():
     g = X.Graph(graph_text("fire"))
     plan = X.device_plan(g, "b200", 32, "bf16")
     assert [s["tag"] for s in plan["steps"]] == ["split"]
+
+
+@pytest.mark.parametrize("name", ["fire", "inc3a", "merge", "straight"])
+def test_bf16_autotuned_within_tolerance(name):
+    """The measured-time tuner changes tiles / staging / weight residency /
+    grid shape only: results stay within the bf16 tolerance."""
+    import torch
+    text = graph_text(name)
+    og = O.load_graph(text)
+    w = O.seeded_weights(og, 3)
+    x = O.seeded_batch(og, 5, 4)
+    g = X.Graph(text)
+    e = X.Engine(g, O.flat_weights(og, w), "b200", "bf16", max_batch=4)
+    e.set_input(torch.from_numpy(x).cuda())
+    e.forward(4)
+    chosen = e.autotune(4, reps=2, topk=3)
+    assert chosen and all(c["us"] > 0 for c in chosen)
+    e.set_input(torch.from_numpy(x).cuda())
+    e.forward(4)
+    ref = O.run_batch(og, x, w, og.outputs)
+    for o in og.outputs:
+        err = O.normwise(e.read(o, 4).cpu().numpy(), ref[o])
+        assert err <= TOL, (name, o, err)
