@@ -28,7 +28,7 @@ cudaError_t launch_seeded_nhwc(float* dst, unsigned long long seed, unsigned lon
                                int cs, cudaStream_t st);
 // kernels_bf16.cu
 cudaError_t init_fused_bf16();
-cudaError_t launch_fused_bf16(const BParams& P, int batch, cudaStream_t st);
+cudaError_t launch_fused_bf16(const BParams& P, int batch, cudaStream_t st, int n0 = 0);
 int occupancy_fused_bf16(int smem_bytes, int tmem_cols);
 cudaError_t launch_nchw_to_nhwc_bf16(const float* src, __nv_bfloat16* dst, int N, int C, int H, int W, int cs, cudaStream_t st);
 cudaError_t launch_nhwc_bf16_to_nchw(const __nv_bfloat16* src, int cs, int coff, float* dst, int N, int C, int H, int W,
@@ -354,6 +354,11 @@ Engine::~Engine() {
     for (auto& P : bparams_)
         if (P) cudaFree(const_cast<void*>(P->dev_copy));
     cudaFree(staging_);
+    if (out_staging_) cudaFree(out_staging_);
+    if (copy_in_) {
+        cudaStreamDestroy(copy_in_), cudaStreamDestroy(copy_out_);
+        for (cudaEvent_t ev : chunk_ev_) cudaEventDestroy(ev);
+    }
     if (capture_) cudaStreamDestroy(capture_);
 }
 
@@ -392,6 +397,40 @@ void Engine::set_input_seeded(const std::string& name, uint64_t seed, uint64_t f
                    "seeded fill");
     else
         cuda_check(launch_seeded_nhwc(allocs_[size_t(t.alloc)], seed, first_image, batch, t.C, t.H, t.W, t.cstride, st), "seeded fill");
+}
+
+bool Engine::range_capable() const {
+    if (esz_ != 2) return false;
+    for (size_t i = 0; i < plan_.steps.size(); ++i)
+        if (plan_.steps[i].kind != StepSpec::FUSED || !bparams_[i]) return false;
+    return true;
+}
+
+// Images [n0, n0 + count) only (bf16 plans made of fused kernels: the kernels
+// take the image offset; see run_host).
+void Engine::forward_range(int n0, int count, cudaStream_t st) {
+    if (n0 < 0 || count < 1 || n0 + count > max_batch_) fail(ErrorKind::validation, "image range out of bounds");
+    if (!range_capable()) fail(ErrorKind::validation, "forward_range needs a bf16 plan of fused kernels only");
+    const long long key = -(1LL + (long long)n0 * 65536 + count);  // negative keys: ranges (positive: whole batches)
+    auto it = graphs_.find(int(key));
+    if (it == graphs_.end()) {
+        if (!capture_) cuda_check(cudaStreamCreateWithFlags(&capture_, cudaStreamNonBlocking), "capture stream");
+        cudaGraph_t graph;
+        cuda_check(cudaStreamBeginCapture(capture_, cudaStreamCaptureModeThreadLocal), "begin capture");
+        try {
+            for (size_t i = 0; i < plan_.steps.size(); ++i)
+                cuda_check(launch_fused_bf16(*bparams_[i], count, capture_, n0), "fused block (bf16, range)");
+        } catch (...) {
+            cudaStreamEndCapture(capture_, &graph);
+            throw;
+        }
+        cuda_check(cudaStreamEndCapture(capture_, &graph), "end capture");
+        cudaGraphExec_t exec;
+        cuda_check(cudaGraphInstantiate(&exec, graph, 0), "graph instantiate");
+        cudaGraphDestroy(graph);
+        it = graphs_.emplace(int(key), exec).first;
+    }
+    cuda_check(cudaGraphLaunch(it->second, st), "graph launch");
 }
 
 void Engine::launch_step(size_t i, int batch, cudaStream_t st) {
@@ -485,19 +524,68 @@ void Engine::read_output_nchw(const std::string& name, float* d, int batch, cuda
         cuda_check(launch_nhwc_to_nchw(allocs_[size_t(t.alloc)], t.cstride, t.coff, d, batch, t.C, t.H, t.W, st), "nhwc_to_nchw");
 }
 
+// End to end from host memory.  bf16 plans made only of fused kernels are
+// pipelined over chunks of images: the H2D copy of chunk c+1 (copy stream)
+// overlaps the layout conversion + forward of chunk c (caller's stream), and
+// each chunk's result is read back as soon as it is ready (second copy
+// stream), so the PCIe transfer -- the e2e bound for 224x224x3 fp32 inputs --
+// hides the compute.  Other plans: H2D, forward, D2H in sequence.
 void Engine::run_host(const float* h_in, int batch, const std::string& out_name, float* h_out, cudaStream_t st) {
     if (batch < 1 || batch > max_batch_) fail(ErrorKind::validation, "batch out of range");
     cuda_check(cudaSetDevice(device_), "cudaSetDevice");
     const GraphInput& in = g_.inputs[0];
-    const size_t n_in = size_t(in_shape_.elements()) * batch;  // user-facing NCHW input
-    cuda_check(cudaMemcpyAsync(staging_, h_in, n_in * 4, cudaMemcpyHostToDevice, st), "H2D input");
-    set_input_nchw(in.name, staging_, batch, st);
-    forward(batch, st, true);
+    const size_t img_in = size_t(in_shape_.elements());  // user-facing NCHW input, per image
     const TensorSlot& t = slot(out_name);
-    const size_t n_out = size_t(t.C) * t.H * t.W * batch;
-    if (n_out > staging_floats_) fail(ErrorKind::validation, "output larger than the staging buffer");
-    read_output_nchw(out_name, staging_, batch, st);
-    cuda_check(cudaMemcpyAsync(h_out, staging_, n_out * 4, cudaMemcpyDeviceToHost, st), "D2H output");
+    const size_t img_out = size_t(t.C) * t.H * t.W;
+    if (img_out * batch > staging_floats_) fail(ErrorKind::validation, "output larger than the staging buffer");
+    int chunks = 4;
+    if (const char* c = std::getenv("XLF_E2E_CHUNKS")) chunks = std::max(1, std::atoi(c));
+    chunks = std::min(chunks, batch);
+    if (!range_capable() || chunks == 1) {
+        cuda_check(cudaMemcpyAsync(staging_, h_in, img_in * batch * 4, cudaMemcpyHostToDevice, st), "H2D input");
+        set_input_nchw(in.name, staging_, batch, st);
+        forward(batch, st, true);
+        read_output_nchw(out_name, staging_, batch, st);
+        cuda_check(cudaMemcpyAsync(h_out, staging_, img_out * batch * 4, cudaMemcpyDeviceToHost, st), "D2H output");
+        cuda_check(cudaStreamSynchronize(st), "sync");
+        return;
+    }
+    if (!copy_in_) {
+        cuda_check(cudaStreamCreateWithFlags(&copy_in_, cudaStreamNonBlocking), "copy stream");
+        cuda_check(cudaStreamCreateWithFlags(&copy_out_, cudaStreamNonBlocking), "copy stream");
+        for (int k = 0; k < 2 * kMaxChunks; ++k) cuda_check(cudaEventCreateWithFlags(&chunk_ev_[k], cudaEventDisableTiming), "event");
+        cuda_check(cudaMalloc(&out_staging_, staging_floats_ * 4), "cudaMalloc(output staging)");
+    }
+    chunks = std::min(chunks, int(kMaxChunks));
+    const TensorSlot& xin = slot(in.name);
+    for (int c = 0; c < chunks; ++c) {
+        const int n0 = int((long long)batch * c / chunks), n1 = int((long long)batch * (c + 1) / chunks), cnt = n1 - n0;
+        float* dst = staging_ + size_t(n0) * img_in;
+        cuda_check(cudaMemcpyAsync(dst, h_in + size_t(n0) * img_in, size_t(cnt) * img_in * 4, cudaMemcpyHostToDevice, copy_in_),
+                   "H2D input chunk");
+        cuda_check(cudaEventRecord(chunk_ev_[c], copy_in_), "event");
+        cuda_check(cudaStreamWaitEvent(st, chunk_ev_[c], 0), "wait H2D");
+        __nv_bfloat16* x = reinterpret_cast<__nv_bfloat16*>(allocs_[size_t(xin.alloc)]);
+        if (s2d_)
+            cuda_check(launch_s2d_bf16(dst, 0, 0, x + size_t(n0) * xin.H * xin.W * xin.cstride, cnt, in_shape_.channels, in_shape_.height,
+                                       in_shape_.width, xin.cstride, st),
+                       "space-to-depth input chunk");
+        else
+            cuda_check(launch_nchw_to_nhwc_bf16(dst, x + size_t(n0) * xin.H * xin.W * xin.cstride, cnt, xin.C, xin.H, xin.W,
+                                                xin.cstride, st),
+                       "nchw_to_nhwc chunk");
+        forward_range(n0, cnt, st);
+        const __nv_bfloat16* o = reinterpret_cast<const __nv_bfloat16*>(allocs_[size_t(t.alloc)]);
+        cuda_check(launch_nhwc_bf16_to_nchw(o + size_t(n0) * t.H * t.W * t.cstride, t.cstride, t.coff, out_staging_ + size_t(n0) * img_out,
+                                            cnt, t.C, t.H, t.W, st),
+                   "nhwc_to_nchw chunk");
+        cuda_check(cudaEventRecord(chunk_ev_[kMaxChunks + c], st), "event");
+        cuda_check(cudaStreamWaitEvent(copy_out_, chunk_ev_[kMaxChunks + c], 0), "wait chunk");
+        cuda_check(cudaMemcpyAsync(h_out + size_t(n0) * img_out, out_staging_ + size_t(n0) * img_out, size_t(cnt) * img_out * 4,
+                                   cudaMemcpyDeviceToHost, copy_out_),
+                   "D2H output chunk");
+    }
+    cuda_check(cudaStreamSynchronize(copy_out_), "sync");
     cuda_check(cudaStreamSynchronize(st), "sync");
 }
 

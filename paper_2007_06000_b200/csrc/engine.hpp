@@ -34,6 +34,9 @@ public:
     void set_input_seeded(const std::string& name, uint64_t seed, uint64_t first_image, int batch, cudaStream_t st);
     // All steps for `batch` images (replays a captured CUDA graph when use_graph).
     void forward(int batch, cudaStream_t st, bool use_graph = true);
+    // Images [n0, n0 + count) of every step (bf16 plans of fused kernels only).
+    void forward_range(int n0, int count, cudaStream_t st);
+    bool range_capable() const;
     // One step only (per-block timing / run_fused_block).
     void run_step(int index, int batch, cudaStream_t st);
     // NHWC arena -> NCHW fp32.
@@ -76,7 +79,11 @@ private:
     int esz_ = 4;                // bytes per activation element
     bool s2d_ = false;           // bf16: first conv rewritten on a space-to-depth input
     TensorShape in_shape_;       // user-facing (NCHW) input shape
-    std::map<int, cudaGraphExec_t> graphs_;
+    std::map<int, cudaGraphExec_t> graphs_;  // key > 0: whole batch; < 0: image range (forward_range)
+    static constexpr int kMaxChunks = 16;     // run_host pipelining
+    cudaStream_t copy_in_ = nullptr, copy_out_ = nullptr;
+    cudaEvent_t chunk_ev_[2 * kMaxChunks] = {};
+    float* out_staging_ = nullptr;
 };
 
 std::vector<float> seeded_weights(const Graph& g, uint64_t seed);  // tensor.cpp:42-62 semantics

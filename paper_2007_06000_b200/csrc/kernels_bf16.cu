@@ -90,11 +90,12 @@ __device__ __forceinline__ BRegion src_region_at(const BParams& P, const BOp& op
 }
 
 // Tile tau of the persistent walk: image-major, then channel group, rows, columns.
-__device__ __forceinline__ BTile tile_at(const BParams& P, int tau) {
+__device__ __forceinline__ BTile tile_at(const BParams& P, int tau, int n0) {
     const int per_img = P.grid_h * P.grid_w * P.cgroups, per_cg = P.grid_h * P.grid_w;
     BTile t;
-    t.n = tau / per_img;
-    int r = tau - t.n * per_img;
+    const int ni = tau / per_img;
+    int r = tau - ni * per_img;
+    t.n = n0 + ni;  // absolute image (a launch may cover images [n0, n0 + batch))
     const int cg = r / per_cg;
     r -= cg * per_cg;
     t.ty = r / P.grid_w;
@@ -109,14 +110,14 @@ __device__ __forceinline__ BTile tile_at(const BParams& P, int tau) {
 
 // Block inputs of every tile of this CTA into staging buffer k % nxb; a buffer
 // is refilled once the epilogue released it (x_free, after the tile's last unit).
-__device__ void x_producer(const BParams& P, const CUtensorMap* xmaps, uint8_t* smem, int total, uint64_t* bar_x,
+__device__ void x_producer(const BParams& P, const CUtensorMap* xmaps, uint8_t* smem, int total, int n0, uint64_t* bar_x,
                            uint64_t* x_free) {
     uint32_t bytes = 0;
     for (int k = 0; k < P.nins; ++k) bytes += uint32_t(P.in[k].r.c8) * uint32_t(P.in[k].r.ext_h * P.in[k].r.ext_w * 16);
     const int nxb = P.nxb;
     int k = 0;
     for (int tau = blockIdx.x; tau < total; tau += gridDim.x, ++k) {
-        const BTile t = tile_at(P, tau);
+        const BTile t = tile_at(P, tau, n0);
         const int b = nxb == 2 ? (k & 1) : 0, use = nxb == 2 ? (k >> 1) : k;
         if (use > 0) mbar_sleep_wait(&x_free[b], (use - 1) & 1);
         stamp(P, kTrStart, k);
@@ -642,7 +643,7 @@ __device__ void simt_conv(const BParams& P, const BOp& op, uint8_t* smem, const 
     }
 }
 
-__global__ void __launch_bounds__(kBThreads, kMaxCtasPerSm) fused_bf16_kernel(const __grid_constant__ BParams Pg, int batch) {
+__global__ void __launch_bounds__(kBThreads, kMaxCtasPerSm) fused_bf16_kernel(const __grid_constant__ BParams Pg, int batch, int n0) {
     extern __shared__ __align__(1024) uint8_t smem[];
     __shared__ __align__(8) uint64_t bar_x[2], x_free[2], ring_full[kRingMax], ring_empty[kRingMax], acc_full[kBMaxUnits],
         unit_done[kBMaxUnits];
@@ -676,7 +677,7 @@ __global__ void __launch_bounds__(kBThreads, kMaxCtasPerSm) fused_bf16_kernel(co
     const uint32_t tmem = Pg.tmem_cols ? tmem_slot : 0;
 
     if (warp == kWarpX) {
-        if (lane == 0) x_producer(Pg, Pg.xmap, smem, total, bar_x, x_free);  // starts before Ps lands
+        if (lane == 0) x_producer(Pg, Pg.xmap, smem, total, n0, bar_x, x_free);  // starts before Ps lands
     } else if (warp == kWarpW) {
         if (lane == 0) w_producer(Pg, smem, total, ring_full, ring_empty, &bar_w);
     } else if (warp == kWarpMma) {
@@ -702,7 +703,7 @@ __global__ void __launch_bounds__(kBThreads, kMaxCtasPerSm) fused_bf16_kernel(co
         const int nxb = P.nxb;
         int k = 0;
         for (int tau = blockIdx.x; tau < total; tau += gridDim.x, ++k) {
-            const BTile t = tile_at(P, tau);
+            const BTile t = tile_at(P, tau, n0);
             const int b = nxb == 2 ? (k & 1) : 0, use = nxb == 2 ? (k >> 1) : k;
             const int xdelta = b * P.xstride;
             bool have_x = false;
@@ -872,7 +873,7 @@ int occupancy_fused_bf16(int smem_bytes, int tmem_cols) {
     return occ;
 }
 
-cudaError_t launch_fused_bf16(const BParams& P, int batch, cudaStream_t st) {
+cudaError_t launch_fused_bf16(const BParams& P, int batch, cudaStream_t st, int n0) {
     const long long tiles = (long long)P.grid_h * P.grid_w * P.cgroups * batch;
     int sms = 148;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
@@ -881,7 +882,7 @@ cudaError_t launch_fused_bf16(const BParams& P, int batch, cudaStream_t st) {
     if (P.trace && std::getenv("XLF_TRACE"))
         std::fprintf(stderr, "[xlf] launch: %lld tiles, grid %lld x %d threads, %d B dynamic shared\n", tiles, grid, kBThreads,
                      P.smem_bytes);
-    fused_bf16_kernel<<<dim3(unsigned(grid)), kBThreads, P.smem_bytes, st>>>(P, batch);
+    fused_bf16_kernel<<<dim3(unsigned(grid)), kBThreads, P.smem_bytes, st>>>(P, batch, n0);
     return cudaGetLastError();
 }
 

@@ -96,3 +96,22 @@ def test_bf16_autotuned_within_tolerance(name):
     for o in og.outputs:
         err = O.normwise(e.read(o, 4).cpu().numpy(), ref[o])
         assert err <= TOL, (name, o, err)
+
+
+@pytest.mark.parametrize("chunks", ["1", "3", "4"])
+def test_bf16_run_host_pipelined_matches_device_path(chunks, monkeypatch):
+    """run_host pipelines H2D / compute / D2H over image chunks (bf16 plans):
+    the result equals the device-resident forward of the same inputs."""
+    import torch
+    monkeypatch.setenv("XLF_E2E_CHUNKS", chunks)
+    text = graph_text("squeezenet11")
+    og = O.load_graph(text)
+    w = O.seeded_weights(og, 42)
+    x = O.seeded_batch(og, 7, 6)
+    g = X.Graph(text)
+    e = X.Engine(g, O.flat_weights(og, w), "b200", "bf16", max_batch=6)
+    host = e.run_host(x, "pool10")
+    e.set_input(torch.from_numpy(x).cuda())
+    e.forward(6)
+    dev = e.read("pool10", 6).cpu().numpy()
+    assert np.array_equal(host, dev)
