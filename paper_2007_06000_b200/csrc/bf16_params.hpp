@@ -61,6 +61,7 @@ struct BOp {
     int out_cstride, out_coff;
     int tcol;       // MMA: first TMEM column of this op inside its group
     int wofs;       // MMA, resident weights: byte offset of the op's packed weights in the weight region
+    int gap;        // MMA: global-average-pool epilogue (column sums per tile, no output store)
     int bias_smem;  // byte offset of the op's bias copy in shared memory (-1: none)
 };
 
@@ -115,6 +116,10 @@ struct alignas(64) BParams {
     // into shared memory ONCE per (persistent) CTA at wres_off (wres_bytes)
     // instead of being streamed through the ring for every tile.
     int wres, wres_off, wres_bytes;
+    // gap steps: per-tile column sums (fp32, npad per tile) accumulate in
+    // shared memory at gap_off and are written to gap_part[image][tile][c].
+    int gap_off;
+    float* gap_part;
     int smem_bytes, tmem_cols;
     int ctile, cgroups;  // channel tiling of pool-only steps (0 = all channels)
     // Persistent execution: each CTA walks tiles blockIdx.x, +gridDim.x, ...

@@ -413,7 +413,7 @@ void fill_stats(const Graph& g, const DevicePlan& plan, StepSpec& s) {
             s.macs += double(l.out_shape->elements()) * double(l.conv->macs_per_output());
             s.bytes_algorithmic += double(l.conv->weight_count() + l.conv->bias_count()) * es;
         }
-        if (op.emit) s.bytes_algorithmic += double(l.out_shape->elements()) * es;
+        if (op.emit) s.bytes_algorithmic += double(g.shape_of(s.gap_out.empty() ? op.layer : s.gap_out).elements()) * es;
     }
     if (s.kind != StepSpec::FUSED) {
         s.bytes_algorithmic += double(g.shape_of(s.layers[0]).elements()) * es;
@@ -470,6 +470,26 @@ DevicePlan plan_device(const Graph& g, Partition part, int batch_hint, int smem_
         StepSpec s = step_for_block(g, b);
         if (s.kind == StepSpec::FUSED && !tile(s)) {
             if (!b.fused()) fail(ErrorKind::infeasible, "layer " + b.members[0] + " does not fit shared memory at any tile");
+            // bf16: conv -> global average pool runs as one kernel whose
+            // epilogue reduces (the conv output never reaches HBM).
+            if (bf16 && part == Partition::b200 && s.ops.size() == 2 && s.ops[0].stage == 1 && s.ops[1].stage == 2) {
+                const Layer& c = *g.find_layer(s.ops[0].layer);
+                const Layer& p = *g.find_layer(s.ops[1].layer);
+                if (c.kind == LayerKind::conv && p.kind == LayerKind::pool && p.pool->kind == PoolKind::avg && p.pool->pad == 0 &&
+                    p.pool->kernel == c.out_shape->height && p.pool->kernel == c.out_shape->width && bf16_mma_ok(c) &&
+                    !g.is_output(c.name) && g.consumers_of(c.name).size() == 1) {
+                    StepSpec t = s;
+                    t.tag = "conv+gap";
+                    t.ops.resize(1);
+                    t.ops[0].staged = false, t.ops[0].emit = true, t.ops[0].own_only = false;
+                    t.gap_out = p.name;
+                    t.out_h = c.out_shape->height, t.out_w = c.out_shape->width;
+                    if (tile(t)) {
+                        steps.push_back(t);
+                        continue;
+                    }
+                }
+            }
             // Fused block infeasible on chip: run its members as singletons.
             for (const std::string& m : b.members) {
                 FusionBlock one;
@@ -535,7 +555,7 @@ DevicePlan plan_device(const Graph& g, Partition part, int batch_hint, int smem_
     for (const StepSpec& s : steps) {
         if (s.kind != StepSpec::FUSED) materialized.insert(s.layers[0]);
         for (const OpSpec& op : s.ops)
-            if (op.emit) materialized.insert(op.layer);
+            if (op.emit) materialized.insert(s.gap_out.empty() ? op.layer : s.gap_out);
     }
     // Concat elision (B200): every input of a concat that is consumed by the
     // concat alone becomes a channel-offset view of the concat's allocation.

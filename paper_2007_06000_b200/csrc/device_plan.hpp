@@ -52,6 +52,11 @@ struct StepSpec {
     int wres = 0;       // bf16: weights resident in shared memory (else streamed through the ring)
     int ring_slots = 3; // bf16: ring depth when streamed
     int grid_all = 0;   // bf16: one tile per CTA (grid = tiles) instead of a persistent grid
+    // bf16 conv + global average pool (SqueezeNet conv10 -> pool10): the
+    // step's single conv op never stores its output; its epilogue reduces
+    // every tile over its cells and the pooled layer `gap_out` (1x1) is
+    // finished by a small reduction kernel.  Tiles are over the conv output.
+    std::string gap_out;
     int ctile = 0;                     // channel tile of pool-only steps (0 = all)
     int smem_bytes = 0;
     // statistics (per image)

@@ -300,6 +300,13 @@ long long layout_bf16(const Graph& g, const StepSpec& s, int th, int tw, BParams
         tmem = std::max(tmem, gcols);
     }
     if (groups.size() > size_t(kBMaxUnits)) return -1;
+    long long gap_off = 0;
+    if (!s.gap_out.empty()) {
+        if (nops != 1 || ops[0].kind != BOP_MMA) return -1;
+        ops[0].gap = 1;
+        gap_off = (bytes + 15) & ~15LL;
+        bytes = gap_off + 4LL * ops[0].nblocks * ops[0].nb * 4;  // column sums, one slot per TMEM lane quadrant
+    }
     // shared copy of the biases the epilogues read
     const long long bias_off = bytes;
     for (BOp& o : ops) {
@@ -369,6 +376,7 @@ long long layout_bf16(const Graph& g, const StepSpec& s, int th, int tw, BParams
         P->cgroups = s.ctile ? r8(g.shape_of(s.inputs[0]).channels) / s.ctile : 1;
         P->tmem_cols = pow2_cols(tmem);
         P->nxb = nxb, P->xstride = int(xstride);
+        P->gap_off = int(gap_off);
     }
     return bytes;
 }
@@ -415,7 +423,7 @@ std::vector<BCandidate> candidates_bf16(const Graph& g, const StepSpec& s, int b
     struct WMode {
         int wres, slots;
     };
-    const WMode wmodes[] = {{1, 3}, {0, 3}, {0, 6}};
+    const WMode wmodes[] = {{1, 3}, {0, 3}, {0, 6}, {0, 8}};
     std::vector<BCandidate> out;
     BParams* P = new BParams;
     for (int nxb = 1; nxb <= 2; ++nxb)

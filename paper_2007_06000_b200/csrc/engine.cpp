@@ -29,6 +29,8 @@ cudaError_t launch_seeded_nhwc(float* dst, unsigned long long seed, unsigned lon
 // kernels_bf16.cu
 cudaError_t init_fused_bf16();
 cudaError_t launch_fused_bf16(const BParams& P, int batch, cudaStream_t st, int n0 = 0);
+cudaError_t launch_gap_finish_bf16(const float* part, int tiles, int np, float scale, __nv_bfloat16* out, int cs, int coff, int C, int n0,
+                                   int N, cudaStream_t st);
 int occupancy_fused_bf16(int smem_bytes, int tmem_cols);
 cudaError_t launch_nchw_to_nhwc_bf16(const float* src, __nv_bfloat16* dst, int N, int C, int H, int W, int cs, cudaStream_t st);
 cudaError_t launch_nhwc_bf16_to_nchw(const __nv_bfloat16* src, int cs, int coff, float* dst, int N, int C, int H, int W,
@@ -238,10 +240,20 @@ std::unique_ptr<BParams> Engine::build_bparams(const StepSpec& s) {
             if (o.kind == BOP_MMA) o.wmma = reinterpret_cast<const __nv_bfloat16*>(weights16_) + woff16_.at(os.layer);
         }
         if (o.emit) {
-            const TensorSlot& t = plan_.tensors.at(os.layer);
+            const TensorSlot& t = plan_.tensors.at(s.gap_out.empty() ? os.layer : s.gap_out);
             o.out = reinterpret_cast<__nv_bfloat16*>(allocs_[size_t(t.alloc)]);
             o.out_cstride = t.cstride, o.out_coff = t.coff;
         }
+    }
+    if (!s.gap_out.empty()) {  // per-tile column sums, [image][tile][npad] fp32
+        const size_t need = size_t(max_batch_) * P->grid_h * P->grid_w * P->ops[0].npad;
+        auto& buf = gap_parts_[s.id];
+        if (buf.second < need) {
+            if (buf.first) cudaFree(buf.first);
+            cuda_check(cudaMalloc(&buf.first, need * 4), "cudaMalloc(gap partials)");
+            buf.second = need;
+        }
+        P->gap_part = buf.first;
     }
     if (const char* d = std::getenv("XLF_DBG")) P->dbg = std::atoi(d);
     if (std::getenv("XLF_TRACE")) {  // phase stamps of a few CTAs (profiling aid)
@@ -302,12 +314,6 @@ std::string Engine::autotune(int batch, int reps, int topk) {
                     cudaFree(const_cast<void*>(P->dev_copy));
                     continue;  // persistent grid already covers every tile
                 }
-                if (std::getenv("XLF_TUNE_VERBOSE")) {
-                    std::fprintf(stderr, "[xlf] tune %s: tile %dx%d nxb %d wres %d slots %d grid_all %d smem %d\n", s.id.c_str(), t.tile_h,
-                                 t.tile_w, t.nxb, t.wres, t.ring_slots, t.grid_all, P->smem_bytes);
-                    cuda_check(launch_fused_bf16(*P, batch, st), "autotune probe launch");
-                    cuda_check(cudaStreamSynchronize(st), "autotune probe sync");
-                }
                 cuda_check(launch_fused_bf16(*P, batch, st), "autotune warm-up");
                 cuda_check(cudaEventRecord(e0, st), "cudaEventRecord");
                 for (int r = 0; r < reps; ++r) cuda_check(launch_fused_bf16(*P, batch, st), "autotune launch");
@@ -317,6 +323,10 @@ std::string Engine::autotune(int batch, int reps, int topk) {
                 cuda_check(cudaEventElapsedTime(&ms, e0, e1), "cudaEventElapsedTime");
                 ms /= float(reps);
                 ++tried;
+                if (std::getenv("XLF_TUNE_VERBOSE"))
+                    std::fprintf(stderr, "[xlf] tune %s: tile %dx%d nxb %d wres %d slots %d grid_all %d smem %d: %.1f us (model %.0f)\n",
+                                 s.id.c_str(), t.tile_h, t.tile_w, t.nxb, t.wres, t.ring_slots, t.grid_all, P->smem_bytes, ms * 1000.0f,
+                                 c.model);
                 if (ms < best_ms) {
                     if (bestP) cudaFree(const_cast<void*>(bestP->dev_copy));
                     best_ms = ms, best = t, bestP = std::move(P);
@@ -355,6 +365,7 @@ Engine::~Engine() {
         if (P) cudaFree(const_cast<void*>(P->dev_copy));
     cudaFree(staging_);
     if (out_staging_) cudaFree(out_staging_);
+    for (auto& [id, b] : gap_parts_) cudaFree(b.first);
     if (copy_in_) {
         cudaStreamDestroy(copy_in_), cudaStreamDestroy(copy_out_);
         for (cudaEvent_t ev : chunk_ev_) cudaEventDestroy(ev);
@@ -399,6 +410,21 @@ void Engine::set_input_seeded(const std::string& name, uint64_t seed, uint64_t f
         cuda_check(launch_seeded_nhwc(allocs_[size_t(t.alloc)], seed, first_image, batch, t.C, t.H, t.W, t.cstride, st), "seeded fill");
 }
 
+// A bf16 fused step over images [n0, n0 + count): the kernel, plus the
+// reduction that finishes a conv + global-average-pool step.
+void Engine::launch_bf16_step(size_t i, int n0, int count, cudaStream_t st) {
+    const BParams& P = *bparams_[i];
+    cuda_check(launch_fused_bf16(P, count, st, n0), "fused block (bf16)");
+    const StepSpec& s = plan_.steps[i];
+    if (s.gap_out.empty()) return;
+    const TensorSlot& t = slot(s.gap_out);
+    const Layer& pool = *g_.find_layer(s.gap_out);
+    const float scale = 1.0f / float(pool.pool->kernel * pool.pool->kernel);
+    cuda_check(launch_gap_finish_bf16(P.gap_part, P.grid_h * P.grid_w, P.ops[0].npad, scale,
+                                      reinterpret_cast<__nv_bfloat16*>(allocs_[size_t(t.alloc)]), t.cstride, t.coff, t.C, n0, count, st),
+               "global average pool finish");
+}
+
 bool Engine::range_capable() const {
     if (esz_ != 2) return false;
     for (size_t i = 0; i < plan_.steps.size(); ++i)
@@ -418,8 +444,7 @@ void Engine::forward_range(int n0, int count, cudaStream_t st) {
         cudaGraph_t graph;
         cuda_check(cudaStreamBeginCapture(capture_, cudaStreamCaptureModeThreadLocal), "begin capture");
         try {
-            for (size_t i = 0; i < plan_.steps.size(); ++i)
-                cuda_check(launch_fused_bf16(*bparams_[i], count, capture_, n0), "fused block (bf16, range)");
+            for (size_t i = 0; i < plan_.steps.size(); ++i) launch_bf16_step(i, n0, count, capture_);
         } catch (...) {
             cudaStreamEndCapture(capture_, &graph);
             throw;
@@ -439,7 +464,7 @@ void Engine::launch_step(size_t i, int batch, cudaStream_t st) {
     auto b16 = [&](const TensorSlot& t) { return reinterpret_cast<__nv_bfloat16*>(allocs_[size_t(t.alloc)]); };
     switch (s.kind) {
     case StepSpec::FUSED:
-        if (bf) cuda_check(launch_fused_bf16(*bparams_[i], batch, st), "fused block (bf16)");
+        if (bf) launch_bf16_step(i, 0, batch, st);
         else cuda_check(launch_fused_fp32(params_[i], batch, prec_ == Precision::fp32_exact, st), "fused block");
         return;
     case StepSpec::CONCAT_COPY: {

@@ -59,6 +59,7 @@ public:
 private:
     void launch_step(size_t i, int batch, cudaStream_t st);
     std::unique_ptr<struct BParams> build_bparams(const StepSpec& s);
+    void launch_bf16_step(size_t i, int n0, int count, cudaStream_t st);
     const TensorSlot& slot(const std::string& n) const;
 
     Graph g_;
@@ -84,6 +85,7 @@ private:
     cudaStream_t copy_in_ = nullptr, copy_out_ = nullptr;
     cudaEvent_t chunk_ev_[2 * kMaxChunks] = {};
     float* out_staging_ = nullptr;
+    std::map<std::string, std::pair<float*, size_t>> gap_parts_;  // conv+gap steps: per-tile partial sums
 };
 
 std::vector<float> seeded_weights(const Graph& g, uint64_t seed);  // tensor.cpp:42-62 semantics

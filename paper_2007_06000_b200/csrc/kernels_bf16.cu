@@ -281,7 +281,7 @@ __device__ void issuer(const BParams& P, uint8_t* smem, uint32_t tmem, int total
 // descriptor fields read from shared memory across those stores; hoisting
 // them once per op avoids a dependent shared load per field per channel.
 struct EpiOp {
-    int relu, c8end, emit, own_only;
+    int relu, c8end, emit, own_only, gap, gap_np;
     int org_mul, org_sub, H, W, out_cstride, out_coff;
     int tile_h, tile_w, grid_h, grid_w;
     int buf_ew, buf_plane;
@@ -293,7 +293,8 @@ struct EpiOp {
 
 __device__ __forceinline__ EpiOp epi_op(const BParams& P, const BOp& op, uint8_t* smem) {
     EpiOp e;
-    e.relu = op.relu, e.c8end = (op.cout + 7) & ~7, e.emit = op.emit, e.own_only = op.own_only;
+    e.relu = op.relu, e.c8end = (op.cout + 7) & ~7, e.emit = op.emit, e.own_only = op.own_only, e.gap = op.gap;
+    e.gap_np = op.gap ? op.nblocks * op.nb : 0;
     e.org_mul = op.org_mul, e.org_sub = op.org_sub, e.H = op.H, e.W = op.W;
     e.out_cstride = op.out_cstride, e.out_coff = op.out_coff;
     e.tile_h = P.tile_h, e.tile_w = P.tile_w, e.grid_h = P.grid_h, e.grid_w = P.grid_w;
@@ -332,7 +333,7 @@ __device__ __forceinline__ CellDst cell_dst(const EpiOp& e, const BTile& t, int 
     d.inside = gy >= 0 && gy < e.H && gx >= 0 && gx < e.W;
     d.sbuf = e.buf ? e.buf + (r * e.buf_ew + c) * 16 : nullptr;
     d.gdst = nullptr;
-    if (e.emit && e.out && valid && d.inside && owns(e, t, gy, gx))
+    if (e.emit && !e.gap && e.out && valid && d.inside && owns(e, t, gy, gx))
         d.gdst = e.out + ((size_t(t.n) * e.H + gy) * e.W + gx) * e.out_cstride + e.out_coff + t.c0;
     return d;
 }
@@ -394,10 +395,10 @@ __device__ __forceinline__ void finish16(const EpiOp& e, const CellDst& d, int c
 __device__ __forceinline__ void finish32(const EpiOp& e, const CellDst& d, bool valid, int ch0, uint32_t ta) {
     uint32_t r[32];
     tmem_ld32_issue(ta, r);
-    const float4* bp = reinterpret_cast<const float4*>(e.bias_p + ch0);
+    const uint32_t bp = e.bias_s + uint32_t(ch0) * 4u;
     float4 b[4];
 #pragma unroll
-    for (int j = 0; j < 4; ++j) b[j] = bp[j];
+    for (int j = 0; j < 4; ++j) b[j] = lds_f4(bp + 16u * j);  // volatile: stays between the TMEM load issue and its wait
     tmem_ld_wait32(r);
     if (!valid) return;
 #pragma unroll
@@ -405,7 +406,7 @@ __device__ __forceinline__ void finish32(const EpiOp& e, const CellDst& d, bool 
         if (ch0 + j >= e.c8end) break;
         if (j == 16) {
 #pragma unroll
-            for (int q = 0; q < 4; ++q) b[q] = bp[4 + q];
+            for (int q = 0; q < 4; ++q) b[q] = lds_f4(bp + 64u + 16u * q);
         }
         float x[8];
         const float4 b0 = b[(j & 15) / 4], b1 = b[(j & 15) / 4 + 1];
@@ -418,6 +419,57 @@ __device__ __forceinline__ void finish32(const EpiOp& e, const CellDst& d, bool 
             for (int k = 0; k < 8; ++k) x[k] = fmaxf(x[k], 0.0f);
         put8(d, ch0 + j, x, e);
     }
+}
+
+// Warp transpose-reduction: on entry lane l holds v[0..31] (row l, columns
+// 0..31); on exit lane l returns the sum of column l over the warp's 32 rows
+// (31 shuffles: at each step a lane keeps the half of its columns selected by
+// its own lane bit and adds the partner's copy of that half).
+__device__ __forceinline__ float warp_colsum32(float* v) {
+    const int lane = threadIdx.x & 31;
+#pragma unroll
+    for (int off = 16; off >= 1; off >>= 1) {
+        const bool upper = (lane & off) != 0;
+#pragma unroll
+        for (int j = 0; j < off; ++j) {
+            const float send = upper ? v[j] : v[j + off];
+            const float keep = upper ? v[j + off] : v[j];
+            v[j] = keep + __shfl_xor_sync(0xffffffffu, send, off);
+        }
+    }
+    return v[0];
+}
+
+// Global-average-pool epilogue: relu(acc + bias) of the cells this tile owns
+// (others contribute 0), summed over the warp's rows and added to the tile's
+// per-column sums in shared memory.  Warp-uniform (all lanes shuffle).
+__device__ __forceinline__ void finish_gap(const EpiOp& e, bool take, int ch0, int ncols, uint32_t ta, float* gsum) {
+    float v[32];
+    if (ncols == 32) {
+        tmem_ld32(ta, v);
+    } else {
+        tmem_ld16(ta, v);
+#pragma unroll
+        for (int j = 16; j < 32; ++j) v[j] = 0.0f;
+    }
+#pragma unroll
+    for (int j = 0; j < 32; j += 4) {
+        if (j >= ncols) {
+            v[j] = v[j + 1] = v[j + 2] = v[j + 3] = 0.0f;
+            continue;
+        }
+        const float4 b = lds_f4(e.bias_s + uint32_t(ch0 + j) * 4u);
+        float x0 = v[j] + b.x, x1 = v[j + 1] + b.y, x2 = v[j + 2] + b.z, x3 = v[j + 3] + b.w;
+        if (e.relu) x0 = fmaxf(x0, 0.0f), x1 = fmaxf(x1, 0.0f), x2 = fmaxf(x2, 0.0f), x3 = fmaxf(x3, 0.0f);
+        // select, not multiply: rows outside the tile hold whatever the
+        // over-read shared memory produced (possibly Inf/NaN)
+        v[j] = take ? x0 : 0.0f, v[j + 1] = take ? x1 : 0.0f, v[j + 2] = take ? x2 : 0.0f, v[j + 3] = take ? x3 : 0.0f;
+    }
+    const float colsum = warp_colsum32(v);
+    const int lane = threadIdx.x & 31;
+    // per-warp slot (no shared float atomics: sm_100 lowers them to a CAS loop)
+    float* slot = gsum + ((threadIdx.x >> 5) & 3) * e.gap_np;  // warps w, w+4 own disjoint columns
+    if (lane < ncols && ch0 + lane < e.c8end) slot[ch0 + lane] += colsum;
 }
 
 // Accumulator -> bias/ReLU/mask -> bf16 -> shared buffer and/or HBM.  Thread
@@ -446,6 +498,12 @@ __device__ void epilogue_mma(const BParams& P, const BOp& op, int nbi, uint8_t* 
             valid = r < ext_h && c < ext_w;
         }
         const CellDst d = cell_dst(e, t, r, c, valid);
+        if (op.gap) {
+            float* gsum = reinterpret_cast<float*>(smem + P.gap_off);
+            const bool take = valid && d.inside;
+            for (int col = col0; col < nb; col += cstep) finish_gap(e, take, chbase + col, min(32, nb - col), tbase + mt * nb + col, gsum);
+            continue;
+        }
         for (int col = col0; col < nb; col += cstep) {
             const uint32_t ta = tbase + mt * nb + col;
             if (nb - col >= 32) {
@@ -698,8 +756,11 @@ __global__ void __launch_bounds__(kBThreads, kMaxCtasPerSm) fused_bf16_kernel(co
             if (op.bias_smem < 0) continue;
             float* dst = reinterpret_cast<float*>(smem + op.bias_smem);
             for (int k = threadIdx.x; k < op.npad; k += kCompute) dst[k] = __ldg(op.bias + k);
+            if (op.gap)
+                for (int k = threadIdx.x; k < 4 * op.npad; k += kCompute) reinterpret_cast<float*>(smem + P.gap_off)[k] = 0.0f;
         }
         named_sync_compute();
+        const int gap_np = P.ops[0].gap ? P.ops[0].npad : 0;  // gap steps have one op
         const int nxb = P.nxb;
         int k = 0;
         for (int tau = blockIdx.x; tau < total; tau += gridDim.x, ++k) {
@@ -729,6 +790,18 @@ __global__ void __launch_bounds__(kBThreads, kMaxCtasPerSm) fused_bf16_kernel(co
             // every unit of this tile is done (MMAs complete, SIMT reads
             // finished): its staging buffer may be refilled
             if (threadIdx.x == 0) mbar_arrive(&x_free[b]), stamp(P, kTrEnd, k);
+            if (gap_np) {  // this tile's column sums -> gap_part[image][tile][c], reset
+                float* gsum = reinterpret_cast<float*>(smem + P.gap_off);
+                const int per_img = P.grid_h * P.grid_w;
+                float* dst = P.gap_part + (size_t(t.n) * per_img + t.ty * P.grid_w + t.tx) * gap_np;
+                for (int c = threadIdx.x; c < gap_np; c += kCompute) {
+                    float a = 0.0f;
+#pragma unroll
+                    for (int w = 0; w < 4; ++w) a += gsum[w * gap_np + c], gsum[w * gap_np + c] = 0.0f;
+                    dst[c] = a;
+                }
+                named_sync_compute();
+            }
         }
     }
     fence_before();
@@ -837,6 +910,21 @@ __global__ void eltwise_bf16(int op, const __nv_bfloat16* __restrict__ a, int ac
     }
 }
 
+// gap steps: out[n][coff + c] = bf16(scale * sum over the image's tiles of
+// part[n][tile][c]) for images [n0, n0 + N).
+__global__ void gap_finish_bf16(const float* __restrict__ part, int tiles, int np, float scale, __nv_bfloat16* __restrict__ out, int cs,
+                                int coff, int C, int n0, int N) {
+    const long long total = (long long)N * C;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total; i += (long long)gridDim.x * blockDim.x) {
+        const long long n = n0 + i / C;
+        const int c = int(i % C);
+        const float* p = part + size_t(n) * tiles * np + c;
+        float acc = 0.0f;
+        for (int t = 0; t < tiles; ++t) acc += p[size_t(t) * np];
+        out[size_t(n) * cs + coff + c] = __float2bfloat16(acc * scale);
+    }
+}
+
 int grid_b(long long work) {
     long long b = (work + 255) / 256;
     return int(b < 148 * 16 ? (b < 1 ? 1 : b) : 148 * 16);
@@ -914,6 +1002,12 @@ cudaError_t launch_s2d_bf16(const float* src, unsigned long long seed, unsigned 
 cudaError_t launch_concat_copy_bf16(const __nv_bfloat16* src, int scs, int sco, __nv_bfloat16* dst, int dcs, int dco, int C,
                                     long long pixels, cudaStream_t st) {
     concat_copy_bf16<<<grid_b(pixels * C), 256, 0, st>>>(src, scs, sco, dst, dcs, dco, C, pixels);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_gap_finish_bf16(const float* part, int tiles, int np, float scale, __nv_bfloat16* out, int cs, int coff, int C, int n0,
+                                   int N, cudaStream_t st) {
+    gap_finish_bf16<<<grid_b((long long)N * C), 256, 0, st>>>(part, tiles, np, scale, out, cs, coff, C, n0, N);
     return cudaGetLastError();
 }
 

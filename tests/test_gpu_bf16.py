@@ -115,3 +115,23 @@ def test_bf16_run_host_pipelined_matches_device_path(chunks, monkeypatch):
     e.forward(6)
     dev = e.read("pool10", 6).cpu().numpy()
     assert np.array_equal(host, dev)
+
+
+@pytest.mark.parametrize("name,batch", [("squeezenet11", 8), ("inc3a", 4), ("fire", 6)])
+def test_bf16_forwards_are_bitwise_reproducible(name, batch):
+    """Race detector: repeated forwards (graph and direct launches) over the
+    same input give bit-identical tensors -- the persistent pipeline's
+    barriers, TMEM reuse and staging buffers leave no timing dependence."""
+    import torch
+    g = X.load_graph(X.graph_path(name))
+    e = X.Engine(g, X.seeded_weights(g, 42), "b200", "bf16", max_batch=batch)
+    names = [n for n in e.materialized() if n not in dict(g.inputs)]
+    outs = []
+    for r in range(4):
+        e.set_input_seeded(42, batch)
+        e.forward(batch, use_graph=(r % 2 == 0))
+        outs.append({n: e.read(n, batch).clone() for n in names})
+    torch.cuda.synchronize()
+    for n in names:
+        for o in outs[1:]:
+            assert torch.equal(outs[0][n], o[n]), n
