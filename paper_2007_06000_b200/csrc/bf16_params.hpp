@@ -40,6 +40,9 @@ constexpr int kRingSlots = 3;
 constexpr int kEpiWarps = XLF_EPI_WARPS;
 constexpr int kMaxCtasPerSm = kEpiWarps <= 4 ? 3 : 2;
 constexpr int kChunkBytes = 16 * 1024;  // weight ring slot
+// Dynamic shared memory per CTA: 227 KB minus the static part (barriers, the
+// descriptor copy: 4 KB) minus 4 KB headroom (ncu's replay needs some).
+constexpr int kSmemBudgetBf16 = 227 * 1024 - 8192;
 constexpr int kRingMax = 8;             // ring slots (P.ring_slots <= this)
 
 struct BOp {

@@ -1,4 +1,5 @@
 #include "device_plan.hpp"
+#include "bf16_params.hpp"
 
 #include <algorithm>
 #include <cmath>
@@ -442,7 +443,7 @@ DevicePlan plan_device(const Graph& g, Partition part, int batch_hint, int smem_
     plan.bf16 = bf16;
     const int cpad = bf16 ? 8 : 4;  // channel padding of HBM tensors (16 bytes)
     auto tile = [&](StepSpec& st) {
-        return bf16 ? choose_tile_bf16(g, st, batch_hint, smem_budget - 4096) : choose_tile(g, st, batch_hint, smem_budget);
+        return bf16 ? choose_tile_bf16(g, st, batch_hint, std::min(smem_budget, kSmemBudgetBf16)) : choose_tile(g, st, batch_hint, smem_budget);
     };
     if (part == Partition::reference) plan.blocks = detect_fusion_blocks(g);
     else if (part == Partition::b200) plan.blocks = detect_fusion_blocks_b200(g);

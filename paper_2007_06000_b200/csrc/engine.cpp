@@ -296,7 +296,7 @@ std::string Engine::autotune(int batch, int reps, int topk) {
         if (s.kind != StepSpec::FUSED || !bparams_[i]) continue;
         // the model ranks tiles within one staging / weight mode reasonably
         // but not across modes: keep the best `topk` of every mode
-        std::vector<BCandidate> all = candidates_bf16(g_, s, batch, 227 * 1024 - 4096), cands;
+        std::vector<BCandidate> all = candidates_bf16(g_, s, batch, kSmemBudgetBf16), cands;
         std::map<std::tuple<int, int, int>, int> per_mode;
         for (const BCandidate& c : all)
             if (per_mode[{c.nxb, c.wres, c.slots}]++ < topk) cands.push_back(c);

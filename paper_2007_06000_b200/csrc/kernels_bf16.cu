@@ -934,7 +934,7 @@ int grid_b(long long work) {
 
 cudaError_t init_fused_bf16() {
     // 227 KB per block minus the static part (barriers + the BParams copy)
-    cudaError_t e = cudaFuncSetAttribute(fused_bf16_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024 - 4096);
+    cudaError_t e = cudaFuncSetAttribute(fused_bf16_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBudgetBf16);
     if (e != cudaSuccess) return e;
     return cudaFuncSetAttribute(fused_bf16_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
 }
