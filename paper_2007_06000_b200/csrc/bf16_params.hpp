@@ -32,13 +32,10 @@ constexpr int kBMaxOps = 8;
 constexpr int kBMaxBufs = 4;
 constexpr int kBMaxUnits = 24;  // (op, N block) pairs
 constexpr int kRingSlots = 3;
-// CTA shape: kEpiWarps epilogue/SIMT warps + 3 role warps (input producer,
-// MMA issuer, weight producer); up to kMaxCtasPerSm resident per SM.
-#ifndef XLF_EPI_WARPS
-#define XLF_EPI_WARPS 8
-#endif
-constexpr int kEpiWarps = XLF_EPI_WARPS;
-constexpr int kMaxCtasPerSm = kEpiWarps <= 4 ? 3 : 2;
+// CTA shapes: 4 or 8 epilogue/SIMT warps + 3 role warps (input producer,
+// MMA issuer, weight producer); the kernel is instantiated for both and the
+// step's descriptor (epi_warps) selects one.  Resident CTAs per SM: <= 3 / 2.
+constexpr int max_ctas_per_sm(int epi_warps) { return epi_warps <= 4 ? 3 : 2; }
 constexpr int kChunkBytes = 16 * 1024;  // weight ring slot
 // Dynamic shared memory per CTA: 227 KB minus the static part (barriers, the
 // descriptor copy: 4 KB) minus 4 KB headroom (ncu's replay needs some).
@@ -132,6 +129,7 @@ struct alignas(64) BParams {
     int nxb, xstride;
     int ctas_per_sm;  // resident CTAs per SM at smem_bytes (grid = 148 x this, capped by the tiles)
     int grid_all;     // 1: grid = tiles (each CTA one tile), else the persistent grid
+    int epi_warps;    // 4 or 8 epilogue/SIMT warps (kernel instantiation)
     // Optional phase trace (XLF_TRACE=1): globaltimer stamps of CTAs with
     // blockIdx.y == 0 and blockIdx.x < kTraceCtas, kTraceEvents each.
     unsigned long long* trace;

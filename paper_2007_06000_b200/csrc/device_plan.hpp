@@ -52,6 +52,7 @@ struct StepSpec {
     int wres = 0;       // bf16: weights resident in shared memory (else streamed through the ring)
     int ring_slots = 3; // bf16: ring depth when streamed
     int grid_all = 0;   // bf16: one tile per CTA (grid = tiles) instead of a persistent grid
+    int epi_warps = 8;  // bf16: epilogue/SIMT warps per CTA (4 or 8)
     // bf16 conv + global average pool (SqueezeNet conv10 -> pool10): the
     // step's single conv op never stores its output; its epilogue reduces
     // every tile over its cells and the pooled layer `gap_out` (1x1) is
@@ -95,7 +96,7 @@ bool choose_tile_bf16(const Graph& g, StepSpec& s, int batch_hint, int smem_budg
 // One configuration of a bf16 step: tile, staging buffers, weight residency /
 // ring depth, shared bytes, and the model's score (SM cycles, lower better).
 struct BCandidate {
-    int th, tw, nxb, wres, slots, smem;
+    int th, tw, nxb, wres, slots, smem, epi_warps;
     double model;
 };
 std::vector<BCandidate> candidates_bf16(const Graph& g, const StepSpec& s, int batch_hint, int smem_budget);

@@ -426,6 +426,7 @@ std::vector<BCandidate> candidates_bf16(const Graph& g, const StepSpec& s, int b
     const WMode wmodes[] = {{1, 3}, {0, 3}, {0, 6}, {0, 8}};
     std::vector<BCandidate> out;
     BParams* P = new BParams;
+    for (int ew : {8, 4})
     for (int nxb = 1; nxb <= 2; ++nxb)
         for (const WMode& wm : wmodes) {
             if (force && nxb != force) continue;
@@ -447,18 +448,19 @@ std::vector<BCandidate> candidates_bf16(const Graph& g, const StepSpec& s, int b
                         if (P->ops[i].emit) out_bytes += double(th) * tw * P->ops[i].npad * 2;
                     const double tiles = double(P->grid_h) * P->grid_w * P->cgroups * std::max(batch_hint, 1);
                     // 228 KB per SM; per CTA: dynamic + static (~4 KB) + 1 KB driver reserve
-                    int occ = std::max(1, std::min(kMaxCtasPerSm, int((228 * 1024) / (sm + 5120))));
+                    int occ = std::max(1, std::min(max_ctas_per_sm(ew), int((228 * 1024) / (sm + 5120))));
                     if (P->tmem_cols) occ = std::min(occ, 512 / P->tmem_cols);
                     double wbytes = 0;  // weights each tile streams from L2 through the ring
                     for (int i = 0; i < P->nops; ++i)
                         if (P->ops[i].kind == BOP_MMA) wbytes += double(P->ops[i].nblocks) * P->ops[i].ksteps * P->ops[i].nb * 32;
                     const double wcost = P->wres ? 0.0 : wbytes * 2000.0 / (double(wm.slots) * kChunkBytes);
                     const double load = in_bytes / 24.0 + 1000.0;
-                    const double compute = out_bytes / 48.0 + wcost + mma / 8192.0 + simt / 128.0 + 800.0 * P->ngroups;
+                    // epilogue / SIMT work spreads over the epilogue warps
+                    const double compute = out_bytes / 48.0 + wcost + mma / 8192.0 + simt / 128.0 * (8.0 / ew) + 800.0 * P->ngroups;
                     const double per_tile = nxb == 2 ? std::max(load, compute) : load + compute;
                     const double t = std::max(std::ceil(tiles / (148.0 * occ)) * per_tile,
                                               tiles * (in_bytes + out_bytes) / (148.0 * 24.0));
-                    out.push_back({th, tw, nxb, P->wres, wm.slots, int(sm), t});
+                    out.push_back({th, tw, nxb, P->wres, wm.slots, int(sm), ew, t});
                 }
         }
     delete P;
@@ -479,6 +481,7 @@ static bool choose_tile_bf16_at(const Graph& g, StepSpec& s, int batch_hint, int
 
 void apply_candidate(StepSpec& s, const BCandidate& c) {
     s.tile_h = c.th, s.tile_w = c.tw, s.smem_bytes = c.smem, s.nxb = c.nxb, s.wres = c.wres, s.ring_slots = c.slots;
+    s.epi_warps = c.epi_warps;
 }
 
 // bf16 weights of every MMA-eligible conv: [nblock][tap][cin/8][nb][8].

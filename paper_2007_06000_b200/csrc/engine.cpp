@@ -31,7 +31,7 @@ cudaError_t init_fused_bf16();
 cudaError_t launch_fused_bf16(const BParams& P, int batch, cudaStream_t st, int n0 = 0);
 cudaError_t launch_gap_finish_bf16(const float* part, int tiles, int np, float scale, __nv_bfloat16* out, int cs, int coff, int C, int n0,
                                    int N, cudaStream_t st);
-int occupancy_fused_bf16(int smem_bytes, int tmem_cols);
+int occupancy_fused_bf16(int smem_bytes, int tmem_cols, int epi_warps);
 cudaError_t launch_nchw_to_nhwc_bf16(const float* src, __nv_bfloat16* dst, int N, int C, int H, int W, int cs, cudaStream_t st);
 cudaError_t launch_nhwc_bf16_to_nchw(const __nv_bfloat16* src, int cs, int coff, float* dst, int N, int C, int H, int W,
                                      cudaStream_t st);
@@ -217,7 +217,8 @@ std::unique_ptr<BParams> Engine::build_bparams(const StepSpec& s) {
     auto P = std::make_unique<BParams>();
     if (layout_bf16(g_, s, s.tile_h, s.tile_w, P.get(), s.nxb, s.wres, s.ring_slots) < 0)
         fail(ErrorKind::internal, "step " + s.id + ": bf16 layout failed");
-    P->ctas_per_sm = occupancy_fused_bf16(P->smem_bytes, P->tmem_cols);
+    P->epi_warps = s.epi_warps;
+    P->ctas_per_sm = occupancy_fused_bf16(P->smem_bytes, P->tmem_cols, P->epi_warps);
     P->grid_all = s.grid_all;
     if (std::getenv("XLF_TRACE"))
         std::fprintf(stderr, "[xlf] step %s: tile %dx%d, %d B shared, %d staging buffer(s), weights %s, %d CTA(s)/SM%s\n",
@@ -297,9 +298,9 @@ std::string Engine::autotune(int batch, int reps, int topk) {
         // the model ranks tiles within one staging / weight mode reasonably
         // but not across modes: keep the best `topk` of every mode
         std::vector<BCandidate> all = candidates_bf16(g_, s, batch, kSmemBudgetBf16), cands;
-        std::map<std::tuple<int, int, int>, int> per_mode;
+        std::map<std::tuple<int, int, int, int>, int> per_mode;
         for (const BCandidate& c : all)
-            if (per_mode[{c.nxb, c.wres, c.slots}]++ < topk) cands.push_back(c);
+            if (per_mode[{c.nxb, c.wres, c.slots, c.epi_warps}]++ < topk) cands.push_back(c);
         float best_ms = 1e30f;
         StepSpec best = s;
         std::unique_ptr<BParams> bestP;
@@ -324,9 +325,9 @@ std::string Engine::autotune(int batch, int reps, int topk) {
                 ms /= float(reps);
                 ++tried;
                 if (std::getenv("XLF_TUNE_VERBOSE"))
-                    std::fprintf(stderr, "[xlf] tune %s: tile %dx%d nxb %d wres %d slots %d grid_all %d smem %d: %.1f us (model %.0f)\n",
-                                 s.id.c_str(), t.tile_h, t.tile_w, t.nxb, t.wres, t.ring_slots, t.grid_all, P->smem_bytes, ms * 1000.0f,
-                                 c.model);
+                    std::fprintf(stderr, "[xlf] tune %s: tile %dx%d nxb %d wres %d slots %d grid_all %d ew %d smem %d: %.1f us (model %.0f)\n",
+                                 s.id.c_str(), t.tile_h, t.tile_w, t.nxb, t.wres, t.ring_slots, t.grid_all, t.epi_warps, P->smem_bytes,
+                                 ms * 1000.0f, c.model);
                 if (ms < best_ms) {
                     if (bestP) cudaFree(const_cast<void*>(bestP->dev_copy));
                     best_ms = ms, best = t, bestP = std::move(P);
@@ -342,7 +343,8 @@ std::string Engine::autotune(int batch, int reps, int topk) {
         bparams_[i] = std::move(bestP);
         js << (first ? "" : ",") << "{\"id\":\"" << s.id << "\",\"tried\":" << tried << ",\"us\":" << best_ms * 1000.0f
            << ",\"tile\":[" << s.tile_h << "," << s.tile_w << "],\"nxb\":" << s.nxb << ",\"wres\":" << s.wres
-           << ",\"ring_slots\":" << s.ring_slots << ",\"grid_all\":" << s.grid_all << ",\"smem_bytes\":" << s.smem_bytes << "}";
+           << ",\"ring_slots\":" << s.ring_slots << ",\"grid_all\":" << s.grid_all << ",\"epi_warps\":" << s.epi_warps
+           << ",\"smem_bytes\":" << s.smem_bytes << "}";
         first = false;
     }
     js << "]";

@@ -42,10 +42,18 @@ namespace {
 
 using namespace umma;
 
-constexpr int kCompute = kEpiWarps * 32;      // warps 0..kEpiWarps-1: epilogue + SIMT ops
-constexpr int kBThreads = kCompute + 96;      // then: input producer, MMA issuer, weight producer
-constexpr int kWarpX = kEpiWarps, kWarpMma = kEpiWarps + 1, kWarpW = kEpiWarps + 2;
-constexpr int kHalves = kCompute / 128;       // epilogue warp groups splitting the accumulator columns
+// CTA shape, a template parameter of the kernel (the tuner picks per step):
+// EW epilogue/SIMT warps (4 or 8), then the input producer, MMA issuer and
+// weight producer warps.  Fewer epilogue warps -> fewer registers per CTA ->
+// more CTAs (more independent tile chains) per SM.
+template <int EW>
+struct Cta {
+    static constexpr int compute = EW * 32;        // warps 0..EW-1: epilogue + SIMT ops
+    static constexpr int threads = compute + 96;
+    static constexpr int wx = EW, wmma = EW + 1, ww = EW + 2;
+    static constexpr int halves = compute / 128;   // epilogue warp groups splitting the accumulator columns
+    static constexpr int min_blocks = EW <= 4 ? 3 : 2;
+};
 
 struct BTile {
     int n, ty, tx, oy0, ox0, c0;
@@ -66,15 +74,17 @@ __device__ __forceinline__ void stamp(const BParams& P, int ev, int k = 0) {
     }
 }
 
-__device__ __forceinline__ void named_sync_compute() { asm volatile("bar.sync 1, %0;\n" ::"n"(kCompute) : "memory"); }
+template <int EW>
+__device__ __forceinline__ void named_sync_compute() { asm volatile("bar.sync 1, %0;\n" ::"n"(Cta<EW>::compute) : "memory"); }
 
 // Epilogue-side wait: ONE thread polls the mbarrier, the other compute warps
 // block in a hardware named barrier (no issue slots).  Eight warps polling a
 // try_wait loop issued a third of all instructions of the kernel and starved
 // the co-resident CTA's epilogue (ncu, profiles/r1_ncu_summary.md).
+template <int EW>
 __device__ __forceinline__ void compute_wait(uint64_t* bar, uint32_t parity) {
     if (threadIdx.x == 0) mbar_sleep_wait(bar, parity);
-    named_sync_compute();
+    named_sync_compute<EW>();
 }
 
 __device__ __forceinline__ const BRegion& src_region(const BParams& P, const BOp& op, int which) {
@@ -476,7 +486,9 @@ __device__ __forceinline__ void finish_gap(const EpiOp& e, bool take, int ch0, i
 // (row = tid % 128) owns TMEM lane `row` = GEMM row = one cell.  With two
 // warp groups, narrow ops (<= 32 columns) split the M tiles between them,
 // wider ones split the columns in 32-column slices.
+template <int EW>
 __device__ void epilogue_mma(const BParams& P, const BOp& op, int nbi, uint8_t* smem, uint32_t tmem, const BTile& t) {
+    constexpr int kHalves = Cta<EW>::halves;
     const EpiOp e = epi_op(P, op, smem);
     const int mtiles = op.mtiles, contig = op.contig, ext_w = op.ext_w, ext_h = op.ext_h, strips = op.strips, nb = op.nb;
     const int row = threadIdx.x & 127, half = kHalves > 1 ? int(threadIdx.x >> 7) : 0;
@@ -566,7 +578,7 @@ __device__ __forceinline__ uint32_t bmax2(uint32_t a, uint32_t b) {
 // (oct) of one output cell, octs fastest: the 8 chunks of a cell sit in 8
 // different bank groups in every region mode, and 8 neighbouring threads
 // store one 128-byte run of the NHWC output.
-template <int MODE, int K, bool MX>
+template <int EW, int MODE, int K, bool MX>
 __device__ void pool_fast(const EpiOp& e, const BRegion& Rg, uint8_t* smem, const BOp& op, const BTile& t) {
     const uint32_t base = smem_u32(smem + Rg.smem_off);
     const int plane = Rg.plane_bytes, rew = Rg.ext_w;
@@ -575,7 +587,7 @@ __device__ void pool_fast(const EpiOp& e, const BRegion& Rg, uint8_t* smem, cons
     const int ncell = op.ext_h * ext_w, c8 = op.npad / 8;
     const float inv = 1.0f / float(kh_ * kw_);
     constexpr int kPer = MODE == kSw128 ? 8 : MODE == kSw32 ? 2 : 1;
-    for (int u = threadIdx.x; u < ncell * c8; u += kCompute) {
+    for (int u = threadIdx.x; u < ncell * c8; u += Cta<EW>::compute) {
         const int cell = u / c8, oct = u - cell * c8;
         const int r = cell / ext_w, c = cell - r * ext_w;
         const int kb = oct / kPer, j = oct - kb * kPer;
@@ -618,20 +630,21 @@ __device__ void pool_fast(const EpiOp& e, const BRegion& Rg, uint8_t* smem, cons
     }
 }
 
-template <int MODE>
+template <int EW, int MODE>
 __device__ __forceinline__ void pool_mode(const EpiOp& e, const BRegion& R, uint8_t* smem, const BOp& op, const BTile& t) {
     if (op.kind == BOP_MAXPOOL) {
-        if (op.kh == 3 && op.kw == 3) pool_fast<MODE, 3, true>(e, R, smem, op, t);
-        else pool_fast<MODE, 0, true>(e, R, smem, op, t);
+        if (op.kh == 3 && op.kw == 3) pool_fast<EW, MODE, 3, true>(e, R, smem, op, t);
+        else pool_fast<EW, MODE, 0, true>(e, R, smem, op, t);
     } else {
-        pool_fast<MODE, 0, false>(e, R, smem, op, t);
+        pool_fast<EW, MODE, 0, false>(e, R, smem, op, t);
     }
 }
 
 // Residual add of two shared plane buffers.
+template <int EW>
 __device__ void simt_add(const EpiOp& e, const BRegion& A, const BRegion& B, uint8_t* smem, const BOp& op, const BTile& t) {
     const int ext_w = op.ext_w, ncell = op.ext_h * ext_w, c8 = op.npad / 8;
-    for (int u = threadIdx.x; u < ncell * c8; u += kCompute) {
+    for (int u = threadIdx.x; u < ncell * c8; u += Cta<EW>::compute) {
         const int cell = u / c8, oct = u - cell * c8;
         const int r = cell / ext_w, c = cell - r * ext_w;
         const uint4 a = lds_u4(smem_u32(smem + A.smem_off + oct * A.plane_bytes + (r * A.ext_w + c) * 16));
@@ -648,20 +661,22 @@ __device__ void simt_add(const EpiOp& e, const BRegion& A, const BRegion& B, uin
     }
 }
 
+template <int EW>
 __device__ void simt_pool_add(const BParams& P, const BOp& op, uint8_t* smem, const BTile& t, int xdelta) {
     const EpiOp e = epi_op(P, op, smem);
     const BRegion R = src_region_at(P, op, op.src, xdelta);
     if (op.kind == BOP_ADD) {
-        simt_add(e, R, P.bufs[op.src2], smem, op, t);
+        simt_add<EW>(e, R, P.bufs[op.src2], smem, op, t);
         return;
     }
-    if (R.mode == kSw128) pool_mode<kSw128>(e, R, smem, op, t);
-    else if (R.mode == kSw32) pool_mode<kSw32>(e, R, smem, op, t);
-    else pool_mode<kPlanes>(e, R, smem, op, t);
+    if (R.mode == kSw128) pool_mode<EW, kSw128>(e, R, smem, op, t);
+    else if (R.mode == kSw32) pool_mode<EW, kSw32>(e, R, smem, op, t);
+    else pool_mode<EW, kPlanes>(e, R, smem, op, t);
 }
 
 // Direct conv for what the tensor-core path does not take (stride != 1,
 // groups, Cin not a multiple of 16).  fp32 accumulate.
+template <int EW>
 __device__ void simt_conv(const BParams& P, const BOp& op, uint8_t* smem, const BTile& t, int xdelta) {
     const EpiOp e = epi_op(P, op, smem);
     const RegionView R = region_view(src_region_at(P, op, op.src, xdelta), smem);
@@ -670,7 +685,7 @@ __device__ void simt_conv(const BParams& P, const BOp& op, uint8_t* smem, const 
     const int cin_g = op.cin / op.group, cout_g = cout / op.group, cp4 = (cout + 3) & ~3;
     const float* wsimt = op.wsimt;
     const float* gbias = op.bias;
-    for (int u = threadIdx.x; u < ncell * c8; u += kCompute) {
+    for (int u = threadIdx.x; u < ncell * c8; u += Cta<EW>::compute) {
         const int cell = u / c8, oct = u - cell * c8;
         const int r = cell / ext_w, c = cell - r * ext_w;
         float acc[8];
@@ -701,7 +716,10 @@ __device__ void simt_conv(const BParams& P, const BOp& op, uint8_t* smem, const 
     }
 }
 
-__global__ void __launch_bounds__(kBThreads, kMaxCtasPerSm) fused_bf16_kernel(const __grid_constant__ BParams Pg, int batch, int n0) {
+template <int EW>
+__global__ void __launch_bounds__(Cta<EW>::threads, Cta<EW>::min_blocks) fused_bf16_kernel(const __grid_constant__ BParams Pg, int batch,
+                                                                                        int n0) {
+    constexpr int kCompute = Cta<EW>::compute, kWarpX = Cta<EW>::wx, kWarpMma = Cta<EW>::wmma, kWarpW = Cta<EW>::ww;
     extern __shared__ __align__(1024) uint8_t smem[];
     __shared__ __align__(8) uint64_t bar_x[2], x_free[2], ring_full[kRingMax], ring_empty[kRingMax], acc_full[kBMaxUnits],
         unit_done[kBMaxUnits];
@@ -749,7 +767,7 @@ __global__ void __launch_bounds__(kBThreads, kMaxCtasPerSm) fused_bf16_kernel(co
         if (elect_one()) issuer(Pg, smem, tmem, total, bar_x, ring_full, ring_empty, acc_full, unit_done, &bar_w);
         __syncwarp();
     } else {
-        compute_wait(&bar_p, 0);
+        compute_wait<EW>(&bar_p, 0);
         // biases of the MMA ops -> shared memory (read by every epilogue)
         for (int i = 0; i < P.nops; ++i) {
             const BOp& op = P.ops[i];
@@ -759,7 +777,7 @@ __global__ void __launch_bounds__(kBThreads, kMaxCtasPerSm) fused_bf16_kernel(co
             if (op.gap)
                 for (int k = threadIdx.x; k < 4 * op.npad; k += kCompute) reinterpret_cast<float*>(smem + P.gap_off)[k] = 0.0f;
         }
-        named_sync_compute();
+        named_sync_compute<EW>();
         const int gap_np = P.ops[0].gap ? P.ops[0].npad : 0;  // gap steps have one op
         const int nxb = P.nxb;
         int k = 0;
@@ -771,20 +789,20 @@ __global__ void __launch_bounds__(kBThreads, kMaxCtasPerSm) fused_bf16_kernel(co
             for (int gi = 0; gi < P.ngroups; ++gi) {
                 const BGroup& G = P.groups[gi];
                 if (G.mma) {
-                    compute_wait(&acc_full[gi], k & 1);
+                    compute_wait<EW>(&acc_full[gi], k & 1);
                     if (threadIdx.x == 0) stamp(P, kTrUnit + 2 * gi, k);
                     fence_after();
                     if (!(P.dbg & 2))
-                        for (int i = G.op0; i < G.op1; ++i) epilogue_mma(P, P.ops[i], G.nbi, smem, tmem, t);
+                        for (int i = G.op0; i < G.op1; ++i) epilogue_mma<EW>(P, P.ops[i], G.nbi, smem, tmem, t);
                 } else {
                     const BOp& op = P.ops[G.op0];
-                    if (!have_x) compute_wait(&bar_x[b], use & 1), have_x = true;
-                    if (op.kind == BOP_SIMT_CONV) simt_conv(P, op, smem, t, xdelta);
-                    else simt_pool_add(P, op, smem, t, xdelta);
+                    if (!have_x) compute_wait<EW>(&bar_x[b], use & 1), have_x = true;
+                    if (op.kind == BOP_SIMT_CONV) simt_conv<EW>(P, op, smem, t, xdelta);
+                    else simt_pool_add<EW>(P, op, smem, t, xdelta);
                 }
                 fence_async_smem();  // epilogue-written buffers are read by later MMAs (async proxy)
                 fence_before();
-                named_sync_compute();
+                named_sync_compute<EW>();
                 if (threadIdx.x == 0) mbar_arrive(&unit_done[gi]), stamp(P, kTrUnit + 2 * gi + 1, k);
             }
             // every unit of this tile is done (MMAs complete, SIMT reads
@@ -800,7 +818,7 @@ __global__ void __launch_bounds__(kBThreads, kMaxCtasPerSm) fused_bf16_kernel(co
                     for (int w = 0; w < 4; ++w) a += gsum[w * gap_np + c], gsum[w * gap_np + c] = 0.0f;
                     dst[c] = a;
                 }
-                named_sync_compute();
+                named_sync_compute<EW>();
             }
         }
     }
@@ -932,33 +950,52 @@ int grid_b(long long work) {
 
 }  // namespace
 
-cudaError_t init_fused_bf16() {
-    // 227 KB per block minus the static part (barriers + the BParams copy)
-    cudaError_t e = cudaFuncSetAttribute(fused_bf16_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBudgetBf16);
+namespace {
+
+template <int EW>
+cudaError_t init_ew() {
+    // 227 KB per block minus the static part (barriers + the BParams copy) and headroom
+    cudaError_t e = cudaFuncSetAttribute(fused_bf16_kernel<EW>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBudgetBf16);
     if (e != cudaSuccess) return e;
-    return cudaFuncSetAttribute(fused_bf16_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    return cudaFuncSetAttribute(fused_bf16_kernel<EW>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
 }
 
-// Resident CTAs per SM: the occupancy API, cross-checked against the
-// shared-memory arithmetic (228 KB per SM, 1 KB reserved per CTA, the static
-// barriers + descriptor copy) and the launch bound of 2.  Over-subscribing is
-// harmless (tiles are independent), under-subscribing halves the overlap.
-int occupancy_fused_bf16(int smem_bytes, int tmem_cols) {
+// Resident CTAs per SM from shared memory (228 KB per SM, 1 KB reserved per
+// CTA, the static barriers + descriptor copy), registers (64 K per SM in four
+// 16 K sub-partition files, warps placed round-robin) and the launch bound;
+// the occupancy API is printed for reference (it under-reports this kernel).
+// Over-subscribing is harmless (tiles are independent), under-subscribing
+// halves the overlap.
+template <int EW>
+int occupancy_ew(int smem_bytes, int tmem_cols) {
     int n = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, fused_bf16_kernel, kBThreads, size_t(smem_bytes)) != cudaSuccess) n = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, fused_bf16_kernel<EW>, Cta<EW>::threads, size_t(smem_bytes)) != cudaSuccess) n = 0;
     cudaFuncAttributes a{};
-    cudaFuncGetAttributes(&a, fused_bf16_kernel);
+    cudaFuncGetAttributes(&a, fused_bf16_kernel<EW>);
     const int by_smem = int((228 * 1024) / (size_t(smem_bytes) + a.sharedSizeBytes + 1024));
-    const int mine = std::max(1, std::min(kMaxCtasPerSm, by_smem));
+    const int warps = Cta<EW>::threads / 32, regs = std::max(a.numRegs, 1);
+    int by_regs = 1;
+    while ((by_regs + 1) * warps <= 64 && ((by_regs + 1) * warps + 3) / 4 * 32 * regs <= 16384) ++by_regs;
+    int occ = std::max(1, std::min(std::min(Cta<EW>::min_blocks, by_regs), by_smem));
     if (std::getenv("XLF_TRACE"))
-        std::fprintf(stderr, "[xlf] occupancy: api %d, smem arithmetic %d (dynamic %d + static %zu)\n", n, mine, smem_bytes,
-                     size_t(a.sharedSizeBytes));
-    int occ = std::max(n, mine);
+        std::fprintf(stderr, "[xlf] occupancy (%d epilogue warps): api %d, arithmetic %d (dynamic %d + static %zu B, %d regs)\n", EW, n,
+                     occ, smem_bytes, size_t(a.sharedSizeBytes), regs);
     // TMEM: 512 columns per SM; a CTA whose tcgen05.alloc cannot be served
     // waits for another CTA to exit, i.e. serialises behind a persistent one
     if (tmem_cols > 0) occ = std::min(occ, std::max(1, 512 / tmem_cols));
     if (const char* f = std::getenv("XLF_CTAS")) occ = std::max(1, std::min(occ, std::atoi(f)));  // profiling aid
     return occ;
+}
+
+}  // namespace
+
+cudaError_t init_fused_bf16() {
+    cudaError_t e = init_ew<4>();
+    return e != cudaSuccess ? e : init_ew<8>();
+}
+
+int occupancy_fused_bf16(int smem_bytes, int tmem_cols, int epi_warps) {
+    return epi_warps == 4 ? occupancy_ew<4>(smem_bytes, tmem_cols) : occupancy_ew<8>(smem_bytes, tmem_cols);
 }
 
 cudaError_t launch_fused_bf16(const BParams& P, int batch, cudaStream_t st, int n0) {
@@ -968,9 +1005,10 @@ cudaError_t launch_fused_bf16(const BParams& P, int batch, cudaStream_t st, int 
     const long long grid = P.grid_all ? tiles : std::min<long long>(tiles, (long long)sms * std::max(1, P.ctas_per_sm));
     if (grid < 1) return cudaSuccess;
     if (P.trace && std::getenv("XLF_TRACE"))
-        std::fprintf(stderr, "[xlf] launch: %lld tiles, grid %lld x %d threads, %d B dynamic shared\n", tiles, grid, kBThreads,
+        std::fprintf(stderr, "[xlf] launch: %lld tiles, grid %lld x %d threads, %d B dynamic shared\n", tiles, grid, P.epi_warps * 32 + 96,
                      P.smem_bytes);
-    fused_bf16_kernel<<<dim3(unsigned(grid)), kBThreads, P.smem_bytes, st>>>(P, batch, n0);
+    if (P.epi_warps == 4) fused_bf16_kernel<4><<<dim3(unsigned(grid)), Cta<4>::threads, P.smem_bytes, st>>>(P, batch, n0);
+    else fused_bf16_kernel<8><<<dim3(unsigned(grid)), Cta<8>::threads, P.smem_bytes, st>>>(P, batch, n0);
     return cudaGetLastError();
 }
 
