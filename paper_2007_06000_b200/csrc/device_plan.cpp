@@ -685,7 +685,7 @@ std::string describe_plan_json(const Graph& g, const DevicePlan& plan) {
         static const char* kinds[] = {"fused", "concat_copy", "add", "relu"};
         os << (i ? "," : "") << "{\"id\":" << q(s.id) << ",\"kind\":" << q(kinds[s.kind]) << ",\"tag\":" << q(s.tag)
            << ",\"mode\":" << q(to_string(s.mode)) << ",\"tile\":[" << s.tile_h << "," << s.tile_w
-           << "],\"out\":[" << s.out_h << "," << s.out_w << "],\"smem_bytes\":" << s.smem_bytes << ",\"nxb\":" << s.nxb << ",\"wres\":" << s.wres << ",\"ring_slots\":" << s.ring_slots << ",\"grid_all\":" << s.grid_all << ",\"epi_warps\":" << s.epi_warps << ",\"macs\":" << s.macs
+           << "],\"out\":[" << s.out_h << "," << s.out_w << "],\"smem_bytes\":" << s.smem_bytes << ",\"nxb\":" << s.nxb << ",\"wres\":" << s.wres << ",\"ring_slots\":" << s.ring_slots << ",\"grid_all\":" << s.grid_all << ",\"epi_warps\":" << s.epi_warps << ",\"tsets\":" << s.tsets << ",\"macs\":" << s.macs
            << ",\"macs_executed\":" << s.macs_executed << ",\"bytes_algorithmic\":" << s.bytes_algorithmic << ",\"inputs\":[";
         for (size_t k = 0; k < s.inputs.size(); ++k) os << (k ? "," : "") << q(s.inputs[k]);
         os << "],\"layers\":[";

@@ -50,7 +50,7 @@ void bf16_nblocks(int cout, int* nblocks, int* nb) {
     *nb = r16(cdiv(n16, *nblocks));
 }
 
-long long layout_bf16(const Graph& g, const StepSpec& s, int th, int tw, BParams* P, int nxb, int wres, int ring_slots) {
+long long layout_bf16(const Graph& g, const StepSpec& s, int th, int tw, BParams* P, int nxb, int wres, int ring_slots, int tsets) {
     const int nops = int(s.ops.size());
     if (nops > kBMaxOps || s.inputs.size() > size_t(kMaxIns)) return -1;
     struct G {
@@ -356,6 +356,7 @@ long long layout_bf16(const Graph& g, const StepSpec& s, int th, int tw, BParams
         xstride = (bytes + 1023) & ~1023LL;
         bytes = xstride + std::max(in_end, in_read);
     }
+    if (tsets == 2 && (nxb != 2 || !any_mma || 2 * pow2_cols(tmem) > 512)) return -1;
     if (P) {
         std::memset(static_cast<void*>(P), 0, sizeof(BParams));
         P->nins = int(ins.size());
@@ -376,6 +377,7 @@ long long layout_bf16(const Graph& g, const StepSpec& s, int th, int tw, BParams
         P->cgroups = s.ctile ? r8(g.shape_of(s.inputs[0]).channels) / s.ctile : 1;
         P->tmem_cols = pow2_cols(tmem);
         P->nxb = nxb, P->xstride = int(xstride);
+        P->tsets = tsets;
         P->gap_off = int(gap_off);
     }
     return bytes;
@@ -427,13 +429,14 @@ std::vector<BCandidate> candidates_bf16(const Graph& g, const StepSpec& s, int b
     std::vector<BCandidate> out;
     BParams* P = new BParams;
     for (int ew : {8, 4})
-    for (int nxb = 1; nxb <= 2; ++nxb)
+    for (int ts = 1; ts <= 2; ++ts)
+    for (int nxb = ts; nxb <= 2; ++nxb)
         for (const WMode& wm : wmodes) {
             if (force && nxb != force) continue;
             if (force_w >= 0 && wm.wres != force_w) continue;
             for (int th = 1; th <= std::min(s.out_h, 32); ++th)
                 for (int tw = 1; tw <= std::min(s.out_w, 32); ++tw) {
-                    const long long sm = layout_bf16(g, s, th, tw, P, nxb, wm.wres, wm.slots);
+                    const long long sm = layout_bf16(g, s, th, tw, P, nxb, wm.wres, wm.slots, ts);
                     if (sm < 0 || sm > smem_budget) continue;
                     if (wm.wres && !P->wres) continue;  // no MMA op: the ring/resident choice is moot
                     double in_bytes = 0, mma = 0, simt = 0;
@@ -449,7 +452,7 @@ std::vector<BCandidate> candidates_bf16(const Graph& g, const StepSpec& s, int b
                     const double tiles = double(P->grid_h) * P->grid_w * P->cgroups * std::max(batch_hint, 1);
                     // 228 KB per SM; per CTA: dynamic + static (~4 KB) + 1 KB driver reserve
                     int occ = std::max(1, std::min(max_ctas_per_sm(ew), int((228 * 1024) / (sm + 5120))));
-                    if (P->tmem_cols) occ = std::min(occ, 512 / P->tmem_cols);
+                    if (P->tmem_cols) occ = std::min(occ, 512 / (P->tmem_cols * ts));
                     double wbytes = 0;  // weights each tile streams from L2 through the ring
                     for (int i = 0; i < P->nops; ++i)
                         if (P->ops[i].kind == BOP_MMA) wbytes += double(P->ops[i].nblocks) * P->ops[i].ksteps * P->ops[i].nb * 32;
@@ -457,13 +460,22 @@ std::vector<BCandidate> candidates_bf16(const Graph& g, const StepSpec& s, int b
                     const double load = in_bytes / 24.0 + 1000.0;
                     // epilogue / SIMT work spreads over the epilogue warps
                     const double compute = out_bytes / 48.0 + wcost + mma / 8192.0 + simt / 128.0 * (8.0 / ew) + 800.0 * P->ngroups;
-                    const double per_tile = nxb == 2 ? std::max(load, compute) : load + compute;
+                    // two accumulator sets hide the MMA time behind the previous tile's epilogue
+                    const double per_tile = (nxb == 2 ? std::max(load, compute) : load + compute) - (ts == 2 ? mma / 8192.0 : 0.0);
                     const double t = std::max(std::ceil(tiles / (148.0 * occ)) * per_tile,
                                               tiles * (in_bytes + out_bytes) / (148.0 * 24.0));
-                    out.push_back({th, tw, nxb, P->wres, wm.slots, int(sm), ew, t});
+                    out.push_back({th, tw, nxb, P->wres, wm.slots, int(sm), ew, ts, t});
                 }
         }
     delete P;
+    // testing aid: XLF_TSETS=2 keeps only double-buffered configurations when any exists
+    if (const char* e = std::getenv("XLF_TSETS")) {
+        const int want = std::atoi(e);
+        std::vector<BCandidate> keep;
+        for (const BCandidate& c : out)
+            if (c.tsets == want) keep.push_back(c);
+        if (!keep.empty()) out.swap(keep);
+    }
     std::stable_sort(out.begin(), out.end(), [](const BCandidate& a, const BCandidate& b) {
         if (a.model < b.model * 0.999) return true;
         if (b.model < a.model * 0.999) return false;
@@ -481,7 +493,7 @@ static bool choose_tile_bf16_at(const Graph& g, StepSpec& s, int batch_hint, int
 
 void apply_candidate(StepSpec& s, const BCandidate& c) {
     s.tile_h = c.th, s.tile_w = c.tw, s.smem_bytes = c.smem, s.nxb = c.nxb, s.wres = c.wres, s.ring_slots = c.slots;
-    s.epi_warps = c.epi_warps;
+    s.epi_warps = c.epi_warps, s.tsets = c.tsets;
 }
 
 // bf16 weights of every MMA-eligible conv: [nblock][tap][cin/8][nb][8].

@@ -215,10 +215,10 @@ Engine::Engine(const Graph& g, int device, Partition part, Precision prec, const
 // with its device copy.
 std::unique_ptr<BParams> Engine::build_bparams(const StepSpec& s) {
     auto P = std::make_unique<BParams>();
-    if (layout_bf16(g_, s, s.tile_h, s.tile_w, P.get(), s.nxb, s.wres, s.ring_slots) < 0)
+    if (layout_bf16(g_, s, s.tile_h, s.tile_w, P.get(), s.nxb, s.wres, s.ring_slots, s.tsets) < 0)
         fail(ErrorKind::internal, "step " + s.id + ": bf16 layout failed");
     P->epi_warps = s.epi_warps;
-    P->ctas_per_sm = occupancy_fused_bf16(P->smem_bytes, P->tmem_cols, P->epi_warps);
+    P->ctas_per_sm = occupancy_fused_bf16(P->smem_bytes, P->tmem_cols * P->tsets, P->epi_warps);
     P->grid_all = s.grid_all;
     if (std::getenv("XLF_TRACE"))
         std::fprintf(stderr, "[xlf] step %s: tile %dx%d, %d B shared, %d staging buffer(s), weights %s, %d CTA(s)/SM%s\n",
@@ -300,7 +300,7 @@ std::string Engine::autotune(int batch, int reps, int topk) {
         std::vector<BCandidate> all = candidates_bf16(g_, s, batch, kSmemBudgetBf16), cands;
         std::map<std::tuple<int, int, int, int>, int> per_mode;
         for (const BCandidate& c : all)
-            if (per_mode[{c.nxb, c.wres, c.slots, c.epi_warps}]++ < topk) cands.push_back(c);
+            if (per_mode[{c.nxb, c.wres, c.slots, c.epi_warps * 4 + c.tsets}]++ < topk) cands.push_back(c);
         float best_ms = 1e30f;
         StepSpec best = s;
         std::unique_ptr<BParams> bestP;
@@ -325,8 +325,8 @@ std::string Engine::autotune(int batch, int reps, int topk) {
                 ms /= float(reps);
                 ++tried;
                 if (std::getenv("XLF_TUNE_VERBOSE"))
-                    std::fprintf(stderr, "[xlf] tune %s: tile %dx%d nxb %d wres %d slots %d grid_all %d ew %d smem %d: %.1f us (model %.0f)\n",
-                                 s.id.c_str(), t.tile_h, t.tile_w, t.nxb, t.wres, t.ring_slots, t.grid_all, t.epi_warps, P->smem_bytes,
+                    std::fprintf(stderr, "[xlf] tune %s: tile %dx%d nxb %d wres %d slots %d grid_all %d ew %d ts %d smem %d: %.1f us (model %.0f)\n",
+                                 s.id.c_str(), t.tile_h, t.tile_w, t.nxb, t.wres, t.ring_slots, t.grid_all, t.epi_warps, t.tsets, P->smem_bytes,
                                  ms * 1000.0f, c.model);
                 if (ms < best_ms) {
                     if (bestP) cudaFree(const_cast<void*>(bestP->dev_copy));
@@ -344,7 +344,7 @@ std::string Engine::autotune(int batch, int reps, int topk) {
         js << (first ? "" : ",") << "{\"id\":\"" << s.id << "\",\"tried\":" << tried << ",\"us\":" << best_ms * 1000.0f
            << ",\"tile\":[" << s.tile_h << "," << s.tile_w << "],\"nxb\":" << s.nxb << ",\"wres\":" << s.wres
            << ",\"ring_slots\":" << s.ring_slots << ",\"grid_all\":" << s.grid_all << ",\"epi_warps\":" << s.epi_warps
-           << ",\"smem_bytes\":" << s.smem_bytes << "}";
+           << ",\"tsets\":" << s.tsets << ",\"smem_bytes\":" << s.smem_bytes << "}";
         first = false;
     }
     js << "]";

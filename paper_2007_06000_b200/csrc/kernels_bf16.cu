@@ -252,7 +252,7 @@ __device__ __forceinline__ void issue_op(const BParams& P, const BOp& op, int nb
 }
 
 __device__ void issuer(const BParams& P, uint8_t* smem, uint32_t tmem, int total, uint64_t* bar_x, uint64_t* ring_full,
-                       uint64_t* ring_empty, uint64_t* acc_full, uint64_t* unit_done, uint64_t* bar_w) {
+                       uint64_t* ring_empty, uint64_t* acc_full, uint64_t* unit_done, uint64_t* acc_free, uint64_t* bar_w) {
     int c = 0, k = 0;
     const uint32_t sbase = smem_u32(smem);
     const int G = P.ngroups, nxb = P.nxb;
@@ -262,24 +262,33 @@ __device__ void issuer(const BParams& P, uint8_t* smem, uint32_t tmem, int total
     for (int gi = 0; gi < G; ++gi) any |= P.groups[gi].mma != 0;
     if (!any) return;
     if (P.wres) mbar_sleep_wait(bar_w, 0);
+    const int ts = P.tsets;
     for (int tau = blockIdx.x; tau < total; tau += gridDim.x, ++k) {
         const int b = nxb == 2 ? (k & 1) : 0, use = nxb == 2 ? (k >> 1) : k;
         const int xdelta = b * P.xstride;
+        // accumulator set: with two sets the issuer runs one tile ahead --
+        // tile k+1's MMAs overlap tile k's epilogue
+        const int s = ts == 2 ? (k & 1) : 0, j = ts == 2 ? (k >> 1) : k;
+        uint64_t* ud = unit_done + s * kBMaxUnits;
         mbar_sleep_wait(&bar_x[b], use & 1);
         stamp(P, kTrXLanded, k);
+        if (ts == 2) {
+            if (j > 0) mbar_sleep_wait(&acc_free[s], (j - 1) & 1);  // tile k-2 (same set) fully done
+        }
         for (int gi = 0; gi < G; ++gi) {
-            // earlier units' epilogues done, in order; unit 0 waits for the
-            // previous tile's last unit (TMEM columns and shared buffers free)
-            if (gi > 0) mbar_sleep_wait(&unit_done[gi - 1], k & 1);
-            else if (k > 0) mbar_sleep_wait(&unit_done[G - 1], (k - 1) & 1);
+            // earlier units' epilogues done, in order; with one set, unit 0
+            // waits for the previous tile's last unit (TMEM columns free)
+            if (gi > 0) mbar_sleep_wait(&ud[gi - 1], j & 1);
+            else if (ts == 1 && k > 0) mbar_sleep_wait(&ud[G - 1], (k - 1) & 1);
             const BGroup& Gr = P.groups[gi];
             if (!Gr.mma) continue;
             fence_after();
             if (gi < 2) stamp(P, 29 + 2 * gi, k);  // group's inputs ready, issue starts
             if (!(P.dbg & 8))
-                for (int i = Gr.op0; i < Gr.op1; ++i) issue_op(P, P.ops[i], Gr.nbi, sbase, tmem, c, ring_full, ring_empty, xdelta);
+                for (int i = Gr.op0; i < Gr.op1; ++i)
+                    issue_op(P, P.ops[i], Gr.nbi, sbase, tmem + uint32_t(s * P.tmem_cols), c, ring_full, ring_empty, xdelta);
             if (gi < 2) stamp(P, 30 + 2 * gi, k);  // group issued
-            commit(&acc_full[gi]);
+            commit(&acc_full[s * kBMaxUnits + gi]);
         }
     }
 }
@@ -721,8 +730,8 @@ __global__ void __launch_bounds__(Cta<EW>::threads, Cta<EW>::min_blocks) fused_b
                                                                                         int n0) {
     constexpr int kCompute = Cta<EW>::compute, kWarpX = Cta<EW>::wx, kWarpMma = Cta<EW>::wmma, kWarpW = Cta<EW>::ww;
     extern __shared__ __align__(1024) uint8_t smem[];
-    __shared__ __align__(8) uint64_t bar_x[2], x_free[2], ring_full[kRingMax], ring_empty[kRingMax], acc_full[kBMaxUnits],
-        unit_done[kBMaxUnits];
+    __shared__ __align__(8) uint64_t bar_x[2], x_free[2], ring_full[kRingMax], ring_empty[kRingMax], acc_full[2 * kBMaxUnits],
+        unit_done[2 * kBMaxUnits], acc_free[2];
     __shared__ uint32_t tmem_slot;
     // The descriptor lives in the kernel-parameter constant bank; the op loops
     // index it with run-time op numbers, and indexed constant loads that miss
@@ -740,12 +749,14 @@ __global__ void __launch_bounds__(Cta<EW>::threads, Cta<EW>::min_blocks) fused_b
         for (int i = 0; i < 2; ++i) mbar_init(&bar_x[i], 1), mbar_init(&x_free[i], 1);
         for (int i = 0; i < kRingMax; ++i) mbar_init(&ring_full[i], 1), mbar_init(&ring_empty[i], 1);
         mbar_init(&bar_w, 1);
-        for (int i = 0; i < Pg.ngroups; ++i) mbar_init(&acc_full[i], 1), mbar_init(&unit_done[i], 1);
+        for (int t = 0; t < Pg.tsets; ++t)
+            for (int i = 0; i < Pg.ngroups; ++i) mbar_init(&acc_full[t * kBMaxUnits + i], 1), mbar_init(&unit_done[t * kBMaxUnits + i], 1);
+        mbar_init(&acc_free[0], 1), mbar_init(&acc_free[1], 1);
         mbar_fence_init();
         mbar_expect_tx(&bar_p, uint32_t(sizeof(BParams)));
         bulk_g2s(&Ps, Pg.dev_copy, uint32_t(sizeof(BParams)), &bar_p);
     }
-    if (warp == kWarpMma && Pg.tmem_cols) tmem_alloc(&tmem_slot, Pg.tmem_cols);
+    if (warp == kWarpMma && Pg.tmem_cols) tmem_alloc(&tmem_slot, Pg.tmem_cols * Pg.tsets);
     fence_before();
     __syncthreads();
     fence_after();
@@ -764,7 +775,7 @@ __global__ void __launch_bounds__(Cta<EW>::threads, Cta<EW>::min_blocks) fused_b
         // (elect.sync, not lane == 0: the compiler then knows one thread is
         // active and moves descriptors to uniform registers without the
         // per-MMA ELECT waterfall it emits for a lane-predicated branch)
-        if (elect_one()) issuer(Pg, smem, tmem, total, bar_x, ring_full, ring_empty, acc_full, unit_done, &bar_w);
+        if (elect_one()) issuer(Pg, smem, tmem, total, bar_x, ring_full, ring_empty, acc_full, unit_done, acc_free, &bar_w);
         __syncwarp();
     } else {
         compute_wait<EW>(&bar_p, 0);
@@ -781,19 +792,22 @@ __global__ void __launch_bounds__(Cta<EW>::threads, Cta<EW>::min_blocks) fused_b
         const int gap_np = P.ops[0].gap ? P.ops[0].npad : 0;  // gap steps have one op
         const int nxb = P.nxb;
         int k = 0;
+        const int ts = P.tsets;
         for (int tau = blockIdx.x; tau < total; tau += gridDim.x, ++k) {
             const BTile t = tile_at(P, tau, n0);
             const int b = nxb == 2 ? (k & 1) : 0, use = nxb == 2 ? (k >> 1) : k;
             const int xdelta = b * P.xstride;
+            const int s = ts == 2 ? (k & 1) : 0, j = ts == 2 ? (k >> 1) : k;
+            const uint32_t tm = tmem + uint32_t(s * P.tmem_cols);
             bool have_x = false;
             for (int gi = 0; gi < P.ngroups; ++gi) {
                 const BGroup& G = P.groups[gi];
                 if (G.mma) {
-                    compute_wait<EW>(&acc_full[gi], k & 1);
+                    compute_wait<EW>(&acc_full[s * kBMaxUnits + gi], j & 1);
                     if (threadIdx.x == 0) stamp(P, kTrUnit + 2 * gi, k);
                     fence_after();
                     if (!(P.dbg & 2))
-                        for (int i = G.op0; i < G.op1; ++i) epilogue_mma<EW>(P, P.ops[i], G.nbi, smem, tmem, t);
+                        for (int i = G.op0; i < G.op1; ++i) epilogue_mma<EW>(P, P.ops[i], G.nbi, smem, tm, t);
                 } else {
                     const BOp& op = P.ops[G.op0];
                     if (!have_x) compute_wait<EW>(&bar_x[b], use & 1), have_x = true;
@@ -803,11 +817,14 @@ __global__ void __launch_bounds__(Cta<EW>::threads, Cta<EW>::min_blocks) fused_b
                 fence_async_smem();  // epilogue-written buffers are read by later MMAs (async proxy)
                 fence_before();
                 named_sync_compute<EW>();
-                if (threadIdx.x == 0) mbar_arrive(&unit_done[gi]), stamp(P, kTrUnit + 2 * gi + 1, k);
+                if (threadIdx.x == 0) mbar_arrive(&unit_done[s * kBMaxUnits + gi]), stamp(P, kTrUnit + 2 * gi + 1, k);
             }
             // every unit of this tile is done (MMAs complete, SIMT reads
-            // finished): its staging buffer may be refilled
-            if (threadIdx.x == 0) mbar_arrive(&x_free[b]), stamp(P, kTrEnd, k);
+            // finished): its staging buffer and accumulator set are free
+            if (threadIdx.x == 0) {
+                mbar_arrive(&x_free[b]), stamp(P, kTrEnd, k);
+                if (ts == 2) mbar_arrive(&acc_free[s]);
+            }
             if (gap_np) {  // this tile's column sums -> gap_part[image][tile][c], reset
                 float* gsum = reinterpret_cast<float*>(smem + P.gap_off);
                 const int per_img = P.grid_h * P.grid_w;
@@ -825,7 +842,7 @@ __global__ void __launch_bounds__(Cta<EW>::threads, Cta<EW>::min_blocks) fused_b
     fence_before();
     __syncthreads();
     fence_after();
-    if (warp == kWarpMma && Pg.tmem_cols) tmem_free(tmem, Pg.tmem_cols);
+    if (warp == kWarpMma && Pg.tmem_cols) tmem_free(tmem, Pg.tmem_cols * Pg.tsets);
 }
 
 // ----------------------------------------------------------------- layout kernels (bf16)
@@ -994,7 +1011,7 @@ cudaError_t init_fused_bf16() {
     return e != cudaSuccess ? e : init_ew<8>();
 }
 
-int occupancy_fused_bf16(int smem_bytes, int tmem_cols, int epi_warps) {
+int occupancy_fused_bf16(int smem_bytes, int tmem_cols, int epi_warps) {  // tmem_cols: per CTA (all sets)
     return epi_warps == 4 ? occupancy_ew<4>(smem_bytes, tmem_cols) : occupancy_ew<8>(smem_bytes, tmem_cols);
 }
 
