@@ -583,10 +583,21 @@ void Engine::run_host(const float* h_in, int batch, const std::string& out_name,
         for (int k = 0; k < 2 * kMaxChunks; ++k) cuda_check(cudaEventCreateWithFlags(&chunk_ev_[k], cudaEventDisableTiming), "event");
         cuda_check(cudaMalloc(&out_staging_, staging_floats_ * 4), "cudaMalloc(output staging)");
     }
-    chunks = std::min(chunks, int(kMaxChunks));
+    chunks = std::min(chunks, int(kMaxChunks) - 1);
+    // Chunk boundaries: equal chunks (measured best); XLF_E2E_RAMP=1 makes the
+    // first and last half size (the first H2D and the last forward are the
+    // only stages nothing overlaps): chunks + 1 pieces of 1/2, 1, ..., 1, 1/2.
+    std::vector<int> cut{0};
+    const bool ramp = std::getenv("XLF_E2E_RAMP") && chunks >= 2 && chunks + 1 <= batch;
+    const int pieces = ramp ? chunks + 1 : chunks;
+    for (int c = 1; c < pieces; ++c) {
+        const double w = ramp ? (c - 0.5) / chunks : double(c) / chunks;  // cumulative share
+        cut.push_back(std::max(cut.back() + 1, std::min(batch - (pieces - c), int(batch * w + 0.5))));
+    }
+    cut.push_back(batch);
     const TensorSlot& xin = slot(in.name);
-    for (int c = 0; c < chunks; ++c) {
-        const int n0 = int((long long)batch * c / chunks), n1 = int((long long)batch * (c + 1) / chunks), cnt = n1 - n0;
+    for (int c = 0; c < pieces; ++c) {
+        const int n0 = cut[size_t(c)], n1 = cut[size_t(c) + 1], cnt = n1 - n0;
         float* dst = staging_ + size_t(n0) * img_in;
         cuda_check(cudaMemcpyAsync(dst, h_in + size_t(n0) * img_in, size_t(cnt) * img_in * 4, cudaMemcpyHostToDevice, copy_in_),
                    "H2D input chunk");
