@@ -35,7 +35,7 @@ constexpr int kRingSlots = 3;
 // CTA shapes: 4 or 8 epilogue/SIMT warps + 3 role warps (input producer,
 // MMA issuer, weight producer); the kernel is instantiated for both and the
 // step's descriptor (epi_warps) selects one.  Resident CTAs per SM: <= 3 / 2.
-constexpr int max_ctas_per_sm(int epi_warps) { return epi_warps <= 4 ? 3 : 2; }
+constexpr int max_ctas_per_sm(int epi_warps) { return epi_warps <= 4 ? 4 : 2; }
 constexpr int kChunkBytes = 16 * 1024;  // weight ring slot
 // Dynamic shared memory per CTA: 227 KB minus the static part (barriers, the
 // descriptor copy: 4 KB) minus 4 KB headroom (ncu's replay needs some).

@@ -52,7 +52,7 @@ struct Cta {
     static constexpr int threads = compute + 96;
     static constexpr int wx = EW, wmma = EW + 1, ww = EW + 2;
     static constexpr int halves = compute / 128;   // epilogue warp groups splitting the accumulator columns
-    static constexpr int min_blocks = EW <= 4 ? 3 : 2;
+    static constexpr int min_blocks = EW <= 4 ? 4 : 2;
 };
 
 struct BTile {
