@@ -2,6 +2,7 @@
 #include "bf16_params.hpp"
 
 #include <algorithm>
+#include <cstdlib>
 #include <cmath>
 #include <functional>
 #include <set>
@@ -510,6 +511,8 @@ DevicePlan plan_device(const Graph& g, Partition part, int batch_hint, int smem_
     // read the same single tensor and whose outputs share one extent run as
     // one kernel (one staged input region), if the union still fits.
     if (part == Partition::b200) {
+        double mb_max_weight = -1;
+        if (const char* e = std::getenv("XLF_MB_MAXW")) mb_max_weight = std::atof(e);
         std::vector<char> gone(steps.size(), 0);
         for (size_t i = 0; i < steps.size(); ++i) {
             if (gone[i] || steps[i].kind != StepSpec::FUSED || steps[i].inputs.size() != 1) continue;
@@ -538,6 +541,14 @@ DevicePlan plan_device(const Graph& g, Partition part, int batch_hint, int smem_
                 m.id += "+" + steps[j].id;
                 m.tag = "multi-branch";
                 m.mode = FusionMode::merge;
+                if (mb_max_weight >= 0) {  // experiment knob: cap on the merged kernel's conv weights (bytes)
+                    double wb = 0;
+                    for (const OpSpec& op : m.ops) {
+                        const Layer& l = *g.find_layer(op.layer);
+                        if (l.kind == LayerKind::conv) wb += double(l.conv->weight_count()) * (bf16 ? 2 : 4);
+                    }
+                    if (wb > mb_max_weight) continue;
+                }
                 if (!tile(m)) continue;
                 steps[i] = m;
                 gone[j] = 1;
