@@ -130,6 +130,7 @@ struct alignas(64) BParams {
     int ctas_per_sm;  // resident CTAs per SM at smem_bytes (grid = 148 x this, capped by the tiles)
     int grid_all;     // 1: grid = tiles (each CTA one tile), else the persistent grid
     int epi_warps;    // 4 or 8 epilogue/SIMT warps (kernel instantiation)
+    int kind;         // step class (kernel instantiation): 0 MMA ops only, 1 with SIMT ops, 2 conv + global average pool
     int tsets;        // accumulator sets in TMEM (2: tile k+1's MMAs run during tile k's epilogue; needs nxb = 2)
     // Optional phase trace (XLF_TRACE=1): globaltimer stamps of CTAs with
     // blockIdx.y == 0 and blockIdx.x < kTraceCtas, kTraceEvents each.

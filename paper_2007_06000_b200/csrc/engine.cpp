@@ -31,7 +31,8 @@ cudaError_t init_fused_bf16();
 cudaError_t launch_fused_bf16(const BParams& P, int batch, cudaStream_t st, int n0 = 0);
 cudaError_t launch_gap_finish_bf16(const float* part, int tiles, int np, float scale, __nv_bfloat16* out, int cs, int coff, int C, int n0,
                                    int N, cudaStream_t st);
-int occupancy_fused_bf16(int smem_bytes, int tmem_cols, int epi_warps);
+int occupancy_fused_bf16(int smem_bytes, int tmem_cols, int epi_warps, int kind);
+int step_kind_bf16(const BParams& P);
 cudaError_t launch_nchw_to_nhwc_bf16(const float* src, __nv_bfloat16* dst, int N, int C, int H, int W, int cs, cudaStream_t st);
 cudaError_t launch_nhwc_bf16_to_nchw(const __nv_bfloat16* src, int cs, int coff, float* dst, int N, int C, int H, int W,
                                      cudaStream_t st);
@@ -218,7 +219,8 @@ std::unique_ptr<BParams> Engine::build_bparams(const StepSpec& s) {
     if (layout_bf16(g_, s, s.tile_h, s.tile_w, P.get(), s.nxb, s.wres, s.ring_slots, s.tsets) < 0)
         fail(ErrorKind::internal, "step " + s.id + ": bf16 layout failed");
     P->epi_warps = s.epi_warps;
-    P->ctas_per_sm = occupancy_fused_bf16(P->smem_bytes, P->tmem_cols * P->tsets, P->epi_warps);
+    P->kind = step_kind_bf16(*P);
+    P->ctas_per_sm = occupancy_fused_bf16(P->smem_bytes, P->tmem_cols * P->tsets, P->epi_warps, P->kind);
     P->grid_all = s.grid_all;
     if (std::getenv("XLF_TRACE"))
         std::fprintf(stderr, "[xlf] step %s: tile %dx%d, %d B shared, %d staging buffer(s), weights %s, %d CTA(s)/SM%s\n",

@@ -495,7 +495,7 @@ __device__ __forceinline__ void finish_gap(const EpiOp& e, bool take, int ch0, i
 // (row = tid % 128) owns TMEM lane `row` = GEMM row = one cell.  With two
 // warp groups, narrow ops (<= 32 columns) split the M tiles between them,
 // wider ones split the columns in 32-column slices.
-template <int EW>
+template <int EW, bool GAP>
 __device__ void epilogue_mma(const BParams& P, const BOp& op, int nbi, uint8_t* smem, uint32_t tmem, const BTile& t) {
     constexpr int kHalves = Cta<EW>::halves;
     const EpiOp e = epi_op(P, op, smem);
@@ -519,7 +519,7 @@ __device__ void epilogue_mma(const BParams& P, const BOp& op, int nbi, uint8_t* 
             valid = r < ext_h && c < ext_w;
         }
         const CellDst d = cell_dst(e, t, r, c, valid);
-        if (op.gap) {
+        if (GAP) {
             float* gsum = reinterpret_cast<float*>(smem + P.gap_off);
             const bool take = valid && d.inside;
             for (int col = col0; col < nb; col += cstep) finish_gap(e, take, chbase + col, min(32, nb - col), tbase + mt * nb + col, gsum);
@@ -725,7 +725,13 @@ __device__ void simt_conv(const BParams& P, const BOp& op, uint8_t* smem, const 
     }
 }
 
-template <int EW>
+// KIND (compile-time step class): kMmaOnly steps (fire modules, plain convs)
+// carry no SIMT / pool / global-average-pool code, so their register
+// allocation is not set by those paths; kSimt adds pools / stride-2 convs /
+// adds; kGap is the conv + global-average-pool epilogue.
+enum : int { kMmaOnly = 0, kSimt = 1, kGap = 2 };
+
+template <int EW, int KIND>
 __global__ void __launch_bounds__(Cta<EW>::threads, Cta<EW>::min_blocks) fused_bf16_kernel(const __grid_constant__ BParams Pg, int batch,
                                                                                         int n0) {
     constexpr int kCompute = Cta<EW>::compute, kWarpX = Cta<EW>::wx, kWarpMma = Cta<EW>::wmma, kWarpW = Cta<EW>::ww;
@@ -789,7 +795,7 @@ __global__ void __launch_bounds__(Cta<EW>::threads, Cta<EW>::min_blocks) fused_b
                 for (int k = threadIdx.x; k < 4 * op.npad; k += kCompute) reinterpret_cast<float*>(smem + P.gap_off)[k] = 0.0f;
         }
         named_sync_compute<EW>();
-        const int gap_np = P.ops[0].gap ? P.ops[0].npad : 0;  // gap steps have one op
+        const int gap_np = KIND == kGap ? P.ops[0].npad : 0;  // gap steps have one op
         const int nxb = P.nxb;
         int k = 0;
         const int ts = P.tsets;
@@ -807,12 +813,14 @@ __global__ void __launch_bounds__(Cta<EW>::threads, Cta<EW>::min_blocks) fused_b
                     if (threadIdx.x == 0) stamp(P, kTrUnit + 2 * gi, k);
                     fence_after();
                     if (!(P.dbg & 2))
-                        for (int i = G.op0; i < G.op1; ++i) epilogue_mma<EW>(P, P.ops[i], G.nbi, smem, tm, t);
+                        for (int i = G.op0; i < G.op1; ++i) epilogue_mma<EW, KIND == kGap>(P, P.ops[i], G.nbi, smem, tm, t);
                 } else {
-                    const BOp& op = P.ops[G.op0];
-                    if (!have_x) compute_wait<EW>(&bar_x[b], use & 1), have_x = true;
-                    if (op.kind == BOP_SIMT_CONV) simt_conv<EW>(P, op, smem, t, xdelta);
-                    else simt_pool_add<EW>(P, op, smem, t, xdelta);
+                    if constexpr (KIND == kSimt) {
+                        const BOp& op = P.ops[G.op0];
+                        if (!have_x) compute_wait<EW>(&bar_x[b], use & 1), have_x = true;
+                        if (op.kind == BOP_SIMT_CONV) simt_conv<EW>(P, op, smem, t, xdelta);
+                        else simt_pool_add<EW>(P, op, smem, t, xdelta);
+                    }
                 }
                 fence_async_smem();  // epilogue-written buffers are read by later MMAs (async proxy)
                 fence_before();
@@ -825,7 +833,7 @@ __global__ void __launch_bounds__(Cta<EW>::threads, Cta<EW>::min_blocks) fused_b
                 mbar_arrive(&x_free[b]), stamp(P, kTrEnd, k);
                 if (ts == 2) mbar_arrive(&acc_free[s]);
             }
-            if (gap_np) {  // this tile's column sums -> gap_part[image][tile][c], reset
+            if (KIND == kGap) {  // this tile's column sums -> gap_part[image][tile][c], reset
                 float* gsum = reinterpret_cast<float*>(smem + P.gap_off);
                 const int per_img = P.grid_h * P.grid_w;
                 float* dst = P.gap_part + (size_t(t.n) * per_img + t.ty * P.grid_w + t.tx) * gap_np;
@@ -972,9 +980,13 @@ namespace {
 template <int EW>
 cudaError_t init_ew() {
     // 227 KB per block minus the static part (barriers + the BParams copy) and headroom
-    cudaError_t e = cudaFuncSetAttribute(fused_bf16_kernel<EW>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBudgetBf16);
-    if (e != cudaSuccess) return e;
-    return cudaFuncSetAttribute(fused_bf16_kernel<EW>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    for (auto fn : {fused_bf16_kernel<EW, kMmaOnly>, fused_bf16_kernel<EW, kSimt>, fused_bf16_kernel<EW, kGap>}) {
+        cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBudgetBf16);
+        if (e != cudaSuccess) return e;
+        e = cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+        if (e != cudaSuccess) return e;
+    }
+    return cudaSuccess;
 }
 
 // Resident CTAs per SM from shared memory (228 KB per SM, 1 KB reserved per
@@ -983,12 +995,13 @@ cudaError_t init_ew() {
 // the occupancy API is printed for reference (it under-reports this kernel).
 // Over-subscribing is harmless (tiles are independent), under-subscribing
 // halves the overlap.
-template <int EW>
+template <int EW, int KIND>
 int occupancy_ew(int smem_bytes, int tmem_cols) {
     int n = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, fused_bf16_kernel<EW>, Cta<EW>::threads, size_t(smem_bytes)) != cudaSuccess) n = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, fused_bf16_kernel<EW, KIND>, Cta<EW>::threads, size_t(smem_bytes)) != cudaSuccess)
+        n = 0;
     cudaFuncAttributes a{};
-    cudaFuncGetAttributes(&a, fused_bf16_kernel<EW>);
+    cudaFuncGetAttributes(&a, fused_bf16_kernel<EW, KIND>);
     const int by_smem = int((228 * 1024) / (size_t(smem_bytes) + a.sharedSizeBytes + 1024));
     const int warps = Cta<EW>::threads / 32, regs = std::max(a.numRegs, 1);
     int by_regs = 1;
@@ -1011,8 +1024,21 @@ cudaError_t init_fused_bf16() {
     return e != cudaSuccess ? e : init_ew<8>();
 }
 
-int occupancy_fused_bf16(int smem_bytes, int tmem_cols, int epi_warps) {  // tmem_cols: per CTA (all sets)
-    return epi_warps == 4 ? occupancy_ew<4>(smem_bytes, tmem_cols) : occupancy_ew<8>(smem_bytes, tmem_cols);
+int occupancy_fused_bf16(int smem_bytes, int tmem_cols, int epi_warps, int kind) {  // tmem_cols: per CTA (all sets)
+    if (epi_warps == 4)
+        return kind == kGap ? occupancy_ew<4, kGap>(smem_bytes, tmem_cols)
+               : kind == kSimt ? occupancy_ew<4, kSimt>(smem_bytes, tmem_cols) : occupancy_ew<4, kMmaOnly>(smem_bytes, tmem_cols);
+    return kind == kGap ? occupancy_ew<8, kGap>(smem_bytes, tmem_cols)
+           : kind == kSimt ? occupancy_ew<8, kSimt>(smem_bytes, tmem_cols) : occupancy_ew<8, kMmaOnly>(smem_bytes, tmem_cols);
+}
+
+// Step class of a descriptor (selects the kernel instantiation).
+int step_kind_bf16(const BParams& P) {
+    for (int i = 0; i < P.nops; ++i)
+        if (P.ops[i].gap) return kGap;
+    for (int i = 0; i < P.nops; ++i)
+        if (P.ops[i].kind != BOP_MMA) return kSimt;
+    return kMmaOnly;
 }
 
 cudaError_t launch_fused_bf16(const BParams& P, int batch, cudaStream_t st, int n0) {
@@ -1024,8 +1050,18 @@ cudaError_t launch_fused_bf16(const BParams& P, int batch, cudaStream_t st, int 
     if (P.trace && std::getenv("XLF_TRACE"))
         std::fprintf(stderr, "[xlf] launch: %lld tiles, grid %lld x %d threads, %d B dynamic shared\n", tiles, grid, P.epi_warps * 32 + 96,
                      P.smem_bytes);
-    if (P.epi_warps == 4) fused_bf16_kernel<4><<<dim3(unsigned(grid)), Cta<4>::threads, P.smem_bytes, st>>>(P, batch, n0);
-    else fused_bf16_kernel<8><<<dim3(unsigned(grid)), Cta<8>::threads, P.smem_bytes, st>>>(P, batch, n0);
+    const dim3 g(static_cast<unsigned>(grid), 1u, 1u);
+#define XLF_LAUNCH(EWV, K) fused_bf16_kernel<EWV, K><<<g, Cta<EWV>::threads, P.smem_bytes, st>>>(P, batch, n0)
+    if (P.epi_warps == 4) {
+        if (P.kind == kGap) XLF_LAUNCH(4, kGap);
+        else if (P.kind == kSimt) XLF_LAUNCH(4, kSimt);
+        else XLF_LAUNCH(4, kMmaOnly);
+    } else {
+        if (P.kind == kGap) XLF_LAUNCH(8, kGap);
+        else if (P.kind == kSimt) XLF_LAUNCH(8, kSimt);
+        else XLF_LAUNCH(8, kMmaOnly);
+    }
+#undef XLF_LAUNCH
     return cudaGetLastError();
 }
 
