@@ -432,8 +432,6 @@ std::vector<BCandidate> candidates_bf16(const Graph& g, const StepSpec& s, int b
     for (int ts = 1; ts <= 2; ++ts)
     for (int nxb = ts; nxb <= 2; ++nxb)
         for (const WMode& wm : wmodes) {
-            if (force && nxb != force) continue;
-            if (force_w >= 0 && wm.wres != force_w) continue;
             for (int th = 1; th <= std::min(s.out_h, 32); ++th)
                 for (int tw = 1; tw <= std::min(s.out_w, 32); ++tw) {
                     const long long sm = layout_bf16(g, s, th, tw, P, nxb, wm.wres, wm.slots, ts);
@@ -468,13 +466,19 @@ std::vector<BCandidate> candidates_bf16(const Graph& g, const StepSpec& s, int b
                 }
         }
     delete P;
-    // testing aid: XLF_TSETS=2 keeps only double-buffered configurations when any exists
-    if (const char* e = std::getenv("XLF_TSETS")) {
-        const int want = std::atoi(e);
+    // testing aids (XLF_XBUF / XLF_WRES / XLF_TSETS): keep only the matching
+    // configurations when any exists for this step
+    auto prefer = [&](auto pred) {
         std::vector<BCandidate> keep;
         for (const BCandidate& c : out)
-            if (c.tsets == want) keep.push_back(c);
+            if (pred(c)) keep.push_back(c);
         if (!keep.empty()) out.swap(keep);
+    };
+    if (force) prefer([&](const BCandidate& c) { return c.nxb == force; });
+    if (force_w >= 0) prefer([&](const BCandidate& c) { return c.wres == force_w; });
+    if (const char* e = std::getenv("XLF_TSETS")) {
+        const int want = std::atoi(e);
+        prefer([&](const BCandidate& c) { return c.tsets == want; });
     }
     std::stable_sort(out.begin(), out.end(), [](const BCandidate& a, const BCandidate& b) {
         if (a.model < b.model * 0.999) return true;

@@ -135,3 +135,35 @@ def test_bf16_forwards_are_bitwise_reproducible(name, batch):
     for n in names:
         for o in outs[1:]:
             assert torch.equal(outs[0][n], o[n]), n
+
+
+FORCED = [
+    {"XLF_XBUF": "1", "XLF_WRES": "0"},
+    {"XLF_XBUF": "2", "XLF_WRES": "1"},
+    {"XLF_XBUF": "2", "XLF_TSETS": "2"},
+    {"XLF_XBUF": "1", "XLF_WRES": "1", "XLF_CTAS": "1"},
+]
+
+
+@pytest.mark.parametrize("env", FORCED, ids=lambda d: ",".join(f"{k[4:]}={v}" for k, v in d.items()))
+@pytest.mark.parametrize("name", ["fire", "inc3a", "straight", "residual", "squeezenet11"])
+def test_bf16_forced_configurations(name, env, monkeypatch):
+    """Every staging / weight-residency / accumulator-set / occupancy mode the
+    tuner may pick computes the same function (bf16 tolerance vs the oracle)."""
+    import torch
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    text = graph_text(name)
+    og = O.load_graph(text)
+    w = O.seeded_weights(og, 3)
+    batch = 3
+    x = O.seeded_batch(og, 5, batch)
+    g = X.Graph(text)
+    e = X.Engine(g, O.flat_weights(og, w), "b200", "bf16", max_batch=batch)
+    e.set_input(torch.from_numpy(x).cuda())
+    e.forward(batch)
+    sample = [0, batch - 1]
+    ref = O.run_batch(og, x[sample], w, og.outputs, threads=2)
+    for o in og.outputs:
+        err = O.normwise(e.read(o, batch).cpu().numpy()[sample], ref[o])
+        assert err <= TOL, (name, env, o, err)
