@@ -301,8 +301,21 @@ std::string Engine::autotune(int batch, int reps, int topk) {
         // but not across modes: keep the best `topk` of every mode
         std::vector<BCandidate> all = candidates_bf16(g_, s, batch, kSmemBudgetBf16), cands;
         std::map<std::tuple<int, int, int, int>, int> per_mode;
-        for (const BCandidate& c : all)
-            if (per_mode[{c.nxb, c.wres, c.slots, c.epi_warps * 4 + c.tsets}]++ < topk) cands.push_back(c);
+        std::map<std::tuple<int, int, int, int>, const BCandidate*> biggest;  // largest tile of each mode
+        for (const BCandidate& c : all) {
+            const auto key = std::make_tuple(c.nxb, c.wres, c.slots, c.epi_warps * 4 + c.tsets);
+            if (per_mode[key]++ < topk) cands.push_back(c);
+            const BCandidate*& bg = biggest[key];
+            if (!bg || c.th * c.tw > bg->th * bg->tw) bg = &c;
+        }
+        // the model under-rates large tiles (weight re-streaming per tile):
+        // also time the largest feasible tile of every mode
+        for (auto& [key, c] : biggest) {
+            bool have = false;
+            for (const BCandidate& d : cands) have |= d.th == c->th && d.tw == c->tw && d.nxb == c->nxb && d.wres == c->wres &&
+                                                      d.slots == c->slots && d.epi_warps == c->epi_warps && d.tsets == c->tsets;
+            if (!have) cands.push_back(*c);
+        }
         float best_ms = 1e30f;
         StepSpec best = s;
         std::unique_ptr<BParams> bestP;
@@ -631,7 +644,7 @@ void Engine::run_host(const float* h_in, int batch, const std::string& out_name,
 
 int Engine::launches_per_forward() const {
     int n = 0;
-    for (const StepSpec& s : plan_.steps) n += s.kind == StepSpec::CONCAT_COPY ? int(s.inputs.size()) : 1;
+    for (const StepSpec& s : plan_.steps) n += s.kind == StepSpec::CONCAT_COPY ? int(s.inputs.size()) : s.gap_out.empty() ? 1 : 2;
     return n;
 }
 
