@@ -504,6 +504,41 @@ DevicePlan plan_device(const Graph& g, Partition part, int batch_hint, int smem_
             }
             continue;
         }
+        // bf16 B200: fusion is not free -- a fused block stages its producers'
+        // (wider) inputs, so its tiles are smaller and a weight-heavy consumer
+        // re-streams its weights for more tiles.  Keep the block fused only if
+        // the planner's model says it beats its layers run as single kernels
+        // plus the HBM round trip of the intermediates (SURVEY §8f rank 1's
+        // model, the same scores the measured tuner starts from).
+        if (bf16 && part == Partition::b200 && s.kind == StepSpec::FUSED && b.fused() && s.gap_out.empty() &&
+            !std::getenv("XLF_ALWAYS_FUSE")) {
+            const int budget = std::min(smem_budget, kSmemBudgetBf16);
+            const std::vector<BCandidate> fc = candidates_bf16(g, s, batch_hint, budget);
+            double fused = fc.empty() ? 1e300 : fc.front().model, single = 0;
+            std::vector<StepSpec> singles;
+            for (const std::string& m : b.members) {
+                FusionBlock one;
+                one.id = b.id + "." + m;
+                one.members = {m};
+                StepSpec t = step_for_block(g, one);
+                if (t.kind != StepSpec::FUSED) {
+                    single = 1e300;
+                    break;
+                }
+                const std::vector<BCandidate> sc = candidates_bf16(g, t, batch_hint, budget);
+                if (sc.empty()) {
+                    single = 1e300;
+                    break;
+                }
+                apply_candidate(t, sc.front());
+                single += sc.front().model;
+                singles.push_back(t);
+            }
+            if (single < 0.85 * fused) {
+                for (StepSpec& t : singles) steps.push_back(t);
+                continue;
+            }
+        }
         steps.push_back(s);
     }
 
