@@ -534,7 +534,12 @@ DevicePlan plan_device(const Graph& g, Partition part, int batch_hint, int smem_
                 single += sc.front().model;
                 singles.push_back(t);
             }
-            if (single < 0.85 * fused) {
+            bool force_split = false;  // experiment knob: XLF_UNFUSE=<block id>[,<block id>...]
+            if (const char* e = std::getenv("XLF_UNFUSE")) {
+                const std::string list = std::string(",") + e + ",";
+                force_split = list.find("," + b.id + ",") != std::string::npos;
+            }
+            if (force_split || single < 0.85 * fused) {
                 for (StepSpec& t : singles) steps.push_back(t);
                 continue;
             }
