@@ -284,9 +284,8 @@ __device__ void issuer(const BParams& P, uint8_t* smem, uint32_t tmem, int total
             if (!Gr.mma) continue;
             fence_after();
             if (gi < 2) stamp(P, 29 + 2 * gi, k);  // group's inputs ready, issue starts
-            if (!(P.dbg & 8))
-                for (int i = Gr.op0; i < Gr.op1; ++i)
-                    issue_op(P, P.ops[i], Gr.nbi, sbase, tmem + uint32_t(s * P.tmem_cols), c, ring_full, ring_empty, xdelta);
+            for (int i = Gr.op0; i < Gr.op1; ++i)
+                issue_op(P, P.ops[i], Gr.nbi, sbase, tmem + uint32_t(s * P.tmem_cols), c, ring_full, ring_empty, xdelta);
             if (gi < 2) stamp(P, 30 + 2 * gi, k);  // group issued
             commit(&acc_full[s * kBMaxUnits + gi]);
         }
