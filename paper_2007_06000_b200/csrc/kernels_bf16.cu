@@ -74,6 +74,12 @@ __device__ __forceinline__ void stamp(const BParams& P, int ev, int k = 0) {
     }
 }
 
+// Programmatic dependent launch: a step's CTAs start (barriers, TMEM, the
+// descriptor and resident weights) while the previous step drains; reads of
+// the previous step's outputs wait here.
+__device__ __forceinline__ void grid_dependency_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void grid_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
 template <int EW>
 __device__ __forceinline__ void named_sync_compute() { asm volatile("bar.sync 1, %0;\n" ::"n"(Cta<EW>::compute) : "memory"); }
 
@@ -126,6 +132,7 @@ __device__ void x_producer(const BParams& P, const CUtensorMap* xmaps, uint8_t* 
     for (int k = 0; k < P.nins; ++k) bytes += uint32_t(P.in[k].r.c8) * uint32_t(P.in[k].r.ext_h * P.in[k].r.ext_w * 16);
     const int nxb = P.nxb;
     int k = 0;
+    grid_dependency_wait();  // the previous step's outputs are this step's inputs
     for (int tau = blockIdx.x; tau < total; tau += gridDim.x, ++k) {
         const BTile t = tile_at(P, tau, n0);
         const int b = nxb == 2 ? (k & 1) : 0, use = nxb == 2 ? (k >> 1) : k;
@@ -749,6 +756,7 @@ __global__ void __launch_bounds__(Cta<EW>::threads, Cta<EW>::min_blocks) fused_b
     __shared__ __align__(8) uint64_t bar_p, bar_w;
     const int warp = __shfl_sync(0xffffffffu, int(threadIdx.x >> 5), 0), lane = threadIdx.x & 31;  // provably warp-uniform
     const int total = Pg.grid_h * Pg.grid_w * Pg.cgroups * batch;
+    grid_launch_dependents();  // every CTA is resident: the next step may be scheduled as SMs free up
     if (threadIdx.x == 0) {
         mbar_init(&bar_p, 1);
         for (int i = 0; i < 2; ++i) mbar_init(&bar_x[i], 1), mbar_init(&x_free[i], 1);
@@ -798,6 +806,7 @@ __global__ void __launch_bounds__(Cta<EW>::threads, Cta<EW>::min_blocks) fused_b
         const int nxb = P.nxb;
         int k = 0;
         const int ts = P.tsets;
+        grid_dependency_wait();  // global stores after the previous step completed (no write/read overlap)
         for (int tau = blockIdx.x; tau < total; tau += gridDim.x, ++k) {
             const BTile t = tile_at(P, tau, n0);
             const int b = nxb == 2 ? (k & 1) : 0, use = nxb == 2 ? (k >> 1) : k;
@@ -1050,7 +1059,13 @@ cudaError_t launch_fused_bf16(const BParams& P, int batch, cudaStream_t st, int 
         std::fprintf(stderr, "[xlf] launch: %lld tiles, grid %lld x %d threads, %d B dynamic shared\n", tiles, grid, P.epi_warps * 32 + 96,
                      P.smem_bytes);
     const dim3 g(static_cast<unsigned>(grid), 1u, 1u);
-#define XLF_LAUNCH(EWV, K) fused_bf16_kernel<EWV, K><<<g, Cta<EWV>::threads, P.smem_bytes, st>>>(P, batch, n0)
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = g, cfg.blockDim = dim3(unsigned(P.epi_warps * 32 + 96)), cfg.dynamicSmemBytes = size_t(P.smem_bytes), cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = std::getenv("XLF_NO_PDL") ? 0 : 1;
+    cfg.attrs = attr, cfg.numAttrs = 1;
+#define XLF_LAUNCH(EWV, K) cudaLaunchKernelEx(&cfg, fused_bf16_kernel<EWV, K>, P, batch, n0)
     if (P.epi_warps == 4) {
         if (P.kind == kGap) XLF_LAUNCH(4, kGap);
         else if (P.kind == kSimt) XLF_LAUNCH(4, kSimt);
