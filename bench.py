@@ -347,7 +347,7 @@ def main():
             "data": "synthetic (SeededStream(42) inputs generated on device, seeded_weights(42))",
             "config": {"workload": "squeezenet_v1.1 224x224 inference, b200 partition (8 fused fire blocks, conv1+pool1 fused)",
                        "batch_per_gpu": B, "global_batch": B * world, "parallelism": f"batch-sharded dp{world}, no collective",
-                       "l2": "no L2 flush needed: one forward moves ~1.6 GB through HBM (126 MB L2), so each iteration starts with its 103 MB bf16 input evicted"},
+                       "l2": "no L2 flush needed: one forward moves > 1.5 GB through HBM (L2 126 MB), so each iteration starts with its input (103 MB bf16 / 205 MB fp32) evicted"},
             "e2e": {"value": round(world * B / (e2e_ms * 1e-3), 2), "unit": "images/s",
                     "h2d_bytes_per_step": int(B * c * h * wd * 4), "d2h_bytes_per_step": int(B * 1000 * 4),
                     "path": "xlf_engine_run_host (C ABI), pinned host buffers"},
