@@ -66,7 +66,7 @@ class ClockSampler:
         try:
             self.fh = open(self.path, "w")
             self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}", "--format=csv,noheader,nounits",
-                                          "-lms", "100"], stdout=self.fh, stderr=subprocess.DEVNULL)
+                                          "-lms", "25"], stdout=self.fh, stderr=subprocess.DEVNULL)
         except Exception:
             self.proc = None
         time.sleep(0.15)
