@@ -36,7 +36,7 @@ constexpr int kRingSlots = 3;
 // MMA issuer, weight producer); the kernel is instantiated for both and the
 // step's descriptor (epi_warps) selects one.  Resident CTAs per SM: <= 3 / 2.
 constexpr int max_ctas_per_sm(int epi_warps) { return epi_warps <= 4 ? 4 : 2; }
-constexpr int kChunkBytes = 16 * 1024;  // weight ring slot
+constexpr int kChunkBytes = 16 * 1024;  // weight ring slot (smallest; the tuner picks 16 / 32 / 64 KB)
 // Dynamic shared memory per CTA: 227 KB minus the static part (barriers, the
 // descriptor copy: 4 KB) minus 4 KB headroom (ncu's replay needs some).
 constexpr int kSmemBudgetBf16 = 227 * 1024 - 8192;

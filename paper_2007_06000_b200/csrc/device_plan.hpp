@@ -54,6 +54,7 @@ struct StepSpec {
     int grid_all = 0;   // bf16: one tile per CTA (grid = tiles) instead of a persistent grid
     int epi_warps = 8;  // bf16: epilogue/SIMT warps per CTA (4 or 8)
     int tsets = 1;      // bf16: TMEM accumulator sets (2 = cross-tile MMA/epilogue overlap)
+    int ring_chunk = 16384;  // bf16: bytes per weight-ring slot
     // bf16 conv + global average pool (SqueezeNet conv10 -> pool10): the
     // step's single conv op never stores its output; its epilogue reduces
     // every tile over its cells and the pooled layer `gap_out` (1x1) is
@@ -92,12 +93,12 @@ DevicePlan plan_device(const Graph& g, Partition part, int batch_hint = 1, int s
 bool bf16_mma_ok(const Layer& l);
 void bf16_nblocks(int cout, int* nblocks, int* nb);
 long long layout_bf16(const Graph& g, const StepSpec& s, int th, int tw, struct BParams* P, int nxb = 1, int wres = 0,
-                      int ring_slots = 3, int tsets = 1);
+                      int ring_slots = 3, int tsets = 1, int chunk = 16384);
 bool choose_tile_bf16(const Graph& g, StepSpec& s, int batch_hint, int smem_budget);
 // One configuration of a bf16 step: tile, staging buffers, weight residency /
 // ring depth, shared bytes, and the model's score (SM cycles, lower better).
 struct BCandidate {
-    int th, tw, nxb, wres, slots, smem, epi_warps, tsets;
+    int th, tw, nxb, wres, slots, smem, epi_warps, tsets, chunk;
     double model;
 };
 std::vector<BCandidate> candidates_bf16(const Graph& g, const StepSpec& s, int batch_hint, int smem_budget);

@@ -50,7 +50,8 @@ void bf16_nblocks(int cout, int* nblocks, int* nb) {
     *nb = r16(cdiv(n16, *nblocks));
 }
 
-long long layout_bf16(const Graph& g, const StepSpec& s, int th, int tw, BParams* P, int nxb, int wres, int ring_slots, int tsets) {
+long long layout_bf16(const Graph& g, const StepSpec& s, int th, int tw, BParams* P, int nxb, int wres, int ring_slots, int tsets,
+                      int chunk) {
     const int nops = int(s.ops.size());
     if (nops > kBMaxOps || s.inputs.size() > size_t(kMaxIns)) return -1;
     struct G {
@@ -250,7 +251,7 @@ long long layout_bf16(const Graph& g, const StepSpec& s, int th, int tw, BParams
                 if (o.contig) o.strips = 1, o.mtiles = cdiv(o.ext_h * o.ext_w, 128);
                 else o.strips = cdiv(o.ext_w, 8), o.mtiles = o.strips * cdiv(o.ext_h, 16);
                 o.ksteps = o.kh * o.kw * (o.cin / 16);
-                o.chunk_steps = std::max(1, kChunkBytes / (o.nb * 32));
+                o.chunk_steps = std::max(1, chunk / (o.nb * 32));
                 if (o.mtiles * o.nb > 512) return -1;  // TMEM: 512 columns
                 tmem = std::max(tmem, o.mtiles * o.nb);
                 any_mma = true;
@@ -326,7 +327,7 @@ long long layout_bf16(const Graph& g, const StepSpec& s, int th, int tw, BParams
             }
         bytes += wres_bytes;
     } else if (any_mma) {
-        bytes += (long long)ring_slots * kChunkBytes;
+        bytes += (long long)ring_slots * chunk;
     }
     // MMA A-operand reads run past their region: contiguous-M ops read whole
     // 128-row tiles, windowed ops whole 16-row x 8-column blocks shifted by
@@ -370,7 +371,7 @@ long long layout_bf16(const Graph& g, const StepSpec& s, int th, int tw, BParams
         P->ngroups = int(groups.size());
         for (size_t i = 0; i < groups.size(); ++i) P->groups[i] = groups[i];
         P->bias_off = int(bias_off), P->bias_bytes = int(bias_bytes);
-        P->ring_off = int(ring_off), P->chunk_bytes = kChunkBytes, P->ring_slots = ring_slots;
+        P->ring_off = int(ring_off), P->chunk_bytes = chunk, P->ring_slots = ring_slots;
         P->wres = any_mma && wres, P->wres_off = int(wres_off), P->wres_bytes = int(wres_bytes);
         P->smem_bytes = int(bytes);
         P->ctile = s.ctile;
@@ -423,9 +424,12 @@ std::vector<BCandidate> candidates_bf16(const Graph& g, const StepSpec& s, int b
     int force_w = -1;
     if (const char* e = std::getenv("XLF_WRES")) force_w = std::atoi(e);
     struct WMode {
-        int wres, slots;
+        int wres, slots, chunk;
     };
-    const WMode wmodes[] = {{1, 3}, {0, 3}, {0, 6}, {0, 8}};
+    // weights resident, or a ring of `slots` x `chunk` bytes (bytes in flight
+    // per L2 round trip; larger chunks amortise the per-copy latency)
+    const WMode wmodes[] = {{1, 3, kChunkBytes}, {0, 3, kChunkBytes}, {0, 6, kChunkBytes}, {0, 8, kChunkBytes},
+                            {0, 3, 2 * kChunkBytes}, {0, 4, 2 * kChunkBytes}, {0, 2, 4 * kChunkBytes}, {0, 3, 4 * kChunkBytes}};
     std::vector<BCandidate> out;
     BParams* P = new BParams;
     for (int ew : {8, 4})
@@ -434,7 +438,7 @@ std::vector<BCandidate> candidates_bf16(const Graph& g, const StepSpec& s, int b
         for (const WMode& wm : wmodes) {
             for (int th = 1; th <= std::min(s.out_h, 32); ++th)
                 for (int tw = 1; tw <= std::min(s.out_w, 32); ++tw) {
-                    const long long sm = layout_bf16(g, s, th, tw, P, nxb, wm.wres, wm.slots, ts);
+                    const long long sm = layout_bf16(g, s, th, tw, P, nxb, wm.wres, wm.slots, ts, wm.chunk);
                     if (sm < 0 || sm > smem_budget) continue;
                     if (wm.wres && !P->wres) continue;  // no MMA op: the ring/resident choice is moot
                     double in_bytes = 0, mma = 0, simt = 0;
@@ -454,7 +458,7 @@ std::vector<BCandidate> candidates_bf16(const Graph& g, const StepSpec& s, int b
                     double wbytes = 0;  // weights each tile streams from L2 through the ring
                     for (int i = 0; i < P->nops; ++i)
                         if (P->ops[i].kind == BOP_MMA) wbytes += double(P->ops[i].nblocks) * P->ops[i].ksteps * P->ops[i].nb * 32;
-                    const double wcost = P->wres ? 0.0 : wbytes * 2000.0 / (double(wm.slots) * kChunkBytes);
+                    const double wcost = P->wres ? 0.0 : wbytes * 2000.0 / (double(wm.slots) * wm.chunk);
                     const double load = in_bytes / 24.0 + 1000.0;
                     // epilogue / SIMT work spreads over the epilogue warps
                     const double compute = out_bytes / 48.0 + wcost + mma / 8192.0 + simt / 128.0 * (8.0 / ew) + 800.0 * P->ngroups;
@@ -462,7 +466,7 @@ std::vector<BCandidate> candidates_bf16(const Graph& g, const StepSpec& s, int b
                     const double per_tile = (nxb == 2 ? std::max(load, compute) : load + compute) - (ts == 2 ? mma / 8192.0 : 0.0);
                     const double t = std::max(std::ceil(tiles / (148.0 * occ)) * per_tile,
                                               tiles * (in_bytes + out_bytes) / (148.0 * 24.0));
-                    out.push_back({th, tw, nxb, P->wres, wm.slots, int(sm), ew, ts, t});
+                    out.push_back({th, tw, nxb, P->wres, wm.slots, int(sm), ew, ts, wm.chunk, t});
                 }
         }
     delete P;
@@ -497,7 +501,7 @@ static bool choose_tile_bf16_at(const Graph& g, StepSpec& s, int batch_hint, int
 
 void apply_candidate(StepSpec& s, const BCandidate& c) {
     s.tile_h = c.th, s.tile_w = c.tw, s.smem_bytes = c.smem, s.nxb = c.nxb, s.wres = c.wres, s.ring_slots = c.slots;
-    s.epi_warps = c.epi_warps, s.tsets = c.tsets;
+    s.epi_warps = c.epi_warps, s.tsets = c.tsets, s.ring_chunk = c.chunk;
 }
 
 // bf16 weights of every MMA-eligible conv: [nblock][tap][cin/8][nb][8].

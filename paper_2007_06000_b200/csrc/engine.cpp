@@ -216,7 +216,7 @@ Engine::Engine(const Graph& g, int device, Partition part, Precision prec, const
 // with its device copy.
 std::unique_ptr<BParams> Engine::build_bparams(const StepSpec& s) {
     auto P = std::make_unique<BParams>();
-    if (layout_bf16(g_, s, s.tile_h, s.tile_w, P.get(), s.nxb, s.wres, s.ring_slots, s.tsets) < 0)
+    if (layout_bf16(g_, s, s.tile_h, s.tile_w, P.get(), s.nxb, s.wres, s.ring_slots, s.tsets, s.ring_chunk) < 0)
         fail(ErrorKind::internal, "step " + s.id + ": bf16 layout failed");
     P->epi_warps = s.epi_warps;
     P->kind = step_kind_bf16(*P);
@@ -303,7 +303,7 @@ std::string Engine::autotune(int batch, int reps, int topk) {
         std::map<std::tuple<int, int, int, int>, int> per_mode;
         std::map<std::tuple<int, int, int, int>, const BCandidate*> biggest;  // largest tile of each mode
         for (const BCandidate& c : all) {
-            const auto key = std::make_tuple(c.nxb, c.wres, c.slots, c.epi_warps * 4 + c.tsets);
+            const auto key = std::make_tuple(c.nxb, c.wres, c.slots * 1000 + c.chunk / 1024, c.epi_warps * 4 + c.tsets);
             if (per_mode[key]++ < topk) cands.push_back(c);
             const BCandidate*& bg = biggest[key];
             if (!bg || c.th * c.tw > bg->th * bg->tw) bg = &c;
@@ -313,7 +313,8 @@ std::string Engine::autotune(int batch, int reps, int topk) {
         for (auto& [key, c] : biggest) {
             bool have = false;
             for (const BCandidate& d : cands) have |= d.th == c->th && d.tw == c->tw && d.nxb == c->nxb && d.wres == c->wres &&
-                                                      d.slots == c->slots && d.epi_warps == c->epi_warps && d.tsets == c->tsets;
+                                                      d.slots == c->slots && d.epi_warps == c->epi_warps && d.tsets == c->tsets &&
+                                                      d.chunk == c->chunk;
             if (!have) cands.push_back(*c);
         }
         float best_ms = 1e30f;
@@ -358,7 +359,7 @@ std::string Engine::autotune(int batch, int reps, int topk) {
         bparams_[i] = std::move(bestP);
         js << (first ? "" : ",") << "{\"id\":\"" << s.id << "\",\"tried\":" << tried << ",\"us\":" << best_ms * 1000.0f
            << ",\"tile\":[" << s.tile_h << "," << s.tile_w << "],\"nxb\":" << s.nxb << ",\"wres\":" << s.wres
-           << ",\"ring_slots\":" << s.ring_slots << ",\"grid_all\":" << s.grid_all << ",\"epi_warps\":" << s.epi_warps
+           << ",\"ring_slots\":" << s.ring_slots << ",\"ring_chunk\":" << s.ring_chunk << ",\"grid_all\":" << s.grid_all << ",\"epi_warps\":" << s.epi_warps
            << ",\"tsets\":" << s.tsets << ",\"smem_bytes\":" << s.smem_bytes << "}";
         first = false;
     }
