@@ -230,7 +230,7 @@ def main():
         # measured-time tuner (part of the product, before the timed region)
         t_tune = time.time()
         e.forward(B, use_graph=False)
-        chosen = e.autotune(B, reps=3, topk=3)
+        chosen = e.autotune(B, reps=3, topk=int(os.environ.get("XLF_TOPK", "3")))
         tune = {"steps_tuned": len(chosen), "seconds": round(time.time() - t_tune, 2)}
         e.set_input_seeded(42, B, first_image=rank * B)
     nsteps = len(e.steps)
