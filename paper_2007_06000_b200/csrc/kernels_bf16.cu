@@ -46,6 +46,8 @@ using namespace umma;
 // EW epilogue/SIMT warps (4 or 8), then the input producer, MMA issuer and
 // weight producer warps.  Fewer epilogue warps -> fewer registers per CTA ->
 // more CTAs (more independent tile chains) per SM.
+constexpr int kSubs = 4;  // accumulator-ready barriers per group (per op, the last shared by the rest)
+
 template <int EW>
 struct Cta {
     static constexpr int compute = EW * 32;        // warps 0..EW-1: epilogue + SIMT ops
@@ -291,10 +293,16 @@ __device__ void issuer(const BParams& P, uint8_t* smem, uint32_t tmem, int total
             if (!Gr.mma) continue;
             fence_after();
             if (gi < 2) stamp(P, 29 + 2 * gi, k);  // group's inputs ready, issue starts
-            for (int i = Gr.op0; i < Gr.op1; ++i)
+            // one commit per op of the group (the first kSubs-1 ops, then one
+            // for the rest): the epilogue starts on an op while the group's
+            // later ops are still on the tensor cores
+            uint64_t* fb = acc_full + (s * kBMaxUnits + gi) * kSubs;
+            for (int i = Gr.op0; i < Gr.op1; ++i) {
                 issue_op(P, P.ops[i], Gr.nbi, sbase, tmem + uint32_t(s * P.tmem_cols), c, ring_full, ring_empty, xdelta);
+                const int sub = i - Gr.op0;
+                if (sub < kSubs - 1 || i == Gr.op1 - 1) commit(&fb[sub < kSubs - 1 ? sub : kSubs - 1]);
+            }
             if (gi < 2) stamp(P, 30 + 2 * gi, k);  // group issued
-            commit(&acc_full[s * kBMaxUnits + gi]);
         }
     }
 }
@@ -742,7 +750,7 @@ __global__ void __launch_bounds__(Cta<EW>::threads, Cta<EW>::min_blocks) fused_b
                                                                                         int n0) {
     constexpr int kCompute = Cta<EW>::compute, kWarpX = Cta<EW>::wx, kWarpMma = Cta<EW>::wmma, kWarpW = Cta<EW>::ww;
     extern __shared__ __align__(1024) uint8_t smem[];
-    __shared__ __align__(8) uint64_t bar_x[2], x_free[2], ring_full[kRingMax], ring_empty[kRingMax], acc_full[2 * kBMaxUnits],
+    __shared__ __align__(8) uint64_t bar_x[2], x_free[2], ring_full[kRingMax], ring_empty[kRingMax], acc_full[2 * kBMaxUnits * kSubs],
         unit_done[2 * kBMaxUnits], acc_free[2];
     __shared__ uint32_t tmem_slot;
     // The descriptor lives in the kernel-parameter constant bank; the op loops
@@ -763,7 +771,10 @@ __global__ void __launch_bounds__(Cta<EW>::threads, Cta<EW>::min_blocks) fused_b
         for (int i = 0; i < kRingMax; ++i) mbar_init(&ring_full[i], 1), mbar_init(&ring_empty[i], 1);
         mbar_init(&bar_w, 1);
         for (int t = 0; t < Pg.tsets; ++t)
-            for (int i = 0; i < Pg.ngroups; ++i) mbar_init(&acc_full[t * kBMaxUnits + i], 1), mbar_init(&unit_done[t * kBMaxUnits + i], 1);
+            for (int i = 0; i < Pg.ngroups; ++i) {
+                mbar_init(&unit_done[t * kBMaxUnits + i], 1);
+                for (int q = 0; q < kSubs; ++q) mbar_init(&acc_full[(t * kBMaxUnits + i) * kSubs + q], 1);
+            }
         mbar_init(&acc_free[0], 1), mbar_init(&acc_free[1], 1);
         mbar_fence_init();
         mbar_expect_tx(&bar_p, uint32_t(sizeof(BParams)));
@@ -817,11 +828,16 @@ __global__ void __launch_bounds__(Cta<EW>::threads, Cta<EW>::min_blocks) fused_b
             for (int gi = 0; gi < P.ngroups; ++gi) {
                 const BGroup& G = P.groups[gi];
                 if (G.mma) {
-                    compute_wait<EW>(&acc_full[s * kBMaxUnits + gi], j & 1);
-                    if (threadIdx.x == 0) stamp(P, kTrUnit + 2 * gi, k);
-                    fence_after();
-                    if (!(P.dbg & 2))
-                        for (int i = G.op0; i < G.op1; ++i) epilogue_mma<EW, KIND == kGap>(P, P.ops[i], G.nbi, smem, tm, t);
+                    uint64_t* fb = acc_full + (s * kBMaxUnits + gi) * kSubs;
+                    for (int i = G.op0; i < G.op1; ++i) {
+                        const int sub = i - G.op0;
+                        if (sub < kSubs) {  // op `sub`'s accumulators (the last slot covers the rest of the group)
+                            compute_wait<EW>(&fb[sub], j & 1);
+                            if (threadIdx.x == 0 && sub == 0) stamp(P, kTrUnit + 2 * gi, k);
+                            fence_after();
+                        }
+                        if (!(P.dbg & 2)) epilogue_mma<EW, KIND == kGap>(P, P.ops[i], G.nbi, smem, tm, t);
+                    }
                 } else {
                     if constexpr (KIND == kSimt) {
                         const BOp& op = P.ops[G.op0];
