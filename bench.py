@@ -64,26 +64,33 @@ class ClockSampler:
         self.stop = threading.Event()
         self.thread = None
 
+    def _sample(self):
+        N, h = self.nvml, self.handle
+        self.samples.append(float(N.nvmlDeviceGetClockInfo(h, N.NVML_CLOCK_SM)))
+        r = N.nvmlDeviceGetCurrentClocksEventReasons(h)
+        for name, bit in self.REASONS.items():
+            if r & bit:
+                self.reasons.add(name)
+
     def _run(self):
         try:
-            import pynvml as N
-            N.nvmlInit()
-            h = N.nvmlDeviceGetHandleByIndex(self.index)
-            self.max_mhz = float(N.nvmlDeviceGetMaxClockInfo(h, N.NVML_CLOCK_SM))
             while not self.stop.is_set():
-                self.samples.append(float(N.nvmlDeviceGetClockInfo(h, N.NVML_CLOCK_SM)))
-                r = N.nvmlDeviceGetCurrentClocksEventReasons(h)
-                for name, bit in self.REASONS.items():
-                    if r & bit:
-                        self.reasons.add(name)
+                self._sample()
                 time.sleep(0.01)
         except Exception:
             pass
 
     def __enter__(self):
-        self.thread = threading.Thread(target=self._run, daemon=True)
-        self.thread.start()
-        time.sleep(0.02)
+        # NVML set up before the timed region starts; then a sample every 10 ms
+        try:
+            import pynvml as N
+            N.nvmlInit()
+            self.nvml, self.handle = N, N.nvmlDeviceGetHandleByIndex(self.index)
+            self.max_mhz = float(N.nvmlDeviceGetMaxClockInfo(self.handle, N.NVML_CLOCK_SM))
+            self.thread = threading.Thread(target=self._run, daemon=True)
+            self.thread.start()
+        except Exception:
+            self.thread = None
         return self
 
     def __exit__(self, *exc):

@@ -252,7 +252,10 @@ std::unique_ptr<BParams> Engine::build_bparams(const StepSpec& s) {
         const size_t need = size_t(max_batch_) * P->grid_h * P->grid_w * P->ops[0].npad;
         auto& buf = gap_parts_[s.id];
         if (buf.second < need) {
-            if (buf.first) cudaFree(buf.first);
+            // grow only; the old buffer stays allocated until the engine dies
+            // (descriptors built earlier -- the tuner's candidates, the current
+            // step -- may still point at it)
+            if (buf.first) retired_.push_back(buf.first);
             cuda_check(cudaMalloc(&buf.first, need * 4), "cudaMalloc(gap partials)");
             buf.second = need;
         }
@@ -384,6 +387,7 @@ Engine::~Engine() {
     cudaFree(staging_);
     if (out_staging_) cudaFree(out_staging_);
     for (auto& [id, b] : gap_parts_) cudaFree(b.first);
+    for (void* p : retired_) cudaFree(p);
     if (copy_in_) {
         cudaStreamDestroy(copy_in_), cudaStreamDestroy(copy_out_);
         for (cudaEvent_t ev : chunk_ev_) cudaEventDestroy(ev);

@@ -86,6 +86,7 @@ private:
     cudaEvent_t chunk_ev_[2 * kMaxChunks] = {};
     float* out_staging_ = nullptr;
     std::map<std::string, std::pair<float*, size_t>> gap_parts_;  // conv+gap steps: per-tile partial sums
+    std::vector<void*> retired_;                                  // outgrown buffers, freed with the engine
 };
 
 std::vector<float> seeded_weights(const Graph& g, uint64_t seed);  // tensor.cpp:42-62 semantics
