@@ -72,6 +72,9 @@ struct BGroup {
     int op0, op1;  // ops [op0, op1)
     int nbi;       // N block (multi-block MMA ops), else 0
     int mma;       // 1: tensor-core group
+    int tbase;     // first TMEM column of the group (ops add their tcol)
+    int wback;     // the issuer waits for the epilogue of group gi - wback (1: in order;
+                   // 2: N blocks alternating between two column sets)
 };
 
 // Layout of a shared region: K-blocks of kb_ch channels; inside a K-block

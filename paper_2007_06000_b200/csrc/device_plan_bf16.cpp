@@ -276,14 +276,17 @@ long long layout_bf16(const Graph& g, const StepSpec& s, int th, int tw, BParams
     for (int i = 0; i < nops; ++i) {
         BOp& o = ops[size_t(i)];
         if (o.kind != BOP_MMA) {
-            groups.push_back({i, i + 1, 0, 0});
+            groups.push_back({i, i + 1, 0, 0, 0, 1});
             continue;
         }
         const int cols = o.mtiles * o.nb;
         if (o.nblocks > 1) {
-            for (int k = 0; k < o.nblocks; ++k) groups.push_back({i, i + 1, k, 1});
+            // N blocks alternate between two column sets when both fit: block
+            // k+1's MMAs run while the epilogue drains block k
+            const bool alt = 2 * cols <= 512 && !std::getenv("XLF_NO_NALT");
+            for (int k = 0; k < o.nblocks; ++k) groups.push_back({i, i + 1, k, 1, alt ? (k & 1) * cols : 0, alt && k > 0 ? 2 : 1});
             o.tcol = 0;
-            tmem = std::max(tmem, cols);
+            tmem = std::max(tmem, alt ? 2 * cols : cols);
             continue;
         }
         const bool join = !groups.empty() && groups.back().mma && groups.back().op1 == i &&
@@ -296,7 +299,7 @@ long long layout_bf16(const Graph& g, const StepSpec& s, int th, int tw, BParams
         } else {
             o.tcol = 0;
             gcols = cols;
-            groups.push_back({i, i + 1, 0, 1});
+            groups.push_back({i, i + 1, 0, 1, 0, 1});
         }
         tmem = std::max(tmem, gcols);
     }

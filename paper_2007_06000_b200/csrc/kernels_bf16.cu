@@ -287,7 +287,7 @@ __device__ void issuer(const BParams& P, uint8_t* smem, uint32_t tmem, int total
         for (int gi = 0; gi < G; ++gi) {
             // earlier units' epilogues done, in order; with one set, unit 0
             // waits for the previous tile's last unit (TMEM columns free)
-            if (gi > 0) mbar_sleep_wait(&ud[gi - 1], j & 1);
+            if (gi >= P.groups[gi].wback) mbar_sleep_wait(&ud[gi - P.groups[gi].wback], j & 1);
             else if (ts == 1 && k > 0) mbar_sleep_wait(&ud[G - 1], (k - 1) & 1);
             const BGroup& Gr = P.groups[gi];
             if (!Gr.mma) continue;
@@ -298,7 +298,7 @@ __device__ void issuer(const BParams& P, uint8_t* smem, uint32_t tmem, int total
             // later ops are still on the tensor cores
             uint64_t* fb = acc_full + (s * kBMaxUnits + gi) * kSubs;
             for (int i = Gr.op0; i < Gr.op1; ++i) {
-                issue_op(P, P.ops[i], Gr.nbi, sbase, tmem + uint32_t(s * P.tmem_cols), c, ring_full, ring_empty, xdelta);
+                issue_op(P, P.ops[i], Gr.nbi, sbase, tmem + uint32_t(s * P.tmem_cols + Gr.tbase), c, ring_full, ring_empty, xdelta);
                 const int sub = i - Gr.op0;
                 if (sub < kSubs - 1 || i == Gr.op1 - 1) commit(&fb[sub < kSubs - 1 ? sub : kSubs - 1]);
             }
@@ -836,7 +836,7 @@ __global__ void __launch_bounds__(Cta<EW>::threads, Cta<EW>::min_blocks) fused_b
                             if (threadIdx.x == 0 && sub == 0) stamp(P, kTrUnit + 2 * gi, k);
                             fence_after();
                         }
-                        if (!(P.dbg & 2)) epilogue_mma<EW, KIND == kGap>(P, P.ops[i], G.nbi, smem, tm, t);
+                        if (!(P.dbg & 2)) epilogue_mma<EW, KIND == kGap>(P, P.ops[i], G.nbi, smem, tm + uint32_t(G.tbase), t);
                     }
                 } else {
                     if constexpr (KIND == kSimt) {
