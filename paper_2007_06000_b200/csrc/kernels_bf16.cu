@@ -610,9 +610,24 @@ __device__ void pool_fast(const EpiOp& e, const BRegion& Rg, uint8_t* smem, cons
     const int ncell = op.ext_h * ext_w, c8 = op.npad / 8;
     const float inv = 1.0f / float(kh_ * kw_);
     constexpr int kPer = MODE == kSw128 ? 8 : MODE == kSw32 ? 2 : 1;
-    for (int u = threadIdx.x; u < ncell * c8; u += Cta<EW>::compute) {
-        const int cell = u / c8, oct = u - cell * c8;
-        const int r = cell / ext_w, c = cell - r * ext_w;
+    // u = cell * c8 + oct, u = tid, tid + T, ...: when c8 divides T the
+    // thread's oct is fixed and its cell advances by T / c8 -- (r, c) are
+    // stepped instead of divided (two integer divisions per unit otherwise).
+    constexpr int T = Cta<EW>::compute;
+    const bool step = (T % c8) == 0;
+    const int oct0 = threadIdx.x % c8, cs = T / c8;
+    const int dr = cs / ext_w, dc = cs - dr * ext_w;
+    int rr = (threadIdx.x / c8) / ext_w, cc = (threadIdx.x / c8) - rr * ext_w;
+    for (int u = threadIdx.x; u < ncell * c8; u += T) {
+        int r, c, oct;
+        if (step) {
+            r = rr, c = cc, oct = oct0;
+            rr += dr, cc += dc;
+            if (cc >= ext_w) cc -= ext_w, ++rr;
+        } else {
+            const int cell = u / c8;
+            oct = u - cell * c8, r = cell / ext_w, c = cell - r * ext_w;
+        }
         const int kb = oct / kPer, j = oct - kb * kPer;
         const uint32_t kbb = base + uint32_t(kb * plane);
         const int c0 = (r * stride + dd) * rew + c * stride + dd;
