@@ -520,6 +520,8 @@ __device__ void epilogue_mma(const BParams& P, const BOp& op, int nbi, uint8_t* 
     const bool split_m = kHalves > 1 && nb <= 32;
     const int mt0 = split_m ? half : 0, mstep = split_m ? kHalves : 1;
     const int col0 = split_m ? 0 : half * 32, cstep = split_m ? 32 : 32 * kHalves;
+    // windowed M tiles: (16-row block, 8-column strip) stepped, not divided
+    int wst = mt0 % strips, wrb = mt0 / strips;
     for (int mt = mt0; mt < mtiles; mt += mstep) {
         int r, c;
         bool valid;
@@ -528,9 +530,10 @@ __device__ void epilogue_mma(const BParams& P, const BOp& op, int nbi, uint8_t* 
             r = idx / ext_w, c = idx - r * ext_w;
             valid = idx < ext_h * ext_w;
         } else {
-            const int st = mt % strips, rb = mt / strips;
-            r = rb * 16 + (row >> 3), c = st * 8 + (row & 7);
+            r = wrb * 16 + (row >> 3), c = wst * 8 + (row & 7);
             valid = r < ext_h && c < ext_w;
+            wst += mstep;
+            while (wst >= strips) wst -= strips, ++wrb;
         }
         const CellDst d = cell_dst(e, t, r, c, valid);
         if (GAP) {

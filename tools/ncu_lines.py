@@ -1,6 +1,9 @@
 """Warp-stall samples of one ncu-captured kernel, aggregated per CUDA source line.
 
-    python tools/ncu_lines.py REPORT.ncu-rep KERNEL_ORDINAL LIB.so [top]
+    python tools/ncu_lines.py REPORT.ncu-rep KERNEL_ORDINAL LIB.so [top] [instance]
+
+`instance` selects the template instantiation in the SASS (e.g. ILi8ELi1E for
+fused_bf16_kernel<8, 1>; see the report's Kernel Name).
 
 Maps each SASS address of the `--page source` view to the source line that
 `nvdisasm -g` attributes to its offset inside the fused bf16 kernel
@@ -17,7 +20,7 @@ import tempfile
 KERNEL = "fused_bf16_kernel"
 
 
-def line_map(lib):
+def line_map(lib, instance=""):
     d = tempfile.mkdtemp()
     subprocess.run(["cuobjdump", "-xelf", "all", os.path.abspath(lib)], cwd=d, capture_output=True)
     m, cur, inside = {}, None, False
@@ -27,7 +30,7 @@ def line_map(lib):
         out = subprocess.run(["nvdisasm", "-g", "-c", os.path.join(d, f)], capture_output=True, text=True).stdout
         for ln in out.splitlines():
             if ln.startswith(".text.") or ln.startswith("//---"):
-                inside = KERNEL in ln
+                inside = KERNEL in ln and instance in ln
                 continue
             if not inside:
                 continue
@@ -44,6 +47,7 @@ def line_map(lib):
 def main():
     rep, kid, lib = sys.argv[1], sys.argv[2], sys.argv[3]
     top = int(sys.argv[4]) if len(sys.argv) > 4 else 40
+    instance = sys.argv[5] if len(sys.argv) > 5 else ""
     out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass", "--kernel-id",
                           f"::regex:{KERNEL}:{kid}"], capture_output=True, text=True).stdout
     rows = [r for r in csv.reader(out.splitlines()[1:]) if len(r) > 10]
@@ -57,7 +61,7 @@ def main():
         seen.add(r[0])
         body.append(r)
     base = int(body[0][0], 16)
-    lm = line_map(lib)
+    lm = line_map(lib, instance)
     agg = collections.defaultdict(lambda: [0, 0, collections.Counter()])
     total = 0
     for r in body:
