@@ -124,6 +124,37 @@ __device__ __forceinline__ BTile tile_at(const BParams& P, int tau, int n0) {
     return t;
 }
 
+// The persistent walk tau = blockIdx.x, +gridDim.x, ... decoded incrementally:
+// tau and the stride are split once into mixed-radix digits (image, channel
+// group, tile row, tile column) and each step adds the stride's digits with
+// carries -- no integer division per tile.
+struct TileWalk {
+    int n, cg, ty, tx;      // current tile (n relative to n0)
+    int dn, dcg, dty, dtx;  // digits of gridDim.x
+    __device__ __forceinline__ void split(const BParams& P, int v, int& a, int& b, int& c, int& d) const {
+        const int per_cg = P.grid_h * P.grid_w, per_img = per_cg * P.cgroups;
+        a = v / per_img, v -= a * per_img;
+        b = v / per_cg, v -= b * per_cg;
+        c = v / P.grid_w, d = v - c * P.grid_w;
+    }
+    __device__ __forceinline__ void init(const BParams& P) {
+        split(P, int(blockIdx.x), n, cg, ty, tx);
+        split(P, int(gridDim.x), dn, dcg, dty, dtx);
+    }
+    __device__ __forceinline__ void next(const BParams& P) {
+        tx += dtx, ty += dty, cg += dcg, n += dn;
+        if (tx >= P.grid_w) tx -= P.grid_w, ++ty;
+        if (ty >= P.grid_h) ty -= P.grid_h, ++cg;
+        if (cg >= P.cgroups) cg -= P.cgroups, ++n;
+    }
+    __device__ __forceinline__ BTile tile(const BParams& P, int n0) const {
+        BTile t;
+        t.n = n0 + n, t.ty = ty, t.tx = tx;
+        t.oy0 = ty * P.tile_h, t.ox0 = tx * P.tile_w, t.c0 = cg * P.ctile;
+        return t;
+    }
+};
+
 // ------------------------------------------------------------------ producers
 
 // Block inputs of every tile of this CTA into staging buffer k % nxb; a buffer
@@ -135,8 +166,10 @@ __device__ void x_producer(const BParams& P, const CUtensorMap* xmaps, uint8_t* 
     const int nxb = P.nxb;
     int k = 0;
     grid_dependency_wait();  // the previous step's outputs are this step's inputs
-    for (int tau = blockIdx.x; tau < total; tau += gridDim.x, ++k) {
-        const BTile t = tile_at(P, tau, n0);
+    TileWalk tw;
+    tw.init(P);
+    for (int tau = blockIdx.x; tau < total; tau += gridDim.x, ++k, tw.next(P)) {
+        const BTile t = tw.tile(P, n0);
         const int b = nxb == 2 ? (k & 1) : 0, use = nxb == 2 ? (k >> 1) : k;
         if (use > 0) mbar_sleep_wait(&x_free[b], (use - 1) & 1);
         stamp(P, kTrStart, k);
@@ -836,8 +869,10 @@ __global__ void __launch_bounds__(Cta<EW>::threads, Cta<EW>::min_blocks) fused_b
         int k = 0;
         const int ts = P.tsets;
         grid_dependency_wait();  // global stores after the previous step completed (no write/read overlap)
-        for (int tau = blockIdx.x; tau < total; tau += gridDim.x, ++k) {
-            const BTile t = tile_at(P, tau, n0);
+        TileWalk tw;
+        tw.init(P);
+        for (int tau = blockIdx.x; tau < total; tau += gridDim.x, ++k, tw.next(P)) {
+            const BTile t = tw.tile(P, n0);
             const int b = nxb == 2 ? (k & 1) : 0, use = nxb == 2 ? (k >> 1) : k;
             const int xdelta = b * P.xstride;
             const int s = ts == 2 ? (k & 1) : 0, j = ts == 2 ? (k >> 1) : k;
