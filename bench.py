@@ -257,6 +257,9 @@ def main():
     # dependent launch), CUDA events on the launching stream.
     with ClockSampler(local) as clk:
         barrier()
+        # profiler range = the timed forwards (`ncu --profile-from-start off`
+        # captures exactly these launches, not the tuner's)
+        torch.cuda.profiler.start()
         t0 = torch.cuda.Event(enable_timing=True)
         t1 = torch.cuda.Event(enable_timing=True)
         t0.record(st)
@@ -264,6 +267,7 @@ def main():
             e.forward(B, use_graph=True)
         t1.record(st)
         barrier()
+        torch.cuda.profiler.stop()
     total_ms = t0.elapsed_time(t1)
     step_ms = torch.tensor([total_ms / args.steps], device="cuda")
     if world > 1:
