@@ -167,3 +167,26 @@ def test_bf16_forced_configurations(name, env, monkeypatch):
     for o in og.outputs:
         err = O.normwise(e.read(o, batch).cpu().numpy()[sample], ref[o])
         assert err <= TOL, (name, env, o, err)
+
+
+WIDE = "name wide\ninput {\n  name d\n  shape [64, 20, 20]\n}\n" + "".join(
+    f"layer {{\n  name c{i}\n  kind conv\n  inputs [d]\n  out_channels {16 + 8 * i}\n  kernel [1, 1]\n  activation relu\n}}\n"
+    for i in range(6)) + "layer {\n  name cat\n  kind concat\n  inputs [c0, c1, c2, c3, c4, c5]\n}\noutput cat\n"
+
+
+def test_bf16_many_parallel_branches():
+    """Six 1x1 branches on one input run as one multi-branch kernel whose MMA
+    group holds more ops than it has per-op accumulator barriers (the last
+    barrier covers the rest): results within the bf16 tolerance."""
+    import torch
+    og = O.load_graph(WIDE)
+    w = O.seeded_weights(og, 3)
+    x = O.seeded_batch(og, 5, 3)
+    g = X.Graph(WIDE)
+    e = X.Engine(g, O.flat_weights(og, w), "b200", "bf16", max_batch=3)
+    assert any(len(s["layers"]) >= 5 for s in e.steps), [s["layers"] for s in e.steps]
+    e.set_input(torch.from_numpy(x).cuda())
+    e.forward(3)
+    ref = O.run_batch(og, x, w, ["cat"])
+    err = O.normwise(e.read("cat", 3).cpu().numpy(), ref["cat"])
+    assert err <= TOL, err
