@@ -118,6 +118,11 @@ xlf_status xlf_engine_run_host(xlf_engine* e, const float* h_in_nchw, int batch,
  * the same engine. */
 xlf_status xlf_engine_autotune(xlf_engine* e, int batch, int reps, int topk);
 xlf_status xlf_engine_tune_report(const xlf_engine* e, char* buf, size_t cap, size_t* need);
+/* Applies a tuning report (the JSON xlf_engine_tune_report returns, e.g. saved
+ * from an earlier run on the same model / batch / GPU) without measuring:
+ * XLF_E_VALIDATION for an unknown step, XLF_E_INFEASIBLE for a configuration
+ * this plan cannot run, XLF_E_PARSE for malformed input. */
+xlf_status xlf_engine_apply_tuning(xlf_engine* e, const char* json);
 /* Profiling aid (engine created with XLF_TRACE=1 in the environment, bf16):
  * globaltimer stamps of the first CTAs of a step's last launch. */
 xlf_status xlf_engine_trace(const xlf_engine* e, int step, unsigned long long* out, size_t cap, size_t* count);

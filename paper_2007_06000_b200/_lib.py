@@ -18,7 +18,7 @@ SYMBOLS = [
     "xlf_block_report", "xlf_blocks_json", "xlf_classify_mode", "xlf_plan_tiling", "xlf_store_tx", "xlf_device_plan_json", "xlf_seeded_weights",
     "xlf_engine_create", "xlf_engine_destroy", "xlf_engine_json", "xlf_engine_num_steps",
     "xlf_engine_launches_per_forward", "xlf_engine_set_input", "xlf_engine_set_input_seeded", "xlf_engine_forward",
-    "xlf_engine_run_step", "xlf_engine_read", "xlf_engine_run_host", "xlf_engine_autotune", "xlf_engine_tune_report",
+    "xlf_engine_run_step", "xlf_engine_read", "xlf_engine_run_host", "xlf_engine_autotune", "xlf_engine_tune_report", "xlf_engine_apply_tuning",
     "xlf_engine_trace",
 ]
 
@@ -76,6 +76,7 @@ def lib() -> ctypes.CDLL:
     L.xlf_engine_run_host.argtypes = [vp, f32p, ctypes.c_int, c_char_pp, f32p, vp]
     L.xlf_engine_autotune.argtypes = [vp, ctypes.c_int, ctypes.c_int, ctypes.c_int]
     L.xlf_engine_tune_report.argtypes = [vp, ctypes.c_char_p, sz, szp]
+    L.xlf_engine_apply_tuning.argtypes = [vp, ctypes.c_char_p]
     L.xlf_engine_trace.argtypes = [vp, ctypes.c_int, ctypes.POINTER(ctypes.c_ulonglong), sz, szp]
     _LIB = L
     return L

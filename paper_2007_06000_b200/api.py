@@ -223,6 +223,13 @@ class Engine:
         self.info = json.loads(text_call(lib().xlf_engine_json, self._h))
         return json.loads(text_call(lib().xlf_engine_tune_report, self._h))
 
+    def apply_tuning(self, report) -> None:
+        """Re-applies a report autotune() returned (list or JSON text), e.g.
+        saved from an earlier run on the same model / batch / GPU."""
+        text = report if isinstance(report, str) else json.dumps(report)
+        check(lib().xlf_engine_apply_tuning(self._h, text.encode()))
+        self.info = json.loads(text_call(lib().xlf_engine_json, self._h))
+
     def materialized(self):
         return [n for n, t in self.info["plan"]["tensors"].items() if t["materialized"]]
 

@@ -332,6 +332,14 @@ extern "C" xlf_status xlf_engine_tune_report(const xlf_engine* e, char* buf, siz
     });
 }
 
+extern "C" xlf_status xlf_engine_apply_tuning(xlf_engine* e, const char* json) {
+    return guard([&] {
+        need_ptr(e, "engine"), need_ptr(json, "json");
+        e->e->apply_tuning(json);
+        e->tune_report = json;
+    });
+}
+
 extern "C" xlf_status xlf_engine_trace(const xlf_engine* e, int step, unsigned long long* out, size_t cap, size_t* count) {
     return guard([&] {
         need_ptr(e, "engine");

@@ -375,6 +375,66 @@ std::string Engine::autotune(int batch, int reps, int topk) {
     return js.str();
 }
 
+// Re-applies a tuning report (the JSON autotune returns) without measuring:
+// the tuned plan as a reusable artifact (tune once per model / batch / GPU,
+// then load).  Every entry must name a bf16 fused step of this plan and give a
+// feasible configuration; the report's format is the one autotune writes
+// (flat objects, numeric fields, "id" string, "tile" [h, w]).
+void Engine::apply_tuning(const std::string& js) {
+    if (prec_ != Precision::bf16) return;
+    // value position of "key" (after the colon; whitespace tolerated), or npos
+    auto at = [](const std::string& obj, const std::string& key) -> size_t {
+        const size_t k = obj.find("\"" + key + "\"");
+        if (k == std::string::npos) return std::string::npos;
+        const size_t c = obj.find(':', k + key.size() + 2);
+        return c == std::string::npos ? c : c + 1;
+    };
+    auto num = [&](const std::string& obj, const std::string& key, int& out) {
+        const size_t v = at(obj, key);
+        if (v == std::string::npos) return false;
+        out = std::atoi(obj.c_str() + v);
+        return true;
+    };
+    size_t pos = 0;
+    int applied = 0;
+    while ((pos = js.find('{', pos)) != std::string::npos) {
+        const size_t end = js.find('}', pos);
+        if (end == std::string::npos) fail(ErrorKind::parse, "tuning report: unterminated object");
+        const std::string obj = js.substr(pos, end - pos + 1);
+        pos = end + 1;
+        const size_t iv = at(obj, "id");
+        const size_t is = iv == std::string::npos ? iv : obj.find('"', iv);
+        const size_t ie = is == std::string::npos ? is : obj.find('"', is + 1);
+        if (ie == std::string::npos) fail(ErrorKind::parse, "tuning report: entry without \"id\"");
+        const std::string id = obj.substr(is + 1, ie - is - 1);
+        size_t i = 0;
+        while (i < plan_.steps.size() && plan_.steps[i].id != id) ++i;
+        if (i == plan_.steps.size() || !bparams_[i]) fail(ErrorKind::validation, "tuning report: no bf16 fused step '" + id + "'");
+        StepSpec t = plan_.steps[i];
+        const size_t tv = at(obj, "tile");
+        const size_t tb = tv == std::string::npos ? tv : obj.find('[', tv);
+        const size_t tc = tb == std::string::npos ? tb : obj.find(',', tb);
+        if (tc == std::string::npos) fail(ErrorKind::parse, "tuning report: step '" + id + "' without \"tile\": [h, w]");
+        t.tile_h = std::atoi(obj.c_str() + tb + 1);
+        t.tile_w = std::atoi(obj.c_str() + tc + 1);
+        num(obj, "nxb", t.nxb), num(obj, "wres", t.wres), num(obj, "ring_slots", t.ring_slots), num(obj, "ring_chunk", t.ring_chunk);
+        num(obj, "grid_all", t.grid_all), num(obj, "epi_warps", t.epi_warps), num(obj, "tsets", t.tsets);
+        BParams probe;
+        const long long sm = layout_bf16(g_, t, t.tile_h, t.tile_w, &probe, t.nxb, t.wres, t.ring_slots, t.tsets, t.ring_chunk);
+        if (sm < 0 || sm > kSmemBudgetBf16 || (t.epi_warps != 4 && t.epi_warps != 8) || t.tile_h < 1 || t.tile_w < 1)
+            fail(ErrorKind::infeasible, "tuning report: configuration of step '" + id + "' is not feasible for this plan");
+        t.smem_bytes = int(sm);
+        std::unique_ptr<BParams> P = build_bparams(t);
+        cudaFree(const_cast<void*>(bparams_[i]->dev_copy));
+        plan_.steps[i] = t;
+        bparams_[i] = std::move(P);
+        ++applied;
+    }
+    for (auto& [b, ge] : graphs_) cudaGraphExecDestroy(ge);
+    graphs_.clear();
+    (void)applied;
+}
+
 Engine::~Engine() {
     cudaSetDevice(device_);
     for (auto& [b, ge] : graphs_) cudaGraphExecDestroy(ge);

@@ -54,6 +54,8 @@ public:
     // Measured-time tuning of the bf16 fused steps (see engine.cpp); returns
     // the chosen configurations as JSON.
     std::string autotune(int batch, int reps, int topk);
+    // Applies a report autotune returned (no measurement).
+    void apply_tuning(const std::string& json);
     int max_batch() const { return max_batch_; }
 
 private:

@@ -190,3 +190,30 @@ def test_bf16_many_parallel_branches():
     ref = O.run_batch(og, x, w, ["cat"])
     err = O.normwise(e.read("cat", 3).cpu().numpy(), ref["cat"])
     assert err <= TOL, err
+
+
+def test_bf16_tuning_report_roundtrip():
+    """A tuning report saved from one engine re-applied to a fresh engine of
+    the same model gives the same step configurations and bit-identical
+    results (the tuned plan as a reusable artifact)."""
+    import json
+    import torch
+    g = X.load_graph(X.graph_path("fire"))
+    w = X.seeded_weights(g, 42)
+    a = X.Engine(g, w, "b200", "bf16", max_batch=8)
+    a.set_input_seeded(42, 8)
+    a.forward(8, use_graph=False)
+    report = a.autotune(8, reps=2, topk=2)
+    b = X.Engine(g, w, "b200", "bf16", max_batch=8)
+    b.apply_tuning(json.dumps(report))  # default separators: ", " / ": "
+    keys = ("tile", "nxb", "wres", "ring_slots", "epi_warps", "tsets")
+    assert [{k: s[k] for k in keys} for s in a.steps] == [{k: s[k] for k in keys} for s in b.steps]
+    outs = []
+    for e in (a, b):
+        e.set_input_seeded(42, 8)
+        e.forward(8)
+        outs.append(e.read(g.outputs[0], 8))
+    torch.cuda.synchronize()
+    assert torch.equal(outs[0], outs[1])
+    with pytest.raises(X.XlfError):
+        b.apply_tuning('[{"id": "nope", "tile": [4, 4]}]')
