@@ -91,8 +91,14 @@ __device__ __forceinline__ void named_sync_compute() { asm volatile("bar.sync 1,
 // the co-resident CTA's epilogue (ncu, profiles/r1_ncu_summary.md).
 template <int EW>
 __device__ __forceinline__ void compute_wait(uint64_t* bar, uint32_t parity) {
+#ifdef XLF_WAIT_CTA
     if (threadIdx.x == 0) mbar_sleep_wait(bar, parity);
     named_sync_compute<EW>();
+#else
+    // every epilogue thread observes the phase itself: warps start on an
+    // accumulator as soon as it is ready, without a CTA-wide barrier
+    mbar_sleep_wait(bar, parity);
+#endif
 }
 
 __device__ __forceinline__ const BRegion& src_region(const BParams& P, const BOp& op, int which) {
