@@ -824,15 +824,15 @@ __global__ void __launch_bounds__(Cta<EW>::threads, Cta<EW>::min_blocks) fused_b
     grid_launch_dependents();  // every CTA is resident: the next step may be scheduled as SMs free up
     if (threadIdx.x == 0) {
         mbar_init(&bar_p, 1);
-        for (int i = 0; i < 2; ++i) mbar_init(&bar_x[i], 1), mbar_init(&x_free[i], 1);
+        for (int i = 0; i < 2; ++i) mbar_init(&bar_x[i], 1), mbar_init(&x_free[i], EW);  // one arrival per epilogue warp
         for (int i = 0; i < kRingMax; ++i) mbar_init(&ring_full[i], 1), mbar_init(&ring_empty[i], 1);
         mbar_init(&bar_w, 1);
         for (int t = 0; t < Pg.tsets; ++t)
             for (int i = 0; i < Pg.ngroups; ++i) {
-                mbar_init(&unit_done[t * kBMaxUnits + i], 1);
+                mbar_init(&unit_done[t * kBMaxUnits + i], EW);
                 for (int q = 0; q < kSubs; ++q) mbar_init(&acc_full[(t * kBMaxUnits + i) * kSubs + q], 1);
             }
-        mbar_init(&acc_free[0], 1), mbar_init(&acc_free[1], 1);
+        mbar_init(&acc_free[0], EW), mbar_init(&acc_free[1], EW);
         mbar_fence_init();
         mbar_expect_tx(&bar_p, uint32_t(sizeof(BParams)));
         bulk_g2s(&Ps, Pg.dev_copy, uint32_t(sizeof(BParams)), &bar_p);
@@ -907,15 +907,22 @@ __global__ void __launch_bounds__(Cta<EW>::threads, Cta<EW>::min_blocks) fused_b
                 }
                 fence_async_smem();  // epilogue-written buffers are read by later MMAs (async proxy)
                 fence_before();
-                named_sync_compute<EW>();
-                if (threadIdx.x == 0) mbar_arrive(&unit_done[s * kBMaxUnits + gi]), stamp(P, kTrUnit + 2 * gi + 1, k);
+                // MMA-only steps: no epilogue reads what another warp wrote, so
+                // each warp releases the unit on its own (the barrier counts
+                // one arrival per warp); SIMT ops and the pooled column sums
+                // read across warps and need the whole group first
+                if constexpr (KIND != kMmaOnly) named_sync_compute<EW>();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&unit_done[s * kBMaxUnits + gi]);
+                if (threadIdx.x == 0) stamp(P, kTrUnit + 2 * gi + 1, k);
             }
             // every unit of this tile is done (MMAs complete, SIMT reads
             // finished): its staging buffer and accumulator set are free
-            if (threadIdx.x == 0) {
-                mbar_arrive(&x_free[b]), stamp(P, kTrEnd, k);
+            if (lane == 0) {
+                mbar_arrive(&x_free[b]);
                 if (ts == 2) mbar_arrive(&acc_free[s]);
             }
+            if (threadIdx.x == 0) stamp(P, kTrEnd, k);
             if (KIND == kGap) {  // this tile's column sums -> gap_part[image][tile][c], reset
                 float* gsum = reinterpret_cast<float*>(smem + P.gap_off);
                 const int per_img = P.grid_h * P.grid_w;
