@@ -161,10 +161,28 @@ struct TileWalk {
     }
 };
 
+// Last group whose MMAs read the staging buffer, when only MMAs read it (no
+// SIMT group): the issuer then releases the buffer with a tcgen05.commit
+// right after that group, so the next tile's input load overlaps the rest of
+// this tile (expand MMAs, epilogues).  -1: the epilogue warps release it after
+// the tile (SIMT ops read the staged input).
+__device__ __forceinline__ int x_release_group(const BParams& P) {
+    if (P.dbg & 16) return -1;
+    int last = -1;
+    for (int gi = 0; gi < P.ngroups; ++gi) {
+        const BGroup& G = P.groups[gi];
+        if (!G.mma) return -1;
+        for (int i = G.op0; i < G.op1; ++i)
+            if (P.ops[i].stage == 1) last = gi;
+    }
+    return last;
+}
+
 // ------------------------------------------------------------------ producers
 
 // Block inputs of every tile of this CTA into staging buffer k % nxb; a buffer
-// is refilled once the epilogue released it (x_free, after the tile's last unit).
+// is refilled once it is released (x_free: the MMAs that read it completed, or
+// the epilogue finished the tile; see x_release_group).
 __device__ void x_producer(const BParams& P, const CUtensorMap* xmaps, uint8_t* smem, int total, int n0, uint64_t* bar_x,
                            uint64_t* x_free) {
     uint32_t bytes = 0;
@@ -299,7 +317,7 @@ __device__ __forceinline__ void issue_op(const BParams& P, const BOp& op, int nb
     }
 }
 
-__device__ void issuer(const BParams& P, uint8_t* smem, uint32_t tmem, int total, uint64_t* bar_x, uint64_t* ring_full,
+__device__ void issuer(const BParams& P, uint8_t* smem, uint32_t tmem, int total, uint64_t* bar_x, uint64_t* x_free, uint64_t* ring_full,
                        uint64_t* ring_empty, uint64_t* acc_full, uint64_t* unit_done, uint64_t* acc_free, uint64_t* bar_w) {
     int c = 0, k = 0;
     const uint32_t sbase = smem_u32(smem);
@@ -311,6 +329,7 @@ __device__ void issuer(const BParams& P, uint8_t* smem, uint32_t tmem, int total
     if (!any) return;
     if (P.wres) mbar_sleep_wait(bar_w, 0);
     const int ts = P.tsets;
+    const int xrel = x_release_group(P);
     for (int tau = blockIdx.x; tau < total; tau += gridDim.x, ++k) {
         const int b = nxb == 2 ? (k & 1) : 0, use = nxb == 2 ? (k >> 1) : k;
         const int xdelta = b * P.xstride;
@@ -341,6 +360,7 @@ __device__ void issuer(const BParams& P, uint8_t* smem, uint32_t tmem, int total
                 const int sub = i - Gr.op0;
                 if (sub < kSubs - 1 || i == Gr.op1 - 1) commit(&fb[sub < kSubs - 1 ? sub : kSubs - 1]);
             }
+            if (gi == xrel) commit(&x_free[b]);      // staging buffer read by every MMA that needs it
             if (gi < 2) stamp(P, 30 + 2 * gi, k);  // group issued
         }
     }
@@ -824,7 +844,8 @@ __global__ void __launch_bounds__(Cta<EW>::threads, Cta<EW>::min_blocks) fused_b
     grid_launch_dependents();  // every CTA is resident: the next step may be scheduled as SMs free up
     if (threadIdx.x == 0) {
         mbar_init(&bar_p, 1);
-        for (int i = 0; i < 2; ++i) mbar_init(&bar_x[i], 1), mbar_init(&x_free[i], EW);  // one arrival per epilogue warp
+        const int xrel = x_release_group(Pg);
+        for (int i = 0; i < 2; ++i) mbar_init(&bar_x[i], 1), mbar_init(&x_free[i], xrel >= 0 ? 1 : EW);  // MMA commit, or one arrival per epilogue warp
         for (int i = 0; i < kRingMax; ++i) mbar_init(&ring_full[i], 1), mbar_init(&ring_empty[i], 1);
         mbar_init(&bar_w, 1);
         for (int t = 0; t < Pg.tsets; ++t)
@@ -856,7 +877,7 @@ __global__ void __launch_bounds__(Cta<EW>::threads, Cta<EW>::min_blocks) fused_b
         // (elect.sync, not lane == 0: the compiler then knows one thread is
         // active and moves descriptors to uniform registers without the
         // per-MMA ELECT waterfall it emits for a lane-predicated branch)
-        if (elect_one()) issuer(Pg, smem, tmem, total, bar_x, ring_full, ring_empty, acc_full, unit_done, acc_free, &bar_w);
+        if (elect_one()) issuer(Pg, smem, tmem, total, bar_x, x_free, ring_full, ring_empty, acc_full, unit_done, acc_free, &bar_w);
         __syncwarp();
     } else {
         compute_wait<EW>(&bar_p, 0);
@@ -872,6 +893,7 @@ __global__ void __launch_bounds__(Cta<EW>::threads, Cta<EW>::min_blocks) fused_b
         named_sync_compute<EW>();
         const int gap_np = KIND == kGap ? P.ops[0].npad : 0;  // gap steps have one op
         const int nxb = P.nxb;
+        const int xrel = x_release_group(P);
         int k = 0;
         const int ts = P.tsets;
         grid_dependency_wait();  // global stores after the previous step completed (no write/read overlap)
@@ -919,7 +941,7 @@ __global__ void __launch_bounds__(Cta<EW>::threads, Cta<EW>::min_blocks) fused_b
             // every unit of this tile is done (MMAs complete, SIMT reads
             // finished): its staging buffer and accumulator set are free
             if (lane == 0) {
-                mbar_arrive(&x_free[b]);
+                if (xrel < 0) mbar_arrive(&x_free[b]);
                 if (ts == 2) mbar_arrive(&acc_free[s]);
             }
             if (threadIdx.x == 0) stamp(P, kTrEnd, k);
