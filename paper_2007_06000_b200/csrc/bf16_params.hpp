@@ -75,6 +75,8 @@ struct BGroup {
     int tbase;     // first TMEM column of the group (ops add their tcol)
     int wback;     // the issuer waits for the epilogue of group gi - wback (1: in order;
                    // 2: N blocks alternating between two column sets)
+    int pwait;     // one accumulator set, gi < wback: the previous tile's last group whose
+                   // TMEM columns overlap this one (its epilogue frees them); -1: none
 };
 
 // Layout of a shared region: K-blocks of kb_ch channels; inside a K-block

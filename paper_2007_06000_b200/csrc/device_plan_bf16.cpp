@@ -276,7 +276,7 @@ long long layout_bf16(const Graph& g, const StepSpec& s, int th, int tw, BParams
     for (int i = 0; i < nops; ++i) {
         BOp& o = ops[size_t(i)];
         if (o.kind != BOP_MMA) {
-            groups.push_back({i, i + 1, 0, 0, 0, 1});
+            groups.push_back({i, i + 1, 0, 0, 0, 1, -1});
             continue;
         }
         const int cols = o.mtiles * o.nb;
@@ -284,7 +284,7 @@ long long layout_bf16(const Graph& g, const StepSpec& s, int th, int tw, BParams
             // N blocks alternate between two column sets when both fit: block
             // k+1's MMAs run while the epilogue drains block k
             const bool alt = 2 * cols <= 512 && !std::getenv("XLF_NO_NALT");
-            for (int k = 0; k < o.nblocks; ++k) groups.push_back({i, i + 1, k, 1, alt ? (k & 1) * cols : 0, alt && k > 0 ? 2 : 1});
+            for (int k = 0; k < o.nblocks; ++k) groups.push_back({i, i + 1, k, 1, alt ? (k & 1) * cols : 0, alt && k > 0 ? 2 : 1, -1});
             o.tcol = 0;
             tmem = std::max(tmem, alt ? 2 * cols : cols);
             continue;
@@ -299,11 +299,51 @@ long long layout_bf16(const Graph& g, const StepSpec& s, int th, int tw, BParams
         } else {
             o.tcol = 0;
             gcols = cols;
-            groups.push_back({i, i + 1, 0, 1, 0, 1});
+            groups.push_back({i, i + 1, 0, 1, 0, 1, -1});
         }
         tmem = std::max(tmem, gcols);
     }
     if (groups.size() > size_t(kBMaxUnits)) return -1;
+    // Single-block MMA groups get disjoint TMEM columns when that fits the
+    // allocation they need anyway, so a group of the next tile can start
+    // while a later group of this tile still drains.
+    auto single = [&](const BGroup& G) { return G.mma && ops[size_t(G.op0)].nblocks == 1; };
+    {
+        int sum = 0;
+        for (const BGroup& G : groups)
+            if (single(G)) sum += ops[size_t(G.op1 - 1)].tcol + ops[size_t(G.op1 - 1)].mtiles * ops[size_t(G.op1 - 1)].nb;
+        bool all_single = true;
+        for (const BGroup& G : groups) all_single &= !G.mma || single(G);
+        if (all_single && sum <= pow2_cols(tmem) && !std::getenv("XLF_NO_TSEP")) {
+            int base = 0;
+            for (BGroup& G : groups)
+                if (single(G)) G.tbase = base, base += ops[size_t(G.op1 - 1)].tcol + ops[size_t(G.op1 - 1)].mtiles * ops[size_t(G.op1 - 1)].nb;
+        }
+    }
+    // what the issuer waits for before a tile's first groups (one accumulator set)
+    auto span = [&](const BGroup& G, int& lo, int& hi) {
+        lo = 1 << 30, hi = 0;
+        for (int i = G.op0; i < G.op1; ++i) {
+            const BOp& o = ops[size_t(i)];
+            lo = std::min(lo, G.tbase + o.tcol), hi = std::max(hi, G.tbase + o.tcol + o.mtiles * o.nb);
+        }
+    };
+    for (size_t gi = 0; gi < groups.size(); ++gi) {
+        BGroup& G = groups[gi];
+        G.pwait = -1;
+        if (!G.mma) continue;
+        int lo, hi;
+        span(G, lo, hi);
+        for (int j = int(groups.size()) - 1; j >= 0; --j) {
+            if (!groups[size_t(j)].mma) continue;
+            int l2, h2;
+            span(groups[size_t(j)], l2, h2);
+            if (l2 < hi && lo < h2) {
+                G.pwait = std::getenv("XLF_NO_PWAIT") ? int(groups.size()) - 1 : j;
+                break;
+            }
+        }
+    }
     long long gap_off = 0;
     if (!s.gap_out.empty()) {
         if (nops != 1 || ops[0].kind != BOP_MMA) return -1;

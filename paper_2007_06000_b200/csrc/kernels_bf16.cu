@@ -343,10 +343,12 @@ __device__ void issuer(const BParams& P, uint8_t* smem, uint32_t tmem, int total
             if (j > 0) mbar_sleep_wait(&acc_free[s], (j - 1) & 1);  // tile k-2 (same set) fully done
         }
         for (int gi = 0; gi < G; ++gi) {
-            // earlier units' epilogues done, in order; with one set, unit 0
-            // waits for the previous tile's last unit (TMEM columns free)
+            // earlier units' epilogues done, in order; with one set, a tile's
+            // first units wait for the previous tile's last unit on their TMEM
+            // columns (pwait: with disjoint group columns the next tile's
+            // first group starts while this tile's later groups drain)
             if (gi >= P.groups[gi].wback) mbar_sleep_wait(&ud[gi - P.groups[gi].wback], j & 1);
-            else if (ts == 1 && k > 0) mbar_sleep_wait(&ud[G - 1], (k - 1) & 1);
+            else if (ts == 1 && k > 0 && P.groups[gi].pwait >= 0) mbar_sleep_wait(&ud[P.groups[gi].pwait], (k - 1) & 1);
             const BGroup& Gr = P.groups[gi];
             if (!Gr.mma) continue;
             fence_after();
