@@ -142,6 +142,11 @@ FORCED = [
     {"XLF_XBUF": "2", "XLF_WRES": "1"},
     {"XLF_XBUF": "2", "XLF_TSETS": "2"},
     {"XLF_XBUF": "1", "XLF_WRES": "1", "XLF_CTAS": "1"},
+    # the earlier synchronisation structure: shared TMEM columns for every
+    # group, a tile's first group waiting for the previous tile's last unit,
+    # staging buffers released by the epilogue warps (XLF_DBG bit 16)
+    {"XLF_NO_TSEP": "1", "XLF_NO_PWAIT": "1", "XLF_DBG": "16"},
+    {"XLF_NO_NALT": "1", "XLF_XBUF": "2"},
 ]
 
 
