@@ -539,7 +539,9 @@ DevicePlan plan_device(const Graph& g, Partition part, int batch_hint, int smem_
                 const std::string list = std::string(",") + e + ",";
                 force_split = list.find("," + b.id + ",") != std::string::npos;
             }
-            if (force_split || single < 0.85 * fused) {
+            double ratio = 0.85;  // model margin a split must win by
+            if (const char* e = std::getenv("XLF_UNFUSE_RATIO")) ratio = std::atof(e);
+            if (force_split || single < ratio * fused) {
                 for (StepSpec& t : singles) steps.push_back(t);
                 continue;
             }
