@@ -1,2 +1,6 @@
-for i in 1 2 3; do XLF_ALWAYS_FUSE=1 XLF_UNFUSE=b3 timeout 300 python bench.py --no-cpu --no-blocks > gpurun_out/b.json 2>/dev/null; python -c "import json; d=json.loads(open('gpurun_out/b.json').read().strip().splitlines()[-1]); k=d['kernels_ms']; print('mix', d['value'], d['ms_per_step'], sum(k.values()), {a:b for a,b in k.items() if a[:2] in ('b3','b4','b5','b6','b7')})"; done
-for i in 1 2; do timeout 300 python bench.py --no-cpu --no-blocks > gpurun_out/b.json 2>/dev/null; python -c "import json; d=json.loads(open('gpurun_out/b.json').read().strip().splitlines()[-1]); k=d['kernels_ms']; print('dflt', d['value'], d['ms_per_step'], sum(k.values()))"; done
+timeout 240 python -m pytest tests/test_gpu_bf16.py -q -x -p no:cacheprovider > gpurun_out/pytest_gpu.log 2>&1; rc=$?; echo "bf16 tests rc=$rc"; tail -1 gpurun_out/pytest_gpu.log
+if [ $rc = 0 ]; then
+timeout 400 python -m pytest tests -m gpu -q -x -p no:cacheprovider > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?"; tail -1 gpurun_out/pytest_gpu.log
+timeout 60 python tests/probes/determinism.py squeezenet11 64 bf16 2>&1 | tail -1
+for i in 1 2; do timeout 90 python bench.py --no-cpu --no-blocks > gpurun_out/b.json 2>/dev/null; python -c "import json; d=json.loads(open('gpurun_out/b.json').read().strip().splitlines()[-1]); print(d['value'], d['e2e']['value'])"; done
+fi
