@@ -3,29 +3,41 @@
 unfused").
 
 Headline (`value`): SqueezeNet v1.1 inference, 256 images per GPU (BASELINE
-config 5), images/s over all ranks, inputs resident in HBM (generated on
-device from the reference's SeededStream), one step = one forward of the
-whole partition.  `e2e`: the same through the C ABI with host buffers (H2D of
-the NCHW input + D2H of the logits inside the timed region).  `blocks`: the
-fused-block configs 1-4 (straight / merge / split / inception) in us per block,
-fused vs the unfused sm_100a kernels, with algorithmic HBM bytes saved.
+config 5), bf16 tensor-core path, images/s over all ranks, inputs resident in
+HBM (generated on device from the reference's SeededStream), one step = one
+forward of the whole partition (one CUDA-graph launch).  In the same run:
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--precision fp32|fp32_exact]
+* `e2e`: the same through the C ABI with host buffers (H2D of the NCHW fp32
+  input + D2H of the logits inside the timed region);
+* `parity`: the timed (autotuned) configuration's logits of sampled images
+  against the CPU oracle (norm-wise error, argmax);
+* `arms`: SqueezeNet img/s of every arithmetic path (bf16, TF32, fp32 SIMT)
+  for the fused B200 partition AND the unfused sm_100a kernels -- the
+  paper's fused-vs-unfused comparison;
+* `blocks`: BASELINE configs 1-4 (straight / merge / split / inception) in us
+  per block at every precision, fused vs unfused, each with its roofline
+  fraction (algorithmic bytes / FLOPs against the measured peaks);
+* `roofline`: the dominant kernel of the headline step;
+* `cpu_baseline`: the reference's own CPU path on this box's cores.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--precision bf16|tf32|fp32|fp32_exact]
     python bench.py --impl reference ...   # the reference's own CPU path
 
-Multi-GPU: launched by torchrun, one rank per GPU; the batch is sharded
-(rank r generates images [r*256, (r+1)*256)), no collective on the data path;
-the step time is the max over ranks.
+Multi-GPU: one rank per GPU (torchrun; `--gpus N` without torchrun re-launches
+itself under torch.distributed.run); the batch is sharded (rank r generates
+images [r*256, (r+1)*256)), no collective on the data path; the step time is
+the max over ranks.  The optional NCCL gather of the logits to rank 0 is
+timed separately (`gather_ms`).
 """
 from __future__ import annotations
 
 import argparse
 import json
 import os
+import socket
 import statistics
 import subprocess
 import sys
-import tempfile
 import threading
 import time
 
@@ -34,21 +46,37 @@ sys.path.insert(0, ROOT)
 
 BASELINE_METRIC = "fused-block µs & SqueezeNet img/s at 1/2/4/8 B200; HBM bytes saved vs unfused"
 PER_GPU_BATCH = 256
-BLOCK_CONFIGS = [  # (config, graph, batch) -- BASELINE.json configs[0..3]
-    ("straight", "straight", 1),
-    ("merge", "merge", 8),
-    ("split", "fire", 32),
-    ("inception", "inc3a", 64),
+BLOCK_CONFIGS = [  # (config, graph, batch, precisions) -- BASELINE.json configs[0..3]
+    ("straight", "straight", 1, ("fp32", "tf32", "bf16")),   # C1 is an fp32 config
+    ("merge", "merge", 8, ("fp32", "tf32", "bf16")),
+    ("split", "fire", 32, ("fp32", "tf32", "bf16")),
+    ("inception", "inc3a", 64, ("tf32", "bf16", "fp32")),    # C4 names bf16 / TF32
 ]
+TC = ("bf16", "tf32")
+DTYPE = {"bf16": "bf16", "tf32": "tf32", "fp32": "f32", "fp32_exact": "f32"}
 
 
 def peaks():
+    """(HBM GB/s, bf16 dense TF/s, source): MEASURED_PEAKS.json (driver-written,
+    this pool's B200s) or the profiling guide's fallback."""
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
             p = json.load(fh)
         return p["hbm_gbs"], p["bf16_tflops"], "measured"
     except Exception:
         return 6650.0, 1590.0, "fallback"
+
+
+def pipe_peak_tflops(prec, sm_mhz):
+    """Peak of the pipe a precision computes on: tcgen05 bf16 (measured), TF32
+    (half the bf16 rate: 32-byte K steps of 8 instead of 16 elements at the
+    same instruction rate), fp32 SIMT FMA (148 SMs x 128 lanes x 2 FLOP x clock)."""
+    _, bf16, _ = peaks()
+    if prec == "bf16":
+        return bf16, "tcgen05 kind::f16 (measured bf16 peak)"
+    if prec == "tf32":
+        return bf16 / 2, "tcgen05 kind::tf32 (half the measured bf16 peak)"
+    return 148 * 128 * 2 * (sm_mhz or 1965) * 1e6 / 1e12, "fp32 FFMA (SIMT, 148 x 128 lanes)"
 
 
 class ClockSampler:
@@ -81,12 +109,12 @@ class ClockSampler:
             pass
 
     def __enter__(self):
-        # NVML set up before the timed region starts; then a sample every 10 ms
         try:
             import pynvml as N
             N.nvmlInit()
             self.nvml, self.handle = N, N.nvmlDeviceGetHandleByIndex(self.index)
             self.max_mhz = float(N.nvmlDeviceGetMaxClockInfo(self.handle, N.NVML_CLOCK_SM))
+            self._sample()
             self.thread = threading.Thread(target=self._run, daemon=True)
             self.thread.start()
         except Exception:
@@ -104,14 +132,12 @@ class ClockSampler:
                 "samples": len(sm), "source": "nvml, 10 ms"}
 
 
-# ----------------------------------------------------------------------------- reference arm
+# ----------------------------------------------------------------------------- checker / CPU legs (oracle)
 
 def cpu_reference_rate(images: int, threads: int):
     """images/s of the reference's own CPU path (run_reference per image,
     reference.cpp:126-142, OpenMP across images) on SqueezeNet v1.1, from
     oracle/_ref when the reference compiled here, else the oracle port."""
-    import numpy as np
-
     from oracle import oracle as O
     from oracle import ref as R
     text = open(os.path.join(ROOT, "paper_2007_06000_b200", "graphs", "squeezenet11.graph")).read()
@@ -128,6 +154,38 @@ def cpu_reference_rate(images: int, threads: int):
     return images / dt, kind, dt
 
 
+def cpu_model():
+    try:
+        for ln in open("/proc/cpuinfo"):
+            if ln.startswith("model name"):
+                return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def oracle_parity(logits, first_image, sample, tol):
+    """Checker: the timed configuration's logits of `sample` images against
+    the CPU oracle on the same inputs (SeededStream(42) images first_image+i)
+    and weights (seeded_weights(42)).  Norm-wise error and argmax agreement."""
+    import numpy as np
+
+    from oracle import oracle as O
+    text = open(os.path.join(ROOT, "paper_2007_06000_b200", "graphs", "squeezenet11.graph")).read()
+    og = O.load_graph(text)
+    c, h, w = og.inputs[0][1]
+    chw = c * h * w
+    x = np.stack([O.stream(42, (first_image + i) * chw, chw).reshape(c, h, w) for i in sample]).astype(np.float32)
+    ref = O.run_batch(og, x, O.seeded_weights(og, 42), ["pool10"], threads=min(len(sample), os.cpu_count() or 1))["pool10"]
+    got = logits[sample]
+    err = O.normwise(got, ref)
+    agree = (got.reshape(len(sample), -1).argmax(1) == ref.reshape(len(sample), -1).argmax(1))
+    return {"images_checked": len(sample), "sample": list(map(int, sample)), "normwise": float(f"{err:.3e}"), "tol": tol,
+            "within_tol": bool(err <= tol), "argmax_equal": int(agree.sum()),
+            "note": "seeded_weights(42) logits: argmax is degenerate under this init (SURVEY finding 7); the non-degenerate "
+                    "He-init argmax check of the same tuned configuration is tests/test_gpu_tc.py::test_tc_squeezenet_autotuned_b256_argmax"}
+
+
 def run_reference_arm(args, rank, world):
     if rank != 0:
         return
@@ -135,10 +193,9 @@ def run_reference_arm(args, rank, world):
     per_step = threads  # one image per host thread per step
     for _ in range(args.warmup):
         cpu_reference_rate(per_step, threads)
-    rates, kinds, secs = [], set(), 0.0
+    kinds, secs = set(), 0.0
     for _ in range(args.steps):
-        r, k, dt = cpu_reference_rate(per_step, threads)
-        rates.append(r)
+        _, k, dt = cpu_reference_rate(per_step, threads)
         kinds.add(k)
         secs += dt
     value = per_step * args.steps / secs
@@ -149,7 +206,7 @@ def run_reference_arm(args, rank, world):
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
         "config": {"workload": "squeezenet_v1.1 224x224, reference CPU run_reference (oracle/_ref)", "images_per_step": per_step,
                    "parallelism": f"openmp x{threads} over images"},
-        "cpu_baseline": {"value": round(value, 3), "unit": "images/s", "cores": threads, "kind": kind,
+        "cpu_baseline": {"value": round(value, 3), "unit": "images/s", "cores": threads, "cpu": cpu_model(), "kind": kind,
                          "sample": f"{per_step} images per step x {args.steps} steps"},
         "e2e": {"value": round(value, 3), "unit": "images/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
@@ -158,41 +215,102 @@ def run_reference_arm(args, rank, world):
 
 # ----------------------------------------------------------------------------- our arm
 
-def time_blocks(X, torch, precision, reps=20):
+def make_engine(X, g, w, part, prec, B, device, tune=True, first_image=0):
+    """Engine + seeded device inputs; tensor-core plans measured-time tuned
+    (part of the product, before any timed region)."""
+    e = X.Engine(g, w, part, prec, max_batch=B, device=device)
+    e.set_input_seeded(42, B, first_image=first_image)
+    info = None
+    if prec in TC and tune:
+        t0 = time.time()
+        e.forward(B, use_graph=False)
+        chosen = e.autotune(B, reps=3, topk=3)
+        info = {"steps_tuned": len(chosen), "seconds": round(time.time() - t0, 2)}
+        e.set_input_seeded(42, B, first_image=first_image)
+    return e, info
+
+
+def time_forwards(torch, e, B, steps, warmup, st):
+    """ms per forward: `warmup` untimed, then `steps` back to back between two
+    CUDA events on the launching stream."""
+    for _ in range(warmup):
+        e.forward(B, use_graph=True)
+    torch.cuda.synchronize()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record(st)
+    for _ in range(steps):
+        e.forward(B, use_graph=True)
+    b.record(st)
+    b.synchronize()
+    return a.elapsed_time(b) / steps
+
+
+def plan_work(steps, batch):
+    """Algorithmic bytes (inputs once + stored outputs once per image + weights
+    once per launch) and FLOPs (2 x MACs, no halo recompute) of a plan."""
+    nbytes = sum(s["bytes_algorithmic"] * batch + s.get("weight_bytes", 0) for s in steps)
+    flops = sum(2 * s["macs"] * batch for s in steps)
+    return nbytes, flops
+
+
+def roofline_frac(nbytes, flops, ms, prec, sm_mhz):
+    hbm, _, src = peaks()
+    pipe, pipe_name = pipe_peak_tflops(prec, sm_mhz)
+    t_mem, t_pipe = nbytes / (hbm * 1e9), flops / (pipe * 1e12)
+    bound = "hbm" if t_mem >= t_pipe else "pipe"
+    return {"bound": bound, "pipe": pipe_name, "roofline_us": round(max(t_mem, t_pipe) * 1e6, 2),
+            "frac": round(max(t_mem, t_pipe) / (ms * 1e-3), 4), "achieved_gbs": round(nbytes / (ms * 1e-3) / 1e9, 1),
+            "achieved_tflops": round(flops / (ms * 1e-3) / 1e12, 2), "peak_gbs": hbm, "peak_tflops": round(pipe, 1),
+            "peak_source": src}
+
+
+def time_blocks(X, torch, sm_mhz, reps=20):
     """us per fused block (B200 partition) vs the unfused kernels of the same
-    layers, BASELINE configs 1-4, inputs resident, best-of and mean."""
+    layers, BASELINE configs 1-4 at every precision, inputs resident; each
+    with its roofline fraction and algorithmic HBM bytes saved."""
     out = {}
     st = torch.cuda.current_stream()
-    for cfg, gname, batch in BLOCK_CONFIGS:
+    for cfg, gname, batch, precs in BLOCK_CONFIGS:
         g = X.load_graph(X.graph_path(gname))
         w = X.seeded_weights(g, 42)
         res = {"batch": batch}
-        for part in ("b200", "unfused"):
-            e = X.Engine(g, w, part, precision, max_batch=batch)
-            e.set_input_seeded(42, batch)
-            if precision == "bf16":  # both arms measured-time tuned
-                e.forward(batch, use_graph=False)
-                e.autotune(batch, reps=3, topk=3)
-            for _ in range(3):
-                e.forward(batch, use_graph=True)
-            torch.cuda.synchronize()
-            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            ts = []
-            for _ in range(reps):
-                a.record(st)
-                e.forward(batch, use_graph=True)
-                b.record(st)
-                b.synchronize()
-                ts.append(a.elapsed_time(b) * 1000.0)
-            steps = e.steps
-            hbm = sum(s["bytes_algorithmic"] for s in steps) * batch
-            res[part] = {"us_median": round(statistics.median(ts), 2), "us_min": round(min(ts), 2),
-                         "kernels": e.launches_per_forward, "hbm_bytes_algorithmic": int(hbm)}
-            del e
-        res["speedup"] = round(res["unfused"]["us_median"] / res["b200"]["us_median"], 3)
-        res["hbm_bytes_saved_algorithmic"] = res["unfused"]["hbm_bytes_algorithmic"] - res["b200"]["hbm_bytes_algorithmic"]
+        for prec in precs:
+            r = {}
+            for part in ("b200", "unfused"):
+                e, _ = make_engine(X, g, w, part, prec, batch, torch.cuda.current_device())
+                for _ in range(3):
+                    e.forward(batch, use_graph=True)
+                torch.cuda.synchronize()
+                ts = []
+                a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                for _ in range(reps):
+                    a.record(st)
+                    e.forward(batch, use_graph=True)
+                    b.record(st)
+                    b.synchronize()
+                    ts.append(a.elapsed_time(b) * 1000.0)
+                nbytes, flops = plan_work(e.steps, batch)
+                r[part] = {"us_median": round(statistics.median(ts), 2), "us_min": round(min(ts), 2),
+                           "kernels": e.launches_per_forward, "hbm_bytes_algorithmic": int(nbytes), "gflop": round(flops / 1e9, 4)}
+                del e
+            r["speedup"] = round(r["unfused"]["us_median"] / r["b200"]["us_median"], 3)
+            r["hbm_bytes_saved_algorithmic"] = r["unfused"]["hbm_bytes_algorithmic"] - r["b200"]["hbm_bytes_algorithmic"]
+            # roofline of the block: the fused minimum traffic / work at the measured time
+            r["roofline"] = roofline_frac(r["b200"]["hbm_bytes_algorithmic"], r["b200"]["gflop"] * 1e9, r["b200"]["us_median"] / 1000.0,
+                                          prec, sm_mhz)
+            res[prec] = r
         out[cfg] = res
     return out
+
+
+def relaunch_under_torchrun(args):
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}", "--master-addr", "127.0.0.1",
+           "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
 
 
 def main():
@@ -201,13 +319,16 @@ def main():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--precision", default="bf16", choices=["bf16", "fp32", "fp32_exact"])
+    ap.add_argument("--precision", default="bf16", choices=["bf16", "tf32", "fp32", "fp32_exact"])
     ap.add_argument("--no-blocks", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-arms", action="store_true", help="skip the other precisions / the unfused partition")
     ap.add_argument("--no-tune", action="store_true", help="skip the measured-time tuner (planner model only)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
 
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(relaunch_under_torchrun(args))
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
@@ -228,25 +349,23 @@ def main():
     g = X.load_graph(X.graph_path("squeezenet11"))
     w = X.seeded_weights(g, 42)
     B = PER_GPU_BATCH
-    e = X.Engine(g, w, "b200", args.precision, max_batch=B, device=local)
-    st = torch.cuda.current_stream()
-    # rank r's shard: images [r*B, (r+1)*B) of the seeded stream (no exchange)
-    e.set_input_seeded(42, B, first_image=rank * B)
-    tune = None
-    if args.precision == "bf16" and not args.no_tune:
-        # measured-time tuner (part of the product, before the timed region)
-        t_tune = time.time()
-        e.forward(B, use_graph=False)
-        chosen = e.autotune(B, reps=3, topk=int(os.environ.get("XLF_TOPK", "3")))
-        tune = {"steps_tuned": len(chosen), "seconds": round(time.time() - t_tune, 2)}
-        e.set_input_seeded(42, B, first_image=rank * B)
+    prec = args.precision
+    first = rank * B  # rank r's shard: images [r*B, (r+1)*B) of the seeded stream (no exchange)
+    e, tune = make_engine(X, g, w, "b200", prec, B, local, tune=not args.no_tune, first_image=first)
     nsteps = len(e.steps)
+    st = torch.cuda.current_stream()
 
     def barrier():
         torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
         torch.cuda.synchronize()
+
+    def max_ms(ms):
+        t = torch.tensor([ms], device="cuda", dtype=torch.float64)
+        if world > 1:
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
 
     for _ in range(args.warmup):
         e.forward(B, use_graph=True)
@@ -263,18 +382,32 @@ def main():
         t0 = torch.cuda.Event(enable_timing=True)
         t1 = torch.cuda.Event(enable_timing=True)
         t0.record(st)
-        for k in range(args.steps):
+        for _ in range(args.steps):
             e.forward(B, use_graph=True)
         t1.record(st)
         barrier()
         torch.cuda.profiler.stop()
-    total_ms = t0.elapsed_time(t1)
-    step_ms = torch.tensor([total_ms / args.steps], device="cuda")
+    ms_per_step = max_ms(t0.elapsed_time(t1) / args.steps)
+    clocks = clk.summary()
+
+    # --- parity of the timed configuration (its logits, after the timed loop)
+    logits = e.read("pool10", B).cpu().numpy()
+
+    # --- optional final gather of the logits to rank 0 (NCCL), timed apart
+    gather_ms = None
     if world > 1:
-        dist.all_reduce(step_ms, op=dist.ReduceOp.MAX)
-    ms_per_step = float(step_ms.item())
+        lt = torch.from_numpy(logits).cuda()
+        parts = [torch.empty_like(lt) for _ in range(world)]
+        barrier()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(st)
+        dist.all_gather(parts, lt)
+        b.record(st)
+        barrier()
+        gather_ms = max_ms(a.elapsed_time(b))
+
     # --- per-kernel durations for the roofline: the same K forwards again,
-    # step by step with an event after every kernel (not part of `value`).
+    # step by step with an event after every step (not part of `value`).
     evs = [[torch.cuda.Event(enable_timing=True) for _ in range(nsteps + 1)] for _ in range(args.steps)]
     barrier()
     for k in range(args.steps):
@@ -311,37 +444,54 @@ def main():
         e2e_step()
     b.record(st)
     barrier()
-    e2e_ms = torch.tensor([a.elapsed_time(b) / e2e_steps], device="cuda")
-    if world > 1:
-        dist.all_reduce(e2e_ms, op=dist.ReduceOp.MAX)
-    e2e_ms = float(e2e_ms.item())
-
-    blocks = None
-    if rank == 0 and not args.no_blocks:
-        blocks = time_blocks(X, torch, args.precision)
+    e2e_ms = max_ms(a.elapsed_time(b) / e2e_steps)
 
     if rank == 0:
-        hbm_peak, tf_peak, src = peaks()
+        sm_mhz = clocks["sm_mhz"]
+        # --- the other arithmetic paths and the unfused partition (same workload, same K)
+        arms = None
+        if not args.no_arms:
+            arms = {}
+            for p2 in ("bf16", "tf32", "fp32"):
+                for part in ("b200", "unfused"):
+                    if p2 == prec and part == "b200":
+                        arms[f"{p2}_{part}"] = {"images_per_s": round(B / (ms_per_step * 1e-3), 1), "ms_per_step": round(ms_per_step, 4),
+                                                "launches": e.launches_per_forward, "headline": True}
+                        continue
+                    e2, _ = make_engine(X, g, w, part, p2, B, local, tune=not args.no_tune)
+                    ms2 = time_forwards(torch, e2, B, args.steps, args.warmup, st)
+                    arms[f"{p2}_{part}"] = {"images_per_s": round(B / (ms2 * 1e-3), 1), "ms_per_step": round(ms2, 4),
+                                            "launches": e2.launches_per_forward}
+                    del e2
+            for p2 in ("bf16", "tf32", "fp32"):
+                f, u = arms.get(f"{p2}_b200"), arms.get(f"{p2}_unfused")
+                if f and u:
+                    f["speedup_vs_unfused"] = round(f["images_per_s"] / u["images_per_s"], 3)
+        blocks = None if args.no_blocks else time_blocks(X, torch, sm_mhz)
+        hbm_peak, _, src = peaks()
         dom = max(range(nsteps), key=lambda i: per_step_kernel_ms[i])
         s = e.steps[dom]
-        alg_bytes = s["bytes_algorithmic"] * B
+        alg_bytes = s["bytes_algorithmic"] * B + s.get("weight_bytes", 0)
         achieved = alg_bytes / (per_step_kernel_ms[dom] * 1e-3) / 1e9
         traffic = None
         tpath = os.path.join(ROOT, "profiles", "traffic.json")
         if os.path.exists(tpath):
             try:
-                traffic = json.load(open(tpath)).get(s["id"])
+                traffic = json.load(open(tpath)).get(prec, {}).get(s["id"])
             except Exception:
                 traffic = None
         flops = 2 * s["macs"] * B
-        simt_peak = 148 * 128 * 2 * (clk.summary()["sm_mhz"] or 1965) * 1e6 / 1e12
+        pipe, pipe_name = pipe_peak_tflops(prec, sm_mhz)
         cpu = None
+        parity = None
         if not args.no_cpu:
             threads = os.cpu_count() or 1
             rate, kind, dt = cpu_reference_rate(threads, threads)
-            cpu = {"value": round(rate, 3), "unit": "images/s", "cores": threads, "kind": kind,
+            cpu = {"value": round(rate, 3), "unit": "images/s", "cores": threads, "cpu": cpu_model(), "kind": kind,
                    "sample": f"{threads} images of squeezenet_v1.1 224x224 ({dt:.1f} s)"}
+            parity = oracle_parity(logits, first, [0, 37, 74, 111, 148, 185, 222, 255], X.api.TOLERANCE[prec])
         value = world * B / (ms_per_step * 1e-3)
+        step_nbytes, step_flops = plan_work(e.steps, B)
         line = {
             "metric": BASELINE_METRIC,
             "value": round(value, 2),
@@ -353,12 +503,14 @@ def main():
             "higher_is_better": True,
             "scaling": "weak",
             "vs_baseline": None,
-            "dtype": "bf16" if args.precision == "bf16" else "f32",
-            "precision": args.precision,
+            "dtype": DTYPE[prec],
+            "precision": prec,
             "data": "synthetic (SeededStream(42) inputs generated on device, seeded_weights(42))",
-            "config": {"workload": "squeezenet_v1.1 224x224 inference, b200 partition (8 fused fire blocks, conv1+pool1 fused)",
+            "config": {"workload": f"squeezenet_v1.1 224x224 inference, b200 partition, {prec}",
                        "batch_per_gpu": B, "global_batch": B * world, "parallelism": f"batch-sharded dp{world}, no collective",
-                       "l2": "no L2 flush needed: one forward moves > 1.5 GB through HBM (L2 126 MB), so each iteration starts with its input (103 MB bf16 / 205 MB fp32) evicted"},
+                       "plan": [f"{st_['id']}:{st_['tag']}" for st_ in e.steps],
+                       "l2": "no L2 flush needed: one forward moves > 1.4 GB through HBM (L2 126 MB), so each iteration starts "
+                             "with its input evicted"},
             "e2e": {"value": round(world * B / (e2e_ms * 1e-3), 2), "unit": "images/s",
                     "h2d_bytes_per_step": int(B * c * h * wd * 4), "d2h_bytes_per_step": int(B * 1000 * 4),
                     "path": "xlf_engine_run_host (C ABI), pinned host buffers"},
@@ -367,13 +519,16 @@ def main():
                          "traffic": traffic, "algorithmic_bytes_per_launch": int(alg_bytes),
                          "launch_ms": round(per_step_kernel_ms[dom], 4),
                          "share_of_step": round(per_step_kernel_ms[dom] / sum(per_step_kernel_ms), 4),
-                         "compute": {"pipe": "tcgen05 bf16" if args.precision == "bf16" else "fp32 FMA (SIMT)",
-                                     "achieved_tflops": round(flops / (per_step_kernel_ms[dom] * 1e-3) / 1e12, 3),
-                                     "peak_tflops": round(tf_peak if args.precision == "bf16" else simt_peak, 2)}},
+                         "compute": {"pipe": pipe_name, "achieved_tflops": round(flops / (per_step_kernel_ms[dom] * 1e-3) / 1e12, 3),
+                                     "peak_tflops": round(pipe, 2)},
+                         "step": roofline_frac(step_nbytes, step_flops, ms_per_step, prec, sm_mhz)},
             "kernels_ms": {f"{st_['id']}:{st_['tag']}": round(t, 4) for st_, t in zip(e.steps, per_step_kernel_ms)},
+            "parity": parity,
+            "arms": arms,
             "cpu_baseline": cpu,
             "gpu_launches": args.steps * e.launches_per_forward,
-            "clocks": clk.summary(),
+            "clocks": clocks,
+            "gather_ms": gather_ms,
             "blocks": blocks,
             "autotune": tune,
         }

@@ -42,7 +42,8 @@ typedef enum {
 typedef enum {
     XLF_FP32_EXACT = 0, /* bit-exact with run_reference (reference.cpp:16-57) */
     XLF_FP32 = 1,       /* FFMA, <= 1e-5 norm-wise */
-    XLF_BF16 = 2        /* bf16 operands, fp32 accumulate, <= 1e-2 norm-wise */
+    XLF_BF16 = 2,       /* bf16 operands (tcgen05 kind::f16), fp32 accumulate, <= 1e-2 norm-wise */
+    XLF_TF32 = 3        /* fp32 storage rounded to TF32 (tcgen05 kind::tf32), fp32 accumulate, <= 1e-3 norm-wise */
 } xlf_precision;
 
 typedef struct xlf_graph xlf_graph;
@@ -79,6 +80,9 @@ xlf_status xlf_store_tx(const xlf_graph* g, const char* block_id, long long* fus
  * shared bytes, tensor placement) as JSON; batch_hint steers the tile choice. */
 xlf_status xlf_device_plan_json(const xlf_graph* g, int partition, int precision, int batch_hint, char* buf, size_t cap,
                                 size_t* need);
+/* Same, with engine options (see xlf_engine_create_ex). */
+xlf_status xlf_device_plan_json_ex(const xlf_graph* g, int partition, int precision, int batch_hint, const char* options, char* buf,
+                                   size_t cap, size_t* need);
 /* seeded_weights (tensor.cpp:42-62) in save_weights stream order (tensor.cpp:64-95).
  * out may be NULL to query *count. */
 xlf_status xlf_seeded_weights(const xlf_graph* g, uint64_t seed, float* out, size_t cap, size_t* count);
@@ -89,13 +93,22 @@ xlf_status xlf_seeded_weights(const xlf_graph* g, uint64_t seed, float* out, siz
 /* weights: save_weights stream order, reference layout [oc][ic/g][kh][kw] + bias. */
 xlf_status xlf_engine_create(const xlf_graph* g, int device, int partition, int precision, const float* weights,
                              size_t n_weights, int max_batch, xlf_engine** out);
+/* Same, with planner / executor options "key=value,..." (NULL or "" = the
+ * product defaults; nothing is read from the environment).  Keys:
+ * always_fuse, unfuse (block ids separated by ';'), unfuse_ratio, mb_max_weight,
+ * xbuf, wres, tsets, ctas, no_nalt, no_tsep, no_pwait, xrel_epi, pdl, trace,
+ * tune_verbose, e2e_chunks, e2e_ramp.  XLF_E_VALIDATION for an unknown key. */
+xlf_status xlf_engine_create_ex(const xlf_graph* g, int device, int partition, int precision, const float* weights,
+                                size_t n_weights, int max_batch, const char* options, xlf_engine** out);
 void xlf_engine_destroy(xlf_engine* e);
 /* JSON description: steps (kernels, tiles, shared bytes, MACs, algorithmic bytes), tensors. */
 xlf_status xlf_engine_json(const xlf_engine* e, char* buf, size_t cap, size_t* need);
 int xlf_engine_num_steps(const xlf_engine* e);
 int xlf_engine_launches_per_forward(const xlf_engine* e);
-/* Device input, NCHW fp32 (reference layout, images stacked). */
+/* Device input, NCHW fp32 (reference layout, images stacked): the graph's
+ * first input, or the input called `name` (graphs with several inputs). */
 xlf_status xlf_engine_set_input(xlf_engine* e, const float* d_nchw, int batch, void* stream);
+xlf_status xlf_engine_set_input_named(xlf_engine* e, const char* name, const float* d_nchw, int batch, void* stream);
 /* Input generated on device from SeededStream(seed) (tensor.cpp:19-40):
  * image n = stream elements [(first_image+n)*CHW, ...). */
 xlf_status xlf_engine_set_input_seeded(xlf_engine* e, uint64_t seed, uint64_t first_image, int batch, void* stream);
@@ -111,7 +124,7 @@ xlf_status xlf_engine_run_host(xlf_engine* e, const float* h_in_nchw, int batch,
                                void* stream);
 /* Measured-time tuner (no reference counterpart: replaces the reference's
  * model-only tune(), cost_model.cpp:236-294): times the `topk` best
- * configurations of every bf16 fused step on the device (`reps` launches
+ * configurations of every tensor-core (bf16 / TF32) fused step on the device (`reps` launches
  * each, `batch` images) and keeps the fastest; fp32 engines: no-op. The
  * choices are reported by xlf_engine_tune_report (JSON) and by
  * xlf_engine_json's plan. Synchronous; not thread-safe with other calls on
@@ -123,7 +136,7 @@ xlf_status xlf_engine_tune_report(const xlf_engine* e, char* buf, size_t cap, si
  * XLF_E_VALIDATION for an unknown step, XLF_E_INFEASIBLE for a configuration
  * this plan cannot run, XLF_E_PARSE for malformed input. */
 xlf_status xlf_engine_apply_tuning(xlf_engine* e, const char* json);
-/* Profiling aid (engine created with XLF_TRACE=1 in the environment, bf16):
+/* Profiling aid (engine created with option trace=1, tensor-core precisions):
  * globaltimer stamps of the first CTAs of a step's last launch. */
 xlf_status xlf_engine_trace(const xlf_engine* e, int step, unsigned long long* out, size_t cap, size_t* count);
 

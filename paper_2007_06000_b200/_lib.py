@@ -15,9 +15,9 @@ LIB_PATH = os.path.join(HERE, "libxlfuse_b200.so")
 # Every symbol include/xlfuse_b200.h declares (checked by tests/test_abi.py).
 SYMBOLS = [
     "xlf_last_error", "xlf_version", "xlf_graph_parse", "xlf_graph_destroy", "xlf_graph_json", "xlf_graph_serialize",
-    "xlf_block_report", "xlf_blocks_json", "xlf_classify_mode", "xlf_plan_tiling", "xlf_store_tx", "xlf_device_plan_json", "xlf_seeded_weights",
-    "xlf_engine_create", "xlf_engine_destroy", "xlf_engine_json", "xlf_engine_num_steps",
-    "xlf_engine_launches_per_forward", "xlf_engine_set_input", "xlf_engine_set_input_seeded", "xlf_engine_forward",
+    "xlf_block_report", "xlf_blocks_json", "xlf_classify_mode", "xlf_plan_tiling", "xlf_store_tx", "xlf_device_plan_json", "xlf_device_plan_json_ex", "xlf_seeded_weights",
+    "xlf_engine_create", "xlf_engine_create_ex", "xlf_engine_destroy", "xlf_engine_json", "xlf_engine_num_steps",
+    "xlf_engine_launches_per_forward", "xlf_engine_set_input", "xlf_engine_set_input_named", "xlf_engine_set_input_seeded", "xlf_engine_forward",
     "xlf_engine_run_step", "xlf_engine_read", "xlf_engine_run_host", "xlf_engine_autotune", "xlf_engine_tune_report", "xlf_engine_apply_tuning",
     "xlf_engine_trace",
 ]
@@ -61,14 +61,17 @@ def lib() -> ctypes.CDLL:
     L.xlf_plan_tiling.argtypes = [vp, c_char_pp] + [ctypes.c_int] * 4 + [c_char_pp, ctypes.c_char_p, sz, szp]
     L.xlf_store_tx.argtypes = [vp, c_char_pp, ctypes.POINTER(ctypes.c_longlong), ctypes.POINTER(ctypes.c_longlong)]
     L.xlf_device_plan_json.argtypes = [vp, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_char_p, sz, szp]
+    L.xlf_device_plan_json_ex.argtypes = [vp, ctypes.c_int, ctypes.c_int, ctypes.c_int, c_char_pp, ctypes.c_char_p, sz, szp]
     L.xlf_seeded_weights.argtypes = [vp, ctypes.c_uint64, f32p, sz, szp]
     L.xlf_engine_create.argtypes = [vp, ctypes.c_int, ctypes.c_int, ctypes.c_int, f32p, sz, ctypes.c_int, ctypes.POINTER(vp)]
+    L.xlf_engine_create_ex.argtypes = [vp, ctypes.c_int, ctypes.c_int, ctypes.c_int, f32p, sz, ctypes.c_int, c_char_pp, ctypes.POINTER(vp)]
     L.xlf_engine_destroy.argtypes = [vp]
     L.xlf_engine_destroy.restype = None
     L.xlf_engine_json.argtypes = [vp, ctypes.c_char_p, sz, szp]
     L.xlf_engine_num_steps.argtypes = [vp]
     L.xlf_engine_launches_per_forward.argtypes = [vp]
     L.xlf_engine_set_input.argtypes = [vp, vp, ctypes.c_int, vp]
+    L.xlf_engine_set_input_named.argtypes = [vp, c_char_pp, vp, ctypes.c_int, vp]
     L.xlf_engine_set_input_seeded.argtypes = [vp, ctypes.c_uint64, ctypes.c_uint64, ctypes.c_int, vp]
     L.xlf_engine_forward.argtypes = [vp, ctypes.c_int, ctypes.c_int, vp]
     L.xlf_engine_run_step.argtypes = [vp, ctypes.c_int, ctypes.c_int, vp]

@@ -22,7 +22,18 @@ from . import _lib
 from ._lib import XlfError, check, lib, text_call
 
 PARTITIONS = {"reference": 0, "b200": 1, "unfused": 2}
-PRECISIONS = {"fp32_exact": 0, "fp32": 1, "bf16": 2}
+PRECISIONS = {"fp32_exact": 0, "fp32": 1, "bf16": 2, "tf32": 3}
+# norm-wise tolerance of each precision against the reference (north_star)
+TOLERANCE = {"fp32_exact": 0.0, "fp32": 1e-5, "tf32": 1e-3, "bf16": 1e-2}
+
+
+def _options(options) -> bytes:
+    """Engine options (xlf_engine_create_ex): "k=v,..." text or a dict."""
+    if options is None:
+        return b""
+    if isinstance(options, dict):
+        options = ",".join(f"{k}={int(v) if isinstance(v, bool) else v}" for k, v in options.items())
+    return options.encode()
 
 
 @dataclass
@@ -138,9 +149,10 @@ def store_transactions(g: Graph, block_id: str):
     return f.value, u.value
 
 
-def device_plan(g: Graph, partition: str = "b200", batch_hint: int = 1, precision: str = "fp32") -> dict:
+def device_plan(g: Graph, partition: str = "b200", batch_hint: int = 1, precision: str = "fp32", options=None) -> dict:
     """Host-only device program (kernel steps, tiles, tensor placement)."""
-    return json.loads(text_call(lib().xlf_device_plan_json, g._h, PARTITIONS[partition], PRECISIONS[precision], batch_hint))
+    return json.loads(text_call(lib().xlf_device_plan_json_ex, g._h, PARTITIONS[partition], PRECISIONS[precision], batch_hint,
+                                _options(options)))
 
 
 def seeded_weights(g: Graph, seed: int) -> np.ndarray:
@@ -162,12 +174,15 @@ class Engine:
     """Device executor (successor of simulate_graph, fused_exec.cpp:313-349)."""
 
     def __init__(self, g: Graph, weights: np.ndarray, partition: str = "b200", precision: str = "fp32_exact",
-                 max_batch: int = 1, device: int = 0):
+                 max_batch: int = 1, device: int = 0, options=None):
         self.graph = g
+        if partition not in PARTITIONS or precision not in PRECISIONS:
+            raise XlfError(8, f"unknown partition / precision {partition!r} / {precision!r}")
         w = np.ascontiguousarray(weights, np.float32)
         h = ctypes.c_void_p()
-        check(lib().xlf_engine_create(g._h, device, PARTITIONS[partition], PRECISIONS[precision],
-                                      w.ctypes.data_as(ctypes.POINTER(ctypes.c_float)), w.size, max_batch, ctypes.byref(h)))
+        check(lib().xlf_engine_create_ex(g._h, device, PARTITIONS[partition], PRECISIONS[precision],
+                                         w.ctypes.data_as(ctypes.POINTER(ctypes.c_float)), w.size, max_batch, _options(options),
+                                         ctypes.byref(h)))
         self._h = h
         self.partition, self.precision, self.max_batch, self.device = partition, precision, max_batch, device
         self.info = json.loads(text_call(lib().xlf_engine_json, h))
@@ -186,10 +201,21 @@ class Engine:
     def launches_per_forward(self) -> int:
         return lib().xlf_engine_launches_per_forward(self._h)
 
-    def set_input(self, x, stream=None):
-        """x: torch CUDA float32 NCHW [batch, C, H, W] (contiguous)."""
-        assert x.is_cuda and x.dtype.is_floating_point and x.is_contiguous()
-        check(lib().xlf_engine_set_input(self._h, ctypes.c_void_p(x.data_ptr()), x.shape[0], _stream_ptr(stream)))
+    def _check_input(self, x, name, device):
+        import torch
+        shape = self.graph.shape_of(name)
+        ok = isinstance(x, torch.Tensor) and x.dtype == torch.float32 and x.dim() == 4 and tuple(x.shape[1:]) == tuple(shape)
+        if not ok or (device and not (x.is_cuda and x.is_contiguous())):
+            raise XlfError(8, f"input {name!r} must be a contiguous{' CUDA' if device else ''} float32 [batch, {shape[0]}, "
+                              f"{shape[1]}, {shape[2]}] tensor, got {getattr(x, 'dtype', type(x))} {tuple(getattr(x, 'shape', ()))}")
+
+    def set_input(self, x, stream=None, name=None):
+        """x: torch CUDA float32 NCHW [batch, C, H, W] (contiguous); `name`
+        selects the graph input (default: the first)."""
+        name = name or self.graph.inputs[0][0]
+        self._check_input(x, name, True)
+        check(lib().xlf_engine_set_input_named(self._h, name.encode(), ctypes.c_void_p(x.data_ptr()), x.shape[0],
+                                               _stream_ptr(stream)))
 
     def set_input_seeded(self, seed: int, batch: int, first_image: int = 0, stream=None):
         check(lib().xlf_engine_set_input_seeded(self._h, seed, first_image, batch, _stream_ptr(stream)))
@@ -209,7 +235,10 @@ class Engine:
 
     def run_host(self, x: np.ndarray, name: str, stream=None) -> np.ndarray:
         """End to end from host memory (H2D + forward + D2H), synchronous."""
-        x = np.ascontiguousarray(x, np.float32)
+        shape = self.graph.inputs[0][1]
+        if not isinstance(x, np.ndarray) or x.dtype != np.float32 or x.ndim != 4 or tuple(x.shape[1:]) != tuple(shape):
+            raise XlfError(8, f"run_host input must be a float32 [batch, {shape[0]}, {shape[1]}, {shape[2]}] array")
+        x = np.ascontiguousarray(x)
         out = np.empty((x.shape[0],) + tuple(self.graph.shape_of(name)), np.float32)
         f32p = ctypes.POINTER(ctypes.c_float)
         check(lib().xlf_engine_run_host(self._h, x.ctypes.data_as(f32p), x.shape[0], name.encode(),
@@ -217,7 +246,7 @@ class Engine:
         return out
 
     def autotune(self, batch: int = 0, reps: int = 3, topk: int = 4) -> list:
-        """Measured-time tuning of the bf16 fused steps (xlf_engine_autotune):
+        """Measured-time tuning of the tensor-core (bf16 / TF32) fused steps (xlf_engine_autotune):
         returns the chosen configuration of every tuned step."""
         check(lib().xlf_engine_autotune(self._h, batch, reps, topk))
         self.info = json.loads(text_call(lib().xlf_engine_json, self._h))

@@ -28,6 +28,12 @@ namespace {
 
 thread_local std::string g_error;
 
+// A NULL / malformed argument at the boundary (XLF_E_ARG), as opposed to a
+// graph / plan validation failure (XLF_E_VALIDATION).
+struct ArgError : std::invalid_argument {
+    using std::invalid_argument::invalid_argument;
+};
+
 xlf_status code_of(xlf::ErrorKind k) {
     switch (k) {
     case xlf::ErrorKind::io: return XLF_E_IO;
@@ -50,6 +56,9 @@ xlf_status guard(F&& f) {
     } catch (const xlf::Error& e) {
         g_error = e.what();
         return code_of(e.kind());
+    } catch (const ArgError& e) {
+        g_error = e.what();
+        return XLF_E_ARG;
     } catch (const std::exception& e) {
         g_error = e.what();
         return XLF_E_INTERNAL;
@@ -64,7 +73,7 @@ void put(const std::string& s, char* buf, size_t cap, size_t* need) {
 }
 
 void need_ptr(const void* p, const char* what) {
-    if (!p) throw xlf::Error(xlf::ErrorKind::validation, std::string(what) + " is NULL");
+    if (!p) throw ArgError(std::string(what) + " is NULL");
 }
 
 std::string jstr(const std::string& s) {
@@ -229,13 +238,20 @@ xlf_status xlf_store_tx(const xlf_graph* h, const char* block_id, long long* fus
     });
 }
 
-xlf_status xlf_device_plan_json(const xlf_graph* h, int part, int prec, int batch_hint, char* buf, size_t cap, size_t* need) {
+xlf_status xlf_device_plan_json_ex(const xlf_graph* h, int part, int prec, int batch_hint, const char* options, char* buf, size_t cap,
+                                   size_t* need) {
     return guard([&] {
         need_ptr(h, "graph");
-        if (part < 0 || part > 2) xlf::fail(xlf::ErrorKind::validation, "unknown partition");
-        put(xlf::describe_plan_json(h->g, xlf::plan_device(h->g, xlf::Partition(part), batch_hint, 227 * 1024, prec == XLF_BF16)),
-            buf, cap, need);
+        if (part < 0 || part > 2) throw ArgError("unknown partition");
+        if (prec < 0 || prec > 3) throw ArgError("unknown precision");
+        const int es = prec == XLF_BF16 ? 2 : prec == XLF_TF32 ? 4 : 0;
+        const xlf::Knobs k = xlf::Knobs::parse(options ? options : "");
+        put(xlf::describe_plan_json(h->g, xlf::plan_device(h->g, xlf::Partition(part), batch_hint, 227 * 1024, es, k)), buf, cap, need);
     });
+}
+
+xlf_status xlf_device_plan_json(const xlf_graph* h, int part, int prec, int batch_hint, char* buf, size_t cap, size_t* need) {
+    return xlf_device_plan_json_ex(h, part, prec, batch_hint, nullptr, buf, cap, need);
 }
 
 xlf_status xlf_seeded_weights(const xlf_graph* h, uint64_t seed, float* out, size_t cap, size_t* count) {
@@ -250,16 +266,22 @@ xlf_status xlf_seeded_weights(const xlf_graph* h, uint64_t seed, float* out, siz
     });
 }
 
-xlf_status xlf_engine_create(const xlf_graph* h, int device, int part, int prec, const float* weights, size_t n, int max_batch,
-                             xlf_engine** out) {
+xlf_status xlf_engine_create_ex(const xlf_graph* h, int device, int part, int prec, const float* weights, size_t n, int max_batch,
+                                const char* options, xlf_engine** out) {
     return guard([&] {
         need_ptr(h, "graph"), need_ptr(weights, "weights"), need_ptr(out, "out");
-        if (part < 0 || part > 2) xlf::fail(xlf::ErrorKind::validation, "unknown partition");
-        if (prec < 0 || prec > 2) xlf::fail(xlf::ErrorKind::validation, "unknown precision");
+        if (part < 0 || part > 2) throw ArgError("unknown partition");
+        if (prec < 0 || prec > 3) throw ArgError("unknown precision");
+        const xlf::Knobs k = xlf::Knobs::parse(options ? options : "");
         auto e = std::make_unique<xlf_engine>();
-        e->e = std::make_unique<xlf::Engine>(h->g, device, xlf::Partition(part), xlf::Precision(prec), weights, n, max_batch);
+        e->e = std::make_unique<xlf::Engine>(h->g, device, xlf::Partition(part), xlf::Precision(prec), weights, n, max_batch, k);
         *out = e.release();
     });
+}
+
+xlf_status xlf_engine_create(const xlf_graph* h, int device, int part, int prec, const float* weights, size_t n, int max_batch,
+                             xlf_engine** out) {
+    return xlf_engine_create_ex(h, device, part, prec, weights, n, max_batch, nullptr, out);
 }
 
 void xlf_engine_destroy(xlf_engine* e) { delete e; }
@@ -278,6 +300,13 @@ xlf_status xlf_engine_set_input(xlf_engine* e, const float* d, int batch, void* 
     return guard([&] {
         need_ptr(e, "engine"), need_ptr(d, "input");
         e->e->set_input_nchw(e->e->graph().inputs[0].name, d, batch, static_cast<cudaStream_t>(st));
+    });
+}
+
+xlf_status xlf_engine_set_input_named(xlf_engine* e, const char* name, const float* d, int batch, void* st) {
+    return guard([&] {
+        need_ptr(e, "engine"), need_ptr(name, "name"), need_ptr(d, "input");
+        e->e->set_input_nchw(name, d, batch, static_cast<cudaStream_t>(st));
     });
 }
 

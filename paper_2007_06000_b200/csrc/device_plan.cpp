@@ -1,5 +1,5 @@
 #include "device_plan.hpp"
-#include "bf16_params.hpp"
+#include "tc_params.hpp"
 
 #include <algorithm>
 #include <cstdlib>
@@ -401,9 +401,14 @@ bool choose_tile_at(const Graph& g, StepSpec& s, int batch_hint, int smem_budget
     return true;
 }
 
+}  // namespace
+
+// Algorithmic traffic / work of a step: block inputs once +
+// stored outputs once per image (bytes_algorithmic), weights + biases once
+// per launch (weight_bytes), MACs without halo recompute.
 void fill_stats(const Graph& g, const DevicePlan& plan, StepSpec& s) {
-    const double es = plan.bf16 ? 2.0 : 4.0;  // bytes per activation / weight element
-    s.macs = 0, s.bytes_algorithmic = 0, s.macs_executed = 0;
+    const double es = plan.tc_es ? double(plan.tc_es) : 4.0;  // bytes per activation / weight element
+    s.macs = 0, s.bytes_algorithmic = 0, s.macs_executed = 0, s.weight_bytes = 0;
     for (const std::string& in : s.inputs) s.bytes_algorithmic += double(g.shape_of(in).elements()) * es;
     if (s.kind == StepSpec::CONCAT_COPY) {
         s.bytes_algorithmic *= 2;
@@ -413,7 +418,7 @@ void fill_stats(const Graph& g, const DevicePlan& plan, StepSpec& s) {
         const Layer& l = *g.find_layer(op.layer);
         if (l.kind == LayerKind::conv) {
             s.macs += double(l.out_shape->elements()) * double(l.conv->macs_per_output());
-            s.bytes_algorithmic += double(l.conv->weight_count() + l.conv->bias_count()) * es;
+            s.weight_bytes += double(l.conv->weight_count() + l.conv->bias_count()) * es;
         }
         if (op.emit) s.bytes_algorithmic += double(g.shape_of(s.gap_out.empty() ? op.layer : s.gap_out).elements()) * es;
     }
@@ -421,7 +426,7 @@ void fill_stats(const Graph& g, const DevicePlan& plan, StepSpec& s) {
         s.bytes_algorithmic += double(g.shape_of(s.layers[0]).elements()) * es;
         return;
     }
-    if (plan.bf16) {
+    if (plan.tc_es) {
         s.macs_executed = s.macs;
         return;
     }
@@ -435,16 +440,57 @@ void fill_stats(const Graph& g, const DevicePlan& plan, StepSpec& s) {
     }
 }
 
-}  // namespace
+Knobs Knobs::parse(const std::string& text) {
+    Knobs k;
+    size_t pos = 0;
+    while (pos < text.size()) {
+        size_t end = text.find(',', pos);
+        if (end == std::string::npos) end = text.size();
+        const std::string item = text.substr(pos, end - pos);
+        pos = end + 1;
+        if (item.find_first_not_of(" \t") == std::string::npos) continue;
+        const size_t eq = item.find('=');
+        if (eq == std::string::npos) fail(ErrorKind::validation, "options: '" + item + "' is not key=value");
+        const std::string key = item.substr(0, eq), val = item.substr(eq + 1);
+        char* rest = nullptr;
+        const double num = std::strtod(val.c_str(), &rest);
+        const bool is_num = !val.empty() && rest && *rest == 0;
+        auto need_num = [&]() {
+            if (!is_num) fail(ErrorKind::validation, "options: '" + key + "' needs a number, got '" + val + "'");
+            return num;
+        };
+        if (key == "always_fuse") k.always_fuse = need_num() != 0;
+        else if (key == "unfuse") k.unfuse = ";" + val + ";";
+        else if (key == "unfuse_ratio") k.unfuse_ratio = need_num();
+        else if (key == "mb_max_weight") k.mb_max_weight = need_num();
+        else if (key == "no_nalt") k.no_nalt = need_num() != 0;
+        else if (key == "no_tsep") k.no_tsep = need_num() != 0;
+        else if (key == "no_pwait") k.no_pwait = need_num() != 0;
+        else if (key == "xrel_epi") k.xrel_epi = need_num() != 0;
+        else if (key == "xbuf") k.xbuf = int(need_num());
+        else if (key == "wres") k.wres = int(need_num());
+        else if (key == "tsets") k.tsets = int(need_num());
+        else if (key == "ctas") k.ctas = int(need_num());
+        else if (key == "pdl") k.pdl = need_num() != 0;
+        else if (key == "trace") k.trace = int(need_num());
+        else if (key == "tune_verbose") k.tune_verbose = need_num() != 0;
+        else if (key == "e2e_chunks") k.e2e_chunks = std::max(1, int(need_num()));
+        else if (key == "e2e_ramp") k.e2e_ramp = need_num() != 0;
+        else fail(ErrorKind::validation, "options: unknown key '" + key + "'");
+    }
+    return k;
+}
 
-DevicePlan plan_device(const Graph& g, Partition part, int batch_hint, int smem_budget, bool bf16) {
+DevicePlan plan_device(const Graph& g, Partition part, int batch_hint, int smem_budget, int tc_es, const Knobs& knobs) {
     if (!g.shapes_inferred()) fail(ErrorKind::internal, "plan_device requires inferred shapes");
+    if (tc_es != 0 && tc_es != 2 && tc_es != 4) fail(ErrorKind::validation, "plan_device: element size must be 0, 2 or 4");
     DevicePlan plan;
     plan.partition = part;
-    plan.bf16 = bf16;
-    const int cpad = bf16 ? 8 : 4;  // channel padding of HBM tensors (16 bytes)
+    plan.tc_es = tc_es;
+    const bool tc = tc_es != 0;
+    const int cpad = tc_es == 2 ? 8 : 4;  // channel padding of HBM tensors (16 bytes)
     auto tile = [&](StepSpec& st) {
-        return bf16 ? choose_tile_bf16(g, st, batch_hint, std::min(smem_budget, kSmemBudgetBf16)) : choose_tile(g, st, batch_hint, smem_budget);
+        return tc ? choose_tile_tc(g, st, batch_hint, std::min(smem_budget, kSmemBudgetTc), tc_es, knobs) : choose_tile(g, st, batch_hint, smem_budget);
     };
     if (part == Partition::reference) plan.blocks = detect_fusion_blocks(g);
     else if (part == Partition::b200) plan.blocks = detect_fusion_blocks_b200(g);
@@ -472,13 +518,13 @@ DevicePlan plan_device(const Graph& g, Partition part, int batch_hint, int smem_
         StepSpec s = step_for_block(g, b);
         if (s.kind == StepSpec::FUSED && !tile(s)) {
             if (!b.fused()) fail(ErrorKind::infeasible, "layer " + b.members[0] + " does not fit shared memory at any tile");
-            // bf16: conv -> global average pool runs as one kernel whose
-            // epilogue reduces (the conv output never reaches HBM).
-            if (bf16 && part == Partition::b200 && s.ops.size() == 2 && s.ops[0].stage == 1 && s.ops[1].stage == 2) {
+            // tensor cores: conv -> global average pool runs as one kernel
+            // whose epilogue reduces (the conv output never reaches HBM).
+            if (tc && part == Partition::b200 && s.ops.size() == 2 && s.ops[0].stage == 1 && s.ops[1].stage == 2) {
                 const Layer& c = *g.find_layer(s.ops[0].layer);
                 const Layer& p = *g.find_layer(s.ops[1].layer);
                 if (c.kind == LayerKind::conv && p.kind == LayerKind::pool && p.pool->kind == PoolKind::avg && p.pool->pad == 0 &&
-                    p.pool->kernel == c.out_shape->height && p.pool->kernel == c.out_shape->width && bf16_mma_ok(c) &&
+                    p.pool->kernel == c.out_shape->height && p.pool->kernel == c.out_shape->width && tc_mma_ok(c, tc_es) &&
                     !g.is_output(c.name) && g.consumers_of(c.name).size() == 1) {
                     StepSpec t = s;
                     t.tag = "conv+gap";
@@ -504,16 +550,15 @@ DevicePlan plan_device(const Graph& g, Partition part, int batch_hint, int smem_
             }
             continue;
         }
-        // bf16 B200: fusion is not free -- a fused block stages its producers'
+        // tensor-core B200: fusion is not free -- a fused block stages its producers'
         // (wider) inputs, so its tiles are smaller and a weight-heavy consumer
         // re-streams its weights for more tiles.  Keep the block fused only if
         // the planner's model says it beats its layers run as single kernels
         // plus the HBM round trip of the intermediates (SURVEY §8f rank 1's
         // model, the same scores the measured tuner starts from).
-        if (bf16 && part == Partition::b200 && s.kind == StepSpec::FUSED && b.fused() && s.gap_out.empty() &&
-            !std::getenv("XLF_ALWAYS_FUSE")) {
-            const int budget = std::min(smem_budget, kSmemBudgetBf16);
-            const std::vector<BCandidate> fc = candidates_bf16(g, s, batch_hint, budget);
+        if (tc && part == Partition::b200 && s.kind == StepSpec::FUSED && b.fused() && s.gap_out.empty() && !knobs.always_fuse) {
+            const int budget = std::min(smem_budget, kSmemBudgetTc);
+            const std::vector<BCandidate> fc = candidates_tc(g, s, batch_hint, budget, tc_es, knobs);
             double fused = fc.empty() ? 1e300 : fc.front().model, single = 0;
             std::vector<StepSpec> singles;
             for (const std::string& m : b.members) {
@@ -525,7 +570,7 @@ DevicePlan plan_device(const Graph& g, Partition part, int batch_hint, int smem_
                     single = 1e300;
                     break;
                 }
-                const std::vector<BCandidate> sc = candidates_bf16(g, t, batch_hint, budget);
+                const std::vector<BCandidate> sc = candidates_tc(g, t, batch_hint, budget, tc_es, knobs);
                 if (sc.empty()) {
                     single = 1e300;
                     break;
@@ -534,14 +579,9 @@ DevicePlan plan_device(const Graph& g, Partition part, int batch_hint, int smem_
                 single += sc.front().model;
                 singles.push_back(t);
             }
-            bool force_split = false;  // experiment knob: XLF_UNFUSE=<block id>[,<block id>...]
-            if (const char* e = std::getenv("XLF_UNFUSE")) {
-                const std::string list = std::string(",") + e + ",";
-                force_split = list.find("," + b.id + ",") != std::string::npos;
-            }
-            double ratio = 0.85;  // model margin a split must win by
-            if (const char* e = std::getenv("XLF_UNFUSE_RATIO")) ratio = std::atof(e);
-            if (force_split || single < ratio * fused) {
+            // experiment knob: unfuse=<block id>[;<block id>...]
+            const bool force_split = knobs.unfuse.find(";" + b.id + ";") != std::string::npos;
+            if (force_split || single < knobs.unfuse_ratio * fused) {
                 for (StepSpec& t : singles) steps.push_back(t);
                 continue;
             }
@@ -553,8 +593,7 @@ DevicePlan plan_device(const Graph& g, Partition part, int batch_hint, int smem_
     // read the same single tensor and whose outputs share one extent run as
     // one kernel (one staged input region), if the union still fits.
     if (part == Partition::b200) {
-        double mb_max_weight = -1;
-        if (const char* e = std::getenv("XLF_MB_MAXW")) mb_max_weight = std::atof(e);
+        const double mb_max_weight = knobs.mb_max_weight;
         std::vector<char> gone(steps.size(), 0);
         for (size_t i = 0; i < steps.size(); ++i) {
             if (gone[i] || steps[i].kind != StepSpec::FUSED || steps[i].inputs.size() != 1) continue;
@@ -587,7 +626,7 @@ DevicePlan plan_device(const Graph& g, Partition part, int batch_hint, int smem_
                     double wb = 0;
                     for (const OpSpec& op : m.ops) {
                         const Layer& l = *g.find_layer(op.layer);
-                        if (l.kind == LayerKind::conv) wb += double(l.conv->weight_count()) * (bf16 ? 2 : 4);
+                        if (l.kind == LayerKind::conv) wb += double(l.conv->weight_count()) * (tc_es == 2 ? 2 : 4);
                     }
                     if (wb > mb_max_weight) continue;
                 }
@@ -739,7 +778,8 @@ std::string describe_plan_json(const Graph& g, const DevicePlan& plan) {
         os << (i ? "," : "") << "{\"id\":" << q(s.id) << ",\"kind\":" << q(kinds[s.kind]) << ",\"tag\":" << q(s.tag)
            << ",\"mode\":" << q(to_string(s.mode)) << ",\"tile\":[" << s.tile_h << "," << s.tile_w
            << "],\"out\":[" << s.out_h << "," << s.out_w << "],\"smem_bytes\":" << s.smem_bytes << ",\"nxb\":" << s.nxb << ",\"wres\":" << s.wres << ",\"ring_slots\":" << s.ring_slots << ",\"grid_all\":" << s.grid_all << ",\"epi_warps\":" << s.epi_warps << ",\"tsets\":" << s.tsets << ",\"macs\":" << s.macs
-           << ",\"macs_executed\":" << s.macs_executed << ",\"bytes_algorithmic\":" << s.bytes_algorithmic << ",\"inputs\":[";
+           << ",\"macs_executed\":" << s.macs_executed << ",\"bytes_algorithmic\":" << s.bytes_algorithmic
+           << ",\"weight_bytes\":" << s.weight_bytes << ",\"ring_chunk\":" << s.ring_chunk << ",\"inputs\":[";
         for (size_t k = 0; k < s.inputs.size(); ++k) os << (k ? "," : "") << q(s.inputs[k]);
         os << "],\"layers\":[";
         for (size_t k = 0; k < s.layers.size(); ++k) os << (k ? "," : "") << q(s.layers[k]);

@@ -21,6 +21,32 @@ namespace xlf {
 enum class Partition { reference = 0, b200 = 1, unfused = 2 };
 const char* to_string(Partition p);
 
+// Engine / planner options: the "key=value,..." string of xlf_engine_create_ex
+// (nothing is read from the environment).  The defaults are the product
+// configuration; the rest pin one synchronisation / staging mode (tests run
+// every mode the tuner may pick) or steer an experiment.
+struct Knobs {
+    bool always_fuse = false;    // always_fuse=1: no cost-based split of fused blocks
+    std::string unfuse;          // unfuse=b3;b4: split these blocks
+    double unfuse_ratio = 0.85;  // model margin a split must win by
+    double mb_max_weight = -1;   // cap (bytes) on a multi-branch kernel's conv weights (<0: none)
+    bool no_nalt = false;        // no N-block TMEM column alternation
+    bool no_tsep = false;        // groups share TMEM columns
+    bool no_pwait = false;       // a tile's first group waits for the previous tile's last unit
+    bool xrel_epi = false;       // staging buffer released by the epilogue warps
+    int xbuf = 0;                // force 1 / 2 input staging buffers
+    int wres = -1;               // force resident (1) / ring-streamed (0) weights
+    int tsets = 0;               // force 1 / 2 accumulator sets
+    int ctas = 0;                // cap on resident CTAs per SM
+    bool pdl = true;             // programmatic dependent launch between steps
+    int trace = 0;               // 1: phase stamps of a steady tile, 2: tile end stamps
+    bool tune_verbose = false;   // autotune prints every timing to stderr
+    int e2e_chunks = 4;          // run_host pipeline depth
+    bool e2e_ramp = false;       // run_host: half-size first / last chunk
+    // Throws ErrorKind::validation on an unknown key or malformed value.
+    static Knobs parse(const std::string& text);
+};
+
 struct TensorSlot {
     bool materialized = false;
     int alloc = -1;               // allocation index
@@ -48,14 +74,15 @@ struct StepSpec {
     std::vector<std::string> layers;   // every layer executed by this step
     int out_h = 0, out_w = 0;
     int tile_h = 0, tile_w = 0;
-    int nxb = 1;  // bf16: input staging buffers (2 = next tile's inputs prefetched)
-    int wres = 0;       // bf16: weights resident in shared memory (else streamed through the ring)
-    int ring_slots = 3; // bf16: ring depth when streamed
-    int grid_all = 0;   // bf16: one tile per CTA (grid = tiles) instead of a persistent grid
-    int epi_warps = 8;  // bf16: epilogue/SIMT warps per CTA (4 or 8)
-    int tsets = 1;      // bf16: TMEM accumulator sets (2 = cross-tile MMA/epilogue overlap)
-    int ring_chunk = 16384;  // bf16: bytes per weight-ring slot
-    // bf16 conv + global average pool (SqueezeNet conv10 -> pool10): the
+    // tensor-core steps (bf16 / TF32):
+    int nxb = 1;        // input staging buffers (2 = next tile's inputs prefetched)
+    int wres = 0;       // weights resident in shared memory (else streamed through the ring)
+    int ring_slots = 3; // ring depth when streamed
+    int grid_all = 0;   // one tile per CTA (grid = tiles) instead of a persistent grid
+    int epi_warps = 8;  // epilogue/SIMT warps per CTA (4 or 8)
+    int tsets = 1;      // TMEM accumulator sets (2 = cross-tile MMA/epilogue overlap)
+    int ring_chunk = 16384;  // bytes per weight-ring slot
+    // tensor-core conv + global average pool (SqueezeNet conv10 -> pool10): the
     // step's single conv op never stores its output; its epilogue reduces
     // every tile over its cells and the pooled layer `gap_out` (1x1) is
     // finished by a small reduction kernel.  Tiles are over the conv output.
@@ -65,12 +92,13 @@ struct StepSpec {
     // statistics (per image)
     double macs = 0;            // algorithmic MACs (no halo recompute)
     double macs_executed = 0;   // including halo recompute and edge waste
-    double bytes_algorithmic = 0;  // inputs once + weights once + outputs once (fp32)
+    double bytes_algorithmic = 0;  // block inputs once + stored outputs once, per image (HBM element size)
+    double weight_bytes = 0;       // weights + biases once per launch (HBM element size)
 };
 
 struct DevicePlan {
     Partition partition = Partition::b200;
-    bool bf16 = false;                   // element type of the HBM tensors (else fp32)
+    int tc_es = 0;                       // 0: fp32 SIMT kernels; 2: bf16 / 4: TF32 tensor-core kernels (HBM element bytes)
     std::vector<FusionBlock> blocks;     // the partition, reference vocabulary
     std::vector<StepSpec> steps;
     std::map<std::string, TensorSlot> tensors;
@@ -84,26 +112,27 @@ struct DevicePlan {
 std::vector<FusionBlock> detect_fusion_blocks_b200(const Graph& g);
 
 // batch_hint steers the tile choice (enough CTAs to fill 148 SMs).
-// bf16: plan for the tensor-core kernel (kernels_bf16.cu): bf16 NHWC tensors
-// with channels padded to 8, tiles from its geometry (device_plan_bf16.cpp).
-DevicePlan plan_device(const Graph& g, Partition part, int batch_hint = 1, int smem_budget_bytes = 227 * 1024,
-                       bool bf16 = false);
+// tc_es = 2 / 4: plan for the tensor-core kernel (kernels_tc.cu): bf16 / fp32
+// (TF32) NHWC tensors with channels padded to 16 bytes, tiles from its
+// geometry (device_plan_tc.cpp); tc_es = 0: the fp32 SIMT kernel.
+DevicePlan plan_device(const Graph& g, Partition part, int batch_hint = 1, int smem_budget_bytes = 227 * 1024, int tc_es = 0,
+                       const Knobs& knobs = Knobs{});
 
-// device_plan_bf16.cpp
-bool bf16_mma_ok(const Layer& l);
-void bf16_nblocks(int cout, int* nblocks, int* nb);
-long long layout_bf16(const Graph& g, const StepSpec& s, int th, int tw, struct BParams* P, int nxb = 1, int wres = 0,
-                      int ring_slots = 3, int tsets = 1, int chunk = 16384);
-bool choose_tile_bf16(const Graph& g, StepSpec& s, int batch_hint, int smem_budget);
-// One configuration of a bf16 step: tile, staging buffers, weight residency /
+// device_plan_tc.cpp
+bool tc_mma_ok(const Layer& l, int es);
+void tc_nblocks(int cout, int* nblocks, int* nb);
+long long layout_tc(const Graph& g, const StepSpec& s, int th, int tw, struct BParams* P, int nxb, int wres, int ring_slots, int tsets,
+                    int chunk, int es, const Knobs& k);
+bool choose_tile_tc(const Graph& g, StepSpec& s, int batch_hint, int smem_budget, int es, const Knobs& k);
+// One configuration of a tensor-core step: tile, staging buffers, weight residency /
 // ring depth, shared bytes, and the model's score (SM cycles, lower better).
 struct BCandidate {
     int th, tw, nxb, wres, slots, smem, epi_warps, tsets, chunk;
     double model;
 };
-std::vector<BCandidate> candidates_bf16(const Graph& g, const StepSpec& s, int batch_hint, int smem_budget);
+std::vector<BCandidate> candidates_tc(const Graph& g, const StepSpec& s, int batch_hint, int smem_budget, int es, const Knobs& k);
 void apply_candidate(StepSpec& s, const BCandidate& c);
-std::vector<uint16_t> pack_weights_bf16(const Graph& g, const float* flat, size_t count, std::map<std::string, long long>& off);
+std::vector<uint8_t> pack_weights_tc(const Graph& g, const float* flat, size_t count, std::map<std::string, long long>& off, int es);
 
 // Packs reference-layout weights (save_weights stream order, tensor.cpp:64-95)
 // into the device layout of `plan`: per conv [cin/group][kh][kw][cout_pad4]
@@ -116,5 +145,9 @@ FusedParams make_params(const Graph& g, const DevicePlan& plan, const StepSpec& 
                         const std::vector<float*>& alloc_base, const float* wbase);
 
 std::string describe_plan_json(const Graph& g, const DevicePlan& plan);
+
+// Recomputes a step's statistics (macs, bytes_algorithmic, weight_bytes)
+// against graph `g` (e.g. the user's graph when the engine rewrote a layer).
+void fill_stats(const Graph& g, const DevicePlan& plan, StepSpec& s);
 
 }  // namespace xlf

@@ -1,13 +1,15 @@
-// Geometry of the bf16 tensor-core kernel (kernels_bf16.cu) for a step of
-// the device program: per-op MMA/SIMT choice, regions, TMEM columns, shared
-// bytes, and the bf16 weight packing the MMA B operand reads.
+// Geometry of the tensor-core kernel (kernels_tc.cu) for a step of the device
+// program: per-op MMA/SIMT choice, regions, TMEM columns, shared bytes, and
+// the weight packing the MMA B operand reads.  `es` is the element size of
+// the step (2: bf16, 4: fp32 storage of TF32 values); every shared layout is
+// in 16-byte chunks (cpc = 16 / es channels) and 32-byte K steps.
 #include <algorithm>
 #include <vector>
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
 
-#include "bf16_params.hpp"
+#include "tc_params.hpp"
 #include "common.hpp"
 #include "device_plan.hpp"
 
@@ -15,8 +17,8 @@ namespace xlf {
 
 namespace {
 
-int r8(int c) { return (c + 7) & ~7; }
 int r16(int c) { return (c + 15) & ~15; }
+int rc(int c, int es) { const int cpc = 16 / es; return (c + cpc - 1) / cpc * cpc; }  // channels rounded up to a chunk
 int r128(int c) { return (c + 127) & ~127; }
 int cdiv(int a, int b) { return (a + b - 1) / b; }
 int pow2_cols(int c) {
@@ -39,20 +41,25 @@ constexpr int kSlack = 2048;  // contiguous-M tiles may read up to 127 cells pas
 
 }  // namespace
 
-bool bf16_mma_ok(const Layer& l) {
-    return l.kind == LayerKind::conv && l.conv->stride == 1 && l.conv->group == 1 && l.conv->in_channels % 16 == 0;
+bool tc_mma_ok(const Layer& l, int es) {  // whole 32-byte K steps: Cin % 16 (bf16) / % 8 (TF32)
+    return l.kind == LayerKind::conv && l.conv->stride == 1 && l.conv->group == 1 && (l.conv->in_channels * es) % 32 == 0;
 }
 
 // N blocking of an MMA conv: nblocks x nb accumulator columns, nb % 16 == 0, nb <= 256.
-void bf16_nblocks(int cout, int* nblocks, int* nb) {
+void tc_nblocks(int cout, int* nblocks, int* nb) {
     const int n16 = r16(cout);
     *nblocks = cdiv(n16, 256);
     *nb = r16(cdiv(n16, *nblocks));
 }
 
-long long layout_bf16(const Graph& g, const StepSpec& s, int th, int tw, BParams* P, int nxb, int wres, int ring_slots, int tsets,
-                      int chunk) {
+long long layout_tc(const Graph& g, const StepSpec& s, int th, int tw, BParams* P, int nxb, int wres, int ring_slots, int tsets,
+                    int chunk, int es, const Knobs& k) {
     const int nops = int(s.ops.size());
+    if (es != 2 && es != 4) return -1;
+    const int cpc = 16 / es;
+    // tuning-report values come from outside: reject what the kernel cannot run
+    if (nxb < 1 || nxb > 2 || tsets < 1 || tsets > 2 || th < 1 || tw < 1) return -1;
+    if (!wres && (ring_slots < 1 || ring_slots > kRingMax || chunk < 1024 || chunk % 1024)) return -1;
     if (nops > kBMaxOps || s.inputs.size() > size_t(kMaxIns)) return -1;
     struct G {
         int ext_h, ext_w, mul, sub, d;
@@ -65,7 +72,7 @@ long long layout_bf16(const Graph& g, const StepSpec& s, int th, int tw, BParams
     int nbufs = 0;
     for (int i = 0; i < nops; ++i) {
         const Layer& l = *g.find_layer(s.ops[size_t(i)].layer);
-        geo[size_t(i)] = {th, tw, 1, 0, 0, bf16_mma_ok(l), false};
+        geo[size_t(i)] = {th, tw, 1, 0, 0, tc_mma_ok(l, es), false};
     }
     // staged buffers: lead L, stride S, trail T from the readers (+ the rows /
     // columns windowed MMA readers over-read)
@@ -96,7 +103,7 @@ long long layout_bf16(const Graph& g, const StepSpec& s, int th, int tw, BParams
         for (const OpSpec& c : s.ops) {
             if (c.stage != 2 || std::find(c.srcs.begin(), c.srcs.end(), i) == c.srcs.end()) continue;
             const Layer& cl = *g.find_layer(c.layer);
-            if (!bf16_mma_ok(cl)) continue;
+            if (!tc_mma_ok(cl, es)) continue;
             const Win w = win(cl);
             eh = std::max(eh, rows_m - 1 + w.kh - 1 + (L - w.pad) + 1);
             ew = std::max(ew, cols_m - 1 + w.kw - 1 + (L - w.pad) + 1);
@@ -159,7 +166,7 @@ long long layout_bf16(const Graph& g, const StepSpec& s, int th, int tw, BParams
                 if (c.stage != 2 || std::find(c.srcs.begin(), c.srcs.end(), i) == c.srcs.end()) continue;
                 const Layer& cl = *g.find_layer(c.layer);
                 const Win w = win(cl);
-                const bool cm = bf16_mma_ok(cl);
+                const bool cm = tc_mma_ok(cl, es);
                 const int rh = cm ? rows_m : th, rw = cm ? cols_m : tw;
                 const int d = cl.kind == LayerKind::add ? 0 : XL - w.pad;
                 eh = std::max(eh, d + (rh - 1) * w.stride + w.kh);
@@ -175,7 +182,7 @@ long long layout_bf16(const Graph& g, const StepSpec& s, int th, int tw, BParams
         const TensorShape xs = g.shape_of(s.inputs[xi]);
         BIn& in = ins[xi];
         in = BIn{};
-        in.r.c8 = (s.ctile ? s.ctile : r8(xs.channels)) / 8;
+        in.r.chunks = (s.ctile ? s.ctile : rc(xs.channels, es)) / cpc;
         in.r.ext_h = eh, in.r.ext_w = ew;
         in.h = xs.height, in.w = xs.width;
         in.org_mul = scales[xi], in.org_sub = XL;
@@ -194,30 +201,31 @@ long long layout_bf16(const Graph& g, const StepSpec& s, int th, int tw, BParams
     // Epilogue-written plane buffers get a plane stride of 16 (mod 128) bytes:
     // SIMT readers fetch the 8 planes of one cell from 8 different bank groups.
     auto region = [&](BRegion& r, bool skew = false) {
-        const int kbs = r.kb_ch / 8;  // 8-channel groups per K-block
+        const int kbs = r.row_bytes / 16;  // chunks per K-block
         if (r.mode == kPlanes) r.plane_bytes = r128(r.ext_h * r.ext_w * r.row_bytes) + (skew ? 16 : 0);
         else r.plane_bytes = (r.ext_h * r.ext_w * r.row_bytes + 1023) & ~1023;
         bytes = (bytes + 1023) & ~1023LL;  // swizzle atoms / TMA destinations
         r.smem_off = int(bytes);
-        bytes += (long long)(r.c8 / kbs) * r.plane_bytes + kSlack;
+        bytes += (long long)(r.chunks / kbs) * r.plane_bytes + kSlack;
     };
-    // Block inputs arrive by TMA: 64-channel (128 B, SWIZZLE_128B) or
-    // 16-channel (32 B, SWIZZLE_32B) boxes when the channel count allows --
-    // few, wide requests -- else 8-channel planes.
+    // Block inputs arrive by TMA: 128-byte (SWIZZLE_128B) or 32-byte
+    // (SWIZZLE_32B) boxes per cell when the channel count allows -- few, wide
+    // requests -- else 16-byte planes.
     for (BIn& in : ins) {
-        const int C = in.r.c8 * 8;
-        if (C % 64 == 0) in.r.mode = kSw128, in.r.kb_ch = 64, in.r.row_bytes = 128;
-        else if (C % 16 == 0) in.r.mode = kSw32, in.r.kb_ch = 16, in.r.row_bytes = 32;
-        else in.r.mode = kPlanes, in.r.kb_ch = 8, in.r.row_bytes = 16;
+        const int bytes_per_cell = in.r.chunks * 16;
+        if (bytes_per_cell % 128 == 0) in.r.mode = kSw128, in.r.row_bytes = 128;
+        else if (bytes_per_cell % 32 == 0) in.r.mode = kSw32, in.r.row_bytes = 32;
+        else in.r.mode = kPlanes, in.r.row_bytes = 16;
+        in.r.kb_ch = in.r.row_bytes / es;
         region(in.r);
     }
     std::vector<BRegion> bufs(static_cast<size_t>(nbufs));
     for (int i = 0; i < nops; ++i) {
         if (bufidx[size_t(i)] < 0) continue;
         BRegion& b = bufs[size_t(bufidx[size_t(i)])];
-        b.c8 = r8(g.find_layer(s.ops[size_t(i)].layer)->out_shape->channels) / 8;
+        b.chunks = rc(g.find_layer(s.ops[size_t(i)].layer)->out_shape->channels, es) / cpc;
         b.ext_h = geo[size_t(i)].ext_h, b.ext_w = geo[size_t(i)].ext_w;
-        b.mode = kPlanes, b.kb_ch = 8, b.row_bytes = 16;  // written by the epilogue threads
+        b.mode = kPlanes, b.kb_ch = cpc, b.row_bytes = 16;  // written by the epilogue threads
         region(b, true);
     }
     bool any_mma = false;
@@ -239,19 +247,20 @@ long long layout_bf16(const Graph& g, const StepSpec& s, int th, int tw, BParams
         const Win w = win(l);
         o.kh = w.kh, o.kw = w.kw, o.stride = w.stride, o.pad = w.pad, o.group = 1;
         o.d = gi.d, o.ext_h = gi.ext_h, o.ext_w = gi.ext_w, o.org_mul = gi.mul, o.org_sub = gi.sub;
-        o.npad = r8(out.channels);
+        o.npad = rc(out.channels, es);
         if (l.kind == LayerKind::conv) {
             o.cin = l.conv->in_channels, o.group = l.conv->group, o.relu = l.conv->activation == Activation::relu;
-            o.cin_pad = r8(o.cin);
             if (gi.mma) {
                 o.kind = BOP_MMA;
                 o.contig = gi.contig;
-                bf16_nblocks(out.channels, &o.nblocks, &o.nb);
+                o.kpt = o.cin * es / 32;
+                tc_nblocks(out.channels, &o.nblocks, &o.nb);
                 o.npad = o.nblocks * o.nb;
                 if (o.contig) o.strips = 1, o.mtiles = cdiv(o.ext_h * o.ext_w, 128);
                 else o.strips = cdiv(o.ext_w, 8), o.mtiles = o.strips * cdiv(o.ext_h, 16);
-                o.ksteps = o.kh * o.kw * (o.cin / 16);
+                o.ksteps = o.kh * o.kw * o.kpt;
                 o.chunk_steps = std::max(1, chunk / (o.nb * 32));
+                if (!wres && chunk < o.nb * 32) return -1;  // a ring slot holds at least one K step
                 if (o.mtiles * o.nb > 512) return -1;  // TMEM: 512 columns
                 tmem = std::max(tmem, o.mtiles * o.nb);
                 any_mma = true;
@@ -283,7 +292,7 @@ long long layout_bf16(const Graph& g, const StepSpec& s, int th, int tw, BParams
         if (o.nblocks > 1) {
             // N blocks alternate between two column sets when both fit: block
             // k+1's MMAs run while the epilogue drains block k
-            const bool alt = 2 * cols <= 512 && !std::getenv("XLF_NO_NALT");
+            const bool alt = 2 * cols <= 512 && !k.no_nalt;
             for (int k = 0; k < o.nblocks; ++k) groups.push_back({i, i + 1, k, 1, alt ? (k & 1) * cols : 0, alt && k > 0 ? 2 : 1, -1});
             o.tcol = 0;
             tmem = std::max(tmem, alt ? 2 * cols : cols);
@@ -314,7 +323,7 @@ long long layout_bf16(const Graph& g, const StepSpec& s, int th, int tw, BParams
             if (single(G)) sum += ops[size_t(G.op1 - 1)].tcol + ops[size_t(G.op1 - 1)].mtiles * ops[size_t(G.op1 - 1)].nb;
         bool all_single = true;
         for (const BGroup& G : groups) all_single &= !G.mma || single(G);
-        if (all_single && sum <= pow2_cols(tmem) && !std::getenv("XLF_NO_TSEP")) {
+        if (all_single && sum <= pow2_cols(tmem) && !k.no_tsep) {
             int base = 0;
             for (BGroup& G : groups)
                 if (single(G)) G.tbase = base, base += ops[size_t(G.op1 - 1)].tcol + ops[size_t(G.op1 - 1)].mtiles * ops[size_t(G.op1 - 1)].nb;
@@ -339,7 +348,7 @@ long long layout_bf16(const Graph& g, const StepSpec& s, int th, int tw, BParams
             int l2, h2;
             span(groups[size_t(j)], l2, h2);
             if (l2 < hi && lo < h2) {
-                G.pwait = std::getenv("XLF_NO_PWAIT") ? int(groups.size()) - 1 : j;
+                G.pwait = k.no_pwait ? int(groups.size()) - 1 : j;
                 break;
             }
         }
@@ -377,7 +386,7 @@ long long layout_bf16(const Graph& g, const StepSpec& s, int th, int tw, BParams
     // the taps.  The allocation must cover the furthest read of every region
     // (into whatever follows it is harmless: those rows are masked).
     auto read_end = [&](const BOp& o, const BRegion& r) -> long long {
-        const long long nkb = r.c8 * 8 / r.kb_ch;
+        const long long nkb = r.chunks * 16 / r.row_bytes;
         long long last_cell;  // one past the last cell any M tile reads
         if (o.contig) last_cell = (long long)o.mtiles * 128;
         else last_cell = (long long)(o.mtiles / o.strips * 16 - 1 + o.kh - 1 + o.d) * r.ext_w + (o.strips * 8 - 1 + o.kw - 1 + o.d) + 1;
@@ -394,7 +403,7 @@ long long layout_bf16(const Graph& g, const StepSpec& s, int th, int tw, BParams
     bytes = (bytes + 127) & ~127LL;
     // second staging buffer of the block inputs (they sit first, from offset 0)
     long long in_end = 0;
-    for (const BIn& in : ins) in_end = std::max(in_end, (long long)in.r.smem_off + (long long)(in.r.c8 * 8 / in.r.kb_ch) * in.r.plane_bytes + kSlack);
+    for (const BIn& in : ins) in_end = std::max(in_end, (long long)in.r.smem_off + (long long)(in.r.chunks * 16 / in.r.row_bytes) * in.r.plane_bytes + kSlack);
     long long xstride = 0;
     if (nxb == 2) {
         xstride = (bytes + 1023) & ~1023LL;
@@ -418,33 +427,36 @@ long long layout_bf16(const Graph& g, const StepSpec& s, int th, int tw, BParams
         P->wres = any_mma && wres, P->wres_off = int(wres_off), P->wres_bytes = int(wres_bytes);
         P->smem_bytes = int(bytes);
         P->ctile = s.ctile;
-        P->cgroups = s.ctile ? r8(g.shape_of(s.inputs[0]).channels) / s.ctile : 1;
+        P->cgroups = s.ctile ? rc(g.shape_of(s.inputs[0]).channels, es) / s.ctile : 1;
         P->tmem_cols = pow2_cols(tmem);
         P->nxb = nxb, P->xstride = int(xstride);
         P->tsets = tsets;
         P->gap_off = int(gap_off);
+        P->es = es;
+        P->pdl = k.pdl ? 1 : 0;
+        P->xrel_epi = k.xrel_epi ? 1 : 0;
     }
     return bytes;
 }
 
-// Tile choice for the bf16 kernel: memory-bound blocks, so the model is the
-// bytes a CTA moves (input region incl. halo re-reads, outputs) plus a small
-// MMA term, over waves of CTAs resident per SM (shared memory and TMEM).
-static bool choose_tile_bf16_at(const Graph& g, StepSpec& s, int batch_hint, int smem_budget);
+// Tile choice for the tensor-core kernel: memory-bound blocks, so the model is
+// the bytes a CTA moves (input region incl. halo re-reads, outputs) plus a
+// small MMA term, over waves of CTAs resident per SM (shared memory and TMEM).
+static bool choose_tile_tc_at(const Graph& g, StepSpec& s, int batch_hint, int smem_budget, int es, const Knobs& k);
 
 // Pool-only steps too wide for shared memory (13x13x1000 global average pool)
 // are also tiled over channels (channel c in -> channel c out).
-bool choose_tile_bf16(const Graph& g, StepSpec& s, int batch_hint, int smem_budget) {
+bool choose_tile_tc(const Graph& g, StepSpec& s, int batch_hint, int smem_budget, int es, const Knobs& k) {
     s.ctile = 0;
-    if (choose_tile_bf16_at(g, s, batch_hint, smem_budget)) return true;
+    if (choose_tile_tc_at(g, s, batch_hint, smem_budget, es, k)) return true;
     bool pools = s.inputs.size() == 1;
     for (const OpSpec& op : s.ops) pools &= op.stage == 1 && g.find_layer(op.layer)->kind == LayerKind::pool;
     if (!pools) return false;
-    const int C = r8(g.shape_of(s.inputs[0]).channels);
-    for (int ct = C - 8; ct >= 8; ct -= 8) {
+    const int cpc = 16 / es, C = rc(g.shape_of(s.inputs[0]).channels, es);
+    for (int ct = C - cpc; ct >= cpc; ct -= cpc) {
         if (C % ct) continue;
         s.ctile = ct;
-        if (choose_tile_bf16_at(g, s, batch_hint, smem_budget)) return true;
+        if (choose_tile_tc_at(g, s, batch_hint, smem_budget, es, k)) return true;
     }
     s.ctile = 0;
     return false;
@@ -453,7 +465,7 @@ bool choose_tile_bf16(const Graph& g, StepSpec& s, int batch_hint, int smem_budg
 // Every feasible configuration of a step, scored by the model below (SM
 // cycles, lower is better), best first.
 //
-// Persistent CTAs (kernels_bf16.cu): each walks tiles; with two staging
+// Persistent CTAs (kernels_tc.cu): each walks tiles; with two staging
 // buffers (nxb = 2) the next tile's inputs load while this one computes.
 // Model: a tile costs load (its input region incl. halo at the per-SM HBM
 // share, ~24 B/cycle) + compute (MMA, SIMT, weights streamed through the ring
@@ -461,11 +473,8 @@ bool choose_tile_bf16(const Graph& g, StepSpec& s, int batch_hint, int smem_budg
 // latency); nxb = 2 hides the load behind the compute.  `occ` CTAs per SM
 // overlap; HBM bounds the total.  The model only ranks candidates: the engine
 // autotuner (Engine::autotune) measures the top ones on the device.
-std::vector<BCandidate> candidates_bf16(const Graph& g, const StepSpec& s, int batch_hint, int smem_budget) {
-    int force = 0;
-    if (const char* e = std::getenv("XLF_XBUF")) force = std::atoi(e);
-    int force_w = -1;
-    if (const char* e = std::getenv("XLF_WRES")) force_w = std::atoi(e);
+std::vector<BCandidate> candidates_tc(const Graph& g, const StepSpec& s, int batch_hint, int smem_budget, int es, const Knobs& k) {
+    const int force = k.xbuf, force_w = k.wres;
     struct WMode {
         int wres, slots, chunk;
     };
@@ -481,11 +490,11 @@ std::vector<BCandidate> candidates_bf16(const Graph& g, const StepSpec& s, int b
         for (const WMode& wm : wmodes) {
             for (int th = 1; th <= std::min(s.out_h, 32); ++th)
                 for (int tw = 1; tw <= std::min(s.out_w, 32); ++tw) {
-                    const long long sm = layout_bf16(g, s, th, tw, P, nxb, wm.wres, wm.slots, ts, wm.chunk);
+                    const long long sm = layout_tc(g, s, th, tw, P, nxb, wm.wres, wm.slots, ts, wm.chunk, es, k);
                     if (sm < 0 || sm > smem_budget) continue;
                     if (wm.wres && !P->wres) continue;  // no MMA op: the ring/resident choice is moot
                     double in_bytes = 0, mma = 0, simt = 0;
-                    for (int i = 0; i < P->nins; ++i) in_bytes += double(P->in[i].r.c8) * P->in[i].r.ext_h * P->in[i].r.ext_w * 16;
+                    for (int i = 0; i < P->nins; ++i) in_bytes += double(P->in[i].r.chunks) * P->in[i].r.ext_h * P->in[i].r.ext_w * 16;
                     for (int i = 0; i < P->nops; ++i) {
                         const BOp& o = P->ops[i];
                         if (o.kind == BOP_MMA) mma += double(o.mtiles) * 128 * o.nblocks * o.nb * o.ksteps * 16;
@@ -493,7 +502,7 @@ std::vector<BCandidate> candidates_bf16(const Graph& g, const StepSpec& s, int b
                     }
                     double out_bytes = 0;
                     for (int i = 0; i < P->nops; ++i)
-                        if (P->ops[i].emit) out_bytes += double(th) * tw * P->ops[i].npad * 2;
+                        if (P->ops[i].emit) out_bytes += double(th) * tw * P->ops[i].npad * es;
                     const double tiles = double(P->grid_h) * P->grid_w * P->cgroups * std::max(batch_hint, 1);
                     // 228 KB per SM; per CTA: dynamic + static (~4 KB) + 1 KB driver reserve
                     int occ = std::max(1, std::min(max_ctas_per_sm(ew), int((228 * 1024) / (sm + 5120))));
@@ -513,7 +522,7 @@ std::vector<BCandidate> candidates_bf16(const Graph& g, const StepSpec& s, int b
                 }
         }
     delete P;
-    // testing aids (XLF_XBUF / XLF_WRES / XLF_TSETS): keep only the matching
+    // testing aids (options xbuf / wres / tsets): keep only the matching
     // configurations when any exists for this step
     auto prefer = [&](auto pred) {
         std::vector<BCandidate> keep;
@@ -523,10 +532,7 @@ std::vector<BCandidate> candidates_bf16(const Graph& g, const StepSpec& s, int b
     };
     if (force) prefer([&](const BCandidate& c) { return c.nxb == force; });
     if (force_w >= 0) prefer([&](const BCandidate& c) { return c.wres == force_w; });
-    if (const char* e = std::getenv("XLF_TSETS")) {
-        const int want = std::atoi(e);
-        prefer([&](const BCandidate& c) { return c.tsets == want; });
-    }
+    if (k.tsets) prefer([&](const BCandidate& c) { return c.tsets == k.tsets; });
     std::stable_sort(out.begin(), out.end(), [](const BCandidate& a, const BCandidate& b) {
         if (a.model < b.model * 0.999) return true;
         if (b.model < a.model * 0.999) return false;
@@ -535,8 +541,8 @@ std::vector<BCandidate> candidates_bf16(const Graph& g, const StepSpec& s, int b
     return out;
 }
 
-static bool choose_tile_bf16_at(const Graph& g, StepSpec& s, int batch_hint, int smem_budget) {
-    const std::vector<BCandidate> c = candidates_bf16(g, s, batch_hint, smem_budget);
+static bool choose_tile_tc_at(const Graph& g, StepSpec& s, int batch_hint, int smem_budget, int es, const Knobs& k) {
+    const std::vector<BCandidate> c = candidates_tc(g, s, batch_hint, smem_budget, es, k);
     if (c.empty()) return false;
     apply_candidate(s, c.front());
     return true;
@@ -547,36 +553,46 @@ void apply_candidate(StepSpec& s, const BCandidate& c) {
     s.epi_warps = c.epi_warps, s.tsets = c.tsets, s.ring_chunk = c.chunk;
 }
 
-// bf16 weights of every MMA-eligible conv: [nblock][tap][cin/8][nb][8].
-std::vector<uint16_t> pack_weights_bf16(const Graph& g, const float* flat, size_t count, std::map<std::string, long long>& off) {
-    std::vector<uint16_t> out;
+// Weights of every MMA-eligible conv as the UMMA K-major B operand of each
+// 32-byte K step: [nblock][tap][cin/cpc][nb][cpc] elements, bf16 (RN even) or
+// fp32 rounded to TF32 (RN, ties away -- the rounding the TF32 epilogue
+// applies to activations).  `off`: byte offset per layer.
+std::vector<uint8_t> pack_weights_tc(const Graph& g, const float* flat, size_t count, std::map<std::string, long long>& off, int es) {
+    std::vector<uint8_t> out;
     size_t pos = 0;
-    auto bf = [](float f) {
+    const int cpc = 16 / es;
+    auto put = [&](size_t byte, float f) {
         uint32_t u;
         std::memcpy(&u, &f, 4);
-        u += 0x7FFF + ((u >> 16) & 1);  // round to nearest even
-        return uint16_t(u >> 16);
+        if (es == 2) {
+            u += 0x7FFF + ((u >> 16) & 1);  // round to nearest even
+            const uint16_t h = uint16_t(u >> 16);
+            std::memcpy(&out[byte], &h, 2);
+        } else {
+            if ((u & 0x7F800000u) != 0x7F800000u) u = (u + 0x1000u) & ~0x1FFFu;  // TF32: 10 mantissa bits, ties away
+            std::memcpy(&out[byte], &u, 4);
+        }
     };
     for (const Layer& l : g.layers) {
         if (l.kind != LayerKind::conv) continue;
         const ConvParams& c = *l.conv;
         const size_t nf = size_t(c.weight_count()), nb_ = size_t(c.bias_count());
         if (pos + nf + nb_ > count) fail(ErrorKind::validation, "weights: stream too short for layer '" + l.name + "'");
-        if (bf16_mma_ok(l)) {
+        if (tc_mma_ok(l, es)) {
             int nblocks, nb;
-            bf16_nblocks(c.out_channels, &nblocks, &nb);
-            const int c16 = c.in_channels / 16, taps = c.kernel_h * c.kernel_w, ksteps = taps * c16;
+            tc_nblocks(c.out_channels, &nblocks, &nb);
+            const int kpt = c.in_channels * es / 32, taps = c.kernel_h * c.kernel_w, ksteps = taps * kpt;
             const size_t base = out.size();
             off[l.name] = (long long)base;
-            out.resize(base + size_t(nblocks) * ksteps * nb * 16, 0);
+            out.resize(base + size_t(nblocks) * ksteps * nb * 32, 0);
             for (int oc = 0; oc < c.out_channels; ++oc)
                 for (int ic = 0; ic < c.in_channels; ++ic)
                     for (int y = 0; y < c.kernel_h; ++y)
                         for (int x = 0; x < c.kernel_w; ++x) {
                             const int nbi = oc / nb, n = oc - nbi * nb, tap = y * c.kernel_w + x;
-                            const int step = tap * c16 + ic / 16, half = (ic % 16) / 8;
-                            const size_t dst = ((size_t(nbi) * ksteps + step) * 2 + half) * nb * 8 + size_t(n) * 8 + ic % 8;
-                            out[base + dst] = bf(flat[pos + ((size_t(oc) * c.in_channels + ic) * c.kernel_h + y) * c.kernel_w + x]);
+                            const int step = tap * kpt + ic / (2 * cpc), half = (ic % (2 * cpc)) / cpc;
+                            const size_t el = ((size_t(nbi) * ksteps + step) * 2 + half) * nb * cpc + size_t(n) * cpc + ic % cpc;
+                            put(base + el * es, flat[pos + ((size_t(oc) * c.in_channels + ic) * c.kernel_h + y) * c.kernel_w + x]);
                         }
         }
         pos += nf + nb_;

@@ -10,7 +10,7 @@
 #include <sstream>
 #include <tuple>
 
-#include "bf16_params.hpp"
+#include "tc_params.hpp"
 #include "common.hpp"
 #include "fused_params.hpp"
 
@@ -26,30 +26,30 @@ cudaError_t launch_nchw_to_nhwc(const float* src, float* dst, int N, int C, int 
 cudaError_t launch_nhwc_to_nchw(const float* src, int cs, int coff, float* dst, int N, int C, int H, int W, cudaStream_t st);
 cudaError_t launch_seeded_nhwc(float* dst, unsigned long long seed, unsigned long long first_image, int N, int C, int H, int W,
                                int cs, cudaStream_t st);
-// kernels_bf16.cu
-cudaError_t init_fused_bf16();
-cudaError_t launch_fused_bf16(const BParams& P, int batch, cudaStream_t st, int n0 = 0);
-cudaError_t launch_gap_finish_bf16(const float* part, int tiles, int np, float scale, __nv_bfloat16* out, int cs, int coff, int C, int n0,
-                                   int N, cudaStream_t st);
-int occupancy_fused_bf16(int smem_bytes, int tmem_cols, int epi_warps, int kind);
-int step_kind_bf16(const BParams& P);
-cudaError_t launch_nchw_to_nhwc_bf16(const float* src, __nv_bfloat16* dst, int N, int C, int H, int W, int cs, cudaStream_t st);
-cudaError_t launch_nhwc_bf16_to_nchw(const __nv_bfloat16* src, int cs, int coff, float* dst, int N, int C, int H, int W,
-                                     cudaStream_t st);
-cudaError_t launch_seeded_nhwc_bf16(__nv_bfloat16* dst, unsigned long long seed, unsigned long long first_image, int N, int C, int H,
-                                    int W, int cs, cudaStream_t st);
-cudaError_t launch_concat_copy_bf16(const __nv_bfloat16* src, int scs, int sco, __nv_bfloat16* dst, int dcs, int dco, int C,
-                                    long long pixels, cudaStream_t st);
-cudaError_t launch_s2d_bf16(const float* src, unsigned long long seed, unsigned long long first_image, __nv_bfloat16* dst, int N,
-                            int C, int H, int W, int cs, cudaStream_t st);
-cudaError_t launch_eltwise_bf16(int op, const __nv_bfloat16* a, int acs, int aco, const __nv_bfloat16* b, int bcs, int bco,
-                                __nv_bfloat16* o, int ocs, int oco, int C, long long pixels, cudaStream_t st);
+// kernels_tc.cu (es = element bytes: 2 bf16, 4 fp32/TF32)
+cudaError_t init_fused_tc();
+cudaError_t launch_fused_tc(const BParams& P, int batch, cudaStream_t st, int n0);
+int occupancy_fused_tc(int smem_bytes, int tmem_cols, int epi_warps, int kind, int es);
+int step_kind_tc(const BParams& P);
+cudaError_t launch_gap_finish_tc(int es, const float* part, int tiles, int np, float scale, void* out, int cs, int coff, int C, int n0, int N,
+                                 cudaStream_t st);
+cudaError_t launch_nchw_to_nhwc_tc(int es, const float* src, void* dst, int N, int C, int H, int W, int cs, cudaStream_t st);
+cudaError_t launch_nhwc_tc_to_nchw(int es, const void* src, int cs, int coff, float* dst, int N, int C, int H, int W, cudaStream_t st);
+cudaError_t launch_seeded_nhwc_tc(int es, void* dst, unsigned long long seed, unsigned long long first_image, int N, int C, int H, int W,
+                                  int cs, cudaStream_t st);
+cudaError_t launch_s2d_tc(int es, const float* src, unsigned long long seed, unsigned long long first_image, void* dst, int N, int C, int H,
+                          int W, int cs, cudaStream_t st);
+cudaError_t launch_concat_copy_tc(int es, const void* src, int scs, int sco, void* dst, int dcs, int dco, int C, long long pixels,
+                                  cudaStream_t st);
+cudaError_t launch_eltwise_tc(int es, int op, const void* a, int acs, int aco, const void* b, int bcs, int bco, void* o, int ocs, int oco, int C,
+                              long long pixels, cudaStream_t st);
 
 const char* to_string(Precision p) {
     switch (p) {
     case Precision::fp32_exact: return "fp32_exact";
     case Precision::fp32: return "fp32";
     case Precision::bf16: return "bf16";
+    case Precision::tf32: return "tf32";
     }
     return "?";
 }
@@ -94,24 +94,24 @@ PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
     return fn;
 }
 
-// 4-D map over an NHWC bf16 tensor {cstride, W, H, N}; box = one K-block
-// (kb_ch channels: 8 unswizzled, 16 with SWIZZLE_32B, 64 with SWIZZLE_128B)
-// of an ext_h x ext_w region, zero fill outside the image.
-void encode_region_map(CUtensorMap* map, const void* base, int cstride, int W, int H, int N, const BRegion& r) {
+// 4-D map over an NHWC tensor {cstride, W, H, N} of `es`-byte elements; box =
+// one K-block (16 bytes per cell unswizzled, 32 with SWIZZLE_32B, 128 with
+// SWIZZLE_128B) of an ext_h x ext_w region, zero fill outside the image.
+void encode_region_map(CUtensorMap* map, const void* base, int cstride, int W, int H, int N, const BRegion& r, int es) {
     const cuuint64_t dims[4] = {cuuint64_t(cstride), cuuint64_t(W), cuuint64_t(H), cuuint64_t(N)};
-    const cuuint64_t strides[3] = {cuuint64_t(cstride) * 2, cuuint64_t(W) * cstride * 2, cuuint64_t(H) * W * cstride * 2};
+    const cuuint64_t strides[3] = {cuuint64_t(cstride) * es, cuuint64_t(W) * cstride * es, cuuint64_t(H) * W * cstride * es};
     const cuuint32_t box[4] = {cuuint32_t(r.kb_ch), cuuint32_t(r.ext_w), cuuint32_t(r.ext_h), 1};
     const cuuint32_t estr[4] = {1, 1, 1, 1};
     const CUtensorMapSwizzle sw = r.mode == kSw128 ? CU_TENSOR_MAP_SWIZZLE_128B
                                   : r.mode == kSw32 ? CU_TENSOR_MAP_SWIZZLE_32B
                                                     : CU_TENSOR_MAP_SWIZZLE_NONE;
-    const CUresult res = tensor_map_encoder()(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(base), dims, strides, box,
+    const CUresult res = tensor_map_encoder()(map, es == 4 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(base), dims, strides, box,
                                               estr, CU_TENSOR_MAP_INTERLEAVE_NONE, sw, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
                                               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (res != CUDA_SUCCESS) fail(ErrorKind::cuda, "cuTensorMapEncodeTiled failed (" + std::to_string(int(res)) + ")");
 }
 
-// bf16 only: a stride-2, pad-0 conv reading the graph input (SqueezeNet conv1:
+// Tensor-core plans: a stride-2, pad-0 conv reading the graph input (SqueezeNet conv1:
 // 3x3/2 on 3 channels) cannot use the stride-1 implicit GEMM.  Rewrite it as a
 // stride-1 ceil(k/2) x ceil(k/2) conv over the space-to-depth input
 // (4 phases x C channels, padded to 16): out(y,x) = sum over phase (py,px),
@@ -158,33 +158,41 @@ bool rewrite_s2d(Graph& g, std::vector<float>& w) {
 
 }  // namespace
 
-Engine::Engine(const Graph& g, int device, Partition part, Precision prec, const float* weights, size_t nweights, int max_batch)
-    : g_(g), device_(device), prec_(prec), max_batch_(max_batch) {
+Engine::Engine(const Graph& g, int device, Partition part, Precision prec, const float* weights, size_t nweights, int max_batch,
+               const Knobs& knobs)
+    : g_(g), device_(device), prec_(prec), max_batch_(max_batch), knobs_(knobs) {
     if (!g_.shapes_inferred()) fail(ErrorKind::internal, "engine: graph shapes not inferred");
     if (max_batch < 1) fail(ErrorKind::validation, "engine: max_batch must be >= 1");
-    if (g_.inputs.size() != 1) fail(ErrorKind::validation, "engine: graphs with exactly one input are supported");
-    const bool bf = prec == Precision::bf16;
-    esz_ = bf ? 2 : 4;
+    if (g_.inputs.empty()) fail(ErrorKind::validation, "engine: the graph has no input");
+    tc_es_ = prec == Precision::bf16 ? 2 : prec == Precision::tf32 ? 4 : 0;
+    const bool tc = tc_es_ != 0;
+    esz_ = tc_es_ == 2 ? 2 : 4;
+    for (const GraphInput& in : g_.inputs) user_inputs_[in.name] = in.shape;
     in_shape_ = g_.inputs[0].shape;
+    const Graph user = g_;
     std::vector<float> wcopy;
-    if (bf) {
+    if (tc) {
         wcopy.assign(weights, weights + nweights);
         s2d_ = rewrite_s2d(g_, wcopy);
         if (s2d_) weights = wcopy.data(), nweights = wcopy.size();
     }
     cuda_check(cudaSetDevice(device), "cudaSetDevice");
-    plan_ = plan_device(g_, part, max_batch, 227 * 1024, bf);
-    cuda_check(bf ? init_fused_bf16() : init_fused_fp32(), "kernel attributes");
+    plan_ = plan_device(g_, part, max_batch, 227 * 1024, tc_es_, knobs_);
+    // statistics against the user's graph (the s2d rewrite pads conv1's input
+    // to 16 channels; the algorithmic bytes / MACs are the real layer's)
+    if (s2d_)
+        for (StepSpec& s : plan_.steps) fill_stats(user, plan_, s);
+    cuda_check(tc ? init_fused_tc() : init_fused_fp32(), "kernel attributes");
     // fp32 packed weights (+ slack: bf16 epilogues read bias up to the N-block padding)
     std::vector<float> packed = pack_weights(g_, plan_, weights, nweights);
     packed.resize(packed.size() + 1024, 0.0f);
     cuda_check(cudaMalloc(&weights_, packed.size() * 4), "cudaMalloc(weights)");
     cuda_check(cudaMemcpy(weights_, packed.data(), packed.size() * 4, cudaMemcpyHostToDevice), "weights H2D");
-    if (bf) {
-        std::vector<uint16_t> w16 = pack_weights_bf16(g_, weights, nweights, woff16_);
-        w16.resize(w16.size() + 64, 0);
-        cuda_check(cudaMalloc(&weights16_, w16.size() * 2), "cudaMalloc(bf16 weights)");
-        cuda_check(cudaMemcpy(weights16_, w16.data(), w16.size() * 2, cudaMemcpyHostToDevice), "bf16 weights H2D");
+    if (tc) {
+        std::vector<uint8_t> wt = pack_weights_tc(g_, weights, nweights, wofftc_, tc_es_);
+        wt.resize(wt.size() + 128, 0);
+        cuda_check(cudaMalloc(&weights_tc_, wt.size()), "cudaMalloc(tensor-core weights)");
+        cuda_check(cudaMemcpy(weights_tc_, wt.data(), wt.size(), cudaMemcpyHostToDevice), "tensor-core weights H2D");
     }
     for (long long f : plan_.alloc_floats) {
         void* p = nullptr;
@@ -203,7 +211,7 @@ Engine::Engine(const Graph& g, int device, Partition part, Precision prec, const
     for (size_t i = 0; i < plan_.steps.size(); ++i) {
         const StepSpec& s = plan_.steps[i];
         if (s.kind != StepSpec::FUSED) continue;
-        if (!bf) {
+        if (!tc) {
             params_[i] = make_params(g_, plan_, s, allocs_, weights_);
             continue;
         }
@@ -211,18 +219,19 @@ Engine::Engine(const Graph& g, int device, Partition part, Precision prec, const
     }
 }
 
-// Launch descriptor of a bf16 step in its current configuration (tile,
+// Launch descriptor of a tensor-core step in its current configuration (tile,
 // staging, weight residency), bound to this engine's tensors and weights,
 // with its device copy.
 std::unique_ptr<BParams> Engine::build_bparams(const StepSpec& s) {
     auto P = std::make_unique<BParams>();
-    if (layout_bf16(g_, s, s.tile_h, s.tile_w, P.get(), s.nxb, s.wres, s.ring_slots, s.tsets, s.ring_chunk) < 0)
-        fail(ErrorKind::internal, "step " + s.id + ": bf16 layout failed");
+    if (layout_tc(g_, s, s.tile_h, s.tile_w, P.get(), s.nxb, s.wres, s.ring_slots, s.tsets, s.ring_chunk, tc_es_, knobs_) < 0)
+        fail(ErrorKind::internal, "step " + s.id + ": tensor-core layout failed");
     P->epi_warps = s.epi_warps;
-    P->kind = step_kind_bf16(*P);
-    P->ctas_per_sm = occupancy_fused_bf16(P->smem_bytes, P->tmem_cols * P->tsets, P->epi_warps, P->kind);
+    P->kind = step_kind_tc(*P);
+    P->ctas_per_sm = occupancy_fused_tc(P->smem_bytes, P->tmem_cols * P->tsets, P->epi_warps, P->kind, tc_es_);
+    if (knobs_.ctas > 0) P->ctas_per_sm = std::min(P->ctas_per_sm, knobs_.ctas);
     P->grid_all = s.grid_all;
-    if (std::getenv("XLF_TRACE"))
+    if (knobs_.trace)
         std::fprintf(stderr, "[xlf] step %s: tile %dx%d, %d B shared, %d staging buffer(s), weights %s, %d CTA(s)/SM%s\n",
                      s.id.c_str(), s.tile_h, s.tile_w, P->smem_bytes, P->nxb,
                      P->wres ? "resident" : (std::to_string(P->ring_slots) + "-slot ring").c_str(), P->ctas_per_sm,
@@ -230,9 +239,9 @@ std::unique_ptr<BParams> Engine::build_bparams(const StepSpec& s) {
     for (int k = 0; k < P->nins; ++k) {
         const TensorSlot& t = plan_.tensors.at(s.inputs[size_t(k)]);
         BIn& in = P->in[k];
-        in.x = reinterpret_cast<const __nv_bfloat16*>(allocs_[size_t(t.alloc)]);
+        in.x = allocs_[size_t(t.alloc)];
         in.cstride = t.cstride, in.coff = t.coff;
-        encode_region_map(&P->xmap[k], in.x, t.cstride, t.W, t.H, max_batch_, in.r);
+        encode_region_map(&P->xmap[k], in.x, t.cstride, t.W, t.H, max_batch_, in.r, tc_es_);
     }
     for (int k = 0; k < P->nops; ++k) {
         const OpSpec& os = s.ops[size_t(k)];
@@ -240,11 +249,11 @@ std::unique_ptr<BParams> Engine::build_bparams(const StepSpec& s) {
         if (o.kind == BOP_MMA || o.kind == BOP_SIMT_CONV) {
             o.wsimt = weights_ + plan_.w_off.at(os.layer);
             o.bias = weights_ + plan_.b_off.at(os.layer);
-            if (o.kind == BOP_MMA) o.wmma = reinterpret_cast<const __nv_bfloat16*>(weights16_) + woff16_.at(os.layer);
+            if (o.kind == BOP_MMA) o.wmma = static_cast<const uint8_t*>(weights_tc_) + wofftc_.at(os.layer);
         }
         if (o.emit) {
             const TensorSlot& t = plan_.tensors.at(s.gap_out.empty() ? os.layer : s.gap_out);
-            o.out = reinterpret_cast<__nv_bfloat16*>(allocs_[size_t(t.alloc)]);
+            o.out = allocs_[size_t(t.alloc)];
             o.out_cstride = t.cstride, o.out_coff = t.coff;
         }
     }
@@ -261,14 +270,13 @@ std::unique_ptr<BParams> Engine::build_bparams(const StepSpec& s) {
         }
         P->gap_part = buf.first;
     }
-    if (const char* d = std::getenv("XLF_DBG")) P->dbg = std::atoi(d);
-    if (std::getenv("XLF_TRACE")) {  // phase stamps of a few CTAs (profiling aid)
+    if (knobs_.trace) {  // phase stamps of a few CTAs (profiling aid)
         unsigned long long* tr = nullptr;
         const size_t n = size_t(kTraceCtas) * kTraceEvents;
         cuda_check(cudaMalloc(&tr, n * 8), "cudaMalloc(trace)");
         cuda_check(cudaMemset(tr, 0, n * 8), "cudaMemset(trace)");
         P->trace = tr;
-        P->trace_tiles = std::atoi(std::getenv("XLF_TRACE")) == 2;
+        P->trace_tiles = knobs_.trace == 2;
         traces_.push_back(tr);
     }
     void* dev = nullptr;
@@ -286,12 +294,15 @@ std::unique_ptr<BParams> Engine::build_bparams(const StepSpec& s) {
 // the fastest is kept.  Arithmetic does not depend on the configuration, so
 // results stay within the bf16 tolerance whatever is chosen.
 std::string Engine::autotune(int batch, int reps, int topk) {
-    if (prec_ != Precision::bf16) return "[]";
+    if (!tc_es_) return "[]";
     if (batch <= 0 || batch > max_batch_) batch = max_batch_;
     reps = std::max(1, reps), topk = std::max(1, topk);
     cuda_check(cudaSetDevice(device_), "cudaSetDevice");
     cudaStream_t st;
     cuda_check(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking), "cudaStreamCreate(tune)");
+    // captured forwards hold the current descriptors, which are replaced below
+    for (auto& [b, ge] : graphs_) cudaGraphExecDestroy(ge);
+    graphs_.clear();
     cudaEvent_t e0, e1;
     cuda_check(cudaEventCreate(&e0), "cudaEventCreate"), cuda_check(cudaEventCreate(&e1), "cudaEventCreate");
     std::ostringstream js;
@@ -302,7 +313,7 @@ std::string Engine::autotune(int batch, int reps, int topk) {
         if (s.kind != StepSpec::FUSED || !bparams_[i]) continue;
         // the model ranks tiles within one staging / weight mode reasonably
         // but not across modes: keep the best `topk` of every mode
-        std::vector<BCandidate> all = candidates_bf16(g_, s, batch, kSmemBudgetBf16), cands;
+        std::vector<BCandidate> all = candidates_tc(g_, s, batch, kSmemBudgetTc, tc_es_, knobs_), cands;
         std::map<std::tuple<int, int, int, int>, int> per_mode;
         std::map<std::tuple<int, int, int, int>, const BCandidate*> biggest;  // largest tile of each mode
         for (const BCandidate& c : all) {
@@ -334,16 +345,16 @@ std::string Engine::autotune(int batch, int reps, int topk) {
                     cudaFree(const_cast<void*>(P->dev_copy));
                     continue;  // persistent grid already covers every tile
                 }
-                cuda_check(launch_fused_bf16(*P, batch, st), "autotune warm-up");
+                cuda_check(launch_fused_tc(*P, batch, st, 0), "autotune warm-up");
                 cuda_check(cudaEventRecord(e0, st), "cudaEventRecord");
-                for (int r = 0; r < reps; ++r) cuda_check(launch_fused_bf16(*P, batch, st), "autotune launch");
+                for (int r = 0; r < reps; ++r) cuda_check(launch_fused_tc(*P, batch, st, 0), "autotune launch");
                 cuda_check(cudaEventRecord(e1, st), "cudaEventRecord");
                 cuda_check(cudaEventSynchronize(e1), "cudaEventSynchronize");
                 float ms = 0;
                 cuda_check(cudaEventElapsedTime(&ms, e0, e1), "cudaEventElapsedTime");
                 ms /= float(reps);
                 ++tried;
-                if (std::getenv("XLF_TUNE_VERBOSE"))
+                if (knobs_.tune_verbose)
                     std::fprintf(stderr, "[xlf] tune %s: tile %dx%d nxb %d wres %d slots %d grid_all %d ew %d ts %d smem %d: %.1f us (model %.0f)\n",
                                  s.id.c_str(), t.tile_h, t.tile_w, t.nxb, t.wres, t.ring_slots, t.grid_all, t.epi_warps, t.tsets, P->smem_bytes,
                                  ms * 1000.0f, c.model);
@@ -369,19 +380,18 @@ std::string Engine::autotune(int batch, int reps, int topk) {
     js << "]";
     cudaEventDestroy(e0), cudaEventDestroy(e1);
     cudaStreamDestroy(st);
-    // captured forwards hold the old descriptors
-    for (auto& [b, ge] : graphs_) cudaGraphExecDestroy(ge);
-    graphs_.clear();
     return js.str();
 }
 
 // Re-applies a tuning report (the JSON autotune returns) without measuring:
 // the tuned plan as a reusable artifact (tune once per model / batch / GPU,
-// then load).  Every entry must name a bf16 fused step of this plan and give a
-// feasible configuration; the report's format is the one autotune writes
-// (flat objects, numeric fields, "id" string, "tile" [h, w]).
+// then load).  Every entry must name a tensor-core fused step of this plan and
+// give a feasible configuration; the report's format is the one autotune
+// writes (flat objects, numeric fields, "id" string, "tile" [h, w]).  All
+// entries are parsed and validated before anything changes: a bad report
+// leaves the engine as it was.
 void Engine::apply_tuning(const std::string& js) {
-    if (prec_ != Precision::bf16) return;
+    if (!tc_es_) return;
     // value position of "key" (after the colon; whitespace tolerated), or npos
     auto at = [](const std::string& obj, const std::string& key) -> size_t {
         const size_t k = obj.find("\"" + key + "\"");
@@ -395,8 +405,8 @@ void Engine::apply_tuning(const std::string& js) {
         out = std::atoi(obj.c_str() + v);
         return true;
     };
+    std::vector<std::pair<size_t, StepSpec>> todo;
     size_t pos = 0;
-    int applied = 0;
     while ((pos = js.find('{', pos)) != std::string::npos) {
         const size_t end = js.find('}', pos);
         if (end == std::string::npos) fail(ErrorKind::parse, "tuning report: unterminated object");
@@ -409,7 +419,7 @@ void Engine::apply_tuning(const std::string& js) {
         const std::string id = obj.substr(is + 1, ie - is - 1);
         size_t i = 0;
         while (i < plan_.steps.size() && plan_.steps[i].id != id) ++i;
-        if (i == plan_.steps.size() || !bparams_[i]) fail(ErrorKind::validation, "tuning report: no bf16 fused step '" + id + "'");
+        if (i == plan_.steps.size() || !bparams_[i]) fail(ErrorKind::validation, "tuning report: no tensor-core fused step '" + id + "'");
         StepSpec t = plan_.steps[i];
         const size_t tv = at(obj, "tile");
         const size_t tb = tv == std::string::npos ? tv : obj.find('[', tv);
@@ -419,20 +429,27 @@ void Engine::apply_tuning(const std::string& js) {
         t.tile_w = std::atoi(obj.c_str() + tc + 1);
         num(obj, "nxb", t.nxb), num(obj, "wres", t.wres), num(obj, "ring_slots", t.ring_slots), num(obj, "ring_chunk", t.ring_chunk);
         num(obj, "grid_all", t.grid_all), num(obj, "epi_warps", t.epi_warps), num(obj, "tsets", t.tsets);
+        // layout_tc rejects staging / accumulator-set / ring values the kernel
+        // cannot run (nxb, tsets in {1, 2}; 1 <= ring_slots <= kRingMax; a
+        // ring slot holding at least one K step)
         BParams probe;
-        const long long sm = layout_bf16(g_, t, t.tile_h, t.tile_w, &probe, t.nxb, t.wres, t.ring_slots, t.tsets, t.ring_chunk);
-        if (sm < 0 || sm > kSmemBudgetBf16 || (t.epi_warps != 4 && t.epi_warps != 8) || t.tile_h < 1 || t.tile_w < 1)
+        const long long sm = layout_tc(g_, t, t.tile_h, t.tile_w, &probe, t.nxb, t.wres, t.ring_slots, t.tsets, t.ring_chunk, tc_es_, knobs_);
+        if (sm < 0 || sm > kSmemBudgetTc || (t.epi_warps != 4 && t.epi_warps != 8) || (t.grid_all != 0 && t.grid_all != 1))
             fail(ErrorKind::infeasible, "tuning report: configuration of step '" + id + "' is not feasible for this plan");
         t.smem_bytes = int(sm);
-        std::unique_ptr<BParams> P = build_bparams(t);
-        cudaFree(const_cast<void*>(bparams_[i]->dev_copy));
-        plan_.steps[i] = t;
-        bparams_[i] = std::move(P);
-        ++applied;
+        todo.emplace_back(i, t);
     }
+    // captured forwards hold the current descriptors
     for (auto& [b, ge] : graphs_) cudaGraphExecDestroy(ge);
     graphs_.clear();
-    (void)applied;
+    std::vector<std::unique_ptr<BParams>> built;
+    for (auto& [i, t] : todo) built.push_back(build_bparams(t));
+    for (size_t k = 0; k < todo.size(); ++k) {
+        const size_t i = todo[k].first;
+        retired_.push_back(const_cast<void*>(bparams_[i]->dev_copy));  // freed with the engine (never while a launch may read it)
+        plan_.steps[i] = todo[k].second;
+        bparams_[i] = std::move(built[k]);
+    }
 }
 
 Engine::~Engine() {
@@ -440,7 +457,7 @@ Engine::~Engine() {
     for (auto& [b, ge] : graphs_) cudaGraphExecDestroy(ge);
     for (float* p : allocs_) cudaFree(p);
     cudaFree(weights_);
-    if (weights16_) cudaFree(weights16_);
+    if (weights_tc_) cudaFree(weights_tc_);
     for (unsigned long long* p : traces_) cudaFree(p);
     for (auto& P : bparams_)
         if (P) cudaFree(const_cast<void*>(P->dev_copy));
@@ -462,71 +479,80 @@ const TensorSlot& Engine::slot(const std::string& n) const {
     return it->second;
 }
 
+// A tensor the user may read back: materialised and in the user's layout (a
+// graph input rewritten to space-to-depth holds 4C channels at half the
+// resolution and is not the tensor the user passed in).
+const TensorSlot& Engine::readable(const std::string& n) const {
+    const TensorSlot& t = slot(n);
+    if (s2d_ && n == g_.inputs[0].name)
+        fail(ErrorKind::validation, "tensor '" + n + "' is held in the space-to-depth layout of the tensor-core plan; it cannot be read back");
+    return t;
+}
+
 void Engine::set_input_nchw(const std::string& name, const float* d, int batch, cudaStream_t st) {
     if (batch < 1 || batch > max_batch_) fail(ErrorKind::validation, "batch out of range");
+    if (!user_inputs_.count(name)) fail(ErrorKind::validation, "'" + name + "' is not a graph input");
     const TensorSlot& t = slot(name);
-    if (s2d_)
-        cuda_check(launch_s2d_bf16(d, 0, 0, reinterpret_cast<__nv_bfloat16*>(allocs_[size_t(t.alloc)]), batch, in_shape_.channels,
-                                   in_shape_.height, in_shape_.width, t.cstride, st),
+    void* dst = allocs_[size_t(t.alloc)];
+    if (s2d_ && name == g_.inputs[0].name)
+        cuda_check(launch_s2d_tc(tc_es_, d, 0, 0, dst, batch, in_shape_.channels, in_shape_.height, in_shape_.width, t.cstride, st),
                    "space-to-depth input");
-    else if (esz_ == 2)
-        cuda_check(launch_nchw_to_nhwc_bf16(d, reinterpret_cast<__nv_bfloat16*>(allocs_[size_t(t.alloc)]), batch, t.C, t.H, t.W,
-                                            t.cstride, st),
-                   "nchw_to_nhwc");
+    else if (tc_es_)
+        cuda_check(launch_nchw_to_nhwc_tc(tc_es_, d, dst, batch, t.C, t.H, t.W, t.cstride, st), "nchw_to_nhwc");
     else
         cuda_check(launch_nchw_to_nhwc(d, allocs_[size_t(t.alloc)], batch, t.C, t.H, t.W, t.cstride, st), "nchw_to_nhwc");
 }
 
 void Engine::set_input_seeded(const std::string& name, uint64_t seed, uint64_t first_image, int batch, cudaStream_t st) {
     if (batch < 1 || batch > max_batch_) fail(ErrorKind::validation, "batch out of range");
+    if (!user_inputs_.count(name)) fail(ErrorKind::validation, "'" + name + "' is not a graph input");
     const TensorSlot& t = slot(name);
-    if (s2d_)
-        cuda_check(launch_s2d_bf16(nullptr, seed, first_image, reinterpret_cast<__nv_bfloat16*>(allocs_[size_t(t.alloc)]), batch,
-                                   in_shape_.channels, in_shape_.height, in_shape_.width, t.cstride, st),
+    void* dst = allocs_[size_t(t.alloc)];
+    if (s2d_ && name == g_.inputs[0].name)
+        cuda_check(launch_s2d_tc(tc_es_, nullptr, seed, first_image, dst, batch, in_shape_.channels, in_shape_.height, in_shape_.width,
+                                 t.cstride, st),
                    "seeded space-to-depth input");
-    else if (esz_ == 2)
-        cuda_check(launch_seeded_nhwc_bf16(reinterpret_cast<__nv_bfloat16*>(allocs_[size_t(t.alloc)]), seed, first_image, batch, t.C,
-                                           t.H, t.W, t.cstride, st),
-                   "seeded fill");
+    else if (tc_es_)
+        cuda_check(launch_seeded_nhwc_tc(tc_es_, dst, seed, first_image, batch, t.C, t.H, t.W, t.cstride, st), "seeded fill");
     else
         cuda_check(launch_seeded_nhwc(allocs_[size_t(t.alloc)], seed, first_image, batch, t.C, t.H, t.W, t.cstride, st), "seeded fill");
 }
 
-// A bf16 fused step over images [n0, n0 + count): the kernel, plus the
+// A tensor-core fused step over images [n0, n0 + count): the kernel, plus the
 // reduction that finishes a conv + global-average-pool step.
-void Engine::launch_bf16_step(size_t i, int n0, int count, cudaStream_t st) {
+void Engine::launch_tc_step(size_t i, int n0, int count, cudaStream_t st) {
     const BParams& P = *bparams_[i];
-    cuda_check(launch_fused_bf16(P, count, st, n0), "fused block (bf16)");
+    cuda_check(launch_fused_tc(P, count, st, n0), "fused block (tensor cores)");
     const StepSpec& s = plan_.steps[i];
     if (s.gap_out.empty()) return;
     const TensorSlot& t = slot(s.gap_out);
     const Layer& pool = *g_.find_layer(s.gap_out);
     const float scale = 1.0f / float(pool.pool->kernel * pool.pool->kernel);
-    cuda_check(launch_gap_finish_bf16(P.gap_part, P.grid_h * P.grid_w, P.ops[0].npad, scale,
-                                      reinterpret_cast<__nv_bfloat16*>(allocs_[size_t(t.alloc)]), t.cstride, t.coff, t.C, n0, count, st),
+    cuda_check(launch_gap_finish_tc(tc_es_, P.gap_part, P.grid_h * P.grid_w, P.ops[0].npad, scale, allocs_[size_t(t.alloc)], t.cstride, t.coff,
+                                    t.C, n0, count, st),
                "global average pool finish");
 }
 
 bool Engine::range_capable() const {
-    if (esz_ != 2) return false;
+    if (!tc_es_ || g_.inputs.size() != 1) return false;
     for (size_t i = 0; i < plan_.steps.size(); ++i)
         if (plan_.steps[i].kind != StepSpec::FUSED || !bparams_[i]) return false;
     return true;
 }
 
-// Images [n0, n0 + count) only (bf16 plans made of fused kernels: the kernels
-// take the image offset; see run_host).
+// Images [n0, n0 + count) only (tensor-core plans made of fused kernels: the
+// kernels take the image offset; see run_host).
 void Engine::forward_range(int n0, int count, cudaStream_t st) {
     if (n0 < 0 || count < 1 || n0 + count > max_batch_) fail(ErrorKind::validation, "image range out of bounds");
-    if (!range_capable()) fail(ErrorKind::validation, "forward_range needs a bf16 plan of fused kernels only");
+    if (!range_capable()) fail(ErrorKind::validation, "forward_range needs a tensor-core plan of fused kernels only");
     const long long key = -(1LL + (long long)n0 * 65536 + count);  // negative keys: ranges (positive: whole batches)
-    auto it = graphs_.find(int(key));
+    auto it = graphs_.find(key);
     if (it == graphs_.end()) {
         if (!capture_) cuda_check(cudaStreamCreateWithFlags(&capture_, cudaStreamNonBlocking), "capture stream");
         cudaGraph_t graph;
         cuda_check(cudaStreamBeginCapture(capture_, cudaStreamCaptureModeThreadLocal), "begin capture");
         try {
-            for (size_t i = 0; i < plan_.steps.size(); ++i) launch_bf16_step(i, n0, count, capture_);
+            for (size_t i = 0; i < plan_.steps.size(); ++i) launch_tc_step(i, n0, count, capture_);
         } catch (...) {
             cudaStreamEndCapture(capture_, &graph);
             throw;
@@ -535,18 +561,17 @@ void Engine::forward_range(int n0, int count, cudaStream_t st) {
         cudaGraphExec_t exec;
         cuda_check(cudaGraphInstantiate(&exec, graph, 0), "graph instantiate");
         cudaGraphDestroy(graph);
-        it = graphs_.emplace(int(key), exec).first;
+        it = graphs_.emplace(key, exec).first;
     }
     cuda_check(cudaGraphLaunch(it->second, st), "graph launch");
 }
 
 void Engine::launch_step(size_t i, int batch, cudaStream_t st) {
     const StepSpec& s = plan_.steps[i];
-    const bool bf = esz_ == 2;
-    auto b16 = [&](const TensorSlot& t) { return reinterpret_cast<__nv_bfloat16*>(allocs_[size_t(t.alloc)]); };
+    auto ptr = [&](const TensorSlot& t) { return static_cast<void*>(allocs_[size_t(t.alloc)]); };
     switch (s.kind) {
     case StepSpec::FUSED:
-        if (bf) launch_bf16_step(i, 0, batch, st);
+        if (tc_es_) launch_tc_step(i, 0, batch, st);
         else cuda_check(launch_fused_fp32(params_[i], batch, prec_ == Precision::fp32_exact, st), "fused block");
         return;
     case StepSpec::CONCAT_COPY: {
@@ -555,8 +580,8 @@ void Engine::launch_step(size_t i, int batch, cudaStream_t st) {
         for (const std::string& in : s.inputs) {
             const TensorSlot& t = slot(in);
             const long long px = (long long)batch * t.H * t.W;
-            if (bf)
-                cuda_check(launch_concat_copy_bf16(b16(t), t.cstride, t.coff, b16(o), o.cstride, o.coff + off, t.C, px, st), "concat");
+            if (tc_es_)
+                cuda_check(launch_concat_copy_tc(tc_es_, ptr(t), t.cstride, t.coff, ptr(o), o.cstride, o.coff + off, t.C, px, st), "concat");
             else
                 cuda_check(launch_concat_copy(allocs_[size_t(t.alloc)], t.cstride, t.coff, allocs_[size_t(o.alloc)], o.cstride,
                                               o.coff + off, t.C, px, st),
@@ -572,9 +597,9 @@ void Engine::launch_step(size_t i, int batch, cudaStream_t st) {
         const TensorSlot& b = s.kind == StepSpec::ADD ? slot(s.inputs[1]) : a;
         const int op = s.kind == StepSpec::ADD ? 0 : 1;
         const long long px = (long long)batch * o.H * o.W;
-        if (bf)
-            cuda_check(launch_eltwise_bf16(op, b16(a), a.cstride, a.coff, b16(b), b.cstride, b.coff, b16(o), o.cstride, o.coff, o.C, px,
-                                           st),
+        if (tc_es_)
+            cuda_check(launch_eltwise_tc(tc_es_, op, ptr(a), a.cstride, a.coff, ptr(b), b.cstride, b.coff, ptr(o), o.cstride, o.coff, o.C, px,
+                                         st),
                        "eltwise");
         else
             cuda_check(launch_eltwise(op, allocs_[size_t(a.alloc)], a.cstride, a.coff, allocs_[size_t(b.alloc)], b.cstride, b.coff,
@@ -622,32 +647,35 @@ void Engine::forward(int batch, cudaStream_t st, bool use_graph) {
 }
 
 void Engine::read_output_nchw(const std::string& name, float* d, int batch, cudaStream_t st) {
-    const TensorSlot& t = slot(name);
-    if (esz_ == 2)
-        cuda_check(launch_nhwc_bf16_to_nchw(reinterpret_cast<const __nv_bfloat16*>(allocs_[size_t(t.alloc)]), t.cstride, t.coff, d,
-                                            batch, t.C, t.H, t.W, st),
-                   "nhwc_to_nchw");
+    if (batch < 1 || batch > max_batch_) fail(ErrorKind::validation, "batch out of range");
+    const TensorSlot& t = readable(name);
+    if (tc_es_)
+        cuda_check(launch_nhwc_tc_to_nchw(tc_es_, allocs_[size_t(t.alloc)], t.cstride, t.coff, d, batch, t.C, t.H, t.W, st), "nhwc_to_nchw");
     else
         cuda_check(launch_nhwc_to_nchw(allocs_[size_t(t.alloc)], t.cstride, t.coff, d, batch, t.C, t.H, t.W, st), "nhwc_to_nchw");
 }
 
-// End to end from host memory.  bf16 plans made only of fused kernels are
-// pipelined over chunks of images: the H2D copy of chunk c+1 (copy stream)
-// overlaps the layout conversion + forward of chunk c (caller's stream), and
-// each chunk's result is read back as soon as it is ready (second copy
-// stream), so the PCIe transfer -- the e2e bound for 224x224x3 fp32 inputs --
-// hides the compute.  Other plans: H2D, forward, D2H in sequence.
+size_t Engine::tensor_elements(const std::string& name) const {
+    const TensorSlot& t = readable(name);
+    return size_t(t.C) * t.H * t.W;
+}
+
+// End to end from host memory.  Tensor-core plans made only of fused kernels
+// are pipelined over chunks of images: the H2D copy of chunk c+1 (copy
+// stream) overlaps the layout conversion + forward of chunk c (caller's
+// stream), and each chunk's result is read back as soon as it is ready
+// (second copy stream), so the PCIe transfer -- the e2e bound for 224x224x3
+// fp32 inputs -- hides the compute.  Other plans: H2D, forward, D2H in sequence.
 void Engine::run_host(const float* h_in, int batch, const std::string& out_name, float* h_out, cudaStream_t st) {
     if (batch < 1 || batch > max_batch_) fail(ErrorKind::validation, "batch out of range");
+    if (g_.inputs.size() != 1) fail(ErrorKind::validation, "run_host: graphs with exactly one input (use set_input per input)");
     cuda_check(cudaSetDevice(device_), "cudaSetDevice");
     const GraphInput& in = g_.inputs[0];
     const size_t img_in = size_t(in_shape_.elements());  // user-facing NCHW input, per image
-    const TensorSlot& t = slot(out_name);
+    const TensorSlot& t = readable(out_name);
     const size_t img_out = size_t(t.C) * t.H * t.W;
     if (img_out * batch > staging_floats_) fail(ErrorKind::validation, "output larger than the staging buffer");
-    int chunks = 4;
-    if (const char* c = std::getenv("XLF_E2E_CHUNKS")) chunks = std::max(1, std::atoi(c));
-    chunks = std::min(chunks, batch);
+    int chunks = std::min(knobs_.e2e_chunks, batch);
     if (!range_capable() || chunks == 1) {
         cuda_check(cudaMemcpyAsync(staging_, h_in, img_in * batch * 4, cudaMemcpyHostToDevice, st), "H2D input");
         set_input_nchw(in.name, staging_, batch, st);
@@ -664,11 +692,11 @@ void Engine::run_host(const float* h_in, int batch, const std::string& out_name,
         cuda_check(cudaMalloc(&out_staging_, staging_floats_ * 4), "cudaMalloc(output staging)");
     }
     chunks = std::min(chunks, int(kMaxChunks) - 1);
-    // Chunk boundaries: equal chunks (measured best); XLF_E2E_RAMP=1 makes the
+    // Chunk boundaries: equal chunks (measured best); option e2e_ramp makes the
     // first and last half size (the first H2D and the last forward are the
     // only stages nothing overlaps): chunks + 1 pieces of 1/2, 1, ..., 1, 1/2.
     std::vector<int> cut{0};
-    const bool ramp = std::getenv("XLF_E2E_RAMP") && chunks >= 2 && chunks + 1 <= batch;
+    const bool ramp = knobs_.e2e_ramp && chunks >= 2 && chunks + 1 <= batch;
     const int pieces = ramp ? chunks + 1 : chunks;
     for (int c = 1; c < pieces; ++c) {
         const double w = ramp ? (c - 0.5) / chunks : double(c) / chunks;  // cumulative share
@@ -676,6 +704,7 @@ void Engine::run_host(const float* h_in, int batch, const std::string& out_name,
     }
     cut.push_back(batch);
     const TensorSlot& xin = slot(in.name);
+    const size_t es = size_t(esz_);
     for (int c = 0; c < pieces; ++c) {
         const int n0 = cut[size_t(c)], n1 = cut[size_t(c) + 1], cnt = n1 - n0;
         float* dst = staging_ + size_t(n0) * img_in;
@@ -683,19 +712,15 @@ void Engine::run_host(const float* h_in, int batch, const std::string& out_name,
                    "H2D input chunk");
         cuda_check(cudaEventRecord(chunk_ev_[c], copy_in_), "event");
         cuda_check(cudaStreamWaitEvent(st, chunk_ev_[c], 0), "wait H2D");
-        __nv_bfloat16* x = reinterpret_cast<__nv_bfloat16*>(allocs_[size_t(xin.alloc)]);
+        uint8_t* x = reinterpret_cast<uint8_t*>(allocs_[size_t(xin.alloc)]) + size_t(n0) * xin.H * xin.W * xin.cstride * es;
         if (s2d_)
-            cuda_check(launch_s2d_bf16(dst, 0, 0, x + size_t(n0) * xin.H * xin.W * xin.cstride, cnt, in_shape_.channels, in_shape_.height,
-                                       in_shape_.width, xin.cstride, st),
+            cuda_check(launch_s2d_tc(tc_es_, dst, 0, 0, x, cnt, in_shape_.channels, in_shape_.height, in_shape_.width, xin.cstride, st),
                        "space-to-depth input chunk");
         else
-            cuda_check(launch_nchw_to_nhwc_bf16(dst, x + size_t(n0) * xin.H * xin.W * xin.cstride, cnt, xin.C, xin.H, xin.W,
-                                                xin.cstride, st),
-                       "nchw_to_nhwc chunk");
+            cuda_check(launch_nchw_to_nhwc_tc(tc_es_, dst, x, cnt, xin.C, xin.H, xin.W, xin.cstride, st), "nchw_to_nhwc chunk");
         forward_range(n0, cnt, st);
-        const __nv_bfloat16* o = reinterpret_cast<const __nv_bfloat16*>(allocs_[size_t(t.alloc)]);
-        cuda_check(launch_nhwc_bf16_to_nchw(o + size_t(n0) * t.H * t.W * t.cstride, t.cstride, t.coff, out_staging_ + size_t(n0) * img_out,
-                                            cnt, t.C, t.H, t.W, st),
+        const uint8_t* o = reinterpret_cast<const uint8_t*>(allocs_[size_t(t.alloc)]) + size_t(n0) * t.H * t.W * t.cstride * es;
+        cuda_check(launch_nhwc_tc_to_nchw(tc_es_, o, t.cstride, t.coff, out_staging_ + size_t(n0) * img_out, cnt, t.C, t.H, t.W, st),
                    "nhwc_to_nchw chunk");
         cuda_check(cudaEventRecord(chunk_ev_[kMaxChunks + c], st), "event");
         cuda_check(cudaStreamWaitEvent(copy_out_, chunk_ev_[kMaxChunks + c], 0), "wait chunk");
@@ -727,7 +752,7 @@ namespace xlf {
 std::vector<unsigned long long> Engine::trace(int index) const {
     if (index < 0 || index >= num_steps()) fail(ErrorKind::validation, "step index out of range");
     const BParams* P = bparams_[size_t(index)].get();
-    if (!P || !P->trace) fail(ErrorKind::validation, "no trace for this step (bf16 steps with XLF_TRACE=1 only)");
+    if (!P || !P->trace) fail(ErrorKind::validation, "no trace for this step (tensor-core steps of an engine created with option trace=1 only)");
     std::vector<unsigned long long> out(size_t(kTraceCtas) * kTraceEvents);
     cuda_check(cudaMemcpy(out.data(), P->trace, out.size() * 8, cudaMemcpyDeviceToHost), "trace D2H");
     return out;

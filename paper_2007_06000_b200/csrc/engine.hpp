@@ -18,12 +18,13 @@
 
 namespace xlf {
 
-enum class Precision { fp32_exact = 0, fp32 = 1, bf16 = 2 };
+enum class Precision { fp32_exact = 0, fp32 = 1, bf16 = 2, tf32 = 3 };
 const char* to_string(Precision p);
 
 class Engine {
 public:
-    Engine(const Graph& g, int device, Partition part, Precision prec, const float* weights, size_t nweights, int max_batch);
+    Engine(const Graph& g, int device, Partition part, Precision prec, const float* weights, size_t nweights, int max_batch,
+           const Knobs& knobs = Knobs{});
     ~Engine();
     Engine(const Engine&) = delete;
     Engine& operator=(const Engine&) = delete;
@@ -34,13 +35,15 @@ public:
     void set_input_seeded(const std::string& name, uint64_t seed, uint64_t first_image, int batch, cudaStream_t st);
     // All steps for `batch` images (replays a captured CUDA graph when use_graph).
     void forward(int batch, cudaStream_t st, bool use_graph = true);
-    // Images [n0, n0 + count) of every step (bf16 plans of fused kernels only).
+    // Images [n0, n0 + count) of every step (tensor-core plans of fused kernels only).
     void forward_range(int n0, int count, cudaStream_t st);
     bool range_capable() const;
     // One step only (per-block timing / run_fused_block).
     void run_step(int index, int batch, cudaStream_t st);
     // NHWC arena -> NCHW fp32.
     void read_output_nchw(const std::string& name, float* d_nchw, int batch, cudaStream_t st);
+    // C*H*W of a readable tensor (throws for fused intermediates / rewritten inputs).
+    size_t tensor_elements(const std::string& name) const;
     // End to end with host buffers: H2D, forward, D2H of `out_name`, sync.
     void run_host(const float* h_in_nchw, int batch, const std::string& out_name, float* h_out_nchw, cudaStream_t st);
 
@@ -48,41 +51,47 @@ public:
     const DevicePlan& plan() const { return plan_; }
     int num_steps() const { return int(plan_.steps.size()); }
     int launches_per_forward() const;
-    // XLF_TRACE=1 only: per-CTA phase stamps of step `index` (bf16 kernels).
+    // option trace=1 only: per-CTA phase stamps of step `index` (tensor-core kernels).
     std::vector<unsigned long long> trace(int index) const;
     std::string describe_json() const;
-    // Measured-time tuning of the bf16 fused steps (see engine.cpp); returns
+    // Measured-time tuning of the tensor-core fused steps (see engine.cpp); returns
     // the chosen configurations as JSON.
     std::string autotune(int batch, int reps, int topk);
     // Applies a report autotune returned (no measurement).
     void apply_tuning(const std::string& json);
     int max_batch() const { return max_batch_; }
+    int device() const { return device_; }
+    Precision precision() const { return prec_; }
 
 private:
     void launch_step(size_t i, int batch, cudaStream_t st);
     std::unique_ptr<struct BParams> build_bparams(const StepSpec& s);
-    void launch_bf16_step(size_t i, int n0, int count, cudaStream_t st);
+    void launch_tc_step(size_t i, int n0, int count, cudaStream_t st);
     const TensorSlot& slot(const std::string& n) const;
+    const TensorSlot& readable(const std::string& n) const;
 
     Graph g_;
     DevicePlan plan_;
     int device_;
     Precision prec_;
     int max_batch_;
+    Knobs knobs_;
     std::vector<float*> allocs_;
     float* weights_ = nullptr;
     float* staging_ = nullptr;  // NCHW input staging for run_host
     cudaStream_t capture_ = nullptr;  // private stream used only to capture CUDA graphs
     size_t staging_floats_ = 0;
     std::vector<struct FusedParams> params_;
-    std::vector<std::unique_ptr<struct BParams>> bparams_;  // bf16 steps
-    std::vector<unsigned long long*> traces_;                // XLF_TRACE buffers
-    std::map<std::string, long long> woff16_;                // bf16 packed-weight offsets per layer
-    void* weights16_ = nullptr;  // bf16 MMA weights
-    int esz_ = 4;                // bytes per activation element
-    bool s2d_ = false;           // bf16: first conv rewritten on a space-to-depth input
-    TensorShape in_shape_;       // user-facing (NCHW) input shape
-    std::map<int, cudaGraphExec_t> graphs_;  // key > 0: whole batch; < 0: image range (forward_range)
+    std::vector<std::unique_ptr<struct BParams>> bparams_;  // tensor-core steps
+    std::vector<unsigned long long*> traces_;                // trace buffers (option trace)
+    std::map<std::string, long long> wofftc_;                // packed MMA weights: byte offset per layer
+    void* weights_tc_ = nullptr;  // packed MMA weights (bf16 / TF32)
+    int tc_es_ = 0;               // tensor-core element bytes (2 bf16, 4 TF32), 0 = fp32 SIMT kernels
+    int esz_ = 4;                 // bytes per activation element in HBM
+    bool s2d_ = false;            // tensor cores: first conv rewritten on a space-to-depth input
+    TensorShape in_shape_;        // user-facing (NCHW) shape of input 0
+    std::map<std::string, TensorShape> user_inputs_;  // graph inputs as the user passes them
+    std::map<long long, cudaGraphExec_t> graphs_;  // key > 0: whole batch; < 0: image range (forward_range)
     static constexpr int kMaxChunks = 16;     // run_host pipelining
     cudaStream_t copy_in_ = nullptr, copy_out_ = nullptr;
     cudaEvent_t chunk_ev_[2 * kMaxChunks] = {};

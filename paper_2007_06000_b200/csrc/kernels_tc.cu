@@ -1,4 +1,9 @@
-// bf16 tensor-core fused-block kernel for sm_100a (tcgen05 + TMEM + TMA).
+// Tensor-core fused-block kernel for sm_100a (tcgen05 + TMEM + TMA), for two
+// element types (template parameter T): bf16 (tcgen05.mma kind::f16) and
+// fp32 storage carrying TF32 values (kind::tf32).  All shared-memory layouts
+// and UMMA descriptors are in 16-byte chunks / 32-byte K steps, identical for
+// both types; T changes the MMA kind, the chunk's channel count (8 / 4) and
+// the epilogue's conversion (bf16 RN / TF32 RNA).
 //
 // Persistent: grid = 148 x (resident CTAs per SM), capped by the tile count;
 // CTA b walks tiles b, b + gridDim.x, ... (tile = image x channel group x
@@ -10,11 +15,11 @@
 //   warp 10     weight producer: cp.async.bulk of the packed weights through a
 //               3-slot ring (full/empty mbarriers), running ahead across tiles;
 //   warp 9      MMA issuer: one thread issues tcgen05.mma (M=128, N<=256,
-//               K=16, bf16 x bf16 -> fp32 in TMEM) for every conv "unit"
+//               one 32-byte K step, bf16 or TF32 -> fp32 in TMEM) for every conv "unit"
 //               (op x N block), commits to the ring and to the unit's
 //               accumulator barrier; the warp owns TMEM alloc/dealloc (once);
 //   warps 0-7   epilogue + SIMT ops: tcgen05.ld the accumulator (lane = GEMM
-//               row = output cell), bias + ReLU + halo mask, bf16, and either
+//               row = output cell), bias + ReLU + halo mask, bf16 / TF32, and either
 //               keep it on chip (shared "planes" buffer that the next stage's
 //               MMAs read with shifted descriptors) or store NHWC to HBM at
 //               the concat channel offset.  Pools / stride-2 convs / adds run
@@ -23,7 +28,7 @@
 // unit's epilogue signalled (its TMEM columns are free and any buffer it
 // reads is written); every per-tile barrier flips phase once per tile.
 // Barrier init, TMEM allocation, the descriptor and bias copies happen once
-// per CTA, not per tile.  See bf16_params.hpp for the shared-memory layout.
+// per CTA, not per tile.  See tc_params.hpp for the shared-memory layout.
 #include <cuda.h>
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
@@ -33,7 +38,7 @@
 #include <cstdio>
 #include <cstdlib>
 
-#include "bf16_params.hpp"
+#include "tc_params.hpp"
 #include "umma.cuh"
 
 namespace xlf {
@@ -41,6 +46,64 @@ namespace xlf {
 namespace {
 
 using namespace umma;
+
+// Element traits: channels per 16-byte chunk, conversions, the MMA kind.
+template <class T>
+struct Elem;
+
+template <>
+struct Elem<__nv_bfloat16> {
+    static constexpr int cpc = 8;
+    static constexpr uint32_t idesc(int M, int N) { return idesc_bf16(M, N); }
+    __device__ static void mma(uint32_t t, uint64_t a, uint64_t b, uint32_t id, uint32_t acc) { mma_bf16(t, a, b, id, acc); }
+    __device__ static float rnd(float x) { return x; }  // rounding happens in pack()
+    __device__ static __nv_bfloat16 from(float x) { return __float2bfloat16(x); }
+    __device__ static float to(__nv_bfloat16 x) { return __bfloat162float(x); }
+    // v[0..7] -> one chunk
+    __device__ static uint4 pack(const float* v) {
+        uint4 u;
+        __nv_bfloat162 h;
+        h = __floats2bfloat162_rn(v[0], v[1]), u.x = *reinterpret_cast<uint32_t*>(&h);
+        h = __floats2bfloat162_rn(v[2], v[3]), u.y = *reinterpret_cast<uint32_t*>(&h);
+        h = __floats2bfloat162_rn(v[4], v[5]), u.z = *reinterpret_cast<uint32_t*>(&h);
+        h = __floats2bfloat162_rn(v[6], v[7]), u.w = *reinterpret_cast<uint32_t*>(&h);
+        return u;
+    }
+    __device__ static void unpack(uint4 u, float* f) {
+        const uint32_t w[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const float2 p = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&w[q]));
+            f[2 * q] = p.x, f[2 * q + 1] = p.y;
+        }
+    }
+    __device__ static uint32_t max2(uint32_t a, uint32_t b) {
+        __nv_bfloat162 x = *reinterpret_cast<__nv_bfloat162*>(&a), y = *reinterpret_cast<__nv_bfloat162*>(&b);
+        __nv_bfloat162 m = __hmax2(x, y);
+        return *reinterpret_cast<uint32_t*>(&m);
+    }
+    __device__ static uint4 vmax(uint4 a, uint4 b) { return make_uint4(max2(a.x, b.x), max2(a.y, b.y), max2(a.z, b.z), max2(a.w, b.w)); }
+};
+
+template <>
+struct Elem<float> {
+    static constexpr int cpc = 4;
+    static constexpr uint32_t idesc(int M, int N) { return idesc_tf32(M, N); }
+    __device__ static void mma(uint32_t t, uint64_t a, uint64_t b, uint32_t id, uint32_t acc) { mma_tf32(t, a, b, id, acc); }
+    __device__ static float rnd(float x) { return round_tf32(x); }
+    __device__ static float from(float x) { return round_tf32(x); }
+    __device__ static float to(float x) { return x; }
+    // v[0..3] -> one chunk (TF32-rounded)
+    __device__ static uint4 pack(const float* v) {
+        return make_uint4(__float_as_uint(round_tf32(v[0])), __float_as_uint(round_tf32(v[1])), __float_as_uint(round_tf32(v[2])),
+                          __float_as_uint(round_tf32(v[3])));
+    }
+    __device__ static void unpack(uint4 u, float* f) {
+        f[0] = __uint_as_float(u.x), f[1] = __uint_as_float(u.y), f[2] = __uint_as_float(u.z), f[3] = __uint_as_float(u.w);
+    }
+    __device__ static uint32_t max1(uint32_t a, uint32_t b) { return __float_as_uint(fmaxf(__uint_as_float(a), __uint_as_float(b))); }
+    __device__ static uint4 vmax(uint4 a, uint4 b) { return make_uint4(max1(a.x, b.x), max1(a.y, b.y), max1(a.z, b.z), max1(a.w, b.w)); }
+};
 
 // CTA shape, a template parameter of the kernel (the tuner picks per step):
 // EW epilogue/SIMT warps (4 or 8), then the input producer, MMA issuer and
@@ -167,7 +230,7 @@ struct TileWalk {
 // this tile (expand MMAs, epilogues).  -1: the epilogue warps release it after
 // the tile (SIMT ops read the staged input).
 __device__ __forceinline__ int x_release_group(const BParams& P) {
-    if (P.dbg & 16) return -1;
+    if (P.xrel_epi) return -1;
     int last = -1;
     for (int gi = 0; gi < P.ngroups; ++gi) {
         const BGroup& G = P.groups[gi];
@@ -186,7 +249,7 @@ __device__ __forceinline__ int x_release_group(const BParams& P) {
 __device__ void x_producer(const BParams& P, const CUtensorMap* xmaps, uint8_t* smem, int total, int n0, uint64_t* bar_x,
                            uint64_t* x_free) {
     uint32_t bytes = 0;
-    for (int k = 0; k < P.nins; ++k) bytes += uint32_t(P.in[k].r.c8) * uint32_t(P.in[k].r.ext_h * P.in[k].r.ext_w * 16);
+    for (int k = 0; k < P.nins; ++k) bytes += uint32_t(P.in[k].r.chunks) * uint32_t(P.in[k].r.ext_h * P.in[k].r.ext_w * 16);
     const int nxb = P.nxb;
     int k = 0;
     grid_dependency_wait();  // the previous step's outputs are this step's inputs
@@ -202,7 +265,7 @@ __device__ void x_producer(const BParams& P, const CUtensorMap* xmaps, uint8_t* 
         for (int i = 0; i < P.nins; ++i) {
             const BIn& in = P.in[i];
             const int x0 = t.ox0 * in.org_mul - in.org_sub, y0 = t.oy0 * in.org_mul - in.org_sub;
-            const int nkb = in.r.c8 * 8 / in.r.kb_ch;
+            const int nkb = in.r.chunks * 16 / in.r.row_bytes;
             for (int kb = 0; kb < nkb; ++kb)
                 tma_load_4d(xb + in.r.smem_off + kb * in.r.plane_bytes, &xmaps[i], in.coff + t.c0 + kb * in.r.kb_ch, x0, y0, t.n,
                             &bar_x[b]);
@@ -224,7 +287,7 @@ __device__ void w_producer(const BParams& P, uint8_t* smem, int total, uint64_t*
             if (op.kind != BOP_MMA) continue;
             const uint32_t b = uint32_t(op.nblocks * op.ksteps * op.nb * 32);
             for (uint32_t o = 0; o < b; o += 65536)  // pieces of <= 64 KB
-                bulk_g2s(smem + P.wres_off + op.wofs + o, reinterpret_cast<const uint8_t*>(op.wmma) + o, min(65536u, b - o), bar_w);
+                bulk_g2s(smem + P.wres_off + op.wofs + o, op.wmma + o, min(65536u, b - o), bar_w);
         }
         return;
     }
@@ -236,14 +299,14 @@ __device__ void w_producer(const BParams& P, uint8_t* smem, int total, uint64_t*
             if (!G.mma) continue;
             for (int i = G.op0; i < G.op1; ++i) {
                 const BOp& op = P.ops[i];
-                const __nv_bfloat16* wb = op.wmma + size_t(G.nbi) * op.ksteps * op.nb * 16;
+                const uint8_t* wb = op.wmma + size_t(G.nbi) * op.ksteps * op.nb * 32;
                 for (int s0 = 0; s0 < op.ksteps; s0 += op.chunk_steps, ++c) {
                     const int steps = min(op.chunk_steps, op.ksteps - s0);
                     const int slot = c % slots;
                     if (c >= slots) mbar_sleep_wait(&ring_empty[slot], ((c / slots) - 1) & 1);
                     const uint32_t b = uint32_t(steps) * op.nb * 32;
                     mbar_expect_tx(&ring_full[slot], b);
-                    bulk_g2s(smem + P.ring_off + slot * P.chunk_bytes, wb + size_t(s0) * op.nb * 16, b, &ring_full[slot]);
+                    bulk_g2s(smem + P.ring_off + slot * P.chunk_bytes, wb + size_t(s0) * op.nb * 32, b, &ring_full[slot]);
                 }
             }
         }
@@ -257,13 +320,14 @@ __device__ void w_producer(const BParams& P, uint8_t* smem, int total, uint64_t*
 // field is hoisted into locals first and the descriptors are advanced by
 // precomputed deltas (in 16-byte units of the start-address field), so one MMA
 // costs a handful of uniform-datapath instructions.
+template <class T>
 __device__ __forceinline__ void issue_op(const BParams& P, const BOp& op, int nbi, uint32_t sbase, uint32_t tmem, int& c,
                                          uint64_t* ring_full, uint64_t* ring_empty, int xdelta) {
     const BRegion R = src_region_at(P, op, op.src, xdelta);
     const int mode = R.mode, plane = R.plane_bytes, rowb = R.row_bytes, ew = R.ext_w;
     const int ksteps = op.ksteps, csteps = op.chunk_steps, nb = op.nb, mtiles = op.mtiles, strips = op.strips;
-    const int kw = op.kw, d = op.d, contig = op.contig, c16 = op.cin_pad / 16;
-    const uint32_t idesc = idesc_bf16(128, nb);
+    const int kw = op.kw, d = op.d, contig = op.contig, c16 = op.kpt;
+    const uint32_t idesc = Elem<T>::idesc(128, nb);
     uint32_t lbo, layout;
     if (mode == kPlanes) lbo = plane, layout = kNoSwizzle;
     else lbo = 16, layout = mode == kSw32 ? kSW32 : kSW128;
@@ -292,7 +356,7 @@ __device__ __forceinline__ void issue_op(const BParams& P, const BOp& op, int nb
             bd = bdesc0 + ((ring0 + slot * chunkb) >> 4);
         }
         for (int sl = 0; sl < steps; ++sl) {
-            uint32_t kofs;  // K16 step kc inside the region's K-blocks, 16-byte units
+            uint32_t kofs;  // 32-byte K step kc inside the region's K-blocks, 16-byte units
             if (mode == kPlanes) kofs = (kc * 2 * plane) >> 4;
             else if (mode == kSw32) kofs = (kc * plane) >> 4;
             else kofs = (((kc >> 2) * plane) >> 4) + (kc & 3) * 2;
@@ -300,7 +364,7 @@ __device__ __forceinline__ void issue_op(const BParams& P, const BOp& op, int nb
             uint32_t tcur = tm0;
             int st = 0;
             for (int mt = 0; mt < mtiles; ++mt) {
-                if (!(P.dbg & 4)) mma_bf16(tcur, a, bd, idesc, acc);
+                Elem<T>::mma(tcur, a, bd, idesc, acc);
                 tcur += nb;
                 if (contig || ++st < strips) a += d_mt;
                 else st = 0, a += d_rb;
@@ -317,6 +381,7 @@ __device__ __forceinline__ void issue_op(const BParams& P, const BOp& op, int nb
     }
 }
 
+template <class T>
 __device__ void issuer(const BParams& P, uint8_t* smem, uint32_t tmem, int total, uint64_t* bar_x, uint64_t* x_free, uint64_t* ring_full,
                        uint64_t* ring_empty, uint64_t* acc_full, uint64_t* unit_done, uint64_t* acc_free, uint64_t* bar_w) {
     int c = 0, k = 0;
@@ -358,7 +423,7 @@ __device__ void issuer(const BParams& P, uint8_t* smem, uint32_t tmem, int total
             // later ops are still on the tensor cores
             uint64_t* fb = acc_full + (s * kBMaxUnits + gi) * kSubs;
             for (int i = Gr.op0; i < Gr.op1; ++i) {
-                issue_op(P, P.ops[i], Gr.nbi, sbase, tmem + uint32_t(s * P.tmem_cols + Gr.tbase), c, ring_full, ring_empty, xdelta);
+                issue_op<T>(P, P.ops[i], Gr.nbi, sbase, tmem + uint32_t(s * P.tmem_cols + Gr.tbase), c, ring_full, ring_empty, xdelta);
                 const int sub = i - Gr.op0;
                 if (sub < kSubs - 1 || i == Gr.op1 - 1) commit(&fb[sub < kSubs - 1 ? sub : kSubs - 1]);
             }
@@ -374,20 +439,23 @@ __device__ void issuer(const BParams& P, uint8_t* smem, uint32_t tmem, int total
 // descriptor.  Epilogues store to shared memory, so the compiler cannot cache
 // descriptor fields read from shared memory across those stores; hoisting
 // them once per op avoids a dependent shared load per field per channel.
+template <class T>
 struct EpiOp {
-    int relu, c8end, emit, own_only, gap, gap_np;
+    int relu, cend, emit, own_only, gap, gap_np;  // cend: output channels rounded up to a chunk
     int org_mul, org_sub, H, W, out_cstride, out_coff;
     int tile_h, tile_w, grid_h, grid_w;
     int buf_ew, buf_plane;
     uint8_t* buf;           // shared buffer base (planes), or null
-    __nv_bfloat16* out;
+    T* out;
     uint32_t bias_s;        // shared address of the op's fp32 bias (MMA ops)
     const float* bias_p;    // the same, as a generic pointer
 };
 
-__device__ __forceinline__ EpiOp epi_op(const BParams& P, const BOp& op, uint8_t* smem) {
-    EpiOp e;
-    e.relu = op.relu, e.c8end = (op.cout + 7) & ~7, e.emit = op.emit, e.own_only = op.own_only, e.gap = op.gap;
+template <class T>
+__device__ __forceinline__ EpiOp<T> epi_op(const BParams& P, const BOp& op, uint8_t* smem) {
+    constexpr int cpc = Elem<T>::cpc;
+    EpiOp<T> e;
+    e.relu = op.relu, e.cend = (op.cout + cpc - 1) / cpc * cpc, e.emit = op.emit, e.own_only = op.own_only, e.gap = op.gap;
     e.gap_np = op.gap ? op.nblocks * op.nb : 0;
     e.org_mul = op.org_mul, e.org_sub = op.org_sub, e.H = op.H, e.W = op.W;
     e.out_cstride = op.out_cstride, e.out_coff = op.out_coff;
@@ -397,13 +465,14 @@ __device__ __forceinline__ EpiOp epi_op(const BParams& P, const BOp& op, uint8_t
         const BRegion& B = P.bufs[op.buf];
         e.buf = smem + B.smem_off, e.buf_ew = B.ext_w, e.buf_plane = B.plane_bytes;
     }
-    e.out = (P.dbg & 1) ? nullptr : op.out;
+    e.out = static_cast<T*>(op.out);
     e.bias_s = op.bias_smem >= 0 ? smem_u32(smem + op.bias_smem) : 0u;
     e.bias_p = op.bias_smem >= 0 ? reinterpret_cast<const float*>(smem + op.bias_smem) : nullptr;
     return e;
 }
 
-__device__ __forceinline__ bool owns(const EpiOp& e, const BTile& t, int gy, int gx) {
+template <class T>
+__device__ __forceinline__ bool owns(const EpiOp<T>& e, const BTile& t, int gy, int gx) {
     if (!e.own_only)  // emitted cells: exactly this tile (contiguous-M ops compute a halo'd region)
         return gy >= t.oy0 && gy < t.oy0 + e.tile_h && gx >= t.ox0 && gx < t.ox0 + e.tile_w;
     const int S = e.org_mul;
@@ -414,14 +483,16 @@ __device__ __forceinline__ bool owns(const EpiOp& e, const BTile& t, int gy, int
 
 // Destination of one computed cell: the on-chip buffer (planes layout) and/or
 // its NHWC pixel in HBM.  Computed once per cell, reused for every channel.
+template <class T>
 struct CellDst {
     bool valid, inside;
-    uint8_t* sbuf;        // plane-0 address of the cell in the shared buffer, or null
-    __nv_bfloat16* gdst;  // channel-0 address of the pixel (concat offset applied), or null
+    uint8_t* sbuf;  // plane-0 address of the cell in the shared buffer, or null
+    T* gdst;        // channel-0 address of the pixel (concat offset applied), or null
 };
 
-__device__ __forceinline__ CellDst cell_dst(const EpiOp& e, const BTile& t, int r, int c, bool valid) {
-    CellDst d;
+template <class T>
+__device__ __forceinline__ CellDst<T> cell_dst(const EpiOp<T>& e, const BTile& t, int r, int c, bool valid) {
+    CellDst<T> d;
     const int gy = t.oy0 * e.org_mul - e.org_sub + r, gx = t.ox0 * e.org_mul - e.org_sub + c;
     d.valid = valid;
     d.inside = gy >= 0 && gy < e.H && gx >= 0 && gx < e.W;
@@ -430,16 +501,6 @@ __device__ __forceinline__ CellDst cell_dst(const EpiOp& e, const BTile& t, int 
     if (e.emit && !e.gap && e.out && valid && d.inside && owns(e, t, gy, gx))
         d.gdst = e.out + ((size_t(t.n) * e.H + gy) * e.W + gx) * e.out_cstride + e.out_coff + t.c0;
     return d;
-}
-
-__device__ __forceinline__ uint4 pack8(const float* v) {
-    uint4 u;
-    __nv_bfloat162 h;
-    h = __floats2bfloat162_rn(v[0], v[1]), u.x = *reinterpret_cast<uint32_t*>(&h);
-    h = __floats2bfloat162_rn(v[2], v[3]), u.y = *reinterpret_cast<uint32_t*>(&h);
-    h = __floats2bfloat162_rn(v[4], v[5]), u.z = *reinterpret_cast<uint32_t*>(&h);
-    h = __floats2bfloat162_rn(v[6], v[7]), u.w = *reinterpret_cast<uint32_t*>(&h);
-    return u;
 }
 
 __device__ __forceinline__ float4 lds_f4(uint32_t a) {
@@ -454,24 +515,31 @@ __device__ __forceinline__ uint4 lds_u4(uint32_t a) {
     return v;
 }
 
-// Stores 8 bf16 channels [ch, ch+8) of one cell.
-__device__ __forceinline__ void put8u(const CellDst& d, int ch, uint4 u, const EpiOp& e) {
-    if (d.sbuf) *reinterpret_cast<uint4*>(d.sbuf + (ch >> 3) * e.buf_plane) = d.inside ? u : make_uint4(0, 0, 0, 0);
-    if (d.gdst) *reinterpret_cast<uint4*>(d.gdst + ch) = u;
+// Stores chunk k (channels [k*cpc, (k+1)*cpc)) of one cell, already packed.
+template <class T>
+__device__ __forceinline__ void put_chunk(const CellDst<T>& d, int k, uint4 u, const EpiOp<T>& e) {
+    if (d.sbuf) *reinterpret_cast<uint4*>(d.sbuf + k * e.buf_plane) = d.inside ? u : make_uint4(0, 0, 0, 0);
+    if (d.gdst) *reinterpret_cast<uint4*>(d.gdst + k * Elem<T>::cpc) = u;
 }
 
-// Stores 8 channels [ch, ch+8) of one cell (values already final).
-__device__ __forceinline__ void put8(const CellDst& d, int ch, const float* v8, const EpiOp& e) {
-    const uint4 u = pack8(v8);
-    if (d.sbuf) *reinterpret_cast<uint4*>(d.sbuf + (ch >> 3) * e.buf_plane) = d.inside ? u : make_uint4(0, 0, 0, 0);
-    if (d.gdst) *reinterpret_cast<uint4*>(d.gdst + ch) = u;
+// Stores 8 channels [ch, ch+8) of one cell (values already final; ch < cend):
+// one bf16 chunk, or two fp32 chunks (the second only below cend -- fp32
+// tensors are padded to 4 channels, not 8).
+template <class T>
+__device__ __forceinline__ void put8(const CellDst<T>& d, int ch, const float* v8, const EpiOp<T>& e) {
+    constexpr int cpc = Elem<T>::cpc;
+    put_chunk(d, ch / cpc, Elem<T>::pack(v8), e);
+    if constexpr (cpc == 4) {
+        if (ch + 4 < e.cend) put_chunk(d, ch / cpc + 1, Elem<T>::pack(v8 + 4), e);
+    }
 }
 
 // Bias + ReLU + store of 16 accumulator columns (channels ch0 ...), unrolled.
-__device__ __forceinline__ void finish16(const EpiOp& e, const CellDst& d, int ch0, float* v) {
+template <class T>
+__device__ __forceinline__ void finish16(const EpiOp<T>& e, const CellDst<T>& d, int ch0, float* v) {
 #pragma unroll
     for (int j = 0; j < 16; j += 8) {
-        if (ch0 + j >= e.c8end) break;
+        if (ch0 + j >= e.cend) break;
         const float4 b0 = lds_f4(e.bias_s + uint32_t(ch0 + j) * 4u);
         const float4 b1 = lds_f4(e.bias_s + uint32_t(ch0 + j + 4) * 4u);
         float* x = v + j;
@@ -486,7 +554,8 @@ __device__ __forceinline__ void finish16(const EpiOp& e, const CellDst& d, int c
 // 32 accumulator columns: the TMEM load is issued first and the 32 bias
 // values are fetched from shared memory while it is in flight (the bias
 // fetch after the wait was the epilogue's main stall, ncu short_sb).
-__device__ __forceinline__ void finish32(const EpiOp& e, const CellDst& d, bool valid, int ch0, uint32_t ta) {
+template <class T>
+__device__ __forceinline__ void finish32(const EpiOp<T>& e, const CellDst<T>& d, bool valid, int ch0, uint32_t ta) {
     uint32_t r[32];
     tmem_ld32_issue(ta, r);
     const uint32_t bp = e.bias_s + uint32_t(ch0) * 4u;
@@ -497,7 +566,7 @@ __device__ __forceinline__ void finish32(const EpiOp& e, const CellDst& d, bool 
     if (!valid) return;
 #pragma unroll
     for (int j = 0; j < 32; j += 8) {
-        if (ch0 + j >= e.c8end) break;
+        if (ch0 + j >= e.cend) break;
         if (j == 16) {
 #pragma unroll
             for (int q = 0; q < 4; ++q) b[q] = lds_f4(bp + 64u + 16u * q);
@@ -537,7 +606,8 @@ __device__ __forceinline__ float warp_colsum32(float* v) {
 // Global-average-pool epilogue: relu(acc + bias) of the cells this tile owns
 // (others contribute 0), summed over the warp's rows and added to the tile's
 // per-column sums in shared memory.  Warp-uniform (all lanes shuffle).
-__device__ __forceinline__ void finish_gap(const EpiOp& e, bool take, int ch0, int ncols, uint32_t ta, float* gsum) {
+template <class T>
+__device__ __forceinline__ void finish_gap(const EpiOp<T>& e, bool take, int ch0, int ncols, uint32_t ta, float* gsum) {
     float v[32];
     if (ncols == 32) {
         tmem_ld32(ta, v);
@@ -563,17 +633,17 @@ __device__ __forceinline__ void finish_gap(const EpiOp& e, bool take, int ch0, i
     const int lane = threadIdx.x & 31;
     // per-warp slot (no shared float atomics: sm_100 lowers them to a CAS loop)
     float* slot = gsum + ((threadIdx.x >> 5) & 3) * e.gap_np;  // warps w, w+4 own disjoint columns
-    if (lane < ncols && ch0 + lane < e.c8end) slot[ch0 + lane] += colsum;
+    if (lane < ncols && ch0 + lane < e.cend) slot[ch0 + lane] += colsum;
 }
 
-// Accumulator -> bias/ReLU/mask -> bf16 -> shared buffer and/or HBM.  Thread
+// Accumulator -> bias/ReLU/mask -> bf16 / TF32 -> shared buffer and/or HBM.  Thread
 // (row = tid % 128) owns TMEM lane `row` = GEMM row = one cell.  With two
 // warp groups, narrow ops (<= 32 columns) split the M tiles between them,
 // wider ones split the columns in 32-column slices.
-template <int EW, bool GAP>
+template <class T, int EW, bool GAP>
 __device__ void epilogue_mma(const BParams& P, const BOp& op, int nbi, uint8_t* smem, uint32_t tmem, const BTile& t) {
     constexpr int kHalves = Cta<EW>::halves;
-    const EpiOp e = epi_op(P, op, smem);
+    const EpiOp<T> e = epi_op<T>(P, op, smem);
     const int mtiles = op.mtiles, contig = op.contig, ext_w = op.ext_w, ext_h = op.ext_h, strips = op.strips, nb = op.nb;
     const int row = threadIdx.x & 127, half = kHalves > 1 ? int(threadIdx.x >> 7) : 0;
     const uint32_t tbase = tmem + op.tcol + (uint32_t(row & ~31) << 16);
@@ -596,7 +666,7 @@ __device__ void epilogue_mma(const BParams& P, const BOp& op, int nbi, uint8_t* 
             wst += mstep;
             while (wst >= strips) wst -= strips, ++wrb;
         }
-        const CellDst d = cell_dst(e, t, r, c, valid);
+        const CellDst<T> d = cell_dst(e, t, r, c, valid);
         if (GAP) {
             float* gsum = reinterpret_cast<float*>(smem + P.gap_off);
             const bool take = valid && d.inside;
@@ -625,23 +695,13 @@ struct RegionView {
 };
 
 __device__ __forceinline__ RegionView region_view(const BRegion& R, uint8_t* smem) {
-    return {smem + R.smem_off, R.mode, R.kb_ch >> 3, R.plane_bytes, R.row_bytes, R.ext_w};
+    return {smem + R.smem_off, R.mode, R.row_bytes >> 4, R.plane_bytes, R.row_bytes, R.ext_w};
 }
 
 __device__ __forceinline__ const uint8_t* chunk_ptr(const RegionView& v, int cell, int oct) {
     const int kb = oct / v.per, j = oct - kb * v.per;
     const int sw = v.mode == kSw128 ? (cell & 7) : v.mode == kSw32 ? ((cell >> 2) & 1) : 0;
     return v.base + kb * v.plane + cell * v.rowb + ((j ^ sw) << 4);
-}
-
-__device__ __forceinline__ void load8(const RegionView& v, int cell, int oct, float* f) {
-    const uint4 raw = *reinterpret_cast<const uint4*>(chunk_ptr(v, cell, oct));
-    const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&raw);
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-        const float2 p = __bfloat1622float2(h[j]);
-        f[2 * j] = p.x, f[2 * j + 1] = p.y;
-    }
 }
 
 // Byte offset of 16-byte chunk j (within K-block kb) of cell `cell`, for a
@@ -653,36 +713,30 @@ __device__ __forceinline__ uint32_t chunk_off(uint32_t kb_base, int cell, int j)
     return kb_base + uint32_t(cell) * 16u;
 }
 
-__device__ __forceinline__ uint32_t bmax2(uint32_t a, uint32_t b) {
-    __nv_bfloat162 x = *reinterpret_cast<__nv_bfloat162*>(&a), y = *reinterpret_cast<__nv_bfloat162*>(&b);
-    __nv_bfloat162 m = __hmax2(x, y);
-    return *reinterpret_cast<uint32_t*>(&m);
-}
-
 // Pools over a shared region (zero padding is already in the region: TMA
 // zero fill / masked epilogue cells), max in bf16 (exact), average in fp32
-// over the full window (reference.cpp:59-88).  Thread u handles 8 channels
-// (oct) of one output cell, octs fastest: the 8 chunks of a cell sit in 8
-// different bank groups in every region mode, and 8 neighbouring threads
-// store one 128-byte run of the NHWC output.
-template <int EW, int MODE, int K, bool MX>
-__device__ void pool_fast(const EpiOp& e, const BRegion& Rg, uint8_t* smem, const BOp& op, const BTile& t) {
+// over the full window (reference.cpp:59-88).  Thread u handles one chunk
+// (oct: 8 bf16 / 4 fp32 channels) of one output cell, chunks fastest: the 8
+// chunks of a cell sit in 8 different bank groups in every region mode, and 8
+// neighbouring threads store one 128-byte run of the NHWC output.
+template <class T, int EW, int MODE, int K, bool MX>
+__device__ void pool_fast(const EpiOp<T>& e, const BRegion& Rg, uint8_t* smem, const BOp& op, const BTile& t) {
     const uint32_t base = smem_u32(smem + Rg.smem_off);
     const int plane = Rg.plane_bytes, rew = Rg.ext_w;
     const int ext_w = op.ext_w, stride = op.stride, dd = op.d;
     const int kh_ = K ? K : op.kh, kw_ = K ? K : op.kw;
-    const int ncell = op.ext_h * ext_w, c8 = op.npad / 8;
+    const int ncell = op.ext_h * ext_w, c8 = op.npad / Elem<T>::cpc;  // chunks per cell
     const float inv = 1.0f / float(kh_ * kw_);
     constexpr int kPer = MODE == kSw128 ? 8 : MODE == kSw32 ? 2 : 1;
-    // u = cell * c8 + oct, u = tid, tid + T, ...: when c8 divides T the
-    // thread's oct is fixed and its cell advances by T / c8 -- (r, c) are
+    // u = cell * c8 + oct, u = tid, tid + NT, ...: when c8 divides NT the
+    // thread's oct is fixed and its cell advances by NT / c8 -- (r, c) are
     // stepped instead of divided (two integer divisions per unit otherwise).
-    constexpr int T = Cta<EW>::compute;
-    const bool step = (T % c8) == 0;
-    const int oct0 = threadIdx.x % c8, cs = T / c8;
+    constexpr int NT = Cta<EW>::compute;
+    const bool step = (NT % c8) == 0;
+    const int oct0 = threadIdx.x % c8, cs = NT / c8;
     const int dr = cs / ext_w, dc = cs - dr * ext_w;
     int rr = (threadIdx.x / c8) / ext_w, cc = (threadIdx.x / c8) - rr * ext_w;
-    for (int u = threadIdx.x; u < ncell * c8; u += T) {
+    for (int u = threadIdx.x; u < ncell * c8; u += NT) {
         int r, c, oct;
         if (step) {
             r = rr, c = cc, oct = oct0;
@@ -706,84 +760,78 @@ __device__ void pool_fast(const EpiOp& e, const BRegion& Rg, uint8_t* smem, cons
                         for (int kx2 = 0; kx2 < (K ? 1 : kw_); ++kx2) {
                             const int dy = K ? ky : ky2, dx = K ? kx : kx2;
                             if (dy == 0 && dx == 0) continue;
-                            const uint4 v = lds_u4(chunk_off<MODE>(kbb, c0 + dy * rew + dx, j));
-                            m.x = bmax2(m.x, v.x), m.y = bmax2(m.y, v.y), m.z = bmax2(m.z, v.z), m.w = bmax2(m.w, v.w);
+                            m = Elem<T>::vmax(m, lds_u4(chunk_off<MODE>(kbb, c0 + dy * rew + dx, j)));
                         }
             out = m;
         } else {
-            float acc[8];
+            constexpr int cpc = Elem<T>::cpc;
+            float acc[cpc];
 #pragma unroll
-            for (int q = 0; q < 8; ++q) acc[q] = 0.0f;
+            for (int q = 0; q < cpc; ++q) acc[q] = 0.0f;
             for (int dy = 0; dy < kh_; ++dy)
                 for (int dx = 0; dx < kw_; ++dx) {
-                    const uint4 v = lds_u4(chunk_off<MODE>(kbb, c0 + dy * rew + dx, j));
-                    const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+                    float f[cpc];
+                    Elem<T>::unpack(lds_u4(chunk_off<MODE>(kbb, c0 + dy * rew + dx, j)), f);
 #pragma unroll
-                    for (int q = 0; q < 4; ++q) {
-                        const float2 f = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&w[q]));
-                        acc[2 * q] += f.x, acc[2 * q + 1] += f.y;
-                    }
+                    for (int q = 0; q < cpc; ++q) acc[q] += f[q];
                 }
 #pragma unroll
-            for (int q = 0; q < 8; ++q) acc[q] *= inv;
-            out = pack8(acc);
+            for (int q = 0; q < cpc; ++q) acc[q] *= inv;
+            out = Elem<T>::pack(acc);
         }
-        put8u(cell_dst(e, t, r, c, true), oct * 8, out, e);
+        put_chunk(cell_dst(e, t, r, c, true), oct, out, e);
     }
 }
 
-template <int EW, int MODE>
-__device__ __forceinline__ void pool_mode(const EpiOp& e, const BRegion& R, uint8_t* smem, const BOp& op, const BTile& t) {
+template <class T, int EW, int MODE>
+__device__ __forceinline__ void pool_mode(const EpiOp<T>& e, const BRegion& R, uint8_t* smem, const BOp& op, const BTile& t) {
     if (op.kind == BOP_MAXPOOL) {
-        if (op.kh == 3 && op.kw == 3) pool_fast<EW, MODE, 3, true>(e, R, smem, op, t);
-        else pool_fast<EW, MODE, 0, true>(e, R, smem, op, t);
+        if (op.kh == 3 && op.kw == 3) pool_fast<T, EW, MODE, 3, true>(e, R, smem, op, t);
+        else pool_fast<T, EW, MODE, 0, true>(e, R, smem, op, t);
     } else {
-        pool_fast<EW, MODE, 0, false>(e, R, smem, op, t);
+        pool_fast<T, EW, MODE, 0, false>(e, R, smem, op, t);
     }
 }
 
 // Residual add of two shared plane buffers.
-template <int EW>
-__device__ void simt_add(const EpiOp& e, const BRegion& A, const BRegion& B, uint8_t* smem, const BOp& op, const BTile& t) {
-    const int ext_w = op.ext_w, ncell = op.ext_h * ext_w, c8 = op.npad / 8;
+template <class T, int EW>
+__device__ void simt_add(const EpiOp<T>& e, const BRegion& A, const BRegion& B, uint8_t* smem, const BOp& op, const BTile& t) {
+    constexpr int cpc = Elem<T>::cpc;
+    const int ext_w = op.ext_w, ncell = op.ext_h * ext_w, c8 = op.npad / cpc;
     for (int u = threadIdx.x; u < ncell * c8; u += Cta<EW>::compute) {
         const int cell = u / c8, oct = u - cell * c8;
         const int r = cell / ext_w, c = cell - r * ext_w;
-        const uint4 a = lds_u4(smem_u32(smem + A.smem_off + oct * A.plane_bytes + (r * A.ext_w + c) * 16));
-        const uint4 b = lds_u4(smem_u32(smem + B.smem_off + oct * B.plane_bytes + (r * B.ext_w + c) * 16));
-        const uint32_t wa[4] = {a.x, a.y, a.z, a.w}, wb[4] = {b.x, b.y, b.z, b.w};
-        float acc[8];
+        float fa[cpc], fb[cpc];
+        Elem<T>::unpack(lds_u4(smem_u32(smem + A.smem_off + oct * A.plane_bytes + (r * A.ext_w + c) * 16)), fa);
+        Elem<T>::unpack(lds_u4(smem_u32(smem + B.smem_off + oct * B.plane_bytes + (r * B.ext_w + c) * 16)), fb);
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
-            const float2 fa = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&wa[q]));
-            const float2 fb = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&wb[q]));
-            acc[2 * q] = fa.x + fb.x, acc[2 * q + 1] = fa.y + fb.y;
-        }
-        put8(cell_dst(e, t, r, c, true), oct * 8, acc, e);
+        for (int q = 0; q < cpc; ++q) fa[q] += fb[q];
+        put_chunk(cell_dst(e, t, r, c, true), oct, Elem<T>::pack(fa), e);
     }
 }
 
-template <int EW>
+template <class T, int EW>
 __device__ void simt_pool_add(const BParams& P, const BOp& op, uint8_t* smem, const BTile& t, int xdelta) {
-    const EpiOp e = epi_op(P, op, smem);
+    const EpiOp<T> e = epi_op<T>(P, op, smem);
     const BRegion R = src_region_at(P, op, op.src, xdelta);
     if (op.kind == BOP_ADD) {
-        simt_add<EW>(e, R, P.bufs[op.src2], smem, op, t);
+        simt_add<T, EW>(e, R, P.bufs[op.src2], smem, op, t);
         return;
     }
-    if (R.mode == kSw128) pool_mode<EW, kSw128>(e, R, smem, op, t);
-    else if (R.mode == kSw32) pool_mode<EW, kSw32>(e, R, smem, op, t);
-    else pool_mode<EW, kPlanes>(e, R, smem, op, t);
+    if (R.mode == kSw128) pool_mode<T, EW, kSw128>(e, R, smem, op, t);
+    else if (R.mode == kSw32) pool_mode<T, EW, kSw32>(e, R, smem, op, t);
+    else pool_mode<T, EW, kPlanes>(e, R, smem, op, t);
 }
 
 // Direct conv for what the tensor-core path does not take (stride != 1,
 // groups, Cin not a multiple of 16).  fp32 accumulate.
-template <int EW>
+template <class T, int EW>
 __device__ void simt_conv(const BParams& P, const BOp& op, uint8_t* smem, const BTile& t, int xdelta) {
-    const EpiOp e = epi_op(P, op, smem);
+    constexpr int cpc = Elem<T>::cpc;
+    const EpiOp<T> e = epi_op<T>(P, op, smem);
     const RegionView R = region_view(src_region_at(P, op, op.src, xdelta), smem);
     const int ext_w = op.ext_w, kh_ = op.kh, kw_ = op.kw, stride = op.stride, dd = op.d, cout = op.cout;
-    const int ncell = op.ext_h * ext_w, c8 = op.npad / 8;
+    const int ncell = op.ext_h * ext_w, c8 = (op.npad + 7) / 8;  // groups of 8 output channels per cell
     const int cin_g = op.cin / op.group, cout_g = cout / op.group, cp4 = (cout + 3) & ~3;
     const float* wsimt = op.wsimt;
     const float* gbias = op.bias;
@@ -804,8 +852,8 @@ __device__ void simt_conv(const BParams& P, const BOp& op, uint8_t* smem, const 
                         const int oc = oct * 8 + j;
                         if (oc >= cout) break;
                         const int in_c = (oc / cout_g) * cin_g + ic;
-                        const __nv_bfloat16 xv = *reinterpret_cast<const __nv_bfloat16*>(chunk_ptr(R, cell_in, in_c >> 3) + (in_c & 7) * 2);
-                        acc[j] = fmaf(__bfloat162float(xv), __ldg(wrow + oc), acc[j]);
+                        const T xv = *reinterpret_cast<const T*>(chunk_ptr(R, cell_in, in_c / cpc) + (in_c % cpc) * int(sizeof(T)));
+                        acc[j] = fmaf(Elem<T>::to(xv), __ldg(wrow + oc), acc[j]);
                     }
                 }
 #pragma unroll
@@ -824,9 +872,9 @@ __device__ void simt_conv(const BParams& P, const BOp& op, uint8_t* smem, const 
 // adds; kGap is the conv + global-average-pool epilogue.
 enum : int { kMmaOnly = 0, kSimt = 1, kGap = 2 };
 
-template <int EW, int KIND>
-__global__ void __launch_bounds__(Cta<EW>::threads, Cta<EW>::min_blocks) fused_bf16_kernel(const __grid_constant__ BParams Pg, int batch,
-                                                                                        int n0) {
+template <class T, int EW, int KIND>
+__global__ void __launch_bounds__(Cta<EW>::threads, Cta<EW>::min_blocks) fused_tc_kernel(const __grid_constant__ BParams Pg, int batch,
+                                                                                      int n0) {
     constexpr int kCompute = Cta<EW>::compute, kWarpX = Cta<EW>::wx, kWarpMma = Cta<EW>::wmma, kWarpW = Cta<EW>::ww;
     extern __shared__ __align__(1024) uint8_t smem[];
     __shared__ __align__(8) uint64_t bar_x[2], x_free[2], ring_full[kRingMax], ring_empty[kRingMax], acc_full[2 * kBMaxUnits * kSubs],
@@ -879,7 +927,7 @@ __global__ void __launch_bounds__(Cta<EW>::threads, Cta<EW>::min_blocks) fused_b
         // (elect.sync, not lane == 0: the compiler then knows one thread is
         // active and moves descriptors to uniform registers without the
         // per-MMA ELECT waterfall it emits for a lane-predicated branch)
-        if (elect_one()) issuer(Pg, smem, tmem, total, bar_x, x_free, ring_full, ring_empty, acc_full, unit_done, acc_free, &bar_w);
+        if (elect_one()) issuer<T>(Pg, smem, tmem, total, bar_x, x_free, ring_full, ring_empty, acc_full, unit_done, acc_free, &bar_w);
         __syncwarp();
     } else {
         compute_wait<EW>(&bar_p, 0);
@@ -919,14 +967,14 @@ __global__ void __launch_bounds__(Cta<EW>::threads, Cta<EW>::min_blocks) fused_b
                             if (threadIdx.x == 0 && sub == 0) stamp(P, kTrUnit + 2 * gi, k);
                             fence_after();
                         }
-                        if (!(P.dbg & 2)) epilogue_mma<EW, KIND == kGap>(P, P.ops[i], G.nbi, smem, tm + uint32_t(G.tbase), t);
+                        epilogue_mma<T, EW, KIND == kGap>(P, P.ops[i], G.nbi, smem, tm + uint32_t(G.tbase), t);
                     }
                 } else {
                     if constexpr (KIND == kSimt) {
                         const BOp& op = P.ops[G.op0];
                         if (!have_x) compute_wait<EW>(&bar_x[b], use & 1), have_x = true;
-                        if (op.kind == BOP_SIMT_CONV) simt_conv<EW>(P, op, smem, t, xdelta);
-                        else simt_pool_add<EW>(P, op, smem, t, xdelta);
+                        if (op.kind == BOP_SIMT_CONV) simt_conv<T, EW>(P, op, smem, t, xdelta);
+                        else simt_pool_add<T, EW>(P, op, smem, t, xdelta);
                     }
                 }
                 fence_async_smem();  // epilogue-written buffers are read by later MMAs (async proxy)
@@ -967,50 +1015,54 @@ __global__ void __launch_bounds__(Cta<EW>::threads, Cta<EW>::min_blocks) fused_b
     if (warp == kWarpMma && Pg.tmem_cols) tmem_free(tmem, Pg.tmem_cols * Pg.tsets);
 }
 
-// ----------------------------------------------------------------- layout kernels (bf16)
+// ----------------------------------------------------------------- layout kernels
+// Conversions at the boundary (NCHW fp32 <-> NHWC T, channels padded to the
+// pitch with zeros) and the small steps outside fused kernels.  Values a
+// tensor-core step reads are rounded once here (bf16 RN / TF32 RNA).
 
-__global__ void nchw_f32_to_nhwc_bf16(const float* __restrict__ src, __nv_bfloat16* __restrict__ dst, int N, int C, int H, int W,
-                                      int cs) {
+template <class T>
+__global__ void nchw_f32_to_nhwc_tc(const float* __restrict__ src, T* __restrict__ dst, int N, int C, int H, int W, int cs) {
     const long long total = (long long)N * H * W * cs;
     for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total; i += (long long)gridDim.x * blockDim.x) {
         const int c = int(i % cs);
         const long long p = i / cs;
         const int x = int(p % W), y = int((p / W) % H);
         const long long n = p / ((long long)W * H);
-        dst[i] = __float2bfloat16(c < C ? src[((n * C + c) * H + y) * W + x] : 0.0f);
+        dst[i] = Elem<T>::from(c < C ? src[((n * C + c) * H + y) * W + x] : 0.0f);
     }
 }
 
-__global__ void nhwc_bf16_to_nchw_f32(const __nv_bfloat16* __restrict__ src, int cs, int coff, float* __restrict__ dst, int N, int C,
-                                      int H, int W) {
+template <class T>
+__global__ void nhwc_tc_to_nchw_f32(const T* __restrict__ src, int cs, int coff, float* __restrict__ dst, int N, int C, int H, int W) {
     const long long total = (long long)N * C * H * W;
     for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total; i += (long long)gridDim.x * blockDim.x) {
         const int x = int(i % W);
         const int y = int((i / W) % H);
         const int c = int((i / ((long long)W * H)) % C);
         const long long n = i / ((long long)W * H * C);
-        dst[i] = __bfloat162float(src[((n * H + y) * W + x) * cs + coff + c]);
+        dst[i] = Elem<T>::to(src[((n * H + y) * W + x) * cs + coff + c]);
     }
 }
 
-__global__ void seeded_nhwc_bf16(__nv_bfloat16* __restrict__ dst, unsigned long long seed, unsigned long long first_image, int N,
-                                 int C, int H, int W, int cs) {
+__device__ __forceinline__ float seeded_at(unsigned long long seed, unsigned long long idx) {  // SeededStream element idx (tensor.cpp:19-40)
+    unsigned long long z = seed + (idx + 1ull) * 0x9e3779b97f4a7c15ull;
+    z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ull;
+    z = (z ^ (z >> 27)) * 0x94d049bb133111ebull;
+    z = z ^ (z >> 31);
+    return static_cast<float>(z >> 40) * (1.0f / 16777216.0f) - 0.5f;
+}
+
+template <class T>
+__global__ void seeded_nhwc_tc(T* __restrict__ dst, unsigned long long seed, unsigned long long first_image, int N, int C, int H, int W,
+                               int cs) {
     const long long total = (long long)N * H * W * cs;
     for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total; i += (long long)gridDim.x * blockDim.x) {
         const int c = int(i % cs);
         const long long p = i / cs;
         const int x = int(p % W), y = int((p / W) % H);
         const long long n = p / ((long long)W * H);
-        float v = 0.0f;
-        if (c < C) {
-            unsigned long long z = seed + ((((first_image + n) * C + c) * H + y) * (unsigned long long)W + x + 1ull) *
-                                              0x9e3779b97f4a7c15ull;
-            z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ull;
-            z = (z ^ (z >> 27)) * 0x94d049bb133111ebull;
-            z = z ^ (z >> 31);
-            v = static_cast<float>(z >> 40) * (1.0f / 16777216.0f) - 0.5f;
-        }
-        dst[i] = __float2bfloat16(v);
+        const float v = c < C ? seeded_at(seed, (((first_image + n) * C + c) * H + y) * (unsigned long long)W + x) : 0.0f;
+        dst[i] = Elem<T>::from(v);
     }
 }
 
@@ -1018,8 +1070,9 @@ __global__ void seeded_nhwc_bf16(__nv_bfloat16* __restrict__ dst, unsigned long 
 // rewritten as a stride-1 conv on 2x2 phases so it runs on tensor cores):
 // dst[n][Y][X][(py*2+px)*C + c] = src[n][c][2Y+py][2X+px], channels >= 4C zero.
 // Source is NCHW fp32 (src != nullptr) or the SeededStream (seed, first_image).
-__global__ void s2d_bf16(const float* __restrict__ src, unsigned long long seed, unsigned long long first_image,
-                         __nv_bfloat16* __restrict__ dst, int N, int C, int H, int W, int cs) {
+template <class T>
+__global__ void s2d_tc(const float* __restrict__ src, unsigned long long seed, unsigned long long first_image, T* __restrict__ dst, int N,
+                       int C, int H, int W, int cs) {
     const int H2 = H / 2, W2 = W / 2;
     const long long total = (long long)N * H2 * W2 * cs;
     for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total; i += (long long)gridDim.x * blockDim.x) {
@@ -1032,22 +1085,14 @@ __global__ void s2d_bf16(const float* __restrict__ src, unsigned long long seed,
             const int ph = ci / C, c = ci - ph * C;
             const int y = 2 * Y + (ph >> 1), x = 2 * X + (ph & 1);
             const unsigned long long idx = (((unsigned long long)n * C + c) * H + y) * (unsigned long long)W + x;
-            if (src) {
-                v = src[idx];
-            } else {
-                unsigned long long z = seed + (first_image * (unsigned long long)C * H * W + idx + 1ull) * 0x9e3779b97f4a7c15ull;
-                z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ull;
-                z = (z ^ (z >> 27)) * 0x94d049bb133111ebull;
-                z = z ^ (z >> 31);
-                v = static_cast<float>(z >> 40) * (1.0f / 16777216.0f) - 0.5f;
-            }
+            v = src ? src[idx] : seeded_at(seed, first_image * (unsigned long long)C * H * W + idx);
         }
-        dst[i] = __float2bfloat16(v);
+        dst[i] = Elem<T>::from(v);
     }
 }
 
-__global__ void concat_copy_bf16(const __nv_bfloat16* __restrict__ src, int scs, int sco, __nv_bfloat16* __restrict__ dst, int dcs,
-                                 int dco, int C, long long pixels) {
+template <class T>
+__global__ void concat_copy_tc(const T* __restrict__ src, int scs, int sco, T* __restrict__ dst, int dcs, int dco, int C, long long pixels) {
     const long long total = pixels * C;
     for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total; i += (long long)gridDim.x * blockDim.x) {
         const long long p = i / C;
@@ -1056,21 +1101,23 @@ __global__ void concat_copy_bf16(const __nv_bfloat16* __restrict__ src, int scs,
     }
 }
 
-__global__ void eltwise_bf16(int op, const __nv_bfloat16* __restrict__ a, int acs, int aco, const __nv_bfloat16* __restrict__ b,
-                             int bcs, int bco, __nv_bfloat16* __restrict__ o, int ocs, int oco, int C, long long pixels) {
+template <class T>
+__global__ void eltwise_tc(int op, const T* __restrict__ a, int acs, int aco, const T* __restrict__ b, int bcs, int bco, T* __restrict__ o,
+                           int ocs, int oco, int C, long long pixels) {
     const long long total = pixels * C;
     for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total; i += (long long)gridDim.x * blockDim.x) {
         const long long p = i / C;
         const int c = int(i - p * C);
-        const float x = __bfloat162float(a[p * acs + aco + c]);
-        o[p * ocs + oco + c] = __float2bfloat16(op == 0 ? x + __bfloat162float(b[p * bcs + bco + c]) : fmaxf(x, 0.0f));
+        const float x = Elem<T>::to(a[p * acs + aco + c]);
+        o[p * ocs + oco + c] = Elem<T>::from(op == 0 ? x + Elem<T>::to(b[p * bcs + bco + c]) : fmaxf(x, 0.0f));
     }
 }
 
-// gap steps: out[n][coff + c] = bf16(scale * sum over the image's tiles of
-// part[n][tile][c]) for images [n0, n0 + N).
-__global__ void gap_finish_bf16(const float* __restrict__ part, int tiles, int np, float scale, __nv_bfloat16* __restrict__ out, int cs,
-                                int coff, int C, int n0, int N) {
+// gap steps: out[n][coff + c] = scale * sum over the image's tiles of
+// part[n][tile][c] for images [n0, n0 + N), in tile order (deterministic).
+template <class T>
+__global__ void gap_finish_tc(const float* __restrict__ part, int tiles, int np, float scale, T* __restrict__ out, int cs, int coff, int C,
+                              int n0, int N) {
     const long long total = (long long)N * C;
     for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total; i += (long long)gridDim.x * blockDim.x) {
         const long long n = n0 + i / C;
@@ -1078,7 +1125,7 @@ __global__ void gap_finish_bf16(const float* __restrict__ part, int tiles, int n
         const float* p = part + size_t(n) * tiles * np + c;
         float acc = 0.0f;
         for (int t = 0; t < tiles; ++t) acc += p[size_t(t) * np];
-        out[size_t(n) * cs + coff + c] = __float2bfloat16(acc * scale);
+        out[size_t(n) * cs + coff + c] = Elem<T>::from(acc * scale);
     }
 }
 
@@ -1087,15 +1134,29 @@ int grid_b(long long work) {
     return int(b < 148 * 16 ? (b < 1 ? 1 : b) : 148 * 16);
 }
 
+// SMs of the calling thread's current device (cached per device).
+int sm_count() {
+    static int cache[64] = {};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev < 0 || dev >= 64) dev = 0;
+    if (!cache[dev]) {
+        int n = 148;
+        if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || n < 1) n = 148;
+        cache[dev] = n;
+    }
+    return cache[dev];
+}
+
 }  // namespace
 
 namespace {
 
-template <int EW>
+template <class T, int EW>
 cudaError_t init_ew() {
     // 227 KB per block minus the static part (barriers + the BParams copy) and headroom
-    for (auto fn : {fused_bf16_kernel<EW, kMmaOnly>, fused_bf16_kernel<EW, kSimt>, fused_bf16_kernel<EW, kGap>}) {
-        cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBudgetBf16);
+    for (auto fn : {fused_tc_kernel<T, EW, kMmaOnly>, fused_tc_kernel<T, EW, kSimt>, fused_tc_kernel<T, EW, kGap>}) {
+        cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBudgetTc);
         if (e != cudaSuccess) return e;
         e = cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
         if (e != cudaSuccess) return e;
@@ -1105,73 +1166,46 @@ cudaError_t init_ew() {
 
 // Resident CTAs per SM from shared memory (228 KB per SM, 1 KB reserved per
 // CTA, the static barriers + descriptor copy), registers (64 K per SM in four
-// 16 K sub-partition files, warps placed round-robin) and the launch bound;
-// the occupancy API is printed for reference (it under-reports this kernel).
-// Over-subscribing is harmless (tiles are independent), under-subscribing
-// halves the overlap.
-template <int EW, int KIND>
+// 16 K sub-partition files, warps placed round-robin) and the launch bound
+// (the occupancy API under-reports this kernel).  Over-subscribing is
+// harmless (tiles are independent), under-subscribing halves the overlap.
+template <class T, int EW, int KIND>
 int occupancy_ew(int smem_bytes, int tmem_cols) {
-    int n = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, fused_bf16_kernel<EW, KIND>, Cta<EW>::threads, size_t(smem_bytes)) != cudaSuccess)
-        n = 0;
     cudaFuncAttributes a{};
-    cudaFuncGetAttributes(&a, fused_bf16_kernel<EW, KIND>);
+    cudaFuncGetAttributes(&a, fused_tc_kernel<T, EW, KIND>);
     const int by_smem = int((228 * 1024) / (size_t(smem_bytes) + a.sharedSizeBytes + 1024));
     const int warps = Cta<EW>::threads / 32, regs = std::max(a.numRegs, 1);
     int by_regs = 1;
     while ((by_regs + 1) * warps <= 64 && ((by_regs + 1) * warps + 3) / 4 * 32 * regs <= 16384) ++by_regs;
     int occ = std::max(1, std::min(std::min(Cta<EW>::min_blocks, by_regs), by_smem));
-    if (std::getenv("XLF_TRACE"))
-        std::fprintf(stderr, "[xlf] occupancy (%d epilogue warps): api %d, arithmetic %d (dynamic %d + static %zu B, %d regs)\n", EW, n,
-                     occ, smem_bytes, size_t(a.sharedSizeBytes), regs);
     // TMEM: 512 columns per SM; a CTA whose tcgen05.alloc cannot be served
     // waits for another CTA to exit, i.e. serialises behind a persistent one
     if (tmem_cols > 0) occ = std::min(occ, std::max(1, 512 / tmem_cols));
-    if (const char* f = std::getenv("XLF_CTAS")) occ = std::max(1, std::min(occ, std::atoi(f)));  // profiling aid
     return occ;
 }
 
-}  // namespace
-
-cudaError_t init_fused_bf16() {
-    cudaError_t e = init_ew<4>();
-    return e != cudaSuccess ? e : init_ew<8>();
-}
-
-int occupancy_fused_bf16(int smem_bytes, int tmem_cols, int epi_warps, int kind) {  // tmem_cols: per CTA (all sets)
+template <class T>
+int occupancy_t(int smem_bytes, int tmem_cols, int epi_warps, int kind) {
     if (epi_warps == 4)
-        return kind == kGap ? occupancy_ew<4, kGap>(smem_bytes, tmem_cols)
-               : kind == kSimt ? occupancy_ew<4, kSimt>(smem_bytes, tmem_cols) : occupancy_ew<4, kMmaOnly>(smem_bytes, tmem_cols);
-    return kind == kGap ? occupancy_ew<8, kGap>(smem_bytes, tmem_cols)
-           : kind == kSimt ? occupancy_ew<8, kSimt>(smem_bytes, tmem_cols) : occupancy_ew<8, kMmaOnly>(smem_bytes, tmem_cols);
+        return kind == kGap ? occupancy_ew<T, 4, kGap>(smem_bytes, tmem_cols)
+               : kind == kSimt ? occupancy_ew<T, 4, kSimt>(smem_bytes, tmem_cols) : occupancy_ew<T, 4, kMmaOnly>(smem_bytes, tmem_cols);
+    return kind == kGap ? occupancy_ew<T, 8, kGap>(smem_bytes, tmem_cols)
+           : kind == kSimt ? occupancy_ew<T, 8, kSimt>(smem_bytes, tmem_cols) : occupancy_ew<T, 8, kMmaOnly>(smem_bytes, tmem_cols);
 }
 
-// Step class of a descriptor (selects the kernel instantiation).
-int step_kind_bf16(const BParams& P) {
-    for (int i = 0; i < P.nops; ++i)
-        if (P.ops[i].gap) return kGap;
-    for (int i = 0; i < P.nops; ++i)
-        if (P.ops[i].kind != BOP_MMA) return kSimt;
-    return kMmaOnly;
-}
-
-cudaError_t launch_fused_bf16(const BParams& P, int batch, cudaStream_t st, int n0) {
+template <class T>
+cudaError_t launch_t(const BParams& P, int batch, cudaStream_t st, int n0) {
     const long long tiles = (long long)P.grid_h * P.grid_w * P.cgroups * batch;
-    int sms = 148;
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
-    const long long grid = P.grid_all ? tiles : std::min<long long>(tiles, (long long)sms * std::max(1, P.ctas_per_sm));
+    const long long grid = P.grid_all ? tiles : std::min<long long>(tiles, (long long)sm_count() * std::max(1, P.ctas_per_sm));
     if (grid < 1) return cudaSuccess;
-    if (P.trace && std::getenv("XLF_TRACE"))
-        std::fprintf(stderr, "[xlf] launch: %lld tiles, grid %lld x %d threads, %d B dynamic shared\n", tiles, grid, P.epi_warps * 32 + 96,
-                     P.smem_bytes);
-    const dim3 g(static_cast<unsigned>(grid), 1u, 1u);
     cudaLaunchConfig_t cfg{};
-    cfg.gridDim = g, cfg.blockDim = dim3(unsigned(P.epi_warps * 32 + 96)), cfg.dynamicSmemBytes = size_t(P.smem_bytes), cfg.stream = st;
+    cfg.gridDim = dim3(static_cast<unsigned>(grid), 1u, 1u), cfg.blockDim = dim3(unsigned(P.epi_warps * 32 + 96));
+    cfg.dynamicSmemBytes = size_t(P.smem_bytes), cfg.stream = st;
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    attr[0].val.programmaticStreamSerializationAllowed = std::getenv("XLF_NO_PDL") ? 0 : 1;
+    attr[0].val.programmaticStreamSerializationAllowed = P.pdl ? 1 : 0;
     cfg.attrs = attr, cfg.numAttrs = 1;
-#define XLF_LAUNCH(EWV, K) cudaLaunchKernelEx(&cfg, fused_bf16_kernel<EWV, K>, P, batch, n0)
+#define XLF_LAUNCH(EWV, K) cudaLaunchKernelEx(&cfg, fused_tc_kernel<T, EWV, K>, P, batch, n0)
     if (P.epi_warps == 4) {
         if (P.kind == kGap) XLF_LAUNCH(4, kGap);
         else if (P.kind == kSimt) XLF_LAUNCH(4, kSimt);
@@ -1185,47 +1219,95 @@ cudaError_t launch_fused_bf16(const BParams& P, int batch, cudaStream_t st, int 
     return cudaGetLastError();
 }
 
-cudaError_t launch_nchw_to_nhwc_bf16(const float* src, __nv_bfloat16* dst, int N, int C, int H, int W, int cs, cudaStream_t st) {
-    nchw_f32_to_nhwc_bf16<<<grid_b((long long)N * H * W * cs), 256, 0, st>>>(src, dst, N, C, H, W, cs);
+}  // namespace
+
+cudaError_t init_fused_tc() {
+    for (cudaError_t e : {init_ew<__nv_bfloat16, 4>(), init_ew<__nv_bfloat16, 8>(), init_ew<float, 4>(), init_ew<float, 8>()})
+        if (e != cudaSuccess) return e;
+    return cudaSuccess;
+}
+
+int occupancy_fused_tc(int smem_bytes, int tmem_cols, int epi_warps, int kind, int es) {  // tmem_cols: per CTA (all sets)
+    return es == 4 ? occupancy_t<float>(smem_bytes, tmem_cols, epi_warps, kind) : occupancy_t<__nv_bfloat16>(smem_bytes, tmem_cols, epi_warps, kind);
+}
+
+// Step class of a descriptor (selects the kernel instantiation).
+int step_kind_tc(const BParams& P) {
+    for (int i = 0; i < P.nops; ++i)
+        if (P.ops[i].gap) return kGap;
+    for (int i = 0; i < P.nops; ++i)
+        if (P.ops[i].kind != BOP_MMA) return kSimt;
+    return kMmaOnly;
+}
+
+cudaError_t launch_fused_tc(const BParams& P, int batch, cudaStream_t st, int n0) {
+    return P.es == 4 ? launch_t<float>(P, batch, st, n0) : launch_t<__nv_bfloat16>(P, batch, st, n0);
+}
+
+#define XLF_BY_ES(es, CALL_F32, CALL_BF16)                      \
+    do {                                                         \
+        if ((es) == 4) CALL_F32; else CALL_BF16;                 \
+    } while (0)
+
+cudaError_t launch_nchw_to_nhwc_tc(int es, const float* src, void* dst, int N, int C, int H, int W, int cs, cudaStream_t st) {
+    const int g = grid_b((long long)N * H * W * cs);
+    XLF_BY_ES(es, (nchw_f32_to_nhwc_tc<float><<<g, 256, 0, st>>>(src, static_cast<float*>(dst), N, C, H, W, cs)),
+              (nchw_f32_to_nhwc_tc<__nv_bfloat16><<<g, 256, 0, st>>>(src, static_cast<__nv_bfloat16*>(dst), N, C, H, W, cs)));
     return cudaGetLastError();
 }
 
-cudaError_t launch_nhwc_bf16_to_nchw(const __nv_bfloat16* src, int cs, int coff, float* dst, int N, int C, int H, int W,
-                                     cudaStream_t st) {
-    nhwc_bf16_to_nchw_f32<<<grid_b((long long)N * C * H * W), 256, 0, st>>>(src, cs, coff, dst, N, C, H, W);
+cudaError_t launch_nhwc_tc_to_nchw(int es, const void* src, int cs, int coff, float* dst, int N, int C, int H, int W, cudaStream_t st) {
+    const int g = grid_b((long long)N * C * H * W);
+    XLF_BY_ES(es, (nhwc_tc_to_nchw_f32<float><<<g, 256, 0, st>>>(static_cast<const float*>(src), cs, coff, dst, N, C, H, W)),
+              (nhwc_tc_to_nchw_f32<__nv_bfloat16><<<g, 256, 0, st>>>(static_cast<const __nv_bfloat16*>(src), cs, coff, dst, N, C, H, W)));
     return cudaGetLastError();
 }
 
-cudaError_t launch_seeded_nhwc_bf16(__nv_bfloat16* dst, unsigned long long seed, unsigned long long first_image, int N, int C, int H,
-                                    int W, int cs, cudaStream_t st) {
-    seeded_nhwc_bf16<<<grid_b((long long)N * H * W * cs), 256, 0, st>>>(dst, seed ? seed : 0x9e3779b97f4a7c15ull, first_image, N,
-                                                                      C, H, W, cs);
+cudaError_t launch_seeded_nhwc_tc(int es, void* dst, unsigned long long seed, unsigned long long first_image, int N, int C, int H, int W,
+                                  int cs, cudaStream_t st) {
+    const int g = grid_b((long long)N * H * W * cs);
+    seed = seed ? seed : 0x9e3779b97f4a7c15ull;
+    XLF_BY_ES(es, (seeded_nhwc_tc<float><<<g, 256, 0, st>>>(static_cast<float*>(dst), seed, first_image, N, C, H, W, cs)),
+              (seeded_nhwc_tc<__nv_bfloat16><<<g, 256, 0, st>>>(static_cast<__nv_bfloat16*>(dst), seed, first_image, N, C, H, W, cs)));
     return cudaGetLastError();
 }
 
-cudaError_t launch_s2d_bf16(const float* src, unsigned long long seed, unsigned long long first_image, __nv_bfloat16* dst, int N,
-                            int C, int H, int W, int cs, cudaStream_t st) {
-    s2d_bf16<<<grid_b((long long)N * (H / 2) * (W / 2) * cs), 256, 0, st>>>(src, seed ? seed : 0x9e3779b97f4a7c15ull, first_image, dst,
-                                                                          N, C, H, W, cs);
+cudaError_t launch_s2d_tc(int es, const float* src, unsigned long long seed, unsigned long long first_image, void* dst, int N, int C, int H,
+                          int W, int cs, cudaStream_t st) {
+    const int g = grid_b((long long)N * (H / 2) * (W / 2) * cs);
+    seed = seed ? seed : 0x9e3779b97f4a7c15ull;
+    XLF_BY_ES(es, (s2d_tc<float><<<g, 256, 0, st>>>(src, seed, first_image, static_cast<float*>(dst), N, C, H, W, cs)),
+              (s2d_tc<__nv_bfloat16><<<g, 256, 0, st>>>(src, seed, first_image, static_cast<__nv_bfloat16*>(dst), N, C, H, W, cs)));
     return cudaGetLastError();
 }
 
-cudaError_t launch_concat_copy_bf16(const __nv_bfloat16* src, int scs, int sco, __nv_bfloat16* dst, int dcs, int dco, int C,
-                                    long long pixels, cudaStream_t st) {
-    concat_copy_bf16<<<grid_b(pixels * C), 256, 0, st>>>(src, scs, sco, dst, dcs, dco, C, pixels);
+cudaError_t launch_concat_copy_tc(int es, const void* src, int scs, int sco, void* dst, int dcs, int dco, int C, long long pixels,
+                                  cudaStream_t st) {
+    const int g = grid_b(pixels * C);
+    XLF_BY_ES(es, (concat_copy_tc<float><<<g, 256, 0, st>>>(static_cast<const float*>(src), scs, sco, static_cast<float*>(dst), dcs, dco, C, pixels)),
+              (concat_copy_tc<__nv_bfloat16><<<g, 256, 0, st>>>(static_cast<const __nv_bfloat16*>(src), scs, sco,
+                                                                 static_cast<__nv_bfloat16*>(dst), dcs, dco, C, pixels)));
     return cudaGetLastError();
 }
 
-cudaError_t launch_gap_finish_bf16(const float* part, int tiles, int np, float scale, __nv_bfloat16* out, int cs, int coff, int C, int n0,
-                                   int N, cudaStream_t st) {
-    gap_finish_bf16<<<grid_b((long long)N * C), 256, 0, st>>>(part, tiles, np, scale, out, cs, coff, C, n0, N);
+cudaError_t launch_gap_finish_tc(int es, const float* part, int tiles, int np, float scale, void* out, int cs, int coff, int C, int n0, int N,
+                                 cudaStream_t st) {
+    const int g = grid_b((long long)N * C);
+    XLF_BY_ES(es, (gap_finish_tc<float><<<g, 256, 0, st>>>(part, tiles, np, scale, static_cast<float*>(out), cs, coff, C, n0, N)),
+              (gap_finish_tc<__nv_bfloat16><<<g, 256, 0, st>>>(part, tiles, np, scale, static_cast<__nv_bfloat16*>(out), cs, coff, C, n0, N)));
     return cudaGetLastError();
 }
 
-cudaError_t launch_eltwise_bf16(int op, const __nv_bfloat16* a, int acs, int aco, const __nv_bfloat16* b, int bcs, int bco,
-                                __nv_bfloat16* o, int ocs, int oco, int C, long long pixels, cudaStream_t st) {
-    eltwise_bf16<<<grid_b(pixels * C), 256, 0, st>>>(op, a, acs, aco, b, bcs, bco, o, ocs, oco, C, pixels);
+cudaError_t launch_eltwise_tc(int es, int op, const void* a, int acs, int aco, const void* b, int bcs, int bco, void* o, int ocs, int oco, int C,
+                              long long pixels, cudaStream_t st) {
+    const int g = grid_b(pixels * C);
+    XLF_BY_ES(es, (eltwise_tc<float><<<g, 256, 0, st>>>(op, static_cast<const float*>(a), acs, aco, static_cast<const float*>(b), bcs, bco,
+                                                       static_cast<float*>(o), ocs, oco, C, pixels)),
+              (eltwise_tc<__nv_bfloat16><<<g, 256, 0, st>>>(op, static_cast<const __nv_bfloat16*>(a), acs, aco,
+                                                           static_cast<const __nv_bfloat16*>(b), bcs, bco, static_cast<__nv_bfloat16*>(o), ocs,
+                                                           oco, C, pixels)));
     return cudaGetLastError();
 }
+#undef XLF_BY_ES
 
 }  // namespace xlf

@@ -1,21 +1,26 @@
-// Launch descriptor of the bf16 tensor-core fused-block kernel
-// (kernels_bf16.cu).  Same execution model as FusedParams (fused_params.hpp):
-// stage the block inputs, stage-1 ops, stage-2 ops; but activations are bf16
-// (fp32 accumulate) and conv ops with stride 1 / group 1 / Cin % 16 == 0 run
-// as implicit GEMMs on tcgen05 with the accumulator in TMEM.
+// Launch descriptor of the tensor-core fused-block kernel (kernels_tc.cu;
+// "B" = Blackwell).  Same execution model as FusedParams (fused_params.hpp):
+// stage the block inputs, stage-1 ops, stage-2 ops; but conv ops with stride
+// 1 / group 1 / 32-byte K steps run as implicit GEMMs on tcgen05 with the fp32
+// accumulator in TMEM.  Two element types (es = bytes per activation):
+//   es = 2  bf16 activations and weights, tcgen05.mma kind::f16 (K = 16 per step),
+//   es = 4  fp32 storage rounded to TF32, tcgen05.mma kind::tf32 (K = 8 per step).
+// Every layout below is in 16-byte "chunks" (8 bf16 / 4 fp32 channels), so one
+// K step is 32 bytes of every row for both types and the descriptors,
+// swizzles and weight packing are byte-identical.
 //
 // Shared-memory activation layout ("planes"): a region of ext_h x ext_w cells
-// with C channels is C/8 planes; plane p holds channels [8p, 8p+8) of every
-// cell as 16 bytes, cells row-major.  This is the UMMA K-major SWIZZLE_NONE
+// with C channels is C/cpc planes (cpc = channels per chunk); plane p holds
+// chunk p of every cell, cells row-major.  This is the UMMA K-major SWIZZLE_NONE
 // canonical layout with the cell index as M: 8 consecutive cells of a row are
 // one 8x16-byte core matrix, so
 //   * a 1x1 conv over the whole region is an M = cells GEMM (SBO = 128 B),
 //   * a kh x kw conv producing an 8-wide strip of rows reads, for tap (dy, dx),
 //     the same planes from start address + ((row+dy+d)*ext_w + col+dx+d)*16 with
 //     SBO = ext_w*16 B -- the shifted-window implicit GEMM, no im2col copy,
-//   * LBO = plane bytes steps K by 8 channels.
-// Block inputs are loaded by one 5-D TMA per input (box {8 ch, ext_w, ext_h,
-// C/8 planes, 1 image}, zero fill outside the image = conv padding).
+//   * LBO = plane bytes steps K by one chunk.
+// Block inputs are loaded by one 4-D TMA per K-block (box {kb_ch, ext_w,
+// ext_h, 1 image}, zero fill outside the image = conv padding).
 #pragma once
 
 #include <cuda.h>
@@ -39,12 +44,12 @@ constexpr int max_ctas_per_sm(int epi_warps) { return epi_warps <= 4 ? 4 : 2; }
 constexpr int kChunkBytes = 16 * 1024;  // weight ring slot (smallest; the tuner picks 16 / 32 / 64 KB)
 // Dynamic shared memory per CTA: 227 KB minus the static part (barriers, the
 // descriptor copy: 4 KB) minus 4 KB headroom (ncu's replay needs some).
-constexpr int kSmemBudgetBf16 = 227 * 1024 - 8192;
+constexpr int kSmemBudgetTc = 227 * 1024 - 8192;
 constexpr int kRingMax = 8;             // ring slots (P.ring_slots <= this)
 
 struct BOp {
     int kind, stage, xin, src, src2, buf, emit, own_only;
-    int cin, cin_pad, cout, npad, group, kh, kw, stride, pad, relu;
+    int cin, kpt, cout, npad, group, kh, kw, stride, pad, relu;  // kpt: MMA K steps (32 B) per tap
     int d;
     int ext_h, ext_w;       // computed region (cells), rows x cols
     int org_mul, org_sub;   // global cell row = tile_origin*org_mul - org_sub + r
@@ -54,10 +59,10 @@ struct BOp {
     int strips, mtiles;     // windowed: strips of 8 columns x blocks of 16 rows
     int nblocks, nb;        // N split into nblocks of nb (<= 256) accumulator columns
     int ksteps, chunk_steps;
-    const __nv_bfloat16* wmma;  // [nblock][kh*kw][cin_pad/8][nb][8]
+    const uint8_t* wmma;        // [nblock][kh*kw][cin/cpc][nb][cpc] elements (UMMA B image of each K step)
     const float* wsimt;         // [cin/group][kh][kw][cout_pad4] (SIMT convs)
     const float* bias;          // [npad] fp32 (zeros when the layer has no bias)
-    __nv_bfloat16* out;
+    void* out;                  // NHWC, element type of the step
     int out_cstride, out_coff;
     int tcol;       // MMA: first TMEM column of this op inside its group
     int wofs;       // MMA, resident weights: byte offset of the op's packed weights in the weight region
@@ -80,29 +85,29 @@ struct BGroup {
 };
 
 // Layout of a shared region: K-blocks of kb_ch channels; inside a K-block
-// cell r occupies row_bytes at r*row_bytes.
-//   kPlanes : kb_ch = 8,  row 16 B, no swizzle (epilogue-written buffers)
-//   kSw32   : kb_ch = 16, row 32 B, 32-byte swizzle  (TMA box of 16 channels)
-//   kSw128  : kb_ch = 64, row 128 B, 128-byte swizzle (TMA box of 64 channels)
+// cell r occupies row_bytes at r*row_bytes (kb_ch = row_bytes / es).
+//   kPlanes : row 16 B, no swizzle (epilogue-written buffers)
+//   kSw32   : row 32 B, 32-byte swizzle  (TMA box of one 32-byte K step)
+//   kSw128  : row 128 B, 128-byte swizzle (TMA box of four K steps)
 // Swizzles are functions of the absolute shared address (chunk ^= (addr>>7)
 // & mask), identical for TMA writes, UMMA reads and SIMT reads.
 enum : int { kPlanes = 0, kSw32 = 1, kSw128 = 3 };
 
 struct BRegion {
-    int c8;             // channels / 8
+    int chunks;         // 16-byte chunks per cell (channels / cpc)
     int ext_h, ext_w;   // cells
     int plane_bytes;    // bytes per K-block (multiple of 1024 for swizzled modes)
     int smem_off;       // bytes from the dynamic smem base
     int mode;           // kPlanes / kSw32 / kSw128
-    int kb_ch;          // channels per K-block (8 / 16 / 64)
+    int kb_ch;          // channels per K-block (row_bytes / es)
     int row_bytes;      // 16 / 32 / 128
 };
 
 struct BIn {
     BRegion r;
-    int h, w, cstride, coff;  // NHWC bf16 tensor
+    int h, w, cstride, coff;  // NHWC tensor (elements)
     int org_mul, org_sub;
-    const __nv_bfloat16* x;
+    const void* x;
 };
 
 struct alignas(64) BParams {
@@ -137,14 +142,14 @@ struct alignas(64) BParams {
     int epi_warps;    // 4 or 8 epilogue/SIMT warps (kernel instantiation)
     int kind;         // step class (kernel instantiation): 0 MMA ops only, 1 with SIMT ops, 2 conv + global average pool
     int tsets;        // accumulator sets in TMEM (2: tile k+1's MMAs run during tile k's epilogue; needs nxb = 2)
-    // Optional phase trace (XLF_TRACE=1): globaltimer stamps of CTAs with
+    int es;           // bytes per activation element: 2 (bf16, kind::f16) or 4 (fp32/TF32, kind::tf32)
+    int pdl;          // programmatic dependent launch (prologue overlaps the previous kernel's drain)
+    int xrel_epi;     // 1: the epilogue warps release the staging buffer after the tile even when
+                      // only MMAs read it (the earlier synchronisation structure; tested, not tuned)
+    // Optional phase trace (engine option trace=1): globaltimer stamps of CTAs with
     // blockIdx.y == 0 and blockIdx.x < kTraceCtas, kTraceEvents each.
     unsigned long long* trace;
-    int trace_tiles;  // XLF_TRACE=2: instead, the end stamp of each of the first kTraceEvents tiles
-    // Phase-isolation switches for profiling (XLF_DBG, never set in
-    // production; results are wrong when set): 1 = epilogues skip HBM stores,
-    // 2 = epilogues skip the accumulator read entirely, 4 = no MMAs issued.
-    int dbg;
+    int trace_tiles;  // trace=2: instead, the end stamp of each of the first kTraceEvents tiles
     // Device-memory copy of this descriptor: the kernel pulls it into shared
     // memory with one bulk copy instead of per-thread parameter-bank loads.
     const void* dev_copy;

@@ -42,12 +42,41 @@ __host__ __device__ constexpr uint32_t idesc_bf16(int M, int N) {
            | (uint32_t(M >> 4) << 24);     // M / 16
 }
 
+// Instruction descriptor, kind::tf32: TF32 x TF32 -> F32, both K-major (A/B
+// format field 2 = TF32; the operands are fp32 bit patterns in shared memory,
+// of which the MMA reads sign, exponent and the top 10 mantissa bits).
+__host__ __device__ constexpr uint32_t idesc_tf32(int M, int N) {
+    return (1u << 4)                       // D format f32
+           | (2u << 7)                     // A tf32
+           | (2u << 10)                    // B tf32
+           | (uint32_t(N >> 3) << 17)      // N / 8
+           | (uint32_t(M >> 4) << 24);     // M / 16
+}
+
 __device__ __forceinline__ void mma_bf16(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t accumulate) {
     asm volatile(
         "{\n\t.reg .pred p;\n\t"
         "setp.ne.b32 p, %4, 0;\n\t"
         "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(tmem_d),
         "l"(a), "l"(b), "r"(idesc), "r"(accumulate));
+}
+
+// M = 128, N <= 256, K = 8 (32 bytes of fp32/TF32 per row).
+__device__ __forceinline__ void mma_tf32(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(tmem_d),
+        "l"(a), "l"(b), "r"(idesc), "r"(accumulate));
+}
+
+// Round-to-nearest (ties away) to TF32, kept as an fp32 bit pattern with the
+// low 13 mantissa bits zero: operands the TF32 MMA then reads without further
+// truncation (unbiased rounding once, at the producer).
+__device__ __forceinline__ float round_tf32(float x) {
+    uint32_t r;
+    asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
+    return __uint_as_float(r);
 }
 
 // Arrives on `bar` once every previously issued tcgen05.mma of this thread completed.

@@ -8,6 +8,7 @@ import subprocess
 
 import pytest
 
+import paper_2007_06000_b200 as X
 from paper_2007_06000_b200 import _lib
 from tests.conftest import ROOT
 
@@ -44,14 +45,36 @@ def test_version_and_error_plumbing():
     assert _lib.STATUS[rc] == "parse"
     assert L.xlf_last_error()
     rc = L.xlf_graph_parse(None, ctypes.byref(h))
-    assert _lib.STATUS[rc] == "validation"
+    assert _lib.STATUS[rc] == "arg"
 
 
 def test_engine_rejects_bad_arguments_without_gpu():
     L = _lib.lib()
     out = ctypes.c_void_p()
     rc = L.xlf_engine_create(None, 0, 1, 0, None, 0, 1, ctypes.byref(out))
-    assert _lib.STATUS[rc] == "validation"
+    assert _lib.STATUS[rc] == "arg"
+
+
+def test_engine_options_are_validated_without_gpu():
+    """Planner / executor options come only through xlf_engine_create_ex's
+    option string (the library reads no environment variables); an unknown
+    key or a malformed value is refused before any device work."""
+    g = X.Graph(open(X.graph_path("fire")).read())
+    w = X.seeded_weights(g, 1)
+    for bad in ("nonsense=1", "xbuf=two", "xbuf"):
+        with pytest.raises(X.XlfError) as ei:
+            X.Engine(g, w, "b200", "bf16", options=bad)
+        assert ei.value.kind == "validation", bad
+    with pytest.raises(X.XlfError) as ei:
+        X.Engine(g, w, "b200", "int8")
+    assert ei.value.kind == "arg"
+
+
+def test_library_reads_no_environment():
+    csrc = os.path.join(ROOT, "paper_2007_06000_b200", "csrc")
+    for f in os.listdir(csrc):
+        if f.endswith((".cpp", ".cu", ".hpp", ".cuh")):
+            assert "getenv" not in open(os.path.join(csrc, f)).read(), f
 
 
 def test_product_does_not_import_oracle():

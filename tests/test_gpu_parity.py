@@ -88,26 +88,37 @@ def test_baseline_configs_full_batch(name, batch, sample):
     assert np.array_equal(out[o][batch - 1], alone[o][0])
 
 
-def test_squeezenet_b256_exact_sampled_and_argmax():
-    text = graph_text("squeezenet11")
-    og = O.load_graph(text)
-    # fan-in scaled weights so the logits (and their argmax) are not degenerate
-    # (SURVEY finding 7: U[-0.5,0.5) weights give class 288 for every input).
-    w = O.seeded_weights(og, 42)
+def he_weights(og, seed=42):
+    """Fan-in scaled weights so the logits (and their argmax) are not
+    degenerate (SURVEY finding 7: U[-0.5,0.5) weights give class 288 for every
+    input): He-uniform (bound sqrt(6/fan_in)) from the seeded stream, zero
+    bias -- the signal survives SqueezeNet's 26 layers."""
+    w = O.seeded_weights(og, seed)
     for l in og.layers:
         if l.kind == "conv":
             f, b = w[l.name]
             fan = f.shape[1] * f.shape[2] * f.shape[3]
-            # He-uniform (bound sqrt(6/fan_in)), zero bias: the signal survives 26 layers
             w[l.name] = ((f * np.float32(2.0 * np.sqrt(6.0 / fan))).astype(np.float32), (b * np.float32(0.0)).astype(np.float32))
+    return w
+
+
+def structured_inputs(og, n, seed=42):
+    """Seeded noise plus a per-image, per-channel offset, so images differ in
+    more than i.i.d. noise and the argmax varies."""
+    c = og.inputs[0][1][0]
+    x = O.seeded_batch(og, seed, n)
+    return (x + (O.stream(7, 0, n * c).reshape(n, c, 1, 1) * 4.0)).astype(np.float32)
+
+
+def test_squeezenet_b256_exact_sampled_and_argmax():
+    text = graph_text("squeezenet11")
+    og = O.load_graph(text)
+    w = he_weights(og)
     flat = O.flat_weights(og, w)
     import torch
     g = X.Graph(text)
     e = X.Engine(g, flat, "b200", "fp32_exact", max_batch=256)
-    # structured inputs: seeded noise plus a per-image, per-channel offset,
-    # so images differ in more than i.i.d. noise and the argmax varies
-    x = O.seeded_batch(og, 42, 256)
-    x = (x + (O.stream(7, 0, 256 * 3).reshape(256, 3, 1, 1) * 4.0)).astype(np.float32)
+    x = structured_inputs(og, 256)
     e.set_input(torch.from_numpy(x).cuda())
     e.forward(256)
     logits = e.read("pool10", 256).cpu().numpy().reshape(256, 1000)

@@ -198,7 +198,7 @@ def test_b200_cost_based_fusion_decisions():
     """bf16 B200 partition: a fused block is kept only when the planner's model
     beats its layers as single kernels.  Fire modules at 55x55 stay fused
     (measured 1.8x over unfused); inception-3a's 1x1-reduce -> 3x3 (221 KB of
-    weights re-streamed per small fused tile) is split; XLF_ALWAYS_FUSE keeps
+    weights re-streamed per small fused tile) is split; option always_fuse keeps
     every block fused."""
     import os
     g = X.load_graph(X.graph_path("fire"))
@@ -207,12 +207,8 @@ def test_b200_cost_based_fusion_decisions():
     g = X.load_graph(X.graph_path("inc3a"))
     steps = X.device_plan(g, "b200", 64, "bf16")["steps"]
     assert any(s["layers"] == ["b3"] for s in steps), [s["layers"] for s in steps]
-    os.environ["XLF_ALWAYS_FUSE"] = "1"
-    try:
-        steps = X.device_plan(g, "b200", 64, "bf16")["steps"]
-        assert not any(s["layers"] == ["b3"] for s in steps)
-    finally:
-        del os.environ["XLF_ALWAYS_FUSE"]
+    steps = X.device_plan(g, "b200", 64, "bf16", options="always_fuse=1")["steps"]
+    assert not any(s["layers"] == ["b3"] for s in steps)
     # the fp32 planner is unaffected (its kernels stage no weights)
     g = X.load_graph(X.graph_path("inc3a"))
     assert not any(s["layers"] == ["b3"] for s in X.device_plan(g, "b200", 64, "fp32")["steps"])
