@@ -74,6 +74,12 @@ xlf_status xlf_classify_mode(const xlf_graph* g, const char* names_csv, char* bu
  * device document, device.cpp:38-62); serialize_plan text (tiling.cpp:493). */
 xlf_status xlf_plan_tiling(const xlf_graph* g, const char* block_id, int tile_h, int tile_w, int grid_h, int grid_w,
                            const char* device, char* buf, size_t cap, size_t* need);
+/* serialize_device (device.cpp:64-90) of a device ("titan_xp" | "tesla_p4" |
+ * "b200" or a device document, parsed and checked by parse_device,
+ * device.cpp:38-62): the DeviceSpec documents the planner and
+ * xlf_block_prepare accept.  paper_2007_06000_b200/devices/b200.device is
+ * this function's output for "b200". */
+xlf_status xlf_device_document(const char* device, char* buf, size_t cap, size_t* need);
 /* Modelled 16-B store transactions fused / unfused (cost_model.cpp:43-55, titan_xp). */
 xlf_status xlf_store_tx(const xlf_graph* g, const char* block_id, long long* fused, long long* unfused);
 /* Device program of a partition (host-only planning: kernel steps, tiles,
@@ -139,6 +145,55 @@ xlf_status xlf_engine_apply_tuning(xlf_engine* e, const char* json);
 /* Profiling aid (engine created with option trace=1, tensor-core precisions):
  * globaltimer stamps of the first CTAs of a step's last launch. */
 xlf_status xlf_engine_trace(const xlf_engine* e, int step, unsigned long long* out, size_t cap, size_t* count);
+
+/* ---- one fused block: replaces run_fused_block (fused_exec.hpp:35-37,
+ *      fused_exec.cpp:30-311) ------------------------------------------- */
+
+typedef struct xlf_block xlf_block;
+
+typedef enum {
+    XLF_LAYOUT_NCHW_F32 = 0, /* reference layout: CHW fp32 per image, images stacked */
+    XLF_LAYOUT_NHWC = 1      /* the engine's HBM layout: bf16 (XLF_BF16) or fp32 (other precisions),
+                                `cstride` elements per pixel, the tensor at channel `coff` (e.g. its
+                                concat slice); both multiples of 16 bytes, address 16-byte aligned.
+                                Inputs: channels past C up to the next 16-byte multiple must be zero;
+                                outputs: those pad channels are written (as zero). */
+} xlf_layout;
+
+/* A caller-owned device tensor (image 0's address; `batch` images follow). */
+typedef struct {
+    void* data;
+    int layout;  /* xlf_layout */
+    int cstride; /* NHWC only */
+    int coff;    /* NHWC only */
+} xlf_tensor_ref;
+
+/* Prepares block `block_id` of `partition` (XLF_PART_REFERENCE: exactly
+ * detect_fusion_blocks, fusion.cpp:147-226; or XLF_PART_B200) for `max_batch`
+ * images on GPU `gpu`.  weights: the WHOLE graph's weights in save_weights order
+ * (the reference's WeightSet).  plan_text: a serialize_plan document
+ * (tiling.cpp:493-527; e.g. from xlf_plan_tiling or the reference planner) whose
+ * tile geometry the kernel runs at, or NULL for the B200 planner's tile; a plan
+ * for another block -> XLF_E_VALIDATION (fused_exec.cpp:33-38), a geometry the
+ * B200 kernel cannot hold -> XLF_E_INFEASIBLE.  device: "b200" (default, NULL),
+ * "titan_xp", "tesla_p4" or a device document (parse_device, device.cpp:38-62):
+ * the transaction size of the counters in xlf_block_json.  An unfused block ->
+ * XLF_E_INTERNAL (as the reference).  The handle is immutable for the caller;
+ * xlf_block_run may be called from several threads (runs on different streams
+ * are ordered by the library: they share the block's staging tensors). */
+xlf_status xlf_block_prepare(const xlf_graph* g, const char* block_id, int partition, const char* plan_text, const char* device, int gpu,
+                             int precision, const float* weights, size_t n_weights, int max_batch, const char* options, xlf_block** out);
+/* JSON: inputs / outputs in the order xlf_block_run takes them (the block's
+ * external inputs in layer order; stored_tensors order, cost_model.cpp:21-41),
+ * tile, element bytes, per-image counters (stored elements, global store
+ * transactions, MACs), the engine's plan. */
+xlf_status xlf_block_json(const xlf_block* b, char* buf, size_t cap, size_t* need);
+/* Runs the block on `batch` images: reads ins[i], writes outs[i] (caller-owned,
+ * any mix of layouts).  Asynchronous and stream-ordered, no host sync.  The
+ * first run with a new set of NHWC addresses builds their descriptors (cached). */
+xlf_status xlf_block_run(xlf_block* b, const xlf_tensor_ref* ins, int n_ins, const xlf_tensor_ref* outs, int n_outs, int batch,
+                         void* stream);
+void xlf_block_destroy(xlf_block* b);
 
 #ifdef __cplusplus
 }

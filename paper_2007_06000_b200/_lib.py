@@ -15,12 +15,20 @@ LIB_PATH = os.path.join(HERE, "libxlfuse_b200.so")
 # Every symbol include/xlfuse_b200.h declares (checked by tests/test_abi.py).
 SYMBOLS = [
     "xlf_last_error", "xlf_version", "xlf_graph_parse", "xlf_graph_destroy", "xlf_graph_json", "xlf_graph_serialize",
-    "xlf_block_report", "xlf_blocks_json", "xlf_classify_mode", "xlf_plan_tiling", "xlf_store_tx", "xlf_device_plan_json", "xlf_device_plan_json_ex", "xlf_seeded_weights",
+    "xlf_block_report", "xlf_blocks_json", "xlf_classify_mode", "xlf_plan_tiling", "xlf_store_tx", "xlf_device_document", "xlf_device_plan_json", "xlf_device_plan_json_ex", "xlf_seeded_weights",
     "xlf_engine_create", "xlf_engine_create_ex", "xlf_engine_destroy", "xlf_engine_json", "xlf_engine_num_steps",
     "xlf_engine_launches_per_forward", "xlf_engine_set_input", "xlf_engine_set_input_named", "xlf_engine_set_input_seeded", "xlf_engine_forward",
     "xlf_engine_run_step", "xlf_engine_read", "xlf_engine_run_host", "xlf_engine_autotune", "xlf_engine_tune_report", "xlf_engine_apply_tuning",
-    "xlf_engine_trace",
+    "xlf_engine_trace", "xlf_block_prepare", "xlf_block_json", "xlf_block_run", "xlf_block_destroy",
 ]
+
+
+class TensorRef(ctypes.Structure):
+    """xlf_tensor_ref: a caller-owned device tensor."""
+    _fields_ = [("data", ctypes.c_void_p), ("layout", ctypes.c_int), ("cstride", ctypes.c_int), ("coff", ctypes.c_int)]
+
+
+LAYOUT_NCHW_F32, LAYOUT_NHWC = 0, 1
 
 STATUS = {0: "ok", 1: "io", 2: "parse", 3: "validation", 4: "infeasible", 5: "verification", 6: "internal", 7: "cuda",
           8: "arg"}
@@ -59,6 +67,7 @@ def lib() -> ctypes.CDLL:
         getattr(L, fn).argtypes = [vp, ctypes.c_int, ctypes.c_char_p, sz, szp]
     L.xlf_classify_mode.argtypes = [vp, c_char_pp, ctypes.c_char_p, sz, szp]
     L.xlf_plan_tiling.argtypes = [vp, c_char_pp] + [ctypes.c_int] * 4 + [c_char_pp, ctypes.c_char_p, sz, szp]
+    L.xlf_device_document.argtypes = [c_char_pp, ctypes.c_char_p, sz, szp]
     L.xlf_store_tx.argtypes = [vp, c_char_pp, ctypes.POINTER(ctypes.c_longlong), ctypes.POINTER(ctypes.c_longlong)]
     L.xlf_device_plan_json.argtypes = [vp, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_char_p, sz, szp]
     L.xlf_device_plan_json_ex.argtypes = [vp, ctypes.c_int, ctypes.c_int, ctypes.c_int, c_char_pp, ctypes.c_char_p, sz, szp]
@@ -81,6 +90,12 @@ def lib() -> ctypes.CDLL:
     L.xlf_engine_tune_report.argtypes = [vp, ctypes.c_char_p, sz, szp]
     L.xlf_engine_apply_tuning.argtypes = [vp, ctypes.c_char_p]
     L.xlf_engine_trace.argtypes = [vp, ctypes.c_int, ctypes.POINTER(ctypes.c_ulonglong), sz, szp]
+    L.xlf_block_prepare.argtypes = [vp, c_char_pp, ctypes.c_int, c_char_pp, c_char_pp, ctypes.c_int, ctypes.c_int, f32p, sz, ctypes.c_int,
+                                    c_char_pp, ctypes.POINTER(vp)]
+    L.xlf_block_json.argtypes = [vp, ctypes.c_char_p, sz, szp]
+    L.xlf_block_run.argtypes = [vp, ctypes.POINTER(TensorRef), ctypes.c_int, ctypes.POINTER(TensorRef), ctypes.c_int, ctypes.c_int, vp]
+    L.xlf_block_destroy.argtypes = [vp]
+    L.xlf_block_destroy.restype = None
     _LIB = L
     return L
 

@@ -19,7 +19,7 @@ from dataclasses import dataclass, field
 import numpy as np
 
 from . import _lib
-from ._lib import XlfError, check, lib, text_call
+from ._lib import TensorRef, XlfError, check, lib, text_call  # noqa: F401
 
 PARTITIONS = {"reference": 0, "b200": 1, "unfused": 2}
 PRECISIONS = {"fp32_exact": 0, "fp32": 1, "bf16": 2, "tf32": 3}
@@ -143,6 +143,11 @@ def plan_tiling(g: Graph, block_id: str, tile, grid, device: str = "titan_xp") -
     return text_call(lib().xlf_plan_tiling, g._h, block_id.encode(), tile[0], tile[1], grid[0], grid[1], device.encode())
 
 
+def device_document(device: str = "b200") -> str:
+    """serialize_device(parse_device / builtin spec) (device.cpp:38-90)."""
+    return text_call(lib().xlf_device_document, device.encode())
+
+
 def store_transactions(g: Graph, block_id: str):
     f, u = ctypes.c_longlong(), ctypes.c_longlong()
     check(lib().xlf_store_tx(g._h, block_id.encode(), ctypes.byref(f), ctypes.byref(u)))
@@ -162,6 +167,15 @@ def seeded_weights(g: Graph, seed: int) -> np.ndarray:
     out = np.empty(n.value, np.float32)
     check(lib().xlf_seeded_weights(g._h, seed, out.ctypes.data_as(ctypes.POINTER(ctypes.c_float)), n.value, ctypes.byref(n)))
     return out
+
+
+def _check_tensor(graph, x, name, device):
+    import torch
+    shape = graph.shape_of(name)
+    ok = isinstance(x, torch.Tensor) and x.dtype == torch.float32 and x.dim() == 4 and tuple(x.shape[1:]) == tuple(shape)
+    if not ok or (device and not (x.is_cuda and x.is_contiguous())):
+        raise XlfError(8, f"input {name!r} must be a contiguous{' CUDA' if device else ''} float32 [batch, {shape[0]}, "
+                          f"{shape[1]}, {shape[2]}] tensor, got {getattr(x, 'dtype', type(x))} {tuple(getattr(x, 'shape', ()))}")
 
 
 def _stream_ptr(stream):
@@ -202,12 +216,7 @@ class Engine:
         return lib().xlf_engine_launches_per_forward(self._h)
 
     def _check_input(self, x, name, device):
-        import torch
-        shape = self.graph.shape_of(name)
-        ok = isinstance(x, torch.Tensor) and x.dtype == torch.float32 and x.dim() == 4 and tuple(x.shape[1:]) == tuple(shape)
-        if not ok or (device and not (x.is_cuda and x.is_contiguous())):
-            raise XlfError(8, f"input {name!r} must be a contiguous{' CUDA' if device else ''} float32 [batch, {shape[0]}, "
-                              f"{shape[1]}, {shape[2]}] tensor, got {getattr(x, 'dtype', type(x))} {tuple(getattr(x, 'shape', ()))}")
+        _check_tensor(self.graph, x, name, device)
 
     def set_input(self, x, stream=None, name=None):
         """x: torch CUDA float32 NCHW [batch, C, H, W] (contiguous); `name`
@@ -275,58 +284,81 @@ def simulate_graph(g: Graph, x, weights: np.ndarray, partition: str = "b200", pr
     return {n: e.read(n, x.shape[0]) for n in names}
 
 
-def block_subgraph(g: Graph, block: FusionBlock) -> tuple:
-    """Graph text holding exactly one block: its external inputs become graph
-    inputs and its stored tensors (cost_model.cpp:21-41) graph outputs."""
-    members = [l for l in g.layers if l["name"] in block.members]
-    names = {l["name"] for l in members}
-    ext = []
-    for l in members:
-        for i in l["inputs"]:
-            if i not in names and i not in ext:
-                ext.append(i)
-    outs = list(block.consumer_stage) if block.fused() else list(block.members)
-    for p in block.producer_stage:
-        if g.consumers_of(p) and any(c not in names for c in g.consumers_of(p)) or p in g.outputs:
-            outs.append(p)
-    lines = [f"name {g.name}_{block.id}"]
-    for i in ext:
-        c, h, w = g.shape_of(i)
-        lines += ["input {", f"  name {i}", f"  shape [{c}, {h}, {w}]", "}"]
-    for l in members:
-        lines += ["layer {", f"  name {l['name']}", f"  kind {l['kind']}", f"  inputs [{', '.join(l['inputs'])}]"]
-        if l["kind"] == "conv":
-            c = l["conv"]
-            lines += [f"  out_channels {c['out_channels']}", f"  kernel [{c['kernel'][0]}, {c['kernel'][1]}]",
-                      f"  pad {c['pad']}", f"  stride {c['stride']}", f"  group {c['group']}",
-                      f"  bias {'true' if c['bias'] else 'false'}", f"  activation {'relu' if c['relu'] else 'none'}"]
-        if l["kind"] == "pool":
-            p = l["pool"]
-            lines += [f"  pool {p['kind']}", f"  kernel {p['kernel']}", f"  stride {p['stride']}", f"  pad {p['pad']}"]
-        lines.append("}")
-    lines += [f"output {o}" for o in outs]
-    return "\n".join(lines) + "\n", ext, outs
+class Block:
+    """One fused block on the GPU: the successor of run_fused_block
+    (fused_exec.hpp:35-37, fused_exec.cpp:30-311) behind xlf_block_prepare /
+    xlf_block_run.  ``plan``: a serialize_plan text (e.g. ``plan_tiling(...)``)
+    whose tile geometry the kernel runs at; None = the B200 planner's tile."""
+
+    def __init__(self, g: Graph, block, weights: np.ndarray, precision: str = "fp32_exact", partition: str = "reference",
+                 plan: str | None = None, device: str = "b200", max_batch: int = 1, gpu: int = 0, options=None):
+        if partition not in ("reference", "b200") or precision not in PRECISIONS:
+            raise XlfError(8, f"unknown partition / precision {partition!r} / {precision!r}")
+        bid = block.id if isinstance(block, FusionBlock) else str(block)
+        w = np.ascontiguousarray(weights, np.float32)
+        h = ctypes.c_void_p()
+        check(lib().xlf_block_prepare(g._h, bid.encode(), PARTITIONS[partition], plan.encode() if plan else None, device.encode(), gpu,
+                                      PRECISIONS[precision], w.ctypes.data_as(ctypes.POINTER(ctypes.c_float)), w.size, max_batch,
+                                      _options(options), ctypes.byref(h)))
+        self._h = h
+        self.graph, self.precision, self.max_batch, self.gpu = g, precision, max_batch, gpu
+        self.info = json.loads(text_call(lib().xlf_block_json, h))
+        self.inputs = [i["name"] for i in self.info["inputs"]]
+        self.outputs = [o["name"] for o in self.info["outputs"]]
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h and _lib._LIB is not None:
+            lib().xlf_block_destroy(h)
+            self._h = None
+
+    @staticmethod
+    def ref(t, layout: str = "nchw", cstride: int = 0, coff: int = 0) -> _lib.TensorRef:
+        """xlf_tensor_ref of a torch CUDA tensor: NCHW fp32, or NHWC in the
+        block's element type (`cstride` elements per pixel, channel `coff`)."""
+        if layout == "nchw":
+            return _lib.TensorRef(t.data_ptr(), _lib.LAYOUT_NCHW_F32, 0, 0)
+        return _lib.TensorRef(t.data_ptr(), _lib.LAYOUT_NHWC, cstride or int(t.shape[-1]), coff)
+
+    def run(self, ins, outs, batch: int, stream=None) -> None:
+        """ins / outs: xlf_tensor_ref lists in the order of self.inputs / self.outputs."""
+        ai = (_lib.TensorRef * max(1, len(ins)))(*ins)
+        ao = (_lib.TensorRef * max(1, len(outs)))(*outs)
+        check(lib().xlf_block_run(self._h, ai, len(ins), ao, len(outs), batch, _stream_ptr(stream)))
 
 
-def block_weights(g: Graph, block: FusionBlock, weights: np.ndarray) -> np.ndarray:
-    parts = []
-    for name, off, nf, nb in g.conv_weight_spans():
-        if name in block.members:
-            parts.append(weights[off:off + nf + nb])
-    return np.concatenate(parts) if parts else np.zeros(0, np.float32)
-
-
-def run_fused_block(g: Graph, block: FusionBlock, values: dict, weights: np.ndarray, precision: str = "fp32_exact"):
-    """fused_exec.cpp:30-311 on the GPU: reads the block's inputs from
-    ``values`` (torch CUDA NCHW), returns its stored tensors."""
+def run_fused_block(g: Graph, block: FusionBlock, values: dict, weights: np.ndarray, precision: str = "fp32_exact",
+                    plan: str | None = None, partition: str = "reference"):
+    """fused_exec.cpp:30-311 on the GPU: reads the block's producer inputs by
+    name from ``values`` (torch CUDA NCHW fp32, caller-owned) and inserts /
+    overwrites its stored tensors (consumer outputs + escaping intermediates,
+    cost_model.cpp:21-41) in ``values``, like the reference.  Returns the
+    names written.  ``weights``: the whole graph's, save_weights order."""
+    import torch
     if not block.fused():
         raise XlfError(6, "run_fused_block: block is not fused")
-    text, ext, outs = block_subgraph(g, block)
-    sub = Graph(text)
-    if len(sub.inputs) != 1:
-        raise XlfError(3, "run_fused_block: blocks with more than one external input are run through simulate_graph")
-    x = values[ext[0]]
-    e = Engine(sub, block_weights(g, block, weights), "reference", precision, max_batch=x.shape[0])
-    e.set_input(x)
-    e.forward(x.shape[0])
-    return {o: e.read(o, x.shape[0]) for o in outs}
+    ins = []
+    for n in _block_inputs(g, block):
+        if n not in values:
+            raise XlfError(6, f"missing input tensor '{n}'")
+        ins.append(values[n])
+    batch = ins[0].shape[0]
+    b = Block(g, block, weights, precision, partition, plan=plan, max_batch=batch, gpu=ins[0].device.index or 0)
+    outs = {o: torch.empty((batch,) + tuple(g.shape_of(o)), dtype=torch.float32, device=ins[0].device) for o in b.outputs}
+    for x, n in zip(ins, b.inputs):
+        _check_tensor(g, x, n, True)
+    b.run([Block.ref(x) for x in ins], [Block.ref(outs[o]) for o in b.outputs], batch)
+    values.update(outs)
+    return list(outs)
+
+
+def _block_inputs(g: Graph, block: FusionBlock) -> list:
+    """External inputs of a block in layer order (xlf_block_prepare's order)."""
+    names = set(block.members)
+    ext = []
+    for l in g.layers:
+        if l["name"] in names:
+            for i in l["inputs"]:
+                if i not in names and i not in ext:
+                    ext.append(i)
+    return ext

@@ -4,7 +4,9 @@
 // error.hpp:21-35).
 #include "../../include/xlfuse_b200.h"
 
+#include <algorithm>
 #include <cstring>
+#include <mutex>
 #include <memory>
 #include <sstream>
 #include <string>
@@ -227,6 +229,13 @@ xlf_status xlf_plan_tiling(const xlf_graph* h, const char* block_id, int th, int
     });
 }
 
+xlf_status xlf_device_document(const char* device, char* buf, size_t cap, size_t* need) {
+    return guard([&] {
+        need_ptr(device, "device");
+        put(xlf::serialize_device(device_named(device)), buf, cap, need);
+    });
+}
+
 xlf_status xlf_store_tx(const xlf_graph* h, const char* block_id, long long* fused, long long* unfused) {
     return guard([&] {
         need_ptr(h, "graph"), need_ptr(fused, "fused"), need_ptr(unfused, "unfused");
@@ -380,3 +389,169 @@ extern "C" xlf_status xlf_engine_trace(const xlf_engine* e, int step, unsigned l
         }
     });
 }
+
+// ---------------------------------------------------------------- one fused block
+// run_fused_block (reference fused_exec.hpp:35-37, fused_exec.cpp:30-311) on the
+// device: the block's layers become a graph of their own (its external inputs
+// = graph inputs, its stored tensors (cost_model.cpp:21-41) = graph outputs),
+// executed by an Engine whose single fused step runs at the reference plan's
+// tile geometry when one is given.
+struct xlf_block {
+    std::unique_ptr<xlf::Engine> e;
+    xlf::FusionBlock block;
+    std::vector<std::string> ins, outs;
+    std::string desc;
+    std::mutex mu;  // xlf_block_run may be called from several threads
+    // runs share the engine's staging tensors (NCHW conversions, partial sums):
+    // a run on another stream waits for the previous run's end
+    cudaEvent_t done = nullptr;
+    cudaStream_t last = nullptr;
+    bool ran = false;
+    ~xlf_block() {
+        if (done) cudaEventDestroy(done);
+    }
+};
+
+namespace {
+
+xlf::Graph block_graph(const xlf::Graph& g, const xlf::FusionBlock& b, std::vector<std::string>& ins, std::vector<std::string>& outs) {
+    xlf::Graph sub;
+    sub.name = g.name + "_" + b.id;
+    auto member = [&](const std::string& n) { return std::find(b.members.begin(), b.members.end(), n) != b.members.end(); };
+    for (const xlf::Layer& l : g.layers) {
+        if (!member(l.name)) continue;
+        for (const std::string& i : l.inputs)
+            if (!member(i) && std::find(ins.begin(), ins.end(), i) == ins.end()) {
+                ins.push_back(i);
+                sub.inputs.push_back({i, g.shape_of(i)});
+            }
+        sub.layers.push_back(l);
+    }
+    for (const auto& [name, elems] : xlf::stored_tensors(g, b)) outs.push_back(name);
+    sub.outputs = outs;
+    return xlf::infer_shapes(sub);
+}
+
+// The block's weights out of the whole graph's (save_weights order, tensor.cpp:64-95).
+std::vector<float> block_weights(const xlf::Graph& g, const xlf::FusionBlock& b, const float* w, size_t n) {
+    std::vector<float> out;
+    size_t pos = 0;
+    for (const xlf::Layer& l : g.layers) {
+        if (l.kind != xlf::LayerKind::conv) continue;
+        const size_t k = size_t(l.conv->weight_count() + l.conv->bias_count());
+        if (pos + k > n) xlf::fail(xlf::ErrorKind::validation, "weights: " + std::to_string(n) + " values, the graph needs more");
+        if (std::find(b.members.begin(), b.members.end(), l.name) != b.members.end()) out.insert(out.end(), w + pos, w + pos + k);
+        pos += k;
+    }
+    if (pos != n) xlf::fail(xlf::ErrorKind::validation, "weights: " + std::to_string(n) + " values, the graph has " + std::to_string(pos));
+    return out;
+}
+
+}  // namespace
+
+extern "C" xlf_status xlf_block_prepare(const xlf_graph* h, const char* block_id, int part, const char* plan_text, const char* device,
+                                        int gpu, int prec, const float* weights, size_t n_weights, int max_batch, const char* options,
+                                        xlf_block** out) {
+    return guard([&] {
+        need_ptr(h, "graph"), need_ptr(block_id, "block_id"), need_ptr(weights, "weights"), need_ptr(out, "out");
+        if (part != XLF_PART_REFERENCE && part != XLF_PART_B200) throw ArgError("blocks come from the reference or b200 partition");
+        if (prec < 0 || prec > 3) throw ArgError("unknown precision");
+        const xlf::Graph& g = h->g;
+        const auto blocks = partition_blocks(g, part);
+        auto b = std::make_unique<xlf_block>();
+        b->block = find_block(blocks, block_id);
+        if (!b->block.fused()) xlf::fail(xlf::ErrorKind::internal, "run_fused_block: block is not fused");
+        const xlf::DeviceSpec dev = device_named(device ? device : "b200");
+        xlf::Knobs k = xlf::Knobs::parse(options ? options : "");
+        k.always_fuse = true;  // the caller asked for this block fused
+        k.no_s2d = true;       // inputs keep their own layout (caller-owned NHWC buffers)
+        std::string tile_src = "b200 planner";
+        int plan_th = 0, plan_tw = 0;
+        if (plan_text && *plan_text) {
+            const xlf::TilingPlan p = xlf::parse_plan(plan_text);
+            if (p.block_id != b->block.id || p.producers != b->block.producer_stage || p.consumers != b->block.consumer_stage)
+                xlf::fail(xlf::ErrorKind::validation, "plan/" + p.block_id + " does not match block " + b->block.id);
+            const xlf::TensorShape o = g.shape_of(b->block.consumer_stage.at(0));
+            const xlf::TileGeometry& geo = p.geometry;
+            if (geo.tile_h < 1 || geo.tile_w < 1 || geo.grid_h != (o.height + geo.tile_h - 1) / geo.tile_h ||
+                geo.grid_w != (o.width + geo.tile_w - 1) / geo.tile_w)
+                xlf::fail(xlf::ErrorKind::validation, "plan/" + p.block_id + ": geometry does not cover the " + std::to_string(o.height) + "x" +
+                                                          std::to_string(o.width) + " output");
+            for (const std::string& m : b->block.members) k.tiles[m] = {geo.tile_h, geo.tile_w};
+            plan_th = geo.tile_h, plan_tw = geo.tile_w;
+            tile_src = "plan (" + p.device_name + ")";
+        }
+        const xlf::Graph sub = block_graph(g, b->block, b->ins, b->outs);
+        const std::vector<float> w = block_weights(g, b->block, weights, n_weights);
+        b->e = std::make_unique<xlf::Engine>(sub, gpu, xlf::Partition(part), xlf::Precision(prec), w.data(), w.size(), max_batch, k);
+        const xlf::DevicePlan& dp = b->e->plan();
+        const bool one = dp.steps.size() == 1 && dp.steps[0].kind == xlf::StepSpec::FUSED &&
+                         dp.steps[0].layers.size() == b->block.members.size();
+        if (!one)
+            xlf::fail(xlf::ErrorKind::infeasible, "block " + b->block.id + " does not fit one B200 kernel at this precision" +
+                                                      (plan_text && *plan_text ? " and the plan's tile geometry" : "") +
+                                                      " (shared memory / TMEM); an engine runs its layers unfused");
+        // description + the reference's counter semantics that do not depend on
+        // the schedule: stored elements and 16-byte store transactions
+        // (cost_model.cpp:15-48, at `device`'s transaction size), ideal MACs
+        std::int64_t stored = 0, tx = 0;
+        for (const auto& [name, elems] : xlf::stored_tensors(g, b->block)) stored += elems, tx += xlf::transactions_for(elems, dev);
+        std::ostringstream os;
+        auto shapes = [&](const std::vector<std::string>& v) {
+            std::string s = "[";
+            for (size_t i = 0; i < v.size(); ++i) {
+                const xlf::TensorShape t = g.shape_of(v[i]);
+                s += (i ? "," : "") + std::string("{\"name\":") + jstr(v[i]) + ",\"shape\":[" + std::to_string(t.channels) + "," +
+                     std::to_string(t.height) + "," + std::to_string(t.width) + "]}";
+            }
+            return s + "]";
+        };
+        const xlf::StepSpec& s = dp.steps[0];
+        os << "{\"block\":" << jstr(b->block.id) << ",\"mode\":" << jstr(xlf::to_string(b->block.mode)) << ",\"inputs\":" << shapes(b->ins)
+           << ",\"outputs\":" << shapes(b->outs) << ",\"element_bytes\":" << b->e->element_bytes() << ",\"tile\":[" << s.tile_h << ","
+           << s.tile_w << "],\"plan_tile\":[" << plan_th << "," << plan_tw << "],\"tile_source\":" << jstr(tile_src) << ",\"device\":" << jstr(dev.name)
+           << ",\"per_image\":{\"stored_elements\":" << stored << ",\"global_store_tx\":" << tx << ",\"macs\":" << std::int64_t(s.macs)
+           << "},\"engine\":" << b->e->describe_json() << "}";
+        b->desc = os.str();
+        *out = b.release();
+    });
+}
+
+extern "C" xlf_status xlf_block_json(const xlf_block* b, char* buf, size_t cap, size_t* need) {
+    return guard([&] {
+        need_ptr(b, "block");
+        put(b->desc, buf, cap, need);
+    });
+}
+
+extern "C" xlf_status xlf_block_run(xlf_block* b, const xlf_tensor_ref* ins, int n_ins, const xlf_tensor_ref* outs, int n_outs, int batch,
+                                    void* stream) {
+    return guard([&] {
+        need_ptr(b, "block"), need_ptr(ins, "ins"), need_ptr(outs, "outs");
+        if (n_ins != int(b->ins.size()) || n_outs != int(b->outs.size()))
+            throw ArgError("block " + b->block.id + " takes " + std::to_string(b->ins.size()) + " input(s) and " + std::to_string(b->outs.size()) +
+                           " output(s)");
+        const cudaStream_t st = static_cast<cudaStream_t>(stream);
+        std::lock_guard<std::mutex> lock(b->mu);
+        xlf::cuda_check(cudaSetDevice(b->e->device()), "cudaSetDevice");
+        if (!b->done) xlf::cuda_check(cudaEventCreateWithFlags(&b->done, cudaEventDisableTiming), "cudaEventCreate");
+        if (b->ran && b->last != st) xlf::cuda_check(cudaStreamWaitEvent(st, b->done, 0), "cudaStreamWaitEvent");
+        std::vector<xlf::Engine::External> ext;
+        for (int i = 0; i < n_ins + n_outs; ++i) {
+            const xlf_tensor_ref& r = i < n_ins ? ins[i] : outs[i - n_ins];
+            const std::string& name = i < n_ins ? b->ins[size_t(i)] : b->outs[size_t(i - n_ins)];
+            need_ptr(r.data, "tensor data");
+            if (r.layout == XLF_LAYOUT_NHWC) ext.push_back({name, r.data, r.cstride, r.coff});
+            else if (r.layout != XLF_LAYOUT_NCHW_F32) throw ArgError("unknown layout for '" + name + "'");
+        }
+        for (int i = 0; i < n_ins; ++i)
+            if (ins[i].layout == XLF_LAYOUT_NCHW_F32) b->e->set_input_nchw(b->ins[size_t(i)], static_cast<const float*>(ins[i].data), batch, st);
+        b->e->forward_external(ext, batch, st);
+        for (int i = 0; i < n_outs; ++i)
+            if (outs[i].layout == XLF_LAYOUT_NCHW_F32) b->e->read_output_nchw(b->outs[size_t(i)], static_cast<float*>(outs[i].data), batch, st);
+        xlf::cuda_check(cudaEventRecord(b->done, st), "cudaEventRecord");
+        b->last = st, b->ran = true;
+    });
+}
+
+extern "C" void xlf_block_destroy(xlf_block* b) { delete b; }

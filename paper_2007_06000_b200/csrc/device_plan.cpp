@@ -346,13 +346,13 @@ double macs_per_output(const Layer& l) {
 
 // Tile choice: minimise modelled time = waves x per-CTA work / occupancy
 // benefit, with per-CTA work including halo recompute and partial-tile waste.
-bool choose_tile_at(const Graph& g, StepSpec& s, int batch_hint, int smem_budget);
+bool choose_tile_at(const Graph& g, StepSpec& s, int batch_hint, int smem_budget, const Knobs& k);
 
 // Pool-only steps whose full-channel region never fits shared memory (a
 // global average pool over 13x13x1000) are tiled over channels as well.
-bool choose_tile(const Graph& g, StepSpec& s, int batch_hint, int smem_budget) {
+bool choose_tile(const Graph& g, StepSpec& s, int batch_hint, int smem_budget, const Knobs& k) {
     s.ctile = 0;
-    if (choose_tile_at(g, s, batch_hint, smem_budget)) return true;
+    if (choose_tile_at(g, s, batch_hint, smem_budget, k)) return true;
     bool pools = s.inputs.size() == 1;
     for (const OpSpec& op : s.ops) pools &= op.stage == 1 && g.find_layer(op.layer)->kind == LayerKind::pool;
     if (!pools) return false;
@@ -360,18 +360,21 @@ bool choose_tile(const Graph& g, StepSpec& s, int batch_hint, int smem_budget) {
     for (int ct = C - 4; ct >= 4; ct -= 4) {
         if (C % ct) continue;
         s.ctile = ct;
-        if (choose_tile_at(g, s, batch_hint, smem_budget)) return true;
+        if (choose_tile_at(g, s, batch_hint, smem_budget, k)) return true;
     }
     s.ctile = 0;
     return false;
 }
 
-bool choose_tile_at(const Graph& g, StepSpec& s, int batch_hint, int smem_budget) {
+bool choose_tile_at(const Graph& g, StepSpec& s, int batch_hint, int smem_budget, const Knobs& k) {
     double best = 1e300;
     int bh = 0, bw = 0, bsm = 0;
-    const int lim_h = std::min(s.out_h, 32), lim_w = std::min(s.out_w, 32);
+    int fh = 0, fw = 0;
+    const bool forced = k.forced_tile(s, &fh, &fw);
+    const int lim_h = forced ? fh : std::min(s.out_h, 32), lim_w = forced ? fw : std::min(s.out_w, 32);
     for (int th = 1; th <= lim_h; ++th)
         for (int tw = 1; tw <= lim_w; ++tw) {
+            if (forced && (fh % th || fw % tw)) continue;  // sub-tiles of the plan's tile (see Knobs::tiles)
             FusedParams fp;
             const long long sm = layout_step(g, s, th, tw, &fp);
             if (sm < 0 || sm > smem_budget) continue;
@@ -393,7 +396,8 @@ bool choose_tile_at(const Graph& g, StepSpec& s, int batch_hint, int smem_budget
             const double ctas = double(fp.grid_h) * fp.grid_w * fp.cgroups * std::max(batch_hint, 1);
             const int occ = std::max(1, std::min(8, int((228 * 1024) / (sm + 1024))));
             const double waves = std::ceil(ctas / (148.0 * occ));
-            const double t = waves * work * occ / std::min(double(occ), 2.0) + 2000.0 * waves;
+            double t = waves * work * occ / std::min(double(occ), 2.0) + 2000.0 * waves;
+            if (forced) t = -double(th) * tw;  // the plan's tile, else its largest feasible sub-tile
             if (t < best * 0.999 || (t <= best * 1.001 && long(th) * tw > long(bh) * bw)) best = t, bh = th, bw = tw, bsm = int(sm);
         }
     if (!bh) return false;
@@ -440,6 +444,18 @@ void fill_stats(const Graph& g, const DevicePlan& plan, StepSpec& s) {
     }
 }
 
+bool Knobs::forced_tile(const StepSpec& s, int* th, int* tw) const {
+    if (tiles.empty()) return false;
+    for (const std::string& l : s.layers) {
+        auto it = tiles.find(l);
+        if (it != tiles.end()) {
+            *th = it->second.first, *tw = it->second.second;
+            return true;
+        }
+    }
+    return false;
+}
+
 Knobs Knobs::parse(const std::string& text) {
     Knobs k;
     size_t pos = 0;
@@ -472,10 +488,23 @@ Knobs Knobs::parse(const std::string& text) {
         else if (key == "tsets") k.tsets = int(need_num());
         else if (key == "ctas") k.ctas = int(need_num());
         else if (key == "pdl") k.pdl = need_num() != 0;
+        else if (key == "no_s2d") k.no_s2d = need_num() != 0;
         else if (key == "trace") k.trace = int(need_num());
         else if (key == "tune_verbose") k.tune_verbose = need_num() != 0;
         else if (key == "e2e_chunks") k.e2e_chunks = std::max(1, int(need_num()));
         else if (key == "e2e_ramp") k.e2e_ramp = need_num() != 0;
+        else if (key == "tile") {
+            std::stringstream ss(val);
+            std::string it;
+            while (std::getline(ss, it, ';')) {
+                const size_t c = it.rfind(':'), x = it.rfind('x');
+                int h = 0, w = 0;
+                if (c == std::string::npos || x == std::string::npos || x < c ||
+                    std::sscanf(it.c_str() + c + 1, "%dx%d", &h, &w) != 2 || h < 1 || w < 1)
+                    fail(ErrorKind::validation, "options: tile entries are <layer>:<h>x<w>, got '" + it + "'");
+                k.tiles[it.substr(0, c)] = {h, w};
+            }
+        }
         else fail(ErrorKind::validation, "options: unknown key '" + key + "'");
     }
     return k;
@@ -490,7 +519,7 @@ DevicePlan plan_device(const Graph& g, Partition part, int batch_hint, int smem_
     const bool tc = tc_es != 0;
     const int cpad = tc_es == 2 ? 8 : 4;  // channel padding of HBM tensors (16 bytes)
     auto tile = [&](StepSpec& st) {
-        return tc ? choose_tile_tc(g, st, batch_hint, std::min(smem_budget, kSmemBudgetTc), tc_es, knobs) : choose_tile(g, st, batch_hint, smem_budget);
+        return tc ? choose_tile_tc(g, st, batch_hint, std::min(smem_budget, kSmemBudgetTc), tc_es, knobs) : choose_tile(g, st, batch_hint, smem_budget, knobs);
     };
     if (part == Partition::reference) plan.blocks = detect_fusion_blocks(g);
     else if (part == Partition::b200) plan.blocks = detect_fusion_blocks_b200(g);

@@ -39,10 +39,19 @@ struct Knobs {
     int tsets = 0;               // force 1 / 2 accumulator sets
     int ctas = 0;                // cap on resident CTAs per SM
     bool pdl = true;             // programmatic dependent launch between steps
+    bool no_s2d = false;         // keep a stride-2 first conv on its own input (no space-to-depth rewrite)
     int trace = 0;               // 1: phase stamps of a steady tile, 2: tile end stamps
     bool tune_verbose = false;   // autotune prints every timing to stderr
     int e2e_chunks = 4;          // run_host pipeline depth
     bool e2e_ramp = false;       // run_host: half-size first / last chunk
+    // tile=<layer>:<h>x<w>;...: the step executing <layer> runs at this output
+    // tile (a reference TilingPlan's geometry, xlf_block_prepare) or, when the
+    // B200 kernel cannot hold it, at its largest feasible exact sub-tile (h' | h,
+    // w' | w: every plan tile is a union of kernel tiles; results do not depend
+    // on the tiling)
+    std::map<std::string, std::pair<int, int>> tiles;
+    // The forced tile of step `s` (true), from any of its layers.
+    bool forced_tile(const struct StepSpec& s, int* th, int* tw) const;
     // Throws ErrorKind::validation on an unknown key or malformed value.
     static Knobs parse(const std::string& text);
 };

@@ -483,13 +483,16 @@ std::vector<BCandidate> candidates_tc(const Graph& g, const StepSpec& s, int bat
     const WMode wmodes[] = {{1, 3, kChunkBytes}, {0, 3, kChunkBytes}, {0, 6, kChunkBytes}, {0, 8, kChunkBytes},
                             {0, 3, 2 * kChunkBytes}, {0, 4, 2 * kChunkBytes}, {0, 2, 4 * kChunkBytes}, {0, 3, 4 * kChunkBytes}};
     std::vector<BCandidate> out;
+    int fh = 0, fw = 0;
+    const bool forced = k.forced_tile(s, &fh, &fw);  // a reference plan's geometry
     BParams* P = new BParams;
     for (int ew : {8, 4})
     for (int ts = 1; ts <= 2; ++ts)
     for (int nxb = ts; nxb <= 2; ++nxb)
         for (const WMode& wm : wmodes) {
-            for (int th = 1; th <= std::min(s.out_h, 32); ++th)
-                for (int tw = 1; tw <= std::min(s.out_w, 32); ++tw) {
+            for (int th = 1; th <= (forced ? fh : std::min(s.out_h, 32)); ++th)
+                for (int tw = 1; tw <= (forced ? fw : std::min(s.out_w, 32)); ++tw) {
+                    if (forced && (fh % th || fw % tw)) continue;  // the plan's tile or an exact sub-tile
                     const long long sm = layout_tc(g, s, th, tw, P, nxb, wm.wres, wm.slots, ts, wm.chunk, es, k);
                     if (sm < 0 || sm > smem_budget) continue;
                     if (wm.wres && !P->wres) continue;  // no MMA op: the ring/resident choice is moot
@@ -538,6 +541,14 @@ std::vector<BCandidate> candidates_tc(const Graph& g, const StepSpec& s, int bat
         if (b.model < a.model * 0.999) return false;
         return long(a.th) * a.tw > long(b.th) * b.tw;  // ties: the larger tile
     });
+    if (forced && !out.empty()) {  // the plan's tile, else its largest feasible sub-tile (any staging / weight mode)
+        long best = 0;
+        for (const BCandidate& c : out) best = std::max(best, long(c.th) * c.tw);
+        std::vector<BCandidate> keep;
+        for (const BCandidate& c : out)
+            if (long(c.th) * c.tw == best) keep.push_back(c);
+        out.swap(keep);
+    }
     return out;
 }
 

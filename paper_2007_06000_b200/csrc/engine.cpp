@@ -173,7 +173,7 @@ Engine::Engine(const Graph& g, int device, Partition part, Precision prec, const
     std::vector<float> wcopy;
     if (tc) {
         wcopy.assign(weights, weights + nweights);
-        s2d_ = rewrite_s2d(g_, wcopy);
+        s2d_ = !knobs_.no_s2d && rewrite_s2d(g_, wcopy);
         if (s2d_) weights = wcopy.data(), nweights = wcopy.size();
     }
     cuda_check(cudaSetDevice(device), "cudaSetDevice");
@@ -300,9 +300,9 @@ std::string Engine::autotune(int batch, int reps, int topk) {
     cuda_check(cudaSetDevice(device_), "cudaSetDevice");
     cudaStream_t st;
     cuda_check(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking), "cudaStreamCreate(tune)");
-    // captured forwards hold the current descriptors, which are replaced below
-    for (auto& [b, ge] : graphs_) cudaGraphExecDestroy(ge);
-    graphs_.clear();
+    // captured forwards and external-address descriptors hold the current
+    // configurations, which are replaced below
+    drop_derived();
     cudaEvent_t e0, e1;
     cuda_check(cudaEventCreate(&e0), "cudaEventCreate"), cuda_check(cudaEventCreate(&e1), "cudaEventCreate");
     std::ostringstream js;
@@ -439,9 +439,8 @@ void Engine::apply_tuning(const std::string& js) {
         t.smem_bytes = int(sm);
         todo.emplace_back(i, t);
     }
-    // captured forwards hold the current descriptors
-    for (auto& [b, ge] : graphs_) cudaGraphExecDestroy(ge);
-    graphs_.clear();
+    // captured forwards and external-address descriptors hold the current configurations
+    drop_derived();
     std::vector<std::unique_ptr<BParams>> built;
     for (auto& [i, t] : todo) built.push_back(build_bparams(t));
     for (size_t k = 0; k < todo.size(); ++k) {
@@ -450,6 +449,15 @@ void Engine::apply_tuning(const std::string& js) {
         plan_.steps[i] = todo[k].second;
         bparams_[i] = std::move(built[k]);
     }
+}
+
+void Engine::drop_derived() {
+    for (auto& [b, ge] : graphs_) cudaGraphExecDestroy(ge);
+    graphs_.clear();
+    for (auto& [key, x] : ext_sets_)
+        for (auto& P : x->bp)
+            if (P) retired_.push_back(const_cast<void*>(P->dev_copy));  // a queued launch may still read it
+    ext_sets_.clear();
 }
 
 Engine::~Engine() {
@@ -464,6 +472,9 @@ Engine::~Engine() {
     cudaFree(staging_);
     if (out_staging_) cudaFree(out_staging_);
     for (auto& [id, b] : gap_parts_) cudaFree(b.first);
+    for (auto& [key, x] : ext_sets_)
+        for (auto& P : x->bp)
+            if (P) cudaFree(const_cast<void*>(P->dev_copy));
     for (void* p : retired_) cudaFree(p);
     if (copy_in_) {
         cudaStreamDestroy(copy_in_), cudaStreamDestroy(copy_out_);
@@ -644,6 +655,77 @@ void Engine::forward(int batch, cudaStream_t st, bool use_graph) {
         it = graphs_.emplace(batch, exec).first;
     }
     cuda_check(cudaGraphLaunch(it->second, st), "graph launch");
+}
+
+// Caller-owned tensors: the allocation of each named tensor is replaced by the
+// caller's address (the tensor must own its allocation: a concat view shares
+// it with its siblings), the descriptors of every fused step are rebuilt
+// against the substituted table once per distinct address set, and the steps
+// are launched with the substituted table in place.
+void Engine::forward_external(const std::vector<External>& ext, int batch, cudaStream_t st) {
+    if (batch < 1 || batch > max_batch_) fail(ErrorKind::validation, "batch out of range");
+    cuda_check(cudaSetDevice(device_), "cudaSetDevice");
+    const int cpc = 16 / esz_;
+    std::string key;
+    for (const External& x : ext) {
+        const TensorSlot& t = slot(x.name);
+        if (s2d_ && x.name == g_.inputs[0].name)
+            fail(ErrorKind::validation, "input '" + x.name + "' is read in space-to-depth layout by this plan; pass it as NCHW");
+        const int cp = (t.C + cpc - 1) / cpc * cpc;
+        if (!x.ptr || reinterpret_cast<uintptr_t>(x.ptr) % 16)
+            fail(ErrorKind::validation, "tensor '" + x.name + "': NHWC address must be non-NULL and 16-byte aligned");
+        if (x.cstride % cpc || x.coff % cpc || x.coff < 0 || x.coff + cp > x.cstride)
+            fail(ErrorKind::validation, "tensor '" + x.name + "': channel pitch " + std::to_string(x.cstride) + " / offset " +
+                                            std::to_string(x.coff) + " must be multiples of " + std::to_string(cpc) +
+                                            " elements (16 bytes) holding " + std::to_string(cp) + " channels");
+        int sharing = 0;
+        for (const auto& [n, u] : plan_.tensors) sharing += u.materialized && u.alloc == t.alloc;
+        if (sharing != 1) fail(ErrorKind::validation, "tensor '" + x.name + "' shares its allocation (a concat view) and cannot be bound alone");
+        key += x.name + "@" + std::to_string(reinterpret_cast<uintptr_t>(x.ptr)) + "/" + std::to_string(x.cstride) + "/" +
+               std::to_string(x.coff) + ";";
+    }
+    auto it = ext_sets_.find(key);
+    if (it == ext_sets_.end()) {
+        auto set = std::make_unique<ExtSet>();
+        set->allocs = allocs_;
+        set->tensors = plan_.tensors;
+        for (const External& x : ext) {
+            TensorSlot& t = set->tensors.at(x.name);
+            set->allocs[size_t(t.alloc)] = static_cast<float*>(x.ptr);
+            t.cstride = x.cstride, t.coff = x.coff;
+        }
+        std::swap(allocs_, set->allocs), std::swap(plan_.tensors, set->tensors);
+        try {
+            set->bp.resize(plan_.steps.size());
+            set->fp.resize(plan_.steps.size());
+            for (size_t i = 0; i < plan_.steps.size(); ++i) {
+                const StepSpec& s = plan_.steps[i];
+                if (s.kind != StepSpec::FUSED) continue;
+                if (tc_es_) set->bp[i] = build_bparams(s);
+                else set->fp[i] = make_params(g_, plan_, s, allocs_, weights_);
+            }
+        } catch (...) {
+            std::swap(allocs_, set->allocs), std::swap(plan_.tensors, set->tensors);
+            for (auto& P : set->bp)
+                if (P) cudaFree(const_cast<void*>(P->dev_copy));
+            throw;
+        }
+        std::swap(allocs_, set->allocs), std::swap(plan_.tensors, set->tensors);
+        it = ext_sets_.emplace(key, std::move(set)).first;
+    }
+    ExtSet& x = *it->second;
+    // launch with the substituted table (restored on every exit path)
+    struct Swap {
+        Engine* e;
+        ExtSet* x;
+        void flip() {
+            std::swap(e->allocs_, x->allocs), std::swap(e->plan_.tensors, x->tensors);
+            std::swap(e->bparams_, x->bp), std::swap(e->params_, x->fp);
+        }
+        ~Swap() { flip(); }
+    } sw{this, &x};
+    sw.flip();
+    for (size_t i = 0; i < plan_.steps.size(); ++i) launch_step(i, batch, st);
 }
 
 void Engine::read_output_nchw(const std::string& name, float* d, int batch, cudaStream_t st) {

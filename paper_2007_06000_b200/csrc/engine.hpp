@@ -40,6 +40,18 @@ public:
     bool range_capable() const;
     // One step only (per-block timing / run_fused_block).
     void run_step(int index, int batch, cudaStream_t st);
+    // Caller-owned NHWC tensors (xlf_block_run): every step reads / writes the
+    // named graph inputs and materialised tensors at external device addresses
+    // (element type of the engine's HBM layout, `cstride` elements per pixel,
+    // the tensor at channel `coff`).  Descriptors for a set of addresses are
+    // built once and cached; no CUDA graph.
+    struct External {
+        std::string name;
+        void* ptr;
+        int cstride, coff;
+    };
+    void forward_external(const std::vector<External>& ext, int batch, cudaStream_t st);
+    int element_bytes() const { return esz_; }
     // NHWC arena -> NCHW fp32.
     void read_output_nchw(const std::string& name, float* d_nchw, int batch, cudaStream_t st);
     // C*H*W of a readable tensor (throws for fused intermediates / rewritten inputs).
@@ -65,6 +77,7 @@ public:
 
 private:
     void launch_step(size_t i, int batch, cudaStream_t st);
+    void drop_derived();  // CUDA graphs + external-address descriptors of the current configurations
     std::unique_ptr<struct BParams> build_bparams(const StepSpec& s);
     void launch_tc_step(size_t i, int n0, int count, cudaStream_t st);
     const TensorSlot& slot(const std::string& n) const;
@@ -98,6 +111,13 @@ private:
     float* out_staging_ = nullptr;
     std::map<std::string, std::pair<float*, size_t>> gap_parts_;  // conv+gap steps: per-tile partial sums
     std::vector<void*> retired_;                                  // outgrown buffers, freed with the engine
+    struct ExtSet {  // descriptors of one set of caller-owned addresses
+        std::vector<float*> allocs;
+        std::map<std::string, TensorSlot> tensors;
+        std::vector<std::unique_ptr<struct BParams>> bp;
+        std::vector<struct FusedParams> fp;
+    };
+    std::map<std::string, std::unique_ptr<ExtSet>> ext_sets_;
 };
 
 std::vector<float> seeded_weights(const Graph& g, uint64_t seed);  // tensor.cpp:42-62 semantics

@@ -68,11 +68,12 @@ def test_run_fused_block_and_simulate_graph_api():
     w = X.seeded_weights(g, 42)
     x = O.seeded_batch(og, 42, 2)
     blk = [b for b in X.detect_fusion_blocks(g) if b.fused()][0]
-    outs = X.run_fused_block(g, blk, {"data": torch.from_numpy(x).cuda()}, w)
+    values = {"data": torch.from_numpy(x).cuda()}
+    written = X.run_fused_block(g, blk, values, w)
     ref = O.run_batch(og, x, O.seeded_weights(og, 42), ["fire_expand1", "fire_expand3"])
-    assert set(outs) == {"fire_expand1", "fire_expand3"}
-    for k in outs:
-        assert np.array_equal(outs[k].cpu().numpy(), ref[k])
+    assert set(written) == {"fire_expand1", "fire_expand3"}
+    for k in written:
+        assert np.array_equal(values[k].cpu().numpy(), ref[k])
     sim = X.simulate_graph(g, torch.from_numpy(x).cuda(), w, "reference", "fp32_exact")
     full = O.run_batch(og, x, O.seeded_weights(og, 42), og.outputs)
     assert np.array_equal(sim["fire_concat"].cpu().numpy(), full["fire_concat"])

@@ -212,3 +212,18 @@ def test_b200_cost_based_fusion_decisions():
     # the fp32 planner is unaffected (its kernels stage no weights)
     g = X.load_graph(X.graph_path("inc3a"))
     assert not any(s["layers"] == ["b3"] for s in X.device_plan(g, "b200", 64, "fp32")["steps"])
+
+
+def test_b200_device_document_round_trips():
+    """paper_2007_06000_b200/devices/b200.device is serialize_device(b200_spec)
+    in the reference's format (device.cpp:38-90); parsing it gives it back, and
+    the reference planner's plan_tiling accepts it as a device."""
+    path = os.path.join(X.DEVICES, "b200.device")
+    text = open(path).read()
+    assert X.device_document("b200") in text
+    assert X.device_document(text) == X.device_document("b200")
+    g = X.load_graph(X.graph_path("b1"))
+    b = [b for b in X.detect_fusion_blocks(g) if b.fused()][0]
+    h, w = g.shape_of(b.consumer_stage[0])[1:]
+    plan = X.plan_tiling(g, b.id, (11, 11), (-(-h // 11), -(-w // 11)), text)
+    assert "b200" in plan
