@@ -341,16 +341,28 @@ def main():
 
     import paper_2007_06000_b200 as X
 
+    # one rank per GPU; with fewer GPUs than ranks (a dry run of the N-rank
+    # path on a 1-GPU box) ranks share devices and the bookkeeping collectives
+    # run on gloo -- the line says so in "backend"
+    ngpu = torch.cuda.device_count()
+    local = local % max(1, ngpu)
     torch.cuda.set_device(local)
+    backend = None
     if world > 1:
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        backend = "nccl" if ngpu >= world else "gloo"
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group("gloo")
+    coll_dev = "cuda" if backend != "gloo" else "cpu"
 
     g = X.load_graph(X.graph_path("squeezenet11"))
     w = X.seeded_weights(g, 42)
     B = PER_GPU_BATCH
     prec = args.precision
-    first = rank * B  # rank r's shard: images [r*B, (r+1)*B) of the seeded stream (no exchange)
+    from paper_2007_06000_b200 import dist as D
+    first, _ = D.shard(rank, world, B)  # rank r's shard: images [r*B, (r+1)*B) of the seeded stream (no exchange)
     e, tune = make_engine(X, g, w, "b200", prec, B, local, tune=not args.no_tune, first_image=first)
     nsteps = len(e.steps)
     st = torch.cuda.current_stream()
@@ -362,7 +374,7 @@ def main():
         torch.cuda.synchronize()
 
     def max_ms(ms):
-        t = torch.tensor([ms], device="cuda", dtype=torch.float64)
+        t = torch.tensor([ms], device=coll_dev, dtype=torch.float64)
         if world > 1:
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
@@ -396,7 +408,7 @@ def main():
     # --- optional final gather of the logits to rank 0 (NCCL), timed apart
     gather_ms = None
     if world > 1:
-        lt = torch.from_numpy(logits).cuda()
+        lt = torch.from_numpy(logits).to(coll_dev)
         parts = [torch.empty_like(lt) for _ in range(world)]
         barrier()
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -529,6 +541,8 @@ def main():
             "gpu_launches": args.steps * e.launches_per_forward,
             "clocks": clocks,
             "gather_ms": gather_ms,
+            "backend": backend if world > 1 else None,
+            "devices_visible": ngpu,
             "blocks": blocks,
             "autotune": tune,
         }

@@ -195,6 +195,32 @@ xlf_status xlf_block_run(xlf_block* b, const xlf_tensor_ref* ins, int n_ins, con
                          void* stream);
 void xlf_block_destroy(xlf_block* b);
 
+/* ---- several GPUs of one node (batch-sharded simulate_graph,
+ *      fused_exec.cpp:313-349) ------------------------------ */
+
+typedef struct xlf_multi xlf_multi;
+
+/* Images [*first, *first + *count) of device slot `slot` when `batch` images
+ * are split over n devices: contiguous, sizes differ by at most one (the first
+ * batch % n slots take one more); n*B images give slot k exactly [k*B, (k+1)*B). */
+xlf_status xlf_shard(int batch, int n_devices, int slot, int* first, int* count);
+/* One engine per listed device (weights replicated), each driven by its own
+ * host worker thread and stream; no collective on the data path. */
+xlf_status xlf_multi_create(const xlf_graph* g, const int* devices, int n_devices, int partition, int precision, const float* weights,
+                            size_t n_weights, int max_batch_per_device, const char* options, xlf_multi** out);
+void xlf_multi_destroy(xlf_multi* m);
+/* Every device tunes its engine (concurrently); see xlf_engine_autotune. */
+xlf_status xlf_multi_autotune(xlf_multi* m, int batch_per_device, int reps, int topk);
+/* End to end from host memory over all devices (xlf_shard ranges of `batch`):
+ * each device copies in its images, runs them and writes its slice of tensor
+ * `name` into h_out (NCHW).  Synchronous.  ms_per_device (n values, may be
+ * NULL): each device's wall time. */
+xlf_status xlf_multi_run_host(xlf_multi* m, const float* h_in, int batch, const char* name, float* h_out, double* ms_per_device);
+/* Device-resident throughput: device k generates images [k*B, (k+1)*B) of
+ * SeededStream(seed) (B = batch_per_device) and times `steps` forwards after
+ * `warmup` (CUDA events on its stream); ms_per_device[k] = ms per forward. */
+xlf_status xlf_multi_time_seeded(xlf_multi* m, uint64_t seed, int batch_per_device, int steps, int warmup, double* ms_per_device);
+
 #ifdef __cplusplus
 }
 #endif

@@ -5,7 +5,7 @@ include/xlfuse_b200.h; this package is the Python face of that ABI.
 """
 import os
 
-from .api import (Block, Engine, FusionBlock, Graph, ModeResult, XlfError, block_assignment_report, classify_mode,  # noqa: F401
+from .api import (Block, Engine, MultiEngine, shard_range, FusionBlock, Graph, ModeResult, XlfError, block_assignment_report, classify_mode,  # noqa: F401
                   detect_fusion_blocks, device_document, device_plan, load_graph, parse_graph, plan_tiling, run_fused_block, seeded_weights,
                   simulate_graph, store_transactions)
 

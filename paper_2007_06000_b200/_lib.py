@@ -20,6 +20,7 @@ SYMBOLS = [
     "xlf_engine_launches_per_forward", "xlf_engine_set_input", "xlf_engine_set_input_named", "xlf_engine_set_input_seeded", "xlf_engine_forward",
     "xlf_engine_run_step", "xlf_engine_read", "xlf_engine_run_host", "xlf_engine_autotune", "xlf_engine_tune_report", "xlf_engine_apply_tuning",
     "xlf_engine_trace", "xlf_block_prepare", "xlf_block_json", "xlf_block_run", "xlf_block_destroy",
+    "xlf_shard", "xlf_multi_create", "xlf_multi_destroy", "xlf_multi_autotune", "xlf_multi_run_host", "xlf_multi_time_seeded",
 ]
 
 
@@ -96,6 +97,14 @@ def lib() -> ctypes.CDLL:
     L.xlf_block_run.argtypes = [vp, ctypes.POINTER(TensorRef), ctypes.c_int, ctypes.POINTER(TensorRef), ctypes.c_int, ctypes.c_int, vp]
     L.xlf_block_destroy.argtypes = [vp]
     L.xlf_block_destroy.restype = None
+    ip, dp = ctypes.POINTER(ctypes.c_int), ctypes.POINTER(ctypes.c_double)
+    L.xlf_shard.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int, ip, ip]
+    L.xlf_multi_create.argtypes = [vp, ip, ctypes.c_int, ctypes.c_int, ctypes.c_int, f32p, sz, ctypes.c_int, c_char_pp, ctypes.POINTER(vp)]
+    L.xlf_multi_destroy.argtypes = [vp]
+    L.xlf_multi_destroy.restype = None
+    L.xlf_multi_autotune.argtypes = [vp, ctypes.c_int, ctypes.c_int, ctypes.c_int]
+    L.xlf_multi_run_host.argtypes = [vp, f32p, ctypes.c_int, c_char_pp, f32p, dp]
+    L.xlf_multi_time_seeded.argtypes = [vp, ctypes.c_uint64, ctypes.c_int, ctypes.c_int, ctypes.c_int, dp]
     _LIB = L
     return L
 

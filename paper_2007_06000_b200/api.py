@@ -272,6 +272,57 @@ class Engine:
         return [n for n, t in self.info["plan"]["tensors"].items() if t["materialized"]]
 
 
+def shard_range(batch: int, n: int, k: int):
+    """(first, count) of device slot k of n for `batch` images (xlf_shard)."""
+    f, c = ctypes.c_int(), ctypes.c_int()
+    check(lib().xlf_shard(batch, n, k, ctypes.byref(f), ctypes.byref(c)))
+    return f.value, c.value
+
+
+class MultiEngine:
+    """Several GPUs of one node in one process (xlf_multi_*): one engine per
+    device, batch-sharded, one host worker thread + stream per device."""
+
+    def __init__(self, g: Graph, weights: np.ndarray, devices, partition: str = "b200", precision: str = "bf16",
+                 max_batch_per_device: int = 1, options=None):
+        if partition not in PARTITIONS or precision not in PRECISIONS:
+            raise XlfError(8, f"unknown partition / precision {partition!r} / {precision!r}")
+        self.graph, self.devices = g, list(devices)
+        w = np.ascontiguousarray(weights, np.float32)
+        dev = (ctypes.c_int * len(self.devices))(*self.devices)
+        h = ctypes.c_void_p()
+        check(lib().xlf_multi_create(g._h, dev, len(self.devices), PARTITIONS[partition], PRECISIONS[precision],
+                                     w.ctypes.data_as(ctypes.POINTER(ctypes.c_float)), w.size, max_batch_per_device, _options(options),
+                                     ctypes.byref(h)))
+        self._h = h
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h and _lib._LIB is not None:
+            lib().xlf_multi_destroy(h)
+            self._h = None
+
+    def autotune(self, batch_per_device: int = 0, reps: int = 3, topk: int = 3):
+        check(lib().xlf_multi_autotune(self._h, batch_per_device, reps, topk))
+
+    def run_host(self, x: np.ndarray, name: str):
+        """(outputs NCHW, per-device ms): the batch split by shard_range."""
+        shape = self.graph.inputs[0][1]
+        if not isinstance(x, np.ndarray) or x.dtype != np.float32 or x.ndim != 4 or tuple(x.shape[1:]) != tuple(shape):
+            raise XlfError(8, f"run_host input must be a float32 [batch, {shape[0]}, {shape[1]}, {shape[2]}] array")
+        x = np.ascontiguousarray(x)
+        out = np.empty((x.shape[0],) + tuple(self.graph.shape_of(name)), np.float32)
+        ms = (ctypes.c_double * len(self.devices))()
+        f32p = ctypes.POINTER(ctypes.c_float)
+        check(lib().xlf_multi_run_host(self._h, x.ctypes.data_as(f32p), x.shape[0], name.encode(), out.ctypes.data_as(f32p), ms))
+        return out, list(ms)
+
+    def time_seeded(self, seed: int, batch_per_device: int, steps: int = 10, warmup: int = 3):
+        ms = (ctypes.c_double * len(self.devices))()
+        check(lib().xlf_multi_time_seeded(self._h, seed, batch_per_device, steps, warmup, ms))
+        return list(ms)
+
+
 def simulate_graph(g: Graph, x, weights: np.ndarray, partition: str = "b200", precision: str = "fp32_exact",
                    names=None):
     """Runs the whole schedule on the GPU (fused_exec.cpp:313-349 semantics);

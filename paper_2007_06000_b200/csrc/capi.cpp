@@ -16,6 +16,7 @@
 #include "engine.hpp"
 #include "fusion.hpp"
 #include "graph.hpp"
+#include "multi.hpp"
 #include "tiling.hpp"
 
 struct xlf_graph {
@@ -555,3 +556,55 @@ extern "C" xlf_status xlf_block_run(xlf_block* b, const xlf_tensor_ref* ins, int
 }
 
 extern "C" void xlf_block_destroy(xlf_block* b) { delete b; }
+
+// ---------------------------------------------------------------- several GPUs
+struct xlf_multi {
+    std::unique_ptr<xlf::MultiEngine> m;
+};
+
+extern "C" xlf_status xlf_shard(int batch, int n, int slot, int* first, int* count) {
+    return guard([&] {
+        need_ptr(first, "first"), need_ptr(count, "count");
+        xlf::shard_range(batch, n, slot, first, count);
+    });
+}
+
+extern "C" xlf_status xlf_multi_create(const xlf_graph* h, const int* devices, int n, int part, int prec, const float* weights, size_t nw,
+                                       int max_batch_per_device, const char* options, xlf_multi** out) {
+    return guard([&] {
+        need_ptr(h, "graph"), need_ptr(devices, "devices"), need_ptr(weights, "weights"), need_ptr(out, "out");
+        if (part < 0 || part > 2) throw ArgError("unknown partition");
+        if (prec < 0 || prec > 3) throw ArgError("unknown precision");
+        if (n < 1 || n > 64) throw ArgError("n_devices must be 1..64");
+        const xlf::Knobs k = xlf::Knobs::parse(options ? options : "");
+        auto m = std::make_unique<xlf_multi>();
+        m->m = std::make_unique<xlf::MultiEngine>(h->g, std::vector<int>(devices, devices + n), xlf::Partition(part), xlf::Precision(prec),
+                                                  weights, nw, max_batch_per_device, k);
+        *out = m.release();
+    });
+}
+
+extern "C" void xlf_multi_destroy(xlf_multi* m) { delete m; }
+
+extern "C" xlf_status xlf_multi_autotune(xlf_multi* m, int batch_per_device, int reps, int topk) {
+    return guard([&] {
+        need_ptr(m, "multi");
+        m->m->autotune(batch_per_device, reps, topk);
+    });
+}
+
+extern "C" xlf_status xlf_multi_run_host(xlf_multi* m, const float* h_in, int batch, const char* name, float* h_out, double* ms) {
+    return guard([&] {
+        need_ptr(m, "multi"), need_ptr(h_in, "input"), need_ptr(name, "name"), need_ptr(h_out, "output");
+        const std::vector<double> t = m->m->run_host(h_in, batch, name, h_out);
+        if (ms) std::copy(t.begin(), t.end(), ms);
+    });
+}
+
+extern "C" xlf_status xlf_multi_time_seeded(xlf_multi* m, uint64_t seed, int batch_per_device, int steps, int warmup, double* ms) {
+    return guard([&] {
+        need_ptr(m, "multi"), need_ptr(ms, "ms");
+        const std::vector<double> t = m->m->time_seeded(seed, batch_per_device, steps, warmup);
+        std::copy(t.begin(), t.end(), ms);
+    });
+}

@@ -52,6 +52,7 @@ public:
     };
     void forward_external(const std::vector<External>& ext, int batch, cudaStream_t st);
     int element_bytes() const { return esz_; }
+    size_t user_input_elements() const { return size_t(in_shape_.elements()); }  // C*H*W of input 0 as the user passes it
     // NHWC arena -> NCHW fp32.
     void read_output_nchw(const std::string& name, float* d_nchw, int batch, cudaStream_t st);
     // C*H*W of a readable tensor (throws for fused intermediates / rewritten inputs).

@@ -6,15 +6,22 @@ Inference is embarrassingly parallel over images: rank r of W owns images
 collective runs on the data path.  The only collectives are bookkeeping:
 the max-over-ranks step time, and the optional final gather of the logits
 to rank 0 (NCCL on GPUs, gloo in the CPU tests).
+
+Two ways to run N GPUs: one process per GPU (torchrun; bench.py, this module
+for the bookkeeping) or one process for all of them (api.MultiEngine,
+xlf_multi_*: a native host worker thread + stream per device).  Both shard
+with the same rule (xlf_shard).
 """
 from __future__ import annotations
 
 
 def shard(rank: int, world: int, per_rank: int):
-    """(first_image, count) of `rank` -- weak scaling, fixed images per rank."""
+    """(first_image, count) of `rank` -- weak scaling, fixed images per rank:
+    the library's shard rule (xlf_shard, the MultiEngine's) over world*per_rank images."""
     if not (0 <= rank < world) or per_rank < 1:
         raise ValueError("bad shard request")
-    return rank * per_rank, per_rank
+    from .api import shard_range
+    return shard_range(world * per_rank, world, rank)
 
 
 def max_over_ranks(value: float, device=None) -> float:

@@ -1,7 +1,9 @@
-"""N>1 path on CPU: world_size-2 gloo processes shard a batch exactly as
-bench.py does (rank r owns images [r*B, (r+1)*B) of the seeded stream), run
-their shard independently (no exchange on the data path) and gather to rank 0;
-the result must equal the single-process run bit for bit."""
+"""N>1 path on CPU: world_size-2 gloo processes shard a batch with the
+library's shard rule (xlf_shard, which bench.py and the MultiEngine use: rank
+r owns images [r*B, (r+1)*B) of the seeded stream), compute their shard
+independently (the CPU oracle stands in for the device: no GPU here; no
+exchange on the data path) and gather to rank 0; the result must equal the
+single-process run bit for bit."""
 import os
 import socket
 
@@ -55,6 +57,17 @@ def test_batch_sharding_gloo(tmp_path, world):
     x = O.seeded_batch(og, 42, world * per_rank)
     ref = O.run_batch(og, x, O.seeded_weights(og, 42), ["conv2"])["conv2"]
     assert got.shape == ref.shape and np.array_equal(got, ref)
+
+
+def test_library_shard_rule_ragged():
+    """xlf_shard (the MultiEngine's rule): contiguous, sizes differ by <= 1."""
+    from paper_2007_06000_b200 import shard_range
+    for batch in (0, 1, 5, 7, 255, 256, 2048):
+        for n in (1, 2, 3, 4, 8):
+            ranges = [shard_range(batch, n, k) for k in range(n)]
+            seen = [i for f, c in ranges for i in range(f, f + c)]
+            assert seen == list(range(batch))
+            assert max(c for _, c in ranges) - min(c for _, c in ranges) <= 1
 
 
 def test_shard_covers_batch_once():
