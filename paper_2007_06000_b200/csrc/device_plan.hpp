@@ -39,6 +39,7 @@ struct Knobs {
     int tsets = 0;               // force 1 / 2 accumulator sets
     int ctas = 0;                // cap on resident CTAs per SM
     bool pdl = true;             // programmatic dependent launch between steps
+    bool no_stem = false;        // the first conv + max-pool through the generic fused-block kernel, not the stem kernel
     bool no_s2d = false;         // keep a stride-2 first conv on its own input (no space-to-depth rewrite)
     int trace = 0;               // 1: phase stamps of a steady tile, 2: tile end stamps
     bool tune_verbose = false;   // autotune prints every timing to stderr

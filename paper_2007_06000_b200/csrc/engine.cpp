@@ -4,6 +4,7 @@
 #include <cudaTypedefs.h>
 
 #include <algorithm>
+#include <cmath>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -11,6 +12,7 @@
 #include <tuple>
 
 #include "tc_params.hpp"
+#include "stem_params.hpp"
 #include "common.hpp"
 #include "fused_params.hpp"
 
@@ -38,9 +40,11 @@ cudaError_t launch_nhwc_tc_to_nchw(int es, const void* src, int cs, int coff, fl
 cudaError_t launch_seeded_nhwc_tc(int es, void* dst, unsigned long long seed, unsigned long long first_image, int N, int C, int H, int W,
                                   int cs, cudaStream_t st);
 cudaError_t launch_s2d_tc(int es, const float* src, unsigned long long seed, unsigned long long first_image, void* dst, int N, int C, int H,
-                          int W, int cs, cudaStream_t st);
+                          int W, int cs, int planar, cudaStream_t st);
 cudaError_t launch_concat_copy_tc(int es, const void* src, int scs, int sco, void* dst, int dcs, int dco, int C, long long pixels,
                                   cudaStream_t st);
+// kernels_stem.cu
+cudaError_t launch_stem(const StemParams& P, int batch, cudaStream_t st, int n0);
 cudaError_t launch_eltwise_tc(int es, int op, const void* a, int acs, int aco, const void* b, int bcs, int bco, void* o, int ocs, int oco, int C,
                               long long pixels, cudaStream_t st);
 
@@ -208,6 +212,7 @@ Engine::Engine(const Graph& g, int device, Partition part, Precision prec, const
     cuda_check(cudaMalloc(&staging_, staging_floats_ * 4), "cudaMalloc(staging)");
     params_.resize(plan_.steps.size());
     bparams_.resize(plan_.steps.size());
+    stems_.resize(plan_.steps.size());
     for (size_t i = 0; i < plan_.steps.size(); ++i) {
         const StepSpec& s = plan_.steps[i];
         if (s.kind != StepSpec::FUSED) continue;
@@ -215,8 +220,96 @@ Engine::Engine(const Graph& g, int device, Partition part, Precision prec, const
             params_[i] = make_params(g_, plan_, s, allocs_, weights_);
             continue;
         }
+        if (auto st = build_stem(s)) {
+            stems_[i] = std::move(st);
+            plan_.steps[i].tag = "stem";
+            s2d_planar_ = 1;  // the stem reads the space-to-depth input row-planar (see s2d_tc)
+            continue;
+        }
         bparams_[i] = build_bparams(s);
     }
+}
+
+// The stem kernel (kernels_stem.cu) takes a step that is exactly: the first
+// conv of the graph rewritten on the space-to-depth input (stride 1, whole
+// 32-byte K steps, one N block of 32 | npad <= 128 columns, output rows <= 128
+// wide) -> its 3x3/2 pad-0 max-pool, the conv output not stored.  Returns
+// null for any other step (the generic fused-block kernel runs it).
+std::unique_ptr<StemParams> Engine::build_stem(const StepSpec& s) {
+    if (!s2d_ || !tc_es_ || knobs_.no_stem || s.kind != StepSpec::FUSED || s.ops.size() != 2 || s.inputs.size() != 1 ||
+        s.inputs[0] != g_.inputs[0].name)
+        return nullptr;
+    const OpSpec &oc = s.ops[0], &op = s.ops[1];
+    const Layer& c = *g_.find_layer(oc.layer);
+    const Layer& p = *g_.find_layer(op.layer);
+    if (c.kind != LayerKind::conv || p.kind != LayerKind::pool || oc.stage != 1 || op.stage != 2 || oc.emit || !op.emit ||
+        p.pool->kind != PoolKind::max || p.pool->kernel != 3 || p.pool->stride != 2 || p.pool->pad != 0 || !tc_mma_ok(c, tc_es_) ||
+        c.conv->activation != Activation::relu)
+        return nullptr;
+    int nblocks = 0, nb = 0;
+    tc_nblocks(c.conv->out_channels, &nblocks, &nb);
+    const TensorShape in = g_.shape_of(s.inputs[0]), co = *c.out_shape, po = *p.out_shape;
+    if (nblocks != 1 || (nb != 64 && nb != 128) || co.width > 128 || in.width > 256 || c.conv->kernel_h > 4 || c.conv->kernel_w > 4) return nullptr;
+    auto P = std::make_unique<StemParams>();
+    const TensorSlot& xt = plan_.tensors.at(s.inputs[0]);
+    const TensorSlot& ot = plan_.tensors.at(p.name);
+    const int cpc = 16 / tc_es_;
+    P->es = tc_es_;
+    P->Hin = in.height, P->Win = in.width, P->planes = xt.cstride / cpc;
+    P->kh = c.conv->kernel_h, P->kw = c.conv->kernel_w;
+    P->Hc = co.height, P->Wc = co.width, P->cout = co.channels, P->npad = nb;
+    P->Hp = po.height, P->Wp = po.width;
+    if (P->planes * cpc != c.conv->in_channels || P->planes % 2) return nullptr;
+    P->wmma = static_cast<const uint8_t*>(weights_tc_) + wofftc_.at(c.name);
+    P->w_bytes = P->kh * P->kw * P->planes * nb * 16;
+    P->bias = weights_ + plan_.b_off.at(c.name);
+    P->out = allocs_[size_t(ot.alloc)], P->out_cstride = ot.cstride, P->out_coff = ot.coff;
+    // bands of pooled rows: balance units over the persistent grid at max_batch
+    P->ctas_per_sm = 2;
+    const long long grid = 148LL * P->ctas_per_sm;
+    double best = 1e300;
+    for (int br = 2; br <= std::min(P->Hp, 16); ++br) {
+        const int bands = (P->Hp + br - 1) / br;
+        const double t = std::ceil(double(max_batch_) * bands / grid) * (2.0 * br + 1 + 2.0);  // conv rows per band + per-band latency
+        if (t < best) best = t, P->band_rows = br, P->bands = bands;
+    }
+    P->slots = kStemSlots;
+    P->acc_slots = nb == 64 ? 4 : 2;  // as the kernel instantiation (kernels_stem.cu)
+    P->tmem_cols = 32;
+    while (P->tmem_cols < P->acc_slots * nb) P->tmem_cols *= 2;
+    auto up = [](int v, int a) { return (v + a - 1) / a * a; };
+    P->plane_bytes = in.width * 16;  // planes of a row are contiguous (row-planar input)
+    P->slot_bytes = up(P->planes * P->plane_bytes, 128);
+    P->ring_off = 0;
+    P->w_off = up(P->slots * P->slot_bytes, 1024);
+    P->stage_off = up(P->w_off + P->w_bytes, 1024);
+    P->stage_bytes = 128 * nb * tc_es_;
+    P->bias_off = P->stage_off + 2 * P->stage_bytes;
+    P->smem_bytes = P->bias_off + nb * 4;
+    if (P->smem_bytes > kStemSmemMax) return nullptr;
+    P->pdl = knobs_.pdl ? 1 : 0;
+    // input rows, row-planar (s2d_tc planar): one input row = row_elems contiguous
+    // elements = `lines` lines of `inner` elements; the map is 2-D {inner, lines
+    // of the whole batch}, one box = one input row (lines of >= 256 bytes: TMA
+    // moves a box line by line, 16-byte lines would starve it)
+    const long long row_elems = (long long)P->planes * in.width * cpc;
+    int inner = 0;
+    for (int d = 256; d >= cpc; d -= cpc)
+        if (row_elems % d == 0) {
+            inner = d;
+            break;
+        }
+    if (!inner || row_elems / inner > 256) return nullptr;
+    P->row_lines = int(row_elems / inner);
+    const cuuint64_t dims[2] = {cuuint64_t(inner), cuuint64_t((long long)max_batch_ * in.height * P->row_lines)};
+    const cuuint64_t strides[1] = {cuuint64_t(inner) * tc_es_};
+    const cuuint32_t box[2] = {cuuint32_t(inner), cuuint32_t(P->row_lines)};
+    const cuuint32_t estr[2] = {1, 1};
+    const CUresult res = tensor_map_encoder()(&P->xmap, tc_es_ == 4 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2,
+                                              allocs_[size_t(xt.alloc)], dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                                              CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (res != CUDA_SUCCESS) fail(ErrorKind::cuda, "cuTensorMapEncodeTiled (stem) failed (" + std::to_string(int(res)) + ")");
+    return P;
 }
 
 // Launch descriptor of a tensor-core step in its current configuration (tile,
@@ -506,7 +599,7 @@ void Engine::set_input_nchw(const std::string& name, const float* d, int batch, 
     const TensorSlot& t = slot(name);
     void* dst = allocs_[size_t(t.alloc)];
     if (s2d_ && name == g_.inputs[0].name)
-        cuda_check(launch_s2d_tc(tc_es_, d, 0, 0, dst, batch, in_shape_.channels, in_shape_.height, in_shape_.width, t.cstride, st),
+        cuda_check(launch_s2d_tc(tc_es_, d, 0, 0, dst, batch, in_shape_.channels, in_shape_.height, in_shape_.width, t.cstride, s2d_planar_, st),
                    "space-to-depth input");
     else if (tc_es_)
         cuda_check(launch_nchw_to_nhwc_tc(tc_es_, d, dst, batch, t.C, t.H, t.W, t.cstride, st), "nchw_to_nhwc");
@@ -521,7 +614,7 @@ void Engine::set_input_seeded(const std::string& name, uint64_t seed, uint64_t f
     void* dst = allocs_[size_t(t.alloc)];
     if (s2d_ && name == g_.inputs[0].name)
         cuda_check(launch_s2d_tc(tc_es_, nullptr, seed, first_image, dst, batch, in_shape_.channels, in_shape_.height, in_shape_.width,
-                                 t.cstride, st),
+                                 t.cstride, s2d_planar_, st),
                    "seeded space-to-depth input");
     else if (tc_es_)
         cuda_check(launch_seeded_nhwc_tc(tc_es_, dst, seed, first_image, batch, t.C, t.H, t.W, t.cstride, st), "seeded fill");
@@ -532,6 +625,10 @@ void Engine::set_input_seeded(const std::string& name, uint64_t seed, uint64_t f
 // A tensor-core fused step over images [n0, n0 + count): the kernel, plus the
 // reduction that finishes a conv + global-average-pool step.
 void Engine::launch_tc_step(size_t i, int n0, int count, cudaStream_t st) {
+    if (stems_[i]) {
+        cuda_check(launch_stem(*stems_[i], count, st, n0), "stem (conv + max-pool, tensor cores)");
+        return;
+    }
     const BParams& P = *bparams_[i];
     cuda_check(launch_fused_tc(P, count, st, n0), "fused block (tensor cores)");
     const StepSpec& s = plan_.steps[i];
@@ -547,7 +644,7 @@ void Engine::launch_tc_step(size_t i, int n0, int count, cudaStream_t st) {
 bool Engine::range_capable() const {
     if (!tc_es_ || g_.inputs.size() != 1) return false;
     for (size_t i = 0; i < plan_.steps.size(); ++i)
-        if (plan_.steps[i].kind != StepSpec::FUSED || !bparams_[i]) return false;
+        if (plan_.steps[i].kind != StepSpec::FUSED || !(bparams_[i] || stems_[i])) return false;
     return true;
 }
 
@@ -667,6 +764,8 @@ void Engine::forward_external(const std::vector<External>& ext, int batch, cudaS
     cuda_check(cudaSetDevice(device_), "cudaSetDevice");
     const int cpc = 16 / esz_;
     std::string key;
+    for (const auto& st : stems_)
+        if (st && !ext.empty()) fail(ErrorKind::validation, "caller-owned tensors are not supported by plans with a stem step");
     for (const External& x : ext) {
         const TensorSlot& t = slot(x.name);
         if (s2d_ && x.name == g_.inputs[0].name)
@@ -796,7 +895,7 @@ void Engine::run_host(const float* h_in, int batch, const std::string& out_name,
         cuda_check(cudaStreamWaitEvent(st, chunk_ev_[c], 0), "wait H2D");
         uint8_t* x = reinterpret_cast<uint8_t*>(allocs_[size_t(xin.alloc)]) + size_t(n0) * xin.H * xin.W * xin.cstride * es;
         if (s2d_)
-            cuda_check(launch_s2d_tc(tc_es_, dst, 0, 0, x, cnt, in_shape_.channels, in_shape_.height, in_shape_.width, xin.cstride, st),
+            cuda_check(launch_s2d_tc(tc_es_, dst, 0, 0, x, cnt, in_shape_.channels, in_shape_.height, in_shape_.width, xin.cstride, s2d_planar_, st),
                        "space-to-depth input chunk");
         else
             cuda_check(launch_nchw_to_nhwc_tc(tc_es_, dst, x, cnt, xin.C, xin.H, xin.W, xin.cstride, st), "nchw_to_nhwc chunk");

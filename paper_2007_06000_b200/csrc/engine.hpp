@@ -80,6 +80,7 @@ private:
     void launch_step(size_t i, int batch, cudaStream_t st);
     void drop_derived();  // CUDA graphs + external-address descriptors of the current configurations
     std::unique_ptr<struct BParams> build_bparams(const StepSpec& s);
+    std::unique_ptr<struct StemParams> build_stem(const StepSpec& s);
     void launch_tc_step(size_t i, int n0, int count, cudaStream_t st);
     const TensorSlot& slot(const std::string& n) const;
     const TensorSlot& readable(const std::string& n) const;
@@ -97,12 +98,14 @@ private:
     size_t staging_floats_ = 0;
     std::vector<struct FusedParams> params_;
     std::vector<std::unique_ptr<struct BParams>> bparams_;  // tensor-core steps
+    std::vector<std::unique_ptr<struct StemParams>> stems_;  // steps run by the stem kernel (conv + max-pool)
     std::vector<unsigned long long*> traces_;                // trace buffers (option trace)
     std::map<std::string, long long> wofftc_;                // packed MMA weights: byte offset per layer
     void* weights_tc_ = nullptr;  // packed MMA weights (bf16 / TF32)
     int tc_es_ = 0;               // tensor-core element bytes (2 bf16, 4 TF32), 0 = fp32 SIMT kernels
     int esz_ = 4;                 // bytes per activation element in HBM
     bool s2d_ = false;            // tensor cores: first conv rewritten on a space-to-depth input
+    int s2d_planar_ = 0;          // ... stored row-planar (the stem kernel reads it)
     TensorShape in_shape_;        // user-facing (NCHW) shape of input 0
     std::map<std::string, TensorShape> user_inputs_;  // graph inputs as the user passes them
     std::map<long long, cudaGraphExec_t> graphs_;  // key > 0: whole batch; < 0: image range (forward_range)

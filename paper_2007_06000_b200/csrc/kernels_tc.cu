@@ -1070,9 +1070,12 @@ __global__ void seeded_nhwc_tc(T* __restrict__ dst, unsigned long long seed, uns
 // rewritten as a stride-1 conv on 2x2 phases so it runs on tensor cores):
 // dst[n][Y][X][(py*2+px)*C + c] = src[n][c][2Y+py][2X+px], channels >= 4C zero.
 // Source is NCHW fp32 (src != nullptr) or the SeededStream (seed, first_image).
+// planar != 0: "row-planar" instead of NHWC -- image n, row Y holds the row's
+// 16-byte channel planes one after the other ([n][Y][plane][X][cpc]), so a
+// whole input row is one contiguous run (the stem kernel's TMA layout).
 template <class T>
 __global__ void s2d_tc(const float* __restrict__ src, unsigned long long seed, unsigned long long first_image, T* __restrict__ dst, int N,
-                       int C, int H, int W, int cs) {
+                       int C, int H, int W, int cs, int planar) {
     const int H2 = H / 2, W2 = W / 2;
     const long long total = (long long)N * H2 * W2 * cs;
     for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total; i += (long long)gridDim.x * blockDim.x) {
@@ -1087,7 +1090,9 @@ __global__ void s2d_tc(const float* __restrict__ src, unsigned long long seed, u
             const unsigned long long idx = (((unsigned long long)n * C + c) * H + y) * (unsigned long long)W + x;
             v = src ? src[idx] : seeded_at(seed, first_image * (unsigned long long)C * H * W + idx);
         }
-        dst[i] = Elem<T>::from(v);
+        constexpr int cpc = Elem<T>::cpc;
+        const long long o = planar ? (((n * H2 + Y) * (cs / cpc) + ci / cpc) * W2 + X) * cpc + ci % cpc : i;
+        dst[o] = Elem<T>::from(v);
     }
 }
 
@@ -1273,11 +1278,11 @@ cudaError_t launch_seeded_nhwc_tc(int es, void* dst, unsigned long long seed, un
 }
 
 cudaError_t launch_s2d_tc(int es, const float* src, unsigned long long seed, unsigned long long first_image, void* dst, int N, int C, int H,
-                          int W, int cs, cudaStream_t st) {
+                          int W, int cs, int planar, cudaStream_t st) {
     const int g = grid_b((long long)N * (H / 2) * (W / 2) * cs);
     seed = seed ? seed : 0x9e3779b97f4a7c15ull;
-    XLF_BY_ES(es, (s2d_tc<float><<<g, 256, 0, st>>>(src, seed, first_image, static_cast<float*>(dst), N, C, H, W, cs)),
-              (s2d_tc<__nv_bfloat16><<<g, 256, 0, st>>>(src, seed, first_image, static_cast<__nv_bfloat16*>(dst), N, C, H, W, cs)));
+    XLF_BY_ES(es, (s2d_tc<float><<<g, 256, 0, st>>>(src, seed, first_image, static_cast<float*>(dst), N, C, H, W, cs, planar)),
+              (s2d_tc<__nv_bfloat16><<<g, 256, 0, st>>>(src, seed, first_image, static_cast<__nv_bfloat16*>(dst), N, C, H, W, cs, planar)));
     return cudaGetLastError();
 }
 
