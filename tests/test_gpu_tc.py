@@ -321,3 +321,31 @@ def test_tc_rewritten_input_is_not_readable(prec):
         e.read("data", 2)
     with pytest.raises(X.XlfError):
         e.read("pool10", 3)  # batch beyond max_batch
+
+
+@pytest.mark.parametrize("prec", PRECS)
+def test_stem_kernel_matches_generic_path(prec):
+    """SqueezeNet conv1 + pool1 run by the stem kernel (kernels_stem.cu) vs the
+    generic fused-block kernel (option no_stem=1): both within the tolerance
+    of the oracle on pool1, for a batch whose bands straddle the persistent
+    grid unevenly (37 images), and the TF32 stem bit-identical to the generic
+    path (max commutes with the monotone bias / ReLU / rounding)."""
+    import torch
+    text = graph_text("squeezenet11")
+    og = O.load_graph(text)
+    w = O.flat_weights(og, O.seeded_weights(og, 42))
+    g = X.Graph(text)
+    outs = {}
+    for opt in ("", "no_stem=1"):
+        e = X.Engine(g, w, "b200", prec, max_batch=37, options=opt)
+        assert ("stem" in [s["tag"] for s in e.steps]) == (opt == "")
+        e.set_input_seeded(42, 37)
+        e.forward(37)
+        outs[opt] = e.read("pool1", 37).cpu().numpy()
+    torch.cuda.synchronize()
+    x = O.seeded_batch(og, 42, 37)[[0, 18, 36]]
+    ref = O.run_batch(og, x, O.seeded_weights(og, 42), ["pool1"])["pool1"]
+    for o in outs.values():
+        assert O.normwise(o[[0, 18, 36]], ref) <= TOL[prec]
+    if prec == "tf32":
+        assert np.array_equal(outs[""], outs["no_stem=1"])
