@@ -487,6 +487,7 @@ Knobs Knobs::parse(const std::string& text) {
         else if (key == "wres") k.wres = int(need_num());
         else if (key == "tsets") k.tsets = int(need_num());
         else if (key == "ctas") k.ctas = int(need_num());
+        else if (key == "nsplit") k.nsplit = int(need_num());
         else if (key == "pdl") k.pdl = need_num() != 0;
         else if (key == "no_s2d") k.no_s2d = need_num() != 0;
         else if (key == "no_stem") k.no_stem = need_num() != 0;
@@ -807,7 +808,7 @@ std::string describe_plan_json(const Graph& g, const DevicePlan& plan) {
         static const char* kinds[] = {"fused", "concat_copy", "add", "relu"};
         os << (i ? "," : "") << "{\"id\":" << q(s.id) << ",\"kind\":" << q(kinds[s.kind]) << ",\"tag\":" << q(s.tag)
            << ",\"mode\":" << q(to_string(s.mode)) << ",\"tile\":[" << s.tile_h << "," << s.tile_w
-           << "],\"out\":[" << s.out_h << "," << s.out_w << "],\"smem_bytes\":" << s.smem_bytes << ",\"nxb\":" << s.nxb << ",\"wres\":" << s.wres << ",\"ring_slots\":" << s.ring_slots << ",\"grid_all\":" << s.grid_all << ",\"epi_warps\":" << s.epi_warps << ",\"tsets\":" << s.tsets << ",\"macs\":" << s.macs
+           << "],\"out\":[" << s.out_h << "," << s.out_w << "],\"smem_bytes\":" << s.smem_bytes << ",\"nxb\":" << s.nxb << ",\"wres\":" << s.wres << ",\"ring_slots\":" << s.ring_slots << ",\"grid_all\":" << s.grid_all << ",\"epi_warps\":" << s.epi_warps << ",\"tsets\":" << s.tsets << ",\"nsplit\":" << s.nsplit << ",\"macs\":" << s.macs
            << ",\"macs_executed\":" << s.macs_executed << ",\"bytes_algorithmic\":" << s.bytes_algorithmic
            << ",\"weight_bytes\":" << s.weight_bytes << ",\"ring_chunk\":" << s.ring_chunk << ",\"inputs\":[";
         for (size_t k = 0; k < s.inputs.size(); ++k) os << (k ? "," : "") << q(s.inputs[k]);

@@ -38,6 +38,7 @@ struct Knobs {
     int wres = -1;               // force resident (1) / ring-streamed (0) weights
     int tsets = 0;               // force 1 / 2 accumulator sets
     int ctas = 0;                // cap on resident CTAs per SM
+    int nsplit = 0;              // force output-channel groups (tensor-core steps that can split)
     bool pdl = true;             // programmatic dependent launch between steps
     bool no_stem = false;        // the first conv + max-pool through the generic fused-block kernel, not the stem kernel
     bool no_s2d = false;         // keep a stride-2 first conv on its own input (no space-to-depth rewrite)
@@ -92,6 +93,7 @@ struct StepSpec {
     int epi_warps = 8;  // epilogue/SIMT warps per CTA (4 or 8)
     int tsets = 1;      // TMEM accumulator sets (2 = cross-tile MMA/epilogue overlap)
     int ring_chunk = 16384;  // bytes per weight-ring slot
+    int nsplit = 1;     // output-channel groups over the grid's y dimension (weights of a group resident per CTA)
     // tensor-core conv + global average pool (SqueezeNet conv10 -> pool10): the
     // step's single conv op never stores its output; its epilogue reduces
     // every tile over its cells and the pooled layer `gap_out` (1x1) is
@@ -139,10 +141,14 @@ bool choose_tile_tc(const Graph& g, StepSpec& s, int batch_hint, int smem_budget
 struct BCandidate {
     int th, tw, nxb, wres, slots, smem, epi_warps, tsets, chunk;
     double model;
+    int nsplit;
 };
 std::vector<BCandidate> candidates_tc(const Graph& g, const StepSpec& s, int batch_hint, int smem_budget, int es, const Knobs& k);
 void apply_candidate(StepSpec& s, const BCandidate& c);
 std::vector<uint8_t> pack_weights_tc(const Graph& g, const float* flat, size_t count, std::map<std::string, long long>& off, int es);
+// One MMA conv's packed weights with an explicit N blocking (nblocks x nb
+// columns, zero past cout): the packing of an N-split op (BOp::gch).
+std::vector<uint8_t> pack_layer_tc(const Graph& g, const std::string& layer, const float* flat, size_t count, int es, int nb, int nblocks);
 
 // Packs reference-layout weights (save_weights stream order, tensor.cpp:64-95)
 // into the device layout of `plan`: per conv [cin/group][kh][kw][cout_pad4]

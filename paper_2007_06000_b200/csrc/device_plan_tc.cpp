@@ -228,6 +228,21 @@ long long layout_tc(const Graph& g, const StepSpec& s, int th, int tw, BParams* 
         b.mode = kPlanes, b.kb_ch = cpc, b.row_bytes = 16;  // written by the epilogue threads
         region(b, true);
     }
+    // N split (s.nsplit > 1): MMA-only steps whose terminal ops (stage 2 of a
+    // two-stage block, else every op) split their output channels over the
+    // grid's y dimension; stage-1 producers of a two-stage block are
+    // recomputed by every channel group, and must not escape to HBM.
+    const int nsplit = std::max(1, s.nsplit);
+    bool two_stage = false;
+    for (const OpSpec& op : s.ops) two_stage |= op.stage == 2;
+    if (nsplit > 1) {
+        for (int i = 0; i < nops; ++i) {
+            const OpSpec& op = s.ops[size_t(i)];
+            if (!geo[size_t(i)].mma) return -1;
+            if (two_stage ? (op.stage == 1 ? op.emit : !op.emit) : !op.emit) return -1;
+        }
+    }
+    auto split_op = [&](int i) { return nsplit > 1 && (!two_stage || s.ops[size_t(i)].stage == 2); };
     bool any_mma = false;
     int tmem = 0;
     std::vector<BOp> ops(static_cast<size_t>(nops));
@@ -255,6 +270,12 @@ long long layout_tc(const Graph& g, const StepSpec& s, int th, int tw, BParams* 
                 o.contig = gi.contig;
                 o.kpt = o.cin * es / 32;
                 tc_nblocks(out.channels, &o.nblocks, &o.nb);
+                if (split_op(i)) {  // one N block of gch channels per group
+                    const int gch = r16(cdiv(r16(out.channels), nsplit));
+                    if (gch > 256 || gch * (nsplit - 1) >= out.channels) return -1;  // one block per group, no empty group
+                    o.nblocks = 1, o.nb = gch, o.gch = gch;
+                    o.gwb = (long long)o.kh * o.kw * o.kpt * gch * 32;
+                }
                 o.npad = o.nblocks * o.nb;
                 if (o.contig) o.strips = 1, o.mtiles = cdiv(o.ext_h * o.ext_w, 128);
                 else o.strips = cdiv(o.ext_w, 8), o.mtiles = o.strips * cdiv(o.ext_h, 16);
@@ -433,6 +454,8 @@ long long layout_tc(const Graph& g, const StepSpec& s, int th, int tw, BParams* 
         P->tsets = tsets;
         P->gap_off = int(gap_off);
         P->es = es;
+        P->nsplit = nsplit;
+        P->gap_np_total = ops[0].gap ? nsplit * ops[0].npad : ops[0].npad;
         P->pdl = k.pdl ? 1 : 0;
         P->xrel_epi = k.xrel_epi ? 1 : 0;
     }
@@ -486,14 +509,29 @@ std::vector<BCandidate> candidates_tc(const Graph& g, const StepSpec& s, int bat
     int fh = 0, fw = 0;
     const bool forced = k.forced_tile(s, &fh, &fw);  // a reference plan's geometry
     BParams* P = new BParams;
+    // channel-group counts this step can split into (1 = no split)
+    std::vector<int> splits{1};
+    for (int ns : {2, 4, 8}) {
+        StepSpec t = s;
+        t.nsplit = ns;
+        if (layout_tc(g, t, 1, 1, nullptr, 1, 1, 3, 1, kChunkBytes, es, k) >= 0 ||
+            layout_tc(g, t, std::min(s.out_h, 8), std::min(s.out_w, 8), nullptr, 1, 0, 3, 1, 4 * kChunkBytes, es, k) >= 0)
+            splits.push_back(ns);
+    }
+    StepSpec sv = s;
+    for (int ns : splits)
     for (int ew : {8, 4})
     for (int ts = 1; ts <= 2; ++ts)
     for (int nxb = ts; nxb <= 2; ++nxb)
         for (const WMode& wm : wmodes) {
+            // channel groups exist to keep a group's weights resident: with a
+            // split, only resident weights and the shallowest ring are tried
+            if (ns > 1 && !wm.wres && (wm.slots != 3 || wm.chunk != kChunkBytes)) continue;
+            sv.nsplit = ns;
             for (int th = 1; th <= (forced ? fh : std::min(s.out_h, 32)); ++th)
                 for (int tw = 1; tw <= (forced ? fw : std::min(s.out_w, 32)); ++tw) {
                     if (forced && (fh % th || fw % tw)) continue;  // the plan's tile or an exact sub-tile
-                    const long long sm = layout_tc(g, s, th, tw, P, nxb, wm.wres, wm.slots, ts, wm.chunk, es, k);
+                    const long long sm = layout_tc(g, sv, th, tw, P, nxb, wm.wres, wm.slots, ts, wm.chunk, es, k);
                     if (sm < 0 || sm > smem_budget) continue;
                     if (wm.wres && !P->wres) continue;  // no MMA op: the ring/resident choice is moot
                     double in_bytes = 0, mma = 0, simt = 0;
@@ -506,7 +544,7 @@ std::vector<BCandidate> candidates_tc(const Graph& g, const StepSpec& s, int bat
                     double out_bytes = 0;
                     for (int i = 0; i < P->nops; ++i)
                         if (P->ops[i].emit) out_bytes += double(th) * tw * P->ops[i].npad * es;
-                    const double tiles = double(P->grid_h) * P->grid_w * P->cgroups * std::max(batch_hint, 1);
+                    const double tiles = double(P->grid_h) * P->grid_w * P->cgroups * std::max(batch_hint, 1) * ns;
                     // 228 KB per SM; per CTA: dynamic + static (~4 KB) + 1 KB driver reserve
                     int occ = std::max(1, std::min(max_ctas_per_sm(ew), int((228 * 1024) / (sm + 5120))));
                     if (P->tmem_cols) occ = std::min(occ, 512 / (P->tmem_cols * ts));
@@ -521,7 +559,7 @@ std::vector<BCandidate> candidates_tc(const Graph& g, const StepSpec& s, int bat
                     const double per_tile = (nxb == 2 ? std::max(load, compute) : load + compute) - (ts == 2 ? mma / 8192.0 : 0.0);
                     const double t = std::max(std::ceil(tiles / (148.0 * occ)) * per_tile,
                                               tiles * (in_bytes + out_bytes) / (148.0 * 24.0));
-                    out.push_back({th, tw, nxb, P->wres, wm.slots, int(sm), ew, ts, wm.chunk, t});
+                    out.push_back({th, tw, nxb, P->wres, wm.slots, int(sm), ew, ts, wm.chunk, t, ns});
                 }
         }
     delete P;
@@ -536,6 +574,7 @@ std::vector<BCandidate> candidates_tc(const Graph& g, const StepSpec& s, int bat
     if (force) prefer([&](const BCandidate& c) { return c.nxb == force; });
     if (force_w >= 0) prefer([&](const BCandidate& c) { return c.wres == force_w; });
     if (k.tsets) prefer([&](const BCandidate& c) { return c.tsets == k.tsets; });
+    if (k.nsplit) prefer([&](const BCandidate& c) { return c.nsplit == k.nsplit; });
     std::stable_sort(out.begin(), out.end(), [](const BCandidate& a, const BCandidate& b) {
         if (a.model < b.model * 0.999) return true;
         if (b.model < a.model * 0.999) return false;
@@ -561,29 +600,49 @@ static bool choose_tile_tc_at(const Graph& g, StepSpec& s, int batch_hint, int s
 
 void apply_candidate(StepSpec& s, const BCandidate& c) {
     s.tile_h = c.th, s.tile_w = c.tw, s.smem_bytes = c.smem, s.nxb = c.nxb, s.wres = c.wres, s.ring_slots = c.slots;
-    s.epi_warps = c.epi_warps, s.tsets = c.tsets, s.ring_chunk = c.chunk;
+    s.epi_warps = c.epi_warps, s.tsets = c.tsets, s.ring_chunk = c.chunk, s.nsplit = c.nsplit;
 }
 
 // Weights of every MMA-eligible conv as the UMMA K-major B operand of each
 // 32-byte K step: [nblock][tap][cin/cpc][nb][cpc] elements, bf16 (RN even) or
 // fp32 rounded to TF32 (RN, ties away -- the rounding the TF32 epilogue
 // applies to activations).  `off`: byte offset per layer.
+namespace {
+void put_tc(std::vector<uint8_t>& out, size_t byte, float f, int es) {
+    uint32_t u;
+    std::memcpy(&u, &f, 4);
+    if (es == 2) {
+        u += 0x7FFF + ((u >> 16) & 1);  // round to nearest even
+        const uint16_t h = uint16_t(u >> 16);
+        std::memcpy(&out[byte], &h, 2);
+    } else {
+        if ((u & 0x7F800000u) != 0x7F800000u) u = (u + 0x1000u) & ~0x1FFFu;  // TF32: 10 mantissa bits, ties away
+        std::memcpy(&out[byte], &u, 4);
+    }
+}
+
+// Appends layer l's packed weights (nblocks x nb columns) read from w (its
+// filter [oc][ic][kh][kw]) to out.
+void pack_conv_tc(std::vector<uint8_t>& out, const ConvParams& c, const float* w, int es, int nblocks, int nb) {
+    const int cpc = 16 / es;
+    const int kpt = c.in_channels * es / 32, taps = c.kernel_h * c.kernel_w, ksteps = taps * kpt;
+    const size_t base = out.size();
+    out.resize(base + size_t(nblocks) * ksteps * nb * 32, 0);
+    for (int oc = 0; oc < c.out_channels; ++oc)
+        for (int ic = 0; ic < c.in_channels; ++ic)
+            for (int y = 0; y < c.kernel_h; ++y)
+                for (int x = 0; x < c.kernel_w; ++x) {
+                    const int nbi = oc / nb, n = oc - nbi * nb, tap = y * c.kernel_w + x;
+                    const int step = tap * kpt + ic / (2 * cpc), half = (ic % (2 * cpc)) / cpc;
+                    const size_t el = ((size_t(nbi) * ksteps + step) * 2 + half) * nb * cpc + size_t(n) * cpc + ic % cpc;
+                    put_tc(out, base + el * es, w[((size_t(oc) * c.in_channels + ic) * c.kernel_h + y) * c.kernel_w + x], es);
+                }
+}
+}  // namespace
+
 std::vector<uint8_t> pack_weights_tc(const Graph& g, const float* flat, size_t count, std::map<std::string, long long>& off, int es) {
     std::vector<uint8_t> out;
     size_t pos = 0;
-    const int cpc = 16 / es;
-    auto put = [&](size_t byte, float f) {
-        uint32_t u;
-        std::memcpy(&u, &f, 4);
-        if (es == 2) {
-            u += 0x7FFF + ((u >> 16) & 1);  // round to nearest even
-            const uint16_t h = uint16_t(u >> 16);
-            std::memcpy(&out[byte], &h, 2);
-        } else {
-            if ((u & 0x7F800000u) != 0x7F800000u) u = (u + 0x1000u) & ~0x1FFFu;  // TF32: 10 mantissa bits, ties away
-            std::memcpy(&out[byte], &u, 4);
-        }
-    };
     for (const Layer& l : g.layers) {
         if (l.kind != LayerKind::conv) continue;
         const ConvParams& c = *l.conv;
@@ -592,23 +651,29 @@ std::vector<uint8_t> pack_weights_tc(const Graph& g, const float* flat, size_t c
         if (tc_mma_ok(l, es)) {
             int nblocks, nb;
             tc_nblocks(c.out_channels, &nblocks, &nb);
-            const int kpt = c.in_channels * es / 32, taps = c.kernel_h * c.kernel_w, ksteps = taps * kpt;
-            const size_t base = out.size();
-            off[l.name] = (long long)base;
-            out.resize(base + size_t(nblocks) * ksteps * nb * 32, 0);
-            for (int oc = 0; oc < c.out_channels; ++oc)
-                for (int ic = 0; ic < c.in_channels; ++ic)
-                    for (int y = 0; y < c.kernel_h; ++y)
-                        for (int x = 0; x < c.kernel_w; ++x) {
-                            const int nbi = oc / nb, n = oc - nbi * nb, tap = y * c.kernel_w + x;
-                            const int step = tap * kpt + ic / (2 * cpc), half = (ic % (2 * cpc)) / cpc;
-                            const size_t el = ((size_t(nbi) * ksteps + step) * 2 + half) * nb * cpc + size_t(n) * cpc + ic % cpc;
-                            put(base + el * es, flat[pos + ((size_t(oc) * c.in_channels + ic) * c.kernel_h + y) * c.kernel_w + x]);
-                        }
+            off[l.name] = (long long)out.size();
+            pack_conv_tc(out, c, flat + pos, es, nblocks, nb);
         }
         pos += nf + nb_;
     }
     return out;
+}
+
+std::vector<uint8_t> pack_layer_tc(const Graph& g, const std::string& layer, const float* flat, size_t count, int es, int nb, int nblocks) {
+    size_t pos = 0;
+    for (const Layer& l : g.layers) {
+        if (l.kind != LayerKind::conv) continue;
+        const size_t n = size_t(l.conv->weight_count() + l.conv->bias_count());
+        if (l.name == layer) {
+            if (pos + n > count || !tc_mma_ok(l, es) || nblocks * nb < l.conv->out_channels)
+                fail(ErrorKind::internal, "pack_layer_tc: cannot pack '" + layer + "'");
+            std::vector<uint8_t> out;
+            pack_conv_tc(out, *l.conv, flat + pos, es, nblocks, nb);
+            return out;
+        }
+        pos += n;
+    }
+    fail(ErrorKind::internal, "pack_layer_tc: no conv '" + layer + "'");
 }
 
 }  // namespace xlf

@@ -193,6 +193,7 @@ Engine::Engine(const Graph& g, int device, Partition part, Precision prec, const
     cuda_check(cudaMalloc(&weights_, packed.size() * 4), "cudaMalloc(weights)");
     cuda_check(cudaMemcpy(weights_, packed.data(), packed.size() * 4, cudaMemcpyHostToDevice), "weights H2D");
     if (tc) {
+        host_w_.assign(weights, weights + nweights);  // N-split ops are packed per channel group on demand (packed_for)
         std::vector<uint8_t> wt = pack_weights_tc(g_, weights, nweights, wofftc_, tc_es_);
         wt.resize(wt.size() + 128, 0);
         cuda_check(cudaMalloc(&weights_tc_, wt.size()), "cudaMalloc(tensor-core weights)");
@@ -312,6 +313,20 @@ std::unique_ptr<StemParams> Engine::build_stem(const StepSpec& s) {
     return P;
 }
 
+// Packed weights of `layer` with nblocks x nb columns (N-split ops: one block
+// per channel group), built once per shape from the host copy.
+const uint8_t* Engine::packed_for(const std::string& layer, int nb, int nblocks) {
+    const std::string key = layer + "/" + std::to_string(nb) + "x" + std::to_string(nblocks);
+    auto it = packed_.find(key);
+    if (it != packed_.end()) return static_cast<const uint8_t*>(it->second);
+    const std::vector<uint8_t> w = pack_layer_tc(g_, layer, host_w_.data(), host_w_.size(), tc_es_, nb, nblocks);
+    void* d = nullptr;
+    cuda_check(cudaMalloc(&d, w.size() + 128), "cudaMalloc(split weights)");
+    cuda_check(cudaMemcpy(d, w.data(), w.size(), cudaMemcpyHostToDevice), "split weights H2D");
+    packed_[key] = d;
+    return static_cast<const uint8_t*>(d);
+}
+
 // Launch descriptor of a tensor-core step in its current configuration (tile,
 // staging, weight residency), bound to this engine's tensors and weights,
 // with its device copy.
@@ -342,7 +357,8 @@ std::unique_ptr<BParams> Engine::build_bparams(const StepSpec& s) {
         if (o.kind == BOP_MMA || o.kind == BOP_SIMT_CONV) {
             o.wsimt = weights_ + plan_.w_off.at(os.layer);
             o.bias = weights_ + plan_.b_off.at(os.layer);
-            if (o.kind == BOP_MMA) o.wmma = static_cast<const uint8_t*>(weights_tc_) + wofftc_.at(os.layer);
+            if (o.kind == BOP_MMA)
+                o.wmma = o.gch ? packed_for(os.layer, o.nb, P->nsplit) : static_cast<const uint8_t*>(weights_tc_) + wofftc_.at(os.layer);
         }
         if (o.emit) {
             const TensorSlot& t = plan_.tensors.at(s.gap_out.empty() ? os.layer : s.gap_out);
@@ -350,8 +366,8 @@ std::unique_ptr<BParams> Engine::build_bparams(const StepSpec& s) {
             o.out_cstride = t.cstride, o.out_coff = t.coff;
         }
     }
-    if (!s.gap_out.empty()) {  // per-tile column sums, [image][tile][npad] fp32
-        const size_t need = size_t(max_batch_) * P->grid_h * P->grid_w * P->ops[0].npad;
+    if (!s.gap_out.empty()) {  // per-tile column sums, [image][tile][npad of all channel groups] fp32
+        const size_t need = size_t(max_batch_) * P->grid_h * P->grid_w * P->gap_np_total;
         auto& buf = gap_parts_[s.id];
         if (buf.second < need) {
             // grow only; the old buffer stays allocated until the engine dies
@@ -410,7 +426,7 @@ std::string Engine::autotune(int batch, int reps, int topk) {
         std::map<std::tuple<int, int, int, int>, int> per_mode;
         std::map<std::tuple<int, int, int, int>, const BCandidate*> biggest;  // largest tile of each mode
         for (const BCandidate& c : all) {
-            const auto key = std::make_tuple(c.nxb, c.wres, c.slots * 1000 + c.chunk / 1024, c.epi_warps * 4 + c.tsets);
+            const auto key = std::make_tuple(c.nxb, c.wres, c.slots * 1000 + c.chunk / 1024, (c.epi_warps * 4 + c.tsets) * 16 + c.nsplit);
             if (per_mode[key]++ < topk) cands.push_back(c);
             const BCandidate*& bg = biggest[key];
             if (!bg || c.th * c.tw > bg->th * bg->tw) bg = &c;
@@ -421,7 +437,7 @@ std::string Engine::autotune(int batch, int reps, int topk) {
             bool have = false;
             for (const BCandidate& d : cands) have |= d.th == c->th && d.tw == c->tw && d.nxb == c->nxb && d.wres == c->wres &&
                                                       d.slots == c->slots && d.epi_warps == c->epi_warps && d.tsets == c->tsets &&
-                                                      d.chunk == c->chunk;
+                                                      d.chunk == c->chunk && d.nsplit == c->nsplit;
             if (!have) cands.push_back(*c);
         }
         float best_ms = 1e30f;
@@ -434,7 +450,7 @@ std::string Engine::autotune(int batch, int reps, int topk) {
                 apply_candidate(t, c);
                 t.grid_all = ga;
                 std::unique_ptr<BParams> P = build_bparams(t);
-                if (ga && P->ctas_per_sm * 148LL >= (long long)P->grid_h * P->grid_w * P->cgroups * batch) {
+                if (ga && P->ctas_per_sm * 148LL >= (long long)P->grid_h * P->grid_w * P->cgroups * batch * std::max(1, P->nsplit)) {
                     cudaFree(const_cast<void*>(P->dev_copy));
                     continue;  // persistent grid already covers every tile
                 }
@@ -448,8 +464,8 @@ std::string Engine::autotune(int batch, int reps, int topk) {
                 ms /= float(reps);
                 ++tried;
                 if (knobs_.tune_verbose)
-                    std::fprintf(stderr, "[xlf] tune %s: tile %dx%d nxb %d wres %d slots %d grid_all %d ew %d ts %d smem %d: %.1f us (model %.0f)\n",
-                                 s.id.c_str(), t.tile_h, t.tile_w, t.nxb, t.wres, t.ring_slots, t.grid_all, t.epi_warps, t.tsets, P->smem_bytes,
+                    std::fprintf(stderr, "[xlf] tune %s: tile %dx%d nxb %d wres %d slots %d grid_all %d ew %d ts %d ns %d smem %d: %.1f us (model %.0f)\n",
+                                 s.id.c_str(), t.tile_h, t.tile_w, t.nxb, t.wres, t.ring_slots, t.grid_all, t.epi_warps, t.tsets, t.nsplit, P->smem_bytes,
                                  ms * 1000.0f, c.model);
                 if (ms < best_ms) {
                     if (bestP) cudaFree(const_cast<void*>(bestP->dev_copy));
@@ -467,7 +483,7 @@ std::string Engine::autotune(int batch, int reps, int topk) {
         js << (first ? "" : ",") << "{\"id\":\"" << s.id << "\",\"tried\":" << tried << ",\"us\":" << best_ms * 1000.0f
            << ",\"tile\":[" << s.tile_h << "," << s.tile_w << "],\"nxb\":" << s.nxb << ",\"wres\":" << s.wres
            << ",\"ring_slots\":" << s.ring_slots << ",\"ring_chunk\":" << s.ring_chunk << ",\"grid_all\":" << s.grid_all << ",\"epi_warps\":" << s.epi_warps
-           << ",\"tsets\":" << s.tsets << ",\"smem_bytes\":" << s.smem_bytes << "}";
+           << ",\"tsets\":" << s.tsets << ",\"nsplit\":" << s.nsplit << ",\"smem_bytes\":" << s.smem_bytes << "}";
         first = false;
     }
     js << "]";
@@ -521,7 +537,7 @@ void Engine::apply_tuning(const std::string& js) {
         t.tile_h = std::atoi(obj.c_str() + tb + 1);
         t.tile_w = std::atoi(obj.c_str() + tc + 1);
         num(obj, "nxb", t.nxb), num(obj, "wres", t.wres), num(obj, "ring_slots", t.ring_slots), num(obj, "ring_chunk", t.ring_chunk);
-        num(obj, "grid_all", t.grid_all), num(obj, "epi_warps", t.epi_warps), num(obj, "tsets", t.tsets);
+        num(obj, "grid_all", t.grid_all), num(obj, "epi_warps", t.epi_warps), num(obj, "tsets", t.tsets), num(obj, "nsplit", t.nsplit);
         // layout_tc rejects staging / accumulator-set / ring values the kernel
         // cannot run (nxb, tsets in {1, 2}; 1 <= ring_slots <= kRingMax; a
         // ring slot holding at least one K step)
@@ -569,6 +585,7 @@ Engine::~Engine() {
         for (auto& P : x->bp)
             if (P) cudaFree(const_cast<void*>(P->dev_copy));
     for (void* p : retired_) cudaFree(p);
+    for (auto& [k, p] : packed_) cudaFree(p);
     if (copy_in_) {
         cudaStreamDestroy(copy_in_), cudaStreamDestroy(copy_out_);
         for (cudaEvent_t ev : chunk_ev_) cudaEventDestroy(ev);
@@ -636,7 +653,7 @@ void Engine::launch_tc_step(size_t i, int n0, int count, cudaStream_t st) {
     const TensorSlot& t = slot(s.gap_out);
     const Layer& pool = *g_.find_layer(s.gap_out);
     const float scale = 1.0f / float(pool.pool->kernel * pool.pool->kernel);
-    cuda_check(launch_gap_finish_tc(tc_es_, P.gap_part, P.grid_h * P.grid_w, P.ops[0].npad, scale, allocs_[size_t(t.alloc)], t.cstride, t.coff,
+    cuda_check(launch_gap_finish_tc(tc_es_, P.gap_part, P.grid_h * P.grid_w, P.gap_np_total, scale, allocs_[size_t(t.alloc)], t.cstride, t.coff,
                                     t.C, n0, count, st),
                "global average pool finish");
 }

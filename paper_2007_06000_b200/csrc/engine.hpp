@@ -81,6 +81,7 @@ private:
     void drop_derived();  // CUDA graphs + external-address descriptors of the current configurations
     std::unique_ptr<struct BParams> build_bparams(const StepSpec& s);
     std::unique_ptr<struct StemParams> build_stem(const StepSpec& s);
+    const uint8_t* packed_for(const std::string& layer, int nb, int nblocks);
     void launch_tc_step(size_t i, int n0, int count, cudaStream_t st);
     const TensorSlot& slot(const std::string& n) const;
     const TensorSlot& readable(const std::string& n) const;
@@ -102,6 +103,8 @@ private:
     std::vector<unsigned long long*> traces_;                // trace buffers (option trace)
     std::map<std::string, long long> wofftc_;                // packed MMA weights: byte offset per layer
     void* weights_tc_ = nullptr;  // packed MMA weights (bf16 / TF32)
+    std::vector<float> host_w_;   // the weights as given (after a space-to-depth rewrite): split packings
+    std::map<std::string, void*> packed_;  // layer/nb x nblocks -> packed weights of N-split ops
     int tc_es_ = 0;               // tensor-core element bytes (2 bf16, 4 TF32), 0 = fp32 SIMT kernels
     int esz_ = 4;                 // bytes per activation element in HBM
     bool s2d_ = false;            // tensor cores: first conv rewritten on a space-to-depth input

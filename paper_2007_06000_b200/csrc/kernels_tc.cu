@@ -126,6 +126,7 @@ struct BTile {
 
 // Trace stamps of the first tile of CTAs 0..kTraceCtas-1 (k = tile ordinal of the CTA).
 __device__ __forceinline__ void stamp(const BParams& P, int ev, int k = 0) {
+    if (blockIdx.y != 0) return;
     if (P.trace && P.trace_tiles && ev == kTrEnd && k < kTraceEvents && blockIdx.x < kTraceCtas) {
         unsigned long long t;
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
@@ -286,8 +287,9 @@ __device__ void w_producer(const BParams& P, uint8_t* smem, int total, uint64_t*
             const BOp& op = P.ops[i];
             if (op.kind != BOP_MMA) continue;
             const uint32_t b = uint32_t(op.nblocks * op.ksteps * op.nb * 32);
+            const uint8_t* src = op.wmma + (op.gch ? op.gwb * blockIdx.y : 0);  // this CTA row's channel group
             for (uint32_t o = 0; o < b; o += 65536)  // pieces of <= 64 KB
-                bulk_g2s(smem + P.wres_off + op.wofs + o, op.wmma + o, min(65536u, b - o), bar_w);
+                bulk_g2s(smem + P.wres_off + op.wofs + o, src + o, min(65536u, b - o), bar_w);
         }
         return;
     }
@@ -299,7 +301,7 @@ __device__ void w_producer(const BParams& P, uint8_t* smem, int total, uint64_t*
             if (!G.mma) continue;
             for (int i = G.op0; i < G.op1; ++i) {
                 const BOp& op = P.ops[i];
-                const uint8_t* wb = op.wmma + size_t(G.nbi) * op.ksteps * op.nb * 32;
+                const uint8_t* wb = op.wmma + (op.gch ? op.gwb * blockIdx.y : 0) + size_t(G.nbi) * op.ksteps * op.nb * 32;
                 for (int s0 = 0; s0 < op.ksteps; s0 += op.chunk_steps, ++c) {
                     const int steps = min(op.chunk_steps, op.ksteps - s0);
                     const int slot = c % slots;
@@ -459,6 +461,11 @@ __device__ __forceinline__ EpiOp<T> epi_op(const BParams& P, const BOp& op, uint
     e.gap_np = op.gap ? op.nblocks * op.nb : 0;
     e.org_mul = op.org_mul, e.org_sub = op.org_sub, e.H = op.H, e.W = op.W;
     e.out_cstride = op.out_cstride, e.out_coff = op.out_coff;
+    if (op.gch) {  // channel group blockIdx.y: channels [g*gch, g*gch + gch) stored at their offset
+        const int g0 = int(blockIdx.y) * op.gch;
+        e.out_coff += g0;
+        e.cend = max(0, min(op.gch, e.cend - g0));
+    }
     e.tile_h = P.tile_h, e.tile_w = P.tile_w, e.grid_h = P.grid_h, e.grid_w = P.grid_w;
     e.buf = nullptr, e.buf_ew = 0, e.buf_plane = 0;
     if (op.buf >= 0) {
@@ -936,7 +943,8 @@ __global__ void __launch_bounds__(Cta<EW>::threads, Cta<EW>::min_blocks) fused_t
             const BOp& op = P.ops[i];
             if (op.bias_smem < 0) continue;
             float* dst = reinterpret_cast<float*>(smem + op.bias_smem);
-            for (int k = threadIdx.x; k < op.npad; k += kCompute) dst[k] = __ldg(op.bias + k);
+            const int g0 = op.gch ? int(blockIdx.y) * op.gch : 0;  // channel group of this CTA row
+            for (int k = threadIdx.x; k < op.npad; k += kCompute) dst[k] = g0 + k < op.cout ? __ldg(op.bias + g0 + k) : 0.0f;
             if (op.gap)
                 for (int k = threadIdx.x; k < 4 * op.npad; k += kCompute) reinterpret_cast<float*>(smem + P.gap_off)[k] = 0.0f;
         }
@@ -998,7 +1006,7 @@ __global__ void __launch_bounds__(Cta<EW>::threads, Cta<EW>::min_blocks) fused_t
             if (KIND == kGap) {  // this tile's column sums -> gap_part[image][tile][c], reset
                 float* gsum = reinterpret_cast<float*>(smem + P.gap_off);
                 const int per_img = P.grid_h * P.grid_w;
-                float* dst = P.gap_part + (size_t(t.n) * per_img + t.ty * P.grid_w + t.tx) * gap_np;
+                float* dst = P.gap_part + (size_t(t.n) * per_img + t.ty * P.grid_w + t.tx) * P.gap_np_total + blockIdx.y * gap_np;
                 for (int c = threadIdx.x; c < gap_np; c += kCompute) {
                     float a = 0.0f;
 #pragma unroll
@@ -1201,10 +1209,12 @@ int occupancy_t(int smem_bytes, int tmem_cols, int epi_warps, int kind) {
 template <class T>
 cudaError_t launch_t(const BParams& P, int batch, cudaStream_t st, int n0) {
     const long long tiles = (long long)P.grid_h * P.grid_w * P.cgroups * batch;
-    const long long grid = P.grid_all ? tiles : std::min<long long>(tiles, (long long)sm_count() * std::max(1, P.ctas_per_sm));
+    const int ns = std::max(1, P.nsplit);  // channel groups: grid rows
+    const long long grid = P.grid_all ? tiles
+                                      : std::min<long long>(tiles, std::max<long long>(1, (long long)sm_count() * std::max(1, P.ctas_per_sm) / ns));
     if (grid < 1) return cudaSuccess;
     cudaLaunchConfig_t cfg{};
-    cfg.gridDim = dim3(static_cast<unsigned>(grid), 1u, 1u), cfg.blockDim = dim3(unsigned(P.epi_warps * 32 + 96));
+    cfg.gridDim = dim3(static_cast<unsigned>(grid), unsigned(ns), 1u), cfg.blockDim = dim3(unsigned(P.epi_warps * 32 + 96));
     cfg.dynamicSmemBytes = size_t(P.smem_bytes), cfg.stream = st;
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;

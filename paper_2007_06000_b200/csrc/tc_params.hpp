@@ -68,6 +68,11 @@ struct BOp {
     int wofs;       // MMA, resident weights: byte offset of the op's packed weights in the weight region
     int gap;        // MMA: global-average-pool epilogue (column sums per tile, no output store)
     int bias_smem;  // byte offset of the op's bias copy in shared memory (-1: none)
+    // N split over the grid's y dimension (BParams::nsplit): this op computes
+    // channels [g*gch, (g+1)*gch) in CTA row g (npad = gch; its packed weights
+    // for group g start at wmma + g*gwb bytes).  gch = 0: not split.
+    int gch;
+    long long gwb;
 };
 
 // A group is what one commit / one epilogue pass covers: consecutive MMA ops
@@ -143,6 +148,11 @@ struct alignas(64) BParams {
     int kind;         // step class (kernel instantiation): 0 MMA ops only, 1 with SIMT ops, 2 conv + global average pool
     int tsets;        // accumulator sets in TMEM (2: tile k+1's MMAs run during tile k's epilogue; needs nxb = 2)
     int es;           // bytes per activation element: 2 (bf16, kind::f16) or 4 (fp32/TF32, kind::tf32)
+    // N split: the grid is (persistent CTAs, nsplit); CTA row g computes the
+    // g-th channel group of every split op (BOp::gch) with only that group's
+    // weights resident; unsplit (stage-1 producer) ops are computed by every row.
+    int nsplit;
+    int gap_np_total;  // gap steps: channels per tile row of gap_part (all groups)
     int pdl;          // programmatic dependent launch (prologue overlaps the previous kernel's drain)
     int xrel_epi;     // 1: the epilogue warps release the staging buffer after the tile even when
                       // only MMAs read it (the earlier synchronisation structure; tested, not tuned)

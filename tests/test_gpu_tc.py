@@ -208,6 +208,11 @@ FORCED = [
     # staging buffers released by the epilogue warps
     {"no_tsep": 1, "no_pwait": 1, "xrel_epi": 1},
     {"no_nalt": 1, "xbuf": 2},
+    # output channels split over the grid's y dimension (channel groups with
+    # resident weight slices; two-stage blocks recompute their producer)
+    {"nsplit": 2, "always_fuse": 1},
+    {"nsplit": 4, "wres": 0},
+    {"nsplit": 8, "xbuf": 2, "tsets": 2},
 ]
 
 
@@ -349,3 +354,26 @@ def test_stem_kernel_matches_generic_path(prec):
         assert O.normwise(o[[0, 18, 36]], ref) <= TOL[prec]
     if prec == "tf32":
         assert np.array_equal(outs[""], outs["no_stem=1"])
+
+
+@pytest.mark.parametrize("prec", PRECS)
+def test_nsplit_matches_unsplit(prec):
+    """Channel groups compute the unsplit function: SqueezeNet logits with
+    every splittable step forced to 2 / 4 groups equal the unsplit plan up to
+    the summation order of the global-average-pool partial sums, which
+    follows the tile choice (the per-element arithmetic is identical: same
+    MMA K order, same epilogue)."""
+    import torch
+    g = X.load_graph(X.graph_path("squeezenet11"))
+    w = X.seeded_weights(g, 42)
+    outs = []
+    for opt in ("nsplit=1", "nsplit=2", "nsplit=4"):
+        e = X.Engine(g, w, "b200", prec, max_batch=5, options=opt)
+        if opt != "nsplit=1":
+            assert any(s["nsplit"] > 1 for s in e.steps), opt
+        e.set_input_seeded(42, 5)
+        e.forward(5)
+        outs.append(e.read("pool10", 5).cpu().numpy())
+    torch.cuda.synchronize()
+    for o in outs[1:]:
+        assert O.normwise(o, outs[0]) <= 1e-6
