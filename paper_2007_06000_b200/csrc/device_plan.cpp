@@ -491,6 +491,7 @@ Knobs Knobs::parse(const std::string& text) {
         else if (key == "pdl") k.pdl = need_num() != 0;
         else if (key == "no_s2d") k.no_s2d = need_num() != 0;
         else if (key == "no_stem") k.no_stem = need_num() != 0;
+        else if (key == "no_pw") k.no_pw = need_num() != 0;
         else if (key == "trace") k.trace = int(need_num());
         else if (key == "tune_verbose") k.tune_verbose = need_num() != 0;
         else if (key == "e2e_chunks") k.e2e_chunks = std::max(1, int(need_num()));

@@ -40,6 +40,7 @@ struct Knobs {
     int ctas = 0;                // cap on resident CTAs per SM
     int nsplit = 0;              // force output-channel groups (tensor-core steps that can split)
     bool pdl = true;             // programmatic dependent launch between steps
+    bool no_pw = false;          // 1x1 convs through the generic fused-block kernel, not the pointwise GEMM kernel
     bool no_stem = false;        // the first conv + max-pool through the generic fused-block kernel, not the stem kernel
     bool no_s2d = false;         // keep a stride-2 first conv on its own input (no space-to-depth rewrite)
     int trace = 0;               // 1: phase stamps of a steady tile, 2: tile end stamps

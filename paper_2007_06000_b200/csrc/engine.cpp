@@ -13,6 +13,7 @@
 
 #include "tc_params.hpp"
 #include "stem_params.hpp"
+#include "pw_params.hpp"
 #include "common.hpp"
 #include "fused_params.hpp"
 
@@ -45,6 +46,9 @@ cudaError_t launch_concat_copy_tc(int es, const void* src, int scs, int sco, voi
                                   cudaStream_t st);
 // kernels_stem.cu
 cudaError_t launch_stem(const StemParams& P, int batch, cudaStream_t st, int n0);
+// kernels_pw.cu
+cudaError_t launch_pw(const PwParams& P, int n0, int count, cudaStream_t st);
+cudaError_t launch_pw_gap_finish(const PwParams& P, int C, float scale, void* out, int cs, int coff, int n0, int count, cudaStream_t st);
 cudaError_t launch_eltwise_tc(int es, int op, const void* a, int acs, int aco, const void* b, int bcs, int bco, void* o, int ocs, int oco, int C,
                               long long pixels, cudaStream_t st);
 
@@ -214,6 +218,7 @@ Engine::Engine(const Graph& g, int device, Partition part, Precision prec, const
     params_.resize(plan_.steps.size());
     bparams_.resize(plan_.steps.size());
     stems_.resize(plan_.steps.size());
+    pws_.resize(plan_.steps.size());
     for (size_t i = 0; i < plan_.steps.size(); ++i) {
         const StepSpec& s = plan_.steps[i];
         if (s.kind != StepSpec::FUSED) continue;
@@ -225,6 +230,12 @@ Engine::Engine(const Graph& g, int device, Partition part, Precision prec, const
             stems_[i] = std::move(st);
             plan_.steps[i].tag = "stem";
             s2d_planar_ = 1;  // the stem reads the space-to-depth input row-planar (see s2d_tc)
+            continue;
+        }
+        if (auto pw = build_pw(s)) {
+            pws_[i] = std::move(pw);
+            plan_.steps[i].tag = s.gap_out.empty() ? "pointwise" : "pointwise+gap";
+            plan_.steps[i].nsplit = pws_[i]->nsplit;
             continue;
         }
         bparams_[i] = build_bparams(s);
@@ -310,6 +321,82 @@ std::unique_ptr<StemParams> Engine::build_stem(const StepSpec& s) {
                                               allocs_[size_t(xt.alloc)], dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
                                               CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (res != CUDA_SUCCESS) fail(ErrorKind::cuda, "cuTensorMapEncodeTiled (stem) failed (" + std::to_string(int(res)) + ")");
+    return P;
+}
+
+// The pointwise-conv GEMM kernel (kernels_pw.cu) takes a step that is one
+// 1x1 / stride-1 / pad-0 conv (optionally + global average pool): its pixels
+// across images form one GEMM M dimension.  Output channels are split into
+// groups whose weights stay resident (<= 128 KB per CTA).
+std::unique_ptr<PwParams> Engine::build_pw(const StepSpec& s) {
+    if (!tc_es_ || knobs_.no_pw || s.kind != StepSpec::FUSED || s.ops.size() != 1 || s.inputs.size() != 1) return nullptr;
+    const OpSpec& op = s.ops[0];
+    const Layer& l = *g_.find_layer(op.layer);
+    if (op.stage != 1 || !op.emit || !tc_mma_ok(l, tc_es_) || l.conv->kernel_h != 1 || l.conv->kernel_w != 1 || l.conv->pad != 0) return nullptr;
+    if (s2d_ && s.inputs[0] == g_.inputs[0].name) return nullptr;  // row-planar / rewritten input
+    const TensorSlot& xt = plan_.tensors.at(s.inputs[0]);
+    const int HW = xt.H * xt.W;
+    const bool gap = !s.gap_out.empty();
+    if (gap && HW < 32) return nullptr;
+    auto P = std::make_unique<PwParams>();
+    const int cpc = 16 / tc_es_, N = (l.conv->out_channels + 15) / 16 * 16;
+    P->es = tc_es_, P->HW = HW, P->coff_in = xt.coff;
+    P->ksteps = l.conv->in_channels * tc_es_ / 32;
+    P->kchunks = (P->ksteps + 3) / 4;
+    P->cout = l.conv->out_channels, P->relu = l.conv->activation == Activation::relu;
+    // channel groups: the fewest whose weights fit 128 KB resident and N <= 256
+    int G = 1;
+    for (;; ++G) {
+        const int gch = (((N + G - 1) / G) + 15) / 16 * 16;
+        if (gch <= 256 && (long long)P->ksteps * gch * 32 <= 128 * 1024) {
+            P->gch = gch;
+            break;
+        }
+        if (G > 16) return nullptr;
+    }
+    if (knobs_.nsplit > 0) {  // testing aid: force the group count when it is valid
+        const int gch = (((N + knobs_.nsplit - 1) / knobs_.nsplit) + 15) / 16 * 16;
+        if (gch <= 256 && (long long)P->ksteps * gch * 32 <= 200 * 1024 && gch * (knobs_.nsplit - 1) < P->cout) G = knobs_.nsplit, P->gch = gch;
+    }
+    P->nsplit = G;
+    P->wmma = G == 1 && P->gch == [&] { int nbk, nb; tc_nblocks(l.conv->out_channels, &nbk, &nb); return nbk == 1 ? nb : -1; }()
+                  ? static_cast<const uint8_t*>(weights_tc_) + wofftc_.at(l.name)
+                  : packed_for(l.name, P->gch, G);
+    P->gwb = (long long)P->ksteps * P->gch * 32;
+    P->bias = weights_ + plan_.b_off.at(l.name);
+    const std::string out_name = gap ? s.gap_out : l.name;
+    const TensorSlot& ot = plan_.tensors.at(gap ? l.name : out_name);
+    (void)cpc;
+    if (!gap) P->out = allocs_[size_t(ot.alloc)], P->out_cstride = ot.cstride, P->out_coff = ot.coff;
+    P->gap = gap;
+    P->ring_off = 0;
+    P->w_off = kPwStages * 128 * 128;
+    P->bias_off = P->w_off + int(P->gwb);
+    P->smem_bytes = P->bias_off + P->gch * 4;
+    P->tmem_cols = 32;
+    while (P->tmem_cols < 2 * P->gch) P->tmem_cols *= 2;
+    P->ctas_per_sm = 1;  // 10 warps x ~124 registers: one CTA per SM
+    P->pdl = knobs_.pdl ? 1 : 0;
+    if (gap) {
+        const size_t warps = size_t((max_batch_ * (long long)HW + 127) / 128) * 4;
+        const size_t need = warps * 2 * size_t(G) * P->gch;
+        auto& buf = gap_parts_[s.id];
+        if (buf.second < need) {
+            if (buf.first) retired_.push_back(buf.first);
+            cuda_check(cudaMalloc(&buf.first, need * 4), "cudaMalloc(gap partials)");
+            buf.second = need;
+        }
+        P->gap_part = buf.first;
+    }
+    // A: 2-D {cstride, max_batch * HW}, box = 128 bytes of channels x 128 pixels, 128-byte swizzle
+    const cuuint64_t dims[2] = {cuuint64_t(xt.cstride), cuuint64_t((long long)max_batch_ * HW)};
+    const cuuint64_t strides[1] = {cuuint64_t(xt.cstride) * tc_es_};
+    const cuuint32_t box[2] = {cuuint32_t(128 / tc_es_), 128};
+    const cuuint32_t estr[2] = {1, 1};
+    const CUresult res = tensor_map_encoder()(&P->amap, tc_es_ == 4 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2,
+                                              allocs_[size_t(xt.alloc)], dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                                              CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (res != CUDA_SUCCESS) fail(ErrorKind::cuda, "cuTensorMapEncodeTiled (pointwise) failed (" + std::to_string(int(res)) + ")");
     return P;
 }
 
@@ -646,6 +733,18 @@ void Engine::launch_tc_step(size_t i, int n0, int count, cudaStream_t st) {
         cuda_check(launch_stem(*stems_[i], count, st, n0), "stem (conv + max-pool, tensor cores)");
         return;
     }
+    if (pws_[i]) {
+        const PwParams& P = *pws_[i];
+        cuda_check(launch_pw(P, n0, count, st), "pointwise conv (tensor cores)");
+        const StepSpec& s = plan_.steps[i];
+        if (!s.gap_out.empty()) {
+            const TensorSlot& t = slot(s.gap_out);
+            const Layer& pool = *g_.find_layer(s.gap_out);
+            const float scale = 1.0f / float(pool.pool->kernel * pool.pool->kernel);
+            cuda_check(launch_pw_gap_finish(P, t.C, scale, allocs_[size_t(t.alloc)], t.cstride, t.coff, n0, count, st), "global average pool finish");
+        }
+        return;
+    }
     const BParams& P = *bparams_[i];
     cuda_check(launch_fused_tc(P, count, st, n0), "fused block (tensor cores)");
     const StepSpec& s = plan_.steps[i];
@@ -661,7 +760,7 @@ void Engine::launch_tc_step(size_t i, int n0, int count, cudaStream_t st) {
 bool Engine::range_capable() const {
     if (!tc_es_ || g_.inputs.size() != 1) return false;
     for (size_t i = 0; i < plan_.steps.size(); ++i)
-        if (plan_.steps[i].kind != StepSpec::FUSED || !(bparams_[i] || stems_[i])) return false;
+        if (plan_.steps[i].kind != StepSpec::FUSED || !(bparams_[i] || stems_[i] || pws_[i])) return false;
     return true;
 }
 
@@ -781,8 +880,9 @@ void Engine::forward_external(const std::vector<External>& ext, int batch, cudaS
     cuda_check(cudaSetDevice(device_), "cudaSetDevice");
     const int cpc = 16 / esz_;
     std::string key;
-    for (const auto& st : stems_)
-        if (st && !ext.empty()) fail(ErrorKind::validation, "caller-owned tensors are not supported by plans with a stem step");
+    for (size_t i = 0; i < stems_.size(); ++i)
+        if ((stems_[i] || pws_[i]) && !ext.empty())
+            fail(ErrorKind::validation, "caller-owned tensors are not supported by plans with stem / pointwise steps");
     for (const External& x : ext) {
         const TensorSlot& t = slot(x.name);
         if (s2d_ && x.name == g_.inputs[0].name)

@@ -82,6 +82,7 @@ private:
     std::unique_ptr<struct BParams> build_bparams(const StepSpec& s);
     std::unique_ptr<struct StemParams> build_stem(const StepSpec& s);
     const uint8_t* packed_for(const std::string& layer, int nb, int nblocks);
+    std::unique_ptr<struct PwParams> build_pw(const StepSpec& s);
     void launch_tc_step(size_t i, int n0, int count, cudaStream_t st);
     const TensorSlot& slot(const std::string& n) const;
     const TensorSlot& readable(const std::string& n) const;
@@ -100,6 +101,7 @@ private:
     std::vector<struct FusedParams> params_;
     std::vector<std::unique_ptr<struct BParams>> bparams_;  // tensor-core steps
     std::vector<std::unique_ptr<struct StemParams>> stems_;  // steps run by the stem kernel (conv + max-pool)
+    std::vector<std::unique_ptr<struct PwParams>> pws_;      // steps run by the pointwise-conv GEMM kernel
     std::vector<unsigned long long*> traces_;                // trace buffers (option trace)
     std::map<std::string, long long> wofftc_;                // packed MMA weights: byte offset per layer
     void* weights_tc_ = nullptr;  // packed MMA weights (bf16 / TF32)

@@ -377,3 +377,38 @@ def test_nsplit_matches_unsplit(prec):
     torch.cuda.synchronize()
     for o in outs[1:]:
         assert O.normwise(o, outs[0]) <= 1e-6
+
+
+@pytest.mark.parametrize("prec", PRECS)
+@pytest.mark.parametrize("batch,opts", [(3, ""), (37, ""), (5, "nsplit=4")])
+def test_pointwise_gemm_kernel(prec, batch, opts):
+    """1x1 convs through the pointwise GEMM kernel (kernels_pw.cu: pixels of
+    all images as one M dimension, M tiles crossing image boundaries; conv10 +
+    global average pool with per-warp, per-image partial sums) against the
+    generic kernel (no_pw=1) and the oracle, at batches whose tiles straddle
+    images unevenly."""
+    import torch
+    text = graph_text("squeezenet11")
+    og = O.load_graph(text)
+    w = O.flat_weights(og, O.seeded_weights(og, 42))
+    g = X.Graph(text)
+    outs = {}
+    for opt in (opts, "no_pw=1"):
+        e = X.Engine(g, w, "b200", prec, max_batch=batch, options=opt)
+        tags = [s["tag"] for s in e.steps]
+        assert ("pointwise+gap" in tags) == (opt != "no_pw=1"), tags
+        e.set_input_seeded(42, batch)
+        e.forward(batch)
+        outs[opt] = {n: e.read(n, batch).cpu().numpy() for n in ("fire9_squeeze", "pool10")}
+    torch.cuda.synchronize()
+    sample = [0, batch - 1]
+    x = O.seeded_batch(og, 42, batch)[sample]
+    ref = O.run_batch(og, x, O.seeded_weights(og, 42), ["fire9_squeeze", "pool10"])
+    # the network output against the oracle (the tolerance's scope); the deep
+    # intermediate against the generic kernel: both paths accumulate the same
+    # 20 layers of bf16 / TF32 rounding before it
+    assert O.normwise(outs[opts]["pool10"][sample], ref["pool10"]) <= TOL[prec]
+    for n in ("fire9_squeeze", "pool10"):
+        assert O.normwise(outs[opts][n], outs["no_pw=1"][n]) <= TOL[prec], n
+    print(prec, batch, opts, "fire9_squeeze vs oracle: pw", O.normwise(outs[opts]["fire9_squeeze"][sample], ref["fire9_squeeze"]),
+          "generic", O.normwise(outs["no_pw=1"]["fire9_squeeze"][sample], ref["fire9_squeeze"]))
