@@ -492,6 +492,10 @@ Knobs Knobs::parse(const std::string& text) {
         else if (key == "no_s2d") k.no_s2d = need_num() != 0;
         else if (key == "no_stem") k.no_stem = need_num() != 0;
         else if (key == "no_pw") k.no_pw = need_num() != 0;
+        else if (key == "no_fire") k.no_fire = need_num() != 0;
+        else if (key == "fire_g") k.fire_g = int(need_num());
+        else if (key == "fire_r") k.fire_r = int(need_num());
+        else if (key == "fire_nsplit") k.fire_nsplit = int(need_num());
         else if (key == "trace") k.trace = int(need_num());
         else if (key == "tune_verbose") k.tune_verbose = need_num() != 0;
         else if (key == "e2e_chunks") k.e2e_chunks = std::max(1, int(need_num()));
@@ -548,6 +552,15 @@ DevicePlan plan_device(const Graph& g, Partition part, int batch_hint, int smem_
     std::vector<StepSpec> steps;
     for (const FusionBlock& b : ordered) {
         StepSpec s = step_for_block(g, b);
+        // Split blocks the fire kernel takes stay fused: its squeeze plane never
+        // leaves shared memory and its units are whole images or row bands, so
+        // neither the generic kernel's tile limits nor the tile-size penalty the
+        // cost model below prices apply.
+        if (tc && b.fused() && fire_feasible(g, s, tc_es, batch_hint, knobs)) {
+            tile(s);  // generic geometry for the statistics only (the engine replaces it)
+            steps.push_back(s);
+            continue;
+        }
         if (s.kind == StepSpec::FUSED && !tile(s)) {
             if (!b.fused()) fail(ErrorKind::infeasible, "layer " + b.members[0] + " does not fit shared memory at any tile");
             // tensor cores: conv -> global average pool runs as one kernel
@@ -626,11 +639,13 @@ DevicePlan plan_device(const Graph& g, Partition part, int batch_hint, int smem_
     // one kernel (one staged input region), if the union still fits.
     if (part == Partition::b200) {
         const double mb_max_weight = knobs.mb_max_weight;
-        std::vector<char> gone(steps.size(), 0);
+        std::vector<char> gone(steps.size(), 0), fire(steps.size(), 0);
+        // steps the fire kernel runs keep their own kernel
+        for (size_t i = 0; i < steps.size(); ++i) fire[i] = tc && fire_feasible(g, steps[i], tc_es, batch_hint, knobs);
         for (size_t i = 0; i < steps.size(); ++i) {
-            if (gone[i] || steps[i].kind != StepSpec::FUSED || steps[i].inputs.size() != 1) continue;
+            if (gone[i] || fire[i] || steps[i].kind != StepSpec::FUSED || steps[i].inputs.size() != 1) continue;
             for (size_t j = i + 1; j < steps.size(); ++j) {
-                if (gone[j] || steps[j].kind != StepSpec::FUSED || steps[j].inputs != steps[i].inputs) continue;
+                if (gone[j] || fire[j] || steps[j].kind != StepSpec::FUSED || steps[j].inputs != steps[i].inputs) continue;
                 if (steps[j].out_h != steps[i].out_h || steps[j].out_w != steps[i].out_w) continue;
                 StepSpec m = steps[i];
                 const int base = int(m.ops.size());

@@ -43,6 +43,8 @@ struct Knobs {
     bool no_pw = false;          // 1x1 convs through the generic fused-block kernel, not the pointwise GEMM kernel
     bool no_stem = false;        // the first conv + max-pool through the generic fused-block kernel, not the stem kernel
     bool no_s2d = false;         // keep a stride-2 first conv on its own input (no space-to-depth rewrite)
+    bool no_fire = false;        // split-mode squeeze -> expand blocks through the generic fused-block kernel, not the fire kernel
+    int fire_g = 0, fire_r = 0, fire_nsplit = 0;  // force the fire kernel's unit (G images / R-row bands) and channel groups
     int trace = 0;               // 1: phase stamps of a steady tile, 2: tile end stamps
     bool tune_verbose = false;   // autotune prints every timing to stderr
     int e2e_chunks = 4;          // run_host pipeline depth
@@ -130,6 +132,12 @@ std::vector<FusionBlock> detect_fusion_blocks_b200(const Graph& g);
 // geometry (device_plan_tc.cpp); tc_es = 0: the fp32 SIMT kernel.
 DevicePlan plan_device(const Graph& g, Partition part, int batch_hint = 1, int smem_budget_bytes = 227 * 1024, int tc_es = 0,
                        const Knobs& knobs = Knobs{});
+
+// fire_plan.cpp: steps the fire kernel (kernels_fire.cu) runs -- a 1x1 squeeze
+// staged on chip feeding stride-1 "same" expand convs (k <= 3) of one width.
+bool fire_step_ok(const Graph& g, const StepSpec& s, int es);
+// ... and the kernel has a unit / channel split that fits at `batch` images.
+bool fire_feasible(const Graph& g, const StepSpec& s, int es, int batch, const Knobs& k);
 
 // device_plan_tc.cpp
 bool tc_mma_ok(const Layer& l, int es);

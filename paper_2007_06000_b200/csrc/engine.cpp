@@ -4,6 +4,7 @@
 #include <cudaTypedefs.h>
 
 #include <algorithm>
+#include <array>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -14,6 +15,7 @@
 #include "tc_params.hpp"
 #include "stem_params.hpp"
 #include "pw_params.hpp"
+#include "fire_params.hpp"
 #include "common.hpp"
 #include "fused_params.hpp"
 
@@ -48,6 +50,11 @@ cudaError_t launch_concat_copy_tc(int es, const void* src, int scs, int sco, voi
 cudaError_t launch_stem(const StemParams& P, int batch, cudaStream_t st, int n0);
 // kernels_pw.cu
 cudaError_t launch_pw(const PwParams& P, int n0, int count, cudaStream_t st);
+cudaError_t launch_fire(const FireParams& P, int n0, int count, cudaStream_t st);
+int fire_layout(FireParams& P, int nst, int nplane, bool staged);
+void fire_shape(const Graph& g, const StepSpec& s, int es, FireParams& P);
+bool fire_choose(FireParams& P, int batch, int sms, int force_nsplit, int force_g, int force_r, double* model_out);
+std::vector<std::pair<double, FireParams>> fire_candidates(const FireParams& P, int batch, int sms, int force_nsplit, int force_g, int force_r);
 cudaError_t launch_pw_gap_finish(const PwParams& P, int C, float scale, void* out, int cs, int coff, int n0, int count, cudaStream_t st);
 cudaError_t launch_eltwise_tc(int es, int op, const void* a, int acs, int aco, const void* b, int bcs, int bco, void* o, int ocs, int oco, int C,
                               long long pixels, cudaStream_t st);
@@ -219,6 +226,7 @@ Engine::Engine(const Graph& g, int device, Partition part, Precision prec, const
     bparams_.resize(plan_.steps.size());
     stems_.resize(plan_.steps.size());
     pws_.resize(plan_.steps.size());
+    fires_.resize(plan_.steps.size());
     for (size_t i = 0; i < plan_.steps.size(); ++i) {
         const StepSpec& s = plan_.steps[i];
         if (s.kind != StepSpec::FUSED) continue;
@@ -230,6 +238,16 @@ Engine::Engine(const Graph& g, int device, Partition part, Precision prec, const
             stems_[i] = std::move(st);
             plan_.steps[i].tag = "stem";
             s2d_planar_ = 1;  // the stem reads the space-to-depth input row-planar (see s2d_tc)
+            continue;
+        }
+        if (auto fp = build_fire(s)) {
+            fires_[i] = std::move(fp);
+            StepSpec& t = plan_.steps[i];
+            t.tag = "fire";
+            t.nsplit = fires_[i]->nsplit;
+            t.tile_h = fires_[i]->G > 1 ? fires_[i]->G * fires_[i]->H : fires_[i]->R;  // unit: G images or an R-row band
+            t.tile_w = fires_[i]->W;
+            t.smem_bytes = fires_[i]->smem_bytes;
             continue;
         }
         if (auto pw = build_pw(s)) {
@@ -400,6 +418,56 @@ std::unique_ptr<PwParams> Engine::build_pw(const StepSpec& s) {
     return P;
 }
 
+// The fire kernel (kernels_fire.cu) takes a split block whose producer is a
+// 1x1 squeeze staged on chip and whose consumers are stride-1 "same" expand
+// convs of one width (fire_step_ok); its unit / channel split / ring are
+// chosen by fire_choose at max_batch.
+std::unique_ptr<FireParams> Engine::build_fire(const StepSpec& s, int fns, int fg, int fr) {
+    int th, tw;
+    if (!tc_es_ || knobs_.no_fire || !fire_step_ok(g_, s, tc_es_) || knobs_.forced_tile(s, &th, &tw)) return nullptr;
+    if (s2d_ && s.inputs[0] == g_.inputs[0].name) return nullptr;  // row-planar / rewritten input
+    const Layer& sq = *g_.find_layer(s.ops[0].layer);
+    const TensorSlot& xt = plan_.tensors.at(s.inputs[0]);
+    auto P = std::make_unique<FireParams>();
+    const int es = tc_es_;
+    fire_shape(g_, s, es, *P);
+    P->coff_in = xt.coff;
+    P->sq_bias = weights_ + plan_.b_off.at(sq.name);
+    for (int o = 0; o < P->nops; ++o) {
+        const Layer& l = *g_.find_layer(s.ops[size_t(o) + 1].layer);
+        FireOp& op = P->op[o];
+        op.bias = weights_ + plan_.b_off.at(l.name);
+        const TensorSlot& ot = plan_.tensors.at(l.name);
+        op.out = allocs_[size_t(ot.alloc)], op.out_cstride = ot.cstride, op.out_coff = ot.coff;
+    }
+    int sms = 148;
+    cuda_check(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device_), "SM count");
+    double model = 0;
+    if (fns <= 0 && fg <= 0 && fr <= 0) fns = knobs_.fire_nsplit, fg = knobs_.fire_g, fr = knobs_.fire_r;
+    if (!fire_choose(*P, max_batch_, sms, fns, fg, fr, &model)) return nullptr;
+    P->wsq = packed_for(sq.name, P->S, 1);
+    for (int o = 0; o < P->nops; ++o) P->op[o].w = packed_for(s.ops[size_t(o) + 1].layer, P->gch, P->nsplit);
+    P->pdl = knobs_.pdl ? 1 : 0;
+    if (knobs_.trace) {  // globaltimer stamps of CTA (0, 0) (profiling aid)
+        unsigned long long* tr = nullptr;
+        const size_t n = size_t(3) * kFireTraceN * 2;
+        cuda_check(cudaMalloc(&tr, n * 8), "cudaMalloc(trace)");
+        cuda_check(cudaMemset(tr, 0, n * 8), "cudaMemset(trace)");
+        P->trace = tr;
+        traces_.push_back(tr);
+    }
+    // squeeze A: 2-D {cstride, max_batch * HW}, box = 128 bytes of channels x 128 pixels, 128-byte swizzle
+    const cuuint64_t dims[2] = {cuuint64_t(xt.cstride), cuuint64_t((long long)max_batch_ * P->HW)};
+    const cuuint64_t strides[1] = {cuuint64_t(xt.cstride) * es};
+    const cuuint32_t box[2] = {cuuint32_t(128 / es), 128};
+    const cuuint32_t estr[2] = {1, 1};
+    const CUresult res = tensor_map_encoder()(&P->amap, es == 4 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2,
+                                              allocs_[size_t(xt.alloc)], dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                                              CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (res != CUDA_SUCCESS) fail(ErrorKind::cuda, "cuTensorMapEncodeTiled (fire) failed (" + std::to_string(int(res)) + ")");
+    return P;
+}
+
 // Packed weights of `layer` with nblocks x nb columns (N-split ops: one block
 // per channel group), built once per shape from the host copy.
 const uint8_t* Engine::packed_for(const std::string& layer, int nb, int nblocks) {
@@ -504,6 +572,50 @@ std::string Engine::autotune(int batch, int reps, int topk) {
     std::ostringstream js;
     js << "[";
     bool first = true;
+    // fire steps: the model's best configurations of every channel split (and
+    // the current one) timed on the device; the fastest is kept
+    for (size_t i = 0; i < plan_.steps.size(); ++i) {
+        if (!fires_[i]) continue;
+        const StepSpec& s = plan_.steps[i];
+        FireParams shape{};
+        fire_shape(g_, s, tc_es_, shape);
+        std::vector<std::array<int, 3>> cands = {{fires_[i]->nsplit, fires_[i]->G, fires_[i]->R}};
+        std::map<int, int> per_split;
+        for (const auto& [model, Q] : fire_candidates(shape, batch, 148, 0, 0, 0)) {
+            const std::array<int, 3> c = {Q.nsplit, Q.G, Q.R};
+            if (per_split[Q.nsplit]++ < topk + 2 && std::find(cands.begin(), cands.end(), c) == cands.end()) cands.push_back(c);
+        }
+        float best_ms = 1e30f;
+        std::unique_ptr<FireParams> bestP;
+        int tried = 0;
+        for (const auto& c : cands) {
+            std::unique_ptr<FireParams> P = build_fire(s, c[0], c[1], c[2]);
+            if (!P) continue;
+            cuda_check(launch_fire(*P, 0, batch, st), "autotune warm-up");
+            cuda_check(cudaEventRecord(e0, st), "cudaEventRecord");
+            for (int r = 0; r < reps; ++r) cuda_check(launch_fire(*P, 0, batch, st), "autotune launch");
+            cuda_check(cudaEventRecord(e1, st), "cudaEventRecord");
+            cuda_check(cudaEventSynchronize(e1), "cudaEventSynchronize");
+            float ms = 0;
+            cuda_check(cudaEventElapsedTime(&ms, e0, e1), "cudaEventElapsedTime");
+            ms /= float(reps);
+            ++tried;
+            if (knobs_.tune_verbose)
+                std::fprintf(stderr, "[xlf] tune %s (fire): nsplit %d G %d R %d ring %d planes %d smem %d: %.1f us\n", s.id.c_str(), P->nsplit, P->G,
+                             P->R, P->nst, P->nplane, P->smem_bytes, ms * 1000.0f);
+            if (ms < best_ms) best_ms = ms, bestP = std::move(P);
+        }
+        if (!bestP) continue;
+        fires_[i] = std::move(bestP);
+        StepSpec& t = plan_.steps[i];
+        t.nsplit = fires_[i]->nsplit;
+        t.tile_h = fires_[i]->G > 1 ? fires_[i]->G * fires_[i]->H : fires_[i]->R;
+        t.smem_bytes = fires_[i]->smem_bytes;
+        js << (first ? "" : ",") << "{\"id\":\"" << s.id << "\",\"kernel\":\"fire\",\"tried\":" << tried << ",\"us\":" << best_ms * 1000.0f
+           << ",\"nsplit\":" << fires_[i]->nsplit << ",\"G\":" << fires_[i]->G << ",\"R\":" << fires_[i]->R << ",\"smem_bytes\":" << fires_[i]->smem_bytes
+           << "}";
+        first = false;
+    }
     for (size_t i = 0; i < plan_.steps.size(); ++i) {
         StepSpec& s = plan_.steps[i];
         if (s.kind != StepSpec::FUSED || !bparams_[i]) continue;
@@ -602,6 +714,7 @@ void Engine::apply_tuning(const std::string& js) {
         return true;
     };
     std::vector<std::pair<size_t, StepSpec>> todo;
+    std::vector<std::pair<size_t, std::array<int, 3>>> fire_todo;
     size_t pos = 0;
     while ((pos = js.find('{', pos)) != std::string::npos) {
         const size_t end = js.find('}', pos);
@@ -615,6 +728,14 @@ void Engine::apply_tuning(const std::string& js) {
         const std::string id = obj.substr(is + 1, ie - is - 1);
         size_t i = 0;
         while (i < plan_.steps.size() && plan_.steps[i].id != id) ++i;
+        if (i < plan_.steps.size() && fires_[i]) {  // fire step: channel split and unit
+            int ns = 0, G = 0, R = 0;
+            if (!num(obj, "nsplit", ns) || !num(obj, "G", G) || !num(obj, "R", R))
+                fail(ErrorKind::parse, "tuning report: fire step '" + id + "' needs \"nsplit\", \"G\" and \"R\"");
+            if (ns < 1 || G < 1 || R < 1) fail(ErrorKind::infeasible, "tuning report: configuration of step '" + id + "' is not feasible for this plan");
+            fire_todo.push_back({i, {ns, G, R}});
+            continue;
+        }
         if (i == plan_.steps.size() || !bparams_[i]) fail(ErrorKind::validation, "tuning report: no tensor-core fused step '" + id + "'");
         StepSpec t = plan_.steps[i];
         const size_t tv = at(obj, "tile");
@@ -635,8 +756,22 @@ void Engine::apply_tuning(const std::string& js) {
         t.smem_bytes = int(sm);
         todo.emplace_back(i, t);
     }
+    std::vector<std::unique_ptr<FireParams>> fire_built;
+    for (auto& [i, c] : fire_todo) {
+        fire_built.push_back(build_fire(plan_.steps[i], c[0], c[1], c[2]));
+        if (!fire_built.back() || fire_built.back()->nsplit != c[0] || fire_built.back()->G != c[1] || fire_built.back()->R != c[2])
+            fail(ErrorKind::infeasible, "tuning report: configuration of step '" + plan_.steps[i].id + "' is not feasible for this plan");
+    }
     // captured forwards and external-address descriptors hold the current configurations
     drop_derived();
+    for (size_t k = 0; k < fire_todo.size(); ++k) {
+        const size_t i = fire_todo[k].first;
+        fires_[i] = std::move(fire_built[k]);
+        StepSpec& t = plan_.steps[i];
+        t.nsplit = fires_[i]->nsplit;
+        t.tile_h = fires_[i]->G > 1 ? fires_[i]->G * fires_[i]->H : fires_[i]->R;
+        t.smem_bytes = fires_[i]->smem_bytes;
+    }
     std::vector<std::unique_ptr<BParams>> built;
     for (auto& [i, t] : todo) built.push_back(build_bparams(t));
     for (size_t k = 0; k < todo.size(); ++k) {
@@ -733,6 +868,10 @@ void Engine::launch_tc_step(size_t i, int n0, int count, cudaStream_t st) {
         cuda_check(launch_stem(*stems_[i], count, st, n0), "stem (conv + max-pool, tensor cores)");
         return;
     }
+    if (fires_[i]) {
+        cuda_check(launch_fire(*fires_[i], n0, count, st), "fire block (squeeze -> expand, tensor cores)");
+        return;
+    }
     if (pws_[i]) {
         const PwParams& P = *pws_[i];
         cuda_check(launch_pw(P, n0, count, st), "pointwise conv (tensor cores)");
@@ -760,7 +899,7 @@ void Engine::launch_tc_step(size_t i, int n0, int count, cudaStream_t st) {
 bool Engine::range_capable() const {
     if (!tc_es_ || g_.inputs.size() != 1) return false;
     for (size_t i = 0; i < plan_.steps.size(); ++i)
-        if (plan_.steps[i].kind != StepSpec::FUSED || !(bparams_[i] || stems_[i] || pws_[i])) return false;
+        if (plan_.steps[i].kind != StepSpec::FUSED || !(bparams_[i] || stems_[i] || pws_[i] || fires_[i])) return false;
     return true;
 }
 
@@ -914,10 +1053,14 @@ void Engine::forward_external(const std::vector<External>& ext, int batch, cudaS
         try {
             set->bp.resize(plan_.steps.size());
             set->fp.resize(plan_.steps.size());
+            set->fr.resize(plan_.steps.size());
             for (size_t i = 0; i < plan_.steps.size(); ++i) {
                 const StepSpec& s = plan_.steps[i];
                 if (s.kind != StepSpec::FUSED) continue;
-                if (tc_es_) set->bp[i] = build_bparams(s);
+                if (fires_[i]) {  // same configuration, the caller's addresses
+                    set->fr[i] = build_fire(s, fires_[i]->nsplit, fires_[i]->G, fires_[i]->R);
+                    if (!set->fr[i]) fail(ErrorKind::internal, "step " + s.id + ": fire kernel descriptor for caller-owned tensors");
+                } else if (tc_es_) set->bp[i] = build_bparams(s);
                 else set->fp[i] = make_params(g_, plan_, s, allocs_, weights_);
             }
         } catch (...) {
@@ -936,7 +1079,7 @@ void Engine::forward_external(const std::vector<External>& ext, int batch, cudaS
         ExtSet* x;
         void flip() {
             std::swap(e->allocs_, x->allocs), std::swap(e->plan_.tensors, x->tensors);
-            std::swap(e->bparams_, x->bp), std::swap(e->params_, x->fp);
+            std::swap(e->bparams_, x->bp), std::swap(e->params_, x->fp), std::swap(e->fires_, x->fr);
         }
         ~Swap() { flip(); }
     } sw{this, &x};
@@ -1049,6 +1192,11 @@ namespace xlf {
 
 std::vector<unsigned long long> Engine::trace(int index) const {
     if (index < 0 || index >= num_steps()) fail(ErrorKind::validation, "step index out of range");
+    if (const FireParams* F = fires_[size_t(index)].get(); F && F->trace) {
+        std::vector<unsigned long long> out(size_t(3) * kFireTraceN * 2);
+        cuda_check(cudaMemcpy(out.data(), F->trace, out.size() * 8, cudaMemcpyDeviceToHost), "trace D2H");
+        return out;
+    }
     const BParams* P = bparams_[size_t(index)].get();
     if (!P || !P->trace) fail(ErrorKind::validation, "no trace for this step (tensor-core steps of an engine created with option trace=1 only)");
     std::vector<unsigned long long> out(size_t(kTraceCtas) * kTraceEvents);

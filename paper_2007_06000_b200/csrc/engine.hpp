@@ -83,6 +83,8 @@ private:
     std::unique_ptr<struct StemParams> build_stem(const StepSpec& s);
     const uint8_t* packed_for(const std::string& layer, int nb, int nblocks);
     std::unique_ptr<struct PwParams> build_pw(const StepSpec& s);
+    // nsplit / G / R > 0 force the fire kernel's channel split / unit (else the knobs, else its model)
+    std::unique_ptr<struct FireParams> build_fire(const StepSpec& s, int nsplit = 0, int G = 0, int R = 0);
     void launch_tc_step(size_t i, int n0, int count, cudaStream_t st);
     const TensorSlot& slot(const std::string& n) const;
     const TensorSlot& readable(const std::string& n) const;
@@ -102,6 +104,7 @@ private:
     std::vector<std::unique_ptr<struct BParams>> bparams_;  // tensor-core steps
     std::vector<std::unique_ptr<struct StemParams>> stems_;  // steps run by the stem kernel (conv + max-pool)
     std::vector<std::unique_ptr<struct PwParams>> pws_;      // steps run by the pointwise-conv GEMM kernel
+    std::vector<std::unique_ptr<struct FireParams>> fires_;  // split blocks run by the fire kernel (squeeze plane on chip)
     std::vector<unsigned long long*> traces_;                // trace buffers (option trace)
     std::map<std::string, long long> wofftc_;                // packed MMA weights: byte offset per layer
     void* weights_tc_ = nullptr;  // packed MMA weights (bf16 / TF32)
@@ -125,6 +128,7 @@ private:
         std::map<std::string, TensorSlot> tensors;
         std::vector<std::unique_ptr<struct BParams>> bp;
         std::vector<struct FusedParams> fp;
+        std::vector<std::unique_ptr<struct FireParams>> fr;
     };
     std::map<std::string, std::unique_ptr<ExtSet>> ext_sets_;
 };

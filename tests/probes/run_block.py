@@ -1,6 +1,6 @@
 """Runs one graph's forward a few times (profiling target for ncu).
 
-    python tests/probes/run_block.py fire 32 bf16 b200 5 [tune]
+    python tests/probes/run_block.py fire 32 bf16 b200 5 [tune|notune] [options]
 
 With `tune`, the engine is autotuned first (as bench.py does) and only the
 forwards run inside cudaProfilerStart/Stop: profile with
@@ -20,7 +20,8 @@ def main():
     name, batch, prec, part, reps = sys.argv[1], int(sys.argv[2]), sys.argv[3], sys.argv[4], int(sys.argv[5])
     tune = len(sys.argv) > 6 and sys.argv[6] == "tune"
     g = X.load_graph(X.graph_path(name))
-    e = X.Engine(g, X.seeded_weights(g, 42), part, prec, max_batch=batch)
+    opts = sys.argv[7] if len(sys.argv) > 7 else ""
+    e = X.Engine(g, X.seeded_weights(g, 42), part, prec, max_batch=batch, options=opts)
     e.set_input_seeded(42, batch)
     if tune and prec == "bf16":
         e.forward(batch, use_graph=False)

@@ -275,11 +275,13 @@ def test_tc_tuning_report_roundtrip(prec):
     w = X.seeded_weights(g, 42)
     # one fused split step (its expand3 op is the widest: a 1 KB ring chunk is
     # smaller than one of its K steps)
-    a = X.Engine(g, w, "b200", prec, max_batch=8, options="always_fuse=1")
+    # (the generic fused-block kernel's configurations: the fire kernel's are
+    # covered by test_gpu_fire.py)
+    a = X.Engine(g, w, "b200", prec, max_batch=8, options="always_fuse=1,no_fire=1")
     a.set_input_seeded(42, 8)
     a.forward(8, use_graph=False)
     report = a.autotune(8, reps=2, topk=2)
-    b = X.Engine(g, w, "b200", prec, max_batch=8, options="always_fuse=1")
+    b = X.Engine(g, w, "b200", prec, max_batch=8, options="always_fuse=1,no_fire=1")
     b.apply_tuning(json.dumps(report))  # default separators: ", " / ": "
     keys = ("tile", "nxb", "wres", "ring_slots", "epi_warps", "tsets")
     assert [{k: s[k] for k in keys} for s in a.steps] == [{k: s[k] for k in keys} for s in b.steps]
@@ -393,13 +395,14 @@ def test_pointwise_gemm_kernel(prec, batch, opts):
     w = O.flat_weights(og, O.seeded_weights(og, 42))
     g = X.Graph(text)
     outs = {}
-    for opt in (opts, "no_pw=1"):
+    for key in (opts, "no_pw=1"):  # (no_fire: the squeezes are pointwise steps of their own)
+        opt = "no_fire=1" + ("," + key if key else "")
         e = X.Engine(g, w, "b200", prec, max_batch=batch, options=opt)
         tags = [s["tag"] for s in e.steps]
-        assert ("pointwise+gap" in tags) == (opt != "no_pw=1"), tags
+        assert ("pointwise+gap" in tags) == ("no_pw=1" not in opt), tags
         e.set_input_seeded(42, batch)
         e.forward(batch)
-        outs[opt] = {n: e.read(n, batch).cpu().numpy() for n in ("fire9_squeeze", "pool10")}
+        outs[key] = {n: e.read(n, batch).cpu().numpy() for n in ("fire9_squeeze", "pool10")}
     torch.cuda.synchronize()
     sample = [0, batch - 1]
     x = O.seeded_batch(og, 42, batch)[sample]
@@ -410,5 +413,3 @@ def test_pointwise_gemm_kernel(prec, batch, opts):
     assert O.normwise(outs[opts]["pool10"][sample], ref["pool10"]) <= TOL[prec]
     for n in ("fire9_squeeze", "pool10"):
         assert O.normwise(outs[opts][n], outs["no_pw=1"][n]) <= TOL[prec], n
-    print(prec, batch, opts, "fire9_squeeze vs oracle: pw", O.normwise(outs[opts]["fire9_squeeze"][sample], ref["fire9_squeeze"]),
-          "generic", O.normwise(outs["no_pw=1"]["fire9_squeeze"][sample], ref["fire9_squeeze"]))

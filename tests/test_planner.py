@@ -195,19 +195,29 @@ def test_device_plans_cover_every_layer(name, part):
 
 
 def test_b200_cost_based_fusion_decisions():
-    """bf16 B200 partition: a fused block is kept only when the planner's model
-    beats its layers as single kernels.  Fire modules at 55x55 stay fused
-    (measured 1.8x over unfused); inception-3a's 1x1-reduce -> 3x3 (221 KB of
-    weights re-streamed per small fused tile) is split; option always_fuse keeps
-    every block fused."""
-    import os
+    """bf16 B200 partition.  Split / straight blocks of a 1x1 reduce into
+    stride-1 expand convs run on the fire kernel (kernels_fire.cu: squeeze
+    plane on chip, whole-image or row-band units) and stay fused -- all eight
+    SqueezeNet fire modules and inception-3a's 1x1-reduce -> 3x3.  Without it
+    (option no_fire=1) a fused block is kept only when the planner's model
+    beats its layers as single kernels: inception's reduce -> 3x3 (221 KB of
+    weights re-streamed per small fused tile) is split; option always_fuse
+    keeps every block fused."""
     g = X.load_graph(X.graph_path("fire"))
-    tags = [s["tag"] for s in X.device_plan(g, "b200", 32, "bf16")["steps"]]
-    assert tags == ["split"]
+    steps = X.device_plan(g, "b200", 32, "bf16")["steps"]
+    assert [s["tag"] for s in steps] == ["split"]
+    g = X.load_graph(X.graph_path("squeezenet11"))
+    steps = X.device_plan(g, "b200", 256, "bf16")["steps"]
+    fires = [s for s in steps if s["tag"] == "split"]
+    assert len(fires) == 8 and all(len(s["layers"]) == 3 for s in fires), [s["layers"] for s in steps]
+    steps = X.device_plan(g, "b200", 256, "bf16", options="no_fire=1")["steps"]
+    assert any(s["layers"] == ["fire9_squeeze"] for s in steps)
     g = X.load_graph(X.graph_path("inc3a"))
     steps = X.device_plan(g, "b200", 64, "bf16")["steps"]
+    assert any(s["layers"] == ["r3", "b3"] for s in steps), [s["layers"] for s in steps]
+    steps = X.device_plan(g, "b200", 64, "bf16", options="no_fire=1")["steps"]
     assert any(s["layers"] == ["b3"] for s in steps), [s["layers"] for s in steps]
-    steps = X.device_plan(g, "b200", 64, "bf16", options="always_fuse=1")["steps"]
+    steps = X.device_plan(g, "b200", 64, "bf16", options="no_fire=1,always_fuse=1")["steps"]
     assert not any(s["layers"] == ["b3"] for s in steps)
     # the fp32 planner is unaffected (its kernels stage no weights)
     g = X.load_graph(X.graph_path("inc3a"))

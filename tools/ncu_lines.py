@@ -17,7 +17,7 @@ import subprocess
 import sys
 import tempfile
 
-KERNEL = "fused_bf16_kernel"
+KERNEL = os.environ.get("NCU_KERNEL", "fused_bf16_kernel")
 
 
 def line_map(lib, instance=""):
@@ -25,8 +25,6 @@ def line_map(lib, instance=""):
     subprocess.run(["cuobjdump", "-xelf", "all", os.path.abspath(lib)], cwd=d, capture_output=True)
     m, cur, inside = {}, None, False
     for f in os.listdir(d):
-        if "bf16" not in f:
-            continue
         out = subprocess.run(["nvdisasm", "-g", "-c", os.path.join(d, f)], capture_output=True, text=True).stdout
         for ln in out.splitlines():
             if ln.startswith(".text.") or ln.startswith("//---"):
