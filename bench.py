@@ -51,6 +51,7 @@ BLOCK_CONFIGS = [  # (config, graph, batch, precisions) -- BASELINE.json configs
     ("merge", "merge", 8, ("fp32", "tf32", "bf16")),
     ("split", "fire", 32, ("fp32", "tf32", "bf16")),
     ("inception", "inc3a", 64, ("tf32", "bf16", "fp32")),    # C4 names bf16 / TF32
+    ("depthwise", "a2", 64, ("fp32", "tf32", "bf16")),       # paper a.2: depthwise 3x3 -> 1x1
 ]
 TC = ("bf16", "tf32")
 DTYPE = {"bf16": "bf16", "tf32": "tf32", "fp32": "f32", "fp32_exact": "f32"}

@@ -580,10 +580,15 @@ std::string Engine::autotune(int batch, int reps, int topk) {
         FireParams shape{};
         fire_shape(g_, s, tc_es_, shape);
         std::vector<std::array<int, 3>> cands = {{fires_[i]->nsplit, fires_[i]->G, fires_[i]->R}};
+        // the model ranks unit shapes only roughly (it misses per-unit latency
+        // chains): time the best 8 * topk by the model, at least topk per split
         std::map<int, int> per_split;
-        for (const auto& [model, Q] : fire_candidates(shape, batch, 148, 0, 0, 0)) {
+        const auto all = fire_candidates(shape, batch, 148, 0, 0, 0);
+        for (size_t k = 0; k < all.size(); ++k) {
+            const FireParams& Q = all[k].second;
             const std::array<int, 3> c = {Q.nsplit, Q.G, Q.R};
-            if (per_split[Q.nsplit]++ < topk + 2 && std::find(cands.begin(), cands.end(), c) == cands.end()) cands.push_back(c);
+            if ((int(k) < 8 * topk || per_split[Q.nsplit] < topk) && std::find(cands.begin(), cands.end(), c) == cands.end())
+                cands.push_back(c), ++per_split[Q.nsplit];
         }
         float best_ms = 1e30f;
         std::unique_ptr<FireParams> bestP;
