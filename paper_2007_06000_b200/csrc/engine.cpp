@@ -431,6 +431,7 @@ std::unique_ptr<FireParams> Engine::build_fire(const StepSpec& s, int fns, int f
     auto P = std::make_unique<FireParams>();
     const int es = tc_es_;
     fire_shape(g_, s, es, *P);
+    P->stage_mode = knobs_.fire_stage;
     P->coff_in = xt.coff;
     P->sq_bias = weights_ + plan_.b_off.at(sq.name);
     for (int o = 0; o < P->nops; ++o) {
@@ -579,6 +580,7 @@ std::string Engine::autotune(int batch, int reps, int topk) {
         const StepSpec& s = plan_.steps[i];
         FireParams shape{};
         fire_shape(g_, s, tc_es_, shape);
+        shape.stage_mode = knobs_.fire_stage;
         std::vector<std::array<int, 3>> cands = {{fires_[i]->nsplit, fires_[i]->G, fires_[i]->R}};
         // the model ranks unit shapes only roughly (it misses per-unit latency
         // chains): time the best 8 * topk by the model, at least topk per split

@@ -65,6 +65,7 @@ struct FireParams {
     int ring_off, wsq_off, plane_off, sqbias_off, stage_off, smem_bytes;  // stage: 8 epilogue warps x 4 KB store staging (-1: direct stores)
     int pdl;
     unsigned long long* trace;  // option trace=1: 3 roles x kFireTraceN x (code, globaltimer) of CTA (0, 0)
+    int stage_mode;             // host planning only: 0 direct stores, 1 staged through shared memory (option fire_stage)
 };
 
 }  // namespace xlf

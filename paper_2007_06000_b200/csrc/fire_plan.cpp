@@ -114,17 +114,21 @@ std::vector<std::pair<double, FireParams>> fire_candidates(const FireParams& P, 
             Q.seg = P.es == 2 && gch % 64 == 0 ? 64 : 32;  // 128-byte store segments when the op's channels allow
             fire_geometry(P.H, P.W, G, R, pmax, &Q.Ts, &Q.Te, &Q.plane_cells);
             for (int o = 0; o < Q.nops; ++o) Q.op[o].gwb = (long long)Q.op[o].kh * Q.op[o].kw * (Q.S / cpc) * gch * 16;
-            // staged stores, then the deepest ring with two planes, else one
-            // plane; without store staging only if nothing else fits
+            // the deepest ring with two planes, else one plane; stores direct
+            // (staged through shared memory only on request: measured 7 %
+            // slower on fire2/3, the staging adds shared-memory traffic and a
+            // shuffle per store to a kernel bound by per-warp latency)
             int nst = 0, npl = 0;
             bool stg = true;
-            for (int st = 1; st >= 0 && !nst; --st)
+            for (int st = 0; st <= 1 && !nst; ++st) {
+                if (st != (P.stage_mode == 1 ? 1 : 0)) continue;
                 for (int pl = 2; pl >= 1 && !nst; --pl)
                     for (int s = kFireStages; s >= 3; --s)
                         if (fire_layout(Q, s, pl, st != 0) > 0) {
                             nst = s, npl = pl, stg = st != 0;
                             break;
                         }
+            }
             if (!nst) continue;
             fire_layout(Q, nst, npl, stg);
             Q.sq_cols = sq_cols;
@@ -187,6 +191,7 @@ bool fire_feasible(const Graph& g, const StepSpec& s, int es, int batch, const K
     if (k.forced_tile(s, &th, &tw)) return false;  // a reference plan's tile drives the generic kernel (xlf_block_prepare)
     FireParams P{};
     fire_shape(g, s, es, P);
+    P.stage_mode = k.fire_stage;
     return fire_choose(P, std::max(1, batch), 148, k.fire_nsplit, k.fire_g, k.fire_r, nullptr);
 }
 
