@@ -422,7 +422,7 @@ std::unique_ptr<PwParams> Engine::build_pw(const StepSpec& s) {
 // 1x1 squeeze staged on chip and whose consumers are stride-1 "same" expand
 // convs of one width (fire_step_ok); its unit / channel split / ring are
 // chosen by fire_choose at max_batch.
-std::unique_ptr<FireParams> Engine::build_fire(const StepSpec& s, int fns, int fg, int fr) {
+std::unique_ptr<FireParams> Engine::build_fire(const StepSpec& s, int fns, int fg, int fr, int sqs) {
     int th, tw;
     if (!tc_es_ || knobs_.no_fire || !fire_step_ok(g_, s, tc_es_) || knobs_.forced_tile(s, &th, &tw)) return nullptr;
     if (s2d_ && s.inputs[0] == g_.inputs[0].name) return nullptr;  // row-planar / rewritten input
@@ -432,6 +432,7 @@ std::unique_ptr<FireParams> Engine::build_fire(const StepSpec& s, int fns, int f
     const int es = tc_es_;
     fire_shape(g_, s, es, *P);
     P->stage_mode = knobs_.fire_stage;
+    P->sq_stream_mode = sqs < 0 ? knobs_.fire_sqs : sqs ? 1 : 2;
     P->coff_in = xt.coff;
     P->sq_bias = weights_ + plan_.b_off.at(sq.name);
     for (int o = 0; o < P->nops; ++o) {
@@ -581,14 +582,15 @@ std::string Engine::autotune(int batch, int reps, int topk) {
         FireParams shape{};
         fire_shape(g_, s, tc_es_, shape);
         shape.stage_mode = knobs_.fire_stage;
-        std::vector<std::array<int, 3>> cands = {{fires_[i]->nsplit, fires_[i]->G, fires_[i]->R}};
+        shape.sq_stream_mode = knobs_.fire_sqs;
+        std::vector<std::array<int, 4>> cands = {{fires_[i]->nsplit, fires_[i]->G, fires_[i]->R, fires_[i]->sq_stream}};
         // the model ranks unit shapes only roughly (it misses per-unit latency
         // chains): time the best 8 * topk by the model, at least topk per split
         std::map<int, int> per_split;
         const auto all = fire_candidates(shape, batch, 148, 0, 0, 0);
         for (size_t k = 0; k < all.size(); ++k) {
             const FireParams& Q = all[k].second;
-            const std::array<int, 3> c = {Q.nsplit, Q.G, Q.R};
+            const std::array<int, 4> c = {Q.nsplit, Q.G, Q.R, Q.sq_stream};
             if ((int(k) < 8 * topk || per_split[Q.nsplit] < topk) && std::find(cands.begin(), cands.end(), c) == cands.end())
                 cands.push_back(c), ++per_split[Q.nsplit];
         }
@@ -596,7 +598,7 @@ std::string Engine::autotune(int batch, int reps, int topk) {
         std::unique_ptr<FireParams> bestP;
         int tried = 0;
         for (const auto& c : cands) {
-            std::unique_ptr<FireParams> P = build_fire(s, c[0], c[1], c[2]);
+            std::unique_ptr<FireParams> P = build_fire(s, c[0], c[1], c[2], c[3]);
             if (!P) continue;
             cuda_check(launch_fire(*P, 0, batch, st), "autotune warm-up");
             cuda_check(cudaEventRecord(e0, st), "cudaEventRecord");
@@ -608,8 +610,8 @@ std::string Engine::autotune(int batch, int reps, int topk) {
             ms /= float(reps);
             ++tried;
             if (knobs_.tune_verbose)
-                std::fprintf(stderr, "[xlf] tune %s (fire): nsplit %d G %d R %d ring %d planes %d smem %d: %.1f us\n", s.id.c_str(), P->nsplit, P->G,
-                             P->R, P->nst, P->nplane, P->smem_bytes, ms * 1000.0f);
+                std::fprintf(stderr, "[xlf] tune %s (fire): nsplit %d G %d R %d sqs %d ring %d planes %d smem %d: %.1f us\n", s.id.c_str(), P->nsplit,
+                             P->G, P->R, P->sq_stream, P->nst, P->nplane, P->smem_bytes, ms * 1000.0f);
             if (ms < best_ms) best_ms = ms, bestP = std::move(P);
         }
         if (!bestP) continue;
@@ -619,7 +621,8 @@ std::string Engine::autotune(int batch, int reps, int topk) {
         t.tile_h = fires_[i]->G > 1 ? fires_[i]->G * fires_[i]->H : fires_[i]->R;
         t.smem_bytes = fires_[i]->smem_bytes;
         js << (first ? "" : ",") << "{\"id\":\"" << s.id << "\",\"kernel\":\"fire\",\"tried\":" << tried << ",\"us\":" << best_ms * 1000.0f
-           << ",\"nsplit\":" << fires_[i]->nsplit << ",\"G\":" << fires_[i]->G << ",\"R\":" << fires_[i]->R << ",\"smem_bytes\":" << fires_[i]->smem_bytes
+           << ",\"nsplit\":" << fires_[i]->nsplit << ",\"G\":" << fires_[i]->G << ",\"R\":" << fires_[i]->R << ",\"sqs\":" << fires_[i]->sq_stream
+           << ",\"smem_bytes\":" << fires_[i]->smem_bytes
            << "}";
         first = false;
     }
@@ -721,7 +724,7 @@ void Engine::apply_tuning(const std::string& js) {
         return true;
     };
     std::vector<std::pair<size_t, StepSpec>> todo;
-    std::vector<std::pair<size_t, std::array<int, 3>>> fire_todo;
+    std::vector<std::pair<size_t, std::array<int, 4>>> fire_todo;
     size_t pos = 0;
     while ((pos = js.find('{', pos)) != std::string::npos) {
         const size_t end = js.find('}', pos);
@@ -736,11 +739,12 @@ void Engine::apply_tuning(const std::string& js) {
         size_t i = 0;
         while (i < plan_.steps.size() && plan_.steps[i].id != id) ++i;
         if (i < plan_.steps.size() && fires_[i]) {  // fire step: channel split and unit
-            int ns = 0, G = 0, R = 0;
+            int ns = 0, G = 0, R = 0, sqs = -1;
+            num(obj, "sqs", sqs);
             if (!num(obj, "nsplit", ns) || !num(obj, "G", G) || !num(obj, "R", R))
                 fail(ErrorKind::parse, "tuning report: fire step '" + id + "' needs \"nsplit\", \"G\" and \"R\"");
             if (ns < 1 || G < 1 || R < 1) fail(ErrorKind::infeasible, "tuning report: configuration of step '" + id + "' is not feasible for this plan");
-            fire_todo.push_back({i, {ns, G, R}});
+            fire_todo.push_back({i, {ns, G, R, sqs}});
             continue;
         }
         if (i == plan_.steps.size() || !bparams_[i]) fail(ErrorKind::validation, "tuning report: no tensor-core fused step '" + id + "'");
@@ -765,8 +769,9 @@ void Engine::apply_tuning(const std::string& js) {
     }
     std::vector<std::unique_ptr<FireParams>> fire_built;
     for (auto& [i, c] : fire_todo) {
-        fire_built.push_back(build_fire(plan_.steps[i], c[0], c[1], c[2]));
-        if (!fire_built.back() || fire_built.back()->nsplit != c[0] || fire_built.back()->G != c[1] || fire_built.back()->R != c[2])
+        fire_built.push_back(build_fire(plan_.steps[i], c[0], c[1], c[2], c[3]));
+        if (!fire_built.back() || fire_built.back()->nsplit != c[0] || fire_built.back()->G != c[1] || fire_built.back()->R != c[2] ||
+            (c[3] >= 0 && fire_built.back()->sq_stream != c[3]))
             fail(ErrorKind::infeasible, "tuning report: configuration of step '" + plan_.steps[i].id + "' is not feasible for this plan");
     }
     // captured forwards and external-address descriptors hold the current configurations
@@ -1065,7 +1070,7 @@ void Engine::forward_external(const std::vector<External>& ext, int batch, cudaS
                 const StepSpec& s = plan_.steps[i];
                 if (s.kind != StepSpec::FUSED) continue;
                 if (fires_[i]) {  // same configuration, the caller's addresses
-                    set->fr[i] = build_fire(s, fires_[i]->nsplit, fires_[i]->G, fires_[i]->R);
+                    set->fr[i] = build_fire(s, fires_[i]->nsplit, fires_[i]->G, fires_[i]->R, fires_[i]->sq_stream);
                     if (!set->fr[i]) fail(ErrorKind::internal, "step " + s.id + ": fire kernel descriptor for caller-owned tensors");
                 } else if (tc_es_) set->bp[i] = build_bparams(s);
                 else set->fp[i] = make_params(g_, plan_, s, allocs_, weights_);

@@ -56,6 +56,8 @@ struct FireParams {
     FireOp op[kFireMaxOps];
     int gch, nsplit;      // channels per group of every expand op; groups (grid y)
     int nst;              // ring stages
+    int stage_bytes;      // ring stage: 128 x 128-byte input chunk (+ that K chunk's squeeze weights when sq_stream)
+    int sq_stream;        // squeeze weights streamed through the ring per K chunk instead of resident
     int nplane;           // squeeze planes (2: the next unit's squeeze overlaps this unit's expand)
     int plane_cells;      // cells per plane, incl. one leading slack cell
     int plane_bytes;      // plane_cells * 16 * schunks
@@ -66,6 +68,7 @@ struct FireParams {
     int pdl;
     unsigned long long* trace;  // option trace=1: 3 roles x kFireTraceN x (code, globaltimer) of CTA (0, 0)
     int stage_mode;             // host planning only: 0 direct stores, 1 staged through shared memory (option fire_stage)
+    int sq_stream_mode;         // host planning only: 0 either, 1 streamed squeeze weights only, 2 resident only (option fire_sqs)
 };
 
 }  // namespace xlf

@@ -63,9 +63,10 @@ int fire_layout(FireParams& P, int nst, int nplane, bool staged) {
     int off = 0;
     P.nst = nst, P.nplane = nplane;
     P.ring_off = 0;
-    off = nst * 128 * 128;
+    P.stage_bytes = 128 * 128 + (P.sq_stream ? up(4 * P.S * 32, 1024) : 0);  // stages stay 1024-aligned (SWIZZLE_128B)
+    off = nst * P.stage_bytes;
     P.wsq_off = off;
-    off = up(off + P.ksteps * P.S * 32, 128);
+    if (!P.sq_stream) off = up(off + P.ksteps * P.S * 32, 128);
     for (int o = 0; o < P.nops; ++o) {
         P.op[o].w_off = off;
         off = up(off + int(P.op[o].gwb), 128);
@@ -97,8 +98,11 @@ std::vector<std::pair<double, FireParams>> fire_candidates(const FireParams& P, 
     const int sq_cols = P.S <= 32 ? 32 : P.S <= 64 ? 64 : 128;
     const double bw_chip = 3300.0;  // HBM bytes per SM cycle, whole chip (~6.5 TB/s at 1.965 GHz)
     std::vector<std::pair<double, FireParams>> out;
+    for (int sqs : {0, 1})
     for (int ns : {1, 2, 4}) {
         if (force_nsplit > 0 && ns != force_nsplit) continue;
+        if (P.sq_stream_mode == 1 && sqs == 0) continue;
+        if (P.sq_stream_mode == 2 && sqs == 1) continue;
         if (cout % (32 * ns)) continue;  // whole 32-column store segments per op and group
         const int gch = cout / ns;
         if (gch > 256 || 2 * sq_cols + 2 * P.nops * gch > 512) continue;  // two expand accumulators (every op of an M tile each)
@@ -110,6 +114,7 @@ std::vector<std::pair<double, FireParams>> fire_candidates(const FireParams& P, 
             if (force_r > 0 && R != force_r) continue;
             if (G > 1 && G > batch) continue;
             FireParams Q = P;
+            Q.sq_stream = sqs;
             Q.nsplit = ns, Q.gch = gch, Q.G = G, Q.R = R, Q.bands = cdiv(P.H, R);
             Q.seg = P.es == 2 && gch % 64 == 0 ? 64 : 32;  // 128-byte store segments when the op's channels allow
             fire_geometry(P.H, P.W, G, R, pmax, &Q.Ts, &Q.Te, &Q.plane_cells);
@@ -149,7 +154,9 @@ std::vector<std::pair<double, FireParams>> fire_candidates(const FireParams& P, 
             const double l2 = (px_in * Q.ksteps * 32 + px_out * Q.nops * gch * P.es) / (6000.0 / active);
             // TMEM reads (64 B / cycle per SM) of every squeeze and expand accumulator
             const double tmem = (double(Q.Ts) * P.S + double(Q.Te) * Q.nops * gch) * 128 * 4 / 64.0;
-            const double unit = std::max({sq_mma + ex_mma, mem, l2, tmem * 2.0}) + (npl == 2 ? 600.0 : 1500.0);
+            // streamed squeeze weights: re-read from L2 per squeeze tile
+            const double l2w = sqs ? double(Q.Ts) * Q.ksteps * P.S * 32 / (6000.0 / active) : 0.0;
+            const double unit = std::max({sq_mma + ex_mma, mem, l2 + l2w, tmem * 2.0}) + (npl == 2 ? 600.0 : 1500.0);
             out.push_back({rounds * unit, Q});
         }
     }
@@ -192,6 +199,7 @@ bool fire_feasible(const Graph& g, const StepSpec& s, int es, int batch, const K
     FireParams P{};
     fire_shape(g, s, es, P);
     P.stage_mode = k.fire_stage;
+    P.sq_stream_mode = k.fire_sqs;
     return fire_choose(P, std::max(1, batch), 148, k.fire_nsplit, k.fire_g, k.fire_r, nullptr);
 }
 

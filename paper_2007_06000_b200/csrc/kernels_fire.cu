@@ -217,7 +217,7 @@ __global__ void __launch_bounds__(kThreads, 1) fire_kernel(const __grid_constant
 
     if (warp == kProd) {
         if (lane == 0) {
-            const uint32_t sqb = uint32_t(P.ksteps) * uint32_t(P.S) * 32u;
+            const uint32_t sqb = P.sq_stream ? 0u : uint32_t(P.ksteps) * uint32_t(P.S) * 32u;  // resident squeeze weights
             uint32_t wb = sqb;
             for (int o = 0; o < P.nops; ++o) wb += uint32_t(P.op[o].gwb);
             mbar_expect_tx(&wbar, wb);
@@ -237,8 +237,15 @@ __global__ void __launch_bounds__(kThreads, 1) fire_kernel(const __grid_constant
                         const int s = it % P.nst;
                         if (it >= P.nst) mbar_sleep_wait(&empty[s], uint32_t(it / P.nst - 1) & 1u);
                         stamp(P, 2, tn, 50, it);
-                        mbar_expect_tx(&full[s], kStageBytes);
-                        tma_2d(smem + P.ring_off + s * kStageBytes, &P.amap, P.coff_in + kc * kc_elems, U.p0 + ts * 128, &full[s]);
+                        uint8_t* stage = smem + P.ring_off + s * P.stage_bytes;
+                        if (P.sq_stream) {  // this K chunk's squeeze weights ride along with the input chunk
+                            const uint32_t b = uint32_t(min(4, P.ksteps - kc * 4)) * uint32_t(P.S) * 32u;
+                            mbar_expect_tx(&full[s], kStageBytes + b);
+                            bulk_g2s(stage + kStageBytes, P.wsq + size_t(kc) * 4 * P.S * 32, b, &full[s]);
+                        } else {
+                            mbar_expect_tx(&full[s], kStageBytes);
+                        }
+                        tma_2d(stage, &P.amap, P.coff_in + kc * kc_elems, U.p0 + ts * 128, &full[s]);
                     }
             }
         }
@@ -254,6 +261,7 @@ __global__ void __launch_bounds__(kThreads, 1) fire_kernel(const __grid_constant
             const uint64_t bsq0 = sdesc(smem_u32(smem + P.wsq_off), uint32_t(P.S) * 16u, 128u, kNoSwizzle);
             const uint32_t bsq_step = (uint32_t(P.S) * 32u) >> 4;
             const uint64_t ring0 = sdesc(ring, 16u, 1024u, kSW128);
+            const uint64_t bsq_ring = sdesc(ring + uint32_t(kStageBytes), uint32_t(P.S) * 16u, 128u, kNoSwizzle);
             const int nst = P.nst, kchunks = P.kchunks, ksteps = P.ksteps, Ts = P.Ts, nops = P.nops, gch = P.gch, Wp = P.Wp;
             const int nks = P.schunks / 2;                        // expand K steps per tap
             const uint32_t da = (2u * PS) >> 4, db = 2u * uint32_t(gch);  // next K step: A (two plane chunks), B
@@ -293,7 +301,8 @@ __global__ void __launch_bounds__(kThreads, 1) fire_kernel(const __grid_constant
                             mbar_wait(&full[s], uint32_t(it / nst) & 1u);
                             fence_after();
                             const int steps = min(4, ksteps - kc * 4);
-                            uint64_t ad = ring0 + uint64_t(s * (kStageBytes >> 4));
+                            uint64_t ad = ring0 + uint64_t(s * (P.stage_bytes >> 4));
+                            if (P.sq_stream) bd = bsq_ring + uint64_t(s * (P.stage_bytes >> 4));  // this chunk's weights in the stage
                             for (int kk = 0; kk < steps; ++kk) {
                                 FElem<T>::mma(d, ad, bd, idsq, acc);
                                 acc = 1;
