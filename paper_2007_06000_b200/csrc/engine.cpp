@@ -16,6 +16,7 @@
 #include "stem_params.hpp"
 #include "pw_params.hpp"
 #include "fire_params.hpp"
+#include "dw_params.hpp"
 #include "common.hpp"
 #include "fused_params.hpp"
 
@@ -51,6 +52,7 @@ cudaError_t launch_stem(const StemParams& P, int batch, cudaStream_t st, int n0)
 // kernels_pw.cu
 cudaError_t launch_pw(const PwParams& P, int n0, int count, cudaStream_t st);
 cudaError_t launch_fire(const FireParams& P, int n0, int count, cudaStream_t st);
+cudaError_t launch_dw(const DwParams& P, int n0, int count, cudaStream_t st);
 int fire_layout(FireParams& P, int nst, int nplane, bool staged);
 void fire_shape(const Graph& g, const StepSpec& s, int es, FireParams& P);
 bool fire_choose(FireParams& P, int batch, int sms, int force_nsplit, int force_g, int force_r, double* model_out);
@@ -227,9 +229,17 @@ Engine::Engine(const Graph& g, int device, Partition part, Precision prec, const
     stems_.resize(plan_.steps.size());
     pws_.resize(plan_.steps.size());
     fires_.resize(plan_.steps.size());
+    dws_.resize(plan_.steps.size());
     for (size_t i = 0; i < plan_.steps.size(); ++i) {
         const StepSpec& s = plan_.steps[i];
         if (s.kind != StepSpec::FUSED) continue;
+        if (auto dp = build_dw(s)) {
+            dws_[i] = std::move(dp);
+            plan_.steps[i].tag = s.ops.size() == 2 ? "depthwise+pointwise" : "depthwise";
+            plan_.steps[i].tile_h = dws_[i]->tile_h, plan_.steps[i].tile_w = dws_[i]->tile_w;
+            plan_.steps[i].smem_bytes = dws_[i]->smem_bytes;
+            continue;
+        }
         if (!tc) {
             params_[i] = make_params(g_, plan_, s, allocs_, weights_);
             continue;
@@ -415,6 +425,68 @@ std::unique_ptr<PwParams> Engine::build_pw(const StepSpec& s) {
                                               allocs_[size_t(xt.alloc)], dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
                                               CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (res != CUDA_SUCCESS) fail(ErrorKind::cuda, "cuTensorMapEncodeTiled (pointwise) failed (" + std::to_string(int(res)) + ")");
+    return P;
+}
+
+// The depthwise kernel (kernels_dw.cu) takes a step that is one depthwise
+// conv (groups == in == out channels <= 32, <= 25 taps, stride 1 / 2) on the
+// step's input, alone or followed by a 1x1 conv reading only its output (the
+// depthwise output then stays in registers).  Every precision: fp32 SIMT
+// arithmetic (reference order in fp32_exact), HBM tensors in the engine's
+// element type.
+std::unique_ptr<DwParams> Engine::build_dw(const StepSpec& s) {
+    if (knobs_.no_dw || s.kind != StepSpec::FUSED || s.inputs.size() != 1 || s.ops.empty() || s.ops.size() > 2 || !s.gap_out.empty()) return nullptr;
+    if (s2d_ && s.inputs[0] == g_.inputs[0].name) return nullptr;
+    const OpSpec& o0 = s.ops[0];
+    const Layer& d = *g_.find_layer(o0.layer);
+    if (d.kind != LayerKind::conv || o0.stage != 1 || o0.xin != 0) return nullptr;
+    const ConvParams& c = *d.conv;
+    if (c.group != c.in_channels || c.out_channels != c.in_channels || c.in_channels > kDwMaxC || c.kernel_h * c.kernel_w > kDwMaxTaps ||
+        (c.stride != 1 && c.stride != 2) || d.inputs.size() != 1 || d.inputs[0] != s.inputs[0])
+        return nullptr;
+    const Layer* p = nullptr;
+    if (s.ops.size() == 2) {
+        const OpSpec& o1 = s.ops[1];
+        p = g_.find_layer(o1.layer);
+        if (!p || p->kind != LayerKind::conv || o0.emit || o1.stage != 2 || !o1.emit || o1.srcs.size() != 1 || o1.srcs[0] != 0) return nullptr;
+        const ConvParams& q = *p->conv;
+        if (q.kernel_h != 1 || q.kernel_w != 1 || q.stride != 1 || q.pad != 0 || q.group != 1 || q.in_channels != c.out_channels) return nullptr;
+    } else if (!o0.emit) {
+        return nullptr;
+    }
+    auto P = std::make_unique<DwParams>();
+    const TensorSlot& xt = plan_.tensors.at(s.inputs[0]);
+    const TensorSlot& ot = plan_.tensors.at(p ? p->name : d.name);
+    const TensorShape out = *d.out_shape;
+    P->es = esz_;
+    P->exact = prec_ == Precision::fp32_exact;
+    P->tf32 = prec_ == Precision::tf32;
+    P->H = xt.H, P->W = xt.W, P->C = c.in_channels, P->Ho = out.height, P->Wo = out.width;
+    P->kh = c.kernel_h, P->kw = c.kernel_w, P->pad = c.pad, P->stride = c.stride;
+    P->in = allocs_[size_t(xt.alloc)], P->in_cstride = xt.cstride, P->in_coff = xt.coff;
+    P->wdw = weights_ + plan_.w_off.at(d.name);
+    P->bdw = c.has_bias ? weights_ + plan_.b_off.at(d.name) : nullptr;
+    P->relu_dw = c.activation == Activation::relu;
+    P->pw = p != nullptr;
+    if (p) {
+        P->cout = p->conv->out_channels;
+        P->wpw = weights_ + plan_.w_off.at(p->name);
+        P->bpw = p->conv->has_bias ? weights_ + plan_.b_off.at(p->name) : nullptr;
+        P->relu_pw = p->conv->activation == Activation::relu;
+    }
+    P->out = allocs_[size_t(ot.alloc)], P->out_cstride = ot.cstride, P->out_coff = ot.coff;
+    P->out_c = p ? P->cout : P->C;
+    P->tile_w = c.stride == 1 ? 32 : 16;
+    P->tile_h = kDwThreads / P->tile_w;
+    P->cin_h = (P->tile_h - 1) * c.stride + c.kernel_h;
+    P->cin_w = (P->tile_w - 1) * c.stride + c.kernel_w;
+    const int c4 = (P->C + 3) / 4 * 4;
+    P->cp = (c4 / 4) % 2 ? c4 : c4 + 4;  // odd number of float4s per cell: conflict-free float4 reads across a warp
+    P->cw = c4;
+    P->cpw = p ? (P->cout + 3) / 4 * 4 : 0;
+    P->smem_bytes = (P->cin_h * P->cin_w * P->cp + c.kernel_h * c.kernel_w * P->cw + P->cw + (p ? P->C * P->cpw + P->cpw : 0)) * 4;
+    if (P->smem_bytes > 227 * 1024) return nullptr;
+    P->pdl = knobs_.pdl ? 1 : 0;
     return P;
 }
 
@@ -876,6 +948,10 @@ void Engine::set_input_seeded(const std::string& name, uint64_t seed, uint64_t f
 // A tensor-core fused step over images [n0, n0 + count): the kernel, plus the
 // reduction that finishes a conv + global-average-pool step.
 void Engine::launch_tc_step(size_t i, int n0, int count, cudaStream_t st) {
+    if (dws_[i]) {
+        cuda_check(launch_dw(*dws_[i], n0, count, st), "depthwise (+ pointwise)");
+        return;
+    }
     if (stems_[i]) {
         cuda_check(launch_stem(*stems_[i], count, st, n0), "stem (conv + max-pool, tensor cores)");
         return;
@@ -911,7 +987,7 @@ void Engine::launch_tc_step(size_t i, int n0, int count, cudaStream_t st) {
 bool Engine::range_capable() const {
     if (!tc_es_ || g_.inputs.size() != 1) return false;
     for (size_t i = 0; i < plan_.steps.size(); ++i)
-        if (plan_.steps[i].kind != StepSpec::FUSED || !(bparams_[i] || stems_[i] || pws_[i] || fires_[i])) return false;
+        if (plan_.steps[i].kind != StepSpec::FUSED || !(bparams_[i] || stems_[i] || pws_[i] || fires_[i] || dws_[i])) return false;
     return true;
 }
 
@@ -946,7 +1022,8 @@ void Engine::launch_step(size_t i, int batch, cudaStream_t st) {
     auto ptr = [&](const TensorSlot& t) { return static_cast<void*>(allocs_[size_t(t.alloc)]); };
     switch (s.kind) {
     case StepSpec::FUSED:
-        if (tc_es_) launch_tc_step(i, 0, batch, st);
+        if (dws_[i]) cuda_check(launch_dw(*dws_[i], 0, batch, st), "depthwise (+ pointwise)");
+        else if (tc_es_) launch_tc_step(i, 0, batch, st);
         else cuda_check(launch_fused_fp32(params_[i], batch, prec_ == Precision::fp32_exact, st), "fused block");
         return;
     case StepSpec::CONCAT_COPY: {
@@ -1066,10 +1143,14 @@ void Engine::forward_external(const std::vector<External>& ext, int batch, cudaS
             set->bp.resize(plan_.steps.size());
             set->fp.resize(plan_.steps.size());
             set->fr.resize(plan_.steps.size());
+            set->dw.resize(plan_.steps.size());
             for (size_t i = 0; i < plan_.steps.size(); ++i) {
                 const StepSpec& s = plan_.steps[i];
                 if (s.kind != StepSpec::FUSED) continue;
-                if (fires_[i]) {  // same configuration, the caller's addresses
+                if (dws_[i]) {
+                    set->dw[i] = build_dw(s);
+                    if (!set->dw[i]) fail(ErrorKind::internal, "step " + s.id + ": depthwise descriptor for caller-owned tensors");
+                } else if (fires_[i]) {  // same configuration, the caller's addresses
                     set->fr[i] = build_fire(s, fires_[i]->nsplit, fires_[i]->G, fires_[i]->R, fires_[i]->sq_stream);
                     if (!set->fr[i]) fail(ErrorKind::internal, "step " + s.id + ": fire kernel descriptor for caller-owned tensors");
                 } else if (tc_es_) set->bp[i] = build_bparams(s);
@@ -1091,7 +1172,7 @@ void Engine::forward_external(const std::vector<External>& ext, int batch, cudaS
         ExtSet* x;
         void flip() {
             std::swap(e->allocs_, x->allocs), std::swap(e->plan_.tensors, x->tensors);
-            std::swap(e->bparams_, x->bp), std::swap(e->params_, x->fp), std::swap(e->fires_, x->fr);
+            std::swap(e->bparams_, x->bp), std::swap(e->params_, x->fp), std::swap(e->fires_, x->fr), std::swap(e->dws_, x->dw);
         }
         ~Swap() { flip(); }
     } sw{this, &x};

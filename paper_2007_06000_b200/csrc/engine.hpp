@@ -84,6 +84,7 @@ private:
     const uint8_t* packed_for(const std::string& layer, int nb, int nblocks);
     std::unique_ptr<struct PwParams> build_pw(const StepSpec& s);
     // nsplit / G / R > 0 force the fire kernel's channel split / unit (else the knobs, else its model)
+    std::unique_ptr<struct DwParams> build_dw(const StepSpec& s);
     std::unique_ptr<struct FireParams> build_fire(const StepSpec& s, int nsplit = 0, int G = 0, int R = 0, int sqs = -1);
     void launch_tc_step(size_t i, int n0, int count, cudaStream_t st);
     const TensorSlot& slot(const std::string& n) const;
@@ -105,6 +106,7 @@ private:
     std::vector<std::unique_ptr<struct StemParams>> stems_;  // steps run by the stem kernel (conv + max-pool)
     std::vector<std::unique_ptr<struct PwParams>> pws_;      // steps run by the pointwise-conv GEMM kernel
     std::vector<std::unique_ptr<struct FireParams>> fires_;  // split blocks run by the fire kernel (squeeze plane on chip)
+    std::vector<std::unique_ptr<struct DwParams>> dws_;      // depthwise (+ pointwise) steps (every precision)
     std::vector<unsigned long long*> traces_;                // trace buffers (option trace)
     std::map<std::string, long long> wofftc_;                // packed MMA weights: byte offset per layer
     void* weights_tc_ = nullptr;  // packed MMA weights (bf16 / TF32)
@@ -129,6 +131,7 @@ private:
         std::vector<std::unique_ptr<struct BParams>> bp;
         std::vector<struct FusedParams> fp;
         std::vector<std::unique_ptr<struct FireParams>> fr;
+        std::vector<std::unique_ptr<struct DwParams>> dw;
     };
     std::map<std::string, std::unique_ptr<ExtSet>> ext_sets_;
 };
