@@ -30,7 +30,8 @@ struct DwParams {
     int relu_pw;
     void* out;              // NHWC (the pointwise output, else the depthwise output)
     int out_cstride, out_coff, out_c;  // out_c: channels written
-    int tile_h, tile_w;     // output pixels per CTA (tile_h * tile_w == kDwThreads)
+    int px;                 // output pixels per thread along a row (2: stride 1, C <= 16; else 1)
+    int tile_h, tile_w;     // output pixels per CTA (tile_h * tile_w == px * kDwThreads)
     int cin_h, cin_w, cp;   // staged input tile (rows, cols), channel pitch in shared memory (floats)
     int cw, cpw;            // padded weight pitches: C_pad4, cout_pad4
     int smem_bytes;

@@ -476,8 +476,9 @@ std::unique_ptr<DwParams> Engine::build_dw(const StepSpec& s) {
     }
     P->out = allocs_[size_t(ot.alloc)], P->out_cstride = ot.cstride, P->out_coff = ot.coff;
     P->out_c = p ? P->cout : P->C;
+    P->px = c.stride == 1 && c.in_channels <= kDwMaxC / 2 ? 2 : 1;
     P->tile_w = c.stride == 1 ? 32 : 16;
-    P->tile_h = kDwThreads / P->tile_w;
+    P->tile_h = kDwThreads * P->px / P->tile_w;
     P->cin_h = (P->tile_h - 1) * c.stride + c.kernel_h;
     P->cin_w = (P->tile_w - 1) * c.stride + c.kernel_w;
     const int c4 = (P->C + 3) / 4 * 4;

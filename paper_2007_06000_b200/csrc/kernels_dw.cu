@@ -72,10 +72,14 @@ __device__ __forceinline__ void store4(__nv_bfloat16* p, float4 v, int valid, bo
     }
 }
 
-template <class T, bool EXACT>
+// PX output pixels per thread along a row (stride 1: 2, sharing the weight
+// loads and the overlapping input columns; stride 2: 1).  (4 pixels per
+// thread measured slower: 100 registers, 92 KB tiles, 2 CTAs per SM.)
+template <class T, bool EXACT, int PX>
 __global__ void __launch_bounds__(kDwThreads) dw_kernel(const __grid_constant__ DwParams P, int n0) {
     extern __shared__ __align__(16) float sm[];
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    constexpr int CM = PX == 1 ? kDwMaxC : kDwMaxC / 2;  // channels held per pixel
     const int C = P.C, cp = P.cp, taps = P.kh * P.kw;
     float* xs = sm;                                            // [cin_h][cin_w][cp]
     float* wd = xs + P.cin_h * P.cin_w * cp;                   // [taps][cw]
@@ -95,74 +99,116 @@ __global__ void __launch_bounds__(kDwThreads) dw_kernel(const __grid_constant__ 
     const int n = n0 + blockIdx.y;
     const int iy0 = ty0 * P.stride - P.pad, ix0 = tx0 * P.stride - P.pad;
     const T* in = static_cast<const T*>(P.in) + size_t(n) * P.H * P.W * P.in_cstride + P.in_coff;
-    const int c4 = (C + 3) / 4;
-    for (int i = threadIdx.x; i < P.cin_h * P.cin_w * c4; i += kDwThreads) {
-        const int q = i % c4, cell = i / c4, r = cell / P.cin_w, c = cell % P.cin_w;
-        const int iy = iy0 + r, ix = ix0 + c;
-        float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-        if (iy >= 0 && iy < P.H && ix >= 0 && ix < P.W) v = load4(in + (size_t(iy) * P.W + ix) * P.in_cstride + q * 4);
-        *reinterpret_cast<float4*>(xs + cell * cp + q * 4) = v;
+    // stage the input tile: thread -> (cell, 4-channel chunk q), q fastest;
+    // cells advance by a fixed step, (row, col) tracked without division
+    const int c4 = (C + 3) / 4, cells = P.cin_h * P.cin_w;
+    if (kDwThreads % c4 == 0) {
+        const int q = threadIdx.x % c4, step = kDwThreads / c4;
+        int cell = threadIdx.x / c4, r = cell / P.cin_w, c = cell - r * P.cin_w;
+        const int dr = step / P.cin_w, dc = step - dr * P.cin_w;
+        for (; cell < cells; cell += step) {
+            const int iy = iy0 + r, ix = ix0 + c;
+            float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+            if (iy >= 0 && iy < P.H && ix >= 0 && ix < P.W) v = load4(in + (size_t(iy) * P.W + ix) * P.in_cstride + q * 4);
+            *reinterpret_cast<float4*>(xs + cell * cp + q * 4) = v;
+            r += dr, c += dc;
+            if (c >= P.cin_w) c -= P.cin_w, ++r;
+        }
+    } else {
+        for (int i = threadIdx.x; i < cells * c4; i += kDwThreads) {
+            const int q = i % c4, cell = i / c4, r = cell / P.cin_w, c = cell % P.cin_w;
+            const int iy = iy0 + r, ix = ix0 + c;
+            float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+            if (iy >= 0 && iy < P.H && ix >= 0 && ix < P.W) v = load4(in + (size_t(iy) * P.W + ix) * P.in_cstride + q * 4);
+            *reinterpret_cast<float4*>(xs + cell * cp + q * 4) = v;
+        }
     }
     __syncthreads();
-    const int ty = threadIdx.x / P.tile_w, tx = threadIdx.x % P.tile_w;
+    const int tpr = P.tile_w / PX;  // threads per tile row
+    const int ty = threadIdx.x / tpr, tx = (threadIdx.x % tpr) * PX;
     const int oy = ty0 + ty, ox = tx0 + tx;
     if (oy >= P.Ho || ox >= P.Wo) return;
-    // depthwise: every channel of this pixel, taps in kh -> kw order
-    float d[kDwMaxC];
+    // depthwise: every channel of PX pixels, taps in kh -> kw order per pixel
+    float d[PX][CM];
 #pragma unroll
-    for (int c = 0; c < kDwMaxC; ++c) d[c] = 0.0f;
-    for (int ky = 0; ky < P.kh; ++ky)
+    for (int p = 0; p < PX; ++p)
+#pragma unroll
+        for (int c = 0; c < CM; ++c) d[p][c] = 0.0f;
+    for (int ky = 0; ky < P.kh; ++ky) {
+        const float* xrow = xs + ((ty * P.stride + ky) * P.cin_w + tx * P.stride) * cp;
         for (int kx = 0; kx < P.kw; ++kx) {
-            const float* xp = xs + ((ty * P.stride + ky) * P.cin_w + tx * P.stride + kx) * cp;
             const float* wt = wd + (ky * P.kw + kx) * P.cw;
 #pragma unroll
-            for (int c = 0; c < kDwMaxC; c += 4) {
+            for (int c = 0; c < CM; c += 4) {
                 if (c >= C) break;
-                const float4 x4 = load4(xp + c), w4 = load4(wt + c);
-                d[c] = mac<EXACT>(d[c], w4.x, x4.x), d[c + 1] = mac<EXACT>(d[c + 1], w4.y, x4.y);
-                d[c + 2] = mac<EXACT>(d[c + 2], w4.z, x4.z), d[c + 3] = mac<EXACT>(d[c + 3], w4.w, x4.w);
+                const float4 w4 = load4(wt + c);
+#pragma unroll
+                for (int p = 0; p < PX; ++p) {
+                    const float4 x4 = load4(xrow + ((p * P.stride + kx) * cp) + c);
+                    d[p][c] = mac<EXACT>(d[p][c], w4.x, x4.x), d[p][c + 1] = mac<EXACT>(d[p][c + 1], w4.y, x4.y);
+                    d[p][c + 2] = mac<EXACT>(d[p][c + 2], w4.z, x4.z), d[p][c + 3] = mac<EXACT>(d[p][c + 3], w4.w, x4.w);
+                }
             }
         }
-#pragma unroll
-    for (int c = 0; c < kDwMaxC; ++c) {
-        if (c >= C) break;
-        float y = add<EXACT>(d[c], bd[c]);
-        if (P.relu_dw) y = y < 0.0f ? 0.0f : y;
-        d[c] = y;
     }
-    T* out = static_cast<T*>(P.out) + (size_t(n) * P.Ho * P.Wo + size_t(oy) * P.Wo + ox) * P.out_cstride + P.out_coff;
+#pragma unroll
+    for (int c = 0; c < CM; ++c) {
+        if (c >= C) break;
+        const float b = bd[c];
+#pragma unroll
+        for (int p = 0; p < PX; ++p) {
+            float y = add<EXACT>(d[p][c], b);
+            if (P.relu_dw) y = y < 0.0f ? 0.0f : y;
+            d[p][c] = y;
+        }
+    }
+    T* out0 = static_cast<T*>(P.out) + (size_t(n) * P.Ho * P.Wo + size_t(oy) * P.Wo + ox) * P.out_cstride + P.out_coff;
+    const int npx = min(PX, P.Wo - ox);
     if (!P.pw) {
 #pragma unroll
-        for (int c = 0; c < kDwMaxC; c += 4) {
-            if (c >= C) break;
-            store4(out + c, make_float4(d[c], d[c + 1], d[c + 2], d[c + 3]), C - c, P.tf32);
+        for (int p = 0; p < PX; ++p) {
+            if (p >= npx) break;
+#pragma unroll
+            for (int c = 0; c < CM; c += 4) {
+                if (c >= C) break;
+                store4(out0 + p * P.out_cstride + c, make_float4(d[p][c], d[p][c + 1], d[p][c + 2], d[p][c + 3]), C - c, P.tf32);
+            }
         }
         return;
     }
     // pointwise over the depthwise channels (ic order), 4 outputs at a time
     for (int oc = 0; oc < P.cout; oc += 4) {
-        float a[4] = {0.f, 0.f, 0.f, 0.f};
+        float a[PX][4];
 #pragma unroll
-        for (int ic = 0; ic < kDwMaxC; ++ic) {
+        for (int p = 0; p < PX; ++p) a[p][0] = a[p][1] = a[p][2] = a[p][3] = 0.0f;
+#pragma unroll
+        for (int ic = 0; ic < CM; ++ic) {
             if (ic >= C) break;
             const float4 w4 = load4(wp + ic * P.cpw + oc);
-            a[0] = mac<EXACT>(a[0], w4.x, d[ic]), a[1] = mac<EXACT>(a[1], w4.y, d[ic]);
-            a[2] = mac<EXACT>(a[2], w4.z, d[ic]), a[3] = mac<EXACT>(a[3], w4.w, d[ic]);
+#pragma unroll
+            for (int p = 0; p < PX; ++p) {
+                a[p][0] = mac<EXACT>(a[p][0], w4.x, d[p][ic]), a[p][1] = mac<EXACT>(a[p][1], w4.y, d[p][ic]);
+                a[p][2] = mac<EXACT>(a[p][2], w4.z, d[p][ic]), a[p][3] = mac<EXACT>(a[p][3], w4.w, d[p][ic]);
+            }
         }
         const float4 b4 = load4(bp + oc);
-        a[0] = add<EXACT>(a[0], b4.x), a[1] = add<EXACT>(a[1], b4.y), a[2] = add<EXACT>(a[2], b4.z), a[3] = add<EXACT>(a[3], b4.w);
-        if (P.relu_pw)
 #pragma unroll
-            for (int j = 0; j < 4; ++j) a[j] = a[j] < 0.0f ? 0.0f : a[j];
-        store4(out + oc, make_float4(a[0], a[1], a[2], a[3]), P.cout - oc, P.tf32);
+        for (int p = 0; p < PX; ++p) {
+            if (p >= npx) break;
+            float y[4] = {add<EXACT>(a[p][0], b4.x), add<EXACT>(a[p][1], b4.y), add<EXACT>(a[p][2], b4.z), add<EXACT>(a[p][3], b4.w)};
+            if (P.relu_pw)
+#pragma unroll
+                for (int j = 0; j < 4; ++j) y[j] = y[j] < 0.0f ? 0.0f : y[j];
+            store4(out0 + p * P.out_cstride + oc, make_float4(y[0], y[1], y[2], y[3]), P.cout - oc, P.tf32);
+        }
     }
 }
 
-template <class T, bool EXACT>
+template <class T, bool EXACT, int PX>
 cudaError_t launch_t(const DwParams& P, int n0, int count, cudaStream_t st) {
     static bool init = false;
     if (!init) {
-        cudaError_t e = cudaFuncSetAttribute(dw_kernel<T, EXACT>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+        cudaError_t e = cudaFuncSetAttribute(dw_kernel<T, EXACT, PX>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
         if (e != cudaSuccess) return e;
         init = true;
     }
@@ -174,15 +220,19 @@ cudaError_t launch_t(const DwParams& P, int n0, int count, cudaStream_t st) {
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     attr[0].val.programmaticStreamSerializationAllowed = P.pdl ? 1 : 0;
     cfg.attrs = attr, cfg.numAttrs = 1;
-    cudaLaunchKernelEx(&cfg, dw_kernel<T, EXACT>, P, n0);
+    cudaLaunchKernelEx(&cfg, dw_kernel<T, EXACT, PX>, P, n0);
     return cudaGetLastError();
 }
 
 }  // namespace
 
 cudaError_t launch_dw(const DwParams& P, int n0, int count, cudaStream_t st) {
-    if (P.es == 2) return launch_t<__nv_bfloat16, false>(P, n0, count, st);
-    return P.exact ? launch_t<float, true>(P, n0, count, st) : launch_t<float, false>(P, n0, count, st);
+    if (P.px == 2) {
+        if (P.es == 2) return launch_t<__nv_bfloat16, false, 2>(P, n0, count, st);
+        return P.exact ? launch_t<float, true, 2>(P, n0, count, st) : launch_t<float, false, 2>(P, n0, count, st);
+    }
+    if (P.es == 2) return launch_t<__nv_bfloat16, false, 1>(P, n0, count, st);
+    return P.exact ? launch_t<float, true, 1>(P, n0, count, st) : launch_t<float, false, 1>(P, n0, count, st);
 }
 
 }  // namespace xlf
