@@ -8,7 +8,7 @@ for tool in memcheck racecheck synccheck; do
   echo "sanitizer $tool rc=$? $(grep -c '^ok' $O/san_$tool.log) cases; $(grep -m1 'ERROR SUMMARY' $O/san_$tool.log)"
 done
 for prec in $PRECS; do
-for cfg in "straight 1" "merge 8" "fire 32" "inc3a 64" "squeezenet11 256"; do
+for cfg in "straight 1" "merge 8" "fire 32" "inc3a 64" "a2 64" "squeezenet11 256"; do
   set -- $cfg
   for part in b200 unfused; do
     timeout 600 ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum --clock-control none \
