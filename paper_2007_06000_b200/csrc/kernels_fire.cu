@@ -34,10 +34,6 @@
 #include "fire_params.hpp"
 #include "umma.cuh"
 
-#ifndef FIRE_EXP
-#define FIRE_EXP 0  // experiment builds only (tools/build_exp.sh); 0 in the product
-#endif
-
 namespace xlf {
 
 namespace {
@@ -339,7 +335,7 @@ __global__ void __launch_bounds__(kThreads, 1) fire_kernel(const __grid_constant
                                 for (int kx = 0; kx < okw[o]; ++kx, ++atap) {
                                     uint64_t ad = atap;
                                     for (int kk = 0; kk < nks; ++kk) {
-                                        if (FIRE_EXP != 3) FElem<T>::mma(d, ad, bd, idex, acc);
+                                        FElem<T>::mma(d, ad, bd, idex, acc);
                                         acc = 1;
                                         ad += da;
                                         bd += db;
@@ -480,46 +476,94 @@ __global__ void __launch_bounds__(kThreads, 1) fire_kernel(const __grid_constant
                     // warp stores whole segments -- 32 / pieces cells per
                     // instruction, every 16-byte piece of a cell by its own lane --
                     // instead of 32 cells' 16-byte fragments per instruction.
-                    const int cpl = 32 / pieces;  // cells per store instruction
-                    for (int o = 0; o < P.nops; ++o) {
-                        const FireOp& op = P.op[o];
-                        const uint32_t bsm = smem_u32(smem + op.bias_off);
-                        T* dsto = valid ? static_cast<T*>(op.out) + pix * op.out_cstride + op.out_coff + g * P.gch : nullptr;
-                        for (int k = (half + o * spo) & 1; k < spo; k += 2) {  // segments of the op whose global index has this parity
-                            const int c0 = k * SEG;
-                            for (int h = 0; h < SEG; h += 32) {
-                                float v[32];
-                                tmem_ld32(tmem + tl + exc0 + uint32_t(a * JW + o * P.gch + c0 + h), v);
+                    if (!staged) {
+                        // direct stores: this warp's 32-column chunks of the job (global
+                        // chunk index of parity `half`), two TMEM loads in flight per pass
+                        // (TMEM reads are latency-bound per warp: one wait for both)
+                        T* dst[kFireMaxOps];
+#pragma unroll
+                        for (int o = 0; o < kFireMaxOps; ++o)
+                            dst[o] = valid && o < P.nops ? static_cast<T*>(P.op[o].out) + pix * P.op[o].out_cstride + P.op[o].out_coff + g * P.gch
+                                                         : nullptr;
+                        const int nch = JW / 32;
+                        const uint32_t tj = tmem + tl + exc0 + uint32_t(a * JW);
+                        for (int cb = half; cb < nch; cb += 4) {
+                            const bool two = cb + 2 < nch;
+                            uint32_t r0[32], r1[32];
+                            tmem_ld32_issue(tj + uint32_t(cb * 32), r0);
+                            if (two) tmem_ld32_issue(tj + uint32_t((cb + 2) * 32), r1);
+                            tmem_ld_wait32(r0);
+                            if (two) tmem_ld_wait32(r1);
+#pragma unroll
+                            for (int u = 0; u < 2; ++u) {
+                                if (u == 1 && !two) break;
+                                int o = 0, c0 = (cb + 2 * u) * 32;
+                                while (c0 >= P.gch) c0 -= P.gch, ++o;
+                                const FireOp& op = P.op[o];
+                                const uint32_t bsm = smem_u32(smem + op.bias_off) + uint32_t(c0) * 4u;
+                                T* d = dst[0];
+#pragma unroll
+                                for (int oo = 1; oo < kFireMaxOps; ++oo)
+                                    if (o == oo) d = dst[oo];
+                                const bool relu = op.relu;
 #pragma unroll
                                 for (int j = 0; j < 32; j += 8) {
-                                    const float4 b0 = ld_shared_f4(bsm + uint32_t(c0 + h + j) * 4u), b1 = ld_shared_f4(bsm + uint32_t(c0 + h + j + 4) * 4u);
-                                    float w[8] = {v[j] + b0.x, v[j + 1] + b0.y, v[j + 2] + b0.z, v[j + 3] + b0.w,
-                                                  v[j + 4] + b1.x, v[j + 5] + b1.y, v[j + 6] + b1.z, v[j + 7] + b1.w};
-                                    if (op.relu)
+                                    const float4 b0 = ld_shared_f4(bsm + uint32_t(j) * 4u), b1 = ld_shared_f4(bsm + uint32_t(j + 4) * 4u);
+                                    const uint32_t* r = u ? r1 : r0;
+                                    float w[8] = {__uint_as_float(r[j]) + b0.x,     __uint_as_float(r[j + 1]) + b0.y, __uint_as_float(r[j + 2]) + b0.z,
+                                                  __uint_as_float(r[j + 3]) + b0.w, __uint_as_float(r[j + 4]) + b1.x, __uint_as_float(r[j + 5]) + b1.y,
+                                                  __uint_as_float(r[j + 6]) + b1.z, __uint_as_float(r[j + 7]) + b1.w};
+                                    if (relu)
 #pragma unroll
                                         for (int e = 0; e < 8; ++e) w[e] = fmaxf(w[e], 0.0f);
+                                    if (d)
 #pragma unroll
-                                    for (int e = 0; e < 8; e += cpc) {
-                                        if (staged) {
-                                            const int pc = (h + j + e) / cpc;  // piece of this cell's segment
-                                            st_shared16(stg + uint32_t(lane * RB + ((pc ^ skey) << 4)), FElem<T>::pack(w + e));
-                                        } else if (dsto) {
-                                            *reinterpret_cast<uint4*>(dsto + c0 + h + j + e) = FElem<T>::pack(w + e);
+                                        for (int e = 0; e < 8; e += cpc) *reinterpret_cast<uint4*>(d + c0 + j + e) = FElem<T>::pack(w + e);
+                                }
+                            }
+                        }
+                    } else {
+                        const int cpl = 32 / pieces;  // cells per store instruction
+                        for (int o = 0; o < P.nops; ++o) {
+                            const FireOp& op = P.op[o];
+                            const uint32_t bsm = smem_u32(smem + op.bias_off);
+                            T* dsto = valid ? static_cast<T*>(op.out) + pix * op.out_cstride + op.out_coff + g * P.gch : nullptr;
+                            for (int k = (half + o * spo) & 1; k < spo; k += 2) {  // segments of the op whose global index has this parity
+                                const int c0 = k * SEG;
+                                for (int h = 0; h < SEG; h += 32) {
+                                    float v[32];
+                                    tmem_ld32(tmem + tl + exc0 + uint32_t(a * JW + o * P.gch + c0 + h), v);
+    #pragma unroll
+                                    for (int j = 0; j < 32; j += 8) {
+                                        const float4 b0 = ld_shared_f4(bsm + uint32_t(c0 + h + j) * 4u), b1 = ld_shared_f4(bsm + uint32_t(c0 + h + j + 4) * 4u);
+                                        float w[8] = {v[j] + b0.x, v[j + 1] + b0.y, v[j + 2] + b0.z, v[j + 3] + b0.w,
+                                                      v[j + 4] + b1.x, v[j + 5] + b1.y, v[j + 6] + b1.z, v[j + 7] + b1.w};
+                                        if (op.relu)
+    #pragma unroll
+                                            for (int e = 0; e < 8; ++e) w[e] = fmaxf(w[e], 0.0f);
+    #pragma unroll
+                                        for (int e = 0; e < 8; e += cpc) {
+                                            if (staged) {
+                                                const int pc = (h + j + e) / cpc;  // piece of this cell's segment
+                                                st_shared16(stg + uint32_t(lane * RB + ((pc ^ skey) << 4)), FElem<T>::pack(w + e));
+                                            } else if (dsto) {
+                                                *reinterpret_cast<uint4*>(dsto + c0 + h + j + e) = FElem<T>::pack(w + e);
+                                            }
                                         }
                                     }
                                 }
+                                if (!staged) continue;
+                                __syncwarp();
+    #pragma unroll 4
+                                for (int m = 0; m < 32; m += cpl) {
+                                    const int c = m + lane / pieces, q = lane % pieces;
+                                    const unsigned long long dp = __shfl_sync(0xffffffffu, reinterpret_cast<unsigned long long>(dsto), c);
+                                    const int key = (c >> rshift) & (pieces - 1);
+                                    const uint4 val = ld_shared_u4(stg + uint32_t(c * RB + ((q ^ key) << 4)));
+                                    if (dp) *reinterpret_cast<uint4*>(reinterpret_cast<T*>(dp) + c0 + q * cpc) = val;
+                                }
+                                __syncwarp();
                             }
-                            if (!staged) continue;
-                            __syncwarp();
-#pragma unroll 4
-                            for (int m = 0; m < 32; m += cpl) {
-                                const int c = m + lane / pieces, q = lane % pieces;
-                                const unsigned long long dp = __shfl_sync(0xffffffffu, reinterpret_cast<unsigned long long>(dsto), c);
-                                const int key = (c >> rshift) & (pieces - 1);
-                                const uint4 val = ld_shared_u4(stg + uint32_t(c * RB + ((q ^ key) << 4)));
-                                if (dp && FIRE_EXP != 1) *reinterpret_cast<uint4*>(reinterpret_cast<T*>(dp) + c0 + q * cpc) = val;
-                            }
-                            __syncwarp();
                         }
                     }
                     fence_before();

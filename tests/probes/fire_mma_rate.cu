@@ -10,7 +10,7 @@
 #include "umma.cuh"
 using namespace xlf::umma;
 
-__global__ void k(int jobs, int N, int nks, int busy, float* gout, unsigned long long* out) {
+__global__ void k(int jobs, int N, int nks, int busy, float* gout, unsigned long long* out, int dcol0 = 0, int dstep = 256) {
     extern __shared__ __align__(1024) uint8_t smem[];
     __shared__ uint64_t bar, never;
     __shared__ uint32_t slot;
@@ -44,7 +44,7 @@ __global__ void k(int jobs, int N, int nks, int busy, float* gout, unsigned long
                     for (int kx = 0; kx < 3; ++kx, ++atap) {
                         uint64_t ad = atap;
                         for (int kk = 0; kk < nks; ++kk) {
-                            mma_bf16(tmem + uint32_t((j & 1) * 256), ad, bd, idesc, acc);
+                            mma_bf16(tmem + uint32_t(dcol0 + (j & 1) * dstep), ad, bd, idesc, acc);
                             acc = 1;
                             ad += da;
                             bd += db;
@@ -77,6 +77,17 @@ __global__ void k(int jobs, int N, int nks, int busy, float* gout, unsigned long
             for (int i = 0; i < 32; ++i) acc += v[i];
         }
         if (acc == 1.2345f) gout[0] = acc;
+    } else if (busy == 4) {  // shared-memory stores + loads (plane writes / staging)
+        const int t = threadIdx.x - 32;
+        uint32_t base = smem_u32(smem) + 150 * 1024 + (t % 128) * 16;
+        uint32_t acc = 0;
+        while (!done) {
+            asm volatile("st.shared.v4.b32 [%0], {%1, %1, %1, %1};" ::"r"(base), "r"(acc) : "memory");
+            uint32_t v;
+            asm volatile("ld.shared.b32 %0, [%1];" : "=r"(v) : "r"(base + 4096) : "memory");
+            acc += v;
+        }
+        if (acc == 12345) gout[1] = float(acc);
     } else if (busy == 3) {  // scattered 16-byte global stores (the epilogue's pattern)
         const int t = threadIdx.x - 32;
         int r = 0;
@@ -91,16 +102,82 @@ __global__ void k(int jobs, int N, int nks, int busy, float* gout, unsigned long
     if (warp == 0) tmem_free(tmem, 512);
 }
 
+// The fire kernel's round: a squeeze tile (4 MMAs, N = 16, A in a SWIZZLE_128B
+// stage) + commit, then an expand tile (e1: 1 MMA, e3: 9 shifted MMAs, N = 64)
+// + commit, with the kernel's shared-memory placement (plane stride 16256 B).
+__global__ void kround(int jobs, int with_sq, unsigned long long* out, int fence_mode = 0) {
+    extern __shared__ __align__(1024) uint8_t smem[];
+    __shared__ uint64_t bar, jb;
+    __shared__ uint32_t slot;
+    const int warp = threadIdx.x / 32;
+    for (int i = threadIdx.x; i < 200 * 1024 / 4; i += blockDim.x) reinterpret_cast<uint32_t*>(smem)[i] = 0x3f803f80u * (i & 1);
+    if (threadIdx.x == 0) mbar_init(&bar, 1), mbar_init(&jb, 1), mbar_fence_init();
+    if (warp == 0) tmem_alloc(&slot, 512);
+    fence_async_smem();
+    fence_before();
+    __syncthreads();
+    fence_after();
+    const uint32_t tmem = slot;
+    if (warp == 0 && elect_one()) {
+        const uint32_t sb = smem_u32(smem);
+        const int Wp = 56;
+        const uint32_t PS = 1016 * 16;
+        const uint32_t plane = sb + 120 * 1024, wex = sb + 96 * 1024 + 2048, wsq = sb + 96 * 1024;
+        const uint64_t aplane = sdesc(plane + uint32_t(1 + Wp) * 16u, PS, 128, kNoSwizzle);
+        const uint64_t ring0 = sdesc(sb, 16u, 1024u, kSW128);
+        const uint64_t bsq = sdesc(wsq, 16 * 16, 128, kNoSwizzle);
+        const uint32_t idsq = idesc_bf16(128, 16), idex = idesc_bf16(128, 64);
+        long long t0 = clock64();
+        __shared__ uint64_t done_bar;
+        mbar_init(&done_bar, 1);
+        mbar_fence_init();
+        mbar_arrive(&done_bar);  // phase 0 complete: waits on parity 0 return at once
+        for (int j = 0; j < jobs; ++j) {
+            if (fence_mode & 1) fence_after();
+            if (fence_mode & 2) mbar_wait(&done_bar, 0);
+            if (fence_mode & 4) fence_before();
+            if (with_sq) {
+                uint64_t ad = ring0 + uint64_t((j % 6) * 1024), bd = bsq;
+                for (int kk = 0; kk < 4; ++kk) mma_bf16(tmem + 0 + (j & 1) * 32, ad, bd, idsq, kk > 0), ad += 2, bd += 32;
+                commit(&jb);
+            }
+            const uint64_t ajob = aplane + uint64_t((j % 7) * 128);
+            const uint32_t d = tmem + 64 + uint32_t((j % 3) * 128);
+            mma_bf16(d, ajob, sdesc(wex, 64 * 16, 128, kNoSwizzle), idex, 0);
+            uint64_t arow = ajob + uint64_t(int64_t(-Wp - 1)), bd = sdesc(wex + 2048, 64 * 16, 128, kNoSwizzle);
+            uint32_t acc = 0;
+            for (int ky = 0; ky < 3; ++ky, arow += uint64_t(Wp)) {
+                uint64_t atap = arow;
+                for (int kx = 0; kx < 3; ++kx, ++atap) {
+                    mma_bf16(d + 64, atap, bd, idex, acc);
+                    acc = 1;
+                    bd += 128;
+                }
+            }
+            commit(&jb);
+        }
+        long long t1 = clock64();
+        commit(&bar);
+        mbar_wait(&bar, 0);
+        long long t2 = clock64();
+        out[0] = t1 - t0, out[1] = t2 - t0;
+    }
+    fence_before();
+    __syncthreads();
+    fence_after();
+    if (warp == 0) tmem_free(tmem, 512);
+}
+
 int main() {
     unsigned long long* d;
     float* g;
     cudaMalloc(&d, 16);
     cudaMalloc(&g, size_t(1024) * 224 * 64 * 4 + 1024 * 1024);
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    const char* names[] = {"alone", "+256 pollers", "+256 TMEM readers", "+256 scattered stores"};
-    for (int busy = 0; busy < 4; ++busy)
-        for (int N : {64, 128, 256})
-            for (int nks : {1, 4}) {
+    const char* names[] = {"alone", "+256 pollers", "+256 TMEM readers", "+256 scattered stores", "+256 smem st/ld"};
+    for (int busy = 0; busy < 1; ++busy)
+        for (int N : {64, 128})
+            for (int nks : {1, 2}) {
                 unsigned long long h[2];
                 const int jobs = 200;
                 k<<<1, busy ? 288 : 32, 200 * 1024>>>(jobs, N, nks, busy, g, d);
@@ -108,5 +185,20 @@ int main() {
                 const double n = jobs * 9.0 * nks;
                 printf("%-22s N=%3d nks=%d: issue %.1f cyc/mma, complete %.1f cyc/mma\n", names[busy], N, nks, h[0] / n, h[1] / n);
             }
+    for (int dc : {0, 32, 64, 96})
+        for (int ds : {128, 256}) {
+            unsigned long long h[2];
+            k<<<1, 32, 200 * 1024>>>(200, 64, 1, 0, g, d, dc, ds);
+            cudaMemcpy(h, d, 16, cudaMemcpyDeviceToHost);
+            printf("dcol %3d step %3d N=64 nks=1: %.1f cyc/mma\n", dc, ds, h[1] / 1800.0);
+        }
+    cudaFuncSetAttribute(kround, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    for (int fm : {0, 1, 2, 3, 4, 7})
+        for (int sq : {0, 1}) {
+            unsigned long long h[2];
+            kround<<<1, 32, 200 * 1024>>>(200, sq, d, fm);
+            cudaMemcpy(h, d, 16, cudaMemcpyDeviceToHost);
+            printf("kernel round (squeeze %d, fence mode %d): %.0f cycles per round\n", sq, fm, h[1] / 200.0);
+        }
     printf("%s\n", cudaGetErrorString(cudaDeviceSynchronize()));
 }

@@ -2,7 +2,7 @@
 the MMA issuer's wait / issue / commit stamps, the epilogue's wait / done
 stamps and the producer's ring stamps, relative to the first stamp.
 
-    python tests/probes/fire_trace.py [layer-prefix] [batch] [options]
+    python tests/probes/fire_trace.py [layer-prefix] [batch] [options] [graph]
 """
 import ctypes
 import os
@@ -17,14 +17,15 @@ from paper_2007_06000_b200 import _lib  # noqa: E402
 
 N = 1024
 NAMES = {11: "mma sq wait", 21: "mma sq issue", 31: "mma sq commit", 12: "mma ex wait", 22: "mma ex issue", 32: "mma ex commit",
+         23: "mma ex first issued", 24: "mma ex all issued",
          41: "epi sq wait", 51: "epi sq got", 61: "epi sq done", 42: "epi ex wait", 52: "epi ex got", 62: "epi ex done", 50: "tma"}
 
 
 def main():
     which = sys.argv[1] if len(sys.argv) > 1 else "fire2"
     batch = int(sys.argv[2]) if len(sys.argv) > 2 else 256
-    opts = "trace=1" + ("," + sys.argv[3] if len(sys.argv) > 3 else "")
-    g = X.load_graph(X.graph_path("squeezenet11"))
+    opts = "trace=1" + ("," + sys.argv[3] if len(sys.argv) > 3 and sys.argv[3] else "")
+    g = X.load_graph(X.graph_path(sys.argv[4] if len(sys.argv) > 4 else "squeezenet11"))
     e = X.Engine(g, X.seeded_weights(g, 42), "b200", "bf16", max_batch=batch, options=opts)
     e.set_input_seeded(42, batch)
     e.forward(batch, use_graph=False)
