@@ -515,6 +515,9 @@ std::unique_ptr<FireParams> Engine::build_fire(const StepSpec& s, int fns, int f
         const TensorSlot& ot = plan_.tensors.at(l.name);
         op.out = allocs_[size_t(ot.alloc)], op.out_cstride = ot.cstride, op.out_coff = ot.coff;
     }
+    P->st32 = 1;
+    for (int o = 0; o < P->nops; ++o)
+        if ((P->op[o].out_cstride * es) % 32 || (P->op[o].out_coff * es) % 32 || reinterpret_cast<uintptr_t>(P->op[o].out) % 32) P->st32 = 0;
     int sms = 148;
     cuda_check(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device_), "SM count");
     double model = 0;

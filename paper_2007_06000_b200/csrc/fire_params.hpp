@@ -66,6 +66,7 @@ struct FireParams {
     int seg;              // expand store segment: channels of one op per warp pass (64 bf16 if gch % 64 == 0, else 32)
     int ring_off, wsq_off, plane_off, sqbias_off, stage_off, smem_bytes;  // stage: 8 epilogue warps x 4 KB store staging (-1: direct stores)
     int pdl;
+    int st32;             // every op's output pixel / channel offsets are 32-byte aligned: 256-bit stores
     unsigned long long* trace;  // option trace=1: 3 roles x kFireTraceN x (code, globaltimer) of CTA (0, 0)
     int stage_mode;             // host planning only: 0 direct stores, 1 staged through shared memory (option fire_stage)
     int sq_stream_mode;         // host planning only: 0 either, 1 streamed squeeze weights only, 2 resident only (option fire_sqs)

@@ -82,6 +82,13 @@ __device__ __forceinline__ void tma_2d(void* smem, const void* desc, int c0, int
         : "memory");
 }
 
+// 32-byte (256-bit) global store: a whole L2 sector per thread
+__device__ __forceinline__ void st_global32(void* p, uint4 a, uint4 b) {
+    asm volatile("st.global.v8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"l"(p), "r"(a.x), "r"(a.y), "r"(a.z), "r"(a.w), "r"(b.x), "r"(b.y),
+                 "r"(b.z), "r"(b.w)
+                 : "memory");
+}
+
 __device__ __forceinline__ void st_shared16(uint32_t addr, uint4 v) {
     asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w) : "memory");
 }
@@ -487,6 +494,7 @@ __global__ void __launch_bounds__(kThreads, 1) fire_kernel(const __grid_constant
                                                          : nullptr;
                         const int nch = JW / 32;
                         const uint32_t tj = tmem + tl + exc0 + uint32_t(a * JW);
+                        const bool st32 = P.st32 != 0;
                         for (int cb = half; cb < nch; cb += 4) {
                             const bool two = cb + 2 < nch;
                             uint32_t r0[32], r1[32];
@@ -506,19 +514,31 @@ __global__ void __launch_bounds__(kThreads, 1) fire_kernel(const __grid_constant
                                 for (int oo = 1; oo < kFireMaxOps; ++oo)
                                     if (o == oo) d = dst[oo];
                                 const bool relu = op.relu;
+                                // 32-byte stores: 2 x 16-byte packs per 32-byte piece (16 bf16 / 8 fp32 channels)
+                                constexpr int JP = 2 * cpc;  // channels per 32-byte piece
 #pragma unroll
-                                for (int j = 0; j < 32; j += 8) {
-                                    const float4 b0 = ld_shared_f4(bsm + uint32_t(j) * 4u), b1 = ld_shared_f4(bsm + uint32_t(j + 4) * 4u);
+                                for (int j = 0; j < 32; j += JP) {
                                     const uint32_t* r = u ? r1 : r0;
-                                    float w[8] = {__uint_as_float(r[j]) + b0.x,     __uint_as_float(r[j + 1]) + b0.y, __uint_as_float(r[j + 2]) + b0.z,
-                                                  __uint_as_float(r[j + 3]) + b0.w, __uint_as_float(r[j + 4]) + b1.x, __uint_as_float(r[j + 5]) + b1.y,
-                                                  __uint_as_float(r[j + 6]) + b1.z, __uint_as_float(r[j + 7]) + b1.w};
-                                    if (relu)
+                                    uint4 pk[2];
 #pragma unroll
-                                        for (int e = 0; e < 8; ++e) w[e] = fmaxf(w[e], 0.0f);
-                                    if (d)
+                                    for (int hh = 0; hh < 2; ++hh) {
+                                        const int jj = j + hh * cpc;
+                                        float w[cpc];
 #pragma unroll
-                                        for (int e = 0; e < 8; e += cpc) *reinterpret_cast<uint4*>(d + c0 + j + e) = FElem<T>::pack(w + e);
+                                        for (int e = 0; e < cpc; e += 4) {
+                                            const float4 b4 = ld_shared_f4(bsm + uint32_t(jj + e) * 4u);
+                                            w[e] = __uint_as_float(r[jj + e]) + b4.x, w[e + 1] = __uint_as_float(r[jj + e + 1]) + b4.y;
+                                            w[e + 2] = __uint_as_float(r[jj + e + 2]) + b4.z, w[e + 3] = __uint_as_float(r[jj + e + 3]) + b4.w;
+                                        }
+                                        if (relu)
+#pragma unroll
+                                            for (int e = 0; e < cpc; ++e) w[e] = fmaxf(w[e], 0.0f);
+                                        pk[hh] = FElem<T>::pack(w);
+                                    }
+                                    if (d) {
+                                        if (st32) st_global32(d + c0 + j, pk[0], pk[1]);
+                                        else *reinterpret_cast<uint4*>(d + c0 + j) = pk[0], *reinterpret_cast<uint4*>(d + c0 + j + cpc) = pk[1];
+                                    }
                                 }
                             }
                         }
