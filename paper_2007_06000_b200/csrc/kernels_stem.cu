@@ -298,12 +298,43 @@ __global__ void __launch_bounds__(kStemThreads, 2) stem_kernel(const __grid_cons
             for (int lr = 0; lr < nconv; ++lr, ++c) {
                 const int a = c & (Acc - 1);
                 PROF_T0
-                mbar_wait(&accf[a], uint32_t(c >> AccL) & 1u);
+                mbar_sleep_wait(&accf[a], uint32_t(c >> AccL) & 1u);  // suspended, not spinning: the other CTA's warps issue
                 PROF_ADD(w_accf)
                 fence_after();
                 const uint32_t ta = trow + uint32_t(a * N);
                 const bool closes = lr > 0 && !(lr & 1);
                 const uint32_t stage = (emitted & 1) ? stage0 + uint32_t(P.stage_bytes) : stage0;
+                if constexpr (NCH <= 2) {
+                    // every chunk of the row in flight at once (TMEM reads are
+                    // latency-bound per warp), one wait
+                    uint32_t rv[NCH][32];
+#pragma unroll
+                    for (int h = 0; h < NCH; ++h) tmem_ld32_issue(ta + uint32_t(h * 32), rv[h]);
+#pragma unroll
+                    for (int h = 0; h < NCH; ++h) tmem_ld_wait32(rv[h]);
+                    if (lr == 0) {
+#pragma unroll
+                        for (int h = 0; h < NCH; ++h)
+#pragma unroll
+                            for (int k = 0; k < 32; ++k) vm[h * 32 + k] = __uint_as_float(rv[h][k]);
+                    } else if (!closes) {
+#pragma unroll
+                        for (int h = 0; h < NCH; ++h)
+#pragma unroll
+                            for (int k = 0; k < 32; ++k) vm[h * 32 + k] = fmaxf(vm[h * 32 + k], __uint_as_float(rv[h][k]));
+                    } else {
+#pragma unroll
+                        for (int h = 0; h < NCH; ++h) {
+                            float m[32];
+#pragma unroll
+                            for (int k = 0; k < 32; ++k) {
+                                const float v = __uint_as_float(rv[h][k]);
+                                m[k] = fmaxf(vm[h * 32 + k], v), vm[h * 32 + k] = v;
+                            }
+                            stage_part<T, NCH>(stage, t, h, m);
+                        }
+                    }
+                } else {
                 if (lr == 0) {
 #pragma unroll
                     for (int h = 0; h < NCH; ++h) tmem_ld32(ta + uint32_t(h * 32), vm + h * 32);
@@ -325,6 +356,7 @@ __global__ void __launch_bounds__(kStemThreads, 2) stem_kernel(const __grid_cons
                         for (int k = 0; k < 32; ++k) m[k] = fmaxf(vm[h * 32 + k], v[k]), vm[h * 32 + k] = v[k];
                         stage_part<T, NCH>(stage, t, h, m);
                     }
+                }
                 }
                 fence_before();
                 __syncwarp();
