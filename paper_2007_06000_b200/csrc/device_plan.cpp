@@ -494,6 +494,7 @@ Knobs Knobs::parse(const std::string& text) {
         else if (key == "no_pw") k.no_pw = need_num() != 0;
         else if (key == "no_fire") k.no_fire = need_num() != 0;
         else if (key == "no_dw") k.no_dw = need_num() != 0;
+        else if (key == "pw_mc") k.pw_mc = need_num() != 0;
         else if (key == "fire_g") k.fire_g = int(need_num());
         else if (key == "fire_r") k.fire_r = int(need_num());
         else if (key == "fire_nsplit") k.fire_nsplit = int(need_num());

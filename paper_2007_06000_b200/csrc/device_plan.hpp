@@ -43,6 +43,7 @@ struct Knobs {
     bool no_pw = false;          // 1x1 convs through the generic fused-block kernel, not the pointwise GEMM kernel
     bool no_stem = false;        // the first conv + max-pool through the generic fused-block kernel, not the stem kernel
     bool no_s2d = false;         // keep a stride-2 first conv on its own input (no space-to-depth rewrite)
+    bool pw_mc = false;          // pointwise channel groups as one cluster with the input multicast (TMA .multicast::cluster)
     bool no_dw = false;          // depthwise (+ pointwise) steps through the generic kernels, not the depthwise kernel
     bool no_fire = false;        // split-mode squeeze -> expand blocks through the generic fused-block kernel, not the fire kernel
     int fire_g = 0, fire_r = 0, fire_nsplit = 0;  // force the fire kernel's unit (G images / R-row bands) and channel groups

@@ -387,6 +387,10 @@ std::unique_ptr<PwParams> Engine::build_pw(const StepSpec& s) {
         if (gch <= 256 && (long long)P->ksteps * gch * 32 <= 200 * 1024 && gch * (knobs_.nsplit - 1) < P->cout) G = knobs_.nsplit, P->gch = gch;
     }
     P->nsplit = G;
+    // option pw_mc=1: the channel groups of an M tile as one cluster, its A
+    // chunks loaded once and multicast (measured slower on conv10: 67 -> 79 us,
+    // 8-CTA clusters limit the resident grid and run the groups in lock step)
+    P->mc = knobs_.pw_mc && G >= 2 && G <= 8 ? G : 1;
     P->wmma = G == 1 && P->gch == [&] { int nbk, nb; tc_nblocks(l.conv->out_channels, &nbk, &nb); return nbk == 1 ? nb : -1; }()
                   ? static_cast<const uint8_t*>(weights_tc_) + wofftc_.at(l.name)
                   : packed_for(l.name, P->gch, G);

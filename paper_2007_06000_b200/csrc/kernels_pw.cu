@@ -96,9 +96,15 @@ __global__ void __launch_bounds__(kPwThreads, 1) pw_kernel(const __grid_constant
     const int rows = count * P.HW, mtiles = (rows + 127) / 128;
     const int row0 = n0 * P.HW;
     const int g = blockIdx.y, gch = P.gch;
+    // cluster multicast (mc > 1): the mc channel groups of one M tile form a
+    // cluster; rank 0 loads each A chunk once and multicasts it to all of
+    // them, and frees a stage only when every CTA released it
+    const int mc = P.mc > 1 ? P.mc : 1;
+    const uint32_t rank = mc > 1 ? cluster_rank() : 0u;
+    const uint16_t all = uint16_t((1u << mc) - 1u), rel = uint16_t((1u << rank) | 1u);
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     if (threadIdx.x == 0) {
-        for (int s = 0; s < kPwStages; ++s) mbar_init(&full[s], 1), mbar_init(&empty[s], 1);
+        for (int s = 0; s < kPwStages; ++s) mbar_init(&full[s], 1), mbar_init(&empty[s], rank == 0 ? uint32_t(mc) : 1u);
         for (int a = 0; a < 2; ++a) mbar_init(&accf[a], 1), mbar_init(&acce[a], kPwEpi / 32);
         mbar_init(&wbar, 1);
         mbar_fence_init();
@@ -106,6 +112,7 @@ __global__ void __launch_bounds__(kPwThreads, 1) pw_kernel(const __grid_constant
     if (warp == kPwMma) tmem_alloc(&tmem_slot, uint32_t(P.tmem_cols));
     fence_before();
     __syncthreads();
+    if (mc > 1) cluster_sync();  // peers' barriers initialised before any multicast / remote arrival
     fence_after();
     const uint32_t tmem = tmem_slot;
     const uint32_t ring = smem_u32(smem + P.ring_off), wsm = smem_u32(smem + P.w_off);
@@ -124,8 +131,13 @@ __global__ void __launch_bounds__(kPwThreads, 1) pw_kernel(const __grid_constant
                     const int s = it % kPwStages;
                     if (it >= kPwStages) mbar_sleep_wait(&empty[s], uint32_t(it / kPwStages - 1) & 1u);
                     mbar_expect_tx(&full[s], kStageBytes);
-                    tma_2d(smem + P.ring_off + s * kStageBytes, &P.amap, P.coff_in + kc * kc_elems, row0 + m * 128, &full[s]);
+                    if (mc == 1) tma_2d(smem + P.ring_off + s * kStageBytes, &P.amap, P.coff_in + kc * kc_elems, row0 + m * 128, &full[s]);
+                    else if (rank == 0)
+                        tma_load_2d_mc(smem + P.ring_off + s * kStageBytes, &P.amap, P.coff_in + kc * kc_elems, row0 + m * 128, &full[s], all);
                 }
+            // the leader consumes every stage's last release (remote arrivals) before it may exit
+            if (mc > 1 && rank == 0)
+                for (int k = max(0, it - kPwStages); k < it; ++k) mbar_sleep_wait(&empty[k % kPwStages], uint32_t(k / kPwStages) & 1u);
         }
     } else if (warp == kPwMma) {
         if (elect_one()) {
@@ -152,7 +164,8 @@ __global__ void __launch_bounds__(kPwThreads, 1) pw_kernel(const __grid_constant
                         acc = 1;
                         bd += bstep;
                     }
-                    commit(&empty[s]);
+                    if (mc == 1) commit(&empty[s]);
+                    else commit_mc(&empty[s], rel);  // own stage (pacing this CTA's expect_tx) + the leader's
                 }
                 commit(&accf[a]);
             }
@@ -231,6 +244,7 @@ __global__ void __launch_bounds__(kPwThreads, 1) pw_kernel(const __grid_constant
     }
     fence_before();
     __syncthreads();
+    if (mc > 1) cluster_sync();
     fence_after();
     if (warp == kPwMma) tmem_free(tmem, uint32_t(P.tmem_cols));
 }
@@ -263,14 +277,27 @@ cudaError_t launch_t(const PwParams& P, int n0, int count, cudaStream_t st) {
     int sms = 148, dev = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    const int gx = std::max(1, std::min(mtiles, sms * std::max(1, P.ctas_per_sm) / std::max(1, P.nsplit)));
+    int gx = std::max(1, std::min(mtiles, sms * std::max(1, P.ctas_per_sm) / std::max(1, P.nsplit)));
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(unsigned(gx), unsigned(std::max(1, P.nsplit)), 1u), cfg.blockDim = dim3(kPwThreads);
     cfg.dynamicSmemBytes = size_t(P.smem_bytes), cfg.stream = st;
-    cudaLaunchAttribute attr[1];
+    cudaLaunchAttribute attr[2];
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     attr[0].val.programmaticStreamSerializationAllowed = P.pdl ? 1 : 0;
     cfg.attrs = attr, cfg.numAttrs = 1;
+    if (P.mc > 1) {  // the channel groups of an M tile as one cluster; as many clusters as can be resident
+        attr[1].id = cudaLaunchAttributeClusterDimension;
+        attr[1].val.clusterDim.x = 1, attr[1].val.clusterDim.y = unsigned(P.mc), attr[1].val.clusterDim.z = 1;
+        cfg.numAttrs = 2;
+        static int max_clusters = 0;
+        if (!max_clusters) {
+            cudaLaunchConfig_t q = cfg;
+            q.gridDim = dim3(unsigned(sms), unsigned(P.mc), 1u);
+            if (cudaOccupancyMaxActiveClusters(&max_clusters, pw_kernel<T>, &q) != cudaSuccess || max_clusters < 1) max_clusters = 1;
+        }
+        gx = std::max(1, std::min(mtiles, max_clusters));
+        cfg.gridDim.x = unsigned(gx);
+    }
     cudaLaunchKernelEx(&cfg, pw_kernel<T>, P, n0, count);
     return cudaGetLastError();
 }

@@ -34,6 +34,7 @@ struct PwParams {
     int smem_bytes, ring_off, w_off, bias_off;
     int tmem_cols;        // 2 accumulator sets x gch (power of two)
     int ctas_per_sm, pdl;
+    int mc;               // > 1: the nsplit channel groups of an M tile run as one cluster, A chunks multicast (TMA .multicast::cluster)
 };
 
 }  // namespace xlf

@@ -382,13 +382,14 @@ def test_nsplit_matches_unsplit(prec):
 
 
 @pytest.mark.parametrize("prec", PRECS)
-@pytest.mark.parametrize("batch,opts", [(3, ""), (37, ""), (5, "nsplit=4")])
+@pytest.mark.parametrize("batch,opts", [(3, ""), (37, ""), (5, "nsplit=4"), (37, "pw_mc=1")])
 def test_pointwise_gemm_kernel(prec, batch, opts):
     """1x1 convs through the pointwise GEMM kernel (kernels_pw.cu: pixels of
     all images as one M dimension, M tiles crossing image boundaries; conv10 +
     global average pool with per-warp, per-image partial sums) against the
     generic kernel (no_pw=1) and the oracle, at batches whose tiles straddle
-    images unevenly."""
+    images unevenly; pw_mc=1 runs the channel groups of an M tile as one
+    cluster with the input chunks multicast."""
     import torch
     text = graph_text("squeezenet11")
     og = O.load_graph(text)
