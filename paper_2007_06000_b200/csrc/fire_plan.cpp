@@ -105,6 +105,9 @@ std::vector<std::pair<double, FireParams>> fire_candidates(const FireParams& P, 
         if (P.sq_stream_mode == 2 && sqs == 1) continue;
         if (cout % (32 * ns)) continue;  // whole 32-column store segments per op and group
         const int gch = cout / ns;
+        // N < 64 expand MMAs cost as much as N = 64 ones (measured: inception-3a's
+        // reduce -> 3x3 at 4 groups of 32 took 61 us against 42 us unfused)
+        if (gch < std::min(64, cout)) continue;
         if (gch > 256 || 2 * sq_cols + 2 * P.nops * gch > 512) continue;  // two expand accumulators (every op of an M tile each)
         std::vector<std::pair<int, int>> shapes;  // (G, R)
         for (int G = 1; G <= 8; ++G) shapes.push_back({G, P.H});

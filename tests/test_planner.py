@@ -198,7 +198,8 @@ def test_b200_cost_based_fusion_decisions():
     """bf16 B200 partition.  Split / straight blocks of a 1x1 reduce into
     stride-1 expand convs run on the fire kernel (kernels_fire.cu: squeeze
     plane on chip, whole-image or row-band units) and stay fused -- all eight
-    SqueezeNet fire modules and inception-3a's 1x1-reduce -> 3x3.  Without it
+    SqueezeNet fire modules (not inception-3a's 1x1-reduce -> 3x3, whose
+    weights would force 32-channel groups).  Without it
     (option no_fire=1) a fused block is kept only when the planner's model
     beats its layers as single kernels: inception's reduce -> 3x3 (221 KB of
     weights re-streamed per small fused tile) is split; option always_fuse
@@ -213,8 +214,10 @@ def test_b200_cost_based_fusion_decisions():
     steps = X.device_plan(g, "b200", 256, "bf16", options="no_fire=1")["steps"]
     assert any(s["layers"] == ["fire9_squeeze"] for s in steps)
     g = X.load_graph(X.graph_path("inc3a"))
+    # the fire kernel would need 4 groups of 32 channels for inception's 3x3
+    # (weights), which it does not take: the cost model splits the block
     steps = X.device_plan(g, "b200", 64, "bf16")["steps"]
-    assert any(s["layers"] == ["r3", "b3"] for s in steps), [s["layers"] for s in steps]
+    assert any(s["layers"] == ["b3"] for s in steps), [s["layers"] for s in steps]
     steps = X.device_plan(g, "b200", 64, "bf16", options="no_fire=1")["steps"]
     assert any(s["layers"] == ["b3"] for s in steps), [s["layers"] for s in steps]
     steps = X.device_plan(g, "b200", 64, "bf16", options="no_fire=1,always_fuse=1")["steps"]
