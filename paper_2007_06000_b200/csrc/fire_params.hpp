@@ -62,7 +62,8 @@ struct FireParams {
     int plane_cells;      // cells per plane, incl. one leading slack cell
     int plane_bytes;      // plane_cells * 16 * schunks
     int sq_cols;          // TMEM columns per squeeze accumulator (two of them)
-    int nexslots;         // expand accumulators (nops * gch columns each: every op of one M tile)
+    int nexslots;         // expand accumulators (nops * gch columns each: every op of one M tile; gch with per_op)
+    int per_op;           // one expand job per (M tile, op) instead of per M tile (two whole-tile accumulators would not fit TMEM)
     int seg;              // expand store segment: channels of one op per warp pass (64 bf16 if gch % 64 == 0, else 32)
     int ring_off, wsq_off, plane_off, sqbias_off, stage_off, smem_bytes;  // stage: 8 epilogue warps x 4 KB store staging (-1: direct stores)
     int pdl;

@@ -108,7 +108,9 @@ std::vector<std::pair<double, FireParams>> fire_candidates(const FireParams& P, 
         // N < 64 expand MMAs cost as much as N = 64 ones (measured: inception-3a's
         // reduce -> 3x3 at 4 groups of 32 took 61 us against 42 us unfused)
         if (gch < std::min(64, cout)) continue;
-        if (gch > 256 || 2 * sq_cols + 2 * P.nops * gch > 512) continue;  // two expand accumulators (every op of an M tile each)
+        if (gch > 256 || 2 * sq_cols + 2 * gch > 512) continue;  // two expand accumulators, at least one op each
+        // every op of an M tile in one job when two such accumulators fit TMEM, else one job per op
+        const int per_op = 2 * sq_cols + 2 * P.nops * gch > 512 ? 1 : 0;
         std::vector<std::pair<int, int>> shapes;  // (G, R)
         for (int G = 1; G <= 8; ++G) shapes.push_back({G, P.H});
         for (int R = 1; R < P.H; ++R) shapes.push_back({1, R});
@@ -140,7 +142,8 @@ std::vector<std::pair<double, FireParams>> fire_candidates(const FireParams& P, 
             if (!nst) continue;
             fire_layout(Q, nst, npl, stg);
             Q.sq_cols = sq_cols;
-            Q.nexslots = std::min(kFireMaxExSlots, (512 - 2 * sq_cols) / (Q.nops * gch));
+            Q.per_op = per_op;
+            Q.nexslots = std::min(kFireMaxExSlots, (512 - 2 * sq_cols) / ((per_op ? 1 : Q.nops) * gch));
             // model (SM cycles)
             const int units = G > 1 ? cdiv(batch, G) : batch * Q.bands;
             const long long items = (long long)units * ns;

@@ -129,7 +129,7 @@ __device__ __forceinline__ Round round_of(const FireParams& P, int r, int nu) {
     Round R;
     if (P.nplane == 2) R.sq = r < nu ? r : -1, R.ex = r >= 1 ? r - 1 : -1;
     else R.sq = r, R.ex = r;
-    R.ns = R.sq >= 0 ? P.Ts : 0, R.ne = R.ex >= 0 ? P.Te : 0;
+    R.ns = R.sq >= 0 ? P.Ts : 0, R.ne = R.ex >= 0 ? P.Te * (P.per_op ? P.nops : 1) : 0;
     return R;
 }
 // Walks the jobs of a round: squeeze tile (idx, true) or expand tile (idx,
@@ -200,7 +200,8 @@ __global__ void __launch_bounds__(kThreads, 1) fire_kernel(const __grid_constant
     const int nu = int(blockIdx.x) < units ? (units - 1 - int(blockIdx.x)) / int(gridDim.x) + 1 : 0;
     const int rounds = nu == 0 ? 0 : P.nplane == 2 ? nu + 1 : nu;
     const int NE = P.nexslots;
-    const int JW = P.nops * P.gch;  // TMEM columns of one expand job (every op of one M tile)
+    const int JW = (P.per_op ? 1 : P.nops) * P.gch;  // TMEM columns of one expand job (every op of one M tile, or one op)
+    const int nj = P.per_op ? P.nops : 1;             // expand jobs per M tile
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     if (threadIdx.x == 0) {
         for (int s = 0; s < P.nst; ++s) mbar_init(&full[s], 1), mbar_init(&empty[s], 1);
@@ -328,12 +329,14 @@ __global__ void __launch_bounds__(kThreads, 1) fire_kernel(const __grid_constant
                         if (ex_cnt >= NE) mbar_wait(&exe[a], uint32_t(ex_cnt / NE - 1) & 1u);
                         fence_after();
                         stamp(P, 0, tn, 22, ex_cnt);
-                        const uint64_t ajob = aplane + uint64_t(idx * 128);
+                        const int te = idx / nj, o0 = idx - te * nj;  // per-op jobs: op o0 of tile te; else every op
+                        const uint64_t ajob = aplane + uint64_t(te * 128);
                         const uint32_t dj = tmem + exc0 + uint32_t(a * JW);
 #pragma unroll
                         for (int o = 0; o < kFireMaxOps; ++o) {
                             if (o >= nops) break;
-                            const uint32_t d = dj + uint32_t(o * gch);
+                            if (nj > 1 && o != o0) continue;
+                            const uint32_t d = dj + uint32_t((nj > 1 ? 0 : o) * gch);
                             uint64_t arow = ajob + uint64_t(int64_t(osh[o]));  // shift >= -(Wp + 1): no borrow out of the field
                             uint64_t bd = ob[o];
                             uint32_t acc = 0;
@@ -467,8 +470,9 @@ __global__ void __launch_bounds__(kThreads, 1) fire_kernel(const __grid_constant
                         __syncwarp();
                         if (lane == 0) mbar_arrive(&plf[pls]);
                     }
-                } else {  // ---------------------------------------------------- expand tile idx of unit R.ex
-                    const int q = P.Wp + idx * 128 + t;
+                } else {  // ---------------------------------------------------- expand job idx of unit R.ex
+                    const int te = idx / nj, o0 = idx - te * nj;  // M tile; op of a per-op job
+                    const int q = P.Wp + te * 128 + t;
                     const int pr = fdiv(q, P.Wp, iWp), cc = q - pr * P.Wp;
                     const int ii = fdiv(pr, Rp, iRp), rr = pr - ii * Rp, ir = Ue.r0 + rr - 1;
                     const bool valid = cc >= 1 && ii < Ue.ni && rr >= 1 && ir < P.H;
@@ -505,7 +509,7 @@ __global__ void __launch_bounds__(kThreads, 1) fire_kernel(const __grid_constant
 #pragma unroll
                             for (int u = 0; u < 2; ++u) {
                                 if (u == 1 && !two) break;
-                                int o = 0, c0 = (cb + 2 * u) * 32;
+                                int o = nj > 1 ? o0 : 0, c0 = (cb + 2 * u) * 32;
                                 while (c0 >= P.gch) c0 -= P.gch, ++o;
                                 const FireOp& op = P.op[o];
                                 const uint32_t bsm = smem_u32(smem + op.bias_off) + uint32_t(c0) * 4u;
@@ -545,14 +549,16 @@ __global__ void __launch_bounds__(kThreads, 1) fire_kernel(const __grid_constant
                     } else {
                         const int cpl = 32 / pieces;  // cells per store instruction
                         for (int o = 0; o < P.nops; ++o) {
+                            if (nj > 1 && o != o0) continue;
                             const FireOp& op = P.op[o];
                             const uint32_t bsm = smem_u32(smem + op.bias_off);
+                            const int ocol = nj > 1 ? 0 : o;  // the op's column block inside the job
                             T* dsto = valid ? static_cast<T*>(op.out) + pix * op.out_cstride + op.out_coff + g * P.gch : nullptr;
                             for (int k = (half + o * spo) & 1; k < spo; k += 2) {  // segments of the op whose global index has this parity
                                 const int c0 = k * SEG;
                                 for (int h = 0; h < SEG; h += 32) {
                                     float v[32];
-                                    tmem_ld32(tmem + tl + exc0 + uint32_t(a * JW + o * P.gch + c0 + h), v);
+                                    tmem_ld32(tmem + tl + exc0 + uint32_t(a * JW + ocol * P.gch + c0 + h), v);
     #pragma unroll
                                     for (int j = 0; j < 32; j += 8) {
                                         const float4 b0 = ld_shared_f4(bsm + uint32_t(c0 + h + j) * 4u), b1 = ld_shared_f4(bsm + uint32_t(c0 + h + j + 4) * 4u);

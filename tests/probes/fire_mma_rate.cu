@@ -7,6 +7,8 @@
 // nvcc -gencode arch=compute_100a,code=sm_100a -O3 -I../../paper_2007_06000_b200/csrc fire_mma_rate.cu -o fire_mma_rate
 #include <cstdio>
 #include <cstdint>
+#include <cuda.h>
+#include <cudaTypedefs.h>
 #include "umma.cuh"
 using namespace xlf::umma;
 
@@ -105,7 +107,15 @@ __global__ void k(int jobs, int N, int nks, int busy, float* gout, unsigned long
 // The fire kernel's round: a squeeze tile (4 MMAs, N = 16, A in a SWIZZLE_128B
 // stage) + commit, then an expand tile (e1: 1 MMA, e3: 9 shifted MMAs, N = 64)
 // + commit, with the kernel's shared-memory placement (plane stride 16256 B).
-__global__ void kround(int jobs, int with_sq, unsigned long long* out, int fence_mode = 0) {
+__device__ __forceinline__ bool lane_is0() { return (threadIdx.x & 31) == 0; }
+__device__ __forceinline__ void tma2d(void* smem, const void* desc, int c0, int c1, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];\n" ::"r"(smem_u32(smem)),
+        "l"(desc), "r"(c0), "r"(c1), "r"(smem_u32(bar))
+        : "memory");
+}
+
+__global__ void kround(int jobs, int with_sq, unsigned long long* out, int fence_mode = 0, const __grid_constant__ CUtensorMap tmap = CUtensorMap{}, int tma = 0) {
     extern __shared__ __align__(1024) uint8_t smem[];
     __shared__ uint64_t bar, jb;
     __shared__ uint32_t slot;
@@ -118,7 +128,22 @@ __global__ void kround(int jobs, int with_sq, unsigned long long* out, int fence
     __syncthreads();
     fence_after();
     const uint32_t tmem = slot;
-    if (warp == 0 && elect_one()) {
+    __shared__ volatile int stop;
+    __shared__ uint64_t tb;
+    if (threadIdx.x == 0) stop = 0, mbar_init(&tb, 1), mbar_fence_init();
+    __syncthreads();
+    if (warp == 1) {  // concurrent TMA: 16 KB boxes into a separate region, back to back
+        if (tma && lane_is0()) {
+            uint32_t ph = 0;
+            int r = 0;
+            while (!stop) {
+                mbar_expect_tx(&tb, 16384);
+                tma2d(smem + 176 * 1024, &tmap, 0, (r++ * 128) & 65535, &tb);
+                mbar_wait(&tb, ph);
+                ph ^= 1;
+            }
+        }
+    } else if (warp == 0 && elect_one()) {
         const uint32_t sb = smem_u32(smem);
         const int Wp = 56;
         const uint32_t PS = 1016 * 16;
@@ -161,6 +186,7 @@ __global__ void kround(int jobs, int with_sq, unsigned long long* out, int fence
         mbar_wait(&bar, 0);
         long long t2 = clock64();
         out[0] = t1 - t0, out[1] = t2 - t0;
+        stop = 1;
     }
     fence_before();
     __syncthreads();
@@ -192,13 +218,32 @@ int main() {
             cudaMemcpy(h, d, 16, cudaMemcpyDeviceToHost);
             printf("dcol %3d step %3d N=64 nks=1: %.1f cyc/mma\n", dc, ds, h[1] / 1800.0);
         }
-    cudaFuncSetAttribute(kround, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    for (int fm : {0, 1, 2, 3, 4, 7})
+    cudaFuncSetAttribute(kround, cudaFuncAttributeMaxDynamicSharedMemorySize, 210 * 1024);
+    // a 2-D tensor {64 bf16 channels, 65536 rows} for the concurrent TMA loads
+    void* gsrc;
+    cudaMalloc(&gsrc, size_t(65536) * 128);
+    CUtensorMap tm;
+    void* fp = nullptr;
+    cudaDriverEntryPointQueryResult qr;
+    cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fp, cudaEnableDefault, &qr);
+    const cuuint64_t dims[2] = {64, 65536};
+    const cuuint64_t strides[1] = {128};
+    const cuuint32_t box[2] = {64, 128}, es[2] = {1, 1};
+    reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fp)(&tm, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, gsrc, dims, strides, box, es,
+                                                           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                                                           CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    for (int tma : {0, 1})
         for (int sq : {0, 1}) {
             unsigned long long h[2];
-            kround<<<1, 32, 200 * 1024>>>(200, sq, d, fm);
+            kround<<<1, 64, 210 * 1024>>>(200, sq, d, 0, tm, tma);
             cudaMemcpy(h, d, 16, cudaMemcpyDeviceToHost);
-            printf("kernel round (squeeze %d, fence mode %d): %.0f cycles per round\n", sq, fm, h[1] / 200.0);
+            printf("kernel round (squeeze %d, concurrent TMA %d): %.0f cycles per round\n", sq, tma, h[1] / 200.0);
         }
+    for (int tma : {0, 1}) {  // all SMs at once
+        unsigned long long h[2];
+        kround<<<148, 64, 210 * 1024>>>(200, 1, d, 0, tm, tma);
+        cudaMemcpy(h, d, 16, cudaMemcpyDeviceToHost);
+        printf("148 CTAs, kernel round (squeeze 1, concurrent TMA %d): %.0f cycles per round\n", tma, h[1] / 200.0);
+    }
     printf("%s\n", cudaGetErrorString(cudaDeviceSynchronize()));
 }

