@@ -21,7 +21,7 @@
 
 namespace xlf {
 
-constexpr int kFireStages = 6;     // max squeeze-input ring stages (128 px x 128 B each)
+constexpr int kFireStages = 6;     // max squeeze-input ring stages (128 px x 128 or 64 B each)
 constexpr int kFireMaxOps = 4;     // expand ops
 constexpr int kFireMaxExSlots = 8; // expand accumulator slots in TMEM
 constexpr int kFireSmemMax = 227 * 1024 - 1024;
@@ -41,11 +41,12 @@ struct FireOp {
 };
 
 struct FireParams {
-    CUtensorMap amap;     // squeeze A: 2-D {cstride_in, max_batch * H * W}, box {128 bytes of channels, 128 pixels}, SWIZZLE_128B
+    CUtensorMap amap;     // squeeze A: 2-D {cstride_in, max_batch * H * W}, box {cb bytes of channels, 128 pixels}, SWIZZLE_128B / 64B
+    int cb;               // input chunk bytes per pixel per stage: 128 (SWIZZLE_128B) or 64 (SWIZZLE_64B)
     int es;               // element bytes (2 bf16 kind::f16 / 4 TF32 kind::tf32)
     int H, W, HW, Wp;     // Wp = W + 1
     int coff_in;          // first input channel inside its allocation (concat view)
-    int kchunks, ksteps;  // squeeze K: 128-byte chunks / 32-byte MMA steps
+    int kchunks, ksteps;  // squeeze K: cb-byte chunks / 32-byte MMA steps
     int S, schunks;       // squeeze channels (multiple of 16) / 16-byte chunks per plane cell
     const uint8_t* wsq;   // squeeze packed B [ksteps * 2][S][cpc]
     const float* sq_bias;
@@ -56,7 +57,7 @@ struct FireParams {
     FireOp op[kFireMaxOps];
     int gch, nsplit;      // channels per group of every expand op; groups (grid y)
     int nst;              // ring stages
-    int stage_bytes;      // ring stage: 128 x 128-byte input chunk (+ that K chunk's squeeze weights when sq_stream)
+    int stage_bytes;      // ring stage: 128 x cb-byte input chunk (+ that K chunk's squeeze weights when sq_stream)
     int sq_stream;        // squeeze weights streamed through the ring per K chunk instead of resident
     int nplane;           // squeeze planes (2: the next unit's squeeze overlaps this unit's expand)
     int plane_cells;      // cells per plane, incl. one leading slack cell
@@ -70,6 +71,7 @@ struct FireParams {
     int st32;             // every op's output pixel / channel offsets are 32-byte aligned: 256-bit stores
     unsigned long long* trace;  // option trace=1: 3 roles x kFireTraceN x (code, globaltimer) of CTA (0, 0)
     int stage_mode;             // host planning only: 0 direct stores, 1 staged through shared memory (option fire_stage)
+    int cb_mode;                // host planning only: chunk width 128 (0: default) or 64 (option fire_cb)
     int sq_stream_mode;         // host planning only: 0 either, 1 streamed squeeze weights only, 2 resident only (option fire_sqs)
 };
 

@@ -63,7 +63,7 @@ int fire_layout(FireParams& P, int nst, int nplane, bool staged) {
     int off = 0;
     P.nst = nst, P.nplane = nplane;
     P.ring_off = 0;
-    P.stage_bytes = 128 * 128 + (P.sq_stream ? up(4 * P.S * 32, 1024) : 0);  // stages stay 1024-aligned (SWIZZLE_128B)
+    P.stage_bytes = 128 * P.cb + (P.sq_stream ? up((P.cb / 32) * P.S * 32, 1024) : 0);  // stages stay 1024-aligned (swizzle atoms)
     off = nst * P.stage_bytes;
     P.wsq_off = off;
     if (!P.sq_stream) off = up(off + P.ksteps * P.S * 32, 128);
@@ -98,9 +98,14 @@ std::vector<std::pair<double, FireParams>> fire_candidates(const FireParams& P, 
     const int sq_cols = P.S <= 32 ? 32 : P.S <= 64 ? 64 : 128;
     const double bw_chip = 3300.0;  // HBM bytes per SM cycle, whole chip (~6.5 TB/s at 1.965 GHz)
     std::vector<std::pair<double, FireParams>> out;
+    for (int cb : {128, 64})
     for (int sqs : {0, 1})
     for (int ns : {1, 2, 4}) {
         if (force_nsplit > 0 && ns != force_nsplit) continue;
+        // 64-byte chunks only on request: they let wider expand weights stay
+        // resident (fire8/9 at two channel groups) but measured slower on
+        // every SqueezeNet fire step and on inception's r3 -> b3
+        if (cb != (P.cb_mode ? P.cb_mode : 128)) continue;
         if (P.sq_stream_mode == 1 && sqs == 0) continue;
         if (P.sq_stream_mode == 2 && sqs == 1) continue;
         if (cout % (32 * ns)) continue;  // whole 32-column store segments per op and group
@@ -119,6 +124,8 @@ std::vector<std::pair<double, FireParams>> fire_candidates(const FireParams& P, 
             if (force_r > 0 && R != force_r) continue;
             if (G > 1 && G > batch) continue;
             FireParams Q = P;
+            Q.cb = cb;
+            Q.kchunks = (Q.ksteps * 32 + cb - 1) / cb;
             Q.sq_stream = sqs;
             Q.nsplit = ns, Q.gch = gch, Q.G = G, Q.R = R, Q.bands = cdiv(P.H, R);
             Q.seg = P.es == 2 && gch % 64 == 0 ? 64 : 32;  // 128-byte store segments when the op's channels allow
@@ -133,7 +140,7 @@ std::vector<std::pair<double, FireParams>> fire_candidates(const FireParams& P, 
             for (int st = 0; st <= 1 && !nst; ++st) {
                 if (st != (P.stage_mode == 1 ? 1 : 0)) continue;
                 for (int pl = 2; pl >= 1 && !nst; --pl)
-                    for (int s = kFireStages; s >= 3; --s)
+                    for (int s = kFireStages; s >= (cb == 64 ? 2 : 3); --s)
                         if (fire_layout(Q, s, pl, st != 0) > 0) {
                             nst = s, npl = pl, stg = st != 0;
                             break;
@@ -184,6 +191,7 @@ void fire_shape(const Graph& g, const StepSpec& s, int es, FireParams& P) {
     const TensorShape in = g.shape_of(s.inputs[0]);
     P.es = es, P.H = in.height, P.W = in.width, P.HW = in.height * in.width, P.Wp = in.width + 1;
     P.ksteps = sq.conv->in_channels * es / 32;
+    P.cb = 128;
     P.kchunks = (P.ksteps + 3) / 4;
     P.S = sq.conv->out_channels;
     P.schunks = P.S * es / 16;
@@ -206,6 +214,7 @@ bool fire_feasible(const Graph& g, const StepSpec& s, int es, int batch, const K
     fire_shape(g, s, es, P);
     P.stage_mode = k.fire_stage;
     P.sq_stream_mode = k.fire_sqs;
+    P.cb_mode = k.fire_cb;
     return fire_choose(P, std::max(1, batch), 148, k.fire_nsplit, k.fire_g, k.fire_r, nullptr);
 }
 

@@ -43,7 +43,9 @@ using namespace umma;
 constexpr int kEpi = 256;  // 8 epilogue warps: two per TMEM lane quadrant
 constexpr int kThreads = kEpi + 64;
 constexpr int kProd = kEpi / 32, kMma = kEpi / 32 + 1;
-constexpr int kStageBytes = 128 * 128;
+// Squeeze-input stages: 128 pixels x a K chunk of P.cb bytes (128: SWIZZLE_128B,
+// 4 K steps; 64: SWIZZLE_64B, 2 K steps -- narrow stages leave room for
+// larger resident expand weights).
 constexpr int kTmemCols = 512;
 
 template <class T>
@@ -232,7 +234,9 @@ __global__ void __launch_bounds__(kThreads, 1) fire_kernel(const __grid_constant
                 for (uint32_t o = 0; o < b; o += 65536) bulk_g2s(smem + P.op[k].w_off + o, src + o, min(65536u, b - o), &wbar);
             }
             asm volatile("griddepcontrol.wait;" ::: "memory");  // the input is the previous step's output
-            const int kc_elems = 128 / P.es;
+            const int kc_elems = P.cb / P.es;
+            const int kpc = P.cb / 32;                  // K steps per chunk
+            const uint32_t abytes = 128u * uint32_t(P.cb);  // input bytes per stage
             int it = 0, tn = 0;
             for (int k = 0; k < nu; ++k) {  // squeeze tiles in unit order (every round order keeps them in it)
                 const Unit U = unit_of(P, int(blockIdx.x) + k * int(gridDim.x), n0, count);
@@ -243,11 +247,11 @@ __global__ void __launch_bounds__(kThreads, 1) fire_kernel(const __grid_constant
                         stamp(P, 2, tn, 50, it);
                         uint8_t* stage = smem + P.ring_off + s * P.stage_bytes;
                         if (P.sq_stream) {  // this K chunk's squeeze weights ride along with the input chunk
-                            const uint32_t b = uint32_t(min(4, P.ksteps - kc * 4)) * uint32_t(P.S) * 32u;
-                            mbar_expect_tx(&full[s], kStageBytes + b);
-                            bulk_g2s(stage + kStageBytes, P.wsq + size_t(kc) * 4 * P.S * 32, b, &full[s]);
+                            const uint32_t b = uint32_t(min(kpc, P.ksteps - kc * kpc)) * uint32_t(P.S) * 32u;
+                            mbar_expect_tx(&full[s], abytes + b);
+                            bulk_g2s(stage + abytes, P.wsq + size_t(kc) * kpc * P.S * 32, b, &full[s]);
                         } else {
-                            mbar_expect_tx(&full[s], kStageBytes);
+                            mbar_expect_tx(&full[s], abytes);
                         }
                         tma_2d(stage, &P.amap, P.coff_in + kc * kc_elems, U.p0 + ts * 128, &full[s]);
                     }
@@ -264,8 +268,9 @@ __global__ void __launch_bounds__(kThreads, 1) fire_kernel(const __grid_constant
             const uint32_t idsq = FElem<T>::idesc(P.S), idex = FElem<T>::idesc(P.gch);
             const uint64_t bsq0 = sdesc(smem_u32(smem + P.wsq_off), uint32_t(P.S) * 16u, 128u, kNoSwizzle);
             const uint32_t bsq_step = (uint32_t(P.S) * 32u) >> 4;
-            const uint64_t ring0 = sdesc(ring, 16u, 1024u, kSW128);
-            const uint64_t bsq_ring = sdesc(ring + uint32_t(kStageBytes), uint32_t(P.S) * 16u, 128u, kNoSwizzle);
+            const uint64_t ring0 = P.cb == 128 ? sdesc(ring, 16u, 1024u, kSW128) : sdesc(ring, 16u, 512u, kSW64);
+            const uint64_t bsq_ring = sdesc(ring + 128u * uint32_t(P.cb), uint32_t(P.S) * 16u, 128u, kNoSwizzle);
+            const int kpc = P.cb / 32;  // K steps per input chunk
             const int nst = P.nst, kchunks = P.kchunks, ksteps = P.ksteps, Ts = P.Ts, nops = P.nops, gch = P.gch, Wp = P.Wp;
             const int nks = P.schunks / 2;                        // expand K steps per tap
             const uint32_t da = (2u * PS) >> 4, db = 2u * uint32_t(gch);  // next K step: A (two plane chunks), B
@@ -304,13 +309,13 @@ __global__ void __launch_bounds__(kThreads, 1) fire_kernel(const __grid_constant
                             const int s = it % nst;
                             mbar_wait(&full[s], uint32_t(it / nst) & 1u);
                             fence_after();
-                            const int steps = min(4, ksteps - kc * 4);
+                            const int steps = min(kpc, ksteps - kc * kpc);
                             uint64_t ad = ring0 + uint64_t(s * (P.stage_bytes >> 4));
                             if (P.sq_stream) bd = bsq_ring + uint64_t(s * (P.stage_bytes >> 4));  // this chunk's weights in the stage
                             for (int kk = 0; kk < steps; ++kk) {
                                 FElem<T>::mma(d, ad, bd, idsq, acc);
                                 acc = 1;
-                                ad += 2;  // +32 bytes inside the 128-byte swizzle row
+                                ad += 2;  // +32 bytes inside the swizzle row
                                 bd += bsq_step;
                             }
                             commit(&empty[s]);
