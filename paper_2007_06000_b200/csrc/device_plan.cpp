@@ -501,6 +501,7 @@ Knobs Knobs::parse(const std::string& text) {
         else if (key == "fire_stage") k.fire_stage = int(need_num());
         else if (key == "fire_sqs") k.fire_sqs = int(need_num());
         else if (key == "fire_cb") k.fire_cb = int(need_num());
+        else if (key == "fire_cps") k.fire_cps = int(need_num());
         else if (key == "trace") k.trace = int(need_num());
         else if (key == "tune_verbose") k.tune_verbose = need_num() != 0;
         else if (key == "e2e_chunks") k.e2e_chunks = std::max(1, int(need_num()));

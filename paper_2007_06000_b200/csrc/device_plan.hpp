@@ -47,6 +47,7 @@ struct Knobs {
     bool no_dw = false;          // depthwise (+ pointwise) steps through the generic kernels, not the depthwise kernel
     bool no_fire = false;        // split-mode squeeze -> expand blocks through the generic fused-block kernel, not the fire kernel
     int fire_g = 0, fire_r = 0, fire_nsplit = 0;  // force the fire kernel's unit (G images / R-row bands) and channel groups
+    int fire_cps = 0;            // fire kernel CTAs per SM: 0 planner's choice, 1 or 2
     int fire_cb = 0;             // fire kernel squeeze-input chunk: 0 planner's choice, 128 or 64 bytes per pixel per stage
     int fire_sqs = 0;            // fire kernel squeeze weights: 0 planner's choice, 1 streamed through the ring, 2 resident
     int fire_stage = 0;          // fire kernel stores: 0 direct (16-byte fragments), 1 staged through shared memory (whole segments)

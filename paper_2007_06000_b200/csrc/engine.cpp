@@ -499,7 +499,7 @@ std::unique_ptr<DwParams> Engine::build_dw(const StepSpec& s) {
 // 1x1 squeeze staged on chip and whose consumers are stride-1 "same" expand
 // convs of one width (fire_step_ok); its unit / channel split / ring are
 // chosen by fire_choose at max_batch.
-std::unique_ptr<FireParams> Engine::build_fire(const StepSpec& s, int fns, int fg, int fr, int sqs, int cb) {
+std::unique_ptr<FireParams> Engine::build_fire(const StepSpec& s, int fns, int fg, int fr, int sqs, int cb, int cps) {
     int th, tw;
     if (!tc_es_ || knobs_.no_fire || !fire_step_ok(g_, s, tc_es_) || knobs_.forced_tile(s, &th, &tw)) return nullptr;
     if (s2d_ && s.inputs[0] == g_.inputs[0].name) return nullptr;  // row-planar / rewritten input
@@ -511,6 +511,7 @@ std::unique_ptr<FireParams> Engine::build_fire(const StepSpec& s, int fns, int f
     P->stage_mode = knobs_.fire_stage;
     P->sq_stream_mode = sqs < 0 ? knobs_.fire_sqs : sqs ? 1 : 2;
     P->cb_mode = cb > 0 ? cb : knobs_.fire_cb;
+    P->cps_mode = cps > 0 ? cps : knobs_.fire_cps;
     P->coff_in = xt.coff;
     P->sq_bias = weights_ + plan_.b_off.at(sq.name);
     for (int o = 0; o < P->nops; ++o) {
@@ -666,16 +667,17 @@ std::string Engine::autotune(int batch, int reps, int topk) {
         shape.stage_mode = knobs_.fire_stage;
         shape.sq_stream_mode = knobs_.fire_sqs;
         shape.cb_mode = knobs_.fire_cb;
-        std::vector<std::array<int, 5>> cands = {{fires_[i]->nsplit, fires_[i]->G, fires_[i]->R, fires_[i]->sq_stream, fires_[i]->cb}};
+        shape.cps_mode = knobs_.fire_cps;
+        std::vector<std::array<int, 6>> cands = {{fires_[i]->nsplit, fires_[i]->G, fires_[i]->R, fires_[i]->sq_stream, fires_[i]->cb, fires_[i]->cps}};
         // the model ranks unit shapes only roughly (it misses per-unit latency
         // chains): time the best 8 * topk by the model and at least topk of
         // every (split, whole images / row bands, squeeze-weight mode) family
-        std::map<std::array<int, 3>, int> per_family;
+        std::map<std::array<int, 4>, int> per_family;
         const auto all = fire_candidates(shape, batch, 148, 0, 0, 0);
         for (size_t k = 0; k < all.size(); ++k) {
             const FireParams& Q = all[k].second;
-            const std::array<int, 5> c = {Q.nsplit, Q.G, Q.R, Q.sq_stream, Q.cb};
-            int& fam = per_family[{Q.nsplit, Q.G > 1, Q.sq_stream}];
+            const std::array<int, 6> c = {Q.nsplit, Q.G, Q.R, Q.sq_stream, Q.cb, Q.cps};
+            int& fam = per_family[{Q.nsplit, Q.G > 1, Q.sq_stream, Q.cps}];
             if ((int(k) < 8 * topk || fam < topk) && std::find(cands.begin(), cands.end(), c) == cands.end())
                 cands.push_back(c), ++fam;
         }
@@ -683,7 +685,7 @@ std::string Engine::autotune(int batch, int reps, int topk) {
         std::unique_ptr<FireParams> bestP;
         int tried = 0;
         for (const auto& c : cands) {
-            std::unique_ptr<FireParams> P = build_fire(s, c[0], c[1], c[2], c[3], c[4]);
+            std::unique_ptr<FireParams> P = build_fire(s, c[0], c[1], c[2], c[3], c[4], c[5]);
             if (!P) continue;
             cuda_check(launch_fire(*P, 0, batch, st), "autotune warm-up");
             cuda_check(cudaEventRecord(e0, st), "cudaEventRecord");
@@ -695,8 +697,8 @@ std::string Engine::autotune(int batch, int reps, int topk) {
             ms /= float(reps);
             ++tried;
             if (knobs_.tune_verbose)
-                std::fprintf(stderr, "[xlf] tune %s (fire): nsplit %d G %d R %d sqs %d cb %d ring %d planes %d smem %d: %.1f us\n", s.id.c_str(), P->nsplit,
-                             P->G, P->R, P->sq_stream, P->cb, P->nst, P->nplane, P->smem_bytes, ms * 1000.0f);
+                std::fprintf(stderr, "[xlf] tune %s (fire): nsplit %d G %d R %d sqs %d cb %d cps %d ring %d planes %d smem %d: %.1f us\n", s.id.c_str(), P->nsplit,
+                             P->G, P->R, P->sq_stream, P->cb, P->cps, P->nst, P->nplane, P->smem_bytes, ms * 1000.0f);
             if (ms < best_ms) best_ms = ms, bestP = std::move(P);
         }
         if (!bestP) continue;
@@ -706,7 +708,7 @@ std::string Engine::autotune(int batch, int reps, int topk) {
         t.tile_h = fires_[i]->G > 1 ? fires_[i]->G * fires_[i]->H : fires_[i]->R;
         t.smem_bytes = fires_[i]->smem_bytes;
         js << (first ? "" : ",") << "{\"id\":\"" << s.id << "\",\"kernel\":\"fire\",\"tried\":" << tried << ",\"us\":" << best_ms * 1000.0f
-           << ",\"nsplit\":" << fires_[i]->nsplit << ",\"G\":" << fires_[i]->G << ",\"R\":" << fires_[i]->R << ",\"sqs\":" << fires_[i]->sq_stream << ",\"cb\":" << fires_[i]->cb
+           << ",\"nsplit\":" << fires_[i]->nsplit << ",\"G\":" << fires_[i]->G << ",\"R\":" << fires_[i]->R << ",\"sqs\":" << fires_[i]->sq_stream << ",\"cb\":" << fires_[i]->cb << ",\"cps\":" << fires_[i]->cps
            << ",\"smem_bytes\":" << fires_[i]->smem_bytes
            << "}";
         first = false;
@@ -809,7 +811,7 @@ void Engine::apply_tuning(const std::string& js) {
         return true;
     };
     std::vector<std::pair<size_t, StepSpec>> todo;
-    std::vector<std::pair<size_t, std::array<int, 5>>> fire_todo;
+    std::vector<std::pair<size_t, std::array<int, 6>>> fire_todo;
     size_t pos = 0;
     while ((pos = js.find('{', pos)) != std::string::npos) {
         const size_t end = js.find('}', pos);
@@ -824,13 +826,13 @@ void Engine::apply_tuning(const std::string& js) {
         size_t i = 0;
         while (i < plan_.steps.size() && plan_.steps[i].id != id) ++i;
         if (i < plan_.steps.size() && fires_[i]) {  // fire step: channel split and unit
-            int ns = 0, G = 0, R = 0, sqs = -1, cb = 0;
-            num(obj, "sqs", sqs), num(obj, "cb", cb);
+            int ns = 0, G = 0, R = 0, sqs = -1, cb = 0, cps = 0;
+            num(obj, "sqs", sqs), num(obj, "cb", cb), num(obj, "cps", cps);
             if (!num(obj, "nsplit", ns) || !num(obj, "G", G) || !num(obj, "R", R))
                 fail(ErrorKind::parse, "tuning report: fire step '" + id + "' needs \"nsplit\", \"G\" and \"R\"");
             if (ns < 1 || G < 1 || R < 1) fail(ErrorKind::infeasible, "tuning report: configuration of step '" + id + "' is not feasible for this plan");
-            if (cb != 0 && cb != 64 && cb != 128) fail(ErrorKind::infeasible, "tuning report: configuration of step '" + id + "' is not feasible for this plan");
-            fire_todo.push_back({i, {ns, G, R, sqs, cb}});
+            if ((cb != 0 && cb != 64 && cb != 128) || cps < 0 || cps > 2) fail(ErrorKind::infeasible, "tuning report: configuration of step '" + id + "' is not feasible for this plan");
+            fire_todo.push_back({i, {ns, G, R, sqs, cb, cps}});
             continue;
         }
         if (i == plan_.steps.size() || !bparams_[i]) fail(ErrorKind::validation, "tuning report: no tensor-core fused step '" + id + "'");
@@ -855,9 +857,10 @@ void Engine::apply_tuning(const std::string& js) {
     }
     std::vector<std::unique_ptr<FireParams>> fire_built;
     for (auto& [i, c] : fire_todo) {
-        fire_built.push_back(build_fire(plan_.steps[i], c[0], c[1], c[2], c[3], c[4]));
+        fire_built.push_back(build_fire(plan_.steps[i], c[0], c[1], c[2], c[3], c[4], c[5]));
         if (!fire_built.back() || fire_built.back()->nsplit != c[0] || fire_built.back()->G != c[1] || fire_built.back()->R != c[2] ||
-            (c[3] >= 0 && fire_built.back()->sq_stream != c[3]) || (c[4] > 0 && fire_built.back()->cb != c[4]))
+            (c[3] >= 0 && fire_built.back()->sq_stream != c[3]) || (c[4] > 0 && fire_built.back()->cb != c[4]) ||
+            (c[5] > 0 && fire_built.back()->cps != c[5]))
             fail(ErrorKind::infeasible, "tuning report: configuration of step '" + plan_.steps[i].id + "' is not feasible for this plan");
     }
     // captured forwards and external-address descriptors hold the current configurations
@@ -1165,7 +1168,7 @@ void Engine::forward_external(const std::vector<External>& ext, int batch, cudaS
                     set->dw[i] = build_dw(s);
                     if (!set->dw[i]) fail(ErrorKind::internal, "step " + s.id + ": depthwise descriptor for caller-owned tensors");
                 } else if (fires_[i]) {  // same configuration, the caller's addresses
-                    set->fr[i] = build_fire(s, fires_[i]->nsplit, fires_[i]->G, fires_[i]->R, fires_[i]->sq_stream, fires_[i]->cb);
+                    set->fr[i] = build_fire(s, fires_[i]->nsplit, fires_[i]->G, fires_[i]->R, fires_[i]->sq_stream, fires_[i]->cb, fires_[i]->cps);
                     if (!set->fr[i]) fail(ErrorKind::internal, "step " + s.id + ": fire kernel descriptor for caller-owned tensors");
                 } else if (tc_es_) set->bp[i] = build_bparams(s);
                 else set->fp[i] = make_params(g_, plan_, s, allocs_, weights_);

@@ -85,7 +85,7 @@ private:
     std::unique_ptr<struct PwParams> build_pw(const StepSpec& s);
     // nsplit / G / R > 0 force the fire kernel's channel split / unit (else the knobs, else its model)
     std::unique_ptr<struct DwParams> build_dw(const StepSpec& s);
-    std::unique_ptr<struct FireParams> build_fire(const StepSpec& s, int nsplit = 0, int G = 0, int R = 0, int sqs = -1, int cb = 0);
+    std::unique_ptr<struct FireParams> build_fire(const StepSpec& s, int nsplit = 0, int G = 0, int R = 0, int sqs = -1, int cb = 0, int cps = 0);
     void launch_tc_step(size_t i, int n0, int count, cudaStream_t st);
     const TensorSlot& slot(const std::string& n) const;
     const TensorSlot& readable(const std::string& n) const;

@@ -25,6 +25,7 @@ constexpr int kFireStages = 6;     // max squeeze-input ring stages (128 px x 12
 constexpr int kFireMaxOps = 4;     // expand ops
 constexpr int kFireMaxExSlots = 8; // expand accumulator slots in TMEM
 constexpr int kFireSmemMax = 227 * 1024 - 1024;
+constexpr int kFireSmemMax2 = 111 * 1024;  // per CTA with two CTAs per SM (228 KB per SM less 1 KB reserved + 2 KB static per CTA)
 constexpr int kFireTraceN = 1024;  // trace events per role (option trace=1)
 
 struct FireOp {
@@ -42,6 +43,7 @@ struct FireOp {
 
 struct FireParams {
     CUtensorMap amap;     // squeeze A: 2-D {cstride_in, max_batch * H * W}, box {cb bytes of channels, 128 pixels}, SWIZZLE_128B / 64B
+    int cps;              // CTAs per SM: 1 (8 epilogue warps, 512 TMEM columns) or 2 (4 epilogue warps, 256 columns, <= kFireSmemMax2 bytes each)
     int cb;               // input chunk bytes per pixel per stage: 128 (SWIZZLE_128B) or 64 (SWIZZLE_64B)
     int es;               // element bytes (2 bf16 kind::f16 / 4 TF32 kind::tf32)
     int H, W, HW, Wp;     // Wp = W + 1
@@ -71,6 +73,7 @@ struct FireParams {
     int st32;             // every op's output pixel / channel offsets are 32-byte aligned: 256-bit stores
     unsigned long long* trace;  // option trace=1: 3 roles x kFireTraceN x (code, globaltimer) of CTA (0, 0)
     int stage_mode;             // host planning only: 0 direct stores, 1 staged through shared memory (option fire_stage)
+    int cps_mode;               // host planning only: 0 either, else 1 / 2 CTAs per SM (option fire_cps)
     int cb_mode;                // host planning only: chunk width 128 (0: default) or 64 (option fire_cb)
     int sq_stream_mode;         // host planning only: 0 either, 1 streamed squeeze weights only, 2 resident only (option fire_sqs)
 };

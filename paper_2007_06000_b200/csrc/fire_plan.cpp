@@ -75,7 +75,7 @@ int fire_layout(FireParams& P, int nst, int nplane, bool staged) {
     P.plane_bytes = P.plane_cells * 16 * (P.S / cpc);
     off = up(off + nplane * P.plane_bytes, 128);
     P.stage_off = staged ? off : -1;
-    if (staged) off += 8 * 4096;  // 8 epilogue warps x 32 cells x (64 or 128 bytes)
+    if (staged) off += (P.cps == 2 ? 4 : 8) * 4096;  // epilogue warps x 32 cells x (64 or 128 bytes)
     P.sqbias_off = off;
     off += P.S * 4;
     for (int o = 0; o < P.nops; ++o) {
@@ -83,7 +83,7 @@ int fire_layout(FireParams& P, int nst, int nplane, bool staged) {
         off += P.gch * 4;
     }
     P.smem_bytes = up(off, 128);
-    return P.smem_bytes <= kFireSmemMax ? P.smem_bytes : -1;
+    return P.smem_bytes <= (P.cps == 2 ? kFireSmemMax2 : kFireSmemMax) ? P.smem_bytes : -1;
 }
 
 // Every feasible (nsplit, G, R) for P (H, W, S, ksteps, nops, op[].kh / pad /
@@ -98,6 +98,7 @@ std::vector<std::pair<double, FireParams>> fire_candidates(const FireParams& P, 
     const int sq_cols = P.S <= 32 ? 32 : P.S <= 64 ? 64 : 128;
     const double bw_chip = 3300.0;  // HBM bytes per SM cycle, whole chip (~6.5 TB/s at 1.965 GHz)
     std::vector<std::pair<double, FireParams>> out;
+    for (int cps : {1, 2})
     for (int cb : {128, 64})
     for (int sqs : {0, 1})
     for (int ns : {1, 2, 4}) {
@@ -106,6 +107,8 @@ std::vector<std::pair<double, FireParams>> fire_candidates(const FireParams& P, 
         // resident (fire8/9 at two channel groups) but measured slower on
         // every SqueezeNet fire step and on inception's r3 -> b3
         if (cb != (P.cb_mode ? P.cb_mode : 128)) continue;
+        if (P.cps_mode && cps != P.cps_mode) continue;
+        const int tcols = 512 / cps;  // TMEM columns of one CTA
         if (P.sq_stream_mode == 1 && sqs == 0) continue;
         if (P.sq_stream_mode == 2 && sqs == 1) continue;
         if (cout % (32 * ns)) continue;  // whole 32-column store segments per op and group
@@ -113,9 +116,9 @@ std::vector<std::pair<double, FireParams>> fire_candidates(const FireParams& P, 
         // N < 64 expand MMAs cost as much as N = 64 ones (measured: inception-3a's
         // reduce -> 3x3 at 4 groups of 32 took 61 us against 42 us unfused)
         if (gch < std::min(64, cout)) continue;
-        if (gch > 256 || 2 * sq_cols + 2 * gch > 512) continue;  // two expand accumulators, at least one op each
+        if (gch > 256 || 2 * sq_cols + 2 * gch > tcols) continue;  // two expand accumulators, at least one op each
         // every op of an M tile in one job when two such accumulators fit TMEM, else one job per op
-        const int per_op = 2 * sq_cols + 2 * P.nops * gch > 512 ? 1 : 0;
+        const int per_op = 2 * sq_cols + 2 * P.nops * gch > tcols ? 1 : 0;
         std::vector<std::pair<int, int>> shapes;  // (G, R)
         for (int G = 1; G <= 8; ++G) shapes.push_back({G, P.H});
         for (int R = 1; R < P.H; ++R) shapes.push_back({1, R});
@@ -125,6 +128,7 @@ std::vector<std::pair<double, FireParams>> fire_candidates(const FireParams& P, 
             if (G > 1 && G > batch) continue;
             FireParams Q = P;
             Q.cb = cb;
+            Q.cps = cps;
             Q.kchunks = (Q.ksteps * 32 + cb - 1) / cb;
             Q.sq_stream = sqs;
             Q.nsplit = ns, Q.gch = gch, Q.G = G, Q.R = R, Q.bands = cdiv(P.H, R);
@@ -150,12 +154,13 @@ std::vector<std::pair<double, FireParams>> fire_candidates(const FireParams& P, 
             fire_layout(Q, nst, npl, stg);
             Q.sq_cols = sq_cols;
             Q.per_op = per_op;
-            Q.nexslots = std::min(kFireMaxExSlots, (512 - 2 * sq_cols) / ((per_op ? 1 : Q.nops) * gch));
+            Q.nexslots = std::min(kFireMaxExSlots, (tcols - 2 * sq_cols) / ((per_op ? 1 : Q.nops) * gch));
             // model (SM cycles)
             const int units = G > 1 ? cdiv(batch, G) : batch * Q.bands;
             const long long items = (long long)units * ns;
-            const int active = int(std::min<long long>(items, sms));
-            const double rounds = std::ceil(double(items) / sms);
+            const int active = int(std::min<long long>(items, (long long)sms * cps));
+            const double rounds = std::ceil(double(items) / (sms * cps));
+            const double share = cps == 2 && items > sms ? 2.0 : 1.0;  // two CTAs share an SM's tensor pipe and TMEM read ports
             const double mma_n = std::max(16.0, 0.53 * gch);
             const double sq_mma = double(Q.Ts) * Q.ksteps * std::max(16.0, 0.53 * Q.S);
             const double ex_mma = double(Q.Te) * taps * (Q.S / cpc / 2) * mma_n;
@@ -169,7 +174,7 @@ std::vector<std::pair<double, FireParams>> fire_candidates(const FireParams& P, 
             const double tmem = (double(Q.Ts) * P.S + double(Q.Te) * Q.nops * gch) * 128 * 4 / 64.0;
             // streamed squeeze weights: re-read from L2 per squeeze tile
             const double l2w = sqs ? double(Q.Ts) * Q.ksteps * P.S * 32 / (6000.0 / active) : 0.0;
-            const double unit = std::max({sq_mma + ex_mma, mem, l2 + l2w, tmem * 2.0}) + (npl == 2 ? 600.0 : 1500.0);
+            const double unit = std::max({(sq_mma + ex_mma) * share, mem, l2 + l2w, tmem * 2.0 * share}) + (npl == 2 ? 600.0 : 1500.0);
             out.push_back({rounds * unit, Q});
         }
     }
@@ -191,7 +196,7 @@ void fire_shape(const Graph& g, const StepSpec& s, int es, FireParams& P) {
     const TensorShape in = g.shape_of(s.inputs[0]);
     P.es = es, P.H = in.height, P.W = in.width, P.HW = in.height * in.width, P.Wp = in.width + 1;
     P.ksteps = sq.conv->in_channels * es / 32;
-    P.cb = 128;
+    P.cb = 128, P.cps = 1;
     P.kchunks = (P.ksteps + 3) / 4;
     P.S = sq.conv->out_channels;
     P.schunks = P.S * es / 16;
@@ -215,6 +220,7 @@ bool fire_feasible(const Graph& g, const StepSpec& s, int es, int batch, const K
     P.stage_mode = k.fire_stage;
     P.sq_stream_mode = k.fire_sqs;
     P.cb_mode = k.fire_cb;
+    P.cps_mode = k.fire_cps;
     return fire_choose(P, std::max(1, batch), 148, k.fire_nsplit, k.fire_g, k.fire_r, nullptr);
 }
 

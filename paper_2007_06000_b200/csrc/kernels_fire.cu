@@ -40,13 +40,20 @@ namespace {
 
 using namespace umma;
 
-constexpr int kEpi = 256;  // 8 epilogue warps: two per TMEM lane quadrant
-constexpr int kThreads = kEpi + 64;
-constexpr int kProd = kEpi / 32, kMma = kEpi / 32 + 1;
+// CTAs per SM (P.cps): 1 -- 8 epilogue warps (two per TMEM lane quadrant), all
+// 512 TMEM columns; 2 -- two independent unit pipelines per SM, each with 4
+// epilogue warps, 256 TMEM columns and half the shared memory.
 // Squeeze-input stages: 128 pixels x a K chunk of P.cb bytes (128: SWIZZLE_128B,
 // 4 K steps; 64: SWIZZLE_64B, 2 K steps -- narrow stages leave room for
 // larger resident expand weights).
-constexpr int kTmemCols = 512;
+template <int CPS>
+struct Cfg {
+    static constexpr int kEpi = CPS == 1 ? 256 : 128;
+    static constexpr int kThreads = kEpi + 64;
+    static constexpr int kProd = kEpi / 32, kMma = kEpi / 32 + 1;
+    static constexpr int kGroups = kEpi / 128;  // epilogue warps per TMEM lane quadrant
+    static constexpr int kTmemCols = 512 / CPS;
+};
 
 template <class T>
 struct FElem;
@@ -189,8 +196,10 @@ __device__ __forceinline__ float4 ld_shared_f4(uint32_t addr) {
     return v;
 }
 
-template <class T>
-__global__ void __launch_bounds__(kThreads, 1) fire_kernel(const __grid_constant__ FireParams P, int n0, int count) {
+template <class T, int CPS>
+__global__ void __launch_bounds__(Cfg<CPS>::kThreads, CPS) fire_kernel(const __grid_constant__ FireParams P, int n0, int count) {
+    constexpr int kEpi = Cfg<CPS>::kEpi, kProd = Cfg<CPS>::kProd, kMma = Cfg<CPS>::kMma, kTmemCols = Cfg<CPS>::kTmemCols;
+    constexpr int NGR = Cfg<CPS>::kGroups;
     extern __shared__ __align__(1024) uint8_t smem[];
     __shared__ __align__(8) uint64_t full[kFireStages], empty[kFireStages], sqf[2], sqe[2], exf[kFireMaxExSlots], exe[kFireMaxExSlots],
         plf[2], ple[2], wbar;
@@ -369,7 +378,8 @@ __global__ void __launch_bounds__(kThreads, 1) fire_kernel(const __grid_constant
         __syncwarp();
     } else {
         // ---------------------------------------------------------------- epilogue warps
-        const int t = threadIdx.x & 127, half = threadIdx.x >> 7;  // TMEM lane (M row); column chunks / segments of this warp: index % 2 == half
+        // TMEM lane (M row); column chunks / segments of this warp: index % NGR == half
+        const int t = threadIdx.x & 127, half = threadIdx.x >> 7;
         float* sqbias = reinterpret_cast<float*>(smem + P.sqbias_off);
         for (int c = threadIdx.x; c < P.S; c += kEpi) sqbias[c] = __ldg(P.sq_bias + c);
         for (int o = 0; o < P.nops; ++o) {
@@ -445,7 +455,7 @@ __global__ void __launch_bounds__(kThreads, 1) fire_kernel(const __grid_constant
                         const int rw = fdiv(rem, P.W, iW), c = rem - rw * P.W;
                         cell = (n * Rp + (rw - Us.r0 + 1)) * P.Wp + c + 1;
                     }
-                    for (int c0 = 32 * half; c0 < P.S; c0 += 64) {  // 32-column chunks of the squeeze, alternating between warp groups
+                    for (int c0 = 32 * half; c0 < P.S; c0 += 32 * NGR) {  // 32-column chunks of the squeeze, alternating between warp groups
                         const int nc = min(32, P.S - c0);
                         float v[32];
                         if (nc == 32) tmem_ld32(tmem + tl + uint32_t(a * P.sq_cols + c0), v);
@@ -504,17 +514,17 @@ __global__ void __launch_bounds__(kThreads, 1) fire_kernel(const __grid_constant
                         const int nch = JW / 32;
                         const uint32_t tj = tmem + tl + exc0 + uint32_t(a * JW);
                         const bool st32 = P.st32 != 0;
-                        for (int cb = half; cb < nch; cb += 4) {
-                            const bool two = cb + 2 < nch;
+                        for (int cb = half; cb < nch; cb += 2 * NGR) {
+                            const bool two = cb + NGR < nch;
                             uint32_t r0[32], r1[32];
                             tmem_ld32_issue(tj + uint32_t(cb * 32), r0);
-                            if (two) tmem_ld32_issue(tj + uint32_t((cb + 2) * 32), r1);
+                            if (two) tmem_ld32_issue(tj + uint32_t((cb + NGR) * 32), r1);
                             tmem_ld_wait32(r0);
                             if (two) tmem_ld_wait32(r1);
 #pragma unroll
                             for (int u = 0; u < 2; ++u) {
                                 if (u == 1 && !two) break;
-                                int o = nj > 1 ? o0 : 0, c0 = (cb + 2 * u) * 32;
+                                int o = nj > 1 ? o0 : 0, c0 = (cb + NGR * u) * 32;
                                 while (c0 >= P.gch) c0 -= P.gch, ++o;
                                 const FireOp& op = P.op[o];
                                 const uint32_t bsm = smem_u32(smem + op.bias_off) + uint32_t(c0) * 4u;
@@ -559,7 +569,7 @@ __global__ void __launch_bounds__(kThreads, 1) fire_kernel(const __grid_constant
                             const uint32_t bsm = smem_u32(smem + op.bias_off);
                             const int ocol = nj > 1 ? 0 : o;  // the op's column block inside the job
                             T* dsto = valid ? static_cast<T*>(op.out) + pix * op.out_cstride + op.out_coff + g * P.gch : nullptr;
-                            for (int k = (half + o * spo) & 1; k < spo; k += 2) {  // segments of the op whose global index has this parity
+                            for (int k = NGR == 1 ? 0 : (half + o * spo) & 1; k < spo; k += NGR) {  // segments of the op whose global index has this parity
                                 const int c0 = k * SEG;
                                 for (int h = 0; h < SEG; h += 32) {
                                     float v[32];
@@ -612,11 +622,11 @@ __global__ void __launch_bounds__(kThreads, 1) fire_kernel(const __grid_constant
     if (warp == kMma) tmem_free(tmem, uint32_t(kTmemCols));
 }
 
-template <class T>
+template <class T, int CPS>
 cudaError_t launch_t(const FireParams& P, int n0, int count, cudaStream_t st) {
     static bool init = false;
     if (!init) {
-        cudaError_t e = cudaFuncSetAttribute(fire_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, kFireSmemMax);
+        cudaError_t e = cudaFuncSetAttribute(fire_kernel<T, CPS>, cudaFuncAttributeMaxDynamicSharedMemorySize, kFireSmemMax);
         if (e != cudaSuccess) return e;
         init = true;
     }
@@ -624,22 +634,23 @@ cudaError_t launch_t(const FireParams& P, int n0, int count, cudaStream_t st) {
     int sms = 148, dev = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    const int gx = std::max(1, std::min(units, sms / std::max(1, P.nsplit)));
+    const int gx = std::max(1, std::min(units, CPS * sms / std::max(1, P.nsplit)));
     cudaLaunchConfig_t cfg{};
-    cfg.gridDim = dim3(unsigned(gx), unsigned(std::max(1, P.nsplit)), 1u), cfg.blockDim = dim3(kThreads);
+    cfg.gridDim = dim3(unsigned(gx), unsigned(std::max(1, P.nsplit)), 1u), cfg.blockDim = dim3(Cfg<CPS>::kThreads);
     cfg.dynamicSmemBytes = size_t(P.smem_bytes), cfg.stream = st;
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     attr[0].val.programmaticStreamSerializationAllowed = P.pdl ? 1 : 0;
     cfg.attrs = attr, cfg.numAttrs = 1;
-    cudaLaunchKernelEx(&cfg, fire_kernel<T>, P, n0, count);
+    cudaLaunchKernelEx(&cfg, fire_kernel<T, CPS>, P, n0, count);
     return cudaGetLastError();
 }
 
 }  // namespace
 
 cudaError_t launch_fire(const FireParams& P, int n0, int count, cudaStream_t st) {
-    return P.es == 4 ? launch_t<float>(P, n0, count, st) : launch_t<__nv_bfloat16>(P, n0, count, st);
+    if (P.cps == 2) return P.es == 4 ? launch_t<float, 2>(P, n0, count, st) : launch_t<__nv_bfloat16, 2>(P, n0, count, st);
+    return P.es == 4 ? launch_t<float, 1>(P, n0, count, st) : launch_t<__nv_bfloat16, 1>(P, n0, count, st);
 }
 
 }  // namespace xlf

@@ -73,9 +73,13 @@ def test_fire_unit_shapes_are_bitwise_identical(prec):
     for opts in ["fire_nsplit=1,fire_g=1,fire_r=55", "fire_nsplit=1,fire_r=8", "fire_nsplit=2,fire_r=4", "fire_nsplit=2,fire_g=2",
                  "fire_nsplit=2,fire_g=3", "fire_nsplit=4,fire_g=1", "fire_nsplit=4,fire_r=7", "",
                  # 64-byte squeeze-input chunks (SWIZZLE_64B stages): same K order, same bits
-                 "fire_cb=64,fire_nsplit=1,fire_r=8", "fire_cb=64,fire_nsplit=2,fire_g=2", "fire_cb=64,fire_sqs=1", "fire_cb=64"]:
+                 "fire_cb=64,fire_nsplit=1,fire_r=8", "fire_cb=64,fire_nsplit=2,fire_g=2", "fire_cb=64,fire_sqs=1", "fire_cb=64",
+                 # two CTAs per SM (4 epilogue warps, 256 TMEM columns each)
+                 "fire_cps=2", "fire_cps=2,fire_nsplit=1,fire_r=4", "fire_cps=2,fire_nsplit=2,fire_g=2", "fire_cps=2,fire_stage=1"]:
         e, _, _ = _engine("squeezenet11", prec, batch, opts)
         cb = "64" if "fire_cb=64" in opts else "any"
+        cb += ",cps2" if "fire_cps=2" in opts else ""
+        cb += ",staged" if "fire_stage=1" in opts else ""
         shapes = (cb,) + tuple((s["id"], s["tile"][0], s["nsplit"]) for s in e.steps if s["tag"] == "fire")
         if not shapes or shapes in seen:
             continue
@@ -92,7 +96,7 @@ def test_fire_unit_shapes_are_bitwise_identical(prec):
             earlier = [f for f in FIRES[:FIRES.index(n)]]
             if all(f in fired and f in base_fired for f in earlier):
                 assert np.array_equal(out[n], base[n]), (opts, n)
-    assert len(seen) >= (6 if prec == "bf16" else 5)
+    assert len(seen) >= (9 if prec == "bf16" else 8)
 
 
 @pytest.mark.parametrize("name,batch,prec", [("fire", 32, "bf16"), ("fire", 32, "tf32"), ("b1", 3, "bf16"), ("b1", 3, "tf32")])
