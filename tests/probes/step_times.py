@@ -1,6 +1,6 @@
 """Per-step device time of a tuned bf16 engine (CUDA events around each step).
 
-    python tests/probes/step_times.py inc3a 64 b200
+    python tests/probes/step_times.py inc3a 64 b200 [precision]
 """
 import os
 import sys
@@ -14,11 +14,13 @@ import paper_2007_06000_b200 as X  # noqa: E402
 
 def main():
     name, batch, part = sys.argv[1], int(sys.argv[2]), sys.argv[3]
+    prec = sys.argv[4] if len(sys.argv) > 4 else "bf16"
     g = X.load_graph(X.graph_path(name))
-    e = X.Engine(g, X.seeded_weights(g, 42), part, "bf16", max_batch=batch)
+    e = X.Engine(g, X.seeded_weights(g, 42), part, prec, max_batch=batch)
     e.set_input_seeded(42, batch)
     e.forward(batch, use_graph=False)
-    e.autotune(batch, reps=3, topk=3)
+    if prec in ("bf16", "tf32"):
+        e.autotune(batch, reps=3, topk=3)
     n = len(e.steps)
     st = torch.cuda.current_stream()
     for _ in range(3):
