@@ -217,12 +217,12 @@ def run_reference_arm(args, rank, world):
 # ----------------------------------------------------------------------------- our arm
 
 def make_engine(X, g, w, part, prec, B, device, tune=True, first_image=0):
-    """Engine + seeded device inputs; tensor-core plans measured-time tuned
-    (part of the product, before any timed region)."""
+    """Engine + seeded device inputs; plans measured-time tuned (tensor-core
+    and fp32 SIMT steps; part of the product, before any timed region)."""
     e = X.Engine(g, w, part, prec, max_batch=B, device=device)
     e.set_input_seeded(42, B, first_image=first_image)
     info = None
-    if prec in TC and tune:
+    if tune:
         t0 = time.time()
         e.forward(B, use_graph=False)
         chosen = e.autotune(B, reps=3, topk=3)

@@ -255,7 +255,7 @@ class Engine:
         return out
 
     def autotune(self, batch: int = 0, reps: int = 3, topk: int = 4) -> list:
-        """Measured-time tuning of the tensor-core (bf16 / TF32) fused steps (xlf_engine_autotune):
+        """Measured-time tuning of the fused steps (bf16 / TF32 tensor-core, fp32 SIMT tiles; xlf_engine_autotune):
         returns the chosen configuration of every tuned step."""
         check(lib().xlf_engine_autotune(self._h, batch, reps, topk))
         self.info = json.loads(text_call(lib().xlf_engine_json, self._h))

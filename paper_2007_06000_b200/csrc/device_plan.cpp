@@ -200,6 +200,56 @@ StepSpec step_for_block(const Graph& g, const FusionBlock& b) {
     return s;
 }
 
+// Cells of slack after a staged region / buffer that a kxk (k > 1) conv
+// reads: the register-blocked conv computes whole CX-cell row windows, so the
+// last row's window reads up to (CX-1)*S + kw-1 <= 9 cells past the region
+// (values discarded, never stored).  1x1 convs clamp instead (conv_rb).
+constexpr int kSlackCells = 10;
+
+// Per-thread instructions of one register-blocked conv unit (kernels_fp32.cu
+// conv_rb): per (ic, kh) the row window loads, OCV/4 weight loads per tap and
+// CX*OCV FMAs per tap; 1x1: per 4 channels CX 16-byte loads, OCV weight loads
+// and 4*CX*OCV FMAs.
+double rb_unit_instr(const FOp& o, int cx, int ocv) {
+    if (o.kw == 1) return (o.cin / 4.0) * (cx + ocv + 4.0 * cx * ocv);
+    const int win = (cx - 1) * o.stride + o.kw;
+    return double(o.cin) * o.kh * (win + o.kw * ocv / 4.0 + double(o.kw) * cx * ocv);
+}
+
+// Threads of one register-blocked conv op per tile (conv_rb's lane mapping:
+// channel groups padded to a multiple of min(8, groups)).
+double rb_units(const FOp& o, int cx, int ocv) {
+    const int QV = o.cout_pad / ocv, B = std::min(8, QV);
+    return double(o.ext_h) * ((o.ext_w + cx - 1) / cx) * double((QV + B - 1) / B * B);
+}
+
+// Register-blocked variant of a conv op: the (cx, ocv) instantiation that
+// minimises one CTA's serial work for the op (rounds of 256 threads x
+// per-thread instructions), the larger block on ties; cx = 0 keeps the
+// generic cell-quad path (grouped convs, widths / strides not instantiated).
+void rb_variant(FOp& o) {
+    o.cx = o.ocv = 0;
+    if (o.kind != OP_CONV || o.group != 1) return;
+    const bool inst = (o.kw == 1 && o.stride == 1) || (o.kw == 3 && o.kh == 3 && o.stride <= 2) || (o.kw == 5 && o.stride == 1);
+    if (!inst) return;
+    static const int kVariants[4][2] = {{8, 8}, {4, 8}, {4, 4}, {2, 4}};
+    // Variants that give every thread of the CTA a unit: fewest warp
+    // instructions (the largest block that fits); otherwise (small tiles) the
+    // one with the shortest serial chain.
+    double best_full = 1e300, best_lat = 1e300;
+    int full[2] = {0, 0}, lat[2] = {0, 0};
+    for (const auto& v : kVariants) {
+        if (o.cout_pad % v[1] || (v[0] == 8 && (o.stride != 1 || o.kw > 3))) continue;  // instantiated set (conv_rb_v)
+        const double units = rb_units(o, v[0], v[1]);
+        const double per = rb_unit_instr(o, v[0], v[1]);
+        const double wi = std::ceil(units / 32.0) * per, l = std::ceil(units / 256.0) * per;
+        if (units >= 256 && wi < best_full * 0.999) best_full = wi, full[0] = v[0], full[1] = v[1];
+        if (l < best_lat * 0.999) best_lat = l, lat[0] = v[0], lat[1] = v[1];
+    }
+    const int* pick = full[0] ? full : lat;
+    o.cx = pick[0], o.ocv = pick[1];
+}
+
 struct OpGeom {
     int ext_h, ext_w, org_mul, org_sub, d;
 };
@@ -280,7 +330,13 @@ long long layout_step(const Graph& g, const StepSpec& s, int th, int tw, FusedPa
         in.org_mul = scale < 0 ? 1 : scale, in.org_sub = XL;
         in.ext_h = eh, in.ext_w = ew, in.cpitch = smem_pitch(in.c);
         in.smem_off = int(floats);
-        floats += (long long)eh * ew * in.cpitch;
+        bool window_reader = false;
+        for (int i = 0; i < nops; ++i) {
+            const OpSpec& op = s.ops[size_t(i)];
+            const Layer& l = *g.find_layer(op.layer);
+            window_reader |= op.stage == 1 && op.xin == int(xi) && l.kind == LayerKind::conv && l.conv->kernel_w > 1;
+        }
+        floats += (long long)(eh * ew + (window_reader ? kSlackCells : 0)) * in.cpitch;
     }
     std::vector<FBuf> bufs(static_cast<size_t>(nbufs));
     for (int i = 0; i < nops; ++i) {
@@ -290,7 +346,13 @@ long long layout_step(const Graph& g, const StepSpec& s, int th, int tw, FusedPa
         b.channels = os.channels, b.cpitch = smem_pitch(os.channels);
         b.ext_h = geo[size_t(i)].ext_h, b.ext_w = geo[size_t(i)].ext_w;
         b.smem_off = int(floats);
-        floats += (long long)b.ext_h * b.ext_w * b.cpitch;
+        bool window_reader = false;
+        for (const OpSpec& c : s.ops) {
+            const Layer& l = *g.find_layer(c.layer);
+            window_reader |= c.stage == 2 && std::find(c.srcs.begin(), c.srcs.end(), i) != c.srcs.end() && l.kind == LayerKind::conv &&
+                             l.conv->kernel_w > 1;
+        }
+        floats += (long long)(b.ext_h * b.ext_w + (window_reader ? kSlackCells : 0)) * b.cpitch;
     }
     if (fp) {
         *fp = FusedParams{};
@@ -333,19 +395,55 @@ long long layout_step(const Graph& g, const StepSpec& s, int th, int tw, FusedPa
             o.d = geo[size_t(i)].d;
             o.ext_h = geo[size_t(i)].ext_h, o.ext_w = geo[size_t(i)].ext_w;
             o.org_mul = geo[size_t(i)].org_mul, o.org_sub = geo[size_t(i)].org_sub;
+            if (s.rb) rb_variant(o);
         }
     }
     return floats * 4;
 }
 
-double macs_per_output(const Layer& l) {
-    if (l.kind == LayerKind::conv) return double(l.conv->macs_per_output());
-    if (l.kind == LayerKind::pool) return double(l.pool->kernel) * l.pool->kernel;
-    return 1.0;
+// Modelled SM cycles of one fp32 step at a tile: per CTA, the serial
+// per-thread instruction count (rounds of 256 threads over each op's units,
+// input staging) and the warp instructions it issues; the busiest SM runs
+// ceil(CTAs / 148) CTAs, `occ` at a time, issuing <= 4 warp instructions per
+// cycle.  Halo recompute and partial tiles / row windows show up as units.
+double fp32_tile_cycles(const FusedParams& fp, int batch, long long smem) {
+    double lat = 0, wi = 0;
+    auto add = [&](double units, double per) {
+        lat += std::ceil(units / 256.0) * per;
+        wi += std::ceil(units / 32.0) * per;
+    };
+    for (int i = 0; i < fp.nins; ++i) add(double(fp.in[i].ext_h) * fp.in[i].ext_w * fp.in[i].c / 4.0, 6.0);
+    for (int i = 0; i < fp.nops; ++i) {
+        const FOp& o = fp.ops[i];
+        const double cells = double(o.ext_h) * o.ext_w, Q = o.cout_pad / 4;
+        if (o.kind == OP_CONV && o.cx)
+            add(rb_units(o, o.cx, o.ocv), rb_unit_instr(o, o.cx, o.ocv) * 1.3);
+        else if (o.kind == OP_CONV) {
+            const int PX = cells * Q >= 8 * 256 && o.group == 1 ? 8 : 4;
+            add(std::ceil(cells / PX) * Q, double(o.cin / o.group) * o.kh * o.kw * (1 + PX + 4 * PX) * 1.3);
+        } else
+            add(cells * Q, 3.0 * o.kh * o.kw + 8);
+    }
+    // Weights stream from L2 through L1 (~64 B/cycle per SM); past what L1
+    // keeps beside the CTAs' shared memory, every round of units re-reads them.
+    const int occ = std::max(1, std::min(2, int((228 * 1024) / (smem + 1024))));  // <= 2 CTAs: registers
+    const double l1_keep = std::max(16.0 * 1024, (256.0 * 1024 - double(occ) * smem) / occ / 2);
+    double l2 = 0;
+    for (int i = 0; i < fp.nops; ++i) {
+        const FOp& o = fp.ops[i];
+        if (o.kind != OP_CONV) continue;
+        const double wb = double(o.cin / o.group) * o.kh * o.kw * o.cout_pad * 4;
+        const double units = o.cx ? rb_units(o, o.cx, o.ocv)
+                                  : double(o.ext_h) * o.ext_w * o.cout_pad / 16;
+        l2 += wb > l1_keep ? wb * std::ceil(units / 256.0) : wb;
+    }
+    const double ctas = double(fp.grid_h) * fp.grid_w * fp.cgroups * std::max(batch, 1);
+    const double per_sm = std::ceil(ctas / 148.0);
+    const double conc = std::min(double(occ), per_sm);
+    return std::max({per_sm * wi / 3.0, per_sm * l2 / 64.0, std::ceil(per_sm / conc) * (lat + 1500.0)}) + 300.0 * per_sm;
 }
 
-// Tile choice: minimise modelled time = waves x per-CTA work / occupancy
-// benefit, with per-CTA work including halo recompute and partial-tile waste.
+// Tile choice: minimise the modelled SM cycles (fp32_tile_cycles).
 bool choose_tile_at(const Graph& g, StepSpec& s, int batch_hint, int smem_budget, const Knobs& k);
 
 // Pool-only steps whose full-channel region never fits shared memory (a
@@ -378,27 +476,9 @@ bool choose_tile_at(const Graph& g, StepSpec& s, int batch_hint, int smem_budget
             FusedParams fp;
             const long long sm = layout_step(g, s, th, tw, &fp);
             if (sm < 0 || sm > smem_budget) continue;
-            double work = 0;
-            for (int i = 0; i < fp.nops; ++i) {
-                const FOp& o = fp.ops[i];
-                work += double(o.ext_h) * o.ext_w * o.cout_pad * macs_per_output(*g.find_layer(s.ops[size_t(i)].layer));
-            }
-            for (int i = 0; i < fp.nins; ++i) work += double(fp.in[i].ext_h) * fp.in[i].ext_w * fp.in[i].c;
-            // Weight traffic: every 8-cell block of a unit re-reads its weights
-            // through L1; past ~64 KB they come from L2 each time (conv10: 2 MB).
-            for (int i = 0; i < fp.nops; ++i) {
-                const FOp& o = fp.ops[i];
-                if (o.kind != OP_CONV) continue;
-                const double wb = double(o.cin / o.group) * o.kh * o.kw * o.cout_pad * 4;
-                const double blocks = std::ceil(double(o.ext_h) * o.ext_w / 8.0);
-                work += 0.5 * (wb > 64 * 1024 ? wb * blocks : wb);
-            }
-            const double ctas = double(fp.grid_h) * fp.grid_w * fp.cgroups * std::max(batch_hint, 1);
-            const int occ = std::max(1, std::min(8, int((228 * 1024) / (sm + 1024))));
-            const double waves = std::ceil(ctas / (148.0 * occ));
-            double t = waves * work * occ / std::min(double(occ), 2.0) + 2000.0 * waves;
-            if (forced) t = -double(th) * tw;  // the plan's tile, else its largest feasible sub-tile
-            if (t < best * 0.999 || (t <= best * 1.001 && long(th) * tw > long(bh) * bw)) best = t, bh = th, bw = tw, bsm = int(sm);
+            const double t = fp32_tile_cycles(fp, batch_hint, sm);
+            const double key = forced ? -double(th) * tw : t;  // the plan's tile, else its largest feasible sub-tile
+            if (key < best * 0.999 || (key <= best * 1.001 && long(th) * tw > long(bh) * bw)) best = key, bh = th, bw = tw, bsm = int(sm);
         }
     if (!bh) return false;
     s.tile_h = bh, s.tile_w = bw, s.smem_bytes = bsm;
@@ -406,6 +486,25 @@ bool choose_tile_at(const Graph& g, StepSpec& s, int batch_hint, int smem_budget
 }
 
 }  // namespace
+
+std::vector<F32Candidate> candidates_fp32(const Graph& g, const StepSpec& s, int batch_hint, int smem_budget) {
+    std::vector<F32Candidate> out;
+    StepSpec t = s;
+    for (int rb = 0; rb < 2; ++rb) {
+        t.rb = rb;
+        for (int th = 1; th <= std::min(s.out_h, 32); ++th)
+            for (int tw = 1; tw <= std::min(s.out_w, 32); ++tw) {
+                FusedParams fp;
+                const long long sm = layout_step(g, t, th, tw, &fp);
+                if (sm < 0 || sm > smem_budget) continue;
+                out.push_back({th, tw, rb, int(sm), fp32_tile_cycles(fp, batch_hint, sm)});
+            }
+    }
+    std::stable_sort(out.begin(), out.end(), [](const F32Candidate& a, const F32Candidate& b) { return a.model < b.model; });
+    return out;
+}
+
+long long fp32_layout_bytes(const Graph& g, const StepSpec& s, int th, int tw) { return layout_step(g, s, th, tw, nullptr); }
 
 // Algorithmic traffic / work of a step: block inputs once +
 // stored outputs once per image (bytes_algorithmic), weights + biases once
@@ -830,7 +929,7 @@ std::string describe_plan_json(const Graph& g, const DevicePlan& plan) {
         static const char* kinds[] = {"fused", "concat_copy", "add", "relu"};
         os << (i ? "," : "") << "{\"id\":" << q(s.id) << ",\"kind\":" << q(kinds[s.kind]) << ",\"tag\":" << q(s.tag)
            << ",\"mode\":" << q(to_string(s.mode)) << ",\"tile\":[" << s.tile_h << "," << s.tile_w
-           << "],\"out\":[" << s.out_h << "," << s.out_w << "],\"smem_bytes\":" << s.smem_bytes << ",\"nxb\":" << s.nxb << ",\"wres\":" << s.wres << ",\"ring_slots\":" << s.ring_slots << ",\"grid_all\":" << s.grid_all << ",\"epi_warps\":" << s.epi_warps << ",\"tsets\":" << s.tsets << ",\"nsplit\":" << s.nsplit << ",\"macs\":" << s.macs
+           << "],\"out\":[" << s.out_h << "," << s.out_w << "],\"smem_bytes\":" << s.smem_bytes << ",\"nxb\":" << s.nxb << ",\"wres\":" << s.wres << ",\"ring_slots\":" << s.ring_slots << ",\"grid_all\":" << s.grid_all << ",\"epi_warps\":" << s.epi_warps << ",\"tsets\":" << s.tsets << ",\"nsplit\":" << s.nsplit << ",\"rb\":" << s.rb << ",\"macs\":" << s.macs
            << ",\"macs_executed\":" << s.macs_executed << ",\"bytes_algorithmic\":" << s.bytes_algorithmic
            << ",\"weight_bytes\":" << s.weight_bytes << ",\"ring_chunk\":" << s.ring_chunk << ",\"inputs\":[";
         for (size_t k = 0; k < s.inputs.size(); ++k) os << (k ? "," : "") << q(s.inputs[k]);

@@ -103,6 +103,7 @@ struct StepSpec {
     int tsets = 1;      // TMEM accumulator sets (2 = cross-tile MMA/epilogue overlap)
     int ring_chunk = 16384;  // bytes per weight-ring slot
     int nsplit = 1;     // output-channel groups over the grid's y dimension (weights of a group resident per CTA)
+    int rb = 1;         // fp32: register-blocked conv variants allowed (0 = the generic cell-quad path)
     // tensor-core conv + global average pool (SqueezeNet conv10 -> pool10): the
     // step's single conv op never stores its output; its epilogue reduces
     // every tile over its cells and the pooled layer `gap_out` (1x1) is
@@ -158,6 +159,16 @@ struct BCandidate {
     double model;
     int nsplit;
 };
+// fp32 SIMT steps: every feasible (tile, register-blocked on/off) ranked by
+// the SM-cycle model (fp32_tile_cycles), best first; the measured-time tuner
+// times the best of each mode.
+struct F32Candidate {
+    int th, tw, rb, smem;
+    double model;
+};
+std::vector<F32Candidate> candidates_fp32(const Graph& g, const StepSpec& s, int batch_hint, int smem_budget);
+// Shared bytes of an fp32 step at a tile (-1 = infeasible); the step's `rb` applies.
+long long fp32_layout_bytes(const Graph& g, const StepSpec& s, int th, int tw);
 std::vector<BCandidate> candidates_tc(const Graph& g, const StepSpec& s, int batch_hint, int smem_budget, int es, const Knobs& k);
 void apply_candidate(StepSpec& s, const BCandidate& c);
 std::vector<uint8_t> pack_weights_tc(const Graph& g, const float* flat, size_t count, std::map<std::string, long long>& off, int es);

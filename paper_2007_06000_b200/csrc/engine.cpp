@@ -10,6 +10,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <sstream>
+#include <set>
 #include <tuple>
 
 #include "tc_params.hpp"
@@ -642,8 +643,66 @@ std::unique_ptr<BParams> Engine::build_bparams(const StepSpec& s) {
 // events (`reps` launches after one warm-up, on the engine's own tensors) and
 // the fastest is kept.  Arithmetic does not depend on the configuration, so
 // results stay within the bf16 tolerance whatever is chosen.
+// fp32 SIMT steps: the model's best `topk` tiles with and without the
+// register-blocked convs, plus the largest feasible tile of each and the
+// planner's choice, timed on the device; the fastest is kept.  Every choice
+// computes the same per-element arithmetic (fixed accumulation order), so
+// fp32_exact stays bit-identical to the oracle whatever is picked.
+std::string Engine::autotune_fp32(int batch, int reps, int topk, cudaStream_t st, cudaEvent_t e0, cudaEvent_t e1) {
+    std::ostringstream js;
+    bool first = true;
+    const bool exact = prec_ == Precision::fp32_exact;
+    for (size_t i = 0; i < plan_.steps.size(); ++i) {
+        StepSpec& s = plan_.steps[i];
+        if (s.kind != StepSpec::FUSED || dws_[i]) continue;
+        const std::vector<F32Candidate> all = candidates_fp32(g_, s, batch, 227 * 1024);
+        std::vector<F32Candidate> cands = {{s.tile_h, s.tile_w, s.rb, s.smem_bytes, 0.0}};
+        int per_mode[2] = {0, 0};
+        const F32Candidate* biggest[2] = {nullptr, nullptr};
+        for (const F32Candidate& c : all) {  // the SIMT model is coarse: time >= 8 per mode
+            if (per_mode[c.rb]++ < std::max(8, 2 * topk)) cands.push_back(c);
+            if (!biggest[c.rb] || c.th * c.tw > biggest[c.rb]->th * biggest[c.rb]->tw) biggest[c.rb] = &c;
+        }
+        for (const F32Candidate* c : biggest)
+            if (c) cands.push_back(*c);
+        float best_ms = 1e30f;
+        StepSpec best = s;
+        FusedParams bestP{};
+        int tried = 0;
+        std::set<std::array<int, 3>> seen;
+        for (const F32Candidate& c : cands) {
+            if (!seen.insert({c.th, c.tw, c.rb}).second) continue;
+            StepSpec t = s;
+            t.tile_h = c.th, t.tile_w = c.tw, t.rb = c.rb;
+            const long long sm = fp32_layout_bytes(g_, t, c.th, c.tw);
+            if (sm < 0 || sm > 227 * 1024) continue;
+            t.smem_bytes = int(sm);
+            const FusedParams P = make_params(g_, plan_, t, allocs_, weights_);
+            cuda_check(launch_fused_fp32(P, batch, exact, st), "autotune warm-up");
+            cuda_check(cudaEventRecord(e0, st), "cudaEventRecord");
+            for (int r = 0; r < reps; ++r) cuda_check(launch_fused_fp32(P, batch, exact, st), "autotune launch");
+            cuda_check(cudaEventRecord(e1, st), "cudaEventRecord");
+            cuda_check(cudaEventSynchronize(e1), "cudaEventSynchronize");
+            float ms = 0;
+            cuda_check(cudaEventElapsedTime(&ms, e0, e1), "cudaEventElapsedTime");
+            ms /= float(reps);
+            ++tried;
+            if (knobs_.tune_verbose)
+                std::fprintf(stderr, "[xlf] tune %s (fp32): tile %dx%d rb %d smem %d: %.1f us (model %.0f)\n", s.id.c_str(), c.th, c.tw, c.rb,
+                             int(sm), ms * 1000.0f, c.model);
+            if (ms < best_ms) best_ms = ms, best = t, bestP = P;
+        }
+        if (!tried) continue;
+        s = best;
+        params_[i] = bestP;
+        js << (first ? "" : ",") << "{\"id\":\"" << s.id << "\",\"kernel\":\"fp32\",\"tried\":" << tried << ",\"us\":" << best_ms * 1000.0f
+           << ",\"tile\":[" << s.tile_h << "," << s.tile_w << "],\"rb\":" << s.rb << ",\"smem_bytes\":" << s.smem_bytes << "}";
+        first = false;
+    }
+    return js.str();
+}
+
 std::string Engine::autotune(int batch, int reps, int topk) {
-    if (!tc_es_) return "[]";
     if (batch <= 0 || batch > max_batch_) batch = max_batch_;
     reps = std::max(1, reps), topk = std::max(1, topk);
     cuda_check(cudaSetDevice(device_), "cudaSetDevice");
@@ -657,6 +716,7 @@ std::string Engine::autotune(int batch, int reps, int topk) {
     std::ostringstream js;
     js << "[";
     bool first = true;
+    if (!tc_es_) js << autotune_fp32(batch, std::max(1, reps), std::max(1, topk), st, e0, e1);
     // fire steps: the model's best configurations of every channel split (and
     // the current one) timed on the device; the fastest is kept
     for (size_t i = 0; i < plan_.steps.size(); ++i) {
@@ -796,7 +856,6 @@ std::string Engine::autotune(int batch, int reps, int topk) {
 // entries are parsed and validated before anything changes: a bad report
 // leaves the engine as it was.
 void Engine::apply_tuning(const std::string& js) {
-    if (!tc_es_) return;
     // value position of "key" (after the colon; whitespace tolerated), or npos
     auto at = [](const std::string& obj, const std::string& key) -> size_t {
         const size_t k = obj.find("\"" + key + "\"");
@@ -833,6 +892,22 @@ void Engine::apply_tuning(const std::string& js) {
             if (ns < 1 || G < 1 || R < 1) fail(ErrorKind::infeasible, "tuning report: configuration of step '" + id + "' is not feasible for this plan");
             if ((cb != 0 && cb != 64 && cb != 128) || cps < 0 || cps > 2) fail(ErrorKind::infeasible, "tuning report: configuration of step '" + id + "' is not feasible for this plan");
             fire_todo.push_back({i, {ns, G, R, sqs, cb, cps}});
+            continue;
+        }
+        if (!tc_es_) {  // fp32 SIMT step: tile and register-blocked convs on / off
+            if (i == plan_.steps.size() || plan_.steps[i].kind != StepSpec::FUSED || dws_[i])
+                fail(ErrorKind::validation, "tuning report: no fp32 fused step '" + id + "'");
+            StepSpec t = plan_.steps[i];
+            const size_t tv = at(obj, "tile");
+            const size_t tb = tv == std::string::npos ? tv : obj.find('[', tv);
+            const size_t tc = tb == std::string::npos ? tb : obj.find(',', tb);
+            if (tc == std::string::npos) fail(ErrorKind::parse, "tuning report: step '" + id + "' without \"tile\": [h, w]");
+            t.tile_h = std::atoi(obj.c_str() + tb + 1), t.tile_w = std::atoi(obj.c_str() + tc + 1);
+            num(obj, "rb", t.rb);
+            const long long sm = t.tile_h < 1 || t.tile_w < 1 || (t.rb != 0 && t.rb != 1) ? -1 : fp32_layout_bytes(g_, t, t.tile_h, t.tile_w);
+            if (sm < 0 || sm > 227 * 1024) fail(ErrorKind::infeasible, "tuning report: configuration of step '" + id + "' is not feasible for this plan");
+            t.smem_bytes = int(sm);
+            todo.emplace_back(i, t);
             continue;
         }
         if (i == plan_.steps.size() || !bparams_[i]) fail(ErrorKind::validation, "tuning report: no tensor-core fused step '" + id + "'");
@@ -872,6 +947,13 @@ void Engine::apply_tuning(const std::string& js) {
         t.nsplit = fires_[i]->nsplit;
         t.tile_h = fires_[i]->G > 1 ? fires_[i]->G * fires_[i]->H : fires_[i]->R;
         t.smem_bytes = fires_[i]->smem_bytes;
+    }
+    if (!tc_es_) {
+        for (auto& [i, t] : todo) {
+            plan_.steps[i] = t;
+            params_[i] = make_params(g_, plan_, t, allocs_, weights_);
+        }
+        return;
     }
     std::vector<std::unique_ptr<BParams>> built;
     for (auto& [i, t] : todo) built.push_back(build_bparams(t));

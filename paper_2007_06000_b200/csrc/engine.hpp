@@ -67,9 +67,10 @@ public:
     // option trace=1 only: per-CTA phase stamps of step `index` (tensor-core kernels).
     std::vector<unsigned long long> trace(int index) const;
     std::string describe_json() const;
-    // Measured-time tuning of the tensor-core fused steps (see engine.cpp); returns
+    // Measured-time tuning of the fused steps (tensor-core and fp32 SIMT, see engine.cpp); returns
     // the chosen configurations as JSON.
     std::string autotune(int batch, int reps, int topk);
+    std::string autotune_fp32(int batch, int reps, int topk, cudaStream_t st, cudaEvent_t e0, cudaEvent_t e1);
     // Applies a report autotune returned (no measurement).
     void apply_tuning(const std::string& json);
     int max_batch() const { return max_batch_; }

@@ -45,6 +45,11 @@ struct FOp {
     float* out;       // NHWC destination base (image 0, channel 0 of the destination tensor)
     int out_cstride;  // channels per pixel of the destination allocation
     int out_coff;     // channel offset inside it
+    // Register-blocked conv (kernels_fp32.cu conv_rb): a thread computes cx
+    // consecutive cells of one row x ocv output channels.  0 = the generic
+    // cell-quad path (grouped convs, kernel widths / strides without an
+    // instantiation).  Chosen by the planner (device_plan.cpp rb_variant).
+    int cx, ocv;
 };
 
 struct FBuf {

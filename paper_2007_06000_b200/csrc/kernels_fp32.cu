@@ -158,6 +158,140 @@ __device__ void conv_op(const FusedParams& P, const FOp& op, float* smem, const 
     }
 }
 
+// Register-blocked conv (group 1, kernel width KW, stride S): a thread owns
+// CX consecutive cells of one row x OCV output channels (CX*OCV accumulators).
+// For every (ic, kh) it loads the (CX-1)*S+KW input values of its row window
+// once (shared memory, broadcast across the lanes of one window) and reuses
+// each for up to KW taps x OCV channels; weights come as OCV/4 float4 loads
+// per tap through L1 ([ic][kh][kw][cout_pad]; thread q owns the channel
+// quads q, q + QV, ...).  Eight lanes share a window and read 8 adjacent
+// quads (one 128-byte line), four windows per warp: each FMA instruction
+// costs ~1/CX/8 weight wavefronts + ~1/OCV/8 input wavefronts, so the L1 /
+// shared data path (128 B per cycle) stays below the FMA issue rate.  The accumulation
+// order of every output is still ic -> kh -> kw (reference.cpp:34-49), so
+// EXACT stays bit-identical to the oracle.  1x1 convs read 4 channels of a
+// cell with one 16-byte load (same order: ic, ic+1, ic+2, ic+3).
+// Cells past the row end are computed from the next row / the region slack
+// (layout_step reserves it) and never stored.
+template <int KW, int S, int CX, int OCV, bool EXACT>
+__device__ void conv_rb(const FusedParams& P, const FOp& op, float* smem, const TileCtx& t) {
+    const Src s = src_of(P, op, smem, op.src);
+    const int segs = (op.ext_w + CX - 1) / CX;
+    const int QV = op.cout_pad / OCV;
+    // Lanes: groups of B = min(8, QV) channel groups share one row window, so
+    // a warp's weight load covers <= 128 contiguous bytes (one L1 wavefront)
+    // and its input loads touch 32 / B windows (rows fastest: different banks).
+    const int B = QV < 8 ? QV : 8;
+    const int NV = op.ext_h * segs;
+    const int nunits = NV * ((QV + B - 1) / B) * B;
+    const int kh_ = op.kh, cin = op.cin;
+    const int wstride = op.cout_pad;
+    constexpr int WIN = (CX - 1) * S + KW;
+    for (int u = threadIdx.x; u < nunits; u += kThreads) {
+        const int ql = u % B, t1 = u / B;
+        const int v = t1 % NV, q = (t1 / NV) * B + ql;
+        if (q >= QV) continue;
+        const int sg = v / op.ext_h, r = v - sg * op.ext_h;
+        const int c0 = sg * CX;
+        const float* xb = s.p + ((r * S + op.d) * s.w + c0 * S + op.d) * s.cp;
+        const float* wq = op.w + 4 * q;  // quads q, q + QV, ...: each weight load of a warp is contiguous
+        float acc[CX][OCV];
+#pragma unroll
+        for (int i = 0; i < CX; ++i)
+#pragma unroll
+            for (int o = 0; o < OCV; ++o) acc[i][o] = 0.0f;
+        if constexpr (KW == 1 && S == 1) {
+            // cells past the row end re-read its last cell (no region slack for 1x1 readers)
+            int xo[CX];
+#pragma unroll
+            for (int i = 0; i < CX; ++i) xo[i] = min(i, op.ext_w - 1 - c0) * s.cp;
+            int ic = 0;
+            for (; ic + 4 <= cin; ic += 4) {
+                float4 xv[CX];
+#pragma unroll
+                for (int i = 0; i < CX; ++i) xv[i] = *reinterpret_cast<const float4*>(xb + xo[i] + ic);
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    float wv[OCV];
+#pragma unroll
+                    for (int o = 0; o < OCV; o += 4) {
+                        const float4 w4 = __ldg(reinterpret_cast<const float4*>(wq + (ic + k) * wstride + o * QV));
+                        wv[o] = w4.x, wv[o + 1] = w4.y, wv[o + 2] = w4.z, wv[o + 3] = w4.w;
+                    }
+#pragma unroll
+                    for (int i = 0; i < CX; ++i) {
+                        const float xk = k == 0 ? xv[i].x : k == 1 ? xv[i].y : k == 2 ? xv[i].z : xv[i].w;
+#pragma unroll
+                        for (int o = 0; o < OCV; ++o) acc[i][o] = mac<EXACT>(acc[i][o], xk, wv[o]);
+                    }
+                }
+            }
+            for (; ic < cin; ++ic) {
+                float wv[OCV];
+#pragma unroll
+                for (int o = 0; o < OCV; o += 4) {
+                    const float4 w4 = __ldg(reinterpret_cast<const float4*>(wq + ic * wstride + o * QV));
+                    wv[o] = w4.x, wv[o + 1] = w4.y, wv[o + 2] = w4.z, wv[o + 3] = w4.w;
+                }
+#pragma unroll
+                for (int i = 0; i < CX; ++i) {
+                    const float xk = xb[xo[i] + ic];
+#pragma unroll
+                    for (int o = 0; o < OCV; ++o) acc[i][o] = mac<EXACT>(acc[i][o], xk, wv[o]);
+                }
+            }
+        } else {
+            for (int ic = 0; ic < cin; ++ic) {
+#pragma unroll
+                for (int kh = 0; kh < (KW == 3 ? 3 : 16); ++kh) {  // 3x3: rows unrolled (conv_rb_v passes kh == 3 only)
+                    if (KW != 3 && kh >= kh_) break;
+                    const float* xr = xb + kh * s.w * s.cp + ic;
+                    float xv[WIN];
+#pragma unroll
+                    for (int j = 0; j < WIN; ++j) xv[j] = xr[j * s.cp];
+                    const float* wr = wq + (ic * kh_ + kh) * KW * wstride;
+#pragma unroll
+                    for (int kw = 0; kw < KW; ++kw) {
+                        float wv[OCV];
+#pragma unroll
+                        for (int o = 0; o < OCV; o += 4) {
+                            const float4 w4 = __ldg(reinterpret_cast<const float4*>(wr + kw * wstride + o * QV));
+                            wv[o] = w4.x, wv[o + 1] = w4.y, wv[o + 2] = w4.z, wv[o + 3] = w4.w;
+                        }
+#pragma unroll
+                        for (int i = 0; i < CX; ++i)
+#pragma unroll
+                            for (int o = 0; o < OCV; ++o) acc[i][o] = mac<EXACT>(acc[i][o], xv[i * S + kw], wv[o]);
+                    }
+                }
+            }
+        }
+#pragma unroll
+        for (int o = 0; o < OCV; o += 4) {
+            const float4 b4 = __ldg(reinterpret_cast<const float4*>(op.b + 4 * q + o * QV));
+#pragma unroll
+            for (int i = 0; i < CX; ++i) {
+                if (c0 + i >= op.ext_w) continue;
+                float4 vv = make_float4(addb<EXACT>(acc[i][o], b4.x), addb<EXACT>(acc[i][o + 1], b4.y),
+                                        addb<EXACT>(acc[i][o + 2], b4.z), addb<EXACT>(acc[i][o + 3], b4.w));
+                if (op.relu) vv = make_float4(relu_ref(vv.x), relu_ref(vv.y), relu_ref(vv.z), relu_ref(vv.w));
+                store_cell(P, op, smem, t, r * op.ext_w + c0 + i, q + (o >> 2) * QV, vv);
+            }
+        }
+    }
+}
+
+template <int KW, int S, bool EXACT>
+__device__ __forceinline__ void conv_rb_v(const FusedParams& P, const FOp& op, float* smem, const TileCtx& t) {
+    if (op.ocv == 8) {
+        if constexpr (S == 1 && KW <= 3)  // 8x8 blocks only where the row window stays <= 10 values
+            if (op.cx == 8) return conv_rb<KW, S, 8, 8, EXACT>(P, op, smem, t);
+        return conv_rb<KW, S, 4, 8, EXACT>(P, op, smem, t);
+    }
+    if (op.cx == 4) return conv_rb<KW, S, 4, 4, EXACT>(P, op, smem, t);
+    return conv_rb<KW, S, 2, 4, EXACT>(P, op, smem, t);
+}
+
 // Max / avg pool with the reference's semantics: padding reads 0.0 for both
 // kinds (reference.cpp:73-76), avg divides by the full window (:80-83); the
 // window is summed in kh, kw order.
@@ -206,6 +340,14 @@ __device__ __forceinline__ void run_op(const FusedParams& P, const FOp& op, floa
     if (op.kind == OP_MAXPOOL) return pool_op<false>(P, op, smem, t);
     if (op.kind == OP_AVGPOOL) return pool_op<true>(P, op, smem, t);
     if (op.kind == OP_ADD) return add_op(P, op, smem, t);
+    if (op.cx) {  // planner-chosen register-blocked variant (rb_variant)
+        if (op.kw == 1) return conv_rb_v<1, 1, EXACT>(P, op, smem, t);
+        if (op.kw == 3) {  // rb_variant admits 3-wide kernels with 3 rows only
+            if (op.stride == 1) return conv_rb_v<3, 1, EXACT>(P, op, smem, t);
+            return conv_rb_v<3, 2, EXACT>(P, op, smem, t);
+        }
+        return conv_rb_v<5, 1, EXACT>(P, op, smem, t);
+    }
     const int ncell = op.ext_h * op.ext_w;
     const bool big = ncell * (op.cout_pad >> 2) >= 8 * kThreads;
     if (op.group != 1) return conv_op<0, 0, 4, EXACT, true>(P, op, smem, t);
@@ -222,7 +364,7 @@ __device__ __forceinline__ void run_op(const FusedParams& P, const FOp& op, floa
 }
 
 template <bool EXACT>
-__global__ void __launch_bounds__(kThreads) fused_block_kernel(const __grid_constant__ FusedParams P) {
+__global__ void __launch_bounds__(kThreads, 2) fused_block_kernel(const __grid_constant__ FusedParams P) {
     extern __shared__ __align__(16) float smem[];
     TileCtx t;
     t.n = blockIdx.y;

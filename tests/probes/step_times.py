@@ -19,8 +19,7 @@ def main():
     e = X.Engine(g, X.seeded_weights(g, 42), part, prec, max_batch=batch)
     e.set_input_seeded(42, batch)
     e.forward(batch, use_graph=False)
-    if prec in ("bf16", "tf32"):
-        e.autotune(batch, reps=3, topk=3)
+    e.autotune(batch, reps=3, topk=3)
     n = len(e.steps)
     st = torch.cuda.current_stream()
     for _ in range(3):

@@ -69,6 +69,41 @@ def test_fp32_ffma_within_1e5(name):
             assert O.normwise(out[o], ref[o]) <= 1e-5, (name, part, o)
 
 
+@pytest.mark.parametrize("name,batch", [("squeezenet11", 4), ("inc3a", 4), ("straight", 1), ("merge", 8), ("a1", 2)])
+def test_fp32_autotuned_plans_stay_exact(golden, name, batch):
+    """The fp32 tuner (tiles x register-blocked convs on / off, engine.cpp
+    autotune_fp32) changes only the work split, never an output's
+    accumulation order: fp32_exact stays bit-identical to the oracle and FFMA
+    within 1e-5, and the report re-applies to a fresh engine unchanged."""
+    import torch
+    text = graph_text(name)
+    og = O.load_graph(text)
+    w = O.seeded_weights(og, 42)
+    x = O.seeded_batch(og, 42, batch)
+    ref = O.run_batch(og, x, w, og.outputs, threads=4)
+    g = X.Graph(text)
+    for prec in ("fp32_exact", "fp32"):
+        e = X.Engine(g, O.flat_weights(og, w), "b200", prec, max_batch=batch)
+        e.set_input(torch.from_numpy(x).cuda())
+        e.forward(batch, use_graph=False)
+        report = e.autotune(batch, reps=1, topk=2)
+        assert report and all(r["kernel"] == "fp32" and r["tried"] >= 1 for r in report)
+        e.forward(batch)
+        out = e.read(g.outputs[0], batch).cpu().numpy()
+        r = ref[og.outputs[0]]
+        if prec == "fp32_exact":
+            assert np.array_equal(out, r), f"{name}: tuned fp32_exact plan differs from the oracle"
+        else:
+            assert O.normwise(out, r) <= 1e-5
+        e2 = X.Engine(g, O.flat_weights(og, w), "b200", prec, max_batch=batch)
+        e2.apply_tuning(report)
+        assert [(s["tile"], s.get("rb")) for s in e2.steps] == [(s["tile"], s.get("rb")) for s in e.steps]
+        e2.set_input(torch.from_numpy(x).cuda())
+        e2.forward(batch)
+        assert np.array_equal(e2.read(g.outputs[0], batch).cpu().numpy(), out)
+    torch.cuda.synchronize()
+
+
 # BASELINE configs at their full batch: C1 straight N=1, C2 merge N=8,
 # C3 fire N=32, C4 inception-3a N=64 (fp32 here; bf16/TF32 tolerance tests
 # live with the tensor-core path).
