@@ -227,7 +227,7 @@ double rb_units(const FOp& o, int cx, int ocv) {
 // minimises one CTA's serial work for the op (rounds of 256 threads x
 // per-thread instructions), the larger block on ties; cx = 0 keeps the
 // generic cell-quad path (grouped convs, widths / strides not instantiated).
-void rb_variant(FOp& o) {
+void rb_variant(FOp& o, int threads) {
     o.cx = o.ocv = 0;
     if (o.kind != OP_CONV || o.group != 1) return;
     const bool inst = (o.kw == 1 && o.stride == 1) || (o.kw == 3 && o.kh == 3 && o.stride <= 2) || (o.kw == 5 && o.stride == 1);
@@ -242,8 +242,8 @@ void rb_variant(FOp& o) {
         if (o.cout_pad % v[1] || (v[0] == 8 && (o.stride != 1 || o.kw > 3))) continue;  // instantiated set (conv_rb_v)
         const double units = rb_units(o, v[0], v[1]);
         const double per = rb_unit_instr(o, v[0], v[1]);
-        const double wi = std::ceil(units / 32.0) * per, l = std::ceil(units / 256.0) * per;
-        if (units >= 256 && wi < best_full * 0.999) best_full = wi, full[0] = v[0], full[1] = v[1];
+        const double wi = std::ceil(units / 32.0) * per, l = std::ceil(units / threads) * per;
+        if (units >= threads && wi < best_full * 0.999) best_full = wi, full[0] = v[0], full[1] = v[1];
         if (l < best_lat * 0.999) best_lat = l, lat[0] = v[0], lat[1] = v[1];
     }
     const int* pick = full[0] ? full : lat;
@@ -363,6 +363,7 @@ long long layout_step(const Graph& g, const StepSpec& s, int th, int tw, FusedPa
         fp->grid_h = (s.out_h + th - 1) / th, fp->grid_w = (s.out_w + tw - 1) / tw;
         fp->nops = nops, fp->nbufs = nbufs, fp->smem_floats = int(floats);
         fp->ctile = s.ctile;
+        fp->threads = s.threads == 512 ? 512 : 256;
         fp->cgroups = s.ctile ? round4(g.shape_of(s.inputs[0]).channels) / s.ctile : 1;
         for (int i = 0; i < nbufs; ++i) fp->bufs[i] = bufs[size_t(i)];
         for (int i = 0; i < nops; ++i) {
@@ -395,7 +396,7 @@ long long layout_step(const Graph& g, const StepSpec& s, int th, int tw, FusedPa
             o.d = geo[size_t(i)].d;
             o.ext_h = geo[size_t(i)].ext_h, o.ext_w = geo[size_t(i)].ext_w;
             o.org_mul = geo[size_t(i)].org_mul, o.org_sub = geo[size_t(i)].org_sub;
-            if (s.rb) rb_variant(o);
+            if (s.rb) rb_variant(o, fp->threads);
         }
     }
     return floats * 4;
@@ -408,8 +409,9 @@ long long layout_step(const Graph& g, const StepSpec& s, int th, int tw, FusedPa
 // cycle.  Halo recompute and partial tiles / row windows show up as units.
 double fp32_tile_cycles(const FusedParams& fp, int batch, long long smem) {
     double lat = 0, wi = 0;
+    const double nt = fp.threads;
     auto add = [&](double units, double per) {
-        lat += std::ceil(units / 256.0) * per;
+        lat += std::ceil(units / nt) * per;
         wi += std::ceil(units / 32.0) * per;
     };
     for (int i = 0; i < fp.nins; ++i) add(double(fp.in[i].ext_h) * fp.in[i].ext_w * fp.in[i].c / 4.0, 6.0);
@@ -419,14 +421,14 @@ double fp32_tile_cycles(const FusedParams& fp, int batch, long long smem) {
         if (o.kind == OP_CONV && o.cx)
             add(rb_units(o, o.cx, o.ocv), rb_unit_instr(o, o.cx, o.ocv) * 1.3);
         else if (o.kind == OP_CONV) {
-            const int PX = cells * Q >= 8 * 256 && o.group == 1 ? 8 : 4;
+            const int PX = cells * Q >= 8 * nt && o.group == 1 ? 8 : 4;
             add(std::ceil(cells / PX) * Q, double(o.cin / o.group) * o.kh * o.kw * (1 + PX + 4 * PX) * 1.3);
         } else
             add(cells * Q, 3.0 * o.kh * o.kw + 8);
     }
     // Weights stream from L2 through L1 (~64 B/cycle per SM); past what L1
     // keeps beside the CTAs' shared memory, every round of units re-reads them.
-    const int occ = std::max(1, std::min(2, int((228 * 1024) / (smem + 1024))));  // <= 2 CTAs: registers
+    const int occ = std::max(1, std::min(fp.threads == 512 ? 1 : 2, int((228 * 1024) / (smem + 1024))));  // registers: 128 x 512 per SM
     const double l1_keep = std::max(16.0 * 1024, (256.0 * 1024 - double(occ) * smem) / occ / 2);
     double l2 = 0;
     for (int i = 0; i < fp.nops; ++i) {
@@ -435,7 +437,7 @@ double fp32_tile_cycles(const FusedParams& fp, int batch, long long smem) {
         const double wb = double(o.cin / o.group) * o.kh * o.kw * o.cout_pad * 4;
         const double units = o.cx ? rb_units(o, o.cx, o.ocv)
                                   : double(o.ext_h) * o.ext_w * o.cout_pad / 16;
-        l2 += wb > l1_keep ? wb * std::ceil(units / 256.0) : wb;
+        l2 += wb > l1_keep ? wb * std::ceil(units / nt) : wb;
     }
     const double ctas = double(fp.grid_h) * fp.grid_w * fp.cgroups * std::max(batch, 1);
     const double per_sm = std::ceil(ctas / 148.0);
@@ -490,14 +492,14 @@ bool choose_tile_at(const Graph& g, StepSpec& s, int batch_hint, int smem_budget
 std::vector<F32Candidate> candidates_fp32(const Graph& g, const StepSpec& s, int batch_hint, int smem_budget) {
     std::vector<F32Candidate> out;
     StepSpec t = s;
-    for (int rb = 0; rb < 2; ++rb) {
-        t.rb = rb;
+    for (int mode = 0; mode < 4; ++mode) {
+        t.rb = mode & 1, t.threads = mode & 2 ? 512 : 256;
         for (int th = 1; th <= std::min(s.out_h, 32); ++th)
             for (int tw = 1; tw <= std::min(s.out_w, 32); ++tw) {
                 FusedParams fp;
                 const long long sm = layout_step(g, t, th, tw, &fp);
                 if (sm < 0 || sm > smem_budget) continue;
-                out.push_back({th, tw, rb, int(sm), fp32_tile_cycles(fp, batch_hint, sm)});
+                out.push_back({th, tw, t.rb, t.threads, int(sm), fp32_tile_cycles(fp, batch_hint, sm)});
             }
     }
     std::stable_sort(out.begin(), out.end(), [](const F32Candidate& a, const F32Candidate& b) { return a.model < b.model; });
@@ -929,7 +931,7 @@ std::string describe_plan_json(const Graph& g, const DevicePlan& plan) {
         static const char* kinds[] = {"fused", "concat_copy", "add", "relu"};
         os << (i ? "," : "") << "{\"id\":" << q(s.id) << ",\"kind\":" << q(kinds[s.kind]) << ",\"tag\":" << q(s.tag)
            << ",\"mode\":" << q(to_string(s.mode)) << ",\"tile\":[" << s.tile_h << "," << s.tile_w
-           << "],\"out\":[" << s.out_h << "," << s.out_w << "],\"smem_bytes\":" << s.smem_bytes << ",\"nxb\":" << s.nxb << ",\"wres\":" << s.wres << ",\"ring_slots\":" << s.ring_slots << ",\"grid_all\":" << s.grid_all << ",\"epi_warps\":" << s.epi_warps << ",\"tsets\":" << s.tsets << ",\"nsplit\":" << s.nsplit << ",\"rb\":" << s.rb << ",\"macs\":" << s.macs
+           << "],\"out\":[" << s.out_h << "," << s.out_w << "],\"smem_bytes\":" << s.smem_bytes << ",\"nxb\":" << s.nxb << ",\"wres\":" << s.wres << ",\"ring_slots\":" << s.ring_slots << ",\"grid_all\":" << s.grid_all << ",\"epi_warps\":" << s.epi_warps << ",\"tsets\":" << s.tsets << ",\"nsplit\":" << s.nsplit << ",\"rb\":" << s.rb << ",\"threads\":" << s.threads << ",\"macs\":" << s.macs
            << ",\"macs_executed\":" << s.macs_executed << ",\"bytes_algorithmic\":" << s.bytes_algorithmic
            << ",\"weight_bytes\":" << s.weight_bytes << ",\"ring_chunk\":" << s.ring_chunk << ",\"inputs\":[";
         for (size_t k = 0; k < s.inputs.size(); ++k) os << (k ? "," : "") << q(s.inputs[k]);

@@ -104,6 +104,7 @@ struct StepSpec {
     int ring_chunk = 16384;  // bytes per weight-ring slot
     int nsplit = 1;     // output-channel groups over the grid's y dimension (weights of a group resident per CTA)
     int rb = 1;         // fp32: register-blocked conv variants allowed (0 = the generic cell-quad path)
+    int threads = 256;  // fp32: threads per CTA (256 or 512)
     // tensor-core conv + global average pool (SqueezeNet conv10 -> pool10): the
     // step's single conv op never stores its output; its epilogue reduces
     // every tile over its cells and the pooled layer `gap_out` (1x1) is
@@ -163,7 +164,7 @@ struct BCandidate {
 // the SM-cycle model (fp32_tile_cycles), best first; the measured-time tuner
 // times the best of each mode.
 struct F32Candidate {
-    int th, tw, rb, smem;
+    int th, tw, rb, threads, smem;
     double model;
 };
 std::vector<F32Candidate> candidates_fp32(const Graph& g, const StepSpec& s, int batch_hint, int smem_budget);

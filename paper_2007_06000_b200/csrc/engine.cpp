@@ -656,12 +656,13 @@ std::string Engine::autotune_fp32(int batch, int reps, int topk, cudaStream_t st
         StepSpec& s = plan_.steps[i];
         if (s.kind != StepSpec::FUSED || dws_[i]) continue;
         const std::vector<F32Candidate> all = candidates_fp32(g_, s, batch, 227 * 1024);
-        std::vector<F32Candidate> cands = {{s.tile_h, s.tile_w, s.rb, s.smem_bytes, 0.0}};
-        int per_mode[2] = {0, 0};
-        const F32Candidate* biggest[2] = {nullptr, nullptr};
-        for (const F32Candidate& c : all) {  // the SIMT model is coarse: time >= 8 per mode
-            if (per_mode[c.rb]++ < std::max(8, 2 * topk)) cands.push_back(c);
-            if (!biggest[c.rb] || c.th * c.tw > biggest[c.rb]->th * biggest[c.rb]->tw) biggest[c.rb] = &c;
+        std::vector<F32Candidate> cands = {{s.tile_h, s.tile_w, s.rb, s.threads, s.smem_bytes, 0.0}};
+        int per_mode[4] = {0, 0, 0, 0};
+        const F32Candidate* biggest[4] = {nullptr, nullptr, nullptr, nullptr};
+        for (const F32Candidate& c : all) {  // the SIMT model is coarse: time >= 6 per (rb, threads) mode
+            const int m = c.rb + (c.threads == 512 ? 2 : 0);
+            if (per_mode[m]++ < std::max(6, 2 * topk)) cands.push_back(c);
+            if (!biggest[m] || c.th * c.tw > biggest[m]->th * biggest[m]->tw) biggest[m] = &c;
         }
         for (const F32Candidate* c : biggest)
             if (c) cands.push_back(*c);
@@ -669,11 +670,11 @@ std::string Engine::autotune_fp32(int batch, int reps, int topk, cudaStream_t st
         StepSpec best = s;
         FusedParams bestP{};
         int tried = 0;
-        std::set<std::array<int, 3>> seen;
+        std::set<std::array<int, 4>> seen;
         for (const F32Candidate& c : cands) {
-            if (!seen.insert({c.th, c.tw, c.rb}).second) continue;
+            if (!seen.insert({c.th, c.tw, c.rb, c.threads}).second) continue;
             StepSpec t = s;
-            t.tile_h = c.th, t.tile_w = c.tw, t.rb = c.rb;
+            t.tile_h = c.th, t.tile_w = c.tw, t.rb = c.rb, t.threads = c.threads;
             const long long sm = fp32_layout_bytes(g_, t, c.th, c.tw);
             if (sm < 0 || sm > 227 * 1024) continue;
             t.smem_bytes = int(sm);
@@ -688,15 +689,15 @@ std::string Engine::autotune_fp32(int batch, int reps, int topk, cudaStream_t st
             ms /= float(reps);
             ++tried;
             if (knobs_.tune_verbose)
-                std::fprintf(stderr, "[xlf] tune %s (fp32): tile %dx%d rb %d smem %d: %.1f us (model %.0f)\n", s.id.c_str(), c.th, c.tw, c.rb,
-                             int(sm), ms * 1000.0f, c.model);
+                std::fprintf(stderr, "[xlf] tune %s (fp32): tile %dx%d rb %d threads %d smem %d: %.1f us (model %.0f)\n", s.id.c_str(), c.th, c.tw,
+                             c.rb, c.threads, int(sm), ms * 1000.0f, c.model);
             if (ms < best_ms) best_ms = ms, best = t, bestP = P;
         }
         if (!tried) continue;
         s = best;
         params_[i] = bestP;
         js << (first ? "" : ",") << "{\"id\":\"" << s.id << "\",\"kernel\":\"fp32\",\"tried\":" << tried << ",\"us\":" << best_ms * 1000.0f
-           << ",\"tile\":[" << s.tile_h << "," << s.tile_w << "],\"rb\":" << s.rb << ",\"smem_bytes\":" << s.smem_bytes << "}";
+           << ",\"tile\":[" << s.tile_h << "," << s.tile_w << "],\"rb\":" << s.rb << ",\"threads\":" << s.threads << ",\"smem_bytes\":" << s.smem_bytes << "}";
         first = false;
     }
     return js.str();
@@ -903,8 +904,10 @@ void Engine::apply_tuning(const std::string& js) {
             const size_t tc = tb == std::string::npos ? tb : obj.find(',', tb);
             if (tc == std::string::npos) fail(ErrorKind::parse, "tuning report: step '" + id + "' without \"tile\": [h, w]");
             t.tile_h = std::atoi(obj.c_str() + tb + 1), t.tile_w = std::atoi(obj.c_str() + tc + 1);
-            num(obj, "rb", t.rb);
-            const long long sm = t.tile_h < 1 || t.tile_w < 1 || (t.rb != 0 && t.rb != 1) ? -1 : fp32_layout_bytes(g_, t, t.tile_h, t.tile_w);
+            num(obj, "rb", t.rb), num(obj, "threads", t.threads);
+            const long long sm = t.tile_h < 1 || t.tile_w < 1 || (t.rb != 0 && t.rb != 1) || (t.threads != 256 && t.threads != 512)
+                                     ? -1
+                                     : fp32_layout_bytes(g_, t, t.tile_h, t.tile_w);
             if (sm < 0 || sm > 227 * 1024) fail(ErrorKind::infeasible, "tuning report: configuration of step '" + id + "' is not feasible for this plan");
             t.smem_bytes = int(sm);
             todo.emplace_back(i, t);

@@ -77,6 +77,7 @@ struct FusedParams {
     int ctile, cgroups;
     int nops, nbufs;
     int smem_floats;
+    int threads;  // 256 (two CTAs per SM when shared memory allows) or 512 (one CTA, 16 warps)
     FOp ops[kMaxOps];
     FBuf bufs[kMaxBufs];
 };

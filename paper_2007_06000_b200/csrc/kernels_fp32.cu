@@ -23,7 +23,9 @@ namespace xlf {
 
 namespace {
 
-constexpr int kThreads = 256;
+// Threads per CTA: FusedParams::threads (256, or 512 for steps whose shared
+// memory allows one CTA per SM); loops stride by blockDim.x.
+constexpr int kMaxThreads = 512;
 #define kNegInf __int_as_float(0xff800000)
 
 template <bool EXACT>
@@ -99,7 +101,7 @@ __device__ void conv_op(const FusedParams& P, const FOp& op, float* smem, const 
     const int npb = (ncell + PX - 1) / PX;
     const int cin_g = op.cin / op.group, cout_g = op.cout / op.group;
     const int wstride = op.cout_pad;
-    for (int u = threadIdx.x; u < npb * Q; u += kThreads) {
+    for (int u = threadIdx.x; u < npb * Q; u += blockDim.x) {
         const int pb = u / Q, q = u - pb * Q;
         int base[PX];
 #pragma unroll
@@ -187,7 +189,7 @@ __device__ void conv_rb(const FusedParams& P, const FOp& op, float* smem, const 
     const int kh_ = op.kh, cin = op.cin;
     const int wstride = op.cout_pad;
     constexpr int WIN = (CX - 1) * S + KW;
-    for (int u = threadIdx.x; u < nunits; u += kThreads) {
+    for (int u = threadIdx.x; u < nunits; u += blockDim.x) {
         const int ql = u % B, t1 = u / B;
         const int v = t1 % NV, q = (t1 / NV) * B + ql;
         if (q >= QV) continue;
@@ -300,7 +302,7 @@ __device__ void pool_op(const FusedParams& P, const FOp& op, float* smem, const 
     const Src s = src_of(P, op, smem, op.src);
     const int ncell = op.ext_h * op.ext_w, Q = op.cout_pad >> 2;
     const float inv = static_cast<float>(op.kh * op.kw);
-    for (int u = threadIdx.x; u < ncell * Q; u += kThreads) {
+    for (int u = threadIdx.x; u < ncell * Q; u += blockDim.x) {
         const int cell = u / Q, q = u - cell * Q;
         const int r = cell / op.ext_w, c = cell - r * op.ext_w;
         const float* p0 = s.p + ((r * op.stride + op.d) * s.w + c * op.stride + op.d) * s.cp + 4 * q;
@@ -325,7 +327,7 @@ __device__ void add_op(const FusedParams& P, const FOp& op, float* smem, const T
     const FBuf& a = P.bufs[op.src];
     const FBuf& b = P.bufs[op.src2];
     const int ncell = op.ext_h * op.ext_w, Q = op.cout_pad >> 2;
-    for (int u = threadIdx.x; u < ncell * Q; u += kThreads) {
+    for (int u = threadIdx.x; u < ncell * Q; u += blockDim.x) {
         const int cell = u / Q, q = u - cell * Q;
         const int r = cell / op.ext_w, c = cell - r * op.ext_w;
         const float4 x = *reinterpret_cast<const float4*>(smem + a.smem_off + (r * a.ext_w + c) * a.cpitch + 4 * q);
@@ -349,7 +351,7 @@ __device__ __forceinline__ void run_op(const FusedParams& P, const FOp& op, floa
         return conv_rb_v<5, 1, EXACT>(P, op, smem, t);
     }
     const int ncell = op.ext_h * op.ext_w;
-    const bool big = ncell * (op.cout_pad >> 2) >= 8 * kThreads;
+    const bool big = ncell * (op.cout_pad >> 2) >= 8 * int(blockDim.x);
     if (op.group != 1) return conv_op<0, 0, 4, EXACT, true>(P, op, smem, t);
     if (op.kh == 1 && op.kw == 1) {
         if (big) return conv_op<1, 1, 8, EXACT, false>(P, op, smem, t);
@@ -364,7 +366,7 @@ __device__ __forceinline__ void run_op(const FusedParams& P, const FOp& op, floa
 }
 
 template <bool EXACT>
-__global__ void __launch_bounds__(kThreads, 2) fused_block_kernel(const __grid_constant__ FusedParams P) {
+__global__ void __launch_bounds__(kMaxThreads, 1) fused_block_kernel(const __grid_constant__ FusedParams P) {
     extern __shared__ __align__(16) float smem[];
     TileCtx t;
     t.n = blockIdx.y;
@@ -379,7 +381,7 @@ __global__ void __launch_bounds__(kThreads, 2) fused_block_kernel(const __grid_c
         const int Q = in.c >> 2, ncell = in.ext_h * in.ext_w;
         const int gy0 = t.oy0 * in.org_mul - in.org_sub, gx0 = t.ox0 * in.org_mul - in.org_sub;
         const float* img = in.x + size_t(t.n) * in.h * in.w * in.cstride + in.coff + t.c0;
-        for (int u = threadIdx.x; u < ncell * Q; u += kThreads) {
+        for (int u = threadIdx.x; u < ncell * Q; u += blockDim.x) {
             const int cell = u / Q, q = u - cell * Q;
             const int r = cell / in.ext_w, c = cell - r * in.ext_w;
             const int gy = gy0 + r, gx = gx0 + c;
@@ -496,8 +498,9 @@ cudaError_t init_fused_fp32() {
 cudaError_t launch_fused_fp32(const FusedParams& P, int batch, bool exact, cudaStream_t st) {
     const dim3 grid(P.grid_h * P.grid_w, batch, P.cgroups);
     const size_t smem = size_t(P.smem_floats) * 4;
-    if (exact) fused_block_kernel<true><<<grid, kThreads, smem, st>>>(P);
-    else fused_block_kernel<false><<<grid, kThreads, smem, st>>>(P);
+    const int nt = P.threads == 512 ? 512 : 256;
+    if (exact) fused_block_kernel<true><<<grid, nt, smem, st>>>(P);
+    else fused_block_kernel<false><<<grid, nt, smem, st>>>(P);
     return cudaGetLastError();
 }
 

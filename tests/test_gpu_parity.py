@@ -97,10 +97,22 @@ def test_fp32_autotuned_plans_stay_exact(golden, name, batch):
             assert O.normwise(out, r) <= 1e-5
         e2 = X.Engine(g, O.flat_weights(og, w), "b200", prec, max_batch=batch)
         e2.apply_tuning(report)
-        assert [(s["tile"], s.get("rb")) for s in e2.steps] == [(s["tile"], s.get("rb")) for s in e.steps]
+        key = lambda st: [(s["tile"], s.get("rb"), s.get("threads")) for s in st]  # noqa: E731
+        assert key(e2.steps) == key(e.steps)
         e2.set_input(torch.from_numpy(x).cuda())
         e2.forward(batch)
         assert np.array_equal(e2.read(g.outputs[0], batch).cpu().numpy(), out)
+        # the other CTA size and register blocking on the tuned tiles: same bits
+        for rb, nt in ((0, 512), (1, 512), (1, 256)):
+            alt = [dict(r, rb=rb, threads=nt) for r in report]
+            e3 = X.Engine(g, O.flat_weights(og, w), "b200", prec, max_batch=batch)
+            try:
+                e3.apply_tuning(alt)
+            except X.XlfError:
+                continue  # a 512-thread CTA at this tile may exceed shared memory: reported, not run
+            e3.set_input(torch.from_numpy(x).cuda())
+            e3.forward(batch)
+            assert np.array_equal(e3.read(g.outputs[0], batch).cpu().numpy(), out), (name, prec, rb, nt)
     torch.cuda.synchronize()
 
 
