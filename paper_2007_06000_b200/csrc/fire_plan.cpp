@@ -101,7 +101,7 @@ std::vector<std::pair<double, FireParams>> fire_candidates(const FireParams& P, 
     for (int cps : {1, 2})
     for (int cb : {128, 64})
     for (int sqs : {0, 1})
-    for (int ns : {1, 2, 4}) {
+    for (int ns : {1, 2, 3, 4}) {  // 3: 192- and 384-channel expands at 64-channel groups (TF32 fire6/7 weights fit)
         if (force_nsplit > 0 && ns != force_nsplit) continue;
         // 64-byte chunks only on request: they let wider expand weights stay
         // resident (fire8/9 at two channel groups) but measured slower on
