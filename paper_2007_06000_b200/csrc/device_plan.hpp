@@ -30,6 +30,7 @@ struct Knobs {
     std::string unfuse;          // unfuse=b3;b4: split these blocks
     double unfuse_ratio = 0.85;  // model margin a split must win by
     double mb_max_weight = -1;   // cap (bytes) on a multi-branch kernel's conv weights (<0: none)
+    int mb_pw = 0;               // tensor-core plans: let steps the pointwise kernel would run join multi-branch kernels
     bool no_nalt = false;        // no N-block TMEM column alternation
     bool no_tsep = false;        // groups share TMEM columns
     bool no_pwait = false;       // a tile's first group waits for the previous tile's last unit

@@ -325,13 +325,13 @@ __global__ void __launch_bounds__(kStemThreads, 2) stem_kernel(const __grid_cons
                     } else {
 #pragma unroll
                         for (int h = 0; h < NCH; ++h) {
-                            float m[32];
+                            // the pooled maxima replace the row's values in rv (no third 32-register array)
 #pragma unroll
                             for (int k = 0; k < 32; ++k) {
                                 const float v = __uint_as_float(rv[h][k]);
-                                m[k] = fmaxf(vm[h * 32 + k], v), vm[h * 32 + k] = v;
+                                rv[h][k] = __float_as_uint(fmaxf(vm[h * 32 + k], v)), vm[h * 32 + k] = v;
                             }
-                            stage_part<T, NCH>(stage, t, h, m);
+                            stage_part<T, NCH>(stage, t, h, reinterpret_cast<const float*>(rv[h]));
                         }
                     }
                 } else {

@@ -254,7 +254,8 @@ def test_tc_many_parallel_branches(prec):
     w = O.seeded_weights(og, 3)
     x = O.seeded_batch(og, 5, 3)
     g = X.Graph(WIDE)
-    e = X.Engine(g, O.flat_weights(og, w), "b200", prec, max_batch=3)
+    # mb_pw=1: merge the 1x1 branches although each alone would run on the pointwise kernel
+    e = X.Engine(g, O.flat_weights(og, w), "b200", prec, max_batch=3, options="mb_pw=1")
     assert any(len(s["layers"]) >= 5 for s in e.steps), [s["layers"] for s in e.steps]
     e.set_input(torch.from_numpy(x).cuda())
     e.forward(3)
