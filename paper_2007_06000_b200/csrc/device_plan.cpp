@@ -230,7 +230,8 @@ double rb_units(const FOp& o, int cx, int ocv) {
 void rb_variant(FOp& o, int threads) {
     o.cx = o.ocv = 0;
     if (o.kind != OP_CONV || o.group != 1) return;
-    const bool inst = (o.kw == 1 && o.stride == 1) || (o.kw == 3 && o.kh == 3 && o.stride <= 2) || (o.kw == 5 && o.stride == 1);
+    // instantiated shapes (conv_rb_v): 1x1 stride 1, 3x3 stride 1 / 2, k x 5 stride 1
+    const bool inst = (o.kw == 1 && o.kh == 1 && o.stride == 1) || (o.kw == 3 && o.kh == 3 && o.stride <= 2) || (o.kw == 5 && o.stride == 1);
     if (!inst) return;
     static const int kVariants[4][2] = {{8, 8}, {4, 8}, {4, 4}, {2, 4}};
     // Variants that give every thread of the CTA a unit: fewest warp

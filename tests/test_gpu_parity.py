@@ -116,6 +116,36 @@ def test_fp32_autotuned_plans_stay_exact(golden, name, batch):
     torch.cuda.synchronize()
 
 
+NONSQUARE = "name nonsquare\ninput {\n  name d\n  shape [12, 14, 14]\n}\n" + "".join(
+    f"layer {{\n  name {n}\n  kind conv\n  inputs [{i}]\n  out_channels {c}\n  kernel [{kh}, {kw}]\n  pad 0\n  activation relu\n}}\n"
+    for n, i, c, kh, kw in [("k31", "d", 16, 3, 1), ("k13", "k31", 24, 1, 3), ("k51", "k13", 16, 5, 1), ("k15", "k51", 8, 1, 5),
+                            ("k35", "d", 16, 3, 5), ("k53", "k35", 8, 5, 3)]) + "output k15\noutput k53\n"
+
+
+@pytest.mark.parametrize("part", ["b200", "unfused"])
+def test_nonsquare_kernels_exact(part):
+    """k x 1 / 1 x k / 3x5 / 5x3 convs (shapes outside the register-blocked
+    instantiations, or inside with kh != kw): fp32_exact bit for bit, planner
+    choice and every tuned variant."""
+    import torch
+    og = O.load_graph(NONSQUARE)
+    w = O.seeded_weights(og, 4)
+    x = O.seeded_batch(og, 6, 3)
+    names = [l.name for l in og.layers]
+    ref = O.run_batch(og, x, w, names)
+    g = X.Graph(NONSQUARE)
+    e = X.Engine(g, O.flat_weights(og, w), part, "fp32_exact", max_batch=3)
+    e.set_input(torch.from_numpy(x).cuda())
+    for tune in (False, True):
+        if tune:
+            e.autotune(3, reps=1, topk=2)
+        e.forward(3)
+        for n in names:
+            if n in e.materialized():
+                assert np.array_equal(e.read(n, 3).cpu().numpy(), ref[n]), (part, tune, n)
+    torch.cuda.synchronize()
+
+
 # BASELINE configs at their full batch: C1 straight N=1, C2 merge N=8,
 # C3 fire N=32, C4 inception-3a N=64 (fp32 here; bf16/TF32 tolerance tests
 # live with the tensor-core path).

@@ -16,6 +16,9 @@ CASES = [("squeezenet11", 2, "b200"), ("squeezenet11", 2, "unfused"), ("inc3a", 
          ("a2", 2, "b200"), ("c1", 2, "reference"), ("fire", 3, "b200")]
 
 
+TUNE = os.environ.get("SAN_TUNE", "1") == "1"
+
+
 def main():
     precs = sys.argv[1:] or ["bf16", "fp32_exact"]
     for prec in precs:
@@ -24,6 +27,9 @@ def main():
             e = X.Engine(g, X.seeded_weights(g, 42), part, prec, max_batch=batch)
             e.set_input_seeded(42, batch)
             e.forward(batch, use_graph=False)
+            if TUNE and prec.startswith("fp32"):
+                # the fp32 tuner launches every (tile, register blocking, 256 / 512 threads) candidate
+                e.autotune(batch, reps=1, topk=1)
             e.forward(batch, use_graph=True)
             for n in e.materialized():
                 if n in dict(g.inputs):
