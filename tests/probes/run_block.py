@@ -23,7 +23,7 @@ def main():
     opts = sys.argv[7] if len(sys.argv) > 7 else ""
     e = X.Engine(g, X.seeded_weights(g, 42), part, prec, max_batch=batch, options=opts)
     e.set_input_seeded(42, batch)
-    if tune and prec == "bf16":
+    if tune:
         e.forward(batch, use_graph=False)
         e.autotune(batch, reps=3, topk=3)
         e.set_input_seeded(42, batch)

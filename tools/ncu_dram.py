@@ -5,7 +5,7 @@ dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum --csv`):
 
     python tools/ncu_dram.py run GRAPH BATCH PRECISION PARTITION
 
-(the engine is autotuned first for tensor-core precisions, as bench.py does;
+(the engine is autotuned first, as bench.py does;
 only one forward runs inside cudaProfilerStart/Stop).  Summary of the logs:
 
     python tools/ncu_dram.py summarize OUT.json LOG.csv...   (file names: GRAPH_BATCH_PREC_PART.csv)
@@ -25,7 +25,7 @@ def run(name, batch, prec, part):
     g = X.load_graph(X.graph_path(name))
     e = X.Engine(g, X.seeded_weights(g, 42), part, prec, max_batch=batch)
     e.set_input_seeded(42, batch)
-    if prec in ("bf16", "tf32"):
+    if True:  # every precision is tuned, as bench.py does
         e.forward(batch, use_graph=False)
         e.autotune(batch, reps=3, topk=3)
         e.set_input_seeded(42, batch)
