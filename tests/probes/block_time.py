@@ -22,8 +22,7 @@ def main():
         e = X.Engine(g, w, "b200", prec, max_batch=batch, options=opt)
         e.set_input_seeded(42, batch)
         e.forward(batch, use_graph=False)
-        if prec == "bf16":
-            e.autotune(batch, reps=3, topk=3)
+        e.autotune(batch, reps=3, topk=3)
         for _ in range(3):
             e.forward(batch, use_graph=True)
         torch.cuda.synchronize()
