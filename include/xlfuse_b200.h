@@ -130,8 +130,12 @@ xlf_status xlf_engine_run_host(xlf_engine* e, const float* h_in_nchw, int batch,
                                void* stream);
 /* Measured-time tuner (no reference counterpart: replaces the reference's
  * model-only tune(), cost_model.cpp:236-294): times the `topk` best
- * configurations of every tensor-core (bf16 / TF32) fused step on the device (`reps` launches
- * each, `batch` images) and keeps the fastest; fp32 engines: no-op. The
+ * configurations of every fused step on the device (`reps` launches each,
+ * `batch` images) and keeps the fastest -- tensor-core (bf16 / TF32) steps:
+ * tile, staging, weight residency, epilogue warps, accumulator sets, channel
+ * groups; fp32 SIMT steps: tile, register-blocked convs on / off, 256 / 512
+ * threads per CTA (results do not depend on the choice: fp32_exact stays
+ * bit-identical to the reference). The
  * choices are reported by xlf_engine_tune_report (JSON) and by
  * xlf_engine_json's plan. Synchronous; not thread-safe with other calls on
  * the same engine. */
