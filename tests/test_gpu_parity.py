@@ -336,6 +336,13 @@ def test_random_graphs_exact():
         x = O.seeded_batch(og, trial + 100, 2)
         ref = O.run_batch(og, x, w, ["cat", "p"])
         for part in PARTS:
-            out, _ = run(text, O.flat_weights(og, w), 2, part, "fp32_exact", x=x, names=["cat", "p"])
+            out, e = run(text, O.flat_weights(og, w), 2, part, "fp32_exact", x=x, names=["cat", "p"])
             for n in out:
                 assert np.array_equal(out[n], ref[n]), (trial, part, n, text)
+            if part == "b200":  # every tuned fp32 variant (tile, register blocking, CTA size): same bits
+                import torch
+                e.autotune(2, reps=1, topk=2)
+                e.set_input(torch.from_numpy(x).cuda())
+                e.forward(2)
+                for n in out:
+                    assert np.array_equal(e.read(n, 2).cpu().numpy(), ref[n]), (trial, "tuned", n, text)
