@@ -710,7 +710,15 @@ DevicePlan plan_device(const Graph& g, Partition part, int batch_hint, int smem_
         // the planner's model says it beats its layers run as single kernels
         // plus the HBM round trip of the intermediates (SURVEY §8f rank 1's
         // model, the same scores the measured tuner starts from).
-        if (tc && part == Partition::b200 && s.kind == StepSpec::FUSED && b.fused() && s.gap_out.empty() && !knobs.always_fuse) {
+        // Weightless consumers (conv -> pool) re-stream nothing: the split's
+        // premise does not hold, and the model mis-ranks them (TF32 C1 at
+        // batch 1: 29.7 us split vs 23.1 us fused), so they stay fused.
+        bool pool_consumers = false;
+        for (const OpSpec& op : s.ops)
+            if (op.stage == 2) pool_consumers = true;
+        for (const OpSpec& op : s.ops)
+            if (op.stage == 2 && g.find_layer(op.layer)->kind != LayerKind::pool) pool_consumers = false;
+        if (tc && part == Partition::b200 && s.kind == StepSpec::FUSED && b.fused() && s.gap_out.empty() && !knobs.always_fuse && !pool_consumers) {
             const int budget = std::min(smem_budget, kSmemBudgetTc);
             const std::vector<BCandidate> fc = candidates_tc(g, s, batch_hint, budget, tc_es, knobs);
             double fused = fc.empty() ? 1e300 : fc.front().model, single = 0;
