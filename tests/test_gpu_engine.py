@@ -28,18 +28,21 @@ def test_graph_replay_equals_eager_and_steps():
     assert torch.equal(a, b) and torch.equal(a, c)
 
 
+@pytest.mark.parametrize("opts", ["", "e2e_ramp=0", "e2e_chunks=3"])
 @pytest.mark.parametrize("prec", ["fp32_exact", "bf16"])
-def test_run_host_matches_device_path(prec):
+def test_run_host_matches_device_path(prec, opts):
+    """run_host's chunked H2D / forward / D2H pipeline (half-size end chunks by
+    default, equal chunks with e2e_ramp=0) equals the device path."""
     import torch
     g = X.Graph(graph_text("fire"))
     og = O.load_graph(graph_text("fire"))
     w = X.seeded_weights(g, 42)
-    x = O.seeded_batch(og, 42, 3)
-    e = X.Engine(g, w, "b200", prec, max_batch=3)
+    x = O.seeded_batch(og, 42, 7)
+    e = X.Engine(g, w, "b200", prec, max_batch=7, options=opts)
     host = e.run_host(x, "fire3_concat")
     e.set_input(torch.from_numpy(x).cuda())
-    e.forward(3)
-    dev = e.read("fire3_concat", 3).cpu().numpy()
+    e.forward(7)
+    dev = e.read("fire3_concat", 7).cpu().numpy()
     assert np.array_equal(host, dev)
 
 
